@@ -1,0 +1,125 @@
+/*
+ * bse_b200.h -- C ABI of the B200-native (sm_100a) structure-preserving
+ * Bethe-Salpeter eigensolver.
+ *
+ * The reference package (bse-solver 0.1.0, pure Python/numpy) has no FFI
+ * layer; these entry points sit *under* its Python solver API and replace
+ * the numerical core of each call, one-for-one:
+ *
+ *   bse_solve_spd_pair_*   solvers.solve_real      pkg/src/bse/solvers.py:80-109
+ *                          solvers.solve_complex   pkg/src/bse/solvers.py:29-77
+ *                          (real path; the complex path calls it on the
+ *                          2n x 2n real embedding, D3)
+ *   bse_potrf_dev          kernels.cholesky         pkg/src/bse/kernels.py:43-65
+ *   bse_syevd_dev          kernels.skew_tridiagonalize + phase_fold +
+ *                          tridiag_eig + SkewTridiagonal.apply_q
+ *                                                   pkg/src/bse/kernels.py:194-213,
+ *                                                   :231-240, :460-535, :154-158
+ *   bse_stedc_dev          kernels.tridiag_eig      pkg/src/bse/kernels.py:460-535
+ *   bse_absorption_dev     spectra.absorption_spectrum
+ *                                                   pkg/src/bse/spectra.py:120-151
+ *
+ * Conventions: all matrices are column-major FP64 with explicit leading
+ * dimensions; "_dev" functions take device pointers and a cudaStream_t passed
+ * as void*; "_host" functions take host pointers and do the copies.  No
+ * function throws; each returns a bse_status and never frees caller memory.
+ */
+#ifndef BSE_B200_H
+#define BSE_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  BSE_OK = 0,
+  BSE_NOT_POSITIVE_DEFINITE = 1, /* maps to kernels.NotPositiveDefinite */
+  BSE_NO_CONVERGENCE = 2,        /* maps to kernels.ConvergenceError */
+  BSE_BAD_ARGUMENT = 3,          /* maps to ValueError */
+  BSE_CUDA_ERROR = 4             /* message in bse_last_error() */
+} bse_status;
+
+/* Flags for bse_solve_spd_pair_* / bse_syevd_dev. */
+#define BSE_FLAG_VALUES_ONLY 0x1 /* eigenvalues only (TDA / validation) */
+#define BSE_FLAG_ZPOLISH 0x2     /* Z <- Z (1.5 I - 0.5 Z^T Z) orthogonality polish */
+
+typedef struct bse_info {
+  int64_t pivot_index;  /* first non-positive Cholesky pivot (status 1) */
+  double pivot_value;   /* its value */
+  int32_t failed_factor;/* 0: K = A - B, 1: M = A + B */
+  int32_t reserved;
+  double min_pivot;     /* min_j L_jj^2 of the last successful factor */
+} bse_info;
+
+int bse_version(void);
+const char* bse_last_error(void);
+
+/* Workspace (bytes) needed by bse_solve_spd_pair_dev for dimension n. */
+size_t bse_solve_workspace_bytes(int64_t n, int flags);
+
+/*
+ * Real symmetric-definite product pair (M = A + B, K = A - B, both SPD):
+ *   K = L L^T, W = L^T M L = Z diag(lam^2) Z^T,
+ *   X1 = (L Z + L^{-T} Z Lam) Lam^{-1/2} / 2,  X2 = (L Z - L^{-T} Z Lam) Lam^{-1/2} / 2
+ * lam is returned DESCENDING and strictly positive (core.py:159-162).
+ * M and K are read-only; only their lower triangles are referenced.
+ */
+int bse_solve_spd_pair_dev(int64_t n, const double* dM, int64_t ldm, const double* dK,
+                           int64_t ldk, double* dLam, double* dX1, int64_t ldx1, double* dX2,
+                           int64_t ldx2, void* dWork, size_t work_bytes, int flags, void* stream,
+                           bse_info* info);
+
+/* Same contract with host buffers (copies inside; the e2e path). */
+int bse_solve_spd_pair_host(int64_t n, const double* M, int64_t ldm, const double* K,
+                            int64_t ldk, double* lam, double* X1, int64_t ldx1, double* X2,
+                            int64_t ldx2, int flags, bse_info* info);
+
+/* In-place lower Cholesky (strict upper zeroed). */
+int bse_potrf_dev(int64_t n, double* dA, int64_t lda, void* stream, bse_info* info);
+
+/* Workspace for bse_syevd_dev. */
+size_t bse_syevd_workspace_bytes(int64_t n, int flags);
+
+/* All eigenpairs of a real symmetric matrix (lower triangle of dA is read and
+ * destroyed): two-stage reduction (full -> band -> tridiagonal), divide and
+ * conquer, WY back-transforms.  w ascending; Z columns orthonormal. */
+int bse_syevd_dev(int64_t n, double* dA, int64_t lda, double* dW, double* dZ, int64_t ldz,
+                  void* dWork, size_t work_bytes, int flags, void* stream);
+
+/* Symmetric tridiagonal divide and conquer: d (n), e (n-1) -> w ascending,
+ * Q (n x n) orthonormal eigenvectors.  d and e are overwritten. */
+size_t bse_stedc_workspace_bytes(int64_t n);
+int bse_stedc_dev(int64_t n, double* dD, double* dE, double* dQ, int64_t ldq, void* dWork,
+                  size_t work_bytes, void* stream);
+
+/* Absorption weights and broadened curve (spectra.py:120-151):
+ *   p_j = y_j^H x_j,  w_j = Re[(d_r^H x_j)(y_j^H d_l) / p_j],
+ *   eps(omega_g) = sum_j w_j N(omega_g - lam_j; sigma), |omega - lam| <= 8 sigma,
+ * accumulated in eigenvalue order.  Complex data are interleaved (re, im).
+ * X1, X2: n x n complex (ld in complex elements); dr, dl: 2n complex.
+ * Outputs: weights (n), pairing defect max|p_j - 1| (1), values (ngrid). */
+int bse_absorption_dev(int64_t n, const double* dLam, const double* dX1c, int64_t ldx1,
+                       const double* dX2c, int64_t ldx2, const double* dDr, const double* dDl,
+                       int64_t ngrid, const double* dGrid, double sigma, double* dWeights,
+                       double* dValues, double* dDefect, double* dMinPair, void* stream);
+
+/* Building blocks exposed for tests. */
+int bse_gemm_dev(int transA, int transB, int64_t M, int64_t N, int64_t K, double alpha,
+                 const double* dA, int64_t lda, const double* dB, int64_t ldb, double beta,
+                 double* dC, int64_t ldc, const int32_t* masks /* 9 ints or NULL */,
+                 void* stream);
+/* kind: 0 = A L^{-T} (right), 1 = L^{-T} B (left, trans), 2 = L^{-1} B (left) */
+int bse_trsm_dev(int kind, int64_t n, const double* dL, int64_t ldl, double* dB, int64_t ldb,
+                 int64_t m, void* stream);
+
+/* FP64 peak probe: which 0 = DMMA, 1 = DFMA.  Returns flops of one launch in
+ * *flops and the mean device time over `reps` launches in *ms. */
+int bse_peak_fp64(int which, int blocks, int iters, int reps, double* flops, double* ms);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* BSE_B200_H */

@@ -1,0 +1,94 @@
+// Shared device helpers for the B200 (sm_100a) FP64 BSE eigensolver.
+//
+// FP64 math on sm_100a: tcgen05 has no f64 kind, so dense contractions use the
+// warp-level DMMA path (mma.sync.m8n8k4.f64 -> SASS DMMA.8x8x4) fed from
+// shared memory staged with cp.async (LDGSTS).  Everything here is FP64.
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#define BSE_HD __host__ __device__ __forceinline__
+#define BSE_DEV __device__ __forceinline__
+
+namespace bse {
+
+constexpr double kEps = 2.220446049250313e-16;     // DBL_EPSILON (numpy finfo eps)
+constexpr double kSafmin = 2.2250738585072014e-308; // DBL_MIN (numpy finfo tiny)
+constexpr int kNoMaskLo = -(1 << 30);
+constexpr int kNoMaskHi = (1 << 30);
+
+// ---------------------------------------------------------------------------
+// DMMA: D(8x8) += A(8x4, row) * B(4x8, col), FP64.
+//   a: A[lane>>2][lane&3]   b: B[lane&3][lane>>2]   d: D[lane>>2][2*(lane&3)+{0,1}]
+BSE_DEV void dmma8x8x4(double (&d)[2], double a, double b) {
+  asm volatile(
+      "mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+      : "+d"(d[0]), "+d"(d[1])
+      : "d"(a), "d"(b));
+}
+
+// ---------------------------------------------------------------------------
+// cp.async (LDGSTS).  src-size 0 zero-fills the destination.
+BSE_DEV void cp_async16(void* smem, const void* gmem, bool pred) {
+  unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
+  int sz = pred ? 16 : 0;
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(s), "l"(gmem), "r"(sz));
+}
+BSE_DEV void cp_async8(void* smem, const void* gmem, bool pred) {
+  unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
+  int sz = pred ? 8 : 0;
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(s), "l"(gmem), "r"(sz));
+}
+BSE_DEV void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+template <int N>
+BSE_DEV void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
+
+// ---------------------------------------------------------------------------
+// Reductions
+BSE_DEV double warp_sum(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+BSE_DEV double warp_max(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, o));
+  return v;
+}
+
+// Block-wide sum in fixed order (deterministic).  `red` needs >= 32 doubles.
+BSE_DEV double block_sum(double v, double* red) {
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const int nw = (blockDim.x + 31) >> 5;
+  v = warp_sum(v);
+  __syncthreads();
+  if (lane == 0) red[wid] = v;
+  __syncthreads();
+  double t = 0.0;
+  if (wid == 0) {
+    t = lane < nw ? red[lane] : 0.0;
+    t = warp_sum(t);
+    if (lane == 0) red[0] = t;
+  }
+  __syncthreads();
+  t = red[0];
+  __syncthreads();
+  return t;
+}
+
+// L2-coherent loads for data written by other CTAs of the same launch.
+BSE_DEV double ld_cg(const double* p) { return __ldcg(p); }
+
+// Acquire / release flag helpers for inter-CTA pipelines.
+BSE_DEV int ld_acquire(const int* p) {
+  int v;
+  asm volatile("ld.acquire.gpu.global.s32 %0, [%1];\n" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+BSE_DEV void st_release(int* p, int v) {
+  asm volatile("st.release.gpu.global.s32 [%0], %1;\n" ::"l"(p), "r"(v) : "memory");
+}
+
+BSE_HD long long ceil_div(long long a, long long b) { return (a + b - 1) / b; }
+
+}  // namespace bse

@@ -1,0 +1,259 @@
+// Recursive POTRF / TRSM built from 64-wide in-CTA leaves and the masked DMMA
+// GEMM.  Recursion halves the problem so every off-diagonal update is one
+// large GEMM (the blocked right-looking counterpart of the reference's
+// left-looking GEMV loop, kernels.py:43-65).
+#include "dense.cuh"
+
+namespace bse {
+namespace {
+
+constexpr int kLeaf = 64;
+constexpr int kLds = kLeaf + 1;
+
+// --- POTF2: in-place lower Cholesky of an n x n (n <= 64) diagonal block ---
+__global__ void __launch_bounds__(256) potf2_kernel(double* A, long long lda, int n, int off,
+                                                    DevStatus* st) {
+  __shared__ double T[kLeaf * kLds];  // column-major, T[c*kLds + r]
+  if (st->info >= 0) return;          // an earlier block already failed
+  const int tid = threadIdx.x;
+  for (int idx = tid; idx < n * n; idx += blockDim.x) {
+    const int r = idx % n, c = idx / n;
+    T[c * kLds + r] = (r >= c) ? A[r + c * lda] : 0.0;
+  }
+  for (int j = 0; j < n; ++j) {
+    __syncthreads();
+    const double piv = T[j * kLds + j];
+    if (!(piv > 0.0)) {  // uniform: every thread read the same value
+      if (tid == 0) { st->info = off + j; st->value = piv; }
+      return;
+    }
+    const double d = sqrt(piv);
+    const double inv = 1.0 / d;
+    __syncthreads();
+    if (tid == 0) T[j * kLds + j] = d;
+    for (int i = j + 1 + tid; i < n; i += blockDim.x) T[j * kLds + i] *= inv;
+    __syncthreads();
+    const int w = n - j - 1;
+    for (int idx = tid; idx < w * w; idx += blockDim.x) {
+      const int r = j + 1 + idx % w, c = j + 1 + idx / w;
+      if (r >= c) T[c * kLds + r] -= T[j * kLds + r] * T[j * kLds + c];
+    }
+  }
+  __syncthreads();
+  for (int idx = tid; idx < n * n; idx += blockDim.x) {
+    const int r = idx % n, c = idx / n;
+    A[r + c * lda] = (r >= c) ? T[c * kLds + r] : 0.0;
+  }
+}
+
+// --- X L^T = A for a 64-row slab of A, L n x n (n <= 64) lower ---
+__global__ void __launch_bounds__(kLeaf) trsm_rlt_leaf(const double* __restrict__ L, long long ldl,
+                                                       int n, double* A, long long lda, int m) {
+  extern __shared__ double dyn[];
+  double* Ls = dyn;                  // row-major: Ls[j*kLds + i] = L[j][i]
+  double* As = dyn + kLeaf * kLds;   // row-major: As[r*kLds + j]
+  const int tid = threadIdx.x;
+  const int r0 = blockIdx.x * kLeaf;
+  for (int idx = tid; idx < n * n; idx += blockDim.x) {
+    const int j = idx % n, i = idx / n;  // coalesced along j (rows of L)
+    Ls[j * kLds + i] = (j >= i) ? L[j + i * ldl] : 0.0;
+  }
+  for (int j = 0; j < n; ++j) {
+    const int r = r0 + tid;
+    As[tid * kLds + j] = r < m ? A[r + j * lda] : 0.0;
+  }
+  __syncthreads();
+  double* x = As + tid * kLds;
+  for (int j = 0; j < n; ++j) {
+    double s = x[j];
+    const double* lj = Ls + j * kLds;
+    for (int i = 0; i < j; ++i) s -= x[i] * lj[i];
+    x[j] = s / lj[j];
+  }
+  __syncthreads();
+  for (int j = 0; j < n; ++j) {
+    const int r = r0 + tid;
+    if (r < m) A[r + j * lda] = As[tid * kLds + j];
+  }
+}
+
+// --- L^T X = B (backward) or L X = B (forward) for a 64-column slab of B ---
+template <bool TRANS>
+__global__ void __launch_bounds__(kLeaf) trsm_left_leaf(const double* __restrict__ L, long long ldl,
+                                                        int n, double* B, long long ldb, int ncols) {
+  extern __shared__ double dyn[];
+  double* Ls = dyn;                  // column-major: Ls[c*kLds + r] = L[r][c]
+  double* Bs = dyn + kLeaf * kLds;   // per-column: Bs[c*kLds + i]
+  const int tid = threadIdx.x;
+  const int c0 = blockIdx.x * kLeaf;
+  for (int idx = tid; idx < n * n; idx += blockDim.x) {
+    const int r = idx % n, c = idx / n;
+    Ls[c * kLds + r] = (r >= c) ? L[r + c * ldl] : 0.0;
+  }
+  for (int c = 0; c < kLeaf; ++c) {
+    const int gc = c0 + c;
+    for (int i = tid; i < n; i += blockDim.x) Bs[c * kLds + i] = gc < ncols ? B[i + gc * ldb] : 0.0;
+  }
+  __syncthreads();
+  double* x = Bs + tid * kLds;
+  if (TRANS) {  // L^T x = b: x_j = (b_j - sum_{i>j} L[i][j] x_i) / L[j][j]
+    for (int j = n - 1; j >= 0; --j) {
+      double s = x[j];
+      const double* lc = Ls + j * kLds;  // column j of L
+      for (int i = j + 1; i < n; ++i) s -= lc[i] * x[i];
+      x[j] = s / lc[j];
+    }
+  } else {  // L x = b: x_j = (b_j - sum_{i<j} L[j][i] x_i) / L[j][j]
+    for (int j = 0; j < n; ++j) {
+      double s = x[j];
+      for (int i = 0; i < j; ++i) s -= Ls[i * kLds + j] * x[i];
+      x[j] = s / Ls[j * kLds + j];
+    }
+  }
+  __syncthreads();
+  for (int c = 0; c < kLeaf; ++c) {
+    const int gc = c0 + c;
+    if (gc >= ncols) break;
+    for (int i = tid; i < n; i += blockDim.x) B[i + gc * ldb] = Bs[c * kLds + i];
+  }
+}
+
+__global__ void zero_upper_kernel(double* A, long long lda, int n) {
+  const int r = blockIdx.x * blockDim.x + threadIdx.x;
+  const int c = blockIdx.y;
+  if (r < n && r < c) A[r + (long long)c * lda] = 0.0;
+}
+
+__global__ void symmetrize_kernel(double* A, long long lda, int n) {
+  // tile transpose of the lower triangle into the upper one
+  __shared__ double t[32][33];
+  const int bi = blockIdx.x, bj = blockIdx.y;  // tile (row block bi, col block bj), want bi > bj or ==
+  if (bi < bj) return;
+  const int tx = threadIdx.x, ty = threadIdx.y;  // 32 x 8
+  for (int k = ty; k < 32; k += 8) {
+    const int r = bi * 32 + tx, c = bj * 32 + k;
+    t[k][tx] = (r < n && c < n) ? A[r + (long long)c * lda] : 0.0;
+  }
+  __syncthreads();
+  // write A[c][r] = A[r][c] for r > c
+  for (int k = ty; k < 32; k += 8) {
+    const int rr = bj * 32 + tx;  // destination row (= source col)
+    const int cc = bi * 32 + k;   // destination col (= source row)
+    if (rr < n && cc < n && cc > rr) A[rr + (long long)cc * lda] = t[tx][k];
+  }
+}
+
+constexpr size_t kLeafSmem = 2 * kLeaf * kLds * sizeof(double);
+
+template <auto Kern>
+void ensure_smem() {
+  static bool done = false;  // one flag per kernel
+  if (!done) {
+    cudaFuncSetAttribute(Kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kLeafSmem);
+    done = true;
+  }
+}
+
+int split_point(int n) {
+  int n1 = ((n / 2 + kLeaf - 1) / kLeaf) * kLeaf;
+  if (n1 >= n) n1 = n - kLeaf;
+  return n1;
+}
+
+}  // namespace
+
+cudaError_t trsm_rlt(const double* L, long long ldl, int n, double* A, long long lda, int m,
+                     cudaStream_t s) {
+  if (n <= 0 || m <= 0) return cudaSuccess;
+  if (n <= kLeaf) {
+    ensure_smem<trsm_rlt_leaf>();
+    trsm_rlt_leaf<<<(unsigned)ceil_div(m, kLeaf), kLeaf, kLeafSmem, s>>>(L, ldl, n, A, lda, m);
+    return cudaGetLastError();
+  }
+  const int n1 = split_point(n), n2 = n - n1;
+  cudaError_t e = trsm_rlt(L, ldl, n1, A, lda, m, s);
+  if (e != cudaSuccess) return e;
+  // A2 -= X1 * L21^T
+  GemmProblem p = make_gemm(m, n2, n1, -1.0, A, lda, L + n1, ldl, 1.0, A + n1 * lda, lda);
+  e = gemm(false, true, p, s);
+  if (e != cudaSuccess) return e;
+  return trsm_rlt(L + n1 + n1 * ldl, ldl, n2, A + n1 * lda, lda, m, s);
+}
+
+cudaError_t trsm_llt(const double* L, long long ldl, int n, double* B, long long ldb, int ncols,
+                     cudaStream_t s) {
+  if (n <= 0 || ncols <= 0) return cudaSuccess;
+  if (n <= kLeaf) {
+    ensure_smem<trsm_left_leaf<true>>();
+    trsm_left_leaf<true><<<(unsigned)ceil_div(ncols, kLeaf), kLeaf, kLeafSmem, s>>>(L, ldl, n, B, ldb, ncols);
+    return cudaGetLastError();
+  }
+  const int n1 = split_point(n), n2 = n - n1;
+  cudaError_t e = trsm_llt(L + n1 + n1 * ldl, ldl, n2, B + n1, ldb, ncols, s);
+  if (e != cudaSuccess) return e;
+  // B1 -= L21^T X2
+  GemmProblem p = make_gemm(n1, ncols, n2, -1.0, L + n1, ldl, B + n1, ldb, 1.0, B, ldb);
+  e = gemm(true, false, p, s);
+  if (e != cudaSuccess) return e;
+  return trsm_llt(L, ldl, n1, B, ldb, ncols, s);
+}
+
+cudaError_t trsm_lln(const double* L, long long ldl, int n, double* B, long long ldb, int ncols,
+                     cudaStream_t s) {
+  if (n <= 0 || ncols <= 0) return cudaSuccess;
+  if (n <= kLeaf) {
+    ensure_smem<trsm_left_leaf<false>>();
+    trsm_left_leaf<false><<<(unsigned)ceil_div(ncols, kLeaf), kLeaf, kLeafSmem, s>>>(L, ldl, n, B, ldb, ncols);
+    return cudaGetLastError();
+  }
+  const int n1 = split_point(n), n2 = n - n1;
+  cudaError_t e = trsm_lln(L, ldl, n1, B, ldb, ncols, s);
+  if (e != cudaSuccess) return e;
+  // B2 -= L21 X1
+  GemmProblem p = make_gemm(n2, ncols, n1, -1.0, L + n1, ldl, B, ldb, 1.0, B + n1, ldb);
+  e = gemm(false, false, p, s);
+  if (e != cudaSuccess) return e;
+  return trsm_lln(L + n1 + n1 * ldl, ldl, n2, B + n1, ldb, ncols, s);
+}
+
+static cudaError_t potrf_rec(double* A, long long lda, int n, int off, DevStatus* st,
+                             cudaStream_t s) {
+  if (n <= kLeaf) {
+    potf2_kernel<<<1, 256, 0, s>>>(A, lda, n, off, st);
+    return cudaGetLastError();
+  }
+  const int n1 = split_point(n), n2 = n - n1;
+  cudaError_t e = potrf_rec(A, lda, n1, off, st, s);
+  if (e != cudaSuccess) return e;
+  e = trsm_rlt(A, lda, n1, A + n1, lda, n2, s);  // A21 <- A21 L11^{-T}
+  if (e != cudaSuccess) return e;
+  // A22 -= A21 A21^T (lower triangle only)
+  GemmProblem p = make_gemm(n2, n2, n1, -1.0, A + n1, lda, A + n1, lda, 1.0,
+                            A + n1 + n1 * lda, lda);
+  p.mc = Mask::lower();
+  e = gemm(false, true, p, s);
+  if (e != cudaSuccess) return e;
+  return potrf_rec(A + n1 + n1 * lda, lda, n2, off + n1, st, s);
+}
+
+cudaError_t potrf_lower(double* A, long long lda, int n, DevStatus* st, cudaStream_t s) {
+  if (n <= 0) return cudaSuccess;
+  cudaError_t e = potrf_rec(A, lda, n, 0, st, s);
+  if (e != cudaSuccess) return e;
+  return zero_strict_upper(A, lda, n, s);
+}
+
+cudaError_t zero_strict_upper(double* A, long long lda, int n, cudaStream_t s) {
+  if (n <= 0) return cudaSuccess;
+  zero_upper_kernel<<<dim3((unsigned)ceil_div(n, 256), (unsigned)n), 256, 0, s>>>(A, lda, n);
+  return cudaGetLastError();
+}
+
+cudaError_t symmetrize_from_lower(double* A, long long lda, int n, cudaStream_t s) {
+  if (n <= 0) return cudaSuccess;
+  const unsigned t = (unsigned)ceil_div(n, 32);
+  symmetrize_kernel<<<dim3(t, t), dim3(32, 8), 0, s>>>(A, lda, n);
+  return cudaGetLastError();
+}
+
+}  // namespace bse

@@ -1,0 +1,41 @@
+// Dense triangular building blocks: recursive POTRF, TRSM, TRMM and the
+// congruence W = L^T M L, all expressed as small in-CTA leaf kernels plus the
+// masked DMMA GEMM engine.
+#pragma once
+#include <cuda_runtime.h>
+#include "gemm.cuh"
+
+namespace bse {
+
+// Device-side status written by factorization kernels.
+struct DevStatus {
+  int info;       // -1: ok; >= 0: index of the first non-positive pivot
+  int conv_fail;  // nonzero: an iterative kernel did not converge
+  double value;   // failing pivot value
+  double aux;     // spare (e.g. pivot margin)
+};
+
+// In-place lower Cholesky of the n x n matrix A (column-major, lda); the
+// strict upper triangle is zeroed.  Failure is reported through `st`
+// (first failing pivot, as kernels.py:56-61 in the reference).
+cudaError_t potrf_lower(double* A, long long lda, int n, DevStatus* st, cudaStream_t s);
+
+// A (m x n) <- A * L^{-T}, L n x n lower (right, lower, transposed).
+cudaError_t trsm_rlt(const double* L, long long ldl, int n, double* A, long long lda, int m,
+                     cudaStream_t s);
+
+// B (n x ncols) <- L^{-T} * B (left, lower, transposed: solves L^T X = B).
+cudaError_t trsm_llt(const double* L, long long ldl, int n, double* B, long long ldb, int ncols,
+                     cudaStream_t s);
+
+// B (n x ncols) <- L^{-1} * B (left, lower, no transpose).
+cudaError_t trsm_lln(const double* L, long long ldl, int n, double* B, long long ldb, int ncols,
+                     cudaStream_t s);
+
+// Zero the strict upper triangle of an n x n matrix.
+cudaError_t zero_strict_upper(double* A, long long lda, int n, cudaStream_t s);
+
+// Copy lower triangle to upper (make symmetric).
+cudaError_t symmetrize_from_lower(double* A, long long lda, int n, cudaStream_t s);
+
+}  // namespace bse

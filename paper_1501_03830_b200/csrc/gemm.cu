@@ -1,0 +1,286 @@
+// Masked FP64 GEMM engine: DMMA.8x8x4 tiles fed by a multistage cp.async
+// (LDGSTS) shared-memory pipeline.  See gemm.cuh for the contract.
+#include <cstdio>
+#include "gemm.cuh"
+
+namespace bse {
+namespace {
+
+constexpr int kPad = 4;  // row pad (doubles): keeps half-warp fragment loads conflict-free
+
+template <int BM, int BN, int BK, int WM, int WN, int STAGES, bool TA, bool TB>
+struct Cfg {
+  static constexpr int WARPS_M = BM / WM;
+  static constexpr int WARPS_N = BN / WN;
+  static constexpr int NT = WARPS_M * WARPS_N * 32;
+  // A: TA=false -> [BK][BM+pad] (m contiguous); TA=true -> [BM][BK+pad] (k contiguous)
+  static constexpr int A_LDS = TA ? (BK + kPad) : (BM + kPad);
+  static constexpr int A_ELEMS = TA ? BM * A_LDS : BK * A_LDS;
+  // B: TB=true -> [BK][BN+pad] (n contiguous); TB=false -> [BN][BK+pad] (k contiguous)
+  static constexpr int B_LDS = TB ? (BN + kPad) : (BK + kPad);
+  static constexpr int B_ELEMS = TB ? BK * B_LDS : BN * B_LDS;
+  static constexpr int STAGE = A_ELEMS + B_ELEMS;
+  static constexpr size_t SMEM = size_t(STAGES) * STAGE * sizeof(double);
+};
+
+// Load a ROWS (contiguous) x COLS (strided) tile; element (r, c) lives at
+// g[(r0 + r) + (c0 + c) * ld] and lands at s[c * LDS + r].  Out-of-range
+// elements are zero-filled.
+template <int ROWS, int COLS, int LDS, int VEC, int NT>
+BSE_DEV void load_tile(double* s, const double* g, long long ld, int r0, int c0, int rmax,
+                       int cmax, int tid) {
+  constexpr int CPR = ROWS / VEC;  // chunks per strided line
+  constexpr int CHUNKS = CPR * COLS;
+#pragma unroll
+  for (int id = tid; id < CHUNKS; id += NT) {
+    const int c = id / CPR;
+    const int r = (id % CPR) * VEC;
+    const int gr = r0 + r, gc = c0 + c;
+    double* sp = s + c * LDS + r;
+    const bool cok = gc < cmax;
+    const double* gp = g + (cok ? (long long)gc * ld : 0);
+    if constexpr (VEC == 2) {
+      const bool v0 = cok && gr < rmax, v1 = cok && gr + 1 < rmax;
+      if (v0 && v1) {
+        cp_async16(sp, gp + gr, true);
+      } else {
+        cp_async8(sp, v0 ? gp + gr : g, v0);
+        cp_async8(sp + 1, v1 ? gp + gr + 1 : g, v1);
+      }
+    } else {
+      const bool v0 = cok && gr < rmax;
+      cp_async8(sp, v0 ? gp + gr : g, v0);
+    }
+  }
+}
+
+BSE_DEV double apply_mask(double v, int d, bool inb, const Mask& m) {
+  if (m.unit && d == 0) return inb ? 1.0 : 0.0;
+  return (d < m.lo || d > m.hi) ? 0.0 : v;
+}
+
+template <int BM, int BN, int BK, int WM, int WN, int STAGES, bool TA, bool TB, int VEC>
+BSE_DEV void gemm_tile(const GemmProblem& p, int m0, int n0, double* smem) {
+  using C = Cfg<BM, BN, BK, WM, WN, STAGES, TA, TB>;
+  const int M = p.M, N = p.N, K = p.K;
+  if (m0 >= M || n0 >= N) return;
+  const int tid = threadIdx.x;
+  const int lane = tid & 31, warp = tid >> 5;
+  const int wm = warp % C::WARPS_M, wn = warp / C::WARPS_M;
+  const int mlast = min(m0 + BM, M) - 1, nlast = min(n0 + BN, N) - 1;
+
+  // Output mask: skip tiles with no writable element.
+  {
+    const long long dmin = (long long)n0 - mlast, dmax = (long long)nlast - m0;
+    if (dmax < p.mc.lo || dmin > p.mc.hi) return;
+  }
+
+  // k-range implied by the operand masks.
+  long long kb = 0, ke = K;
+  {
+    const Mask& a = p.ma;
+    const long long lo = a.unit ? min(a.lo, 0) : a.lo, hi = a.unit ? max(a.hi, 0) : a.hi;
+    if (!TA) { kb = max(kb, (long long)m0 + lo); ke = min(ke, (long long)mlast + hi + 1); }
+    else     { kb = max(kb, (long long)m0 - hi); ke = min(ke, (long long)mlast - lo + 1); }
+    const Mask& b = p.mb;
+    const long long blo = b.unit ? min(b.lo, 0) : b.lo, bhi = b.unit ? max(b.hi, 0) : b.hi;
+    if (!TB) { kb = max(kb, (long long)n0 - bhi); ke = min(ke, (long long)nlast - blo + 1); }
+    else     { kb = max(kb, (long long)n0 + blo); ke = min(ke, (long long)nlast + bhi + 1); }
+  }
+  kb = (kb / BK) * BK;
+  const int k_begin = (int)kb;
+  const int ntiles = ke > kb ? (int)ceil_div(ke - kb, BK) : 0;
+
+  constexpr int MI = WM / 8, NJ = WN / 8;
+  double acc[MI][NJ][2];
+#pragma unroll
+  for (int i = 0; i < MI; ++i)
+#pragma unroll
+    for (int j = 0; j < NJ; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+
+  auto load_stage = [&](int st, int kt) {
+    double* sA = smem + st * C::STAGE;
+    double* sB = sA + C::A_ELEMS;
+    const int k0 = k_begin + kt * BK;
+    if constexpr (!TA) load_tile<BM, BK, C::A_LDS, VEC, C::NT>(sA, p.A, p.lda, m0, k0, M, K, tid);
+    else               load_tile<BK, BM, C::A_LDS, VEC, C::NT>(sA, p.A, p.lda, k0, m0, K, M, tid);
+    if constexpr (TB)  load_tile<BN, BK, C::B_LDS, VEC, C::NT>(sB, p.B, p.ldb, n0, k0, N, K, tid);
+    else               load_tile<BK, BN, C::B_LDS, VEC, C::NT>(sB, p.B, p.ldb, k0, n0, K, N, tid);
+  };
+
+#pragma unroll
+  for (int s = 0; s < STAGES - 1; ++s) {
+    if (s < ntiles) load_stage(s, s);
+    cp_async_commit();
+  }
+
+  const bool maskA_on = p.ma.active(), maskB_on = p.mb.active();
+  const int am_base = wm * WM + (lane >> 2);  // + i*8
+  const int bn_base = wn * WN + (lane >> 2);  // + j*8
+  const int kl = lane & 3;
+
+  for (int kt = 0; kt < ntiles; ++kt) {
+    cp_async_wait<STAGES - 2>();
+    __syncthreads();
+    {
+      const int nk = kt + STAGES - 1;
+      if (nk < ntiles) load_stage(nk % STAGES, nk);
+      cp_async_commit();
+    }
+    const double* sA = smem + (kt % STAGES) * C::STAGE;
+    const double* sB = sA + C::A_ELEMS;
+    const int k0 = k_begin + kt * BK;
+
+    // Does this k-tile straddle a mask boundary?
+    bool needA = false, needB = false;
+    if (maskA_on) {
+      const Mask& a = p.ma;
+      long long dmin, dmax;
+      if (!TA) { dmin = (long long)k0 - mlast; dmax = (long long)k0 + BK - 1 - m0; }
+      else     { dmin = (long long)m0 - (k0 + BK - 1); dmax = (long long)mlast - k0; }
+      needA = dmin < a.lo || dmax > a.hi || (a.unit && dmin <= 0 && dmax >= 0);
+    }
+    if (maskB_on) {
+      const Mask& b = p.mb;
+      long long dmin, dmax;
+      if (!TB) { dmin = (long long)n0 - (k0 + BK - 1); dmax = (long long)nlast - k0; }
+      else     { dmin = (long long)k0 - nlast; dmax = (long long)k0 + BK - 1 - n0; }
+      needB = dmin < b.lo || dmax > b.hi || (b.unit && dmin <= 0 && dmax >= 0);
+    }
+
+#pragma unroll
+    for (int kk = 0; kk < BK; kk += 4) {
+      double af[MI], bf[NJ];
+#pragma unroll
+      for (int i = 0; i < MI; ++i) {
+        const int ml = am_base + i * 8, kq = kk + kl;
+        af[i] = TA ? sA[ml * C::A_LDS + kq] : sA[kq * C::A_LDS + ml];
+      }
+#pragma unroll
+      for (int j = 0; j < NJ; ++j) {
+        const int nl = bn_base + j * 8, kq = kk + kl;
+        bf[j] = TB ? sB[kq * C::B_LDS + nl] : sB[nl * C::B_LDS + kq];
+      }
+      if (needA) {
+#pragma unroll
+        for (int i = 0; i < MI; ++i) {
+          const int gm = m0 + am_base + i * 8, gk = k0 + kk + kl;
+          const int d = TA ? gm - gk : gk - gm;
+          af[i] = apply_mask(af[i], d, gm < M && gk < K, p.ma);
+        }
+      }
+      if (needB) {
+#pragma unroll
+        for (int j = 0; j < NJ; ++j) {
+          const int gn = n0 + bn_base + j * 8, gk = k0 + kk + kl;
+          const int d = TB ? gk - gn : gn - gk;
+          bf[j] = apply_mask(bf[j], d, gn < N && gk < K, p.mb);
+        }
+      }
+#pragma unroll
+      for (int i = 0; i < MI; ++i)
+#pragma unroll
+        for (int j = 0; j < NJ; ++j) dmma8x8x4(acc[i][j], af[i], bf[j]);
+    }
+  }
+  cp_async_wait<0>();
+
+  // Epilogue: C = alpha*acc + beta*C under the output mask.
+  const double alpha = p.alpha, beta = p.beta;
+#pragma unroll
+  for (int i = 0; i < MI; ++i) {
+    const int gm = m0 + wm * WM + i * 8 + (lane >> 2);
+    if (gm >= M) continue;
+#pragma unroll
+    for (int j = 0; j < NJ; ++j) {
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const int gn = n0 + wn * WN + j * 8 + kl * 2 + e;
+        if (gn >= N) continue;
+        const int d = gn - gm;
+        if (d < p.mc.lo || d > p.mc.hi) continue;
+        double* cp = p.C + gm + (long long)gn * p.ldc;
+        double v = alpha * acc[i][j][e];
+        if (beta != 0.0) v += beta * *cp;
+        *cp = v;
+      }
+    }
+  }
+}
+
+template <int BM, int BN, int BK, int WM, int WN, int STAGES, bool TA, bool TB, int VEC>
+__global__ void __launch_bounds__(Cfg<BM, BN, BK, WM, WN, STAGES, TA, TB>::NT)
+    gemm_single_kernel(const GemmProblem p) {
+  extern __shared__ __align__(16) double smem[];
+  gemm_tile<BM, BN, BK, WM, WN, STAGES, TA, TB, VEC>(p, blockIdx.x * BM, blockIdx.y * BN, smem);
+}
+
+template <int BM, int BN, int BK, int WM, int WN, int STAGES, bool TA, bool TB, int VEC>
+__global__ void __launch_bounds__(Cfg<BM, BN, BK, WM, WN, STAGES, TA, TB>::NT)
+    gemm_grouped_kernel(const GemmProblem* __restrict__ probs) {
+  extern __shared__ __align__(16) double smem[];
+  const GemmProblem p = probs[blockIdx.z];
+  gemm_tile<BM, BN, BK, WM, WN, STAGES, TA, TB, VEC>(p, blockIdx.x * BM, blockIdx.y * BN, smem);
+}
+
+template <int BM, int BN, int BK, int WM, int WN, int STAGES, bool TA, bool TB, int VEC>
+cudaError_t launch(const GemmProblem* single, const GemmProblem* grouped, int count, int maxM,
+                   int maxN, cudaStream_t s) {
+  using C = Cfg<BM, BN, BK, WM, WN, STAGES, TA, TB>;
+  static bool attr_done = false;  // per-instantiation, set once per process
+  if (!attr_done) {
+    cudaError_t e = cudaFuncSetAttribute(gemm_single_kernel<BM, BN, BK, WM, WN, STAGES, TA, TB, VEC>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM);
+    if (e != cudaSuccess) return e;
+    e = cudaFuncSetAttribute(gemm_grouped_kernel<BM, BN, BK, WM, WN, STAGES, TA, TB, VEC>,
+                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM);
+    if (e != cudaSuccess) return e;
+    attr_done = true;
+  }
+  dim3 grid((unsigned)ceil_div(maxM, BM), (unsigned)ceil_div(maxN, BN), (unsigned)count);
+  if (grid.x == 0 || grid.y == 0 || count == 0) return cudaSuccess;
+  if (single)
+    gemm_single_kernel<BM, BN, BK, WM, WN, STAGES, TA, TB, VEC><<<grid, C::NT, C::SMEM, s>>>(*single);
+  else
+    gemm_grouped_kernel<BM, BN, BK, WM, WN, STAGES, TA, TB, VEC><<<grid, C::NT, C::SMEM, s>>>(grouped);
+  return cudaGetLastError();
+}
+
+template <bool TA, bool TB>
+cudaError_t dispatch(int cfg, int vec, const GemmProblem* single, const GemmProblem* grouped,
+                     int count, int maxM, int maxN, cudaStream_t s) {
+  if (vec == 2) {
+    if (cfg == 0) return launch<128, 128, 16, 64, 32, 4, TA, TB, 2>(single, grouped, count, maxM, maxN, s);
+    return launch<64, 64, 16, 32, 32, 4, TA, TB, 2>(single, grouped, count, maxM, maxN, s);
+  }
+  return launch<64, 64, 16, 32, 32, 4, TA, TB, 1>(single, grouped, count, maxM, maxN, s);
+}
+
+cudaError_t dispatch_all(bool ta, bool tb, int cfg, int vec, const GemmProblem* single,
+                         const GemmProblem* grouped, int count, int maxM, int maxN, cudaStream_t s) {
+  if (!ta && !tb) return dispatch<false, false>(cfg, vec, single, grouped, count, maxM, maxN, s);
+  if (!ta && tb) return dispatch<false, true>(cfg, vec, single, grouped, count, maxM, maxN, s);
+  if (ta && !tb) return dispatch<true, false>(cfg, vec, single, grouped, count, maxM, maxN, s);
+  return dispatch<true, true>(cfg, vec, single, grouped, count, maxM, maxN, s);
+}
+
+bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
+
+}  // namespace
+
+cudaError_t gemm(bool transA, bool transB, const GemmProblem& p, cudaStream_t s) {
+  if (p.M <= 0 || p.N <= 0) return cudaSuccess;
+  const bool v2 = aligned16(p.A) && aligned16(p.B) && ((p.lda | p.ldb) & 1) == 0;
+  const long long big_tiles = ceil_div(p.M, 128) * ceil_div(p.N, 128);
+  const int cfg = (v2 && big_tiles >= 120) ? 0 : 1;
+  return dispatch_all(transA, transB, cfg, v2 ? 2 : 1, &p, nullptr, 1, p.M, p.N, s);
+}
+
+cudaError_t gemm_grouped(bool transA, bool transB, const GemmProblem* probs_dev, int count,
+                         int maxM, int maxN, cudaStream_t s) {
+  // Grouped problems may mix alignments (e.g. D&C nodes at odd offsets): use
+  // the 8-byte path, which is always legal.
+  return dispatch_all(transA, transB, 1, 1, nullptr, probs_dev, count, maxM, maxN, s);
+}
+
+}  // namespace bse

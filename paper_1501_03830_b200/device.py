@@ -1,0 +1,79 @@
+"""Device plumbing: torch owns HBM allocations and streams; the C ABI does the
+math.  Matrices live column-major: an (rows x cols) matrix with leading
+dimension ld is a torch tensor of shape (cols, ld) whose row c is column c.
+"""
+from __future__ import annotations
+
+import ctypes as C
+
+import numpy as np
+
+from . import _lib
+
+
+def _torch():
+    import torch
+    return torch
+
+
+def require_cuda():
+    torch = _torch()
+    if not torch.cuda.is_available():
+        raise RuntimeError("paper_1501_03830_b200 needs a CUDA device (sm_100a); "
+                           "there is no CPU fallback")
+    return torch
+
+
+def stream_ptr(device=None) -> int:
+    torch = _torch()
+    return torch.cuda.current_stream(device).cuda_stream
+
+
+def colmajor_empty(rows: int, cols: int, device, ld: int | None = None, zero=False):
+    """Column-major (rows x cols) FP64 buffer; returns (tensor, ld)."""
+    torch = _torch()
+    ld = max(1, rows if ld is None else ld)
+    ld += ld & 1  # even leading dimension keeps 16-byte cp.async legal
+    f = torch.zeros if zero else torch.empty
+    return f((max(cols, 1), ld), dtype=torch.float64, device=device), ld
+
+
+def to_device_colmajor(a: np.ndarray, device, ld: int | None = None):
+    """Upload a 2-D float64 numpy array as a column-major device matrix."""
+    torch = _torch()
+    a = np.asarray(a, dtype=np.float64)
+    rows, cols = a.shape
+    t, ld = colmajor_empty(rows, cols, device, ld, zero=True)
+    if rows and cols:
+        t[:cols, :rows].copy_(torch.from_numpy(np.ascontiguousarray(a.T)))
+    return t, ld
+
+
+def from_device_colmajor(t, rows: int, cols: int) -> np.ndarray:
+    return t[:cols, :rows].T.cpu().numpy()
+
+
+def view_colmajor(t, rows: int, cols: int):
+    """Torch (rows x cols) view of a column-major buffer (no copy)."""
+    return t[:cols, :rows].T
+
+
+def ptr(t) -> int:
+    return t.data_ptr()
+
+
+def check(status: int, what: str):
+    if status != _lib.BSE_OK:
+        raise RuntimeError(f"{what} failed with status {status}: {_lib.last_error()}")
+
+
+def mask_array(ma=None, mb=None, mc=None):
+    big = 1 << 30
+    out = []
+    for m in (ma, mb, mc):
+        if m is None:
+            out += [-big, big, 0]
+        else:
+            lo, hi, unit = m
+            out += [-big if lo is None else lo, big if hi is None else hi, unit]
+    return (C.c_int32 * 9)(*out)
