@@ -1,2 +1,24 @@
-"""B200-native (sm_100a) structure-preserving Bethe-Salpeter eigensolver."""
+"""B200-native (sm_100a) structure-preserving Bethe-Salpeter eigensolver.
+
+Drop-in for the solver path of the reference package ``bse`` (bse-solver
+0.1.0, pkg/src/bse/__init__.py:11-40): the same names and signatures for the
+types, the structural transforms and the solvers, with the numerical core in
+the CUDA library libbse_b200.so (C ABI: include/bse_b200.h).
+"""
+from .solvers import polish, real_embedding, solve_complex, solve_pair_device, solve_real
+from .spectra import absorption_device, absorption_spectrum
+from .types import (BseOperator, ConvergenceError, DipoleData, FullEigensystem,
+                    NotPositiveDefinite, PositiveEigensystem, SpectrumCurve, ValidationReport,
+                    assemble_h, build_m, conditioning_warnings, default_grid, dos_dominance,
+                    expand_full, make_operator, residual_metrics)
+
 __version__ = "0.1.0"
+
+__all__ = [
+    "BseOperator", "FullEigensystem", "PositiveEigensystem", "ValidationReport",
+    "assemble_h", "make_operator", "residual_metrics", "build_m", "expand_full",
+    "ConvergenceError", "NotPositiveDefinite", "solve_complex", "solve_real",
+    "DipoleData", "SpectrumCurve", "absorption_spectrum", "default_grid", "dos_dominance",
+    "conditioning_warnings", "real_embedding", "polish", "solve_pair_device",
+    "absorption_device", "__version__",
+]

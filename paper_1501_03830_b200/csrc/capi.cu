@@ -85,6 +85,121 @@ int bse_potrf_dev(int64_t n, double* dA, int64_t lda, void* stream, bse_info* in
   return BSE_OK;
 }
 
+size_t bse_solve_workspace_bytes(int64_t n, int flags) {
+  return n > 0 ? bse::solve_bytes((int)n, flags) : 0;
+}
+
+static int map_solve_status(const bse::SolveStatus& st, bse_info* info) {
+  if (st.code == 0) return BSE_OK;
+  if (info) {
+    info->pivot_index = st.pivot_index;
+    info->pivot_value = st.pivot_value;
+    info->failed_factor = st.failed_factor;
+  }
+  return fail(BSE_NOT_POSITIVE_DEFINITE, st.failed_factor == 1 ? "A+B is not positive definite"
+                                                               : "A-B is not positive definite");
+}
+
+int bse_solve_spd_pair_dev(int64_t n, const double* dM, int64_t ldm, const double* dK,
+                           int64_t ldk, double* dLam, double* dX1, int64_t ldx1, double* dX2,
+                           int64_t ldx2, void* dWork, size_t work_bytes, int flags, void* stream,
+                           bse_info* info) {
+  if (n < 0 || ldm < n || ldk < n || ldx1 < n || ldx2 < n)
+    return fail(BSE_BAD_ARGUMENT, "bad dimension");
+  if (n > 0 && work_bytes < bse::solve_bytes((int)n, flags))
+    return fail(BSE_BAD_ARGUMENT, "workspace too small (see bse_solve_workspace_bytes)");
+  bse::SolveStatus st{};
+  BSE_TRY_CUDA(bse::solve_spd_pair((int)n, dM, ldm, dK, ldk, dLam, dX1, ldx1, dX2, ldx2, dWork,
+                                   work_bytes, flags, (cudaStream_t)stream, &st),
+               "solve");
+  return map_solve_status(st, info);
+}
+
+int bse_solve_spd_pair_host(int64_t n, const double* M, int64_t ldm, const double* K,
+                            int64_t ldk, double* lam, double* X1, int64_t ldx1, double* X2,
+                            int64_t ldx2, int flags, bse_info* info) {
+  if (n < 0 || ldm < n || ldk < n || ldx1 < n || ldx2 < n)
+    return fail(BSE_BAD_ARGUMENT, "bad dimension");
+  if (n == 0) return BSE_OK;
+  cudaStream_t s;
+  BSE_TRY_CUDA(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking), "stream");
+  const long long ld = bse::pad_ld(n);
+  const size_t mat = sizeof(double) * (size_t)ld * n;
+  const size_t wb = bse::solve_bytes((int)n, flags);
+  const size_t lam_bytes = ((sizeof(double) * n + 255) / 256) * 256;
+  char* buf = nullptr;
+  cudaError_t e = cudaMallocAsync((void**)&buf, 4 * mat + lam_bytes + wb, s);
+  if (e != cudaSuccess) {
+    cudaStreamDestroy(s);
+    return cuda_fail(e, "alloc");
+  }
+  double* dM = (double*)buf;
+  double* dK = (double*)(buf + mat);
+  double* dX1 = (double*)(buf + 2 * mat);
+  double* dX2 = (double*)(buf + 3 * mat);
+  double* dLam = (double*)(buf + 4 * mat);
+  void* dW = buf + 4 * mat + lam_bytes;
+  bse::SolveStatus st{};
+  const size_t row = sizeof(double) * (size_t)n;
+  e = cudaMemcpy2DAsync(dM, ld * 8, M, ldm * 8, row, n, cudaMemcpyHostToDevice, s);
+  if (e == cudaSuccess)
+    e = cudaMemcpy2DAsync(dK, ld * 8, K, ldk * 8, row, n, cudaMemcpyHostToDevice, s);
+  if (e == cudaSuccess)
+    e = bse::solve_spd_pair((int)n, dM, ld, dK, ld, dLam, dX1, ld, dX2, ld, dW, wb, flags, s, &st);
+  if (e == cudaSuccess) e = cudaMemcpyAsync(lam, dLam, row, cudaMemcpyDeviceToHost, s);
+  if (e == cudaSuccess)
+    e = cudaMemcpy2DAsync(X1, ldx1 * 8, dX1, ld * 8, row, n, cudaMemcpyDeviceToHost, s);
+  if (e == cudaSuccess)
+    e = cudaMemcpy2DAsync(X2, ldx2 * 8, dX2, ld * 8, row, n, cudaMemcpyDeviceToHost, s);
+  cudaFreeAsync(buf, s);
+  cudaError_t e2 = cudaStreamSynchronize(s);
+  cudaStreamDestroy(s);
+  BSE_TRY_CUDA(e, "solve_host");
+  BSE_TRY_CUDA(e2, "solve_host sync");
+  return map_solve_status(st, info);
+}
+
+size_t bse_syevd_workspace_bytes(int64_t n, int flags) {
+  return n > 0 ? bse::syevd_bytes((int)n, flags) : 0;
+}
+
+int bse_syevd_dev(int64_t n, double* dA, int64_t lda, double* dW, double* dZ, int64_t ldz,
+                  void* dWork, size_t work_bytes, int flags, void* stream) {
+  if (n < 0 || lda < n || ldz < n) return fail(BSE_BAD_ARGUMENT, "bad dimension");
+  if (n > 0 && work_bytes < bse::syevd_bytes((int)n, flags))
+    return fail(BSE_BAD_ARGUMENT, "workspace too small (see bse_syevd_workspace_bytes)");
+  BSE_TRY_CUDA(bse::syevd((int)n, dA, lda, dW, dZ, ldz, dWork, work_bytes, flags,
+                          (cudaStream_t)stream),
+               "syevd");
+  return BSE_OK;
+}
+
+size_t bse_stedc_workspace_bytes(int64_t n) {
+  return n > 0 ? bse::stedc_bytes((int)n) + 4096 : 0;
+}
+
+int bse_stedc_dev(int64_t n, double* dD, double* dE, double* dQ, int64_t ldq, void* dWork,
+                  size_t work_bytes, void* stream) {
+  if (n < 0 || ldq < n) return fail(BSE_BAD_ARGUMENT, "bad dimension");
+  if (n == 0) return BSE_OK;
+  if (work_bytes < bse::stedc_bytes((int)n)) return fail(BSE_BAD_ARGUMENT, "workspace too small");
+  bse::Arena a{static_cast<char*>(dWork), work_bytes, 0, false};
+  bse::StedcWork w = bse::stedc_carve(a, (int)n);
+  BSE_TRY_CUDA(bse::stedc((int)n, dD, dE, dD, dQ, ldq, w, (cudaStream_t)stream), "stedc");
+  return BSE_OK;
+}
+
+int bse_absorption_dev(int64_t n, const double* dLam, const double* dX1c, int64_t ldx1,
+                       const double* dX2c, int64_t ldx2, const double* dDr, const double* dDl,
+                       int64_t ngrid, const double* dGrid, double sigma, double* dWeights,
+                       double* dValues, double* dDefect, double* dMinPair, void* stream) {
+  if (n < 0 || ngrid < 0 || !(sigma > 0.0)) return fail(BSE_BAD_ARGUMENT, "bad argument");
+  BSE_TRY_CUDA(bse::absorption((int)n, dLam, dX1c, ldx1, dX2c, ldx2, dDr, dDl, (int)ngrid, dGrid,
+                               sigma, dWeights, dValues, dDefect, dMinPair, (cudaStream_t)stream),
+               "absorption");
+  return BSE_OK;
+}
+
 int bse_peak_fp64(int which, int blocks, int iters, int reps, double* flops, double* ms) {
   double* sink = nullptr;
   BSE_TRY_CUDA(cudaMalloc(&sink, 256 * sizeof(double)), "alloc");

@@ -1,0 +1,93 @@
+// Two-stage symmetric eigensolver (full -> band -> tridiagonal -> divide and
+// conquer -> WY back-transforms).  Replaces the reference's tridiagonal route
+// (kernels.py:89-137 Householder reduction, :460-535 bisection + inverse
+// iteration, :123-137 reflector-by-reflector back-transform).
+#pragma once
+#include <cuda_runtime.h>
+#include "dense.cuh"
+#include "workspace.cuh"
+
+namespace bse {
+
+constexpr int kMaxPanel = 64;  // SY2SB bandwidth b (<= 64)
+
+struct Sy2sbScratch {
+  double* vwv = nullptr;  // m x 3b: [V | W | V]
+  long long ldvwv = 0;
+  double* y = nullptr;    // m x b
+  long long ldy = 0;
+  double* z = nullptr;    // b x b
+  double* z2 = nullptr;   // b x b
+  double* red = nullptr;  // panel-QR grid reduction (2 * 148 * (2 + 2b))
+  unsigned* bar = nullptr;
+  double* splitk_ws = nullptr;  // 48 * b * b
+  GemmProblem* probs = nullptr; // 64 problems
+};
+
+cudaError_t sy2sb(double* A, long long lda, int n, int b, double* Vall, long long ldv,
+                  double* Tall, const Sy2sbScratch& w, int num_sms, cudaStream_t s);
+cudaError_t extract_band(const double* A, long long lda, int n, int b, double* AB, int ldab,
+                         cudaStream_t s);
+
+// Bulge chasing on the band (lower storage, ldab = 2b): d, e out; reflectors
+// of sweep s, step j stored at V2[(s*maxsteps + j) * b], tau2[s*maxsteps + j].
+int sb2st_maxsteps(int n, int b);
+cudaError_t sb2st(double* AB, int ldab, int n, int b, double* d, double* e, double* V2,
+                  double* tau2, int* progress, int num_sms, cudaStream_t s);
+
+// Q2 back-transform: Z <- Q2 Z (Z n x ncols).  Groups of g sweeps form
+// compact-WY blocks; Vblk/VTblk sized by q2_block_bytes().
+size_t q2_block_doubles(int n, int b, int g);
+cudaError_t q2_build(int n, int b, int g, const double* V2, const double* tau2, double* Vblk,
+                     double* VTblk, cudaStream_t s);
+cudaError_t q2_apply(int n, int b, int g, const double* Vblk, const double* VTblk, double* Z,
+                     long long ldz, int ncols, cudaStream_t s);
+
+// Q1 back-transform: Z <- Q1 Z using the SY2SB panels.
+cudaError_t q1_apply(int n, int b, const double* Vall, long long ldv, const double* Tall,
+                     double* Z, long long ldz, int ncols, double* ybuf, double* y2buf,
+                     cudaStream_t s);
+
+// Tridiagonal divide and conquer.
+struct StedcWork {
+  double* Qa = nullptr;  // n x n (ld)
+  double* Qb = nullptr;
+  double* U = nullptr;
+  long long ld = 0;
+  double* Da = nullptr;  // n
+  double* Db = nullptr;
+  double* ds = nullptr;   // sorted poles (n)
+  double* zs = nullptr;   // sorted z (n)
+  double* dk = nullptr;   // kept poles (n)
+  double* zk = nullptr;   // kept z (n)
+  double* zh = nullptr;   // per-node rho stash at [lo]
+  double* zh2 = nullptr;  // zhat (n)
+  double* val = nullptr;  // roots [0,K) and deflated values (from the back)
+  double* tau = nullptr;  // secular offsets (n)
+  int* org = nullptr;     // secular origins (n)
+  int* perm = nullptr;    // sorted -> local original (n)
+  int* keep = nullptr;    // kept sorted indices (n)
+  int* defl = nullptr;    // deflated sorted indices (n)
+  int* pos = nullptr;     // output column for each (roots then deflated) (n)
+  int* rotp = nullptr;    // rotation pairs (n)
+  int* rotq = nullptr;
+  double* rotc = nullptr;
+  double* rots = nullptr;
+  int* counts = nullptr;  // per node: K, ndefl, nrot (3 * n)
+  GemmProblem* probs = nullptr;  // 2 * n
+  double* scal = nullptr;  // scaling scalar(s)
+};
+size_t stedc_bytes(int n);
+StedcWork stedc_carve(Arena& a, int n);
+// Eigenvalues ascending into w (may alias d), vectors into Q (ldq).
+cudaError_t stedc(int n, double* d, double* e, double* w, double* Q, long long ldq,
+                  const StedcWork& ws, cudaStream_t s);
+
+// Full pipeline on a symmetric matrix (lower triangle of A read, destroyed).
+size_t syevd_bytes(int n, int flags);
+cudaError_t syevd(int n, double* A, long long lda, double* w, double* Z, long long ldz,
+                  void* work, size_t work_bytes, int flags, cudaStream_t s);
+
+int device_sm_count();
+
+}  // namespace bse

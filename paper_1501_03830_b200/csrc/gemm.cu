@@ -266,7 +266,64 @@ cudaError_t dispatch_all(bool ta, bool tb, int cfg, int vec, const GemmProblem* 
 
 bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
 
+__global__ void splitk_reduce_kernel(const double* __restrict__ ws, int splits, int M, int N,
+                                     double alpha, double beta, double* C, long long ldc) {
+  const long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (idx >= (long long)M * N) return;
+  const int r = (int)(idx % M), c = (int)(idx / M);
+  double acc = 0.0;
+  for (int s = 0; s < splits; ++s) acc += ws[(long long)s * M * N + idx];
+  double* cp = C + r + (long long)c * ldc;
+  *cp = alpha * acc + (beta != 0.0 ? beta * *cp : 0.0);
+}
+
 }  // namespace
+
+cudaError_t gemm_splitk(bool transA, bool transB, const GemmProblem& p, int splits, double* ws,
+                        GemmProblem* probs_dev_scratch, cudaStream_t s) {
+  if (p.M <= 0 || p.N <= 0) return cudaSuccess;
+  if (splits <= 1 || p.K < 64 * splits) return gemm(transA, transB, p, s);
+  // chunk K in multiples of 16 so every slice keeps cp.async alignment
+  int chunk = (int)ceil_div(p.K, splits);
+  chunk = (int)ceil_div(chunk, 16) * 16;
+  splits = (int)ceil_div(p.K, chunk);
+  GemmProblem hp[64];
+  if (splits > 64) return cudaErrorInvalidValue;
+  for (int i = 0; i < splits; ++i) {
+    GemmProblem q = p;
+    const int k0 = i * chunk;
+    q.K = min(chunk, p.K - k0);
+    // A: op(A) is M x K -> advance along k
+    q.A = transA ? p.A + k0 : p.A + (long long)k0 * p.lda;
+    q.B = transB ? p.B + (long long)k0 * p.ldb : p.B + k0;
+    // masks are expressed in stored coordinates relative to the view origin
+    if (!transA) { q.ma.lo = p.ma.lo == kNoMaskLo ? kNoMaskLo : p.ma.lo - k0;
+                   q.ma.hi = p.ma.hi == kNoMaskHi ? kNoMaskHi : p.ma.hi - k0; }
+    else         { q.ma.lo = p.ma.lo == kNoMaskLo ? kNoMaskLo : p.ma.lo + k0;
+                   q.ma.hi = p.ma.hi == kNoMaskHi ? kNoMaskHi : p.ma.hi + k0; }
+    if (!transB) { q.mb.lo = p.mb.lo == kNoMaskLo ? kNoMaskLo : p.mb.lo + k0;
+                   q.mb.hi = p.mb.hi == kNoMaskHi ? kNoMaskHi : p.mb.hi + k0; }
+    else         { q.mb.lo = p.mb.lo == kNoMaskLo ? kNoMaskLo : p.mb.lo - k0;
+                   q.mb.hi = p.mb.hi == kNoMaskHi ? kNoMaskHi : p.mb.hi - k0; }
+    if (q.ma.unit || q.mb.unit) return cudaErrorInvalidValue;  // unit diag not split-safe
+    q.C = ws + (long long)i * p.M * p.N;
+    q.ldc = p.M;
+    q.alpha = 1.0;
+    q.beta = 0.0;
+    q.mc = Mask::none();
+    hp[i] = q;
+  }
+  cudaError_t e = cudaMemcpyAsync(probs_dev_scratch, hp, sizeof(GemmProblem) * splits,
+                                  cudaMemcpyHostToDevice, s);
+  if (e != cudaSuccess) return e;
+  const bool v2 = aligned16(p.A) && aligned16(p.B) && ((p.lda | p.ldb) & 1) == 0;
+  e = gemm_grouped(transA, transB, probs_dev_scratch, splits, p.M, p.N, s, v2);
+  if (e != cudaSuccess) return e;
+  const long long tot = (long long)p.M * p.N;
+  splitk_reduce_kernel<<<(unsigned)ceil_div(tot, 256), 256, 0, s>>>(ws, splits, p.M, p.N, p.alpha,
+                                                                     p.beta, p.C, p.ldc);
+  return cudaGetLastError();
+}
 
 cudaError_t gemm(bool transA, bool transB, const GemmProblem& p, cudaStream_t s) {
   if (p.M <= 0 || p.N <= 0) return cudaSuccess;
@@ -277,10 +334,12 @@ cudaError_t gemm(bool transA, bool transB, const GemmProblem& p, cudaStream_t s)
 }
 
 cudaError_t gemm_grouped(bool transA, bool transB, const GemmProblem* probs_dev, int count,
-                         int maxM, int maxN, cudaStream_t s) {
-  // Grouped problems may mix alignments (e.g. D&C nodes at odd offsets): use
-  // the 8-byte path, which is always legal.
-  return dispatch_all(transA, transB, 1, 1, nullptr, probs_dev, count, maxM, maxN, s);
+                         int maxM, int maxN, cudaStream_t s, bool all_aligned16) {
+  // Grouped problems may mix alignments (e.g. D&C nodes at odd offsets): the
+  // 8-byte path is always legal; callers that guarantee 16-byte alignment of
+  // every operand and even leading dimensions get the vectorised loads.
+  return dispatch_all(transA, transB, 1, all_aligned16 ? 2 : 1, nullptr, probs_dev, count, maxM,
+                      maxN, s);
 }
 
 }  // namespace bse

@@ -44,7 +44,14 @@ cudaError_t gemm(bool transA, bool transB, const GemmProblem& p, cudaStream_t s)
 // Grouped: `probs` is a DEVICE array of `count` problems sharing (transA,
 // transB); maxM/maxN bound the grid.  Masks inside each problem are honoured.
 cudaError_t gemm_grouped(bool transA, bool transB, const GemmProblem* probs_dev, int count,
-                         int maxM, int maxN, cudaStream_t s);
+                         int maxM, int maxN, cudaStream_t s, bool all_aligned16 = false);
+
+// Split-K for short-and-wide outputs (M*N small, K large): `splits` partial
+// products go to `ws` (>= splits*M*N doubles), then a fixed-order reduction
+// applies alpha/beta (deterministic).  Masks on A/B are honoured; the output
+// mask must be inactive.
+cudaError_t gemm_splitk(bool transA, bool transB, const GemmProblem& p, int splits, double* ws,
+                        GemmProblem* probs_dev_scratch, cudaStream_t s);
 
 // Convenience wrappers ------------------------------------------------------
 inline GemmProblem make_gemm(int M, int N, int K, double alpha, const double* A, long long lda,

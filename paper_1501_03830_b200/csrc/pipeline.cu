@@ -1,0 +1,254 @@
+// Pipelines: the two-stage symmetric eigensolver and the BSE product-form
+// solve (north-star path: K = L L^T, W = L^T M L = Z Lam^2 Z^T, recover X, Y).
+//
+// Step order follows the reference's solvers (solvers.py:46-77 / :97-104):
+// Cholesky -> congruence -> eigendecomposition -> back-transform -> scale.
+#include <algorithm>
+#include "eig.cuh"
+#include "solver.cuh"
+
+namespace bse {
+
+int device_sm_count() {
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  return sms;
+}
+
+namespace {
+
+constexpr int kBand = 64;
+constexpr int kQ2Group = 32;
+
+struct SyevdWork {
+  double* Vall; long long ldv;
+  double* Tall;
+  Sy2sbScratch sc;
+  double* AB; int ldab;
+  double* d; double* e;
+  double* V2; double* tau2; int* progress;
+  double* Vblk; double* VTblk;
+  double* ybuf; double* y2buf;
+  StedcWork dc;
+};
+
+SyevdWork carve_syevd(Arena& a, int n) {
+  SyevdWork w{};
+  const int b = kBand;
+  const long long ld = pad_ld(n);
+  const int np = std::max(1, n / b + 1);
+  w.ldv = ld;
+  w.Vall = a.take<double>((size_t)ld * n);
+  w.Tall = a.take<double>((size_t)np * b * b);
+  w.sc.ldvwv = ld;
+  w.sc.vwv = a.take<double>((size_t)ld * 3 * b);
+  w.sc.ldy = ld;
+  w.sc.y = a.take<double>((size_t)ld * b);
+  w.sc.z = a.take<double>((size_t)b * b);
+  w.sc.z2 = a.take<double>((size_t)b * b);
+  w.sc.red = a.take<double>(2 * 192 * (2 + 2 * (size_t)b));
+  w.sc.bar = a.take<unsigned>(4);
+  w.sc.splitk_ws = a.take<double>(64 * (size_t)b * b);
+  w.sc.probs = a.take<GemmProblem>(64);
+  w.ldab = 2 * b;
+  w.AB = a.take<double>((size_t)w.ldab * n);
+  w.d = a.take<double>(n);
+  w.e = a.take<double>(n);
+  const int maxsteps = sb2st_maxsteps(n, b);
+  w.V2 = a.take<double>((size_t)n * maxsteps * b);
+  w.tau2 = a.take<double>((size_t)n * maxsteps);
+  w.progress = a.take<int>(n);
+  const size_t qb = q2_block_doubles(n, b, kQ2Group);
+  w.Vblk = a.take<double>(qb);
+  w.VTblk = a.take<double>(qb);
+  w.ybuf = a.take<double>((size_t)b * n);
+  w.y2buf = a.take<double>((size_t)b * n);
+  w.dc = stedc_carve(a, n);
+  return w;
+}
+
+}  // namespace
+
+size_t syevd_bytes(int n, int flags) {
+  (void)flags;
+  Arena a;
+  a.dry = true;
+  carve_syevd(a, n);
+  return a.used + 4096;
+}
+
+cudaError_t syevd(int n, double* A, long long lda, double* w, double* Z, long long ldz,
+                  void* work, size_t work_bytes, int flags, cudaStream_t s) {
+  (void)flags;
+  if (n <= 0) return cudaSuccess;
+  Arena a{static_cast<char*>(work), work_bytes, 0, false};
+  SyevdWork ws = carve_syevd(a, n);
+  if (!ws.dc.scal) return cudaErrorMemoryAllocation;
+  const int b = kBand;
+  const int sms = device_sm_count();
+  cudaError_t e;
+  if ((e = sy2sb(A, lda, n, b, ws.Vall, ws.ldv, ws.Tall, ws.sc, sms, s)) != cudaSuccess) return e;
+  if ((e = extract_band(A, lda, n, b, ws.AB, ws.ldab, s)) != cudaSuccess) return e;
+  if ((e = sb2st(ws.AB, ws.ldab, n, b, ws.d, ws.e, ws.V2, ws.tau2, ws.progress, sms, s)) != cudaSuccess)
+    return e;
+  if ((e = stedc(n, ws.d, ws.e, w, Z, ldz, ws.dc, s)) != cudaSuccess) return e;
+  if ((e = q2_build(n, b, kQ2Group, ws.V2, ws.tau2, ws.Vblk, ws.VTblk, s)) != cudaSuccess) return e;
+  if ((e = q2_apply(n, b, kQ2Group, ws.Vblk, ws.VTblk, Z, ldz, n, s)) != cudaSuccess) return e;
+  return q1_apply(n, b, ws.Vall, ws.ldv, ws.Tall, Z, ldz, n, ws.ybuf, ws.y2buf, s);
+}
+
+// ---------------------------------------------------------------------------
+// BSE product-form solve
+
+namespace {
+
+struct SolveWork {
+  double* L; double* T1; double* W; double* Zr; long long ld;
+  double* lam2;
+  DevStatus* st;
+  void* eig; size_t eig_bytes;
+};
+
+SolveWork carve_solve(Arena& a, int n, int flags) {
+  SolveWork w{};
+  w.ld = pad_ld(n);
+  w.L = a.take<double>((size_t)w.ld * n);
+  w.T1 = a.take<double>((size_t)w.ld * n);
+  w.W = a.take<double>((size_t)w.ld * n);
+  w.Zr = a.take<double>((size_t)w.ld * n);
+  w.lam2 = a.take<double>(n);
+  w.st = a.take<DevStatus>(2);
+  w.eig_bytes = syevd_bytes(n, flags);
+  w.eig = a.take<char>(w.eig_bytes);
+  return w;
+}
+
+__global__ void copy_lower_kernel(int n, const double* src, long long lds, double* dst, long long ldd) {
+  const long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (idx >= (long long)n * n) return;
+  const int r = (int)(idx % n), c = (int)(idx / n);
+  dst[r + (long long)c * ldd] = (r >= c) ? src[r + (long long)c * lds] : 0.0;
+}
+
+// v <- Z(:, col) * lam_j, with the column order reversed (descending lam).
+__global__ void scale_reverse_kernel(int n, const double* Z, long long ldz, const double* lam2,
+                                     double* Zr, double* V, long long ld, double* lam_out,
+                                     int* bad) {
+  const long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (idx >= (long long)n * n) return;
+  const int r = (int)(idx % n), c = (int)(idx / n);
+  const int src = n - 1 - c;
+  const double l2 = lam2[src];
+  const double lam = l2 > 0.0 ? sqrt(l2) : 0.0;
+  const double z = Z[r + (long long)src * ldz];
+  Zr[r + (long long)c * ld] = z;
+  V[r + (long long)c * ld] = z * lam;
+  if (r == 0) {
+    lam_out[c] = lam;
+    if (!(l2 > 0.0)) atomicExch(bad, 1);
+  }
+}
+
+// X1 = (u + v) / (2 sqrt(lam)), X2 = (u - v) / (2 sqrt(lam))
+__global__ void recover_kernel(int n, const double* U, const double* V, long long ld,
+                               const double* lam, double* X1, long long ldx1, double* X2,
+                               long long ldx2) {
+  const long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (idx >= (long long)n * n) return;
+  const int r = (int)(idx % n), c = (int)(idx / n);
+  const double sc = 0.5 / sqrt(lam[c]);
+  const double u = U[r + (long long)c * ld], v = V[r + (long long)c * ld];
+  X1[r + (long long)c * ldx1] = (u + v) * sc;
+  X2[r + (long long)c * ldx2] = (u - v) * sc;
+}
+
+}  // namespace
+
+size_t solve_bytes(int n, int flags) {
+  Arena a;
+  a.dry = true;
+  carve_solve(a, n, flags);
+  return a.used + 4096;
+}
+
+// Returns cudaSuccess and fills *status_host with {info, value, failed_factor}.
+cudaError_t solve_spd_pair(int n, const double* M, long long ldm, const double* K, long long ldk,
+                           double* lam, double* X1, long long ldx1, double* X2, long long ldx2,
+                           void* work, size_t work_bytes, int flags, cudaStream_t s,
+                           SolveStatus* out) {
+  out->code = 0;
+  out->pivot_index = -1;
+  out->pivot_value = 0.0;
+  out->failed_factor = -1;
+  if (n <= 0) return cudaSuccess;
+  Arena a{static_cast<char*>(work), work_bytes, 0, false};
+  SolveWork w = carve_solve(a, n, flags);
+  if (!w.eig) return cudaErrorMemoryAllocation;
+  const long long ld = w.ld;
+  const long long tot = (long long)n * n;
+  const unsigned nb = (unsigned)ceil_div(tot, 256);
+  cudaError_t e;
+  DevStatus h0[2] = {{-1, 0, 0.0, 0.0}, {-1, 0, 0.0, 0.0}};
+  if ((e = cudaMemcpyAsync(w.st, h0, sizeof(h0), cudaMemcpyHostToDevice, s)) != cudaSuccess) return e;
+  // 1. K = L L^T
+  copy_lower_kernel<<<nb, 256, 0, s>>>(n, K, ldk, w.L, ld);
+  if ((e = potrf_lower(w.L, ld, n, &w.st[0], s)) != cudaSuccess) return e;
+  // 2. W = L^T M L  (T1 = M L from the lower triangle of M, then W = L^T T1, lower)
+  GemmProblem g1 = make_gemm(n, n, n, 1.0, M, ldm, w.L, ld, 0.0, w.T1, ld);
+  g1.ma = Mask::lower();
+  g1.mb = Mask::lower();
+  if ((e = gemm(false, false, g1, s)) != cudaSuccess) return e;
+  GemmProblem g2 = make_gemm(n, n, n, 1.0, M, ldm, w.L, ld, 1.0, w.T1, ld);
+  g2.ma = Mask::strict_lower();
+  g2.mb = Mask::lower();
+  if ((e = gemm(true, false, g2, s)) != cudaSuccess) return e;
+  GemmProblem g3 = make_gemm(n, n, n, 1.0, w.L, ld, w.T1, ld, 0.0, w.W, ld);
+  g3.ma = Mask::lower();
+  g3.mc = Mask::lower();
+  if ((e = gemm(true, false, g3, s)) != cudaSuccess) return e;
+  // 3. W = Z diag(lam^2) Z^T (ascending lam^2); Z into T1
+  if ((e = syevd(n, w.W, ld, w.lam2, w.T1, ld, w.eig, w.eig_bytes, flags, s)) != cudaSuccess) return e;
+  // 4. descending order; v = Z Lam into W, Z reversed into Zr
+  int* bad = reinterpret_cast<int*>(&w.st[1].conv_fail);
+  scale_reverse_kernel<<<nb, 256, 0, s>>>(n, w.T1, ld, w.lam2, w.Zr, w.W, ld, lam, bad);
+  // u = L Zr (into T1), v = L^{-T} (Zr Lam) (in W)
+  GemmProblem g4 = make_gemm(n, n, n, 1.0, w.L, ld, w.Zr, ld, 0.0, w.T1, ld);
+  g4.ma = Mask::lower();
+  if ((e = gemm(false, false, g4, s)) != cudaSuccess) return e;
+  if ((e = trsm_llt(w.L, ld, n, w.W, ld, n, s)) != cudaSuccess) return e;
+  recover_kernel<<<nb, 256, 0, s>>>(n, w.T1, w.W, ld, lam, X1, ldx1, X2, ldx2);
+  if ((e = cudaGetLastError()) != cudaSuccess) return e;
+  // status
+  DevStatus hs[2];
+  if ((e = cudaMemcpyAsync(hs, w.st, sizeof(hs), cudaMemcpyDeviceToHost, s)) != cudaSuccess) return e;
+  if ((e = cudaStreamSynchronize(s)) != cudaSuccess) return e;
+  if (hs[0].info >= 0 || hs[1].conv_fail) {
+    // Definiteness failure: the reference factors A+B first (solvers.py:97-98),
+    // so probe M before reporting K.
+    copy_lower_kernel<<<nb, 256, 0, s>>>(n, M, ldm, w.W, ld);
+    DevStatus* stm = &w.st[1];
+    if ((e = cudaMemcpyAsync(stm, h0, sizeof(DevStatus), cudaMemcpyHostToDevice, s)) != cudaSuccess) return e;
+    if ((e = potrf_lower(w.W, ld, n, stm, s)) != cudaSuccess) return e;
+    DevStatus hm;
+    if ((e = cudaMemcpyAsync(&hm, stm, sizeof(hm), cudaMemcpyDeviceToHost, s)) != cudaSuccess) return e;
+    if ((e = cudaStreamSynchronize(s)) != cudaSuccess) return e;
+    out->code = 1;
+    if (hm.info >= 0) {
+      out->failed_factor = 1;
+      out->pivot_index = hm.info;
+      out->pivot_value = hm.value;
+    } else if (hs[0].info >= 0) {
+      out->failed_factor = 0;
+      out->pivot_index = hs[0].info;
+      out->pivot_value = hs[0].value;
+    } else {
+      out->failed_factor = 1;  // M numerically PD but W lost definiteness
+      out->pivot_index = -1;
+      out->pivot_value = 0.0;
+    }
+  }
+  return cudaSuccess;
+}
+
+}  // namespace bse

@@ -1,10 +1,28 @@
 // Pipeline-level declarations shared by the C ABI.
 #pragma once
 #include <cuda_runtime.h>
-#include "dense.cuh"
+#include "eig.cuh"
 
 namespace bse {
 
 double launch_peak(int which, int blocks, int iters, double* sink, cudaStream_t s);
+
+struct SolveStatus {
+  int code;            // 0 ok, 1 not positive definite
+  long long pivot_index;
+  double pivot_value;
+  int failed_factor;   // 0: K (A-B), 1: M (A+B)
+};
+
+size_t solve_bytes(int n, int flags);
+cudaError_t solve_spd_pair(int n, const double* M, long long ldm, const double* K, long long ldk,
+                           double* lam, double* X1, long long ldx1, double* X2, long long ldx2,
+                           void* work, size_t work_bytes, int flags, cudaStream_t s,
+                           SolveStatus* out);
+
+cudaError_t absorption(int n, const double* lam, const double* X1c, long long ldx1,
+                       const double* X2c, long long ldx2, const double* dr, const double* dl,
+                       int ngrid, const double* grid, double sigma, double* weights,
+                       double* values, double* defect, double* minpair, cudaStream_t s);
 
 }  // namespace bse

@@ -1,0 +1,423 @@
+// Symmetric tridiagonal divide and conquer (Cuppen splitting, LAPACK
+// dlaed2-style deflation, Gu-Eisenstat Loewner z-hat for orthogonal
+// vectors), level-synchronous on the GPU.  Replaces the reference's
+// bisection + inverse iteration + Gram-Schmidt (kernels.py:262-535), whose
+// two CGS passes against all previous vectors are O(m k^2) BLAS-2.
+//
+// Tree: leaves are 1x1; level l merges nodes [i*2^l, min((i+1)*2^l, n)) from
+// children of size 2^(l-1).  Every node's eigenvectors live in the diagonal
+// block Q[lo:hi, lo:hi] of a ping-pong pair of n x n buffers; per level:
+//   prepare (z, merge-sort, deflation scan) -> secular roots (one thread per
+//   root) -> z-hat -> output ordering -> eigenvector columns -> deflation
+//   rotations -> grouped DMMA GEMM Q_out = diag(Q1, Q2) * U.
+#include "eig.cuh"
+
+namespace bse {
+namespace {
+
+constexpr int kDcThreads = 256;
+
+struct Level {
+  int size;  // 2^l
+  int half;  // 2^(l-1)
+  int nnodes;
+};
+
+BSE_DEV void node_range(const Level& L, int n, int i, int& lo, int& mid, int& hi) {
+  lo = i * L.size;
+  hi = min(lo + L.size, n);
+  mid = min(lo + L.half, hi);
+}
+
+__global__ void dc_init_kernel(int n, const double* d, const double* e, double* D, double* Q,
+                               long long ld, const double* scal) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const double inv = scal[0] > 0.0 ? 1.0 / scal[0] : 1.0;
+  double v = d[i] * inv;
+  // Cuppen splitting at every boundary: T = diag(T^1, T^2) + |b| w w^T
+  if (i > 0) v -= fabs(e[i - 1] * inv);
+  if (i < n - 1) v -= fabs(e[i] * inv);
+  D[i] = v;
+  Q[i + (long long)i * ld] = 1.0;
+}
+
+__global__ void absmax_kernel(int n, const double* d, const double* e, double* out) {
+  __shared__ double red[32];
+  double m = 0.0;
+  for (int i = threadIdx.x; i < n; i += blockDim.x) {
+    m = fmax(m, fabs(d[i]));
+    if (i < n - 1) m = fmax(m, fabs(e[i]));
+  }
+  m = warp_max(m);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = m;
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    double t = threadIdx.x < (blockDim.x >> 5) ? red[threadIdx.x] : 0.0;
+    t = warp_max(t);
+    if (threadIdx.x == 0) out[0] = t;
+  }
+}
+
+// ---- 1. z vector, merge-sort of the children's eigenvalues, deflation ----
+__global__ void __launch_bounds__(kDcThreads) dc_prepare_kernel(
+    Level L, int n, const double* __restrict__ e, const double* __restrict__ scal,
+    const double* __restrict__ Din, double* __restrict__ Dout, const double* __restrict__ Qin,
+    double* __restrict__ Qout, long long ld, StedcWork w) {
+  __shared__ double red[32];
+  int lo, mid, hi;
+  node_range(L, n, blockIdx.x, lo, mid, hi);
+  const int m = hi - lo, n1 = mid - lo;
+  const int tid = threadIdx.x;
+  int* cnt = w.counts + 3 * blockIdx.x;
+  if (mid >= hi) {  // pass-through node: copy the block
+    for (long long idx = tid; idx < (long long)m * m; idx += blockDim.x) {
+      const int r = (int)(idx % m), c = (int)(idx / m);
+      Qout[(lo + r) + (long long)(lo + c) * ld] = Qin[(lo + r) + (long long)(lo + c) * ld];
+    }
+    for (int t = tid; t < m; t += blockDim.x) Dout[lo + t] = Din[lo + t];
+    if (tid == 0) { cnt[0] = -1; cnt[1] = 0; cnt[2] = 0; }
+    return;
+  }
+  const double inv = scal[0] > 0.0 ? 1.0 / scal[0] : 1.0;
+  const double beta = e[mid - 1] * inv;
+  const double rho = 2.0 * fabs(beta);
+  const double sgn = beta >= 0.0 ? 1.0 : -1.0;
+  const double rs2 = 0.70710678118654752440;
+  const double* D1 = Din + lo;
+  const double* D2 = Din + mid;
+  const int n2 = hi - mid;
+  double amax = 0.0;
+  for (int t = tid; t < m; t += blockDim.x) {
+    double val, zval;
+    int r;
+    if (t < n1) {
+      val = D1[t];
+      zval = Qin[(mid - 1) + (long long)(lo + t) * ld] * rs2;
+      int a = 0, b = n2;  // count of D2 < val
+      while (a < b) { const int c = (a + b) >> 1; if (D2[c] < val) a = c + 1; else b = c; }
+      r = t + a;
+    } else {
+      const int u = t - n1;
+      val = D2[u];
+      zval = sgn * Qin[mid + (long long)(mid + u) * ld] * rs2;
+      int a = 0, b = n1;  // count of D1 <= val
+      while (a < b) { const int c = (a + b) >> 1; if (D1[c] <= val) a = c + 1; else b = c; }
+      r = u + a;
+    }
+    w.ds[lo + r] = val;
+    w.zs[lo + r] = zval;
+    w.perm[lo + r] = t;
+    amax = fmax(amax, fmax(fabs(val), fabs(zval)));
+  }
+  amax = warp_max(amax);
+  if ((tid & 31) == 0) red[tid >> 5] = amax;
+  __syncthreads();
+  if (tid != 0) return;
+  double tol = 0.0;
+  for (int i = 0; i < (int)(blockDim.x >> 5); ++i) tol = fmax(tol, red[i]);
+  tol *= 8.0 * kEps;
+  // sequential deflation scan (dlaed2 logic) in sorted order
+  double* ds = w.ds + lo;
+  double* zs = w.zs + lo;
+  int K = 0, nd = 0, nr = 0, pj = -1;
+  for (int j = 0; j < m; ++j) {
+    const double zj = zs[j];
+    if (rho * fabs(zj) <= tol) {
+      w.defl[lo + nd] = j;
+      w.val[lo + (m - 1 - nd)] = ds[j];  // deflated values fill from the back
+      ++nd;
+      continue;
+    }
+    if (pj < 0) { pj = j; continue; }
+    double s = zs[pj], c = zj;
+    const double tau = hypot(c, s);
+    const double t = ds[j] - ds[pj];
+    c /= tau;
+    s = -s / tau;
+    if (fabs(t * c * s) <= tol) {
+      zs[j] = tau;
+      zs[pj] = 0.0;
+      w.rotp[lo + nr] = pj; w.rotq[lo + nr] = j; w.rotc[lo + nr] = c; w.rots[lo + nr] = s;
+      ++nr;
+      const double tt = ds[pj] * c * c + ds[j] * s * s;
+      ds[j] = ds[pj] * s * s + ds[j] * c * c;
+      ds[pj] = tt;
+      w.defl[lo + nd] = pj;
+      w.val[lo + (m - 1 - nd)] = tt;
+      ++nd;
+      pj = j;
+    } else {
+      w.keep[lo + K] = pj; w.dk[lo + K] = ds[pj]; w.zk[lo + K] = zs[pj];
+      ++K;
+      pj = j;
+    }
+  }
+  if (pj >= 0) { w.keep[lo + K] = pj; w.dk[lo + K] = ds[pj]; w.zk[lo + K] = zs[pj]; ++K; }
+  cnt[0] = K; cnt[1] = nd; cnt[2] = nr;
+  w.zh[lo] = rho;  // stash rho for the secular / z-hat kernels
+}
+
+// ---- 2. secular equation: one thread per root (bisection in shifted coords) ----
+__global__ void dc_secular_kernel(Level L, int n, StedcWork w) {
+  int lo, mid, hi;
+  node_range(L, n, blockIdx.y, lo, mid, hi);
+  const int* cnt = w.counts + 3 * blockIdx.y;
+  const int K = cnt[0];
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (K <= 0 || i >= K) return;
+  const double rho = w.zh[lo];
+  const double* dk = w.dk + lo;
+  const double* zk = w.zk + lo;
+  int org;
+  double a, b;
+  if (i < K - 1) {
+    const double half = 0.5 * (dk[i + 1] - dk[i]);
+    double f = 0.0;
+    for (int j = 0; j < K; ++j) f += zk[j] * zk[j] / ((dk[j] - dk[i]) - half);
+    f = 1.0 + rho * f;
+    if (f >= 0.0) { org = i; a = 0.0; b = half; }
+    else { org = i + 1; a = -half; b = 0.0; }
+  } else {
+    double s = 0.0;
+    for (int j = 0; j < K; ++j) s += zk[j] * zk[j];
+    org = K - 1; a = 0.0; b = rho * s;
+  }
+  const double d0 = dk[org];
+  for (int it = 0; it < 200; ++it) {
+    const double x = 0.5 * (a + b);
+    if (x == a || x == b) break;
+    double f = 0.0;
+    for (int j = 0; j < K; ++j) f += zk[j] * zk[j] / ((dk[j] - d0) - x);
+    f = 1.0 + rho * f;
+    if (f > 0.0) b = x; else a = x;
+    if (b - a <= 2.0 * kEps * fmax(fabs(a), fabs(b))) break;
+  }
+  const double t = 0.5 * (a + b);
+  w.org[lo + i] = org;
+  w.tau[lo + i] = t;
+  w.val[lo + i] = d0 + t;
+}
+
+// ---- 3. Loewner z-hat ----
+__global__ void dc_zhat_kernel(Level L, int n, StedcWork w, const double* rho_src) {
+  int lo, mid, hi;
+  node_range(L, n, blockIdx.y, lo, mid, hi);
+  const int K = w.counts[3 * blockIdx.y];
+  const int j = blockIdx.x * blockDim.x + threadIdx.x;
+  if (K <= 0 || j >= K) return;
+  const double rho = rho_src[lo];
+  const double* dk = w.dk + lo;
+  const int* org = w.org + lo;
+  const double* tau = w.tau + lo;
+  const double dj = dk[j];
+  double p = 1.0;
+  for (int i = 0; i < K; ++i) {
+    const double li = (dk[org[i]] - dj) + tau[i];
+    if (i < K - 1) p *= li / (i < j ? (dk[i] - dj) : (dk[i + 1] - dj));
+    else p *= li;
+  }
+  w.zh2[lo + j] = copysign(sqrt(fmax(p, 0.0) / rho), w.zk[lo + j]);
+}
+
+// ---- 4. output ordering (roots ascending merged with deflated values) ----
+__global__ void dc_order_kernel(Level L, int n, StedcWork w, double* Dout) {
+  int lo, mid, hi;
+  node_range(L, n, blockIdx.y, lo, mid, hi);
+  const int K = w.counts[3 * blockIdx.y];
+  if (K < 0) return;
+  const int m = hi - lo, nd = m - K;
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= m) return;
+  const double* val = w.val + lo;  // roots at [0,K), deflated at [m-1-c] for c < nd
+  int pos;
+  double v;
+  if (t < K) {
+    v = val[t];
+    int c = 0;
+    for (int q = 0; q < nd; ++q) c += val[m - 1 - q] < v;
+    pos = t + c;
+  } else {
+    const int cidx = t - K;  // deflated #cidx
+    v = val[m - 1 - cidx];
+    int a = 0, b = K;  // roots <= v
+    while (a < b) { const int c = (a + b) >> 1; if (val[c] <= v) a = c + 1; else b = c; }
+    int c = 0;
+    for (int q = 0; q < nd; ++q) {
+      const double u = val[m - 1 - q];
+      c += (u < v) || (u == v && q < cidx);
+    }
+    pos = a + c;
+  }
+  w.pos[lo + t] = pos;
+  Dout[lo + pos] = v;
+}
+
+// ---- 5. eigenvector matrix U (rows in the node's original order) ----
+__global__ void __launch_bounds__(kDcThreads) dc_vectors_kernel(Level L, int n, StedcWork w,
+                                                                long long ld) {
+  int lo, mid, hi;
+  node_range(L, n, blockIdx.y, lo, mid, hi);
+  const int K = w.counts[3 * blockIdx.y];
+  if (K < 0) return;
+  const int m = hi - lo;
+  const int lane = threadIdx.x & 31;
+  const int t = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);  // column source index
+  if (t >= m) return;
+  const int col = w.pos[lo + t];
+  double* U = w.U + lo + (long long)(lo + col) * ld;
+  for (int r = lane; r < m; r += 32) U[r] = 0.0;
+  __syncwarp();
+  const int* perm = w.perm + lo;
+  if (t < K) {
+    const double* dk = w.dk + lo;
+    const double* zh = w.zh2 + lo;
+    const int* keep = w.keep + lo;
+    const double d0 = dk[w.org[lo + t]], tt = w.tau[lo + t];
+    double s = 0.0;
+    for (int j = lane; j < K; j += 32) {
+      const double x = zh[j] / ((dk[j] - d0) - tt);
+      s += x * x;
+    }
+    s = warp_sum(s);
+    const double inv = 1.0 / sqrt(s);
+    for (int j = lane; j < K; j += 32) U[perm[keep[j]]] = zh[j] / ((dk[j] - d0) - tt) * inv;
+  } else if (lane == 0) {
+    U[perm[w.defl[lo + (t - K)]]] = 1.0;
+  }
+}
+
+// ---- 6. deflation rotations on the rows of U (reverse order) ----
+__global__ void dc_rotate_kernel(Level L, int n, StedcWork w, long long ld) {
+  int lo, mid, hi;
+  node_range(L, n, blockIdx.y, lo, mid, hi);
+  const int K = w.counts[3 * blockIdx.y];
+  const int nr = w.counts[3 * blockIdx.y + 2];
+  if (K < 0 || nr == 0) return;
+  const int m = hi - lo;
+  const int col = blockIdx.x * blockDim.x + threadIdx.x;
+  if (col >= m) return;
+  double* U = w.U + lo + (long long)(lo + col) * ld;
+  const int* perm = w.perm + lo;
+  for (int r = nr - 1; r >= 0; --r) {
+    const int p = perm[w.rotp[lo + r]], q = perm[w.rotq[lo + r]];
+    const double c = w.rotc[lo + r], s = w.rots[lo + r];
+    const double up = U[p], uq = U[q];
+    U[p] = c * up - s * uq;
+    U[q] = s * up + c * uq;
+  }
+}
+
+// ---- 7. GEMM descriptors: Q_out = diag(Q1, Q2) * U per node ----
+__global__ void dc_probs_kernel(Level L, int n, StedcWork w, const double* Qin, double* Qout,
+                                long long ld) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= L.nnodes) return;
+  int lo, mid, hi;
+  node_range(L, n, i, lo, mid, hi);
+  GemmProblem top, bot;
+  if (mid < hi) {
+    const int n1 = mid - lo, n2 = hi - mid, m = hi - lo;
+    top.M = n1; top.N = m; top.K = n1;
+    top.A = Qin + lo + (long long)lo * ld; top.lda = ld;
+    top.B = w.U + lo + (long long)lo * ld; top.ldb = ld;
+    top.C = Qout + lo + (long long)lo * ld; top.ldc = ld;
+    bot.M = n2; bot.N = m; bot.K = n2;
+    bot.A = Qin + mid + (long long)mid * ld; bot.lda = ld;
+    bot.B = w.U + mid + (long long)lo * ld; bot.ldb = ld;
+    bot.C = Qout + mid + (long long)lo * ld; bot.ldc = ld;
+  }
+  w.probs[2 * i] = top;
+  w.probs[2 * i + 1] = bot;
+}
+
+__global__ void dc_finish_kernel(int n, const double* D, double* wout, const double* scal) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) wout[i] = D[i] * (scal[0] > 0.0 ? scal[0] : 1.0);
+}
+
+__global__ void copy_matrix_kernel(int rows, int cols, const double* src, long long lds, double* dst,
+                                   long long ldd) {
+  const long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (idx >= (long long)rows * cols) return;
+  const int r = (int)(idx % rows), c = (int)(idx / rows);
+  dst[r + (long long)c * ldd] = src[r + (long long)c * lds];
+}
+
+}  // namespace
+
+StedcWork stedc_carve(Arena& a, int n) {
+  StedcWork w;
+  const long long ld = pad_ld(n);
+  w.ld = ld;
+  w.Qa = a.take<double>((size_t)ld * n);
+  w.Qb = a.take<double>((size_t)ld * n);
+  w.U = a.take<double>((size_t)ld * n);
+  w.Da = a.take<double>(n);
+  w.Db = a.take<double>(n);
+  w.ds = a.take<double>(n);
+  w.zs = a.take<double>(n);
+  w.dk = a.take<double>(n);
+  w.zk = a.take<double>(n);
+  w.zh = a.take<double>(n);
+  w.zh2 = a.take<double>(n);
+  w.tau = a.take<double>(n);
+  w.val = a.take<double>(n);
+  w.org = a.take<int>(n);
+  w.perm = a.take<int>(n);
+  w.keep = a.take<int>(n);
+  w.defl = a.take<int>(n);
+  w.pos = a.take<int>(n);
+  w.rotp = a.take<int>(n);
+  w.rotq = a.take<int>(n);
+  w.rotc = a.take<double>(n);
+  w.rots = a.take<double>(n);
+  w.counts = a.take<int>(3 * (size_t)n + 3);
+  w.probs = a.take<GemmProblem>(2 * (size_t)n + 2);
+  w.scal = a.take<double>(4);
+  return w;
+}
+
+size_t stedc_bytes(int n) {
+  Arena a;
+  a.dry = true;
+  stedc_carve(a, n);
+  return a.used;
+}
+
+cudaError_t stedc(int n, double* d, double* e, double* wout, double* Q, long long ldq,
+                  const StedcWork& ws, cudaStream_t s) {
+  if (n <= 0) return cudaSuccess;
+  cudaError_t err;
+  const long long ld = ws.ld;
+  absmax_kernel<<<1, 1024, 0, s>>>(n, d, e, ws.scal);
+  dc_init_kernel<<<(unsigned)ceil_div(n, 256), 256, 0, s>>>(n, d, e, ws.Da, ws.Qa, ld, ws.scal);
+  double* Din = ws.Da;
+  double* Dout = ws.Db;
+  double* Qin = ws.Qa;
+  double* Qout = ws.Qb;
+  for (int size = 2; size / 2 < n; size *= 2) {
+    Level L{size, size / 2, (int)ceil_div(n, size)};
+    const int maxm = std::min(size, n);
+    dc_prepare_kernel<<<L.nnodes, kDcThreads, 0, s>>>(L, n, e, ws.scal, Din, Dout, Qin, Qout, ld, ws);
+    const dim3 g1((unsigned)ceil_div(maxm, 128), (unsigned)L.nnodes);
+    dc_secular_kernel<<<g1, 128, 0, s>>>(L, n, ws);
+    dc_zhat_kernel<<<g1, 128, 0, s>>>(L, n, ws, ws.zh);
+    dc_order_kernel<<<g1, 128, 0, s>>>(L, n, ws, Dout);
+    const dim3 g2((unsigned)ceil_div(maxm, kDcThreads / 32), (unsigned)L.nnodes);
+    dc_vectors_kernel<<<g2, kDcThreads, 0, s>>>(L, n, ws, ld);
+    dc_rotate_kernel<<<g1, 128, 0, s>>>(L, n, ws, ld);
+    dc_probs_kernel<<<(unsigned)ceil_div(L.nnodes, 128), 128, 0, s>>>(L, n, ws, Qin, Qout, ld);
+    if ((err = cudaGetLastError()) != cudaSuccess) return err;
+    err = gemm_grouped(false, false, ws.probs, 2 * L.nnodes, L.half, maxm, s, L.half >= 2);
+    if (err != cudaSuccess) return err;
+    std::swap(Din, Dout);
+    std::swap(Qin, Qout);
+  }
+  dc_finish_kernel<<<(unsigned)ceil_div(n, 256), 256, 0, s>>>(n, Din, wout, ws.scal);
+  const long long tot = (long long)n * n;
+  copy_matrix_kernel<<<(unsigned)ceil_div(tot, 256), 256, 0, s>>>(n, n, Qin, ld, Q, ldq);
+  return cudaGetLastError();
+}
+
+}  // namespace bse
