@@ -115,6 +115,13 @@ int bse_gemm_dev(int transA, int transB, int64_t M, int64_t N, int64_t K, double
 int bse_trsm_dev(int kind, int64_t n, const double* dL, int64_t ldl, double* dB, int64_t ldb,
                  int64_t m, void* stream);
 
+/* Instrumentation (bench/profiling): stage timing with CUDA events recorded
+ * on the solve stream, and the number of kernels this library has launched. */
+int bse_profile_enable(int on);
+/* Fills up to max_stages durations (ms) and 32-byte names; returns the count. */
+int bse_profile_read(int max_stages, double* ms, char* names);
+long long bse_launch_count(void);
+
 /* FP64 peak probe: which 0 = DMMA, 1 = DFMA.  Returns flops of one launch in
  * *flops and the mean device time over `reps` launches in *ms. */
 int bse_peak_fp64(int which, int blocks, int iters, int reps, double* flops, double* ms);

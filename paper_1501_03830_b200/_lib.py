@@ -52,6 +52,9 @@ SIGNATURES = {
     "bse_gemm_dev": (_INT, [_INT, _INT, _I64, _I64, _I64, _D, _P, _I64, _P, _I64, _D, _P, _I64,
                             _P, _P]),
     "bse_trsm_dev": (_INT, [_INT, _I64, _P, _I64, _P, _I64, _I64, _P]),
+    "bse_profile_enable": (_INT, [_INT]),
+    "bse_profile_read": (_INT, [_INT, C.POINTER(_D), C.c_char_p]),
+    "bse_launch_count": (C.c_longlong, []),
     "bse_peak_fp64": (_INT, [_INT, _INT, _INT, _INT, C.POINTER(_D), C.POINTER(_D)]),
 }
 

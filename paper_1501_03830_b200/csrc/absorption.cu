@@ -105,10 +105,13 @@ cudaError_t absorption(int n, const double* lam, const double* X1c, long long ld
     absorption_weights_kernel<<<(unsigned)ceil_div(n, 8), 256, 0, s>>>(
         n, reinterpret_cast<const cplx*>(X1c), ldx1, reinterpret_cast<const cplx*>(X2c), ldx2,
         reinterpret_cast<const cplx*>(dr), reinterpret_cast<const cplx*>(dl), weights, tmp, tmp + n);
+    count_launch();
   reduce_minmax_kernel<<<1, 1024, 0, s>>>(n, tmp, tmp + n, minpair, defect);
+  count_launch();
   if (ngrid > 0)
     gaussian_mix_kernel<<<(unsigned)ceil_div(ngrid, 128), 128, 0, s>>>(n, lam, weights, ngrid, grid,
                                                                        sigma, values);
+    count_launch();
   e = cudaGetLastError();
   cudaFreeAsync(tmp, s);
   return e;

@@ -213,6 +213,7 @@ cudaError_t q2_build(int n, int b, int g, const double* V2, const double* tau2, 
     attr = true;
   }
   q2_build_kernel<<<dim3(maxsteps, ngroups), 256, smem, s>>>(n, b, g, maxsteps, V2, tau2, Vblk, VTblk);
+  count_launch();
   return cudaGetLastError();
 }
 
@@ -231,6 +232,7 @@ cudaError_t q2_apply(int n, int b, int g, const double* Vblk, const double* VTbl
   }
   q2_apply_kernel<HB, G><<<(unsigned)ceil_div(ncols, kQ2W), kQ2Threads, smem, s>>>(
       n, b, maxsteps, Vblk, VTblk, Z, ldz, ncols);
+  count_launch();
   return cudaGetLastError();
 }
 

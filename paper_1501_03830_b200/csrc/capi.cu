@@ -200,6 +200,31 @@ int bse_absorption_dev(int64_t n, const double* dLam, const double* dX1c, int64_
   return BSE_OK;
 }
 
+int bse_profile_enable(int on) {
+  bse::StageLog& L = bse::stage_log();
+  L.on = on != 0;
+  L.used = 0;
+  return BSE_OK;
+}
+
+int bse_profile_read(int max_stages, double* ms, char* names) {
+  bse::StageLog& L = bse::stage_log();
+  if (L.used < 2) { L.used = 0; return 0; }
+  cudaError_t e = cudaEventSynchronize(L.ev[L.used - 1]);
+  if (e != cudaSuccess) return -cuda_fail(e, "profile");
+  int k = 0;
+  for (; k < L.used - 1 && k < max_stages; ++k) {
+    float t = 0.f;
+    cudaEventElapsedTime(&t, L.ev[k], L.ev[k + 1]);
+    ms[k] = t;
+    std::snprintf(names + 32 * k, 32, "%s", L.names[k].c_str());
+  }
+  L.used = 0;
+  return k;
+}
+
+long long bse_launch_count(void) { return bse::launch_counter().load(); }
+
 int bse_peak_fp64(int which, int blocks, int iters, int reps, double* flops, double* ms) {
   double* sink = nullptr;
   BSE_TRY_CUDA(cudaMalloc(&sink, 256 * sizeof(double)), "alloc");

@@ -4,6 +4,7 @@
 // warp-level DMMA path (mma.sync.m8n8k4.f64 -> SASS DMMA.8x8x4) fed from
 // shared memory staged with cp.async (LDGSTS).  Everything here is FP64.
 #pragma once
+#include <atomic>
 #include <cstdint>
 #include <cuda_runtime.h>
 
@@ -90,5 +91,15 @@ BSE_DEV void st_release(int* p, int v) {
 }
 
 BSE_HD long long ceil_div(long long a, long long b) { return (a + b - 1) / b; }
+
+// Host-side count of kernel launches issued by this library (bench evidence).
+inline std::atomic<long long>& launch_counter() {
+  static std::atomic<long long> c{0};
+  return c;
+}
+inline void count_launch(long long k = 1) { launch_counter().fetch_add(k, std::memory_order_relaxed); }
+
+// Stage timing with CUDA events (enabled by bse_profile_enable).
+void stage_mark(const char* name, cudaStream_t s);
 
 }  // namespace bse

@@ -168,6 +168,7 @@ cudaError_t trsm_rlt(const double* L, long long ldl, int n, double* A, long long
   if (n <= kLeaf) {
     ensure_smem<trsm_rlt_leaf>();
     trsm_rlt_leaf<<<(unsigned)ceil_div(m, kLeaf), kLeaf, kLeafSmem, s>>>(L, ldl, n, A, lda, m);
+    count_launch();
     return cudaGetLastError();
   }
   const int n1 = split_point(n), n2 = n - n1;
@@ -186,6 +187,7 @@ cudaError_t trsm_llt(const double* L, long long ldl, int n, double* B, long long
   if (n <= kLeaf) {
     ensure_smem<trsm_left_leaf<true>>();
     trsm_left_leaf<true><<<(unsigned)ceil_div(ncols, kLeaf), kLeaf, kLeafSmem, s>>>(L, ldl, n, B, ldb, ncols);
+    count_launch();
     return cudaGetLastError();
   }
   const int n1 = split_point(n), n2 = n - n1;
@@ -204,6 +206,7 @@ cudaError_t trsm_lln(const double* L, long long ldl, int n, double* B, long long
   if (n <= kLeaf) {
     ensure_smem<trsm_left_leaf<false>>();
     trsm_left_leaf<false><<<(unsigned)ceil_div(ncols, kLeaf), kLeaf, kLeafSmem, s>>>(L, ldl, n, B, ldb, ncols);
+    count_launch();
     return cudaGetLastError();
   }
   const int n1 = split_point(n), n2 = n - n1;
@@ -220,6 +223,7 @@ static cudaError_t potrf_rec(double* A, long long lda, int n, int off, DevStatus
                              cudaStream_t s) {
   if (n <= kLeaf) {
     potf2_kernel<<<1, 256, 0, s>>>(A, lda, n, off, st);
+    count_launch();
     return cudaGetLastError();
   }
   const int n1 = split_point(n), n2 = n - n1;
@@ -246,6 +250,7 @@ cudaError_t potrf_lower(double* A, long long lda, int n, DevStatus* st, cudaStre
 cudaError_t zero_strict_upper(double* A, long long lda, int n, cudaStream_t s) {
   if (n <= 0) return cudaSuccess;
   zero_upper_kernel<<<dim3((unsigned)ceil_div(n, 256), (unsigned)n), 256, 0, s>>>(A, lda, n);
+  count_launch();
   return cudaGetLastError();
 }
 
@@ -253,6 +258,7 @@ cudaError_t symmetrize_from_lower(double* A, long long lda, int n, cudaStream_t 
   if (n <= 0) return cudaSuccess;
   const unsigned t = (unsigned)ceil_div(n, 32);
   symmetrize_kernel<<<dim3(t, t), dim3(32, 8), 0, s>>>(A, lda, n);
+  count_launch();
   return cudaGetLastError();
 }
 

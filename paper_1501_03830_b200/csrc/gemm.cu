@@ -243,6 +243,7 @@ cudaError_t launch(const GemmProblem* single, const GemmProblem* grouped, int co
     gemm_single_kernel<BM, BN, BK, WM, WN, STAGES, TA, TB, VEC><<<grid, C::NT, C::SMEM, s>>>(*single);
   else
     gemm_grouped_kernel<BM, BN, BK, WM, WN, STAGES, TA, TB, VEC><<<grid, C::NT, C::SMEM, s>>>(grouped);
+  count_launch();
   return cudaGetLastError();
 }
 
@@ -322,6 +323,7 @@ cudaError_t gemm_splitk(bool transA, bool transB, const GemmProblem& p, int spli
   const long long tot = (long long)p.M * p.N;
   splitk_reduce_kernel<<<(unsigned)ceil_div(tot, 256), 256, 0, s>>>(ws, splits, p.M, p.N, p.alpha,
                                                                      p.beta, p.C, p.ldc);
+  count_launch();
   return cudaGetLastError();
 }
 

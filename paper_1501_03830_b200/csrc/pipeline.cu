@@ -4,10 +4,31 @@
 // Step order follows the reference's solvers (solvers.py:46-77 / :97-104):
 // Cholesky -> congruence -> eigendecomposition -> back-transform -> scale.
 #include <algorithm>
+#include <string>
+#include <vector>
 #include "eig.cuh"
 #include "solver.cuh"
 
 namespace bse {
+
+StageLog& stage_log() {
+  static StageLog log;
+  return log;
+}
+
+void stage_mark(const char* name, cudaStream_t s) {
+  StageLog& L = stage_log();
+  if (!L.on) return;
+  if (L.used >= (int)L.ev.size()) {
+    cudaEvent_t e;
+    cudaEventCreate(&e);
+    L.ev.push_back(e);
+    L.names.emplace_back();
+  }
+  cudaEventRecord(L.ev[L.used], s);
+  L.names[L.used] = name;
+  ++L.used;
+}
 
 int device_sm_count() {
   int dev = 0, sms = 148;
@@ -88,13 +109,19 @@ cudaError_t syevd(int n, double* A, long long lda, double* w, double* Z, long lo
   const int b = kBand;
   const int sms = device_sm_count();
   cudaError_t e;
+  stage_mark("sy2sb", s);
   if ((e = sy2sb(A, lda, n, b, ws.Vall, ws.ldv, ws.Tall, ws.sc, sms, s)) != cudaSuccess) return e;
+  stage_mark("sb2st", s);
   if ((e = extract_band(A, lda, n, b, ws.AB, ws.ldab, s)) != cudaSuccess) return e;
   if ((e = sb2st(ws.AB, ws.ldab, n, b, ws.d, ws.e, ws.V2, ws.tau2, ws.progress, sms, s)) != cudaSuccess)
     return e;
+  stage_mark("stedc", s);
   if ((e = stedc(n, ws.d, ws.e, w, Z, ldz, ws.dc, s)) != cudaSuccess) return e;
+  stage_mark("q2_build", s);
   if ((e = q2_build(n, b, kQ2Group, ws.V2, ws.tau2, ws.Vblk, ws.VTblk, s)) != cudaSuccess) return e;
+  stage_mark("q2_apply", s);
   if ((e = q2_apply(n, b, kQ2Group, ws.Vblk, ws.VTblk, Z, ldz, n, s)) != cudaSuccess) return e;
+  stage_mark("q1_apply", s);
   return q1_apply(n, b, ws.Vall, ws.ldv, ws.Tall, Z, ldz, n, ws.ybuf, ws.y2buf, s);
 }
 
@@ -192,8 +219,11 @@ cudaError_t solve_spd_pair(int n, const double* M, long long ldm, const double* 
   DevStatus h0[2] = {{-1, 0, 0.0, 0.0}, {-1, 0, 0.0, 0.0}};
   if ((e = cudaMemcpyAsync(w.st, h0, sizeof(h0), cudaMemcpyHostToDevice, s)) != cudaSuccess) return e;
   // 1. K = L L^T
+  stage_mark("potrf", s);
   copy_lower_kernel<<<nb, 256, 0, s>>>(n, K, ldk, w.L, ld);
+  count_launch();
   if ((e = potrf_lower(w.L, ld, n, &w.st[0], s)) != cudaSuccess) return e;
+  stage_mark("congruence", s);
   // 2. W = L^T M L  (T1 = M L from the lower triangle of M, then W = L^T T1, lower)
   GemmProblem g1 = make_gemm(n, n, n, 1.0, M, ldm, w.L, ld, 0.0, w.T1, ld);
   g1.ma = Mask::lower();
@@ -209,15 +239,19 @@ cudaError_t solve_spd_pair(int n, const double* M, long long ldm, const double* 
   if ((e = gemm(true, false, g3, s)) != cudaSuccess) return e;
   // 3. W = Z diag(lam^2) Z^T (ascending lam^2); Z into T1
   if ((e = syevd(n, w.W, ld, w.lam2, w.T1, ld, w.eig, w.eig_bytes, flags, s)) != cudaSuccess) return e;
+  stage_mark("recover", s);
   // 4. descending order; v = Z Lam into W, Z reversed into Zr
   int* bad = reinterpret_cast<int*>(&w.st[1].conv_fail);
   scale_reverse_kernel<<<nb, 256, 0, s>>>(n, w.T1, ld, w.lam2, w.Zr, w.W, ld, lam, bad);
+  count_launch();
   // u = L Zr (into T1), v = L^{-T} (Zr Lam) (in W)
   GemmProblem g4 = make_gemm(n, n, n, 1.0, w.L, ld, w.Zr, ld, 0.0, w.T1, ld);
   g4.ma = Mask::lower();
   if ((e = gemm(false, false, g4, s)) != cudaSuccess) return e;
   if ((e = trsm_llt(w.L, ld, n, w.W, ld, n, s)) != cudaSuccess) return e;
   recover_kernel<<<nb, 256, 0, s>>>(n, w.T1, w.W, ld, lam, X1, ldx1, X2, ldx2);
+  count_launch();
+  stage_mark("end", s);
   if ((e = cudaGetLastError()) != cudaSuccess) return e;
   // status
   DevStatus hs[2];
@@ -227,6 +261,7 @@ cudaError_t solve_spd_pair(int n, const double* M, long long ldm, const double* 
     // Definiteness failure: the reference factors A+B first (solvers.py:97-98),
     // so probe M before reporting K.
     copy_lower_kernel<<<nb, 256, 0, s>>>(n, M, ldm, w.W, ld);
+    count_launch();
     DevStatus* stm = &w.st[1];
     if ((e = cudaMemcpyAsync(stm, h0, sizeof(DevStatus), cudaMemcpyHostToDevice, s)) != cudaSuccess) return e;
     if ((e = potrf_lower(w.W, ld, n, stm, s)) != cudaSuccess) return e;

@@ -243,10 +243,12 @@ cudaError_t sb2st(double* AB, int ldab, int n, int b, double* d, double* e, doub
     int grid = std::max(1, std::min(n - 2, std::max(1, per_sm) * num_sms));
     int maxsteps = sb2st_maxsteps(n, b);
     void* args[] = {&AB, &ldab, &n, &b, &V2, &tau2, &maxsteps, &progress};
+    count_launch();
     err = cudaLaunchCooperativeKernel((void*)sb2st_kernel, dim3(grid), dim3(kSbThreads), args, smem, s);
     if (err != cudaSuccess) return err;
   }
   band_to_tridiag_kernel<<<(unsigned)ceil_div(n, 256), 256, 0, s>>>(AB, ldab, n, d, e);
+  count_launch();
   return cudaGetLastError();
 }
 

@@ -3,7 +3,18 @@
 #include <cuda_runtime.h>
 #include "eig.cuh"
 
+#include <string>
+#include <vector>
+
 namespace bse {
+
+struct StageLog {
+  bool on = false;
+  std::vector<cudaEvent_t> ev;
+  std::vector<std::string> names;
+  int used = 0;
+};
+StageLog& stage_log();
 
 double launch_peak(int which, int blocks, int iters, double* sink, cudaStream_t s);
 

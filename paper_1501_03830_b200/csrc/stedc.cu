@@ -391,7 +391,9 @@ cudaError_t stedc(int n, double* d, double* e, double* wout, double* Q, long lon
   cudaError_t err;
   const long long ld = ws.ld;
   absmax_kernel<<<1, 1024, 0, s>>>(n, d, e, ws.scal);
+  count_launch();
   dc_init_kernel<<<(unsigned)ceil_div(n, 256), 256, 0, s>>>(n, d, e, ws.Da, ws.Qa, ld, ws.scal);
+  count_launch();
   double* Din = ws.Da;
   double* Dout = ws.Db;
   double* Qin = ws.Qa;
@@ -400,14 +402,21 @@ cudaError_t stedc(int n, double* d, double* e, double* wout, double* Q, long lon
     Level L{size, size / 2, (int)ceil_div(n, size)};
     const int maxm = std::min(size, n);
     dc_prepare_kernel<<<L.nnodes, kDcThreads, 0, s>>>(L, n, e, ws.scal, Din, Dout, Qin, Qout, ld, ws);
+    count_launch();
     const dim3 g1((unsigned)ceil_div(maxm, 128), (unsigned)L.nnodes);
     dc_secular_kernel<<<g1, 128, 0, s>>>(L, n, ws);
+    count_launch();
     dc_zhat_kernel<<<g1, 128, 0, s>>>(L, n, ws, ws.zh);
+    count_launch();
     dc_order_kernel<<<g1, 128, 0, s>>>(L, n, ws, Dout);
+    count_launch();
     const dim3 g2((unsigned)ceil_div(maxm, kDcThreads / 32), (unsigned)L.nnodes);
     dc_vectors_kernel<<<g2, kDcThreads, 0, s>>>(L, n, ws, ld);
+    count_launch();
     dc_rotate_kernel<<<g1, 128, 0, s>>>(L, n, ws, ld);
+    count_launch();
     dc_probs_kernel<<<(unsigned)ceil_div(L.nnodes, 128), 128, 0, s>>>(L, n, ws, Qin, Qout, ld);
+    count_launch();
     if ((err = cudaGetLastError()) != cudaSuccess) return err;
     err = gemm_grouped(false, false, ws.probs, 2 * L.nnodes, L.half, maxm, s, L.half >= 2);
     if (err != cudaSuccess) return err;
@@ -415,8 +424,10 @@ cudaError_t stedc(int n, double* d, double* e, double* wout, double* Q, long lon
     std::swap(Qin, Qout);
   }
   dc_finish_kernel<<<(unsigned)ceil_div(n, 256), 256, 0, s>>>(n, Din, wout, ws.scal);
+  count_launch();
   const long long tot = (long long)n * n;
   copy_matrix_kernel<<<(unsigned)ceil_div(tot, 256), 256, 0, s>>>(n, n, Qin, ld, Q, ldq);
+  count_launch();
   return cudaGetLastError();
 }
 

@@ -211,6 +211,7 @@ cudaError_t panel_qr(double* P, long long ldp, int m, int bw, double* V, long lo
   cudaError_t e = cudaMemsetAsync(bar, 0, sizeof(unsigned), s);
   if (e != cudaSuccess) return e;
   void* args[] = {&P, &ldp, &m, &bw, &V, &ldv, &V2, &ldv2, &T, &red, &bar, (void*)&R};
+  count_launch();
   if (G == 1)
     return cudaLaunchKernel((void*)panel_qr_kernel, dim3(1), dim3(kPanelThreads), args, smem, s);
   return cudaLaunchCooperativeKernel((void*)panel_qr_kernel, dim3(G), dim3(kPanelThreads), args,
@@ -221,6 +222,7 @@ cudaError_t extract_band(const double* A, long long lda, int n, int b, double* A
                          cudaStream_t s) {
   if (n <= 0) return cudaSuccess;
   extract_band_kernel<<<n, 128, 0, s>>>(A, lda, n, b, AB, ldab);
+  count_launch();
   return cudaGetLastError();
 }
 

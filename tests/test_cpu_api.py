@@ -17,7 +17,7 @@ ROOT = Path(__file__).resolve().parents[1]
 
 def header_symbols():
     text = (ROOT / "include" / "bse_b200.h").read_text()
-    return sorted(set(re.findall(r"^\s*(?:int|size_t|const char\*)\s+(bse_\w+)\s*\(", text, re.M)))
+    return sorted(set(re.findall(r"^\s*(?:int|size_t|const char\*|long long)\s+(bse_\w+)\s*\(", text, re.M)))
 
 
 def test_header_declares_entry_points():
