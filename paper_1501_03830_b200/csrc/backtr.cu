@@ -7,6 +7,7 @@
 //    dependency-respecting order (sweep groups descending, steps ascending)
 //    by a column-slab kernel whose two small products run on DMMA.
 //  * Q1 (SY2SB panels): plain compact-WY, three DMMA GEMMs per panel.
+#include <algorithm>
 #include "eig.cuh"
 
 namespace bse {
@@ -237,26 +238,53 @@ cudaError_t q2_apply(int n, int b, int g, const double* Vblk, const double* VTbl
 }
 
 cudaError_t q1_apply(int n, int b, const double* Vall, long long ldv, const double* Tall,
-                     double* Z, long long ldz, int ncols, double* ybuf, double* y2buf,
-                     cudaStream_t s) {
+                     double* Z, long long ldz, int ncols, const Q1Scratch& w, cudaStream_t s) {
+  // Panels are merged in groups of kQ1Group (compact-WY of the product,
+  // T_g = [[T_A, -T_A (V_A^T V_B) T_B], [0, T_B]]) so the applying GEMMs run
+  // with K = kQ1Group*b instead of b.  Vall must be zero outside the
+  // reflectors (syevd memsets it before SY2SB).
   int np = 0;
   while (n - np * b - b >= 2) ++np;
   cudaError_t e = cudaSuccess;
-  for (int p = np - 1; p >= 0; --p) {
-    const int k = p * b, m = n - k - b;
-    const double* V = Vall + (k + b) + (long long)k * ldv;
-    const double* T = Tall + (size_t)p * b * b;
-    double* Zs = Z + (k + b);
-    // Y = V^T Zs (b x ncols)
-    GemmProblem g1 = make_gemm(b, ncols, m, 1.0, V, ldv, Zs, ldz, 0.0, ybuf, b);
-    if ((e = gemm(true, false, g1, s)) != cudaSuccess) return e;
-    // Y2 = T Y
-    GemmProblem g2 = make_gemm(b, ncols, b, 1.0, T, b, ybuf, b, 0.0, y2buf, b);
-    g2.ma = Mask::upper();
-    if ((e = gemm(false, false, g2, s)) != cudaSuccess) return e;
+  const int G = kQ1Group;
+  for (int pend = np; pend > 0; pend -= G) {
+    const int p0 = std::max(0, pend - G), k = pend - p0, kb = k * b;
+    const int r0 = (p0 + 1) * b, m = n - r0;
+    const double* V = Vall + r0 + (long long)(p0 * b) * ldv;  // m x kb
+    double* Tg = w.tg;                                        // kb x kb (ld kb)
+    // block-diagonal T_p, then the off-diagonal blocks column by column
+    if ((e = cudaMemsetAsync(Tg, 0, sizeof(double) * kb * kb, s)) != cudaSuccess) return e;
+    for (int j = 0; j < k; ++j) {
+      if ((e = cudaMemcpy2DAsync(Tg + (long long)j * b + (long long)j * b * kb, kb * sizeof(double),
+                                 Tall + (size_t)(p0 + j) * b * b, b * sizeof(double),
+                                 b * sizeof(double), b, cudaMemcpyDeviceToDevice, s)) != cudaSuccess)
+        return e;
+    }
+    for (int j = 1; j < k; ++j) {
+      const int jb = j * b;
+      // X = V[:, :jb]^T V[:, jb:jb+b]   (jb x b, K = m)
+      GemmProblem gx = make_gemm(jb, b, m, 1.0, V, ldv, V + (long long)jb * ldv, ldv, 0.0, w.x, jb);
+      if ((e = gemm_splitk(true, false, gx, 16, w.splitk_ws, w.probs, s)) != cudaSuccess) return e;
+      // tmp = T_g[:jb,:jb] X ; T_g[:jb, jb:jb+b] = -tmp T_j
+      GemmProblem g1 = make_gemm(jb, b, jb, 1.0, Tg, kb, w.x, jb, 0.0, w.tmp, jb);
+      g1.ma = Mask::upper();
+      if ((e = gemm(false, false, g1, s)) != cudaSuccess) return e;
+      GemmProblem g2 = make_gemm(jb, b, b, -1.0, w.tmp, jb, Tg + jb + (long long)jb * kb, kb, 0.0,
+                                 Tg + (long long)jb * kb, kb);
+      g2.mb = Mask::upper();
+      if ((e = gemm(false, false, g2, s)) != cudaSuccess) return e;
+    }
+    double* Zs = Z + r0;
+    // Y = V^T Zs (kb x ncols)
+    GemmProblem g3 = make_gemm(kb, ncols, m, 1.0, V, ldv, Zs, ldz, 0.0, w.y, kb);
+    if ((e = gemm(true, false, g3, s)) != cudaSuccess) return e;
+    // Y2 = T_g Y
+    GemmProblem g4 = make_gemm(kb, ncols, kb, 1.0, Tg, kb, w.y, kb, 0.0, w.y2, kb);
+    g4.ma = Mask::upper();
+    if ((e = gemm(false, false, g4, s)) != cudaSuccess) return e;
     // Zs -= V Y2
-    GemmProblem g3 = make_gemm(m, ncols, b, -1.0, V, ldv, y2buf, b, 1.0, Zs, ldz);
-    if ((e = gemm(false, false, g3, s)) != cudaSuccess) return e;
+    GemmProblem g5 = make_gemm(m, ncols, kb, -1.0, V, ldv, w.y2, kb, 1.0, Zs, ldz);
+    if ((e = gemm(false, false, g5, s)) != cudaSuccess) return e;
   }
   return e;
 }

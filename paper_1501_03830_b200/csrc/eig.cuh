@@ -43,10 +43,19 @@ cudaError_t q2_build(int n, int b, int g, const double* V2, const double* tau2, 
 cudaError_t q2_apply(int n, int b, int g, const double* Vblk, const double* VTblk, double* Z,
                      long long ldz, int ncols, cudaStream_t s);
 
-// Q1 back-transform: Z <- Q1 Z using the SY2SB panels.
+// Q1 back-transform: Z <- Q1 Z using the SY2SB panels (merged kQ1Group at a time).
+constexpr int kQ1Group = 4;
+struct Q1Scratch {
+  double* tg = nullptr;    // (G b)^2
+  double* x = nullptr;     // (G b) x b
+  double* tmp = nullptr;   // (G b) x b
+  double* y = nullptr;     // (G b) x ncols
+  double* y2 = nullptr;    // (G b) x ncols
+  double* splitk_ws = nullptr;  // 16 * (G b) * b
+  GemmProblem* probs = nullptr; // 64
+};
 cudaError_t q1_apply(int n, int b, const double* Vall, long long ldv, const double* Tall,
-                     double* Z, long long ldz, int ncols, double* ybuf, double* y2buf,
-                     cudaStream_t s);
+                     double* Z, long long ldz, int ncols, const Q1Scratch& w, cudaStream_t s);
 
 // Tridiagonal divide and conquer.
 struct StedcWork {

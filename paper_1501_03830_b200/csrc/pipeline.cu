@@ -50,7 +50,7 @@ struct SyevdWork {
   double* d; double* e;
   double* V2; double* tau2; int* progress;
   double* Vblk; double* VTblk;
-  double* ybuf; double* y2buf;
+  Q1Scratch q1;
   StedcWork dc;
 };
 
@@ -83,8 +83,14 @@ SyevdWork carve_syevd(Arena& a, int n) {
   const size_t qb = q2_block_doubles(n, b, kQ2Group);
   w.Vblk = a.take<double>(qb);
   w.VTblk = a.take<double>(qb);
-  w.ybuf = a.take<double>((size_t)b * n);
-  w.y2buf = a.take<double>((size_t)b * n);
+  const size_t gb = (size_t)kQ1Group * b;
+  w.q1.tg = a.take<double>(gb * gb);
+  w.q1.x = a.take<double>(gb * b);
+  w.q1.tmp = a.take<double>(gb * b);
+  w.q1.y = a.take<double>(gb * n);
+  w.q1.y2 = a.take<double>(gb * n);
+  w.q1.splitk_ws = a.take<double>(16 * gb * b);
+  w.q1.probs = a.take<GemmProblem>(64);
   w.dc = stedc_carve(a, n);
   return w;
 }
@@ -110,6 +116,7 @@ cudaError_t syevd(int n, double* A, long long lda, double* w, double* Z, long lo
   const int sms = device_sm_count();
   cudaError_t e;
   stage_mark("sy2sb", s);
+  if ((e = cudaMemsetAsync(ws.Vall, 0, sizeof(double) * ws.ldv * n, s)) != cudaSuccess) return e;
   if ((e = sy2sb(A, lda, n, b, ws.Vall, ws.ldv, ws.Tall, ws.sc, sms, s)) != cudaSuccess) return e;
   stage_mark("sb2st", s);
   if ((e = extract_band(A, lda, n, b, ws.AB, ws.ldab, s)) != cudaSuccess) return e;
@@ -122,7 +129,7 @@ cudaError_t syevd(int n, double* A, long long lda, double* w, double* Z, long lo
   stage_mark("q2_apply", s);
   if ((e = q2_apply(n, b, kQ2Group, ws.Vblk, ws.VTblk, Z, ldz, n, s)) != cudaSuccess) return e;
   stage_mark("q1_apply", s);
-  return q1_apply(n, b, ws.Vall, ws.ldv, ws.Tall, Z, ldz, n, ws.ybuf, ws.y2buf, s);
+  return q1_apply(n, b, ws.Vall, ws.ldv, ws.Tall, Z, ldz, n, ws.q1, s);
 }
 
 // ---------------------------------------------------------------------------

@@ -10,21 +10,22 @@
 namespace bse {
 namespace {
 
-constexpr int kSbThreads = 128;
+constexpr int kSbThreads = 256;
 constexpr int kDone = 0x7fffffff;
+constexpr int kLd = kMaxPanel + 1;
+constexpr int kSlots = kMaxPanel * kMaxPanel / kSbThreads;  // 16 block slots per thread
 
 struct SbSmem {
-  double D[kMaxPanel * (kMaxPanel + 1)];  // symmetric block, [c*(b+1) + r]
-  double O[kMaxPanel * (kMaxPanel + 1)];  // off-diagonal block, [c*(b+1) + r]
-  double v[kMaxPanel];
-  double vn[kMaxPanel];
+  double D[kMaxPanel * kLd];  // symmetric block, full, [c*kLd + r]
+  double O[kMaxPanel * kLd];  // off-diagonal block, [c*kLd + r]
+  double v[kMaxPanel];        // current reflector
+  double vn[kMaxPanel];       // new reflector
   double w[kMaxPanel];
-  double red[32];
   double sc[4];
 };
 
-// Householder of x[0..len) held in smem (one warp); writes v (v[0]=1) and
-// returns tau/beta through sc.  LAPACK dlarfg conventions.
+// Householder of x[0..len) (one warp, LAPACK dlarfg conventions): v (v[0]=1),
+// sc[0] = tau, sc[1] = beta.
 BSE_DEV void warp_house(const double* x, int len, double* v, double* sc) {
   const int lane = threadIdx.x & 31;
   double s = 0.0;
@@ -37,14 +38,14 @@ BSE_DEV void warp_house(const double* x, int len, double* v, double* sc) {
     tau = (beta - x0) / beta;
     scale = 1.0 / (x0 - beta);
   }
-  for (int i = lane; i < len; i += 32) v[i] = (i == 0) ? 1.0 : (tau != 0.0 ? x[i] * scale : 0.0);
+  for (int i = lane; i < kMaxPanel; i += 32)
+    v[i] = (i == 0) ? 1.0 : ((i < len && tau != 0.0) ? x[i] * scale : 0.0);
   if (lane == 0) { sc[0] = tau; sc[1] = beta; }
 }
 
 BSE_DEV void wait_progress(const int* progress, int s, int need) {
-  if (s <= 0) return;
-  if (threadIdx.x == 0) {
-    while (ld_acquire(progress + s - 1) < need) __nanosleep(64);
+  if (s > 0 && threadIdx.x == 0) {
+    while (ld_acquire(progress + s - 1) < need) __nanosleep(32);
   }
   __syncthreads();
 }
@@ -57,34 +58,41 @@ BSE_DEV void signal_progress(int* progress, int s, int val) {
   }
 }
 
-// D (len x len symmetric, full in smem) <- H D H, H = I - tau v v^T.
-BSE_DEV void two_sided(double* D, int ldd, int len, const double* v, double tau, double* w,
-                       double* red) {
+// Two-sided D <- H D H (H = I - tau v v^T) on the len x len symmetric block in
+// smem; the lower triangle of the result is stored straight to the band.
+BSE_DEV void two_sided_store(SbSmem& sm, int len, const double* v, double tau, double* AB,
+                             int ldab, int q0) {
   const int tid = threadIdx.x;
-  if (tau == 0.0) return;
-  // p = tau D v
-  for (int i = tid; i < len; i += blockDim.x) {
-    double s = 0.0;
-    for (int k = 0; k < len; ++k) s += D[k * ldd + i] * v[k];
-    w[i] = tau * s;
+  const int lane = tid & 31;
+  // p = tau D v : 4 threads per row
+  {
+    const int r = tid >> 2, q = tid & 3;
+    double acc = 0.0;
+    if (r < len)
+      for (int c = q; c < len; c += 4) acc += sm.D[c * kLd + r] * v[c];
+    acc += __shfl_xor_sync(0xffffffffu, acc, 1);
+    acc += __shfl_xor_sync(0xffffffffu, acc, 2);
+    if (q == 0 && r < kMaxPanel) sm.w[r] = (r < len) ? tau * acc : 0.0;
   }
   __syncthreads();
-  // alpha = -0.5 tau p^T v
   if (tid < 32) {
-    double s = 0.0;
-    for (int i = tid; i < len; i += 32) s += w[i] * v[i];
-    s = warp_sum(s);
-    if (tid == 0) red[0] = -0.5 * tau * s;
+    double a = 0.0;
+    for (int i = lane; i < len; i += 32) a += sm.w[i] * v[i];
+    a = warp_sum(a);
+    if (lane == 0) sm.sc[2] = -0.5 * tau * a;
   }
   __syncthreads();
-  const double alpha = red[0];
-  for (int i = tid; i < len; i += blockDim.x) w[i] += alpha * v[i];
-  __syncthreads();
-  for (int idx = tid; idx < len * len; idx += blockDim.x) {
-    const int r = idx % len, c = idx / len;
-    D[c * ldd + r] -= v[r] * w[c] + w[r] * v[c];
+  const double alpha = sm.sc[2];
+#pragma unroll
+  for (int k = 0; k < kSlots; ++k) {
+    const int idx = tid + k * kSbThreads;
+    const int r = idx & (kMaxPanel - 1), c = idx >> 6;
+    if (r < len && c <= r) {
+      const double wr = sm.w[r] + alpha * v[r], wc = sm.w[c] + alpha * v[c];
+      const double val = sm.D[c * kLd + r] - (v[r] * wc + wr * v[c]);
+      AB[(long long)(q0 + c) * ldab + (r - c)] = val;
+    }
   }
-  __syncthreads();
 }
 
 __global__ void __launch_bounds__(kSbThreads) sb2st_kernel(double* AB, int ldab, int n, int b,
@@ -93,120 +101,118 @@ __global__ void __launch_bounds__(kSbThreads) sb2st_kernel(double* AB, int ldab,
   extern __shared__ __align__(16) unsigned char raw[];
   SbSmem& sm = *reinterpret_cast<SbSmem*>(raw);
   const int tid = threadIdx.x;
-  const int ld = kMaxPanel + 1;
-  auto band = [&](int i, int j) -> double* { return AB + (long long)j * ldab + (i - j); };
+  auto bidx = [&](int i, int j) -> long long { return (long long)j * ldab + (i - j); };
 
   for (int s = blockIdx.x; s < n - 2; s += gridDim.x) {
     // ---------------- step 0: annihilate column s ----------------
     wait_progress(progress, s, 2);
     int p0 = s + 1, p1 = min(s + b, n - 1);
     int lp = p1 - p0 + 1;
-    for (int i = tid; i < lp; i += blockDim.x) sm.w[i] = __ldcg(band(p0 + i, s));
+    {
+      double dreg[kSlots];
+#pragma unroll
+      for (int k = 0; k < kSlots; ++k) {
+        const int idx = tid + k * kSbThreads;
+        const int r = idx & (kMaxPanel - 1), c = idx >> 6;
+        dreg[k] = (r < lp && c <= r) ? __ldcg(AB + bidx(p0 + r, p0 + c)) : 0.0;
+      }
+      if (tid < kMaxPanel) sm.w[tid] = tid < lp ? __ldcg(AB + bidx(p0 + tid, s)) : 0.0;
+#pragma unroll
+      for (int k = 0; k < kSlots; ++k) {
+        const int idx = tid + k * kSbThreads;
+        const int r = idx & (kMaxPanel - 1), c = idx >> 6;
+        if (c <= r) { sm.D[c * kLd + r] = dreg[k]; sm.D[r * kLd + c] = dreg[k]; }
+      }
+    }
     __syncthreads();
     if (tid < 32) warp_house(sm.w, lp, sm.v, sm.sc);
     __syncthreads();
     double tau = sm.sc[0];
-    const double beta0 = sm.sc[1];
-    for (int i = tid; i < lp; i += blockDim.x) *band(p0 + i, s) = (i == 0) ? beta0 : 0.0;
-    double* vslot = V2 + ((long long)s * maxsteps) * b;
-    for (int i = tid; i < b; i += blockDim.x) vslot[i] = i < lp ? sm.v[i] : 0.0;
+    if (tid < lp) AB[bidx(p0 + tid, s)] = (tid == 0) ? sm.sc[1] : 0.0;
+    if (tid < b) V2[((long long)s * maxsteps) * b + tid] = sm.v[tid];
     if (tid == 0) tau2[(long long)s * maxsteps] = tau;
-    // D block
-    for (int idx = tid; idx < lp * lp; idx += blockDim.x) {
-      const int r = idx % lp, c = idx / lp;
-      if (r >= c) {
-        const double x = __ldcg(band(p0 + r, p0 + c));
-        sm.D[c * ld + r] = x;
-        sm.D[r * ld + c] = x;
-      }
-    }
-    __syncthreads();
-    two_sided(sm.D, ld, lp, sm.v, tau, sm.w, sm.red);
-    for (int idx = tid; idx < lp * lp; idx += blockDim.x) {
-      const int r = idx % lp, c = idx / lp;
-      if (r >= c) *band(p0 + r, p0 + c) = sm.D[c * ld + r];
-    }
+    if (tau != 0.0) two_sided_store(sm, lp, sm.v, tau, AB, ldab, p0);
     signal_progress(progress, s, 1);
 
     // ---------------- steps j >= 1: chase the bulge ----------------
-    int j = 1;
-    while (true) {
+    for (int j = 1;; ++j) {
       const int q0 = p1 + 1;
       if (q0 > n - 1) break;
       const int q1 = min(p1 + b, n - 1);
       const int lq = q1 - q0 + 1;
       wait_progress(progress, s, j + 2);
-      // O block rows q0..q1, cols p0..p1
-      for (int idx = tid; idx < lq * lp; idx += blockDim.x) {
-        const int r = idx % lq, c = idx / lq;
-        sm.O[c * ld + r] = __ldcg(band(q0 + r, p0 + c));
+      {
+        double oreg[kSlots], dreg[kSlots];
+#pragma unroll
+        for (int k = 0; k < kSlots; ++k) {
+          const int idx = tid + k * kSbThreads;
+          const int r = idx & (kMaxPanel - 1), c = idx >> 6;
+          oreg[k] = (r < lq && c < lp) ? __ldcg(AB + bidx(q0 + r, p0 + c)) : 0.0;
+          dreg[k] = (r < lq && c <= r) ? __ldcg(AB + bidx(q0 + r, q0 + c)) : 0.0;
+        }
+#pragma unroll
+        for (int k = 0; k < kSlots; ++k) {
+          const int idx = tid + k * kSbThreads;
+          const int r = idx & (kMaxPanel - 1), c = idx >> 6;
+          sm.O[c * kLd + r] = oreg[k];
+          if (c <= r) { sm.D[c * kLd + r] = dreg[k]; sm.D[r * kLd + c] = dreg[k]; }
+        }
       }
       __syncthreads();
       if (tau != 0.0) {
-        // right-apply: O <- O (I - tau v v^T)
-        for (int r = tid; r < lq; r += blockDim.x) {
-          double acc = 0.0;
-          for (int c = 0; c < lp; ++c) acc += sm.O[c * ld + r] * sm.v[c];
-          sm.w[r] = tau * acc;
-        }
+        // right-apply: w = tau O v (4 threads per row), O -= w v^T
+        const int r = tid >> 2, q = tid & 3;
+        double acc = 0.0;
+        for (int c = q; c < lp; c += 4) acc += sm.O[c * kLd + r] * sm.v[c];
+        acc += __shfl_xor_sync(0xffffffffu, acc, 1);
+        acc += __shfl_xor_sync(0xffffffffu, acc, 2);
+        if (q == 0) sm.w[r] = tau * acc;
         __syncthreads();
-        for (int idx = tid; idx < lq * lp; idx += blockDim.x) {
-          const int r = idx % lq, c = idx / lq;
-          sm.O[c * ld + r] -= sm.w[r] * sm.v[c];
+#pragma unroll
+        for (int k = 0; k < kSlots; ++k) {
+          const int idx = tid + k * kSbThreads;
+          const int rr = idx & (kMaxPanel - 1), c = idx >> 6;
+          sm.O[c * kLd + rr] -= sm.w[rr] * sm.v[c];
         }
         __syncthreads();
       }
-      // new reflector from the first column of O
       if (tid < 32) warp_house(sm.O, lq, sm.vn, sm.sc);
       __syncthreads();
       const double taun = sm.sc[0], betan = sm.sc[1];
-      // left-apply to O[:, 1:]: y_c = vn^T O[:, c]
       if (taun != 0.0) {
-        for (int c = 1 + tid; c < lp; c += blockDim.x) {
-          double acc = 0.0;
-          for (int r = 0; r < lq; ++r) acc += sm.vn[r] * sm.O[c * ld + r];
-          sm.w[c] = taun * acc;
-        }
+        // left-apply to columns >= 1: y_c = taun * vn^T O[:, c] (4 threads per column)
+        const int c = tid >> 2, q = tid & 3;
+        double acc = 0.0;
+        for (int r = q; r < lq; r += 4) acc += sm.vn[r] * sm.O[c * kLd + r];
+        acc += __shfl_xor_sync(0xffffffffu, acc, 1);
+        acc += __shfl_xor_sync(0xffffffffu, acc, 2);
+        if (q == 0) sm.w[c] = taun * acc;
         __syncthreads();
-        for (int idx = tid; idx < lq * (lp - 1); idx += blockDim.x) {
-          const int r = idx % lq, c = 1 + idx / lq;
-          sm.O[c * ld + r] -= sm.vn[r] * sm.w[c];
+      }
+      // store O (column 0 = (beta, 0, ...)), reflector, then the two-sided D update
+#pragma unroll
+      for (int k = 0; k < kSlots; ++k) {
+        const int idx = tid + k * kSbThreads;
+        const int r = idx & (kMaxPanel - 1), c = idx >> 6;
+        if (r < lq && c < lp) {
+          double val;
+          if (c == 0) val = (r == 0) ? betan : 0.0;
+          else val = taun != 0.0 ? sm.O[c * kLd + r] - sm.vn[r] * sm.w[c] : sm.O[c * kLd + r];
+          AB[bidx(q0 + r, p0 + c)] = val;
         }
       }
-      __syncthreads();
-      if (tid == 0) sm.O[0] = betan;
-      for (int r = 1 + tid; r < lq; r += blockDim.x) sm.O[r] = 0.0;
-      __syncthreads();
-      for (int idx = tid; idx < lq * lp; idx += blockDim.x) {
-        const int r = idx % lq, c = idx / lq;
-        *band(q0 + r, p0 + c) = sm.O[c * ld + r];
-      }
-      // store reflector (s, j)
-      double* vs = V2 + ((long long)s * maxsteps + j) * b;
-      for (int i = tid; i < b; i += blockDim.x) vs[i] = i < lq ? sm.vn[i] : 0.0;
+      if (tid < b) V2[((long long)s * maxsteps + j) * b + tid] = sm.vn[tid];
       if (tid == 0) tau2[(long long)s * maxsteps + j] = taun;
-      // two-sided on the next diagonal block
-      for (int idx = tid; idx < lq * lq; idx += blockDim.x) {
-        const int r = idx % lq, c = idx / lq;
-        if (r >= c) {
-          const double x = __ldcg(band(q0 + r, q0 + c));
-          sm.D[c * ld + r] = x;
-          sm.D[r * ld + c] = x;
-        }
-      }
       __syncthreads();
-      two_sided(sm.D, ld, lq, sm.vn, taun, sm.w, sm.red);
-      for (int idx = tid; idx < lq * lq; idx += blockDim.x) {
-        const int r = idx % lq, c = idx / lq;
-        if (r >= c) *band(q0 + r, q0 + c) = sm.D[c * ld + r];
-      }
-      for (int i = tid; i < lq; i += blockDim.x) sm.v[i] = sm.vn[i];
+      if (taun != 0.0) two_sided_store(sm, lq, sm.vn, taun, AB, ldab, q0);
+      // the new reflector becomes the current one
+      __syncthreads();
+      if (tid < kMaxPanel) sm.v[tid] = sm.vn[tid];
       tau = taun;
       signal_progress(progress, s, j + 1);
       p0 = q0;
       p1 = q1;
       lp = lq;
-      ++j;
     }
     signal_progress(progress, s, kDone);
     __syncthreads();

@@ -158,7 +158,14 @@ __global__ void __launch_bounds__(kDcThreads) dc_prepare_kernel(
   w.zh[lo] = rho;  // stash rho for the secular / z-hat kernels
 }
 
-// ---- 2. secular equation: one thread per root (bisection in shifted coords) ----
+// ---- 2. secular equation: one thread per root ----
+// Root i of f(lam) = 1 + rho sum_j z_j^2 / (d_j - lam) lies in (d_i, d_{i+1})
+// (last root: (d_{K-1}, d_{K-1} + rho |z|^2]).  It is computed as an offset
+// tau from the closer pole (relative accuracy in tau is what the Loewner
+// formula needs) by a safeguarded rational iteration: f is modelled by
+// c + rho b1/(d_l - x) + rho b2/(d_r - x), fitted to f and f' at the current
+// iterate (the "middle way" of Li / LAPACK dlaed4), with bisection whenever
+// the model step leaves the bracket.  Converges in a handful of sweeps.
 __global__ void dc_secular_kernel(Level L, int n, StedcWork w) {
   int lo, mid, hi;
   node_range(L, n, blockIdx.y, lo, mid, hi);
@@ -169,8 +176,15 @@ __global__ void dc_secular_kernel(Level L, int n, StedcWork w) {
   const double rho = w.zh[lo];
   const double* dk = w.dk + lo;
   const double* zk = w.zk + lo;
-  int org;
-  double a, b;
+  if (K == 1) {
+    const double t = rho * zk[0] * zk[0];
+    w.org[lo] = 0;
+    w.tau[lo] = t;
+    w.val[lo] = dk[0] + t;
+    return;
+  }
+  int org, pl, pr;
+  double a, b;  // bracket for tau with f(a) < 0 <= f(b)
   if (i < K - 1) {
     const double half = 0.5 * (dk[i + 1] - dk[i]);
     double f = 0.0;
@@ -178,22 +192,53 @@ __global__ void dc_secular_kernel(Level L, int n, StedcWork w) {
     f = 1.0 + rho * f;
     if (f >= 0.0) { org = i; a = 0.0; b = half; }
     else { org = i + 1; a = -half; b = 0.0; }
+    pl = i; pr = i + 1;
   } else {
     double s = 0.0;
     for (int j = 0; j < K; ++j) s += zk[j] * zk[j];
     org = K - 1; a = 0.0; b = rho * s;
+    pl = K - 2; pr = K - 1;
   }
   const double d0 = dk[org];
-  for (int it = 0; it < 200; ++it) {
-    const double x = 0.5 * (a + b);
-    if (x == a || x == b) break;
-    double f = 0.0;
-    for (int j = 0; j < K; ++j) f += zk[j] * zk[j] / ((dk[j] - d0) - x);
-    f = 1.0 + rho * f;
-    if (f > 0.0) b = x; else a = x;
-    if (b - a <= 2.0 * kEps * fmax(fabs(a), fabs(b))) break;
+  const double dl = dk[pl] - d0, dr = dk[pr] - d0;
+  double t = 0.5 * (a + b);
+  for (int it = 0; it < 100; ++it) {
+    double psi = 0.0, dpsi = 0.0, phi = 0.0, dphi = 0.0;
+    for (int j = 0; j <= pl; ++j) {
+      const double inv = 1.0 / ((dk[j] - d0) - t);
+      const double q = zk[j] * zk[j] * inv;
+      psi += q;
+      dpsi += q * inv;
+    }
+    for (int j = pr; j < K; ++j) {
+      const double inv = 1.0 / ((dk[j] - d0) - t);
+      const double q = zk[j] * zk[j] * inv;
+      phi += q;
+      dphi += q * inv;
+    }
+    const double f = 1.0 + rho * (psi + phi);
+    if (f == 0.0) break;
+    if (f > 0.0) b = t; else a = t;
+    if (b - a <= 2.0 * kEps * fmax(fabs(a), fabs(b))) { t = 0.5 * (a + b); break; }
+    const double P0 = dl - t, Q0 = dr - t;
+    const double b1 = dpsi * P0 * P0, a1 = psi - dpsi * P0;
+    const double b2 = dphi * Q0 * Q0, a2 = phi - dphi * Q0;
+    const double c = 1.0 + rho * (a1 + a2);
+    const double B = c * (P0 + Q0) + rho * (b1 + b2);
+    const double C0 = f * P0 * Q0;
+    const double disc = B * B - 4.0 * c * C0;
+    double tn;
+    if (disc >= 0.0 && B != 0.0) {
+      const double eta = 2.0 * C0 / (B + copysign(sqrt(disc), B));
+      tn = t + eta;
+    } else {
+      tn = 0.5 * (a + b);
+    }
+    if (!(tn > a && tn < b)) tn = 0.5 * (a + b);
+    const bool done = fabs(tn - t) <= 2.0 * kEps * fabs(tn);
+    t = tn;
+    if (done) break;
   }
-  const double t = 0.5 * (a + b);
   w.org[lo + i] = org;
   w.tau[lo + i] = t;
   w.val[lo + i] = d0 + t;
