@@ -84,27 +84,32 @@ __global__ void __launch_bounds__(256) q2_build_kernel(int n, int b, int g, int 
 }
 
 // Column slab kernel: for each block in order, Z[r0:r0+HB, slab] -= VT (V^T Z).
+// Y = V^T Z reuses V's shared memory, so two CTAs fit per SM and the 256
+// slabs of an n = 16384 problem run as a single wave; Z rows are staged with
+// 16-byte cp.async from the even row below r0.
 template <int HB, int G>
-__global__ void __launch_bounds__(kQ2Threads) q2_apply_kernel(int n, int b, int maxsteps,
-                                                              const double* __restrict__ Vblk,
-                                                              const double* __restrict__ VTblk,
-                                                              double* __restrict__ Z, long long ldz,
-                                                              int ncols) {
-  constexpr int LDV = HB + 4;   // K-major / MN-major conflict-free pads (== 4 mod 16)
+__global__ void __launch_bounds__(kQ2Threads, 2) q2_apply_kernel(int n, int b, int maxsteps,
+                                                                 const double* __restrict__ Vblk,
+                                                                 const double* __restrict__ VTblk,
+                                                                 double* __restrict__ Z,
+                                                                 long long ldz, int ncols) {
+  constexpr int LDV = HB + 4;   // == 4 mod 16: conflict-free fragment loads
   constexpr int LDZ = HB + 4;
   constexpr int LDY = G + 4;
   constexpr int W = kQ2W;
+  static_assert(W * LDY <= G * LDV, "Y must fit in V's buffer");
   extern __shared__ __align__(16) double sm[];
-  double* sV = sm;               // HB x G  [c*LDV + r]
+  double* sV = sm;               // HB x G  [c*LDV + r]; later Y (G x W) [c*LDY + r]
   double* sVT = sV + G * LDV;    // HB x G
-  double* sZ = sVT + G * LDV;    // HB x W  [c*LDZ + r]
-  double* sY = sZ + W * LDZ;     // G x W   [c*LDY + r]
+  double* sZ = sVT + G * LDV;    // (HB+2) x W  [c*LDZ + r]
+  double* sY = sV;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int c0 = blockIdx.x * W;
   const int wcols = min(W, ncols - c0);
   const int nsweeps = n - 2;
   const int ngroups = (int)ceil_div(nsweeps, G);
   const int kl = lane & 3, rl = lane >> 2;
+  const int wm = warp & 1, wn = warp >> 1;
 
   for (int gi = ngroups - 1; gi >= 0; --gi) {
     const int s0 = gi * G;
@@ -115,17 +120,24 @@ __global__ void __launch_bounds__(kQ2Threads) q2_apply_kernel(int n, int b, int 
       const double* gV = Vblk + blk * HB * G;
       const double* gVT = VTblk + blk * HB * G;
       const int rows = min(HB, n - r0);
-      // load V, VT (HB x G) and Z rows
+      const int off = r0 & 1;          // smem row of global row r0
+      const int re = r0 - off;         // even start row
+      const int rows_e = rows + off;   // rows staged
       for (int idx = tid; idx < HB * G / 2; idx += blockDim.x) {
         const int e = idx * 2;
         const int r = e % HB, c = e / HB;
         cp_async16(sV + c * LDV + r, gV + e, true);
         cp_async16(sVT + c * LDV + r, gVT + e, true);
       }
-      for (int idx = tid; idx < HB * W; idx += blockDim.x) {
-        const int r = idx % HB, c = idx / HB;
-        const bool ok = r < rows && c < wcols;
-        cp_async8(sZ + c * LDZ + r, ok ? Z + (r0 + r) + (long long)(c0 + c) * ldz : Z, ok);
+      constexpr int ZCH = (HB + 2) / 2;  // 16-byte chunks per column
+      for (int idx = tid; idx < ZCH * W; idx += blockDim.x) {
+        const int r = (idx % ZCH) * 2, c = idx / ZCH;
+        const bool cok = c < wcols;
+        const double* src = Z + re + r + (long long)(c0 + c) * ldz;
+        double* dst = sZ + c * LDZ + r;
+        const bool v0 = cok && r < rows_e, v1 = cok && r + 1 < rows_e;
+        if (v0 && v1) cp_async16(dst, src, true);
+        else { cp_async8(dst, v0 ? src : Z, v0); cp_async8(dst + 1, v1 ? src + 1 : Z, v1); }
       }
       cp_async_commit();
       cp_async_wait<0>();
@@ -133,21 +145,22 @@ __global__ void __launch_bounds__(kQ2Threads) q2_apply_kernel(int n, int b, int 
       // Y (G x W) = V^T Z : 8 warps as 2 (m) x 4 (n), warp tile (G/2) x 16
       {
         constexpr int WM = G / 2, MI = WM / 8;
-        const int wm = warp & 1, wn = warp >> 1;
         double acc[MI][2][2];
 #pragma unroll
         for (int i = 0; i < MI; ++i) acc[i][0][0] = acc[i][0][1] = acc[i][1][0] = acc[i][1][1] = 0.0;
+#pragma unroll 4
         for (int k = 0; k < HB; k += 4) {
           double af[MI], bf[2];
 #pragma unroll
           for (int i = 0; i < MI; ++i) af[i] = sV[(wm * WM + i * 8 + rl) * LDV + k + kl];
 #pragma unroll
-          for (int jj = 0; jj < 2; ++jj) bf[jj] = sZ[(wn * 16 + jj * 8 + rl) * LDZ + k + kl];
+          for (int jj = 0; jj < 2; ++jj) bf[jj] = sZ[(wn * 16 + jj * 8 + rl) * LDZ + off + k + kl];
 #pragma unroll
           for (int i = 0; i < MI; ++i)
 #pragma unroll
             for (int jj = 0; jj < 2; ++jj) dmma8x8x4(acc[i][jj], af[i], bf[jj]);
         }
+        __syncthreads();  // V consumed: Y overwrites it
 #pragma unroll
         for (int i = 0; i < MI; ++i)
 #pragma unroll
@@ -162,7 +175,6 @@ __global__ void __launch_bounds__(kQ2Threads) q2_apply_kernel(int n, int b, int 
       // Z (HB x W) -= VT Y : 8 warps as 2 (m) x 4 (n), warp tile (HB/2) x 16
       {
         constexpr int WM = HB / 2, MI = WM / 8;
-        const int wm = warp & 1, wn = warp >> 1;
         double acc[MI][2][2];
 #pragma unroll
         for (int i = 0; i < MI; ++i) acc[i][0][0] = acc[i][0][1] = acc[i][1][0] = acc[i][1][1] = 0.0;
@@ -185,7 +197,8 @@ __global__ void __launch_bounds__(kQ2Threads) q2_apply_kernel(int n, int b, int 
 #pragma unroll
             for (int e = 0; e < 2; ++e) {
               const int r = wm * WM + i * 8 + rl, c = wn * 16 + jj * 8 + kl * 2 + e;
-              if (r < rows && c < wcols) Z[(r0 + r) + (long long)(c0 + c) * ldz] = sZ[c * LDZ + r] - acc[i][jj][e];
+              if (r < rows && c < wcols)
+                Z[(r0 + r) + (long long)(c0 + c) * ldz] = sZ[c * LDZ + off + r] - acc[i][jj][e];
             }
       }
       __syncthreads();
@@ -224,8 +237,7 @@ cudaError_t q2_apply(int n, int b, int g, const double* Vblk, const double* VTbl
   if (b != 64 || g != kQ2G) return cudaErrorInvalidValue;
   constexpr int HB = 96, G = kQ2G;  // q2_hb(64, 32)
   const int maxsteps = sb2st_maxsteps(n, b);
-  const size_t smem = sizeof(double) * (2 * (size_t)G * (HB + 4) + (size_t)kQ2W * (HB + 4) +
-                                        (size_t)kQ2W * (G + 4));
+  const size_t smem = sizeof(double) * (2 * (size_t)G * (HB + 4) + (size_t)kQ2W * (HB + 4));
   static bool attr = false;
   if (!attr) {
     cudaFuncSetAttribute(q2_apply_kernel<HB, G>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
@@ -252,6 +264,7 @@ cudaError_t q1_apply(int n, int b, const double* Vall, long long ldv, const doub
     const int r0 = (p0 + 1) * b, m = n - r0;
     const double* V = Vall + r0 + (long long)(p0 * b) * ldv;  // m x kb
     double* Tg = w.tg;                                        // kb x kb (ld kb)
+    stage_mark("q1_tg", s);
     // block-diagonal T_p, then the off-diagonal blocks column by column
     if ((e = cudaMemsetAsync(Tg, 0, sizeof(double) * kb * kb, s)) != cudaSuccess) return e;
     for (int j = 0; j < k; ++j) {
@@ -275,6 +288,7 @@ cudaError_t q1_apply(int n, int b, const double* Vall, long long ldv, const doub
       if ((e = gemm(false, false, g2, s)) != cudaSuccess) return e;
     }
     double* Zs = Z + r0;
+    stage_mark("q1_gemm", s);
     // Y = V^T Zs (kb x ncols)
     GemmProblem g3 = make_gemm(kb, ncols, m, 1.0, V, ldv, Zs, ldz, 0.0, w.y, kb);
     if ((e = gemm(true, false, g3, s)) != cudaSuccess) return e;

@@ -118,6 +118,37 @@ __global__ void __launch_bounds__(kLeaf) trsm_left_leaf(const double* __restrict
   }
 }
 
+// --- inverse of an n x n (n <= 64) lower-triangular block: Y = L^{-1} ---
+// One thread per column j: L y = e_j by forward substitution (exact zeros above j).
+__global__ void __launch_bounds__(kLeaf) trtri_leaf(const double* __restrict__ L, long long ldl,
+                                                    int n, double* __restrict__ Y) {
+  __shared__ double Ls[kLeaf * kLds];  // column-major
+  const int tid = threadIdx.x;
+  for (int idx = tid; idx < n * n; idx += blockDim.x) {
+    const int r = idx % n, c = idx / n;
+    Ls[c * kLds + r] = (r >= c) ? L[r + c * ldl] : 0.0;
+  }
+  __syncthreads();
+  const int j = tid;
+  if (j < n) {
+    double y[kLeaf];
+#pragma unroll
+    for (int i = 0; i < kLeaf; ++i) y[i] = 0.0;
+#pragma unroll
+    for (int i = 0; i < kLeaf; ++i) {
+      if (i < j || i >= n) continue;
+      double s = (i == j) ? 1.0 : 0.0;
+#pragma unroll
+      for (int k = 0; k < kLeaf; ++k)
+        if (k >= j && k < i) s -= Ls[k * kLds + i] * y[k];
+      y[i] = s / Ls[i * kLds + i];
+    }
+#pragma unroll
+    for (int i = 0; i < kLeaf; ++i)
+      if (i < n) Y[i + j * kLeaf] = y[i];
+  }
+}
+
 __global__ void zero_upper_kernel(double* A, long long lda, int n) {
   const int r = blockIdx.x * blockDim.x + threadIdx.x;
   const int c = blockIdx.y;
@@ -154,6 +185,15 @@ void ensure_smem() {
   }
 }
 
+// Per-device scratch for leaf inverses (64 x 64), allocated once.
+double* leaf_scratch() {
+  static double* bufs[64] = {nullptr};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (!bufs[dev]) cudaMalloc(&bufs[dev], sizeof(double) * kLeaf * kLeaf);
+  return bufs[dev];
+}
+
 int split_point(int n) {
   int n1 = ((n / 2 + kLeaf - 1) / kLeaf) * kLeaf;
   if (n1 >= n) n1 = n - kLeaf;
@@ -166,10 +206,14 @@ cudaError_t trsm_rlt(const double* L, long long ldl, int n, double* A, long long
                      cudaStream_t s) {
   if (n <= 0 || m <= 0) return cudaSuccess;
   if (n <= kLeaf) {
-    ensure_smem<trsm_rlt_leaf>();
-    trsm_rlt_leaf<<<(unsigned)ceil_div(m, kLeaf), kLeaf, kLeafSmem, s>>>(L, ldl, n, A, lda, m);
+    // A <- A * (L^{-1})^T : invert the block, then one in-place DMMA GEMM
+    // (N = K = n <= BN, so every CTA reads its full row slab before writing).
+    double* Y = leaf_scratch();
+    trtri_leaf<<<1, kLeaf, 0, s>>>(L, ldl, n, Y);
     count_launch();
-    return cudaGetLastError();
+    GemmProblem p = make_gemm(m, n, n, 1.0, A, lda, Y, kLeaf, 0.0, A, lda);
+    p.mb = Mask::lower();
+    return gemm(false, true, p, s);
   }
   const int n1 = split_point(n), n2 = n - n1;
   cudaError_t e = trsm_rlt(L, ldl, n1, A, lda, m, s);
@@ -185,10 +229,12 @@ cudaError_t trsm_llt(const double* L, long long ldl, int n, double* B, long long
                      cudaStream_t s) {
   if (n <= 0 || ncols <= 0) return cudaSuccess;
   if (n <= kLeaf) {
-    ensure_smem<trsm_left_leaf<true>>();
-    trsm_left_leaf<true><<<(unsigned)ceil_div(ncols, kLeaf), kLeaf, kLeafSmem, s>>>(L, ldl, n, B, ldb, ncols);
+    double* Y = leaf_scratch();
+    trtri_leaf<<<1, kLeaf, 0, s>>>(L, ldl, n, Y);
     count_launch();
-    return cudaGetLastError();
+    GemmProblem p = make_gemm(n, ncols, n, 1.0, Y, kLeaf, B, ldb, 0.0, B, ldb);
+    p.ma = Mask::lower();
+    return gemm(true, false, p, s);
   }
   const int n1 = split_point(n), n2 = n - n1;
   cudaError_t e = trsm_llt(L + n1 + n1 * ldl, ldl, n2, B + n1, ldb, ncols, s);
@@ -204,10 +250,12 @@ cudaError_t trsm_lln(const double* L, long long ldl, int n, double* B, long long
                      cudaStream_t s) {
   if (n <= 0 || ncols <= 0) return cudaSuccess;
   if (n <= kLeaf) {
-    ensure_smem<trsm_left_leaf<false>>();
-    trsm_left_leaf<false><<<(unsigned)ceil_div(ncols, kLeaf), kLeaf, kLeafSmem, s>>>(L, ldl, n, B, ldb, ncols);
+    double* Y = leaf_scratch();
+    trtri_leaf<<<1, kLeaf, 0, s>>>(L, ldl, n, Y);
     count_launch();
-    return cudaGetLastError();
+    GemmProblem p = make_gemm(n, ncols, n, 1.0, Y, kLeaf, B, ldb, 0.0, B, ldb);
+    p.ma = Mask::lower();
+    return gemm(false, false, p, s);
   }
   const int n1 = split_point(n), n2 = n - n1;
   cudaError_t e = trsm_lln(L, ldl, n1, B, ldb, ncols, s);

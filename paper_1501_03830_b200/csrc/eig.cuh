@@ -21,8 +21,10 @@ struct Sy2sbScratch {
   double* red = nullptr;  // panel-QR grid reduction (2 * 148 * (2 + 2b))
   unsigned* bar = nullptr;
   double* splitk_ws = nullptr;  // 48 * b * b
-  GemmProblem* probs = nullptr; // 64 problems
+  double* symm_ws = nullptr;    // kSymmSplits * ld * b
+  GemmProblem* probs = nullptr; // 96 problems
 };
+constexpr int kSymmSplits = 16;
 
 cudaError_t sy2sb(double* A, long long lda, int n, int b, double* Vall, long long ldv,
                   double* Tall, const Sy2sbScratch& w, int num_sms, cudaStream_t s);
@@ -44,7 +46,7 @@ cudaError_t q2_apply(int n, int b, int g, const double* Vblk, const double* VTbl
                      long long ldz, int ncols, cudaStream_t s);
 
 // Q1 back-transform: Z <- Q1 Z using the SY2SB panels (merged kQ1Group at a time).
-constexpr int kQ1Group = 4;
+constexpr int kQ1Group = 8;
 struct Q1Scratch {
   double* tg = nullptr;    // (G b)^2
   double* x = nullptr;     // (G b) x b

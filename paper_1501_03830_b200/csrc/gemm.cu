@@ -278,47 +278,47 @@ __global__ void splitk_reduce_kernel(const double* __restrict__ ws, int splits, 
   *cp = alpha * acc + (beta != 0.0 ? beta * *cp : 0.0);
 }
 
+__global__ void splitk_setup_kernel(const GemmProblem p, bool transA, bool transB, int splits,
+                                    int chunk, double* ws, GemmProblem* out) {
+  const int i = threadIdx.x;
+  if (i >= splits) return;
+  GemmProblem q = p;
+  const int k0 = i * chunk;
+  q.K = min(chunk, p.K - k0);
+  // op(A) is M x K -> advance along k; masks are in stored, view-relative coordinates
+  q.A = transA ? p.A + k0 : p.A + (long long)k0 * p.lda;
+  q.B = transB ? p.B + (long long)k0 * p.ldb : p.B + k0;
+  const int da = transA ? k0 : -k0;   // shift of (c - r) for A's view
+  const int db = transB ? -k0 : k0;   // ... and for B's
+  if (p.ma.lo != kNoMaskLo) q.ma.lo = p.ma.lo + da;
+  if (p.ma.hi != kNoMaskHi) q.ma.hi = p.ma.hi + da;
+  if (p.mb.lo != kNoMaskLo) q.mb.lo = p.mb.lo + db;
+  if (p.mb.hi != kNoMaskHi) q.mb.hi = p.mb.hi + db;
+  q.C = ws + (long long)i * p.M * p.N;
+  q.ldc = p.M;
+  q.alpha = 1.0;
+  q.beta = 0.0;
+  q.mc = Mask{};
+  out[i] = q;
+}
+
 }  // namespace
 
 cudaError_t gemm_splitk(bool transA, bool transB, const GemmProblem& p, int splits, double* ws,
                         GemmProblem* probs_dev_scratch, cudaStream_t s) {
   if (p.M <= 0 || p.N <= 0) return cudaSuccess;
   if (splits <= 1 || p.K < 64 * splits) return gemm(transA, transB, p, s);
+  if (p.ma.unit || p.mb.unit) return cudaErrorInvalidValue;  // unit diag not split-safe
   // chunk K in multiples of 16 so every slice keeps cp.async alignment
   int chunk = (int)ceil_div(p.K, splits);
   chunk = (int)ceil_div(chunk, 16) * 16;
   splits = (int)ceil_div(p.K, chunk);
-  GemmProblem hp[64];
   if (splits > 64) return cudaErrorInvalidValue;
-  for (int i = 0; i < splits; ++i) {
-    GemmProblem q = p;
-    const int k0 = i * chunk;
-    q.K = min(chunk, p.K - k0);
-    // A: op(A) is M x K -> advance along k
-    q.A = transA ? p.A + k0 : p.A + (long long)k0 * p.lda;
-    q.B = transB ? p.B + (long long)k0 * p.ldb : p.B + k0;
-    // masks are expressed in stored coordinates relative to the view origin
-    if (!transA) { q.ma.lo = p.ma.lo == kNoMaskLo ? kNoMaskLo : p.ma.lo - k0;
-                   q.ma.hi = p.ma.hi == kNoMaskHi ? kNoMaskHi : p.ma.hi - k0; }
-    else         { q.ma.lo = p.ma.lo == kNoMaskLo ? kNoMaskLo : p.ma.lo + k0;
-                   q.ma.hi = p.ma.hi == kNoMaskHi ? kNoMaskHi : p.ma.hi + k0; }
-    if (!transB) { q.mb.lo = p.mb.lo == kNoMaskLo ? kNoMaskLo : p.mb.lo + k0;
-                   q.mb.hi = p.mb.hi == kNoMaskHi ? kNoMaskHi : p.mb.hi + k0; }
-    else         { q.mb.lo = p.mb.lo == kNoMaskLo ? kNoMaskLo : p.mb.lo - k0;
-                   q.mb.hi = p.mb.hi == kNoMaskHi ? kNoMaskHi : p.mb.hi - k0; }
-    if (q.ma.unit || q.mb.unit) return cudaErrorInvalidValue;  // unit diag not split-safe
-    q.C = ws + (long long)i * p.M * p.N;
-    q.ldc = p.M;
-    q.alpha = 1.0;
-    q.beta = 0.0;
-    q.mc = Mask::none();
-    hp[i] = q;
-  }
-  cudaError_t e = cudaMemcpyAsync(probs_dev_scratch, hp, sizeof(GemmProblem) * splits,
-                                  cudaMemcpyHostToDevice, s);
-  if (e != cudaSuccess) return e;
+  // descriptors are built on the device: no pageable H2D copy in the hot loop
+  splitk_setup_kernel<<<1, 64, 0, s>>>(p, transA, transB, splits, chunk, ws, probs_dev_scratch);
+  count_launch();
   const bool v2 = aligned16(p.A) && aligned16(p.B) && ((p.lda | p.ldb) & 1) == 0;
-  e = gemm_grouped(transA, transB, probs_dev_scratch, splits, p.M, p.N, s, v2);
+  cudaError_t e = gemm_grouped(transA, transB, probs_dev_scratch, splits, p.M, p.N, s, v2);
   if (e != cudaSuccess) return e;
   const long long tot = (long long)p.M * p.N;
   splitk_reduce_kernel<<<(unsigned)ceil_div(tot, 256), 256, 0, s>>>(ws, splits, p.M, p.N, p.alpha,

@@ -71,7 +71,8 @@ SyevdWork carve_syevd(Arena& a, int n) {
   w.sc.red = a.take<double>(2 * 192 * (2 + 2 * (size_t)b));
   w.sc.bar = a.take<unsigned>(4);
   w.sc.splitk_ws = a.take<double>(64 * (size_t)b * b);
-  w.sc.probs = a.take<GemmProblem>(64);
+  w.sc.symm_ws = a.take<double>((size_t)kSymmSplits * ld * b);
+  w.sc.probs = a.take<GemmProblem>(96);
   w.ldab = 2 * b;
   w.AB = a.take<double>((size_t)w.ldab * n);
   w.d = a.take<double>(n);
@@ -252,9 +253,11 @@ cudaError_t solve_spd_pair(int n, const double* M, long long ldm, const double* 
   scale_reverse_kernel<<<nb, 256, 0, s>>>(n, w.T1, ld, w.lam2, w.Zr, w.W, ld, lam, bad);
   count_launch();
   // u = L Zr (into T1), v = L^{-T} (Zr Lam) (in W)
+  stage_mark("recover_trmm", s);
   GemmProblem g4 = make_gemm(n, n, n, 1.0, w.L, ld, w.Zr, ld, 0.0, w.T1, ld);
   g4.ma = Mask::lower();
   if ((e = gemm(false, false, g4, s)) != cudaSuccess) return e;
+  stage_mark("recover_trsm", s);
   if ((e = trsm_llt(w.L, ld, n, w.W, ld, n, s)) != cudaSuccess) return e;
   recover_kernel<<<nb, 256, 0, s>>>(n, w.T1, w.W, ld, lam, X1, ldx1, X2, ldx2);
   count_launch();

@@ -446,11 +446,14 @@ cudaError_t stedc(int n, double* d, double* e, double* wout, double* Q, long lon
   for (int size = 2; size / 2 < n; size *= 2) {
     Level L{size, size / 2, (int)ceil_div(n, size)};
     const int maxm = std::min(size, n);
+    stage_mark("dc_prepare", s);
     dc_prepare_kernel<<<L.nnodes, kDcThreads, 0, s>>>(L, n, e, ws.scal, Din, Dout, Qin, Qout, ld, ws);
     count_launch();
     const dim3 g1((unsigned)ceil_div(maxm, 128), (unsigned)L.nnodes);
+    stage_mark("dc_secular", s);
     dc_secular_kernel<<<g1, 128, 0, s>>>(L, n, ws);
     count_launch();
+    stage_mark("dc_vectors", s);
     dc_zhat_kernel<<<g1, 128, 0, s>>>(L, n, ws, ws.zh);
     count_launch();
     dc_order_kernel<<<g1, 128, 0, s>>>(L, n, ws, Dout);
@@ -463,6 +466,7 @@ cudaError_t stedc(int n, double* d, double* e, double* wout, double* Q, long lon
     dc_probs_kernel<<<(unsigned)ceil_div(L.nnodes, 128), 128, 0, s>>>(L, n, ws, Qin, Qout, ld);
     count_launch();
     if ((err = cudaGetLastError()) != cudaSuccess) return err;
+    stage_mark("dc_gemm", s);
     err = gemm_grouped(false, false, ws.probs, 2 * L.nnodes, L.half, maxm, s, L.half >= 2);
     if (err != cudaSuccess) return err;
     std::swap(Din, Dout);

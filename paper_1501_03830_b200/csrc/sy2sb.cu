@@ -9,6 +9,7 @@
 // DMMA GEMMs (SYMM as two triangular products, SYR2K on the lower triangle):
 // 4/3 N^3 flops, all on the FP64 tensor pipe.
 #include <cooperative_groups.h>
+#include <algorithm>
 #include "eig.cuh"
 
 namespace bse {
@@ -246,22 +247,29 @@ cudaError_t sy2sb(double* A, long long lda, int n, int b, double* Vall, long lon
     double* slot0 = w.vwv;
     double* slot1 = w.vwv + lw * bw;
     double* slot2 = w.vwv + 2 * lw * bw;
+    stage_mark("sy2sb_panel", s);
     e = panel_qr(P, lda, m, bw, Vp, ldv, slot0, lw, Tp, w.red, w.bar, num_sms, s);
     if (e != cudaSuccess) return e;
     e = cudaMemcpy2DAsync(slot2, lw * sizeof(double), slot0, lw * sizeof(double),
                           (size_t)m * sizeof(double), bw, cudaMemcpyDeviceToDevice, s);
     if (e != cudaSuccess) return e;
+    stage_mark("sy2sb_symm", s);
     // Y = tril(A2) V + tril(A2,-1)^T V
+    // (split-K: the triangular masks give row blocks very different k-ranges;
+    //  splitting K balances them and fills the GPU with thin m x b outputs)
+    const int ssplit = (int)std::min<long long>(kSymmSplits, std::max<long long>(1, m / 1024));
     GemmProblem g1 = make_gemm(m, bw, m, 1.0, A2, lda, slot0, lw, 0.0, w.y, w.ldy);
     g1.ma = Mask::lower();
-    if ((e = gemm(false, false, g1, s)) != cudaSuccess) return e;
+    if ((e = gemm_splitk(false, false, g1, ssplit, w.symm_ws, w.probs, s)) != cudaSuccess) return e;
     GemmProblem g2 = make_gemm(m, bw, m, 1.0, A2, lda, slot0, lw, 1.0, w.y, w.ldy);
     g2.ma = Mask::strict_lower();
-    if ((e = gemm(true, false, g2, s)) != cudaSuccess) return e;
+    if ((e = gemm_splitk(true, false, g2, ssplit, w.symm_ws, w.probs + 32, s)) != cudaSuccess)
+      return e;
     // X = Y T -> slot1
     GemmProblem g3 = make_gemm(m, bw, bw, 1.0, w.y, w.ldy, Tp, bw, 0.0, slot1, lw);
     g3.mb = Mask::upper();
     if ((e = gemm(false, false, g3, s)) != cudaSuccess) return e;
+    stage_mark("sy2sb_small", s);
     // Zs = V^T X (bw x bw), split-K
     GemmProblem g4 = make_gemm(bw, bw, m, 1.0, slot0, lw, slot1, lw, 0.0, w.z, bw);
     const int splits = (int)std::min<long long>(48, std::max<long long>(1, m / 256));
@@ -273,6 +281,7 @@ cudaError_t sy2sb(double* A, long long lda, int n, int b, double* Vall, long lon
     // W = X - 0.5 V Z2 (in slot1)
     GemmProblem g6 = make_gemm(m, bw, bw, -0.5, slot0, lw, w.z2, bw, 1.0, slot1, lw);
     if ((e = gemm(false, false, g6, s)) != cudaSuccess) return e;
+    stage_mark("sy2sb_syr2k", s);
     // A2 -= [V W][W V]^T (lower)
     GemmProblem g7 = make_gemm(m, m, 2 * bw, -1.0, slot0, lw, slot1, lw, 1.0, A2, lda);
     g7.mc = Mask::lower();
