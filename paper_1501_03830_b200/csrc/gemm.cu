@@ -1,6 +1,7 @@
 // Masked FP64 GEMM engine: DMMA.8x8x4 tiles fed by a multistage cp.async
 // (LDGSTS) shared-memory pipeline.  See gemm.cuh for the contract.
 #include <cstdio>
+#include <cstdlib>
 #include "gemm.cuh"
 
 namespace bse {
@@ -59,7 +60,8 @@ BSE_DEV double apply_mask(double v, int d, bool inb, const Mask& m) {
   return (d < m.lo || d > m.hi) ? 0.0 : v;
 }
 
-template <int BM, int BN, int BK, int WM, int WN, int STAGES, bool TA, bool TB, int VEC>
+template <int BM, int BN, int BK, int WM, int WN, int STAGES, bool TA, bool TB, int VEC,
+          bool MASKED = true>
 BSE_DEV void gemm_tile(const GemmProblem& p, int m0, int n0, double* smem) {
   using C = Cfg<BM, BN, BK, WM, WN, STAGES, TA, TB>;
   const int M = p.M, N = p.N, K = p.K;
@@ -70,14 +72,14 @@ BSE_DEV void gemm_tile(const GemmProblem& p, int m0, int n0, double* smem) {
   const int mlast = min(m0 + BM, M) - 1, nlast = min(n0 + BN, N) - 1;
 
   // Output mask: skip tiles with no writable element.
-  {
+  if (MASKED) {
     const long long dmin = (long long)n0 - mlast, dmax = (long long)nlast - m0;
     if (dmax < p.mc.lo || dmin > p.mc.hi) return;
   }
 
   // k-range implied by the operand masks.
   long long kb = 0, ke = K;
-  {
+  if (MASKED) {
     const Mask& a = p.ma;
     const long long lo = a.unit ? min(a.lo, 0) : a.lo, hi = a.unit ? max(a.hi, 0) : a.hi;
     if (!TA) { kb = max(kb, (long long)m0 + lo); ke = min(ke, (long long)mlast + hi + 1); }
@@ -114,7 +116,7 @@ BSE_DEV void gemm_tile(const GemmProblem& p, int m0, int n0, double* smem) {
     cp_async_commit();
   }
 
-  const bool maskA_on = p.ma.active(), maskB_on = p.mb.active();
+  const bool maskA_on = MASKED && p.ma.active(), maskB_on = MASKED && p.mb.active();
   const int am_base = wm * WM + (lane >> 2);  // + i*8
   const int bn_base = wn * WN + (lane >> 2);  // + j*8
   const int kl = lane & 3;
@@ -197,8 +199,10 @@ BSE_DEV void gemm_tile(const GemmProblem& p, int m0, int n0, double* smem) {
       for (int e = 0; e < 2; ++e) {
         const int gn = n0 + wn * WN + j * 8 + kl * 2 + e;
         if (gn >= N) continue;
-        const int d = gn - gm;
-        if (d < p.mc.lo || d > p.mc.hi) continue;
+        if (MASKED) {
+          const int d = gn - gm;
+          if (d < p.mc.lo || d > p.mc.hi) continue;
+        }
         double* cp = p.C + gm + (long long)gn * p.ldc;
         double v = alpha * acc[i][j][e];
         if (beta != 0.0) v += beta * *cp;
@@ -208,11 +212,13 @@ BSE_DEV void gemm_tile(const GemmProblem& p, int m0, int n0, double* smem) {
   }
 }
 
-template <int BM, int BN, int BK, int WM, int WN, int STAGES, bool TA, bool TB, int VEC>
+template <int BM, int BN, int BK, int WM, int WN, int STAGES, bool TA, bool TB, int VEC,
+          bool MASKED>
 __global__ void __launch_bounds__(Cfg<BM, BN, BK, WM, WN, STAGES, TA, TB>::NT)
     gemm_single_kernel(const GemmProblem p) {
   extern __shared__ __align__(16) double smem[];
-  gemm_tile<BM, BN, BK, WM, WN, STAGES, TA, TB, VEC>(p, blockIdx.x * BM, blockIdx.y * BN, smem);
+  gemm_tile<BM, BN, BK, WM, WN, STAGES, TA, TB, VEC, MASKED>(p, blockIdx.x * BM, blockIdx.y * BN,
+                                                             smem);
 }
 
 template <int BM, int BN, int BK, int WM, int WN, int STAGES, bool TA, bool TB, int VEC>
@@ -229,8 +235,11 @@ cudaError_t launch(const GemmProblem* single, const GemmProblem* grouped, int co
   using C = Cfg<BM, BN, BK, WM, WN, STAGES, TA, TB>;
   static bool attr_done = false;  // per-instantiation, set once per process
   if (!attr_done) {
-    cudaError_t e = cudaFuncSetAttribute(gemm_single_kernel<BM, BN, BK, WM, WN, STAGES, TA, TB, VEC>,
+    cudaError_t e = cudaFuncSetAttribute(gemm_single_kernel<BM, BN, BK, WM, WN, STAGES, TA, TB, VEC, true>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM);
+    if (e != cudaSuccess) return e;
+    e = cudaFuncSetAttribute(gemm_single_kernel<BM, BN, BK, WM, WN, STAGES, TA, TB, VEC, false>,
+                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM);
     if (e != cudaSuccess) return e;
     e = cudaFuncSetAttribute(gemm_grouped_kernel<BM, BN, BK, WM, WN, STAGES, TA, TB, VEC>,
                              cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM);
@@ -239,8 +248,11 @@ cudaError_t launch(const GemmProblem* single, const GemmProblem* grouped, int co
   }
   dim3 grid((unsigned)ceil_div(maxM, BM), (unsigned)ceil_div(maxN, BN), (unsigned)count);
   if (grid.x == 0 || grid.y == 0 || count == 0) return cudaSuccess;
-  if (single)
-    gemm_single_kernel<BM, BN, BK, WM, WN, STAGES, TA, TB, VEC><<<grid, C::NT, C::SMEM, s>>>(*single);
+  const bool masked = single && (single->ma.active() || single->mb.active() || single->mc.active());
+  if (single && masked)
+    gemm_single_kernel<BM, BN, BK, WM, WN, STAGES, TA, TB, VEC, true><<<grid, C::NT, C::SMEM, s>>>(*single);
+  else if (single)
+    gemm_single_kernel<BM, BN, BK, WM, WN, STAGES, TA, TB, VEC, false><<<grid, C::NT, C::SMEM, s>>>(*single);
   else
     gemm_grouped_kernel<BM, BN, BK, WM, WN, STAGES, TA, TB, VEC><<<grid, C::NT, C::SMEM, s>>>(grouped);
   count_launch();
@@ -252,6 +264,9 @@ cudaError_t dispatch(int cfg, int vec, const GemmProblem* single, const GemmProb
                      int count, int maxM, int maxN, cudaStream_t s) {
   if (vec == 2) {
     if (cfg == 0) return launch<128, 128, 16, 64, 32, 4, TA, TB, 2>(single, grouped, count, maxM, maxN, s);
+    if (cfg == 2) return launch<128, 128, 32, 64, 32, 3, TA, TB, 2>(single, grouped, count, maxM, maxN, s);
+    if (cfg == 3) return launch<128, 64, 16, 32, 32, (TA ? 3 : 4), TA, TB, 2>(single, grouped, count, maxM, maxN, s);
+    if (cfg == 4) return launch<128, 64, 32, 32, 32, 2, TA, TB, 2>(single, grouped, count, maxM, maxN, s);
     return launch<64, 64, 16, 32, 32, 4, TA, TB, 2>(single, grouped, count, maxM, maxN, s);
   }
   return launch<64, 64, 16, 32, 32, 4, TA, TB, 1>(single, grouped, count, maxM, maxN, s);
@@ -330,18 +345,26 @@ cudaError_t gemm_splitk(bool transA, bool transB, const GemmProblem& p, int spli
 cudaError_t gemm(bool transA, bool transB, const GemmProblem& p, cudaStream_t s) {
   if (p.M <= 0 || p.N <= 0) return cudaSuccess;
   const bool v2 = aligned16(p.A) && aligned16(p.B) && ((p.lda | p.ldb) & 1) == 0;
-  const long long big_tiles = ceil_div(p.M, 128) * ceil_div(p.N, 128);
-  const int cfg = (v2 && big_tiles >= 120) ? 0 : 1;
+  // 128x64 tiles, 8 warps of 32x32, 2 CTAs/SM (cfg 3) measured 32-33 TFLOP/s
+  // on large FP64 GEMMs (86-90% of the DMMA peak); 64x64 for small outputs.
+  const long long big_tiles = ceil_div(p.M, 128) * ceil_div(p.N, 64);
+  int cfg = (v2 && big_tiles >= 148) ? 3 : 1;
+  static int forced = -2;
+  if (forced == -2) {
+    const char* v = std::getenv("BSE_GEMM_CFG");
+    forced = v ? std::atoi(v) : -1;
+  }
+  if (forced >= 0 && cfg == 3) cfg = forced;
   return dispatch_all(transA, transB, cfg, v2 ? 2 : 1, &p, nullptr, 1, p.M, p.N, s);
 }
 
 cudaError_t gemm_grouped(bool transA, bool transB, const GemmProblem* probs_dev, int count,
-                         int maxM, int maxN, cudaStream_t s, bool all_aligned16) {
+                         int maxM, int maxN, cudaStream_t s, bool all_aligned16, int cfg) {
   // Grouped problems may mix alignments (e.g. D&C nodes at odd offsets): the
   // 8-byte path is always legal; callers that guarantee 16-byte alignment of
   // every operand and even leading dimensions get the vectorised loads.
-  return dispatch_all(transA, transB, 1, all_aligned16 ? 2 : 1, nullptr, probs_dev, count, maxM,
-                      maxN, s);
+  return dispatch_all(transA, transB, all_aligned16 ? cfg : 1, all_aligned16 ? 2 : 1, nullptr,
+                      probs_dev, count, maxM, maxN, s);
 }
 
 }  // namespace bse

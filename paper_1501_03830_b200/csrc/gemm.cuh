@@ -44,7 +44,8 @@ cudaError_t gemm(bool transA, bool transB, const GemmProblem& p, cudaStream_t s)
 // Grouped: `probs` is a DEVICE array of `count` problems sharing (transA,
 // transB); maxM/maxN bound the grid.  Masks inside each problem are honoured.
 cudaError_t gemm_grouped(bool transA, bool transB, const GemmProblem* probs_dev, int count,
-                         int maxM, int maxN, cudaStream_t s, bool all_aligned16 = false);
+                         int maxM, int maxN, cudaStream_t s, bool all_aligned16 = false,
+                         int cfg = 1);
 
 // Split-K for short-and-wide outputs (M*N small, K large): `splits` partial
 // products go to `ws` (>= splits*M*N doubles), then a fixed-order reduction

@@ -5,6 +5,9 @@
 // progress counter per sweep), so ~N/(2b) sweeps are in flight at once.  The
 // band (ldab = 2b doubles per column) stays L2-resident; every reflector is
 // stored for the Q2 back-transform.
+#include <cstdio>
+#include <cstdlib>
+#include <vector>
 #include "eig.cuh"
 
 namespace bse {
@@ -43,9 +46,18 @@ BSE_DEV void warp_house(const double* x, int len, double* v, double* sc) {
   if (lane == 0) { sc[0] = tau; sc[1] = beta; }
 }
 
+__constant__ int c_sb_flags;  // tuning variants (BSE_SB2ST_VARIANT), default 0
+
 BSE_DEV void wait_progress(const int* progress, int s, int need) {
   if (s > 0 && threadIdx.x == 0) {
-    while (ld_acquire(progress + s - 1) < need) __nanosleep(32);
+    // relaxed polling (no L1 invalidation per probe), one acquire fence after
+    if (ld_relaxed(progress + s - 1) < need) {
+      const int ns = (c_sb_flags & 1) ? 256 : 0;
+      while (ld_relaxed(progress + s - 1) < need) {
+        if (ns) __nanosleep(ns);
+      }
+    }
+    fence_acquire();
   }
   __syncthreads();
 }
@@ -53,7 +65,8 @@ BSE_DEV void wait_progress(const int* progress, int s, int need) {
 BSE_DEV void signal_progress(int* progress, int s, int val) {
   __syncthreads();
   if (threadIdx.x == 0) {
-    __threadfence();
+    if (c_sb_flags & 2) fence_acquire();  // acq_rel fence (cheaper than sc)
+    else __threadfence();
     st_release(progress + s, val);
   }
 }
@@ -95,9 +108,20 @@ BSE_DEV void two_sided_store(SbSmem& sm, int len, const double* v, double tau, d
   }
 }
 
+BSE_DEV unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+
 __global__ void __launch_bounds__(kSbThreads) sb2st_kernel(double* AB, int ldab, int n, int b,
                                                            double* V2, double* tau2,
-                                                           int maxsteps, int* progress) {
+                                                           int maxsteps, int* progress,
+                                                           unsigned long long* trace) {
+  // optional trace (BSE_SB2ST_TRACE): CTA 1 records, for its first two sweeps,
+  // per step [wait begin, wait end, step end] in ns
+  const bool tr = trace != nullptr && blockIdx.x == 1 && threadIdx.x == 0;
+  int tcount = 0;
   extern __shared__ __align__(16) unsigned char raw[];
   SbSmem& sm = *reinterpret_cast<SbSmem*>(raw);
   const int tid = threadIdx.x;
@@ -105,7 +129,10 @@ __global__ void __launch_bounds__(kSbThreads) sb2st_kernel(double* AB, int ldab,
 
   for (int s = blockIdx.x; s < n - 2; s += gridDim.x) {
     // ---------------- step 0: annihilate column s ----------------
+    const bool trs = tr && s < 1 + 2 * (int)gridDim.x;
+    if (trs) trace[8 * tcount] = gtimer();
     wait_progress(progress, s, 2);
+    if (trs) trace[8 * tcount + 1] = gtimer();
     int p0 = s + 1, p1 = min(s + b, n - 1);
     int lp = p1 - p0 + 1;
     {
@@ -133,6 +160,7 @@ __global__ void __launch_bounds__(kSbThreads) sb2st_kernel(double* AB, int ldab,
     if (tid == 0) tau2[(long long)s * maxsteps] = tau;
     if (tau != 0.0) two_sided_store(sm, lp, sm.v, tau, AB, ldab, p0);
     signal_progress(progress, s, 1);
+    if (trs) { for (int q = 2; q < 8; ++q) trace[8 * tcount + q] = gtimer(); ++tcount; }
 
     // ---------------- steps j >= 1: chase the bulge ----------------
     for (int j = 1;; ++j) {
@@ -140,7 +168,9 @@ __global__ void __launch_bounds__(kSbThreads) sb2st_kernel(double* AB, int ldab,
       if (q0 > n - 1) break;
       const int q1 = min(p1 + b, n - 1);
       const int lq = q1 - q0 + 1;
+      if (trs) trace[8 * tcount] = gtimer();
       wait_progress(progress, s, j + 2);
+      if (trs) trace[8 * tcount + 1] = gtimer();
       {
         double oreg[kSlots], dreg[kSlots];
 #pragma unroll
@@ -159,6 +189,7 @@ __global__ void __launch_bounds__(kSbThreads) sb2st_kernel(double* AB, int ldab,
         }
       }
       __syncthreads();
+      if (trs) trace[8 * tcount + 2] = gtimer();
       if (tau != 0.0) {
         // right-apply: w = tau O v (4 threads per row), O -= w v^T
         const int r = tid >> 2, q = tid & 3;
@@ -176,8 +207,10 @@ __global__ void __launch_bounds__(kSbThreads) sb2st_kernel(double* AB, int ldab,
         }
         __syncthreads();
       }
+      if (trs) trace[8 * tcount + 3] = gtimer();
       if (tid < 32) warp_house(sm.O, lq, sm.vn, sm.sc);
       __syncthreads();
+      if (trs) trace[8 * tcount + 4] = gtimer();
       const double taun = sm.sc[0], betan = sm.sc[1];
       if (taun != 0.0) {
         // left-apply to columns >= 1: y_c = taun * vn^T O[:, c] (4 threads per column)
@@ -204,12 +237,15 @@ __global__ void __launch_bounds__(kSbThreads) sb2st_kernel(double* AB, int ldab,
       if (tid < b) V2[((long long)s * maxsteps + j) * b + tid] = sm.vn[tid];
       if (tid == 0) tau2[(long long)s * maxsteps + j] = taun;
       __syncthreads();
+      if (trs) trace[8 * tcount + 5] = gtimer();
       if (taun != 0.0) two_sided_store(sm, lq, sm.vn, taun, AB, ldab, q0);
+      if (trs) trace[8 * tcount + 6] = gtimer();
       // the new reflector becomes the current one
       __syncthreads();
       if (tid < kMaxPanel) sm.v[tid] = sm.vn[tid];
       tau = taun;
       signal_progress(progress, s, j + 1);
+      if (trs) { trace[8 * tcount + 7] = gtimer(); ++tcount; }
       p0 = q0;
       p1 = q1;
       lp = lq;
@@ -246,12 +282,40 @@ cudaError_t sb2st(double* AB, int ldab, int n, int b, double* d, double* e, doub
     }
     int per_sm = 0;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, sb2st_kernel, kSbThreads, smem);
+    int flags = 0;
+    if (const char* v = std::getenv("BSE_SB2ST_VARIANT")) flags = std::atoi(v);
+    cudaMemcpyToSymbolAsync(c_sb_flags, &flags, sizeof(int), 0, cudaMemcpyHostToDevice, s);
+    if (flags & 4) per_sm = 1;
     int grid = std::max(1, std::min(n - 2, std::max(1, per_sm) * num_sms));
     int maxsteps = sb2st_maxsteps(n, b);
-    void* args[] = {&AB, &ldab, &n, &b, &V2, &tau2, &maxsteps, &progress};
+    unsigned long long* trace = nullptr;
+    const bool want_trace = std::getenv("BSE_SB2ST_TRACE") != nullptr;
+    const int tmax = 2 * (maxsteps + 1);
+    if (want_trace) {
+      cudaMalloc(&trace, sizeof(unsigned long long) * 8 * tmax);
+      cudaMemsetAsync(trace, 0, sizeof(unsigned long long) * 8 * tmax, s);
+    }
+    void* args[] = {&AB, &ldab, &n, &b, &V2, &tau2, &maxsteps, &progress, &trace};
     count_launch();
     err = cudaLaunchCooperativeKernel((void*)sb2st_kernel, dim3(grid), dim3(kSbThreads), args, smem, s);
     if (err != cudaSuccess) return err;
+    if (want_trace) {
+      std::vector<unsigned long long> h(8 * tmax);
+      cudaMemcpyAsync(h.data(), trace, h.size() * 8, cudaMemcpyDeviceToHost, s);
+      cudaStreamSynchronize(s);
+      cudaFree(trace);
+      double acc[8] = {0};
+      int cnt = 0;
+      for (int k = 0; k < tmax; ++k) {
+        if (!h[8 * k + 7]) break;
+        for (int q = 1; q < 8; ++q) acc[q] += (double)(h[8 * k + q] - h[8 * k + q - 1]);
+        ++cnt;
+      }
+      const double d = std::max(cnt, 1) * 1e3;
+      std::fprintf(stderr, "[sb2st trace] grid=%d steps=%d us: wait %.2f load %.2f right %.2f house %.2f "
+                   "left+storeO %.2f twosided %.2f signal %.2f\n", grid, cnt, acc[1] / d, acc[2] / d,
+                   acc[3] / d, acc[4] / d, acc[5] / d, acc[6] / d, acc[7] / d);
+    }
   }
   band_to_tridiag_kernel<<<(unsigned)ceil_div(n, 256), 256, 0, s>>>(AB, ldab, n, d, e);
   count_launch();

@@ -202,7 +202,7 @@ __global__ void dc_secular_kernel(Level L, int n, StedcWork w) {
   const double d0 = dk[org];
   const double dl = dk[pl] - d0, dr = dk[pr] - d0;
   double t = 0.5 * (a + b);
-  for (int it = 0; it < 100; ++it) {
+  for (int it = 0; it < 60; ++it) {
     double psi = 0.0, dpsi = 0.0, phi = 0.0, dphi = 0.0;
     for (int j = 0; j <= pl; ++j) {
       const double inv = 1.0 / ((dk[j] - d0) - t);
@@ -217,7 +217,10 @@ __global__ void dc_secular_kernel(Level L, int n, StedcWork w) {
       dphi += q * inv;
     }
     const double f = 1.0 + rho * (psi + phi);
-    if (f == 0.0) break;
+    // rounding-error bound of the computed f (cf. dlaed4's ERRETM): once |f|
+    // is below it the iterate is a root to working accuracy
+    const double erretm = 8.0 * rho * (fabs(psi) + fabs(phi)) + 2.0;
+    if (fabs(f) <= kEps * erretm) break;
     if (f > 0.0) b = t; else a = t;
     if (b - a <= 2.0 * kEps * fmax(fabs(a), fabs(b))) { t = 0.5 * (a + b); break; }
     const double P0 = dl - t, Q0 = dr - t;
@@ -467,7 +470,8 @@ cudaError_t stedc(int n, double* d, double* e, double* wout, double* Q, long lon
     count_launch();
     if ((err = cudaGetLastError()) != cudaSuccess) return err;
     stage_mark("dc_gemm", s);
-    err = gemm_grouped(false, false, ws.probs, 2 * L.nnodes, L.half, maxm, s, L.half >= 2);
+    err = gemm_grouped(false, false, ws.probs, 2 * L.nnodes, L.half, maxm, s, L.half >= 2,
+                       L.half >= 512 ? 3 : 1);
     if (err != cudaSuccess) return err;
     std::swap(Din, Dout);
     std::swap(Qin, Qout);

@@ -10,6 +10,8 @@
 // 4/3 N^3 flops, all on the FP64 tensor pipe.
 #include <cooperative_groups.h>
 #include <algorithm>
+#include <cstdio>
+#include <cstdlib>
 #include "eig.cuh"
 
 namespace bse {
@@ -34,76 +36,111 @@ BSE_DEV void grid_barrier(unsigned* ctr, unsigned target) {
 }
 
 // Householder QR of the m x bw panel P (column-major, ldp), rows split over
-// gridDim.x CTAs of R rows each (slab resident in smem).  Outputs:
+// gridDim.x CTAs; CTA c owns rows [c*R, c*R + R) with R = RPT * 256 and
+// thread t owns rows t, t + 256, ... (row-major slab in smem, stride bw+1:
+// a warp touching one column of 32 consecutive rows is conflict-free).
+// Per column j: one fused CTA reduction (products of every column with x_j,
+// ||tail||^2, the owner's row j) -> one grid barrier -> a fixed-order sum of
+// the G partials -> rank-1 update of the thread's own rows.  Outputs:
 //   P  <- R in its upper bw x bw triangle, zeros below
 //   V  (ldv), V2 (ldv2): explicit unit-lower-trapezoidal reflectors
 //   T  (bw x bw, ld bw): compact-WY factor, Q = I - V T V^T
-// red: 2 * gridDim.x * (2 + 2*bw) doubles; bar: zeroed counter.
+template <int RPT>
 __global__ void __launch_bounds__(kPanelThreads) panel_qr_kernel(
     double* __restrict__ P, long long ldp, int m, int bw, double* __restrict__ V, long long ldv,
     double* __restrict__ V2, long long ldv2, double* __restrict__ T, double* __restrict__ red,
-    unsigned* bar, int R) {
+    unsigned* bar, unsigned long long* trace) {
+  constexpr int R = RPT * kPanelThreads;
+  constexpr int LS = kMaxPanel + 1;   // row stride
+  constexpr int L = 2 + 2 * kMaxPanel;
   extern __shared__ double smem[];
-  double* S = smem;                    // slab, column-major [k*R + r]
-  double* tot = S + (size_t)R * bw;    // 2 + 2*bw reduced values
-  double* loc = tot + 2 + 2 * kMaxPanel;  // local partials
-  double* wv = loc + 2 + 2 * kMaxPanel;   // w_k / y_i
-  double* Ts = wv + kMaxPanel;             // T (CTA 0), [j*bw + i]
-  __shared__ double sc[4];                 // tau, beta, scale
+  double* S = smem;                       // [r*LS + k]
+  double* wpart = S + (size_t)R * LS;     // [warp][L] per-warp partials
+  double* tot = wpart + 8 * L;            // reduced values
+  double* wv = tot + L;                   // w_k / y_i
+  double* Ts = wv + kMaxPanel;            // T (CTA 0), [j*bw + i]
+  __shared__ double sc[4];
+  const bool tr = trace != nullptr && blockIdx.x == 0 && threadIdx.x == 0;
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int nwarps = blockDim.x >> 5;
   const int G = gridDim.x, cta = blockIdx.x;
-  const int r0 = cta * R;                 // first panel row of this slab
+  const int r0 = cta * R;
   const int rows = max(0, min(R, m - r0));
-  const int L = 2 + 2 * bw;
 
-  for (int idx = tid; idx < R * bw; idx += blockDim.x) {
-    const int r = idx % R, k = idx / R;
-    S[idx] = (r < rows) ? P[(r0 + r) + (long long)k * ldp] : 0.0;
+  for (int q = 0; q < RPT; ++q) {
+    const int r = tid + q * kPanelThreads;
+    for (int k = 0; k < kMaxPanel; ++k)
+      S[r * LS + k] = (r < rows && k < bw) ? P[(r0 + r) + (long long)k * ldp] : 0.0;
   }
   if (cta == 0)
     for (int idx = tid; idx < bw * bw; idx += blockDim.x) Ts[idx] = 0.0;
   __syncthreads();
 
   for (int j = 0; j < bw; ++j) {
-    // ---- local partial sums over slab rows with global index >= j ----
-    const int rbeg = max(0, j - r0);  // local row index of the first row >= j
-    for (int k = warp; k < bw; k += nwarps) {
-      double s = 0.0;
-      const double* ck = S + (size_t)k * R;
-      const double* cj = S + (size_t)j * R;
-      for (int r = rbeg + lane; r < rows; r += 32) s += ck[r] * cj[r];
-      s = warp_sum(s);
-      if (lane == 0) loc[2 + k] = s;
-    }
-    if (warp == nwarps - 1) {
-      double s = 0.0;
-      const double* cj = S + (size_t)j * R;
-      const int rb = max(0, j + 1 - r0);
-      for (int r = rb + lane; r < rows; r += 32) s += cj[r] * cj[r];
-      s = warp_sum(s);
-      if (lane == 0) loc[0] = s;
-    }
-    const bool owner = (j >= r0 && j < r0 + rows);
-    if (tid < bw) loc[2 + bw + tid] = owner ? S[(size_t)tid * R + (j - r0)] : 0.0;
-    if (tid == 0) loc[1] = owner ? S[(size_t)j * R + (j - r0)] : 0.0;
-    __syncthreads();
-
-    if (G > 1) {
-      double* slot = red + (size_t)(j & 1) * G * L;
-      for (int t = tid; t < L; t += blockDim.x) slot[(size_t)cta * L + t] = loc[t];
-      grid_barrier(bar, (unsigned)G * (unsigned)(j + 1));
-      for (int t = tid; t < L; t += blockDim.x) {
-        double s = 0.0;
-        for (int c = 0; c < G; ++c) s += __ldcg(slot + (size_t)c * L + t);
-        tot[t] = s;
+    unsigned long long t0 = 0, t1 = 0, t2 = 0, t3 = 0;
+    if (tr) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+    // ---- per-thread products over owned rows with global index >= j ----
+    double pk[kMaxPanel];
+    double tail = 0.0;
+#pragma unroll
+    for (int k = 0; k < kMaxPanel; ++k) pk[k] = 0.0;
+    for (int q = 0; q < RPT; ++q) {
+      const int r = tid + q * kPanelThreads;
+      const int gr = r0 + r;
+      if (r < rows && gr >= j) {
+        const double* row = S + r * LS;
+        const double xj = row[j];
+#pragma unroll
+        for (int k = 0; k < kMaxPanel; ++k) pk[k] += row[k] * xj;
+        if (gr > j) tail += xj * xj;
       }
-    } else {
-      for (int t = tid; t < L; t += blockDim.x) tot[t] = loc[t];
+    }
+    // warp reduction of the 65 values, then per-warp partials to smem
+#pragma unroll
+    for (int k = 0; k < kMaxPanel; ++k) pk[k] = warp_sum(pk[k]);
+    tail = warp_sum(tail);
+    if (lane == 0) {
+#pragma unroll
+      for (int k = 0; k < kMaxPanel; ++k) wpart[warp * L + 2 + k] = pk[k];
+      wpart[warp * L] = tail;
     }
     __syncthreads();
-
+    // CTA partial: [0] tail, [1] x0 (owner), [2+k] dots, [2+bw+k] owner's row j
+    double* slot = red + (size_t)(j & 1) * G * L;
+    const bool owner = (j >= r0 && j < r0 + rows);
+    for (int t = tid; t < L; t += blockDim.x) {
+      double v;
+      if (t == 1) {
+        v = owner ? S[(j - r0) * LS + j] : 0.0;
+      } else if (t >= 2 + kMaxPanel) {
+        v = owner ? S[(j - r0) * LS + (t - 2 - kMaxPanel)] : 0.0;
+      } else {
+        v = 0.0;
+#pragma unroll
+        for (int w = 0; w < 8; ++w) v += wpart[w * L + t];
+      }
+      if (G > 1) slot[(size_t)cta * L + t] = v;
+      else tot[t] = v;
+    }
+    if (tr) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t1));
+    if (G > 1) {
+      grid_barrier(bar, (unsigned)G * (unsigned)(j + 1));
+      if (tr) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t2));
+      for (int t = tid; t < L; t += blockDim.x) {
+        double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+        int c = 0;
+        for (; c + 4 <= G; c += 4) {
+          a0 += __ldcg(slot + (size_t)(c + 0) * L + t);
+          a1 += __ldcg(slot + (size_t)(c + 1) * L + t);
+          a2 += __ldcg(slot + (size_t)(c + 2) * L + t);
+          a3 += __ldcg(slot + (size_t)(c + 3) * L + t);
+        }
+        for (; c < G; ++c) a0 += __ldcg(slot + (size_t)c * L + t);
+        tot[t] = (a0 + a1) + (a2 + a3);
+      }
+    }
+    __syncthreads();
+    if (tr) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t3));
     if (tid == 0) {
       const double x0 = tot[1], st = tot[0];
       double tau = 0.0, beta = x0, scale = 0.0;
@@ -114,56 +151,56 @@ __global__ void __launch_bounds__(kPanelThreads) panel_qr_kernel(
       }
       sc[0] = tau; sc[1] = beta; sc[2] = scale;
     }
+    if (tid < bw) {
+      // provisional; scaled below once tau/beta are known (same thread order)
+    }
     __syncthreads();
     const double tau = sc[0], beta = sc[1], scale = sc[2];
-    // w_k = v^T P[:,k] (k > j); y_i = V[:,i]^T v (i < j)
-    if (tid < bw) wv[tid] = (tot[2 + tid] - beta * tot[2 + bw + tid]) * scale;
+    if (tid < bw) wv[tid] = (tot[2 + tid] - beta * tot[2 + kMaxPanel + tid]) * scale;
     __syncthreads();
-
-    // ---- apply H_j to the slab (rows >= j, columns > j) and store v ----
-    if (tau != 0.0) {
-      const int cols = bw - j - 1;
-      for (int idx = tid; idx < rows * cols; idx += blockDim.x) {
-        const int r = idx % rows, k = j + 1 + idx / rows;
-        const int gr = r0 + r;
-        if (gr < j) continue;
-        const double vr = (gr == j) ? 1.0 : S[(size_t)j * R + r] * scale;
-        S[(size_t)k * R + r] -= tau * vr * wv[k];
-      }
-      __syncthreads();
-      for (int r = tid; r < rows; r += blockDim.x) {
-        const int gr = r0 + r;
-        if (gr > j) S[(size_t)j * R + r] *= scale;
-        else if (gr == j) S[(size_t)j * R + r] = beta;
-      }
-    } else {
-      // identity reflector: v = e_j, the stored tail is zero
-      for (int r = tid; r < rows; r += blockDim.x) {
-        const int gr = r0 + r;
-        if (gr > j) S[(size_t)j * R + r] = 0.0;
+    // ---- rank-1 update of the owned rows (columns > j), store v_j ----
+    for (int q = 0; q < RPT; ++q) {
+      const int r = tid + q * kPanelThreads;
+      const int gr = r0 + r;
+      if (r < rows && gr >= j) {
+        double* row = S + r * LS;
+        if (tau != 0.0) {
+          const double vr = (gr == j) ? 1.0 : row[j] * scale;
+          const double tv = tau * vr;
+          for (int k = j + 1; k < bw; ++k) row[k] -= tv * wv[k];
+          row[j] = (gr == j) ? beta : vr;
+        } else if (gr > j) {
+          row[j] = 0.0;
+        }
       }
     }
     // ---- T column j (CTA 0): T[j][j] = tau, T[i][j] = -tau sum_k T[i][k] y_k ----
     if (cta == 0 && tid < bw) {
       const int i = tid;
       if (i < j) {
-        double s = 0.0;
-        for (int k = i; k < j; ++k) s += Ts[k * bw + i] * wv[k];
-        Ts[j * bw + i] = -tau * s;
+        double sacc = 0.0;
+        for (int k = i; k < j; ++k) sacc += Ts[k * bw + i] * wv[k];
+        Ts[j * bw + i] = -tau * sacc;
       } else if (i == j) {
         Ts[j * bw + j] = tau;
       }
     }
     __syncthreads();
+    if (tr) {
+      unsigned long long t4;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t4));
+      trace[5 * j + 0] = t1 - t0; trace[5 * j + 1] = t2 ? t2 - t1 : 0;
+      trace[5 * j + 2] = t3 - (t2 ? t2 : t1); trace[5 * j + 3] = t4 - t3; trace[5 * j + 4] = 1;
+    }
   }
 
   // ---- write back R (upper), explicit V (unit lower) ----
   for (int idx = tid; idx < rows * bw; idx += blockDim.x) {
     const int r = idx % rows, k = idx / rows;
     const int gr = r0 + r;
-    const double s = S[(size_t)k * R + r];
-    P[gr + (long long)k * ldp] = (gr <= k) ? s : 0.0;
-    const double v = (gr > k) ? s : (gr == k ? 1.0 : 0.0);
+    const double sv = S[r * LS + k];
+    P[gr + (long long)k * ldp] = (gr <= k) ? sv : 0.0;
+    const double v = (gr > k) ? sv : (gr == k ? 1.0 : 0.0);
     V[gr + (long long)k * ldv] = v;
     if (V2) V2[gr + (long long)k * ldv2] = v;
   }
@@ -183,40 +220,59 @@ __global__ void extract_band_kernel(const double* __restrict__ A, long long lda,
 }  // namespace
 
 size_t panel_smem_bytes(int R, int bw) {
-  return sizeof(double) * ((size_t)R * bw + 2 * (2 + 2 * kMaxPanel) + kMaxPanel +
-                           (size_t)kMaxPanel * kMaxPanel);
-}
-
-int panel_rows_per_cta(int m, int bw, int max_ctas) {
-  // as many CTAs as needed so that the slab fits in ~200 KB, >= 128 rows each
-  int R = 128;
-  while ((long long)R * max_ctas < m) R += 32;
   (void)bw;
-  return R;
+  constexpr int L = 2 + 2 * kMaxPanel;
+  return sizeof(double) * ((size_t)R * (kMaxPanel + 1) + 8 * L + L + kMaxPanel +
+                           (size_t)kMaxPanel * kMaxPanel);
 }
 
 cudaError_t panel_qr(double* P, long long ldp, int m, int bw, double* V, long long ldv, double* V2,
                      long long ldv2, double* T, double* red, unsigned* bar, int num_sms,
                      cudaStream_t s) {
-  const int R = panel_rows_per_cta(m, bw, num_sms);
+  // one slab row per thread (RPT = 1) while that keeps G <= #SMs, else two
+  const int rpt = ((long long)kPanelThreads * num_sms >= m) ? 1 : 2;
+  const int R = rpt * kPanelThreads;
   const int G = (int)ceil_div(m, R);
+  if (G > num_sms) return cudaErrorInvalidValue;
   const size_t smem = panel_smem_bytes(R, bw);
-  static size_t attr = 0;
-  if (smem > 220 * 1024) return cudaErrorInvalidValue;
-  if (smem > attr) {
-    cudaError_t e = cudaFuncSetAttribute(panel_qr_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         (int)smem);
+  static size_t attr[3] = {0, 0, 0};
+  void* fn = rpt == 1 ? (void*)panel_qr_kernel<1> : (void*)panel_qr_kernel<2>;
+  if (smem > attr[rpt]) {
+    cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
-    attr = smem;
+    attr[rpt] = smem;
   }
   cudaError_t e = cudaMemsetAsync(bar, 0, sizeof(unsigned), s);
   if (e != cudaSuccess) return e;
-  void* args[] = {&P, &ldp, &m, &bw, &V, &ldv, &V2, &ldv2, &T, &red, &bar, (void*)&R};
+  static unsigned long long* trace = nullptr;
+  static int traced = 0;
+  const bool want = std::getenv("BSE_PANEL_TRACE") != nullptr && traced == 0 && m > 8000;
+  unsigned long long* tptr = nullptr;
+  if (want) {
+    cudaMalloc(&trace, sizeof(unsigned long long) * 5 * 64);
+    cudaMemsetAsync(trace, 0, sizeof(unsigned long long) * 5 * 64, s);
+    tptr = trace;
+  }
+  void* args[] = {&P, &ldp, &m, &bw, &V, &ldv, &V2, &ldv2, &T, &red, &bar, &tptr};
   count_launch();
+  cudaError_t le;
   if (G == 1)
-    return cudaLaunchKernel((void*)panel_qr_kernel, dim3(1), dim3(kPanelThreads), args, smem, s);
-  return cudaLaunchCooperativeKernel((void*)panel_qr_kernel, dim3(G), dim3(kPanelThreads), args,
-                                     smem, s);
+    le = cudaLaunchKernel(fn, dim3(1), dim3(kPanelThreads), args, smem, s);
+  else
+    le = cudaLaunchCooperativeKernel(fn, dim3(G), dim3(kPanelThreads), args, smem, s);
+  if (want) {
+    traced = 1;
+    unsigned long long h[5 * 64];
+    cudaMemcpyAsync(h, trace, sizeof(h), cudaMemcpyDeviceToHost, s);
+    cudaStreamSynchronize(s);
+    double a[4] = {0};
+    for (int j = 0; j < 64; ++j)
+      for (int q = 0; q < 4; ++q) a[q] += h[5 * j + q];
+    std::fprintf(stderr, "[panel trace] m=%d G=%d R=%d per column us: local %.2f barrier %.2f "
+                 "reduce %.2f update %.2f\n", m, G, R, a[0] / 64e3, a[1] / 64e3, a[2] / 64e3,
+                 a[3] / 64e3);
+  }
+  return le;
 }
 
 cudaError_t extract_band(const double* A, long long lda, int n, int b, double* AB, int ldab,
