@@ -24,8 +24,15 @@ struct SbSmem {
   double v[kMaxPanel];        // current reflector
   double vn[kMaxPanel];       // new reflector
   double w[kMaxPanel];
+  double part[4 * kMaxPanel];
   double sc[4];
 };
+
+BSE_DEV unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
 
 // Householder of x[0..len) (one warp, LAPACK dlarfg conventions): v (v[0]=1),
 // sc[0] = tau, sc[1] = beta.
@@ -71,22 +78,60 @@ BSE_DEV void signal_progress(int* progress, int s, int val) {
   }
 }
 
-// Two-sided D <- H D H (H = I - tau v v^T) on the len x len symmetric block in
-// smem; the lower triangle of the result is stored straight to the band.
+// Stage the len x len symmetric block at (q0, q0) (lower triangle in the band)
+// and, optionally, the lq x lp off-diagonal block at (q0, p0) into smem with
+// cp.async: every load of the step is in flight at once (one L2 round trip).
+BSE_DEV void stage_blocks(SbSmem& sm, const double* AB, int ldab, int q0, int len, bool with_o,
+                          int p0, int lp) {
+  const int tid = threadIdx.x;
+#pragma unroll 4
+  for (int k = 0; k < kSlots; ++k) {
+    const int idx = tid + k * kSbThreads;
+    const int r = idx & (kMaxPanel - 1), c = idx >> 6;
+    const bool dv = r < len && c <= r;
+    const double* ds = dv ? AB + (long long)(q0 + c) * ldab + (r - c) : AB;
+    cp_async8(&sm.D[c * kLd + r], ds, dv);
+    if (with_o) {
+      const bool ov = r < len && c < lp;
+      const double* os = ov ? AB + (long long)(p0 + c) * ldab + (q0 + r - p0 - c) : AB;
+      cp_async8(&sm.O[c * kLd + r], os, ov);
+    }
+  }
+  cp_async_commit();
+  cp_async_wait<0>();
+  __syncthreads();
+  // mirror the lower triangle of D into the upper one
+#pragma unroll 4
+  for (int k = 0; k < kSlots; ++k) {
+    const int idx = tid + k * kSbThreads;
+    const int r = idx & (kMaxPanel - 1), c = idx >> 6;
+    if (c > r) sm.D[c * kLd + r] = sm.D[r * kLd + c];
+  }
+  __syncthreads();
+}
+
+// Column-sum matvec out_c = scale * sum_r X[c][r] x[r] (X column-major in smem,
+// 8 columns per warp, lanes over rows: conflict-free, shuffle-reduced).
+BSE_DEV void colsum(const double* X, const double* x, int nrows, double scale, double* out) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+  for (int u = 0; u < kMaxPanel / 8; ++u) {
+    const int c = warp + 8 * u;
+    double a = 0.0;
+    if (lane < nrows) a = X[c * kLd + lane] * x[lane];
+    if (lane + 32 < nrows) a += X[c * kLd + lane + 32] * x[lane + 32];
+    a = warp_sum(a);
+    if (lane == 0) out[c] = scale * a;
+  }
+}
+
+// Two-sided D <- H D H (H = I - tau v v^T) on the staged symmetric block; the
+// lower triangle of the result is stored straight to the band.
 BSE_DEV void two_sided_store(SbSmem& sm, int len, const double* v, double tau, double* AB,
                              int ldab, int q0) {
   const int tid = threadIdx.x;
   const int lane = tid & 31;
-  // p = tau D v : 4 threads per row
-  {
-    const int r = tid >> 2, q = tid & 3;
-    double acc = 0.0;
-    if (r < len)
-      for (int c = q; c < len; c += 4) acc += sm.D[c * kLd + r] * v[c];
-    acc += __shfl_xor_sync(0xffffffffu, acc, 1);
-    acc += __shfl_xor_sync(0xffffffffu, acc, 2);
-    if (q == 0 && r < kMaxPanel) sm.w[r] = (r < len) ? tau * acc : 0.0;
-  }
+  colsum(sm.D, v, len, tau, sm.w);  // D symmetric: column sums == row sums
   __syncthreads();
   if (tid < 32) {
     double a = 0.0;
@@ -108,50 +153,28 @@ BSE_DEV void two_sided_store(SbSmem& sm, int len, const double* v, double tau, d
   }
 }
 
-BSE_DEV unsigned long long gtimer() {
-  unsigned long long t;
-  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
-  return t;
-}
-
 __global__ void __launch_bounds__(kSbThreads) sb2st_kernel(double* AB, int ldab, int n, int b,
                                                            double* V2, double* tau2,
                                                            int maxsteps, int* progress,
                                                            unsigned long long* trace) {
-  // optional trace (BSE_SB2ST_TRACE): CTA 1 records, for its first two sweeps,
-  // per step [wait begin, wait end, step end] in ns
-  const bool tr = trace != nullptr && blockIdx.x == 1 && threadIdx.x == 0;
-  int tcount = 0;
   extern __shared__ __align__(16) unsigned char raw[];
   SbSmem& sm = *reinterpret_cast<SbSmem*>(raw);
   const int tid = threadIdx.x;
+  const int lane = tid & 31, warp = tid >> 5;
+  const bool tr = trace != nullptr && blockIdx.x == 1 && threadIdx.x == 0;
+  int tcount = 0;
   auto bidx = [&](int i, int j) -> long long { return (long long)j * ldab + (i - j); };
 
   for (int s = blockIdx.x; s < n - 2; s += gridDim.x) {
-    // ---------------- step 0: annihilate column s ----------------
     const bool trs = tr && s < 1 + 2 * (int)gridDim.x;
+    // ---------------- step 0: annihilate column s ----------------
     if (trs) trace[8 * tcount] = gtimer();
     wait_progress(progress, s, 2);
     if (trs) trace[8 * tcount + 1] = gtimer();
     int p0 = s + 1, p1 = min(s + b, n - 1);
     int lp = p1 - p0 + 1;
-    {
-      double dreg[kSlots];
-#pragma unroll
-      for (int k = 0; k < kSlots; ++k) {
-        const int idx = tid + k * kSbThreads;
-        const int r = idx & (kMaxPanel - 1), c = idx >> 6;
-        dreg[k] = (r < lp && c <= r) ? __ldcg(AB + bidx(p0 + r, p0 + c)) : 0.0;
-      }
-      if (tid < kMaxPanel) sm.w[tid] = tid < lp ? __ldcg(AB + bidx(p0 + tid, s)) : 0.0;
-#pragma unroll
-      for (int k = 0; k < kSlots; ++k) {
-        const int idx = tid + k * kSbThreads;
-        const int r = idx & (kMaxPanel - 1), c = idx >> 6;
-        if (c <= r) { sm.D[c * kLd + r] = dreg[k]; sm.D[r * kLd + c] = dreg[k]; }
-      }
-    }
-    __syncthreads();
+    if (tid < kMaxPanel) sm.w[tid] = tid < lp ? __ldcg(AB + bidx(p0 + tid, s)) : 0.0;
+    stage_blocks(sm, AB, ldab, p0, lp, false, 0, 0);
     if (tid < 32) warp_house(sm.w, lp, sm.v, sm.sc);
     __syncthreads();
     double tau = sm.sc[0];
@@ -171,33 +194,21 @@ __global__ void __launch_bounds__(kSbThreads) sb2st_kernel(double* AB, int ldab,
       if (trs) trace[8 * tcount] = gtimer();
       wait_progress(progress, s, j + 2);
       if (trs) trace[8 * tcount + 1] = gtimer();
-      {
-        double oreg[kSlots], dreg[kSlots];
-#pragma unroll
-        for (int k = 0; k < kSlots; ++k) {
-          const int idx = tid + k * kSbThreads;
-          const int r = idx & (kMaxPanel - 1), c = idx >> 6;
-          oreg[k] = (r < lq && c < lp) ? __ldcg(AB + bidx(q0 + r, p0 + c)) : 0.0;
-          dreg[k] = (r < lq && c <= r) ? __ldcg(AB + bidx(q0 + r, q0 + c)) : 0.0;
-        }
-#pragma unroll
-        for (int k = 0; k < kSlots; ++k) {
-          const int idx = tid + k * kSbThreads;
-          const int r = idx & (kMaxPanel - 1), c = idx >> 6;
-          sm.O[c * kLd + r] = oreg[k];
-          if (c <= r) { sm.D[c * kLd + r] = dreg[k]; sm.D[r * kLd + c] = dreg[k]; }
-        }
-      }
-      __syncthreads();
+      stage_blocks(sm, AB, ldab, q0, lq, true, p0, lp);
       if (trs) trace[8 * tcount + 2] = gtimer();
       if (tau != 0.0) {
-        // right-apply: w = tau O v (4 threads per row), O -= w v^T
-        const int r = tid >> 2, q = tid & 3;
-        double acc = 0.0;
-        for (int c = q; c < lp; c += 4) acc += sm.O[c * kLd + r] * sm.v[c];
-        acc += __shfl_xor_sync(0xffffffffu, acc, 1);
-        acc += __shfl_xor_sync(0xffffffffu, acc, 2);
-        if (q == 0) sm.w[r] = tau * acc;
+        // right-apply: w = tau O v (row sums: 4 partial sums per row, lanes
+        // over consecutive rows -> conflict-free), O -= w v^T
+        {
+          const int r = tid & (kMaxPanel - 1), q = tid >> 6;
+          double a = 0.0;
+          for (int c = q; c < lp; c += 4) a += sm.O[c * kLd + r] * sm.v[c];
+          sm.part[q * kMaxPanel + r] = a;
+        }
+        __syncthreads();
+        if (tid < kMaxPanel)
+          sm.w[tid] = tau * ((sm.part[tid] + sm.part[kMaxPanel + tid]) +
+                             (sm.part[2 * kMaxPanel + tid] + sm.part[3 * kMaxPanel + tid]));
         __syncthreads();
 #pragma unroll
         for (int k = 0; k < kSlots; ++k) {
@@ -212,14 +223,9 @@ __global__ void __launch_bounds__(kSbThreads) sb2st_kernel(double* AB, int ldab,
       __syncthreads();
       if (trs) trace[8 * tcount + 4] = gtimer();
       const double taun = sm.sc[0], betan = sm.sc[1];
+      // left-apply to columns >= 1: y_c = taun * vn^T O[:, c] (column sums)
       if (taun != 0.0) {
-        // left-apply to columns >= 1: y_c = taun * vn^T O[:, c] (4 threads per column)
-        const int c = tid >> 2, q = tid & 3;
-        double acc = 0.0;
-        for (int r = q; r < lq; r += 4) acc += sm.vn[r] * sm.O[c * kLd + r];
-        acc += __shfl_xor_sync(0xffffffffu, acc, 1);
-        acc += __shfl_xor_sync(0xffffffffu, acc, 2);
-        if (q == 0) sm.w[c] = taun * acc;
+        colsum(sm.O, sm.vn, lq, taun, sm.w);
         __syncthreads();
       }
       // store O (column 0 = (beta, 0, ...)), reflector, then the two-sided D update
@@ -240,7 +246,6 @@ __global__ void __launch_bounds__(kSbThreads) sb2st_kernel(double* AB, int ldab,
       if (trs) trace[8 * tcount + 5] = gtimer();
       if (taun != 0.0) two_sided_store(sm, lq, sm.vn, taun, AB, ldab, q0);
       if (trs) trace[8 * tcount + 6] = gtimer();
-      // the new reflector becomes the current one
       __syncthreads();
       if (tid < kMaxPanel) sm.v[tid] = sm.vn[tid];
       tau = taun;
@@ -253,6 +258,8 @@ __global__ void __launch_bounds__(kSbThreads) sb2st_kernel(double* AB, int ldab,
     signal_progress(progress, s, kDone);
     __syncthreads();
   }
+  (void)lane;
+  (void)warp;
 }
 
 __global__ void band_to_tridiag_kernel(const double* AB, int ldab, int n, double* d, double* e) {
@@ -285,7 +292,7 @@ cudaError_t sb2st(double* AB, int ldab, int n, int b, double* d, double* e, doub
     int flags = 0;
     if (const char* v = std::getenv("BSE_SB2ST_VARIANT")) flags = std::atoi(v);
     cudaMemcpyToSymbolAsync(c_sb_flags, &flags, sizeof(int), 0, cudaMemcpyHostToDevice, s);
-    if (flags & 4) per_sm = 1;
+    if (!(flags & 8)) per_sm = 1;  // default 1 CTA/SM (flag 8 restores full occupancy)
     int grid = std::max(1, std::min(n - 2, std::max(1, per_sm) * num_sms));
     int maxsteps = sb2st_maxsteps(n, b);
     unsigned long long* trace = nullptr;
