@@ -148,8 +148,10 @@ __global__ void __launch_bounds__(kQ2Threads, 2) q2_apply_kernel(int n, int b, i
         double acc[MI][2][2];
 #pragma unroll
         for (int i = 0; i < MI; ++i) acc[i][0][0] = acc[i][0][1] = acc[i][1][0] = acc[i][1][1] = 0.0;
+        // reflector c of the block is nonzero on rows [c, c + b) only
+        const int kbeg = wm * WM, kend = min(HB, wm * WM + WM + b);
 #pragma unroll 4
-        for (int k = 0; k < HB; k += 4) {
+        for (int k = kbeg; k < kend; k += 4) {
           double af[MI], bf[2];
 #pragma unroll
           for (int i = 0; i < MI; ++i) af[i] = sV[(wm * WM + i * 8 + rl) * LDV + k + kl];

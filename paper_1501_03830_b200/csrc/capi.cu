@@ -121,8 +121,24 @@ int bse_solve_spd_pair_host(int64_t n, const double* M, int64_t ldm, const doubl
   if (n < 0 || ldm < n || ldk < n || ldx1 < n || ldx2 < n)
     return fail(BSE_BAD_ARGUMENT, "bad dimension");
   if (n == 0) return BSE_OK;
-  cudaStream_t s;
+  // keep freed workspace in the stream-ordered pool between calls (the
+  // default release threshold of 0 would unmap ~14 n^2 doubles every call)
+  static bool pool_set[64] = {false};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (dev < 64 && !pool_set[dev]) {
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+      uint64_t thr = UINT64_MAX;
+      cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+    }
+    pool_set[dev] = true;
+  }
+  cudaStream_t s, s2;
   BSE_TRY_CUDA(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking), "stream");
+  BSE_TRY_CUDA(cudaStreamCreateWithFlags(&s2, cudaStreamNonBlocking), "stream");
+  cudaEvent_t evM;
+  cudaEventCreateWithFlags(&evM, cudaEventDisableTiming);
   const long long ld = bse::pad_ld(n);
   const size_t mat = sizeof(double) * (size_t)ld * n;
   const size_t wb = bse::solve_bytes((int)n, flags);
@@ -131,6 +147,8 @@ int bse_solve_spd_pair_host(int64_t n, const double* M, int64_t ldm, const doubl
   cudaError_t e = cudaMallocAsync((void**)&buf, 4 * mat + lam_bytes + wb, s);
   if (e != cudaSuccess) {
     cudaStreamDestroy(s);
+    cudaStreamDestroy(s2);
+    cudaEventDestroy(evM);
     return cuda_fail(e, "alloc");
   }
   double* dM = (double*)buf;
@@ -141,11 +159,19 @@ int bse_solve_spd_pair_host(int64_t n, const double* M, int64_t ldm, const doubl
   void* dW = buf + 4 * mat + lam_bytes;
   bse::SolveStatus st{};
   const size_t row = sizeof(double) * (size_t)n;
-  e = cudaMemcpy2DAsync(dM, ld * 8, M, ldm * 8, row, n, cudaMemcpyHostToDevice, s);
+  // K first (Cholesky starts as soon as it lands); M on a second stream,
+  // joined before the congruence
+  e = cudaMemcpy2DAsync(dK, ld * 8, K, ldk * 8, row, n, cudaMemcpyHostToDevice, s);
+  cudaEvent_t evAlloc;
+  cudaEventCreateWithFlags(&evAlloc, cudaEventDisableTiming);
+  cudaEventRecord(evAlloc, s);
+  cudaStreamWaitEvent(s2, evAlloc, 0);
   if (e == cudaSuccess)
-    e = cudaMemcpy2DAsync(dK, ld * 8, K, ldk * 8, row, n, cudaMemcpyHostToDevice, s);
+    e = cudaMemcpy2DAsync(dM, ld * 8, M, ldm * 8, row, n, cudaMemcpyHostToDevice, s2);
+  if (e == cudaSuccess) e = cudaEventRecord(evM, s2);
   if (e == cudaSuccess)
-    e = bse::solve_spd_pair((int)n, dM, ld, dK, ld, dLam, dX1, ld, dX2, ld, dW, wb, flags, s, &st);
+    e = bse::solve_spd_pair((int)n, dM, ld, dK, ld, dLam, dX1, ld, dX2, ld, dW, wb, flags, s, &st,
+                            evM);
   if (e == cudaSuccess) e = cudaMemcpyAsync(lam, dLam, row, cudaMemcpyDeviceToHost, s);
   if (e == cudaSuccess)
     e = cudaMemcpy2DAsync(X1, ldx1 * 8, dX1, ld * 8, row, n, cudaMemcpyDeviceToHost, s);
@@ -154,6 +180,9 @@ int bse_solve_spd_pair_host(int64_t n, const double* M, int64_t ldm, const doubl
   cudaFreeAsync(buf, s);
   cudaError_t e2 = cudaStreamSynchronize(s);
   cudaStreamDestroy(s);
+  cudaStreamDestroy(s2);
+  cudaEventDestroy(evM);
+  cudaEventDestroy(evAlloc);
   BSE_TRY_CUDA(e, "solve_host");
   BSE_TRY_CUDA(e2, "solve_host sync");
   return map_solve_status(st, info);

@@ -211,7 +211,7 @@ size_t solve_bytes(int n, int flags) {
 cudaError_t solve_spd_pair(int n, const double* M, long long ldm, const double* K, long long ldk,
                            double* lam, double* X1, long long ldx1, double* X2, long long ldx2,
                            void* work, size_t work_bytes, int flags, cudaStream_t s,
-                           SolveStatus* out) {
+                           SolveStatus* out, cudaEvent_t m_ready) {
   out->code = 0;
   out->pivot_index = -1;
   out->pivot_value = 0.0;
@@ -231,6 +231,7 @@ cudaError_t solve_spd_pair(int n, const double* M, long long ldm, const double* 
   copy_lower_kernel<<<nb, 256, 0, s>>>(n, K, ldk, w.L, ld);
   count_launch();
   if ((e = potrf_lower(w.L, ld, n, &w.st[0], s)) != cudaSuccess) return e;
+  if (m_ready && (e = cudaStreamWaitEvent(s, m_ready, 0)) != cudaSuccess) return e;
   stage_mark("congruence", s);
   // 2. W = L^T M L  (T1 = M L from the lower triangle of M, then W = L^T T1, lower)
   GemmProblem g1 = make_gemm(n, n, n, 1.0, M, ldm, w.L, ld, 0.0, w.T1, ld);
