@@ -72,7 +72,10 @@ int bse_potrf_dev(int64_t n, double* dA, int64_t lda, void* stream, bse_info* in
   BSE_TRY_CUDA(cudaMallocAsync((void**)&st, sizeof(bse::DevStatus), s), "alloc status");
   bse::DevStatus h0{-1, 0, 0.0, 0.0};
   BSE_TRY_CUDA(cudaMemcpyAsync(st, &h0, sizeof(h0), cudaMemcpyHostToDevice, s), "status init");
-  cudaError_t e = bse::potrf_lower(dA, lda, (int)n, st, s);
+  double* inv = nullptr;
+  cudaError_t e = cudaMallocAsync((void**)&inv, sizeof(double) * bse::potrf_inv_cache_doubles((int)n), s);
+  if (e == cudaSuccess) e = bse::potrf_lower(dA, lda, (int)n, st, s, inv);
+  if (inv) cudaFreeAsync(inv, s);
   bse::DevStatus h;
   if (e == cudaSuccess) e = cudaMemcpyAsync(&h, st, sizeof(h), cudaMemcpyDeviceToHost, s);
   if (e == cudaSuccess) e = cudaStreamSynchronize(s);

@@ -12,8 +12,10 @@ constexpr int kLds = kLeaf + 1;
 
 // --- POTF2: in-place lower Cholesky of an n x n (n <= 64) diagonal block ---
 __global__ void __launch_bounds__(256) potf2_kernel(double* A, long long lda, int n, int off,
-                                                    DevStatus* st) {
-  __shared__ double T[kLeaf * kLds];  // column-major, T[c*kLds + r]
+                                                    DevStatus* st, double* inv) {
+  extern __shared__ double dyn[];
+  double* T = dyn;                    // column-major, T[c*kLds + r]
+  double* Y = dyn + kLeaf * kLds;     // inverse, column-major
   if (st->info >= 0) return;          // an earlier block already failed
   const int tid = threadIdx.x;
   for (int idx = tid; idx < n * n; idx += blockDim.x) {
@@ -43,6 +45,24 @@ __global__ void __launch_bounds__(256) potf2_kernel(double* A, long long lda, in
   for (int idx = tid; idx < n * n; idx += blockDim.x) {
     const int r = idx % n, c = idx / n;
     A[r + c * lda] = (r >= c) ? T[c * kLds + r] : 0.0;
+  }
+  if (inv) {
+    // L^{-1} by column-parallel forward substitution (thread j owns column j;
+    // T reads are warp-broadcasts, Y reads/writes stride kLds: conflict-free)
+    const int j = tid;
+    if (j < n) {
+      for (int i = 0; i < n; ++i) {
+        double sacc = (i == j) ? 1.0 : 0.0;
+        if (i > j)
+          for (int k = j; k < i; ++k) sacc -= T[k * kLds + i] * Y[j * kLds + k];
+        Y[j * kLds + i] = (i < j) ? 0.0 : sacc / T[i * kLds + i];
+      }
+    }
+    __syncthreads();
+    for (int idx = tid; idx < kLeaf * kLeaf; idx += blockDim.x) {
+      const int r = idx % kLeaf, c = idx / kLeaf;
+      inv[r + c * kLeaf] = (r < n && c < n) ? Y[c * kLds + r] : 0.0;
+    }
   }
 }
 
@@ -202,48 +222,60 @@ int split_point(int n) {
 
 }  // namespace
 
+size_t potrf_inv_cache_doubles(int n) { return (size_t)ceil_div(n, kLeaf) * kLeaf * kLeaf; }
+
 cudaError_t trsm_rlt(const double* L, long long ldl, int n, double* A, long long lda, int m,
-                     cudaStream_t s) {
+                     cudaStream_t s, const double* inv) {
   if (n <= 0 || m <= 0) return cudaSuccess;
   if (n <= kLeaf) {
-    // A <- A * (L^{-1})^T : invert the block, then one in-place DMMA GEMM
-    // (N = K = n <= BN, so every CTA reads its full row slab before writing).
-    double* Y = leaf_scratch();
-    trtri_leaf<<<1, kLeaf, 0, s>>>(L, ldl, n, Y);
-    count_launch();
+    // A <- A * (L^{-1})^T : (cached) inverse of the block, then one in-place
+    // DMMA GEMM (N = K = n <= BN: every CTA reads its full row slab first).
+    const double* Y = inv;
+    if (!Y) {
+      double* Yw = leaf_scratch();
+      trtri_leaf<<<1, kLeaf, 0, s>>>(L, ldl, n, Yw);
+      count_launch();
+      Y = Yw;
+    }
     GemmProblem p = make_gemm(m, n, n, 1.0, A, lda, Y, kLeaf, 0.0, A, lda);
     p.mb = Mask::lower();
     return gemm(false, true, p, s);
   }
   const int n1 = split_point(n), n2 = n - n1;
-  cudaError_t e = trsm_rlt(L, ldl, n1, A, lda, m, s);
+  cudaError_t e = trsm_rlt(L, ldl, n1, A, lda, m, s, inv);
   if (e != cudaSuccess) return e;
   // A2 -= X1 * L21^T
   GemmProblem p = make_gemm(m, n2, n1, -1.0, A, lda, L + n1, ldl, 1.0, A + n1 * lda, lda);
   e = gemm(false, true, p, s);
   if (e != cudaSuccess) return e;
-  return trsm_rlt(L + n1 + n1 * ldl, ldl, n2, A + n1 * lda, lda, m, s);
+  return trsm_rlt(L + n1 + n1 * ldl, ldl, n2, A + n1 * lda, lda, m, s,
+                  inv ? inv + (size_t)(n1 / kLeaf) * kLeaf * kLeaf : nullptr);
 }
 
 cudaError_t trsm_llt(const double* L, long long ldl, int n, double* B, long long ldb, int ncols,
-                     cudaStream_t s) {
+                     cudaStream_t s, const double* inv) {
   if (n <= 0 || ncols <= 0) return cudaSuccess;
   if (n <= kLeaf) {
-    double* Y = leaf_scratch();
-    trtri_leaf<<<1, kLeaf, 0, s>>>(L, ldl, n, Y);
-    count_launch();
+    const double* Y = inv;
+    if (!Y) {
+      double* Yw = leaf_scratch();
+      trtri_leaf<<<1, kLeaf, 0, s>>>(L, ldl, n, Yw);
+      count_launch();
+      Y = Yw;
+    }
     GemmProblem p = make_gemm(n, ncols, n, 1.0, Y, kLeaf, B, ldb, 0.0, B, ldb);
     p.ma = Mask::lower();
     return gemm(true, false, p, s);
   }
   const int n1 = split_point(n), n2 = n - n1;
-  cudaError_t e = trsm_llt(L + n1 + n1 * ldl, ldl, n2, B + n1, ldb, ncols, s);
+  cudaError_t e = trsm_llt(L + n1 + n1 * ldl, ldl, n2, B + n1, ldb, ncols, s,
+                           inv ? inv + (size_t)(n1 / kLeaf) * kLeaf * kLeaf : nullptr);
   if (e != cudaSuccess) return e;
   // B1 -= L21^T X2
   GemmProblem p = make_gemm(n1, ncols, n2, -1.0, L + n1, ldl, B + n1, ldb, 1.0, B, ldb);
   e = gemm(true, false, p, s);
   if (e != cudaSuccess) return e;
-  return trsm_llt(L, ldl, n1, B, ldb, ncols, s);
+  return trsm_llt(L, ldl, n1, B, ldb, ncols, s, inv);
 }
 
 cudaError_t trsm_lln(const double* L, long long ldl, int n, double* B, long long ldb, int ncols,
@@ -268,16 +300,17 @@ cudaError_t trsm_lln(const double* L, long long ldl, int n, double* B, long long
 }
 
 static cudaError_t potrf_rec(double* A, long long lda, int n, int off, DevStatus* st,
-                             cudaStream_t s) {
+                             cudaStream_t s, double* inv) {
   if (n <= kLeaf) {
-    potf2_kernel<<<1, 256, 0, s>>>(A, lda, n, off, st);
+    ensure_smem<potf2_kernel>();
+    potf2_kernel<<<1, 256, kLeafSmem, s>>>(A, lda, n, off, st, inv);
     count_launch();
     return cudaGetLastError();
   }
   const int n1 = split_point(n), n2 = n - n1;
-  cudaError_t e = potrf_rec(A, lda, n1, off, st, s);
+  cudaError_t e = potrf_rec(A, lda, n1, off, st, s, inv);
   if (e != cudaSuccess) return e;
-  e = trsm_rlt(A, lda, n1, A + n1, lda, n2, s);  // A21 <- A21 L11^{-T}
+  e = trsm_rlt(A, lda, n1, A + n1, lda, n2, s, inv);  // A21 <- A21 L11^{-T}
   if (e != cudaSuccess) return e;
   // A22 -= A21 A21^T (lower triangle only)
   GemmProblem p = make_gemm(n2, n2, n1, -1.0, A + n1, lda, A + n1, lda, 1.0,
@@ -285,12 +318,14 @@ static cudaError_t potrf_rec(double* A, long long lda, int n, int off, DevStatus
   p.mc = Mask::lower();
   e = gemm(false, true, p, s);
   if (e != cudaSuccess) return e;
-  return potrf_rec(A + n1 + n1 * lda, lda, n2, off + n1, st, s);
+  return potrf_rec(A + n1 + n1 * lda, lda, n2, off + n1, st, s,
+                   inv ? inv + (size_t)(n1 / kLeaf) * kLeaf * kLeaf : nullptr);
 }
 
-cudaError_t potrf_lower(double* A, long long lda, int n, DevStatus* st, cudaStream_t s) {
+cudaError_t potrf_lower(double* A, long long lda, int n, DevStatus* st, cudaStream_t s,
+                        double* inv_cache) {
   if (n <= 0) return cudaSuccess;
-  cudaError_t e = potrf_rec(A, lda, n, 0, st, s);
+  cudaError_t e = potrf_rec(A, lda, n, 0, st, s, inv_cache);
   if (e != cudaSuccess) return e;
   return zero_strict_upper(A, lda, n, s);
 }

@@ -18,15 +18,20 @@ struct DevStatus {
 // In-place lower Cholesky of the n x n matrix A (column-major, lda); the
 // strict upper triangle is zeroed.  Failure is reported through `st`
 // (first failing pivot, as kernels.py:56-61 in the reference).
-cudaError_t potrf_lower(double* A, long long lda, int n, DevStatus* st, cudaStream_t s);
+// inv_cache (optional): ceil(n/64) blocks of 64 x 64 doubles receiving the
+// inverses of the 64-wide diagonal blocks of L, reused by trsm_* (pass the
+// same cache there) so each leaf inverse is computed once.
+size_t potrf_inv_cache_doubles(int n);
+cudaError_t potrf_lower(double* A, long long lda, int n, DevStatus* st, cudaStream_t s,
+                        double* inv_cache = nullptr);
 
 // A (m x n) <- A * L^{-T}, L n x n lower (right, lower, transposed).
 cudaError_t trsm_rlt(const double* L, long long ldl, int n, double* A, long long lda, int m,
-                     cudaStream_t s);
+                     cudaStream_t s, const double* inv = nullptr);
 
 // B (n x ncols) <- L^{-T} * B (left, lower, transposed: solves L^T X = B).
 cudaError_t trsm_llt(const double* L, long long ldl, int n, double* B, long long ldb, int ncols,
-                     cudaStream_t s);
+                     cudaStream_t s, const double* inv = nullptr);
 
 // B (n x ncols) <- L^{-1} * B (left, lower, no transpose).
 cudaError_t trsm_lln(const double* L, long long ldl, int n, double* B, long long ldb, int ncols,

@@ -141,6 +141,7 @@ namespace {
 struct SolveWork {
   double* L; double* T1; double* W; double* Zr; long long ld;
   double* lam2;
+  double* linv;
   DevStatus* st;
   void* eig; size_t eig_bytes;
 };
@@ -153,6 +154,7 @@ SolveWork carve_solve(Arena& a, int n, int flags) {
   w.W = a.take<double>((size_t)w.ld * n);
   w.Zr = a.take<double>((size_t)w.ld * n);
   w.lam2 = a.take<double>(n);
+  w.linv = a.take<double>(potrf_inv_cache_doubles(n));
   w.st = a.take<DevStatus>(2);
   w.eig_bytes = syevd_bytes(n, flags);
   w.eig = a.take<char>(w.eig_bytes);
@@ -230,7 +232,7 @@ cudaError_t solve_spd_pair(int n, const double* M, long long ldm, const double* 
   stage_mark("potrf", s);
   copy_lower_kernel<<<nb, 256, 0, s>>>(n, K, ldk, w.L, ld);
   count_launch();
-  if ((e = potrf_lower(w.L, ld, n, &w.st[0], s)) != cudaSuccess) return e;
+  if ((e = potrf_lower(w.L, ld, n, &w.st[0], s, w.linv)) != cudaSuccess) return e;
   if (m_ready && (e = cudaStreamWaitEvent(s, m_ready, 0)) != cudaSuccess) return e;
   stage_mark("congruence", s);
   // 2. W = L^T M L  (T1 = M L from the lower triangle of M, then W = L^T T1, lower)
@@ -259,7 +261,7 @@ cudaError_t solve_spd_pair(int n, const double* M, long long ldm, const double* 
   g4.ma = Mask::lower();
   if ((e = gemm(false, false, g4, s)) != cudaSuccess) return e;
   stage_mark("recover_trsm", s);
-  if ((e = trsm_llt(w.L, ld, n, w.W, ld, n, s)) != cudaSuccess) return e;
+  if ((e = trsm_llt(w.L, ld, n, w.W, ld, n, s, w.linv)) != cudaSuccess) return e;
   recover_kernel<<<nb, 256, 0, s>>>(n, w.T1, w.W, ld, lam, X1, ldx1, X2, ldx2);
   count_launch();
   stage_mark("end", s);

@@ -10,6 +10,8 @@
 //   prepare (z, merge-sort, deflation scan) -> secular roots (one thread per
 //   root) -> z-hat -> output ordering -> eigenvector columns -> deflation
 //   rotations -> grouped DMMA GEMM Q_out = diag(Q1, Q2) * U.
+#include <cstdio>
+#include <cstdlib>
 #include "eig.cuh"
 
 namespace bse {
@@ -470,6 +472,14 @@ cudaError_t stedc(int n, double* d, double* e, double* wout, double* Q, long lon
     count_launch();
     if ((err = cudaGetLastError()) != cudaSuccess) return err;
     stage_mark("dc_gemm", s);
+    if (std::getenv("BSE_DC_STATS") && L.nnodes <= 4) {
+      int hc[12];
+      cudaMemcpyAsync(hc, ws.counts, sizeof(int) * 3 * L.nnodes, cudaMemcpyDeviceToHost, s);
+      cudaStreamSynchronize(s);
+      for (int q = 0; q < L.nnodes; ++q)
+        std::fprintf(stderr, "[dc] level size %d node %d: K=%d deflated=%d rotations=%d\n", size, q,
+                     hc[3 * q], hc[3 * q + 1], hc[3 * q + 2]);
+    }
     err = gemm_grouped(false, false, ws.probs, 2 * L.nnodes, L.half, maxm, s, L.half >= 2,
                        L.half >= 512 ? 3 : 1);
     if (err != cudaSuccess) return err;
