@@ -5,10 +5,12 @@ Drop-in for the solver path of the reference package ``bse`` (bse-solver
 types, the structural transforms and the solvers, with the numerical core in
 the CUDA library libbse_b200.so (C ABI: include/bse_b200.h).
 """
-from .solvers import polish, real_embedding, solve_complex, solve_pair_device, solve_real
+from .solvers import (hermitian_eigvals, polish, real_embedding, solve_complex, solve_pair_device,
+                      solve_real, syevd_values_device, tda_gap_report)
 from .spectra import absorption_device, absorption_spectrum
 from .types import (BseOperator, ConvergenceError, DipoleData, FullEigensystem,
-                    NotPositiveDefinite, PositiveEigensystem, SpectrumCurve, ValidationReport,
+                    NotPositiveDefinite, PositiveEigensystem, SpectrumCurve, TdaGapReport,
+                    ValidationReport,
                     assemble_h, build_m, conditioning_warnings, default_grid, dos_dominance,
                     expand_full, make_operator, residual_metrics)
 
@@ -20,5 +22,6 @@ __all__ = [
     "ConvergenceError", "NotPositiveDefinite", "solve_complex", "solve_real",
     "DipoleData", "SpectrumCurve", "absorption_spectrum", "default_grid", "dos_dominance",
     "conditioning_warnings", "real_embedding", "polish", "solve_pair_device",
-    "absorption_device", "__version__",
+    "absorption_device", "hermitian_eigvals", "tda_gap_report", "TdaGapReport",
+    "syevd_values_device", "__version__",
 ]

@@ -94,6 +94,10 @@ StedcWork stedc_carve(Arena& a, int n);
 cudaError_t stedc(int n, double* d, double* e, double* w, double* Q, long long ldq,
                   const StedcWork& ws, cudaStream_t s);
 
+// Values only: ascending eigenvalues of the tridiagonal by Sturm bisection.
+cudaError_t tridiag_values(int n, const double* d, const double* e, double* w, double* scratch3,
+                           cudaStream_t s);
+
 // Full pipeline on a symmetric matrix (lower triangle of A read, destroyed).
 size_t syevd_bytes(int n, int flags);
 cudaError_t syevd(int n, double* A, long long lda, double* w, double* Z, long long ldz,

@@ -108,7 +108,6 @@ size_t syevd_bytes(int n, int flags) {
 
 cudaError_t syevd(int n, double* A, long long lda, double* w, double* Z, long long ldz,
                   void* work, size_t work_bytes, int flags, cudaStream_t s) {
-  (void)flags;
   if (n <= 0) return cudaSuccess;
   Arena a{static_cast<char*>(work), work_bytes, 0, false};
   SyevdWork ws = carve_syevd(a, n);
@@ -123,6 +122,10 @@ cudaError_t syevd(int n, double* A, long long lda, double* w, double* Z, long lo
   if ((e = extract_band(A, lda, n, b, ws.AB, ws.ldab, s)) != cudaSuccess) return e;
   if ((e = sb2st(ws.AB, ws.ldab, n, b, ws.d, ws.e, ws.V2, ws.tau2, ws.progress, sms, s)) != cudaSuccess)
     return e;
+  if (flags & 0x1) {  // BSE_FLAG_VALUES_ONLY: no vectors, no back-transforms
+    stage_mark("values", s);
+    return tridiag_values(n, ws.d, ws.e, w, ws.dc.scal, s);
+  }
   stage_mark("stedc", s);
   if ((e = stedc(n, ws.d, ws.e, w, Z, ldz, ws.dc, s)) != cudaSuccess) return e;
   stage_mark("q2_build", s);

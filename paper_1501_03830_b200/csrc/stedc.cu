@@ -394,7 +394,76 @@ __global__ void copy_matrix_kernel(int rows, int cols, const double* src, long l
   dst[r + (long long)c * ldd] = src[r + (long long)c * lds];
 }
 
+// Values only: the i-th smallest eigenvalue of the symmetric tridiagonal
+// (d, e) by bisection on Sturm counts (one thread per eigenvalue), with the
+// pivmin guard and convergence width of the reference's _bisect_values
+// (kernels.py:275-299).
+__global__ void sturm_bisect_kernel(int n, const double* __restrict__ d,
+                                    const double* __restrict__ e, double* __restrict__ w,
+                                    const double* __restrict__ bounds) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const double pivmin = bounds[2];
+  double lo = bounds[0], hi = bounds[1];
+  for (int it = 0; it < 200; ++it) {
+    if (!(hi - lo > 2.0 * kEps * (fabs(lo) + fabs(hi)) + 2.0 * kSafmin)) break;
+    const double x = 0.5 * (lo + hi);
+    int cnt = 0;
+    double q = d[0] - x;
+    if (fabs(q) < pivmin) q = -pivmin;
+    cnt += q < 0.0;
+    for (int k = 1; k < n; ++k) {
+      q = d[k] - x - (e[k - 1] * e[k - 1]) / q;
+      if (fabs(q) < pivmin) q = -pivmin;
+      cnt += q < 0.0;
+    }
+    if (cnt > i) hi = x; else lo = x;
+  }
+  w[i] = 0.5 * (lo + hi);
+}
+
+__global__ void gershgorin_kernel(int n, const double* d, const double* e, double* bounds) {
+  __shared__ double slo[32], shi[32], se[32];
+  double lo = 1e300, hi = -1e300, emax2 = 0.0;
+  for (int i = threadIdx.x; i < n; i += blockDim.x) {
+    double r = 0.0;
+    if (i > 0) r += fabs(e[i - 1]);
+    if (i < n - 1) { r += fabs(e[i]); emax2 = fmax(emax2, e[i] * e[i]); }
+    lo = fmin(lo, d[i] - r);
+    hi = fmax(hi, d[i] + r);
+  }
+  for (int o = 16; o > 0; o >>= 1) {
+    lo = fmin(lo, __shfl_xor_sync(0xffffffffu, lo, o));
+    hi = fmax(hi, __shfl_xor_sync(0xffffffffu, hi, o));
+    emax2 = fmax(emax2, __shfl_xor_sync(0xffffffffu, emax2, o));
+  }
+  const int w = threadIdx.x >> 5;
+  if ((threadIdx.x & 31) == 0) { slo[w] = lo; shi[w] = hi; se[w] = emax2; }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int k = 1; k < (int)(blockDim.x >> 5); ++k) {
+      lo = fmin(lo, slo[k]); hi = fmax(hi, shi[k]); emax2 = fmax(emax2, se[k]);
+    }
+    lo = fmin(lo, slo[0]); hi = fmax(hi, shi[0]); emax2 = fmax(emax2, se[0]);
+    const double pivmin = kSafmin * fmax(1.0, emax2);
+    const double pad = 2.0 * kEps * fmax(fabs(lo), fabs(hi)) + 2.0 * pivmin;
+    bounds[0] = lo - pad;
+    bounds[1] = hi + pad;
+    bounds[2] = pivmin;
+  }
+}
+
 }  // namespace
+
+cudaError_t tridiag_values(int n, const double* d, const double* e, double* w, double* scratch3,
+                           cudaStream_t s) {
+  if (n <= 0) return cudaSuccess;
+  gershgorin_kernel<<<1, 1024, 0, s>>>(n, d, e, scratch3);
+  count_launch();
+  sturm_bisect_kernel<<<(unsigned)ceil_div(n, 128), 128, 0, s>>>(n, d, e, w, scratch3);
+  count_launch();
+  return cudaGetLastError();
+}
 
 StedcWork stedc_carve(Arena& a, int n) {
   StedcWork w;

@@ -155,17 +155,31 @@ def _select_and_polish(lam2, X1, X2, ld, n, dev):
             for t in range(max(k, 1)):
                 lam.append(float(np.mean(vals[2 * t:2 * t + 2])) if 2 * t + 1 < size else float(vals[-1]))
         start = stop
-    # assemble planar complex X1c, X2c (n x n) on device
-    cols1, cols2 = [], []
+    # assemble planar complex X1c, X2c (n x n) on device: one gather for all
+    # simple pairs, cluster blocks copied in place
+    X1c = torch.empty((n, n), dtype=torch.complex128, device=dev)
+    X2c = torch.empty((n, n), dtype=torch.complex128, device=dev)
+    simple_out, simple_src, col = [], [], 0
+    blocks = []
     for s in sel:
         if isinstance(s, int):
-            cols1.append(torch.complex(x1[:n, s], x1[n:, s]).unsqueeze(1))
-            cols2.append(torch.complex(x2[:n, s], -x2[n:, s]).unsqueeze(1))
+            simple_out.append(col)
+            simple_src.append(s)
+            col += 1
         else:
-            cols1.append(s[2])
-            cols2.append(s[3])
-    X1c = torch.cat(cols1, 1)[:, :n].contiguous()
-    X2c = torch.cat(cols2, 1)[:, :n].contiguous()
+            k = s[2].shape[1]
+            blocks.append((col, s[2], s[3]))
+            col += k
+    if simple_src:
+        src = torch.tensor(simple_src, device=dev)
+        dst = torch.tensor(simple_out, device=dev)
+        X1c[:, dst] = torch.complex(x1[:n, src], x1[n:, src])
+        X2c[:, dst] = torch.complex(x2[:n, src], -x2[n:, src])
+    for c0, b1, b2 in blocks:
+        k = min(b1.shape[1], n - c0)
+        if k > 0:
+            X1c[:, c0:c0 + k] = b1[:, :k]
+            X2c[:, c0:c0 + k] = b2[:, :k]
     lam = np.array(lam[:n])
     X1c, X2c = polish(X1c, X2c)
     return lam, X1c, X2c
@@ -212,6 +226,58 @@ def polish(X1c, X2c):
     _gemm(0, 0, 2 * n, 2 * n, 2 * n, 1.0, ptr(Xs), ldx, ptr(Fb), ldf, 0.0, ptr(Out), ldx)
     ov = view_colmajor(Out, 2 * n, 2 * n)
     return torch.complex(ov[:n, :n], ov[:n, n:]), torch.complex(ov[n:, :n], ov[n:, n:])
+
+
+def syevd_values_device(At, lda: int, n: int):
+    """Ascending eigenvalues of the symmetric matrix in At (lower triangle,
+    destroyed) via bse_syevd_dev(BSE_FLAG_VALUES_ONLY): SY2SB + SB2ST + Sturm
+    bisection, no back-transforms."""
+    torch = require_cuda()
+    lib = _lib.load()
+    dev = At.device
+    w = torch.empty(max(n, 1), dtype=torch.float64, device=dev)
+    wb = lib.bse_syevd_workspace_bytes(n, _lib.FLAG_VALUES_ONLY)
+    work = torch.empty(max(int(wb), 1), dtype=torch.uint8, device=dev)
+    st = lib.bse_syevd_dev(n, ptr(At), lda, ptr(w), 0, n, ptr(work), wb, _lib.FLAG_VALUES_ONLY,
+                           stream_ptr(dev))
+    if st != _lib.BSE_OK:
+        raise RuntimeError(f"bse_syevd_dev failed ({st}): {_lib.last_error()}")
+    return w[:n]
+
+
+def hermitian_eigvals(a) -> np.ndarray:
+    """Eigenvalues (descending) of a Hermitian matrix on the GPU.  Complex
+    input goes through the real doubling embedding [[Re A, Im A], [-Im A, Re A]]
+    whose spectrum is A's with every eigenvalue doubled (reference:
+    kernels.hermitian_eig, kernels.py:616-641, values only)."""
+    a = np.asarray(a, dtype=np.complex128)
+    n = a.shape[0]
+    if n == 0:
+        return np.zeros(0)
+    dev = _device()
+    if np.all(a.imag == 0.0):
+        At, lda = to_device_colmajor(0.5 * (a.real + a.real.T), dev)
+        w = syevd_values_device(At, lda, n).cpu().numpy()
+        return w[::-1].copy()
+    t = np.block([[a.real, a.imag], [-a.imag, a.real]])
+    At, lda = to_device_colmajor(0.5 * (t + t.T), dev)
+    w2 = syevd_values_device(At, lda, 2 * n).cpu().numpy()[::-1]
+    return 0.5 * (w2[0::2] + w2[1::2])
+
+
+def tda_gap_report(op: BseOperator, workers: int = 1):
+    """Tamm-Dancoff overestimation gaps g_j = lambda_j(A) - lambda_j(H)
+    (reference: solvers.tda_gap_report, solvers.py:149-160); both spectra on
+    the GPU."""
+    from .types import TdaGapReport
+    lam_a = hermitian_eigvals(op.a)
+    lam_h = solve_complex(op, workers=workers).lambda_plus
+    gaps = lam_a - lam_h
+    scale = float(np.max(np.abs(lam_a))) if lam_a.size else 0.0
+    min_gap = float(np.min(gaps)) if gaps.size else 0.0
+    max_rel = float(np.max(gaps / lam_h)) if gaps.size else 0.0
+    return TdaGapReport(gaps=gaps, max_relative_gap=max_rel, min_gap=min_gap, scale=scale,
+                        certified=bool(min_gap >= -1e-12 * scale))
 
 
 def solve_complex(op: BseOperator, workers: int = 1) -> PositiveEigensystem:

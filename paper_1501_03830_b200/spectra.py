@@ -48,11 +48,11 @@ def absorption_spectrum(pos: PositiveEigensystem, dip: DipoleData, grid=None,
     if grid is None:
         grid = default_grid(pos.lambda_plus, sigma)
     grid = np.asarray(grid, dtype=np.float64)
-    lam = torch.from_numpy(np.ascontiguousarray(pos.lambda_plus)).to(dev)
-    X1c = torch.from_numpy(np.ascontiguousarray(pos.x1.T)).to(dev)
-    X2c = torch.from_numpy(np.ascontiguousarray(pos.x2.T)).to(dev)
-    dr = torch.from_numpy(np.ascontiguousarray(dip.d_r)).to(dev)
-    dl = torch.from_numpy(np.ascontiguousarray(dip.d_l)).to(dev)
+    lam = torch.from_numpy(np.array(pos.lambda_plus)).to(dev)
+    X1c = torch.from_numpy(np.array(pos.x1.T, order="C")).to(dev)
+    X2c = torch.from_numpy(np.array(pos.x2.T, order="C")).to(dev)
+    dr = torch.from_numpy(np.array(dip.d_r)).to(dev)
+    dl = torch.from_numpy(np.array(dip.d_l)).to(dev)
     g = torch.from_numpy(np.ascontiguousarray(grid)).to(dev)
     values, _, defect, minpair = absorption_device(lam, X1c, X2c, dr, dl, g, sigma)
     if n and float(minpair) < 1e-8:

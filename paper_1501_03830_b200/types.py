@@ -169,6 +169,17 @@ class FullEigensystem:
         return self.lam.shape[0] // 2
 
 
+@dataclass(frozen=True)
+class TdaGapReport:
+    """solvers.py:136-146."""
+
+    gaps: np.ndarray
+    max_relative_gap: float
+    min_gap: float
+    scale: float
+    certified: bool
+
+
 def build_m(op: BseOperator) -> np.ndarray:
     """M = [[Re(A+B), Im(A-B)], [-Im(A+B), Re(A-B)]], bitwise symmetric
     (embeddings.py:62-74)."""
