@@ -203,7 +203,7 @@ BSE_DEV void gemm_tile(const GemmProblem& p, int m0, int n0, double* smem) {
           const int d = gn - gm;
           if (d < p.mc.lo || d > p.mc.hi) continue;
         }
-        double* cp = p.C + gm + (long long)gn * p.ldc;
+        double* cp = p.C + gm + (long long)(p.ccol ? p.ccol[gn] : gn) * p.ldc;
         double v = alpha * acc[i][j][e];
         if (beta != 0.0) v += beta * *cp;
         *cp = v;

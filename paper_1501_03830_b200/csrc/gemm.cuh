@@ -36,6 +36,7 @@ struct GemmProblem {
   long long ldc = 0;
   double alpha = 1.0, beta = 0.0;
   Mask ma, mb, mc;
+  const int* ccol = nullptr;  // optional column map: C column n is written at ccol[n]
 };
 
 // Single problem.  transA/transB: op(X) = X^T.

@@ -314,8 +314,9 @@ __global__ void __launch_bounds__(kDcThreads) dc_vectors_kernel(Level L, int n, 
   const int lane = threadIdx.x & 31;
   const int t = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);  // column source index
   if (t >= m) return;
-  const int col = w.pos[lo + t];
-  double* U = w.U + lo + (long long)(lo + col) * ld;
+  // compact order: roots first (t < K), then deflated columns; the merge GEMM
+  // scatters its output to the sorted positions w.pos through a column map
+  double* U = w.U + lo + (long long)(lo + t) * ld;
   for (int r = lane; r < m; r += 32) U[r] = 0.0;
   __syncwarp();
   const int* perm = w.perm + lo;
@@ -368,17 +369,45 @@ __global__ void dc_probs_kernel(Level L, int n, StedcWork w, const double* Qin, 
   GemmProblem top, bot;
   if (mid < hi) {
     const int n1 = mid - lo, n2 = hi - mid, m = hi - lo;
-    top.M = n1; top.N = m; top.K = n1;
+    const int K = w.counts[3 * i], nr = w.counts[3 * i + 2];
+    // deflated columns are unit vectors unless a Givens rotation touched the
+    // node: then they join the GEMM, else dc_copy_deflated moves them
+    const int ncols = (nr > 0) ? m : K;
+    top.M = n1; top.N = ncols; top.K = n1;
+    top.ccol = w.pos + lo; bot.ccol = w.pos + lo;
+    bot.N = ncols;
     top.A = Qin + lo + (long long)lo * ld; top.lda = ld;
     top.B = w.U + lo + (long long)lo * ld; top.ldb = ld;
     top.C = Qout + lo + (long long)lo * ld; top.ldc = ld;
-    bot.M = n2; bot.N = m; bot.K = n2;
+    bot.M = n2; bot.K = n2;
     bot.A = Qin + mid + (long long)mid * ld; bot.lda = ld;
     bot.B = w.U + mid + (long long)lo * ld; bot.ldb = ld;
     bot.C = Qout + mid + (long long)lo * ld; bot.ldc = ld;
   }
   w.probs[2 * i] = top;
   w.probs[2 * i + 1] = bot;
+}
+
+// Deflated (unrotated) columns: the merged eigenvector is the child's
+// eigenvector, copied to its sorted output position (zeros in the other
+// child's rows).  One warp per column.
+__global__ void dc_copy_deflated_kernel(Level L, int n, StedcWork w, const double* Qin,
+                                        double* Qout, long long ld) {
+  int lo, mid, hi;
+  node_range(L, n, blockIdx.y, lo, mid, hi);
+  const int K = w.counts[3 * blockIdx.y], nr = w.counts[3 * blockIdx.y + 2];
+  if (K < 0 || nr > 0) return;
+  const int m = hi - lo, nd = m - K;
+  const int c = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (c >= nd) return;
+  const int lane = threadIdx.x & 31;
+  const int jloc = w.perm[lo + w.defl[lo + c]];  // node-local original column
+  const int outc = w.pos[lo + K + c];
+  const bool first = (lo + jloc) < mid;
+  const int r0 = first ? lo : mid, r1 = first ? mid : hi;
+  const double* src = Qin + (long long)(lo + jloc) * ld;
+  double* dst = Qout + (long long)(lo + outc) * ld;
+  for (int r = lo + lane; r < hi; r += 32) dst[r] = (r >= r0 && r < r1) ? src[r] : 0.0;
 }
 
 __global__ void dc_finish_kernel(int n, const double* D, double* wout, const double* scal) {
@@ -552,6 +581,8 @@ cudaError_t stedc(int n, double* d, double* e, double* wout, double* Q, long lon
     err = gemm_grouped(false, false, ws.probs, 2 * L.nnodes, L.half, maxm, s, L.half >= 2,
                        L.half >= 512 ? 3 : 1);
     if (err != cudaSuccess) return err;
+    dc_copy_deflated_kernel<<<g2, kDcThreads, 0, s>>>(L, n, ws, Qin, Qout, ld);
+    count_launch();
     std::swap(Din, Dout);
     std::swap(Qin, Qout);
   }
