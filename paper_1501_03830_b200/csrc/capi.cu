@@ -172,16 +172,18 @@ int bse_solve_spd_pair_host(int64_t n, const double* M, int64_t ldm, const doubl
   if (e == cudaSuccess)
     e = cudaMemcpy2DAsync(dM, ld * 8, M, ldm * 8, row, n, cudaMemcpyHostToDevice, s2);
   if (e == cudaSuccess) e = cudaEventRecord(evM, s2);
+  // X1/X2 column blocks stream back on s2 while later blocks are recovered
+  bse::HostOut hout{X1, ldx1, X2, ldx2, lam, s2};
   if (e == cudaSuccess)
     e = bse::solve_spd_pair((int)n, dM, ld, dK, ld, dLam, dX1, ld, dX2, ld, dW, wb, flags, s, &st,
-                            evM);
-  if (e == cudaSuccess) e = cudaMemcpyAsync(lam, dLam, row, cudaMemcpyDeviceToHost, s);
-  if (e == cudaSuccess)
-    e = cudaMemcpy2DAsync(X1, ldx1 * 8, dX1, ld * 8, row, n, cudaMemcpyDeviceToHost, s);
-  if (e == cudaSuccess)
-    e = cudaMemcpy2DAsync(X2, ldx2 * 8, dX2, ld * 8, row, n, cudaMemcpyDeviceToHost, s);
+                            evM, &hout);
+  cudaEvent_t evDone;
+  cudaEventCreateWithFlags(&evDone, cudaEventDisableTiming);
+  cudaEventRecord(evDone, s2);
+  cudaStreamWaitEvent(s, evDone, 0);  // device buffers stay alive until the copies finish
   cudaFreeAsync(buf, s);
   cudaError_t e2 = cudaStreamSynchronize(s);
+  cudaEventDestroy(evDone);
   cudaStreamDestroy(s);
   cudaStreamDestroy(s2);
   cudaEventDestroy(evM);

@@ -95,10 +95,33 @@ BSE_DEV void gemm_tile(const GemmProblem& p, int m0, int n0, double* smem) {
 
   constexpr int MI = WM / 8, NJ = WN / 8;
   double acc[MI][NJ][2];
+  // beta != 0 with alpha = +-1: start the accumulators at (beta/alpha) C so
+  // the C read overlaps the pipeline prologue (exact for alpha = +-1)
+  const bool cpre = p.beta != 0.0 && (p.alpha == 1.0 || p.alpha == -1.0) && K <= 512;
+  {
+    const double f = cpre ? p.beta / p.alpha : 0.0;
+    const int klq = (threadIdx.x & 31) & 3, rlq = (threadIdx.x & 31) >> 2;
+    const int wmq = (threadIdx.x >> 5) % C::WARPS_M, wnq = (threadIdx.x >> 5) / C::WARPS_M;
 #pragma unroll
-  for (int i = 0; i < MI; ++i)
+    for (int i = 0; i < MI; ++i)
 #pragma unroll
-    for (int j = 0; j < NJ; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+      for (int j = 0; j < NJ; ++j)
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          double v = 0.0;
+          if (cpre) {
+            const int gm = m0 + wmq * WM + i * 8 + rlq;
+            const int gn = n0 + wnq * WN + j * 8 + klq * 2 + e;
+            bool ok = gm < M && gn < N;
+            if (MASKED && ok) {
+              const int d = gn - gm;
+              ok = d >= p.mc.lo && d <= p.mc.hi;
+            }
+            if (ok) v = f * p.C[gm + (long long)(p.ccol ? p.ccol[gn] : gn) * p.ldc];
+          }
+          acc[i][j][e] = v;
+        }
+  }
 
   auto load_stage = [&](int st, int kt) {
     double* sA = smem + st * C::STAGE;
@@ -205,7 +228,7 @@ BSE_DEV void gemm_tile(const GemmProblem& p, int m0, int n0, double* smem) {
         }
         double* cp = p.C + gm + (long long)(p.ccol ? p.ccol[gn] : gn) * p.ldc;
         double v = alpha * acc[i][j][e];
-        if (beta != 0.0) v += beta * *cp;
+        if (beta != 0.0 && !cpre) v += beta * *cp;
         *cp = v;
       }
     }

@@ -190,12 +190,12 @@ __global__ void scale_reverse_kernel(int n, const double* Z, long long ldz, cons
   }
 }
 
-// X1 = (u + v) / (2 sqrt(lam)), X2 = (u - v) / (2 sqrt(lam))
-__global__ void recover_kernel(int n, const double* U, const double* V, long long ld,
+// X1 = (u + v) / (2 sqrt(lam)), X2 = (u - v) / (2 sqrt(lam))  (n rows, ncols columns)
+__global__ void recover_kernel(int n, int ncols, const double* U, const double* V, long long ld,
                                const double* lam, double* X1, long long ldx1, double* X2,
                                long long ldx2) {
   const long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x;
-  if (idx >= (long long)n * n) return;
+  if (idx >= (long long)n * ncols) return;
   const int r = (int)(idx % n), c = (int)(idx / n);
   const double sc = 0.5 / sqrt(lam[c]);
   const double u = U[r + (long long)c * ld], v = V[r + (long long)c * ld];
@@ -216,7 +216,7 @@ size_t solve_bytes(int n, int flags) {
 cudaError_t solve_spd_pair(int n, const double* M, long long ldm, const double* K, long long ldk,
                            double* lam, double* X1, long long ldx1, double* X2, long long ldx2,
                            void* work, size_t work_bytes, int flags, cudaStream_t s,
-                           SolveStatus* out, cudaEvent_t m_ready) {
+                           SolveStatus* out, cudaEvent_t m_ready, const HostOut* hout) {
   out->code = 0;
   out->pivot_index = -1;
   out->pivot_value = 0.0;
@@ -258,19 +258,56 @@ cudaError_t solve_spd_pair(int n, const double* M, long long ldm, const double* 
   int* bad = reinterpret_cast<int*>(&w.st[1].conv_fail);
   scale_reverse_kernel<<<nb, 256, 0, s>>>(n, w.T1, ld, w.lam2, w.Zr, w.W, ld, lam, bad);
   count_launch();
-  // u = L Zr (into T1), v = L^{-T} (Zr Lam) (in W)
-  stage_mark("recover_trmm", s);
-  GemmProblem g4 = make_gemm(n, n, n, 1.0, w.L, ld, w.Zr, ld, 0.0, w.T1, ld);
-  g4.ma = Mask::lower();
-  if ((e = gemm(false, false, g4, s)) != cudaSuccess) return e;
-  stage_mark("recover_trsm", s);
-  if ((e = trsm_llt(w.L, ld, n, w.W, ld, n, s, w.linv)) != cudaSuccess) return e;
-  recover_kernel<<<nb, 256, 0, s>>>(n, w.T1, w.W, ld, lam, X1, ldx1, X2, ldx2);
-  count_launch();
+  // u = L Zr (into T1), v = L^{-T} (Zr Lam) (in W); with host outputs the
+  // recovery runs in column blocks so each block's D2H copy overlaps the next
+  // block's TRMM/TRSM
+  const int cb = hout ? kRecoverBlock : n;
+  std::vector<cudaEvent_t> evs;
+  for (int c0 = 0; c0 < n; c0 += cb) {
+    const int nc = std::min(cb, n - c0);
+    stage_mark("recover_trmm", s);
+    GemmProblem g4 = make_gemm(n, nc, n, 1.0, w.L, ld, w.Zr + (long long)c0 * ld, ld, 0.0,
+                               w.T1 + (long long)c0 * ld, ld);
+    g4.ma = Mask::lower();
+    if ((e = gemm(false, false, g4, s)) != cudaSuccess) return e;
+    stage_mark("recover_trsm", s);
+    if ((e = trsm_llt(w.L, ld, n, w.W + (long long)c0 * ld, ld, nc, s, w.linv)) != cudaSuccess)
+      return e;
+    const long long tb = (long long)n * nc;
+    recover_kernel<<<(unsigned)ceil_div(tb, 256), 256, 0, s>>>(
+        n, nc, w.T1 + (long long)c0 * ld, w.W + (long long)c0 * ld, ld, lam + c0,
+        X1 + (long long)c0 * ldx1, ldx1, X2 + (long long)c0 * ldx2, ldx2);
+    count_launch();
+    if (hout) {
+      cudaEvent_t ev;
+      cudaEventCreateWithFlags(&ev, cudaEventDisableTiming);
+      evs.push_back(ev);
+      cudaEventRecord(ev, s);
+      cudaStreamWaitEvent(hout->stream, ev, 0);
+      const size_t row = sizeof(double) * (size_t)n;
+      if ((e = cudaMemcpy2DAsync(hout->X1 + (long long)c0 * hout->ldx1, hout->ldx1 * 8,
+                                 X1 + (long long)c0 * ldx1, ldx1 * 8, row, nc,
+                                 cudaMemcpyDeviceToHost, hout->stream)) != cudaSuccess)
+        return e;
+      if ((e = cudaMemcpy2DAsync(hout->X2 + (long long)c0 * hout->ldx2, hout->ldx2 * 8,
+                                 X2 + (long long)c0 * ldx2, ldx2 * 8, row, nc,
+                                 cudaMemcpyDeviceToHost, hout->stream)) != cudaSuccess)
+        return e;
+    }
+  }
+  if (hout) {
+    if ((e = cudaMemcpyAsync(hout->lam, lam, sizeof(double) * n, cudaMemcpyDeviceToHost, s)) !=
+        cudaSuccess)
+      return e;
+  }
   stage_mark("end", s);
   if ((e = cudaGetLastError()) != cudaSuccess) return e;
   // status
   DevStatus hs[2];
+  struct EvGuard {
+    std::vector<cudaEvent_t>& v;
+    ~EvGuard() { for (auto ev : v) cudaEventDestroy(ev); }
+  } guard{evs};
   if ((e = cudaMemcpyAsync(hs, w.st, sizeof(hs), cudaMemcpyDeviceToHost, s)) != cudaSuccess) return e;
   if ((e = cudaStreamSynchronize(s)) != cudaSuccess) return e;
   if (hs[0].info >= 0 || hs[1].conv_fail) {

@@ -25,11 +25,22 @@ struct SolveStatus {
   int failed_factor;   // 0: K (A-B), 1: M (A+B)
 };
 
+// Optional host destination for the e2e path: X1/X2 column blocks are copied
+// on `stream` as soon as they are recovered.
+struct HostOut {
+  double* X1; long long ldx1;
+  double* X2; long long ldx2;
+  double* lam;
+  cudaStream_t stream;
+};
+constexpr int kRecoverBlock = 2048;
+
 size_t solve_bytes(int n, int flags);
 cudaError_t solve_spd_pair(int n, const double* M, long long ldm, const double* K, long long ldk,
                            double* lam, double* X1, long long ldx1, double* X2, long long ldx2,
                            void* work, size_t work_bytes, int flags, cudaStream_t s,
-                           SolveStatus* out, cudaEvent_t m_ready = nullptr);
+                           SolveStatus* out, cudaEvent_t m_ready = nullptr,
+                           const HostOut* hout = nullptr);
 
 cudaError_t absorption(int n, const double* lam, const double* X1c, long long ldx1,
                        const double* X2c, long long ldx2, const double* dr, const double* dl,

@@ -204,3 +204,26 @@ def test_absorption_rejects_degenerate_pairing(dev):
     with pytest.raises(ValueError, match="1e-8"):
         bg.absorption_spectrum(pos, bg.DipoleData(d_r=np.ones(2), d_l=np.ones(2)),
                                grid=np.linspace(0, 2, 5), sigma=0.1)
+
+
+@pytest.mark.parametrize("n", [3, 300, 4500])
+def test_host_entry_matches_device_entry(dev, n):
+    """bse_solve_spd_pair_host (pinned-free host buffers, column-blocked D2H
+    overlapped with the recovery) gives bit-identical results to the device
+    entry used by the Python API."""
+    import ctypes as C
+    from paper_1501_03830_b200 import _lib
+    a, b, _ = configs.config_operator(0, n=n)
+    m = np.asfortranarray(a + b)
+    k = np.asfortranarray(a - b)
+    lam = np.empty(n)
+    x1 = np.empty((n, n), order="F")
+    x2 = np.empty((n, n), order="F")
+    info = _lib.BseInfo()
+    st = _lib.load().bse_solve_spd_pair_host(n, m.ctypes.data, n, k.ctypes.data, n,
+                                             lam.ctypes.data, x1.ctypes.data, n, x2.ctypes.data, n,
+                                             0, C.byref(info))
+    assert st == 0, _lib.last_error()
+    pos = bg.solve_real(bg.make_operator(a, b, kind="real"))
+    assert np.array_equal(lam, pos.lambda_plus)
+    assert np.array_equal(x1, pos.x1.real) and np.array_equal(x2, pos.x2.real)
