@@ -8,14 +8,17 @@
 //    by a column-slab kernel whose two small products run on DMMA.
 //  * Q1 (SY2SB panels): plain compact-WY, three DMMA GEMMs per panel.
 #include <algorithm>
+#include <cstdio>
+#include <cstdlib>
+#include <vector>
 #include "eig.cuh"
 
 namespace bse {
 namespace {
 
 constexpr int kQ2G = 32;      // sweeps per block
-constexpr int kQ2W = 64;      // Z columns per CTA
-constexpr int kQ2Threads = 256;
+constexpr int kQ2W = 112;     // Z columns per CTA (14 warps x 8): 147 CTAs = one wave at n = 16384
+constexpr int kQ2Threads = 448;
 
 BSE_HD int q2_hb(int b, int g) { return ((g + b + 1) / 2) * 2; }  // padded block height
 
@@ -83,128 +86,171 @@ __global__ void __launch_bounds__(256) q2_build_kernel(int n, int b, int g, int 
   }
 }
 
-// Column slab kernel: for each block in order, Z[r0:r0+HB, slab] -= VT (V^T Z).
-// Y = V^T Z reuses V's shared memory, so two CTAs fit per SM and the 256
-// slabs of an n = 16384 problem run as a single wave; Z rows are staged with
-// 16-byte cp.async from the even row below r0.
-template <int HB, int G>
-__global__ void __launch_bounds__(kQ2Threads, 2) q2_apply_kernel(int n, int b, int maxsteps,
+// Column slab kernel, register-resident Z.  Each warp owns 8 columns of Z;
+// the 96 x 8 rows of the current block live in registers in the DMMA
+// accumulator (C) layout, and the B-operand fragments of Y = V^T Z are built
+// from them with warp shuffles, so Z never touches shared memory and the two
+// products need no block barrier.  Consecutive blocks of a sweep group
+// overlap by 32 rows: those stay in registers, the 64 new rows are
+// prefetched into registers while the current block computes, and V, VT are
+// double-buffered in shared memory with cp.async (2 CTAs / SM).  The zero
+// corners of the staircase V (and of VT = V T) are skipped at compile time.
+constexpr int kQ2HB = 96;
+
+BSE_DEV double bfrag(const double (&acc)[12][2], int t, int lane) {
+  // B fragment (k = 4t + lane%4, n = lane/4) of the 96 x 8 tile held in C layout
+  const int kl = lane & 3, rl = lane >> 2;
+  const int src = ((4 * (t & 1) + kl) << 2) + (rl >> 1);
+  const double v0 = __shfl_sync(0xffffffffu, acc[t >> 1][0], src);
+  const double v1 = __shfl_sync(0xffffffffu, acc[t >> 1][1], src);
+  return (rl & 1) ? v1 : v0;
+}
+
+__global__ void __launch_bounds__(kQ2Threads, 1) q2_apply_kernel(int n, int b, int maxsteps,
                                                                  const double* __restrict__ Vblk,
                                                                  const double* __restrict__ VTblk,
                                                                  double* __restrict__ Z,
-                                                                 long long ldz, int ncols) {
-  constexpr int LDV = HB + 4;   // == 4 mod 16: conflict-free fragment loads
-  constexpr int LDZ = HB + 4;
-  constexpr int LDY = G + 4;
-  constexpr int W = kQ2W;
-  static_assert(W * LDY <= G * LDV, "Y must fit in V's buffer");
+                                                                 long long ldz, int ncols,
+                                                                 unsigned long long* trace) {
+  constexpr int HB = kQ2HB, G = kQ2G;
+  constexpr int LDV = HB + 4;  // == 4 mod 16: conflict-free fragment loads
+  constexpr int STAGE = 2 * G * LDV;
+  constexpr int LDN = 64 + 4;  // prefetched rows, [col * LDN + row]
   extern __shared__ __align__(16) double sm[];
-  double* sV = sm;               // HB x G  [c*LDV + r]; later Y (G x W) [c*LDY + r]
-  double* sVT = sV + G * LDV;    // HB x G
-  double* sZ = sVT + G * LDV;    // (HB+2) x W  [c*LDZ + r]
-  double* sY = sV;
+  double* sZn = sm + 2 * STAGE;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int c0 = blockIdx.x * W;
-  const int wcols = min(W, ncols - c0);
+  const int kl = lane & 3, rl = lane >> 2;
+  const int cw = blockIdx.x * kQ2W + warp * 8;  // first column of this warp
   const int nsweeps = n - 2;
   const int ngroups = (int)ceil_div(nsweeps, G);
-  const int kl = lane & 3, rl = lane >> 2;
-  const int wm = warp & 1, wn = warp >> 1;
+  (void)trace;
 
-  for (int gi = ngroups - 1; gi >= 0; --gi) {
+  // flattened block sequence: groups descending, steps ascending
+  auto nsteps_of = [&](int gi) {
     const int s0 = gi * G;
-    for (int j = 0; j < maxsteps; ++j) {
-      const int r0 = s0 + 1 + j * b;
-      if (r0 > n - 1) break;
-      const size_t blk = (size_t)gi * maxsteps + j;
-      const double* gV = Vblk + blk * HB * G;
-      const double* gVT = VTblk + blk * HB * G;
-      const int rows = min(HB, n - r0);
-      const int off = r0 & 1;          // smem row of global row r0
-      const int re = r0 - off;         // even start row
-      const int rows_e = rows + off;   // rows staged
-      for (int idx = tid; idx < HB * G / 2; idx += blockDim.x) {
-        const int e = idx * 2;
-        const int r = e % HB, c = e / HB;
-        cp_async16(sV + c * LDV + r, gV + e, true);
-        cp_async16(sVT + c * LDV + r, gVT + e, true);
-      }
-      constexpr int ZCH = (HB + 2) / 2;  // 16-byte chunks per column
-      for (int idx = tid; idx < ZCH * W; idx += blockDim.x) {
-        const int r = (idx % ZCH) * 2, c = idx / ZCH;
-        const bool cok = c < wcols;
-        const double* src = Z + re + r + (long long)(c0 + c) * ldz;
-        double* dst = sZ + c * LDZ + r;
-        const bool v0 = cok && r < rows_e, v1 = cok && r + 1 < rows_e;
-        if (v0 && v1) cp_async16(dst, src, true);
-        else { cp_async8(dst, v0 ? src : Z, v0); cp_async8(dst + 1, v1 ? src + 1 : Z, v1); }
-      }
-      cp_async_commit();
-      cp_async_wait<0>();
-      __syncthreads();
-      // Y (G x W) = V^T Z : 8 warps as 2 (m) x 4 (n), warp tile (G/2) x 16
-      {
-        constexpr int WM = G / 2, MI = WM / 8;
-        double acc[MI][2][2];
-#pragma unroll
-        for (int i = 0; i < MI; ++i) acc[i][0][0] = acc[i][0][1] = acc[i][1][0] = acc[i][1][1] = 0.0;
-        // reflector c of the block is nonzero on rows [c, c + b) only
-        const int kbeg = wm * WM, kend = min(HB, wm * WM + WM + b);
-#pragma unroll 4
-        for (int k = kbeg; k < kend; k += 4) {
-          double af[MI], bf[2];
-#pragma unroll
-          for (int i = 0; i < MI; ++i) af[i] = sV[(wm * WM + i * 8 + rl) * LDV + k + kl];
-#pragma unroll
-          for (int jj = 0; jj < 2; ++jj) bf[jj] = sZ[(wn * 16 + jj * 8 + rl) * LDZ + off + k + kl];
-#pragma unroll
-          for (int i = 0; i < MI; ++i)
-#pragma unroll
-            for (int jj = 0; jj < 2; ++jj) dmma8x8x4(acc[i][jj], af[i], bf[jj]);
-        }
-        __syncthreads();  // V consumed: Y overwrites it
-#pragma unroll
-        for (int i = 0; i < MI; ++i)
-#pragma unroll
-          for (int jj = 0; jj < 2; ++jj)
-#pragma unroll
-            for (int e = 0; e < 2; ++e) {
-              const int m = wm * WM + i * 8 + rl, c = wn * 16 + jj * 8 + kl * 2 + e;
-              sY[c * LDY + m] = acc[i][jj][e];
-            }
-      }
-      __syncthreads();
-      // Z (HB x W) -= VT Y : 8 warps as 2 (m) x 4 (n), warp tile (HB/2) x 16
-      {
-        constexpr int WM = HB / 2, MI = WM / 8;
-        double acc[MI][2][2];
-#pragma unroll
-        for (int i = 0; i < MI; ++i) acc[i][0][0] = acc[i][0][1] = acc[i][1][0] = acc[i][1][1] = 0.0;
-#pragma unroll
-        for (int k = 0; k < G; k += 4) {
-          double af[MI], bf[2];
-#pragma unroll
-          for (int i = 0; i < MI; ++i) af[i] = sVT[(k + kl) * LDV + wm * WM + i * 8 + rl];
-#pragma unroll
-          for (int jj = 0; jj < 2; ++jj) bf[jj] = sY[(wn * 16 + jj * 8 + rl) * LDY + k + kl];
-#pragma unroll
-          for (int i = 0; i < MI; ++i)
-#pragma unroll
-            for (int jj = 0; jj < 2; ++jj) dmma8x8x4(acc[i][jj], af[i], bf[jj]);
-        }
-#pragma unroll
-        for (int i = 0; i < MI; ++i)
-#pragma unroll
-          for (int jj = 0; jj < 2; ++jj)
-#pragma unroll
-            for (int e = 0; e < 2; ++e) {
-              const int r = wm * WM + i * 8 + rl, c = wn * 16 + jj * 8 + kl * 2 + e;
-              if (r < rows && c < wcols)
-                Z[(r0 + r) + (long long)(c0 + c) * ldz] = sZ[c * LDZ + off + r] - acc[i][jj][e];
-            }
-      }
-      __syncthreads();
+    const long long st = ceil_div(n - 1 - s0, b);  // blocks with r0 <= n-1
+    return (int)(st < maxsteps ? st : maxsteps);
+  };
+  auto issue_vt = [&](int gi, int j, int stage) {
+    const size_t blk = (size_t)gi * maxsteps + j;
+    const double* gV = Vblk + blk * HB * G;
+    const double* gVT = VTblk + blk * HB * G;
+    double* sV = sm + stage * STAGE;
+    double* sVT = sV + G * LDV;
+    for (int idx = tid; idx < HB * G / 2; idx += blockDim.x) {
+      const int e = idx * 2;
+      const int r = e % HB, c = e / HB;
+      cp_async16(sV + c * LDV + r, gV + e, true);
+      cp_async16(sVT + c * LDV + r, gVT + e, true);
     }
+    cp_async_commit();
+  };
+  auto zaddr = [&](int row, int col) { return Z + row + (long long)col * ldz; };
+  auto zload = [&](int row, int col) -> double {
+    return (row < n && col < ncols) ? __ldcg(zaddr(row, col)) : 0.0;
+  };
+
+  double acc[12][2];
+  int gi = ngroups - 1, j = 0, stage = 0;
+  if (gi >= 0) issue_vt(gi, 0, 0);
+  bool group_start = true;
+  // invariant at the top of each iteration: the current block's V/VT is the
+  // newest committed group
+  while (gi >= 0) {
+    const int s0 = gi * G;
+    const int r0 = s0 + 1 + j * b;
+    const int steps = nsteps_of(gi);
+    const bool last = (j + 1 >= steps);
+    // next block in the flattened order -> its V/VT into the other stage
+    int ngi = gi, nj = j + 1;
+    if (last) { ngi = gi - 1; nj = 0; }
+    // cp.async groups in issue order: [new Z rows of this block] [next V/VT]
+    if (!last) {
+      const int rbase = r0 + HB;
+      for (int idx = tid; idx < 64 * kQ2W; idx += blockDim.x) {
+        const int rr = idx & 63, c = idx >> 6;
+        const int row = rbase + rr, col = blockIdx.x * kQ2W + c;
+        const bool ok = row < n && col < ncols;
+        cp_async8(sZn + c * LDN + rr, ok ? zaddr(row, col) : Z, ok);
+      }
+    }
+    cp_async_commit();
+    if (ngi >= 0) issue_vt(ngi, nj, stage ^ 1);
+    else cp_async_commit();
+    if (group_start) {
+#pragma unroll
+      for (int i = 0; i < 12; ++i)
+#pragma unroll
+        for (int e = 0; e < 2; ++e) acc[i][e] = zload(r0 + 8 * i + rl, cw + 2 * kl + e);
+      group_start = false;
+    }
+    cp_async_wait<2>();  // this block's V/VT (issued one iteration earlier)
+    __syncthreads();
+    const double* sV = sm + stage * STAGE;
+    const double* sVT = sV + G * LDV;
+    // Y (32 x 8) = V^T Z: reflector tile q (rows 8q..8q+7 of Y) only meets Z
+    // rows [8q, 8q + 71): k-steps t in [2q, 2q + 17]
+    double y[4][2];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) y[q][0] = y[q][1] = 0.0;
+#pragma unroll
+    for (int t = 0; t < 24; ++t) {
+      const double bf = bfrag(acc, t, lane);
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        if (t >= 2 * q && t <= 2 * q + 17) {
+          const double af = sV[(8 * q + rl) * LDV + 4 * t + kl];
+          dmma8x8x4(y[q], af, bf);
+        }
+      }
+    }
+    // Z (96 x 8) -= VT Y: VT[r][c] = 0 for c < r - 63 (rows >= 64 skip k-steps)
+#pragma unroll
+    for (int t = 0; t < 8; ++t) {
+      // B fragment of -Y (k = reflector 4t + lane%4, n = lane/4)
+      const int src = ((4 * (t & 1) + kl) << 2) + (rl >> 1);
+      const double v0 = __shfl_sync(0xffffffffu, y[t >> 1][0], src);
+      const double v1 = __shfl_sync(0xffffffffu, y[t >> 1][1], src);
+      const double bf = -((rl & 1) ? v1 : v0);
+#pragma unroll
+      for (int i = 0; i < 12; ++i) {
+        const int tmin = i < 8 ? 0 : (8 * i - 63) / 4;
+        if (t >= tmin) {
+          const double af = sVT[(4 * t + kl) * LDV + 8 * i + rl];
+          dmma8x8x4(acc[i], af, bf);
+        }
+      }
+    }
+    // retire rows: all 96 at the end of a group, else the first 64
+    const int nstore = last ? 12 : 8;
+#pragma unroll
+    for (int i = 0; i < 12; ++i) {
+      if (i < nstore) {
+        const int row = r0 + 8 * i + rl;
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          const int col = cw + 2 * kl + e;
+          if (row < n && col < ncols) *zaddr(row, col) = acc[i][e];
+        }
+      }
+    }
+    if (!last) {
+      cp_async_wait<1>();  // the prefetched rows (next V/VT may still be in flight)
+      __syncthreads();
+      const int cl = warp * 8;
+#pragma unroll
+      for (int i = 0; i < 4; ++i) { acc[i][0] = acc[8 + i][0]; acc[i][1] = acc[8 + i][1]; }
+#pragma unroll
+      for (int i = 0; i < 8; ++i)
+#pragma unroll
+        for (int e = 0; e < 2; ++e) acc[4 + i][e] = sZn[(cl + 2 * kl + e) * LDN + 8 * i + rl];
+    } else {
+      group_start = true;
+    }
+    __syncthreads();  // this stage's V/VT are free for the block after next
+    stage ^= 1;
+    gi = ngi;
+    j = nj;
   }
 }
 
@@ -236,17 +282,16 @@ cudaError_t q2_build(int n, int b, int g, const double* V2, const double* tau2, 
 cudaError_t q2_apply(int n, int b, int g, const double* Vblk, const double* VTblk, double* Z,
                      long long ldz, int ncols, cudaStream_t s) {
   if (n <= 2 || ncols <= 0) return cudaSuccess;
-  if (b != 64 || g != kQ2G) return cudaErrorInvalidValue;
-  constexpr int HB = 96, G = kQ2G;  // q2_hb(64, 32)
+  if (b != 64 || g != kQ2G || q2_hb(b, g) != kQ2HB) return cudaErrorInvalidValue;
   const int maxsteps = sb2st_maxsteps(n, b);
-  const size_t smem = sizeof(double) * (2 * (size_t)G * (HB + 4) + (size_t)kQ2W * (HB + 4));
+  const size_t smem = sizeof(double) * (2 * (2 * (size_t)kQ2G * (kQ2HB + 4)) + (size_t)kQ2W * 68);
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(q2_apply_kernel<HB, G>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaFuncSetAttribute(q2_apply_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     attr = true;
   }
-  q2_apply_kernel<HB, G><<<(unsigned)ceil_div(ncols, kQ2W), kQ2Threads, smem, s>>>(
-      n, b, maxsteps, Vblk, VTblk, Z, ldz, ncols);
+  q2_apply_kernel<<<(unsigned)ceil_div(ncols, kQ2W), kQ2Threads, smem, s>>>(
+      n, b, maxsteps, Vblk, VTblk, Z, ldz, ncols, nullptr);
   count_launch();
   return cudaGetLastError();
 }
