@@ -95,14 +95,26 @@ __global__ void __launch_bounds__(kPanelThreads) panel_qr_kernel(
         if (gr > j) tail += xj * xj;
       }
     }
-    // warp reduction of the 65 values, then per-warp partials to smem
+    // warp reduce-scatter butterfly over the 64 products (62 shuffles per
+    // lane instead of 64 full reductions): after step o the lanes with bit o
+    // set keep the upper half of the remaining values
 #pragma unroll
-    for (int k = 0; k < kMaxPanel; ++k) pk[k] = warp_sum(pk[k]);
+    for (int h = kMaxPanel / 2, o = 16; o >= 1; h >>= 1, o >>= 1) {
+      const bool up = (lane & o) != 0;
+#pragma unroll
+      for (int i = 0; i < h; ++i) {
+        const double send = up ? pk[i] : pk[i + h];
+        const double keep = up ? pk[i + h] : pk[i];
+        pk[i] = keep + __shfl_xor_sync(0xffffffffu, send, o);
+      }
+    }
     tail = warp_sum(tail);
-    if (lane == 0) {
-#pragma unroll
-      for (int k = 0; k < kMaxPanel; ++k) wpart[warp * L + 2 + k] = pk[k];
-      wpart[warp * L] = tail;
+    {
+      const int base = ((lane >> 4) & 1) * 32 + ((lane >> 3) & 1) * 16 + ((lane >> 2) & 1) * 8 +
+                       ((lane >> 1) & 1) * 4 + (lane & 1) * 2;
+      wpart[warp * L + 2 + base] = pk[0];
+      wpart[warp * L + 2 + base + 1] = pk[1];
+      if (lane == 0) wpart[warp * L] = tail;
     }
     __syncthreads();
     // CTA partial: [0] tail, [1] x0 (owner), [2+k] dots, [2+bw+k] owner's row j
