@@ -305,6 +305,19 @@ def run_ours(args):
     # sanity: eigenvalues positive, descending
     lam_h = lam.cpu().numpy()
     ok = bool(np.all(lam_h > 0) and np.all(np.diff(lam_h) <= 0))
+    # size-independent verification of the last timed solve (outside the timed
+    # region): per-pair residual / (lam_max ||x||) and ||X1^T X1 - X2^T X2 - I||_F
+    verification = None
+    if not args.no_verify:
+        from paper_1501_03830_b200.verify import pair_residuals_device
+        res, xn, bio = pair_residuals_device(n, Mt, ld, Kt, ld, lam, X1, ld, X2, ld)
+        verification = {"max_pair_residual": (res / (lam[0] * xn)).max().item(),
+                        "biorthogonality_fro": bio.item(),
+                        "gate": "<= 1e-13 n and <= 1e-12 n (SURVEY 8c(8))"}
+        verification["pass"] = bool(verification["max_pair_residual"] <= 1e-13 * n and
+                                    verification["biorthogonality_fro"] <= 1e-12 * n)
+        del res, xn
+        torch.cuda.empty_cache()
 
     # ---- e2e: public C-ABI host entry, pinned host buffers, copies inside ----
     e2e = None
@@ -376,6 +389,7 @@ def run_ours(args):
         "gpu_launches": int(launches),
         "clocks": clk,
         "sanity_lambda_positive_desc": ok,
+        "verification": verification,
     }
     print(json.dumps(line), flush=True)
     if world > 1:
@@ -392,6 +406,7 @@ def main():
     ap.add_argument("--n", type=int, default=16384)
     ap.add_argument("--e2e-steps", type=int, default=1)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-verify", action="store_true")
     ap.add_argument("--config", type=int, default=2, choices=[1, 2],
                     help="2 (default): real n=16384 headline; 1: complex n=2048 side line")
     args = ap.parse_args()

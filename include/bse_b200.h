@@ -18,6 +18,8 @@
  *   bse_stedc_dev          kernels.tridiag_eig      pkg/src/bse/kernels.py:460-535
  *   bse_absorption_dev     spectra.absorption_spectrum
  *                                                   pkg/src/bse/spectra.py:120-151
+ *   bse_pair_residuals_dev core.residual_metrics    pkg/src/bse/core.py:281-294
+ *                          (per-pair form, no dense H / Y: SURVEY 8c(8))
  *
  * Conventions: all matrices are column-major FP64 with explicit leading
  * dimensions; "_dev" functions take device pointers and a cudaStream_t passed
@@ -105,6 +107,20 @@ int bse_absorption_dev(int64_t n, const double* dLam, const double* dX1c, int64_
                        const double* dX2c, int64_t ldx2, const double* dDr, const double* dDl,
                        int64_t ngrid, const double* dGrid, double sigma, double* dWeights,
                        double* dValues, double* dDefect, double* dMinPair, void* stream);
+
+/* Verification without the 2n x 2n H or Y (core.residual_metrics,
+ * core.py:281-294, in the per-pair form of SURVEY 8c(8)).  For a real
+ * solution of (M, K) (lower triangles referenced):
+ *   dRes[j]   = || H [x1_j; x2_j] - lam_j [x1_j; x2_j] ||_2,  H = [[A, B], [-B, -A]]
+ *   dXnorm[j] = || [x1_j; x2_j] ||_2
+ *   *dBio     = || X1^T X1 - X2^T X2 - I ||_F
+ * Cost 6 n^3 flops (two SYMMs and one GEMM); workspace from
+ * bse_residual_workspace_bytes. */
+size_t bse_residual_workspace_bytes(int64_t n);
+int bse_pair_residuals_dev(int64_t n, const double* dM, int64_t ldm, const double* dK, int64_t ldk,
+                           const double* dLam, const double* dX1, int64_t ldx1, const double* dX2,
+                           int64_t ldx2, double* dRes, double* dXnorm, double* dBio, void* dWork,
+                           size_t work_bytes, void* stream);
 
 /* Building blocks exposed for tests. */
 int bse_gemm_dev(int transA, int transB, int64_t M, int64_t N, int64_t K, double alpha,

@@ -8,6 +8,7 @@ the CUDA library libbse_b200.so (C ABI: include/bse_b200.h).
 from .solvers import (hermitian_eigvals, polish, real_embedding, solve_complex, solve_pair_device,
                       solve_real, syevd_values_device, tda_gap_report)
 from .spectra import absorption_device, absorption_spectrum
+from .verify import PairResidualReport, pair_residual_report, pair_residuals_device
 from .types import (BseOperator, ConvergenceError, DipoleData, FullEigensystem,
                     NotPositiveDefinite, PositiveEigensystem, SpectrumCurve, TdaGapReport,
                     ValidationReport,
@@ -23,5 +24,6 @@ __all__ = [
     "DipoleData", "SpectrumCurve", "absorption_spectrum", "default_grid", "dos_dominance",
     "conditioning_warnings", "real_embedding", "polish", "solve_pair_device",
     "absorption_device", "hermitian_eigvals", "tda_gap_report", "TdaGapReport",
-    "syevd_values_device", "__version__",
+    "syevd_values_device", "PairResidualReport", "pair_residual_report",
+    "pair_residuals_device", "__version__",
 ]

@@ -49,6 +49,9 @@ SIGNATURES = {
     "bse_stedc_dev": (_INT, [_I64, _P, _P, _P, _I64, _P, C.c_size_t, _P]),
     "bse_absorption_dev": (_INT, [_I64, _P, _P, _I64, _P, _I64, _P, _P, _I64, _P, _D, _P, _P,
                                   _P, _P, _P]),
+    "bse_residual_workspace_bytes": (C.c_size_t, [_I64]),
+    "bse_pair_residuals_dev": (_INT, [_I64, _P, _I64, _P, _I64, _P, _P, _I64, _P, _I64, _P, _P,
+                                      _P, _P, C.c_size_t, _P]),
     "bse_gemm_dev": (_INT, [_INT, _INT, _I64, _I64, _I64, _D, _P, _I64, _P, _I64, _D, _P, _I64,
                             _P, _P]),
     "bse_trsm_dev": (_INT, [_INT, _I64, _P, _I64, _P, _I64, _I64, _P]),

@@ -234,6 +234,22 @@ int bse_absorption_dev(int64_t n, const double* dLam, const double* dX1c, int64_
   return BSE_OK;
 }
 
+size_t bse_residual_workspace_bytes(int64_t n) { return n > 0 ? bse::verify_bytes((int)n) : 0; }
+
+int bse_pair_residuals_dev(int64_t n, const double* dM, int64_t ldm, const double* dK, int64_t ldk,
+                           const double* dLam, const double* dX1, int64_t ldx1, const double* dX2,
+                           int64_t ldx2, double* dRes, double* dXnorm, double* dBio, void* dWork,
+                           size_t work_bytes, void* stream) {
+  if (n < 0 || (n > 0 && (ldm < n || ldk < n || ldx1 < n || ldx2 < n)))
+    return fail(BSE_BAD_ARGUMENT, "bad dimension");
+  if (n == 0) return BSE_OK;
+  if (work_bytes < bse::verify_bytes((int)n)) return fail(BSE_BAD_ARGUMENT, "workspace too small");
+  BSE_TRY_CUDA(bse::pair_residuals((int)n, dM, ldm, dK, ldk, dLam, dX1, ldx1, dX2, ldx2, dRes,
+                                   dXnorm, dBio, dWork, work_bytes, (cudaStream_t)stream),
+               "pair_residuals");
+  return BSE_OK;
+}
+
 int bse_profile_enable(int on) {
   bse::StageLog& L = bse::stage_log();
   L.on = on != 0;

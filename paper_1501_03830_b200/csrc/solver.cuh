@@ -47,4 +47,12 @@ cudaError_t absorption(int n, const double* lam, const double* X1c, long long ld
                        int ngrid, const double* grid, double sigma, double* weights,
                        double* values, double* defect, double* minpair, cudaStream_t s);
 
+// Per-pair residuals / biorthogonality defect of a real product-form solution
+// (verify.cu).
+size_t verify_bytes(int n);
+cudaError_t pair_residuals(int n, const double* M, long long ldm, const double* K, long long ldk,
+                           const double* lam, const double* X1, long long ldx1, const double* X2,
+                           long long ldx2, double* res, double* xn, double* bio, void* work,
+                           size_t work_bytes, cudaStream_t s);
+
 }  // namespace bse
