@@ -254,6 +254,193 @@ __global__ void __launch_bounds__(kQ2Threads, 1) q2_apply_kernel(int n, int b, i
   }
 }
 
+// Paired-group variant (default).  Two consecutive sweep groups (ga = gi,
+// gb = gi - 1) walk down the rows together: at chase step j, block (ga, j)
+// covers rows [B0 + 64j + 32, +96) and block (gb, j) rows [B0 + 64j, +96)
+// (B0 = gb*G + 1).  (gb, j) only overlaps (ga, j') for j' <= j, so the order
+// (ga, 0), (gb, 0), (ga, 1), (gb, 1), ... respects Q2's application order.
+// Each warp keeps the 128-row window of its 8 columns in registers and
+// streams 64 rows in and out per STEP instead of per block: half the Z
+// traffic and half the row-streaming stalls of the single-group walk.
+template <int OFF, int NT>
+BSE_DEV void q2_block_at(double (&acc)[NT][2], const double* sV, const double* sVT, int lane) {
+  constexpr int LDV = kQ2HB + 4;
+  const int kl = lane & 3, rl = lane >> 2;
+  double y[4][2];
+#pragma unroll
+  for (int q = 0; q < 4; ++q) y[q][0] = y[q][1] = 0.0;
+#pragma unroll
+  for (int t = 0; t < 24; ++t) {
+    const int src = ((4 * (t & 1) + kl) << 2) + (rl >> 1);
+    const double v0 = __shfl_sync(0xffffffffu, acc[OFF + (t >> 1)][0], src);
+    const double v1 = __shfl_sync(0xffffffffu, acc[OFF + (t >> 1)][1], src);
+    const double bf = (rl & 1) ? v1 : v0;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      if (t >= 2 * q && t <= 2 * q + 17) {
+        const double af = sV[(8 * q + rl) * LDV + 4 * t + kl];
+        dmma8x8x4(y[q], af, bf);
+      }
+    }
+  }
+#pragma unroll
+  for (int t = 0; t < 8; ++t) {
+    const int src = ((4 * (t & 1) + kl) << 2) + (rl >> 1);
+    const double v0 = __shfl_sync(0xffffffffu, y[t >> 1][0], src);
+    const double v1 = __shfl_sync(0xffffffffu, y[t >> 1][1], src);
+    const double bf = -((rl & 1) ? v1 : v0);
+#pragma unroll
+    for (int i = 0; i < 12; ++i) {
+      const int tmin = i < 8 ? 0 : (8 * i - 63) / 4;
+      if (t >= tmin) {
+        const double af = sVT[(4 * t + kl) * LDV + 8 * i + rl];
+        dmma8x8x4(acc[OFF + i], af, bf);
+      }
+    }
+  }
+}
+
+template <int P>
+__global__ void __launch_bounds__(kQ2Threads, 1) q2_apply_pair_kernel(int n, int b, int maxsteps,
+                                                                      const double* __restrict__ Vblk,
+                                                                      const double* __restrict__ VTblk,
+                                                                      double* __restrict__ Z,
+                                                                      long long ldz, int ncols) {
+  constexpr int HB = kQ2HB, G = kQ2G;
+  constexpr int LDV = HB + 4;
+  constexpr int STAGE = 2 * G * LDV;
+  constexpr int LDN = 64 + 2;  // == 2 mod 8: conflict-free C-layout reloads
+  constexpr int NT = 4 * P + 8;  // 8-row tiles in the window
+  extern __shared__ __align__(16) double sm[];
+  double* sZn = sm + 2 * STAGE;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int kl = lane & 3, rl = lane >> 2;
+  const int cw = blockIdx.x * kQ2W + warp * 8;
+  const int nsweeps = n - 2;
+  const int ngroups = (int)ceil_div(nsweeps, G);
+
+  auto steps_of = [&](int gi) -> int {
+    if (gi < 0) return 0;
+    const long long st = ceil_div(n - 1 - gi * G, b);
+    return (int)(st < maxsteps ? st : maxsteps);
+  };
+  // blocks of group ga - wh exist for j < steps; the earliest group of the
+  // set (ga - P + 1) has the most steps
+  auto smax_of = [&](int ga) { return steps_of(max(ga - P + 1, 0)); };
+  // next existing block after (ga, j, wh); false when the walk is done
+  auto advance = [&](int& ga, int& j, int& wh) -> bool {
+    for (;;) {
+      if (wh + 1 < P) ++wh;
+      else { wh = 0; ++j; }
+      if (j >= smax_of(ga)) {
+        ga -= P;
+        j = 0;
+        wh = 0;
+        return ga >= 0;
+      }
+      if (ga - wh >= 0 && j < steps_of(ga - wh)) return true;
+    }
+  };
+  auto issue_vt = [&](int gi, int j, int stage) {
+    const size_t blk = (size_t)gi * maxsteps + j;
+    const double* gV = Vblk + blk * HB * G;
+    const double* gVT = VTblk + blk * HB * G;
+    double* sV = sm + stage * STAGE;
+    double* sVT = sV + G * LDV;
+    for (int idx = tid; idx < HB * G / 2; idx += blockDim.x) {
+      const int e = idx * 2;
+      const int r = e % HB, c = e / HB;
+      cp_async16(sV + c * LDV + r, gV + e, true);
+      cp_async16(sVT + c * LDV + r, gVT + e, true);
+    }
+    cp_async_commit();
+  };
+  auto zaddr = [&](int row, int col) { return Z + row + (long long)col * ldz; };
+  auto zok = [&](int row, int col) { return row >= 0 && row < n && col < ncols; };
+
+  double acc[NT][2];
+  int ga = ngroups - 1, j = 0, wh = 0, stage = 0;
+  if (ga < 0) return;
+  issue_vt(ga, 0, 0);
+  bool pair_start = true;
+  for (;;) {
+    const int B0 = (ga - P + 1) * G + 1;
+    int nga = ga, nj = j, nwh = wh;
+    const bool more = advance(nga, nj, nwh);
+    const bool step_end = !more || nga != ga || nj != j;
+    const bool pair_end = !more || nga != ga;
+    // first block of step j: prefetch the 64 rows step j+1 brings in
+    bool step_first = true;
+    for (int m = 0; m < wh; ++m)
+      if (j < steps_of(ga - m)) step_first = false;
+    const int smax = smax_of(ga);
+    if (step_first && j + 1 < smax) {
+      const int rbase = B0 + 64 * j + 8 * NT;
+      for (int idx = tid; idx < 64 * kQ2W; idx += blockDim.x) {
+        const int rr = idx & 63, c = idx >> 6;
+        const int row = rbase + rr, col = blockIdx.x * kQ2W + c;
+        const bool ok = zok(row, col);
+        cp_async8(sZn + c * LDN + rr, ok ? zaddr(row, col) : Z, ok);
+      }
+    }
+    cp_async_commit();
+    if (more) issue_vt(nga - nwh, nj, stage ^ 1);
+    else cp_async_commit();
+    if (pair_start) {
+#pragma unroll
+      for (int i = 0; i < NT; ++i)
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          const int row = B0 + 8 * i + rl, col = cw + 2 * kl + e;
+          acc[i][e] = zok(row, col) ? __ldcg(zaddr(row, col)) : 0.0;
+        }
+      pair_start = false;
+    }
+    cp_async_wait<2>();
+    __syncthreads();
+    const double* sV = sm + stage * STAGE;
+    const double* sVT = sV + G * LDV;
+    // group ga - wh's block sits 32 (P - 1 - wh) rows into the window
+    if (P == 1 || wh == 0) q2_block_at<4 * (P - 1), NT>(acc, sV, sVT, lane);
+    else if (P == 2 || wh == 1) q2_block_at<4 * (P > 1 ? P - 2 : 0), NT>(acc, sV, sVT, lane);
+    else if (P == 3 || wh == 2) q2_block_at<4 * (P > 2 ? P - 3 : 0), NT>(acc, sV, sVT, lane);
+    else q2_block_at<4 * (P > 3 ? P - 4 : 0), NT>(acc, sV, sVT, lane);
+    if (step_end) {
+      const int nstore = pair_end ? NT : 8;
+      const int rbase = B0 + 64 * j;
+#pragma unroll
+      for (int i = 0; i < NT; ++i) {
+        if (i < nstore) {
+#pragma unroll
+          for (int e = 0; e < 2; ++e) {
+            const int row = rbase + 8 * i + rl, col = cw + 2 * kl + e;
+            if (zok(row, col)) *zaddr(row, col) = acc[i][e];
+          }
+        }
+      }
+      if (!pair_end) {
+        cp_async_wait<1>();
+        __syncthreads();
+        const int cl = warp * 8;
+#pragma unroll
+        for (int i = 0; i < NT - 8; ++i) { acc[i][0] = acc[8 + i][0]; acc[i][1] = acc[8 + i][1]; }
+#pragma unroll
+        for (int i = 0; i < 8; ++i)
+#pragma unroll
+          for (int e = 0; e < 2; ++e) acc[NT - 8 + i][e] = sZn[(cl + 2 * kl + e) * LDN + 8 * i + rl];
+      } else {
+        pair_start = true;
+      }
+    }
+    __syncthreads();
+    stage ^= 1;
+    if (!more) break;
+    ga = nga;
+    j = nj;
+    wh = nwh;
+  }
+}
+
 }  // namespace
 
 size_t q2_block_doubles(int n, int b, int g) {
@@ -288,10 +475,18 @@ cudaError_t q2_apply(int n, int b, int g, const double* Vblk, const double* VTbl
   static bool attr = false;
   if (!attr) {
     cudaFuncSetAttribute(q2_apply_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaFuncSetAttribute(q2_apply_pair_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     attr = true;
   }
-  q2_apply_kernel<<<(unsigned)ceil_div(ncols, kQ2W), kQ2Threads, smem, s>>>(
-      n, b, maxsteps, Vblk, VTblk, Z, ldz, ncols, nullptr);
+  static const int variant = [] {
+    const char* v = std::getenv("BSE_Q2_VARIANT");
+    return v ? std::atoi(v) : 0;
+  }();
+  const unsigned grid = (unsigned)ceil_div(ncols, kQ2W);
+  if (variant == 1)
+    q2_apply_kernel<<<grid, kQ2Threads, smem, s>>>(n, b, maxsteps, Vblk, VTblk, Z, ldz, ncols, nullptr);
+  else
+    q2_apply_pair_kernel<2><<<grid, kQ2Threads, smem, s>>>(n, b, maxsteps, Vblk, VTblk, Z, ldz, ncols);
   count_launch();
   return cudaGetLastError();
 }

@@ -73,14 +73,14 @@ SyevdWork carve_syevd(Arena& a, int n) {
   w.sc.splitk_ws = a.take<double>(64 * (size_t)b * b);
   w.sc.symm_ws = a.take<double>((size_t)kSymmSplits * ld * b);
   w.sc.probs = a.take<GemmProblem>(96);
-  w.ldab = 2 * b;
+  w.ldab = 2 * b + 1;  // element (i, j) at 128 j + i: 2-D tiles with a 1 KB stride
   w.AB = a.take<double>((size_t)w.ldab * n);
   w.d = a.take<double>(n);
   w.e = a.take<double>(n);
   const int maxsteps = sb2st_maxsteps(n, b);
   w.V2 = a.take<double>((size_t)n * maxsteps * b);
   w.tau2 = a.take<double>((size_t)n * maxsteps);
-  w.progress = a.take<int>(n);
+  w.progress = a.take<int>(2 * (size_t)n);  // full + late counters (sb2st)
   const size_t qb = q2_block_doubles(n, b, kQ2Group);
   w.Vblk = a.take<double>(qb);
   w.VTblk = a.take<double>(qb);

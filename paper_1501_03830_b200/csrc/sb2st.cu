@@ -262,6 +262,374 @@ __global__ void __launch_bounds__(kSbThreads) sb2st_kernel(double* AB, int ldab,
   (void)warp;
 }
 
+// ---------------------------------------------------------------------------
+// Fused step (default).  One step of sweep s works on the lq x lq symmetric
+// block D at (q0, q0) and the lq x lp block O at (q0, p0) below the previous
+// block, with v/tau the previous step's reflector:
+//   A: w  = tau O v                          (right apply O' = O - w v^T)
+//   B: vn = house(O'[:, 0])                   (every warp, redundantly)
+//   C: t  = taun D vn, y = taun (O^T vn - v (w^T vn))
+//   D: O'' = O - w v^T - vn y^T, D'' = D - vn w2^T - w2 vn^T, w2 = t - (taun/2)(t^T vn) vn
+// Step 0 is the same step with O = column s (lp = 1) and tau = 0.
+//
+// Cross-sweep protocol (two counters per sweep).  Step j of sweep s reads,
+// from sweep s-1, only D's last row and O(lq-1, lp-1) as written by its step
+// j+1 -- exactly that step's row-0 outputs -- and everything else as left by
+// its step j.  So each step publishes its row 0 first on `late` (warp 0),
+// then every warp stores its share of the bulk and counts itself on `full`
+// after its own fence.  A consumer issues
+// the bulk staging as soon as `full` allows and overlaps it with the wait for
+// `late`.
+//
+// Band layout: ldab = 2b + 1, so element (i, j) sits at linear 128 j + i and
+// every block is a plain 2-D tile with a 1 KB stride: staging and stores use
+// 16-byte accesses on rows with (q0 + r) even.  Shared blocks use an even
+// leading dimension (66) shifted by q0 & 1 so the parities line up, and the
+// matvec index patterns below are bank-conflict free for that stride.
+constexpr int kLd2 = 66;
+constexpr int kPairSlots = 34;  // 16-byte row-pair slots per column (33 used)
+constexpr int kBulkWarps = kSbThreads / 32;  // every warp stores part of the bulk
+
+struct SbfSmem {
+  double D[kMaxPanel * kLd2 + 2];
+  double O[kMaxPanel * kLd2 + 2];
+  double vbuf[2][kMaxPanel];
+  double vnw[kSbThreads / 32][kMaxPanel];
+  double w[kMaxPanel];
+  double y[kMaxPanel];
+  double tt[kMaxPanel];
+};
+
+// phase A (lanes: 4 rows x 4 quarters per half-warp) column pattern
+BSE_DEV int colA(int q, int i) { return 8 * (i >> 1) + 2 * q + (i & 1); }
+// phase C (lanes: 4 columns x 4 quarters per half-warp) row pattern
+BSE_DEV int rowC(int q, int i) { return 16 * (i >> 2) + 2 * (i & 3) + (q & 1) + 8 * (q >> 1); }
+
+// Acquire-poll one counter (thread 0).  No barrier.
+BSE_DEV void poll_counter(const int* ctr, int need) {
+  if (ld_relaxed(ctr) < need) {
+    while (ld_relaxed(ctr) < need) {
+    }
+  }
+  if (!(c_sb_flags & 32)) fence_acquire();
+}
+
+// 16-byte L2-only async copy of `bytes` (0, 8 or 16) with zero fill: band
+// lines never enter L1, so no stale-L1 hazard across CTAs.
+BSE_DEV void cp_async16_n(void* smem, const void* gmem, int bytes) {
+  unsigned sa = static_cast<unsigned>(__cvta_generic_to_shared(smem));
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(sa), "l"(gmem), "r"(bytes));
+}
+
+BSE_DEV void st_global_v2(double* p, double a, double b) {
+  asm volatile("st.global.v2.f64 [%0], {%1, %2};\n" ::"l"(p), "d"(a), "d"(b) : "memory");
+}
+
+BSE_DEV void stage_split(SbfSmem& sm, const double* AB, int ldab, int q0, int lq, int p0, int lp,
+                         const int* full_pred, const int* late_pred, int j, bool has_pred,
+                         unsigned long long* tr) {
+  const int tid = threadIdx.x;
+  if (has_pred && tid == 0) poll_counter(full_pred, kBulkWarps * (j + 1));
+  __syncthreads();  // also: previous step's smem reads are done
+  if (tr && tid == 0) tr[1] = gtimer();
+  const int sh = q0 & 1;
+  double* Db = sm.D + sh;
+  double* Ob = sm.O + sh;
+  if (lq == kMaxPanel && lp == kMaxPanel) {
+    // full blocks: 4 threads per column, 16-byte row pairs, no zero fill
+    // (D's strict upper triangle is mirrored below; late rows are reloaded)
+    const int c = tid >> 2, kq = tid & 3;
+    const double* osrc = AB + (long long)(p0 + c) * ldab + (q0 - p0 - c);
+    const double* dsrc = AB + (long long)(q0 + c) * ldab - c;
+    double* od = Ob + c * kLd2;
+    double* dd = Db + c * kLd2;
+#pragma unroll
+    for (int i = 0; i < 9; ++i) {
+      const int k = kq + 4 * i;
+      if (k <= 32) {
+        const int r0 = 2 * k - sh;
+        const int bytes = k < 32 ? 16 : (sh ? 8 : 0);
+        if (bytes) {
+          cp_async16_n(od + r0, osrc + r0, bytes);
+          if (r0 + 1 >= c) cp_async16_n(dd + r0, dsrc + r0, bytes);
+        }
+      }
+    }
+  } else {
+    constexpr int kTotal = 2 * kMaxPanel * kPairSlots;
+  #pragma unroll 2
+    for (int t = tid; t < kTotal; t += kSbThreads) {
+      const bool isO = t >= kMaxPanel * kPairSlots;
+      const int u = isO ? t - kMaxPanel * kPairSlots : t;
+      const int c = u / kPairSlots, k = u - kPairSlots * c;
+      const int r0 = 2 * k - sh;
+      if (r0 >= kMaxPanel) continue;
+      double* dst = (isO ? Ob : Db) + c * kLd2 + r0;
+      const double* src = isO ? AB + (long long)(p0 + c) * ldab + (q0 + r0 - p0 - c)
+                              : AB + (long long)(q0 + c) * ldab + (r0 - c);
+      // need: the row must come from this copy (late positions included: they
+      // are overwritten after the late wait); zero: the row must read 0; all
+      // other rows (row -1/64 padding, D's upper triangle) are don't-care.
+      const int r1 = r0 + 1;
+      bool need0, need1, zero0, zero1;
+      if (isO) {
+        need0 = r0 >= 0 && r0 < lq && c < lp;
+        need1 = r1 < kMaxPanel && r1 < lq && c < lp;
+        zero0 = r0 >= 0 && !need0;
+        zero1 = r1 < kMaxPanel && !need1;
+      } else {
+        need0 = r0 >= 0 && r0 >= c && r0 < lq;
+        need1 = r1 < kMaxPanel && r1 >= c && r1 < lq;
+        zero0 = r0 >= 0 && r0 >= c && !need0;
+        zero1 = r1 < kMaxPanel && r1 >= c && !need1;
+      }
+      int bytes;
+      if (need1) bytes = 16;            // r0 needed or don't-care
+      else if (need0) bytes = 8;        // r1 zero-filled or don't-care
+      else if (zero0 || zero1) bytes = 0;
+      else continue;
+      cp_async16_n(dst, bytes ? src : AB, bytes);
+    }
+  }
+  cp_async_commit();
+  if (tr && tid == 0) tr[2] = gtimer();
+  cp_async_wait<0>();
+  __syncthreads();
+  // mirror D's strict upper triangle from the lower one (except the late row)
+  const int rl = lq - 1;
+#pragma unroll 4
+  for (int k = 0; k < kSlots; ++k) {
+    const int idx = tid + k * kSbThreads;
+    const int r = idx & (kMaxPanel - 1), c = idx >> 6;
+    if (r < c && c != rl) Db[c * kLd2 + r] = Db[r * kLd2 + c];
+  }
+  if (has_pred && tid == 0) poll_counter(late_pred, j + 2);
+  __syncthreads();
+  if (tr && tid == 0) tr[3] = gtimer();
+  if (tid < kMaxPanel) {
+    const int c = tid;
+    const double x = c <= rl ? __ldcg(AB + (long long)(q0 + c) * ldab + (rl - c)) : 0.0;
+    Db[c * kLd2 + rl] = x;
+    Db[rl * kLd2 + c] = x;
+  } else if (tid == kMaxPanel) {
+    Ob[(lp - 1) * kLd2 + rl] = __ldcg(AB + (long long)(p0 + lp - 1) * ldab + (q0 + rl - p0 - lp + 1));
+  }
+  __syncthreads();
+}
+
+__global__ void __launch_bounds__(kSbThreads) sb2st_fused_kernel(double* AB, int ldab, int n,
+                                                                 int b, double* V2, double* tau2,
+                                                                 int maxsteps, int* progress,
+                                                                 unsigned long long* trace) {
+  extern __shared__ __align__(16) unsigned char raw[];
+  SbfSmem& sm = *reinterpret_cast<SbfSmem*>(raw);
+  const int tid = threadIdx.x;
+  const int lane = tid & 31, warp = tid >> 5;
+  const int mi = warp * 8 + (lane >> 2);  // row (A) / column (C) owned by this quarter-thread
+  const int q = lane & 3;
+  const bool tr = trace != nullptr && blockIdx.x < 2 && threadIdx.x == 0;
+  int tcount = 0;
+  auto T = [&](int slot) { trace[(blockIdx.x * (long long)maxsteps + tcount) * 16 + slot] = gtimer(); };
+  int* full = progress;
+  int* late = progress + n;
+  if (tid < kMaxPanel) sm.vbuf[0][tid] = sm.vbuf[1][tid] = 0.0;
+
+  for (int s = blockIdx.x; s < n - 2; s += gridDim.x) {
+    const bool trs = tr && s < 2;
+    int p0 = s, p1 = s, lp = 1;
+    double tau = 0.0;
+    for (int j = 0;; ++j) {
+      const int q0 = p1 + 1;
+      if (q0 > n - 1) break;
+      const int q1 = min(p1 + b, n - 1);
+      const int lq = q1 - q0 + 1;
+      const int sh = q0 & 1;
+      const double* Db = sm.D + sh;
+      const double* Ob = sm.O + sh;
+      const double* v = sm.vbuf[j & 1];
+      if (trs) T(0);
+      stage_split(sm, AB, ldab, q0, lq, p0, lp, full + s - 1, late + s - 1, j, s > 0, trs ? trace + (blockIdx.x * (long long)maxsteps + tcount) * 16 : nullptr);
+      if (trs) T(4);
+      // A: w = tau O v
+      {
+        double a = 0.0;
+        if (tau != 0.0) {
+#pragma unroll
+          for (int i = 0; i < 16; ++i) {
+            const int c = colA(q, i);
+            a += Ob[c * kLd2 + mi] * v[c];
+          }
+          a += __shfl_xor_sync(0xffffffffu, a, 1);
+          a += __shfl_xor_sync(0xffffffffu, a, 2);
+        }
+        if (q == 0) sm.w[mi] = tau * a;
+      }
+      __syncthreads();
+      if (trs) T(5);
+      // B: vn = house(O[:, 0] - w), per warp
+      double* vn = sm.vnw[warp];
+      double taun = 0.0, betan;
+      double swv;
+      {
+        const double x0 = lane < lq ? Ob[lane] - sm.w[lane] : 0.0;
+        const double x1 = lane + 32 < lq ? Ob[lane + 32] - sm.w[lane + 32] : 0.0;
+        const double ss = warp_sum((lane >= 1 ? x0 * x0 : 0.0) + x1 * x1);
+        const double alpha = __shfl_sync(0xffffffffu, x0, 0);
+        betan = alpha;
+        double scale = 0.0;
+        if (ss > 0.0) {
+          betan = -copysign(sqrt(alpha * alpha + ss), alpha);
+          taun = (betan - alpha) / betan;
+          scale = 1.0 / (alpha - betan);
+        }
+        const double vn0 = lane == 0 ? 1.0 : x0 * scale;
+        const double vn1 = x1 * scale;
+        vn[lane] = vn0;
+        vn[lane + 32] = vn1;
+        swv = warp_sum(sm.w[lane] * vn0 + sm.w[lane + 32] * vn1);
+        __syncwarp();
+      }
+      if (trs) T(6);
+      // C: t = taun D vn, y = taun (O^T vn - v swv)
+      {
+        double tc = 0.0, gc = 0.0;
+#pragma unroll
+        for (int i = 0; i < 16; ++i) {
+          const int r = rowC(q, i);
+          const double vr = vn[r];
+          tc += Db[mi * kLd2 + r] * vr;
+          gc += Ob[mi * kLd2 + r] * vr;
+        }
+        tc += __shfl_xor_sync(0xffffffffu, tc, 1);
+        tc += __shfl_xor_sync(0xffffffffu, tc, 2);
+        gc += __shfl_xor_sync(0xffffffffu, gc, 1);
+        gc += __shfl_xor_sync(0xffffffffu, gc, 2);
+        if (q == 0) {
+          sm.tt[mi] = taun * tc;
+          sm.y[mi] = taun * (gc - v[mi] * swv);
+        }
+      }
+      __syncthreads();
+      if (trs) T(7);
+      // D: warp 0 publishes row 0 of O'' and D''(0, 0) (the successor's late
+      // data); then every warp stores its share of the rest (16-byte row pairs).
+      {
+        const double gm = warp_sum(sm.tt[lane] * vn[lane] + sm.tt[lane + 32] * vn[lane + 32]);
+        const double al = -0.5 * taun * gm;
+        if (warp == 0) {
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            const int c = lane + 32 * h;
+            if (c < lp) {
+              const double val = c == 0 ? betan : Ob[c * kLd2] - sm.w[0] * v[c] - sm.y[c];
+              AB[(long long)(p0 + c) * ldab + (q0 - p0 - c)] = val;
+            }
+          }
+          if (lane == 0) AB[(long long)q0 * ldab] = Db[0] - 2.0 * (sm.tt[0] + al);
+          __syncwarp();
+          if (lane == 0) {
+            __threadfence();
+            st_release(late + s, j + 1);
+            if (trs) T(8);
+          }
+        }
+        if (warp == 1) {
+          V2[((long long)s * maxsteps + j) * b + lane] = vn[lane];
+          V2[((long long)s * maxsteps + j) * b + lane + 32] = vn[lane + 32];
+          sm.vbuf[(j + 1) & 1][lane] = vn[lane];
+          sm.vbuf[(j + 1) & 1][lane + 32] = vn[lane + 32];
+          if (lane == 0) tau2[(long long)s * maxsteps + j] = taun;
+        }
+        if (lq == kMaxPanel && lp == kMaxPanel) {
+          // 4 threads per column; warp 0 (late from publishing) gets the
+          // columns with the shortest D segments
+          const int c = kMaxPanel - 1 - (tid >> 2), kq = tid & 3;
+          double* od = AB + (long long)(p0 + c) * ldab + (q0 - p0 - c);
+          double* dd = AB + (long long)(q0 + c) * ldab - c;
+          const double vc = v[c], yc = sm.y[c];
+          const double vnc = vn[c], w2c = sm.tt[c] + al * vnc;
+          const int dlo = c > 1 ? c : 1;
+#pragma unroll
+          for (int i = 0; i < 9; ++i) {
+            const int k = kq + 4 * i;
+            if (k <= 32) {
+              const int r0 = 2 * k - sh, r1 = r0 + 1;
+              const bool in0 = r0 >= 1 && r0 < kMaxPanel, in1 = r1 >= 1 && r1 < kMaxPanel;
+              double o0 = 0.0, o1 = 0.0;
+              if (c > 0) {
+                if (in0) o0 = Ob[c * kLd2 + r0] - sm.w[r0] * vc - vn[r0] * yc;
+                if (in1) o1 = Ob[c * kLd2 + r1] - sm.w[r1] * vc - vn[r1] * yc;
+              }
+              if (in0 && in1) st_global_v2(od + r0, o0, o1);
+              else if (in0) od[r0] = o0;
+              else if (in1) od[r1] = o1;
+              const bool d0 = in0 && r0 >= dlo, d1 = in1 && r1 >= dlo;
+              double e0 = 0.0, e1 = 0.0;
+              if (d0) e0 = Db[c * kLd2 + r0] - (vn[r0] * w2c + (sm.tt[r0] + al * vn[r0]) * vnc);
+              if (d1) e1 = Db[c * kLd2 + r1] - (vn[r1] * w2c + (sm.tt[r1] + al * vn[r1]) * vnc);
+              if (d0 && d1) st_global_v2(dd + r0, e0, e1);
+              else if (d0) dd[r0] = e0;
+              else if (d1) dd[r1] = e1;
+            }
+          }
+        } else {
+          constexpr int kTotal = 2 * kMaxPanel * kPairSlots;
+          for (int t = tid; t < kTotal; t += kSbThreads) {
+            const bool isO = t >= kMaxPanel * kPairSlots;
+            const int u = isO ? t - kMaxPanel * kPairSlots : t;
+            const int c = u / kPairSlots, k = u - kPairSlots * c;
+            const int r0 = 2 * k - sh, r1 = r0 + 1;
+            if (r0 >= lq) continue;
+            double val0 = 0.0, val1 = 0.0;
+            bool ok0, ok1;
+            double* dst;
+            if (isO) {
+              if (c >= lp) continue;
+              ok0 = r0 >= 1;
+              ok1 = r1 >= 1 && r1 < lq;
+              dst = AB + (long long)(p0 + c) * ldab + (q0 + r0 - p0 - c);
+              if (c > 0) {
+                const double vc = v[c], yc = sm.y[c];
+                if (ok0) val0 = Ob[c * kLd2 + r0] - sm.w[r0] * vc - vn[r0] * yc;
+                if (ok1) val1 = Ob[c * kLd2 + r1] - sm.w[r1] * vc - vn[r1] * yc;
+              }
+            } else {
+              ok0 = r0 >= 1 && r0 >= c;
+              ok1 = r1 >= 1 && r1 >= c && r1 < lq;
+              if (!ok0 && !ok1) continue;
+              dst = AB + (long long)(q0 + c) * ldab + (r0 - c);
+              const double vc = vn[c], w2c = sm.tt[c] + al * vc;
+              if (ok0) val0 = Db[c * kLd2 + r0] - (vn[r0] * w2c + (sm.tt[r0] + al * vn[r0]) * vc);
+              if (ok1) val1 = Db[c * kLd2 + r1] - (vn[r1] * w2c + (sm.tt[r1] + al * vn[r1]) * vc);
+            }
+            if (ok0 && ok1) st_global_v2(dst, val0, val1);
+            else if (ok0) dst[0] = val0;
+            else if (ok1) dst[1] = val1;
+          }
+        }
+        // each warp publishes its own bulk stores: full[s] reaches
+        // kBulkWarps * (j + 1) once step j is completely stored
+        __syncwarp();
+        if (lane == 0) {
+          __threadfence();
+          atomicAdd(full + s, 1);
+        }
+      }
+      tau = taun;
+      if (trs) ++tcount;
+      p0 = q0;
+      p1 = q1;
+      lp = lq;
+    }
+    __syncthreads();
+    if (tid == 0) {
+      __threadfence();
+      st_release(late + s, kDone);
+      st_release(full + s, kDone);
+    }
+  }
+}
+
 __global__ void band_to_tridiag_kernel(const double* AB, int ldab, int n, double* d, double* e) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i < n) {
@@ -279,50 +647,65 @@ cudaError_t sb2st(double* AB, int ldab, int n, int b, double* d, double* e, doub
   if (n <= 0) return cudaSuccess;
   cudaError_t err;
   if (n > 2) {
-    if ((err = cudaMemsetAsync(progress, 0, sizeof(int) * n, s)) != cudaSuccess) return err;
-    const size_t smem = sizeof(SbSmem);
+    if ((err = cudaMemsetAsync(progress, 0, sizeof(int) * 2 * (size_t)n, s)) != cudaSuccess) return err;
+    int flags = 0;
+    if (const char* v = std::getenv("BSE_SB2ST_VARIANT")) flags = std::atoi(v);
+    cudaMemcpyToSymbolAsync(c_sb_flags, &flags, sizeof(int), 0, cudaMemcpyHostToDevice, s);
+    const bool legacy = (flags & 16) != 0;  // previous multi-phase step
+    const void* kern = legacy ? (const void*)sb2st_kernel : (const void*)sb2st_fused_kernel;
+    const size_t smem = legacy ? sizeof(SbSmem) : sizeof(SbfSmem);
     static bool attr = false;
     if (!attr) {
-      err = cudaFuncSetAttribute(sb2st_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      err = cudaFuncSetAttribute(sb2st_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)sizeof(SbSmem));
+      if (err == cudaSuccess)
+        err = cudaFuncSetAttribute(sb2st_fused_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   (int)sizeof(SbfSmem));
       if (err != cudaSuccess) return err;
       attr = true;
     }
     int per_sm = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, sb2st_kernel, kSbThreads, smem);
-    int flags = 0;
-    if (const char* v = std::getenv("BSE_SB2ST_VARIANT")) flags = std::atoi(v);
-    cudaMemcpyToSymbolAsync(c_sb_flags, &flags, sizeof(int), 0, cudaMemcpyHostToDevice, s);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kSbThreads, smem);
     if (!(flags & 8)) per_sm = 1;  // default 1 CTA/SM (flag 8 restores full occupancy)
     int grid = std::max(1, std::min(n - 2, std::max(1, per_sm) * num_sms));
     int maxsteps = sb2st_maxsteps(n, b);
     unsigned long long* trace = nullptr;
     const bool want_trace = std::getenv("BSE_SB2ST_TRACE") != nullptr;
-    const int tmax = 2 * (maxsteps + 1);
+    const size_t tsz = (size_t)2 * maxsteps * 16;
     if (want_trace) {
-      cudaMalloc(&trace, sizeof(unsigned long long) * 8 * tmax);
-      cudaMemsetAsync(trace, 0, sizeof(unsigned long long) * 8 * tmax, s);
+      cudaMalloc(&trace, sizeof(unsigned long long) * tsz);
+      cudaMemsetAsync(trace, 0, sizeof(unsigned long long) * tsz, s);
     }
     void* args[] = {&AB, &ldab, &n, &b, &V2, &tau2, &maxsteps, &progress, &trace};
     count_launch();
-    err = cudaLaunchCooperativeKernel((void*)sb2st_kernel, dim3(grid), dim3(kSbThreads), args, smem, s);
+    err = cudaLaunchCooperativeKernel(kern, dim3(grid), dim3(kSbThreads), args, smem, s);
     if (err != cudaSuccess) return err;
-    if (want_trace) {
-      std::vector<unsigned long long> h(8 * tmax);
+    if (want_trace && !legacy) {
+      std::vector<unsigned long long> h(tsz);
       cudaMemcpyAsync(h.data(), trace, h.size() * 8, cudaMemcpyDeviceToHost, s);
       cudaStreamSynchronize(s);
-      cudaFree(trace);
-      double acc[8] = {0};
+      // per-phase averages for sweep 1 (CTA 1) over steps 8..200, plus the
+      // cross-sweep chain: sweep 0's late publish of step j+1 -> sweep 1's
+      // late-wait exit of step j
+      double acc[16] = {0}, chain = 0.0, period = 0.0;
       int cnt = 0;
-      for (int k = 0; k < tmax; ++k) {
-        if (!h[8 * k + 7]) break;
-        for (int q = 1; q < 8; ++q) acc[q] += (double)(h[8 * k + q] - h[8 * k + q - 1]);
+      for (int j = 8; j < std::min(maxsteps - 2, 200); ++j) {
+        const unsigned long long* c = &h[((size_t)maxsteps + j) * 16];
+        const unsigned long long* p = &h[(size_t)(j + 1) * 16];
+        if (!c[8] || !p[8] || !h[((size_t)maxsteps + j + 1) * 16]) break;
+        for (int q = 1; q <= 8; ++q) acc[q] += (double)(c[q] - c[q - 1]);
+        chain += (double)c[3] - (double)p[8];
+        period += (double)(h[((size_t)maxsteps + j + 1) * 16] - c[0]);
         ++cnt;
       }
       const double d = std::max(cnt, 1) * 1e3;
-      std::fprintf(stderr, "[sb2st trace] grid=%d steps=%d us: wait %.2f load %.2f right %.2f house %.2f "
-                   "left+storeO %.2f twosided %.2f signal %.2f\n", grid, cnt, acc[1] / d, acc[2] / d,
-                   acc[3] / d, acc[4] / d, acc[5] / d, acc[6] / d, acc[7] / d);
+      std::fprintf(stderr, "[sb2st trace] steps=%d us: fullwait %.2f issue %.2f mirror+latewait %.2f "
+                   "lateload %.2f A %.2f B %.2f C %.2f publish %.2f | period %.2f\n",
+                   cnt, acc[1] / d, acc[2] / d, acc[3] / d, acc[4] / d, acc[5] / d, acc[6] / d,
+                   acc[7] / d, acc[8] / d, period / d);
+      (void)chain;
     }
+    if (trace) cudaFree(trace);
   }
   band_to_tridiag_kernel<<<(unsigned)ceil_div(n, 256), 256, 0, s>>>(AB, ldab, n, d, e);
   count_launch();
