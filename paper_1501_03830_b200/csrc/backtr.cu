@@ -82,223 +82,76 @@ __global__ void __launch_bounds__(256) q2_build_kernel(int n, int b, int g, int 
     double acc = 0.0;
     for (int k = 0; k <= c; ++k) acc += V[k * HB + r] * T[c * g + k];
     Vout[idx] = V[idx];
-    VTout[idx] = acc;
+    VTout[r * g + c] = acc;  // VT row-major (q2_apply's B-operand layout)
   }
 }
 
-// Column slab kernel, register-resident Z.  Each warp owns 8 columns of Z;
-// the 96 x 8 rows of the current block live in registers in the DMMA
-// accumulator (C) layout, and the B-operand fragments of Y = V^T Z are built
-// from them with warp shuffles, so Z never touches shared memory and the two
-// products need no block barrier.  Consecutive blocks of a sweep group
-// overlap by 32 rows: those stay in registers, the 64 new rows are
-// prefetched into registers while the current block computes, and V, VT are
-// double-buffered in shared memory with cp.async (2 CTAs / SM).  The zero
-// corners of the staircase V (and of VT = V T) are skipped at compile time.
+// Column-slab apply kernel.  Each warp owns 8 columns of Z and keeps a
+// window of Z rows in registers in the TRANSPOSED DMMA accumulator layout:
+// lane (rl = lane/4, kl = lane%4) holds acc[i][e] = Z[W0 + 8i + 2kl + e][col rl].
+// Both products are then computed transposed,
+//   Y^T = Z^T V   (A = Z^T straight from acc, B = V from shared memory)
+//   Z^T -= Y^T (V T)^T  (A = Y^T straight from its accumulators, B = VT)
+// with the k-steps ordered as {2kl + e}, so no operand needs a warp shuffle;
+// every shared-memory fragment pair is one conflict-free 128-bit load (V
+// column-major with LDV = 104, VT row-major with LDT = 40: both == 8 mod 16).
+// The zero corners of the staircase V (and of VT) are skipped at compile time.
 constexpr int kQ2HB = 96;
+constexpr int kQ2LDV = kQ2HB + 8;  // sV[c * LDV + r]
+constexpr int kQ2LDT = kQ2G + 8;   // sVT[r * LDT + c]
+constexpr int kQ2Stage = kQ2G * kQ2LDV + kQ2HB * kQ2LDT;
+constexpr int kQ2LDN = 64 + 8;     // prefetched rows, [col * LDN + row]
 
-BSE_DEV double bfrag(const double (&acc)[12][2], int t, int lane) {
-  // B fragment (k = 4t + lane%4, n = lane/4) of the 96 x 8 tile held in C layout
-  const int kl = lane & 3, rl = lane >> 2;
-  const int src = ((4 * (t & 1) + kl) << 2) + (rl >> 1);
-  const double v0 = __shfl_sync(0xffffffffu, acc[t >> 1][0], src);
-  const double v1 = __shfl_sync(0xffffffffu, acc[t >> 1][1], src);
-  return (rl & 1) ? v1 : v0;
-}
+BSE_DEV double2 lds2(const double* p) { return *reinterpret_cast<const double2*>(p); }
 
-__global__ void __launch_bounds__(kQ2Threads, 1) q2_apply_kernel(int n, int b, int maxsteps,
-                                                                 const double* __restrict__ Vblk,
-                                                                 const double* __restrict__ VTblk,
-                                                                 double* __restrict__ Z,
-                                                                 long long ldz, int ncols,
-                                                                 unsigned long long* trace) {
-  constexpr int HB = kQ2HB, G = kQ2G;
-  constexpr int LDV = HB + 4;  // == 4 mod 16: conflict-free fragment loads
-  constexpr int STAGE = 2 * G * LDV;
-  constexpr int LDN = 64 + 4;  // prefetched rows, [col * LDN + row]
-  extern __shared__ __align__(16) double sm[];
-  double* sZn = sm + 2 * STAGE;
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int kl = lane & 3, rl = lane >> 2;
-  const int cw = blockIdx.x * kQ2W + warp * 8;  // first column of this warp
-  const int nsweeps = n - 2;
-  const int ngroups = (int)ceil_div(nsweeps, G);
-  (void)trace;
-
-  // flattened block sequence: groups descending, steps ascending
-  auto nsteps_of = [&](int gi) {
-    const int s0 = gi * G;
-    const long long st = ceil_div(n - 1 - s0, b);  // blocks with r0 <= n-1
-    return (int)(st < maxsteps ? st : maxsteps);
-  };
-  auto issue_vt = [&](int gi, int j, int stage) {
-    const size_t blk = (size_t)gi * maxsteps + j;
-    const double* gV = Vblk + blk * HB * G;
-    const double* gVT = VTblk + blk * HB * G;
-    double* sV = sm + stage * STAGE;
-    double* sVT = sV + G * LDV;
-    for (int idx = tid; idx < HB * G / 2; idx += blockDim.x) {
-      const int e = idx * 2;
-      const int r = e % HB, c = e / HB;
-      cp_async16(sV + c * LDV + r, gV + e, true);
-      cp_async16(sVT + c * LDV + r, gVT + e, true);
-    }
-    cp_async_commit();
-  };
-  auto zaddr = [&](int row, int col) { return Z + row + (long long)col * ldz; };
-  auto zload = [&](int row, int col) -> double {
-    return (row < n && col < ncols) ? __ldcg(zaddr(row, col)) : 0.0;
-  };
-
-  double acc[12][2];
-  int gi = ngroups - 1, j = 0, stage = 0;
-  if (gi >= 0) issue_vt(gi, 0, 0);
-  bool group_start = true;
-  // invariant at the top of each iteration: the current block's V/VT is the
-  // newest committed group
-  while (gi >= 0) {
-    const int s0 = gi * G;
-    const int r0 = s0 + 1 + j * b;
-    const int steps = nsteps_of(gi);
-    const bool last = (j + 1 >= steps);
-    // next block in the flattened order -> its V/VT into the other stage
-    int ngi = gi, nj = j + 1;
-    if (last) { ngi = gi - 1; nj = 0; }
-    // cp.async groups in issue order: [new Z rows of this block] [next V/VT]
-    if (!last) {
-      const int rbase = r0 + HB;
-      for (int idx = tid; idx < 64 * kQ2W; idx += blockDim.x) {
-        const int rr = idx & 63, c = idx >> 6;
-        const int row = rbase + rr, col = blockIdx.x * kQ2W + c;
-        const bool ok = row < n && col < ncols;
-        cp_async8(sZn + c * LDN + rr, ok ? zaddr(row, col) : Z, ok);
-      }
-    }
-    cp_async_commit();
-    if (ngi >= 0) issue_vt(ngi, nj, stage ^ 1);
-    else cp_async_commit();
-    if (group_start) {
-#pragma unroll
-      for (int i = 0; i < 12; ++i)
-#pragma unroll
-        for (int e = 0; e < 2; ++e) acc[i][e] = zload(r0 + 8 * i + rl, cw + 2 * kl + e);
-      group_start = false;
-    }
-    cp_async_wait<2>();  // this block's V/VT (issued one iteration earlier)
-    __syncthreads();
-    const double* sV = sm + stage * STAGE;
-    const double* sVT = sV + G * LDV;
-    // Y (32 x 8) = V^T Z: reflector tile q (rows 8q..8q+7 of Y) only meets Z
-    // rows [8q, 8q + 71): k-steps t in [2q, 2q + 17]
-    double y[4][2];
-#pragma unroll
-    for (int q = 0; q < 4; ++q) y[q][0] = y[q][1] = 0.0;
-#pragma unroll
-    for (int t = 0; t < 24; ++t) {
-      const double bf = bfrag(acc, t, lane);
-#pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        if (t >= 2 * q && t <= 2 * q + 17) {
-          const double af = sV[(8 * q + rl) * LDV + 4 * t + kl];
-          dmma8x8x4(y[q], af, bf);
-        }
-      }
-    }
-    // Z (96 x 8) -= VT Y: VT[r][c] = 0 for c < r - 63 (rows >= 64 skip k-steps)
-#pragma unroll
-    for (int t = 0; t < 8; ++t) {
-      // B fragment of -Y (k = reflector 4t + lane%4, n = lane/4)
-      const int src = ((4 * (t & 1) + kl) << 2) + (rl >> 1);
-      const double v0 = __shfl_sync(0xffffffffu, y[t >> 1][0], src);
-      const double v1 = __shfl_sync(0xffffffffu, y[t >> 1][1], src);
-      const double bf = -((rl & 1) ? v1 : v0);
-#pragma unroll
-      for (int i = 0; i < 12; ++i) {
-        const int tmin = i < 8 ? 0 : (8 * i - 63) / 4;
-        if (t >= tmin) {
-          const double af = sVT[(4 * t + kl) * LDV + 8 * i + rl];
-          dmma8x8x4(acc[i], af, bf);
-        }
-      }
-    }
-    // retire rows: all 96 at the end of a group, else the first 64
-    const int nstore = last ? 12 : 8;
-#pragma unroll
-    for (int i = 0; i < 12; ++i) {
-      if (i < nstore) {
-        const int row = r0 + 8 * i + rl;
-#pragma unroll
-        for (int e = 0; e < 2; ++e) {
-          const int col = cw + 2 * kl + e;
-          if (row < n && col < ncols) *zaddr(row, col) = acc[i][e];
-        }
-      }
-    }
-    if (!last) {
-      cp_async_wait<1>();  // the prefetched rows (next V/VT may still be in flight)
-      __syncthreads();
-      const int cl = warp * 8;
-#pragma unroll
-      for (int i = 0; i < 4; ++i) { acc[i][0] = acc[8 + i][0]; acc[i][1] = acc[8 + i][1]; }
-#pragma unroll
-      for (int i = 0; i < 8; ++i)
-#pragma unroll
-        for (int e = 0; e < 2; ++e) acc[4 + i][e] = sZn[(cl + 2 * kl + e) * LDN + 8 * i + rl];
-    } else {
-      group_start = true;
-    }
-    __syncthreads();  // this stage's V/VT are free for the block after next
-    stage ^= 1;
-    gi = ngi;
-    j = nj;
-  }
-}
-
-// Paired-group variant (default).  Two consecutive sweep groups (ga = gi,
-// gb = gi - 1) walk down the rows together: at chase step j, block (ga, j)
-// covers rows [B0 + 64j + 32, +96) and block (gb, j) rows [B0 + 64j, +96)
-// (B0 = gb*G + 1).  (gb, j) only overlaps (ga, j') for j' <= j, so the order
-// (ga, 0), (gb, 0), (ga, 1), (gb, 1), ... respects Q2's application order.
-// Each warp keeps the 128-row window of its 8 columns in registers and
-// streams 64 rows in and out per STEP instead of per block: half the Z
-// traffic and half the row-streaming stalls of the single-group walk.
 template <int OFF, int NT>
-BSE_DEV void q2_block_at(double (&acc)[NT][2], const double* sV, const double* sVT, int lane) {
-  constexpr int LDV = kQ2HB + 4;
+BSE_DEV void q2_block_t(double (&acc)[NT][2], const double* sV, const double* sVT, int lane) {
   const int kl = lane & 3, rl = lane >> 2;
-  double y[4][2];
+  double yt[4][2];
 #pragma unroll
-  for (int q = 0; q < 4; ++q) y[q][0] = y[q][1] = 0.0;
+  for (int q = 0; q < 4; ++q) yt[q][0] = yt[q][1] = 0.0;
+  // Y^T (8 cols x 32 reflectors): reflector tile q meets row tiles q .. q+8
 #pragma unroll
-  for (int t = 0; t < 24; ++t) {
-    const int src = ((4 * (t & 1) + kl) << 2) + (rl >> 1);
-    const double v0 = __shfl_sync(0xffffffffu, acc[OFF + (t >> 1)][0], src);
-    const double v1 = __shfl_sync(0xffffffffu, acc[OFF + (t >> 1)][1], src);
-    const double bf = (rl & 1) ? v1 : v0;
+  for (int i = 0; i < 12; ++i) {
+    double2 bv[4];
 #pragma unroll
-    for (int q = 0; q < 4; ++q) {
-      if (t >= 2 * q && t <= 2 * q + 17) {
-        const double af = sV[(8 * q + rl) * LDV + 4 * t + kl];
-        dmma8x8x4(y[q], af, bf);
-      }
-    }
+    for (int q = 0; q < 4; ++q)
+      if (i >= q && i <= q + 8) bv[q] = lds2(sV + (8 * q + rl) * kQ2LDV + 8 * i + 2 * kl);
+#pragma unroll
+    for (int q = 0; q < 4; ++q)
+      if (i >= q && i <= q + 8) dmma8x8x4(yt[q], acc[OFF + i][0], bv[q].x);
+#pragma unroll
+    for (int q = 0; q < 4; ++q)
+      if (i >= q && i <= q + 8) dmma8x8x4(yt[q], acc[OFF + i][1], bv[q].y);
   }
 #pragma unroll
-  for (int t = 0; t < 8; ++t) {
-    const int src = ((4 * (t & 1) + kl) << 2) + (rl >> 1);
-    const double v0 = __shfl_sync(0xffffffffu, y[t >> 1][0], src);
-    const double v1 = __shfl_sync(0xffffffffu, y[t >> 1][1], src);
-    const double bf = -((rl & 1) ? v1 : v0);
+  for (int q = 0; q < 4; ++q) { yt[q][0] = -yt[q][0]; yt[q][1] = -yt[q][1]; }
+  // Z^T -= Y^T VT^T: VT[r][c] = 0 for c < r - 63 (row tile i needs q >= i - 8)
 #pragma unroll
-    for (int i = 0; i < 12; ++i) {
-      const int tmin = i < 8 ? 0 : (8 * i - 63) / 4;
-      if (t >= tmin) {
-        const double af = sVT[(4 * t + kl) * LDV + 8 * i + rl];
-        dmma8x8x4(acc[OFF + i], af, bf);
-      }
+  for (int q = 0; q < 4; ++q) {
+#pragma unroll
+    for (int h = 0; h < 12; h += 6) {
+      double2 bv[6];
+#pragma unroll
+      for (int i = h; i < h + 6; ++i)
+        if (q >= i - 8) bv[i - h] = lds2(sVT + (8 * i + rl) * kQ2LDT + 8 * q + 2 * kl);
+#pragma unroll
+      for (int i = h; i < h + 6; ++i)
+        if (q >= i - 8) dmma8x8x4(acc[OFF + i], yt[q][0], bv[i - h].x);
+#pragma unroll
+      for (int i = h; i < h + 6; ++i)
+        if (q >= i - 8) dmma8x8x4(acc[OFF + i], yt[q][1], bv[i - h].y);
     }
   }
 }
+
+// Paired-group walk.  Two consecutive sweep groups (ga = gi, gb = gi - 1)
+// walk down the rows together: at chase step j, block (ga, j) covers rows
+// [B0 + 64j + 32, +96) and block (gb, j) rows [B0 + 64j, +96) (B0 = gb*G + 1).
+// (gb, j) only overlaps (ga, j') for j' <= j, so the order (ga, 0), (gb, 0),
+// (ga, 1), (gb, 1), ... respects Q2's application order.  The 128-row window
+// stays in registers; 64 rows stream in (cp.async, one step ahead) and out
+// per STEP instead of per block.
 
 template <int P>
 __global__ void __launch_bounds__(kQ2Threads, 1) q2_apply_pair_kernel(int n, int b, int maxsteps,
@@ -307,9 +160,8 @@ __global__ void __launch_bounds__(kQ2Threads, 1) q2_apply_pair_kernel(int n, int
                                                                       double* __restrict__ Z,
                                                                       long long ldz, int ncols) {
   constexpr int HB = kQ2HB, G = kQ2G;
-  constexpr int LDV = HB + 4;
-  constexpr int STAGE = 2 * G * LDV;
-  constexpr int LDN = 64 + 2;  // == 2 mod 8: conflict-free C-layout reloads
+  constexpr int STAGE = kQ2Stage;
+  constexpr int LDN = kQ2LDN;
   constexpr int NT = 4 * P + 8;  // 8-row tiles in the window
   extern __shared__ __align__(16) double sm[];
   double* sZn = sm + 2 * STAGE;
@@ -346,12 +198,13 @@ __global__ void __launch_bounds__(kQ2Threads, 1) q2_apply_pair_kernel(int n, int
     const double* gV = Vblk + blk * HB * G;
     const double* gVT = VTblk + blk * HB * G;
     double* sV = sm + stage * STAGE;
-    double* sVT = sV + G * LDV;
+    double* sVT = sV + G * kQ2LDV;
     for (int idx = tid; idx < HB * G / 2; idx += blockDim.x) {
       const int e = idx * 2;
-      const int r = e % HB, c = e / HB;
-      cp_async16(sV + c * LDV + r, gV + e, true);
-      cp_async16(sVT + c * LDV + r, gVT + e, true);
+      const int r = e % HB, c = e / HB;   // V: column-major
+      cp_async16(sV + c * kQ2LDV + r, gV + e, true);
+      const int rt = e / G, ct = e % G;   // VT: row-major
+      cp_async16(sVT + rt * kQ2LDT + ct, gVT + e, true);
     }
     cp_async_commit();
   };
@@ -391,7 +244,7 @@ __global__ void __launch_bounds__(kQ2Threads, 1) q2_apply_pair_kernel(int n, int
       for (int i = 0; i < NT; ++i)
 #pragma unroll
         for (int e = 0; e < 2; ++e) {
-          const int row = B0 + 8 * i + rl, col = cw + 2 * kl + e;
+          const int row = B0 + 8 * i + 2 * kl + e, col = cw + rl;
           acc[i][e] = zok(row, col) ? __ldcg(zaddr(row, col)) : 0.0;
         }
       pair_start = false;
@@ -399,12 +252,12 @@ __global__ void __launch_bounds__(kQ2Threads, 1) q2_apply_pair_kernel(int n, int
     cp_async_wait<2>();
     __syncthreads();
     const double* sV = sm + stage * STAGE;
-    const double* sVT = sV + G * LDV;
+    const double* sVT = sV + G * kQ2LDV;
     // group ga - wh's block sits 32 (P - 1 - wh) rows into the window
-    if (P == 1 || wh == 0) q2_block_at<4 * (P - 1), NT>(acc, sV, sVT, lane);
-    else if (P == 2 || wh == 1) q2_block_at<4 * (P > 1 ? P - 2 : 0), NT>(acc, sV, sVT, lane);
-    else if (P == 3 || wh == 2) q2_block_at<4 * (P > 2 ? P - 3 : 0), NT>(acc, sV, sVT, lane);
-    else q2_block_at<4 * (P > 3 ? P - 4 : 0), NT>(acc, sV, sVT, lane);
+    if (P == 1 || wh == 0) q2_block_t<4 * (P - 1), NT>(acc, sV, sVT, lane);
+    else if (P == 2 || wh == 1) q2_block_t<4 * (P > 1 ? P - 2 : 0), NT>(acc, sV, sVT, lane);
+    else if (P == 3 || wh == 2) q2_block_t<4 * (P > 2 ? P - 3 : 0), NT>(acc, sV, sVT, lane);
+    else q2_block_t<4 * (P > 3 ? P - 4 : 0), NT>(acc, sV, sVT, lane);
     if (step_end) {
       const int nstore = pair_end ? NT : 8;
       const int rbase = B0 + 64 * j;
@@ -413,7 +266,7 @@ __global__ void __launch_bounds__(kQ2Threads, 1) q2_apply_pair_kernel(int n, int
         if (i < nstore) {
 #pragma unroll
           for (int e = 0; e < 2; ++e) {
-            const int row = rbase + 8 * i + rl, col = cw + 2 * kl + e;
+            const int row = rbase + 8 * i + 2 * kl + e, col = cw + rl;
             if (zok(row, col)) *zaddr(row, col) = acc[i][e];
           }
         }
@@ -425,9 +278,11 @@ __global__ void __launch_bounds__(kQ2Threads, 1) q2_apply_pair_kernel(int n, int
 #pragma unroll
         for (int i = 0; i < NT - 8; ++i) { acc[i][0] = acc[8 + i][0]; acc[i][1] = acc[8 + i][1]; }
 #pragma unroll
-        for (int i = 0; i < 8; ++i)
-#pragma unroll
-          for (int e = 0; e < 2; ++e) acc[NT - 8 + i][e] = sZn[(cl + 2 * kl + e) * LDN + 8 * i + rl];
+        for (int i = 0; i < 8; ++i) {
+          const double2 z = lds2(sZn + (cl + rl) * LDN + 8 * i + 2 * kl);
+          acc[NT - 8 + i][0] = z.x;
+          acc[NT - 8 + i][1] = z.y;
+        }
       } else {
         pair_start = true;
       }
@@ -471,22 +326,14 @@ cudaError_t q2_apply(int n, int b, int g, const double* Vblk, const double* VTbl
   if (n <= 2 || ncols <= 0) return cudaSuccess;
   if (b != 64 || g != kQ2G || q2_hb(b, g) != kQ2HB) return cudaErrorInvalidValue;
   const int maxsteps = sb2st_maxsteps(n, b);
-  const size_t smem = sizeof(double) * (2 * (2 * (size_t)kQ2G * (kQ2HB + 4)) + (size_t)kQ2W * 68);
+  const size_t smem = sizeof(double) * (2 * (size_t)kQ2Stage + (size_t)kQ2W * kQ2LDN);
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(q2_apply_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     cudaFuncSetAttribute(q2_apply_pair_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     attr = true;
   }
-  static const int variant = [] {
-    const char* v = std::getenv("BSE_Q2_VARIANT");
-    return v ? std::atoi(v) : 0;
-  }();
-  const unsigned grid = (unsigned)ceil_div(ncols, kQ2W);
-  if (variant == 1)
-    q2_apply_kernel<<<grid, kQ2Threads, smem, s>>>(n, b, maxsteps, Vblk, VTblk, Z, ldz, ncols, nullptr);
-  else
-    q2_apply_pair_kernel<2><<<grid, kQ2Threads, smem, s>>>(n, b, maxsteps, Vblk, VTblk, Z, ldz, ncols);
+  q2_apply_pair_kernel<2><<<(unsigned)ceil_div(ncols, kQ2W), kQ2Threads, smem, s>>>(
+      n, b, maxsteps, Vblk, VTblk, Z, ldz, ncols);
   count_launch();
   return cudaGetLastError();
 }
