@@ -171,10 +171,11 @@ __global__ void __launch_bounds__(kQ2Threads, 1) q2_apply_pair_kernel(int n, int
   const int nsweeps = n - 2;
   const int ngroups = (int)ceil_div(nsweeps, G);
 
+  (void)b;  // == 64 (checked by the host)
   auto steps_of = [&](int gi) -> int {
     if (gi < 0) return 0;
-    const long long st = ceil_div(n - 1 - gi * G, b);
-    return (int)(st < maxsteps ? st : maxsteps);
+    const int st = (n - 1 - gi * G + 63) >> 6;
+    return st < maxsteps ? st : maxsteps;
   };
   // blocks of group ga - wh exist for j < steps; the earliest group of the
   // set (ga - P + 1) has the most steps
@@ -208,8 +209,13 @@ __global__ void __launch_bounds__(kQ2Threads, 1) q2_apply_pair_kernel(int n, int
     }
     cp_async_commit();
   };
-  auto zaddr = [&](int row, int col) { return Z + row + (long long)col * ldz; };
-  auto zok = [&](int row, int col) { return row >= 0 && row < n && col < ncols; };
+  // this lane's column of Z (rows added per access); prefetch thread's column
+  const bool colok = cw + rl < ncols;
+  double* const zc = Z + (long long)(colok ? cw + rl : 0) * ldz;
+  const int prr = tid & 63;           // prefetch row (kQ2Threads % 64 == 0)
+  const int pc0 = tid >> 6;           // first prefetch column, step 7
+  static_assert(kQ2Threads % 64 == 0, "prefetch mapping");
+  constexpr int kPStep = kQ2Threads / 64;
 
   double acc[NT][2];
   int ga = ngroups - 1, j = 0, wh = 0, stage = 0;
@@ -222,35 +228,41 @@ __global__ void __launch_bounds__(kQ2Threads, 1) q2_apply_pair_kernel(int n, int
     const bool more = advance(nga, nj, nwh);
     const bool step_end = !more || nga != ga || nj != j;
     const bool pair_end = !more || nga != ga;
-    // first block of step j: prefetch the 64 rows step j+1 brings in
-    bool step_first = true;
-    for (int m = 0; m < wh; ++m)
-      if (j < steps_of(ga - m)) step_first = false;
-    const int smax = smax_of(ga);
-    if (step_first && j + 1 < smax) {
-      const int rbase = B0 + 64 * j + 8 * NT;
-      for (int idx = tid; idx < 64 * kQ2W; idx += blockDim.x) {
-        const int rr = idx & 63, c = idx >> 6;
-        const int row = rbase + rr, col = blockIdx.x * kQ2W + c;
-        const bool ok = zok(row, col);
-        cp_async8(sZn + c * LDN + rr, ok ? zaddr(row, col) : Z, ok);
-      }
-    }
-    cp_async_commit();
-    if (more) issue_vt(nga - nwh, nj, stage ^ 1);
-    else cp_async_commit();
     if (pair_start) {
 #pragma unroll
       for (int i = 0; i < NT; ++i)
 #pragma unroll
         for (int e = 0; e < 2; ++e) {
-          const int row = B0 + 8 * i + 2 * kl + e, col = cw + rl;
-          acc[i][e] = zok(row, col) ? __ldcg(zaddr(row, col)) : 0.0;
+          const int row = B0 + 8 * i + 2 * kl + e;
+          acc[i][e] = (colok && row >= 0 && row < n) ? __ldcg(zc + row) : 0.0;
         }
       pair_start = false;
     }
-    cp_async_wait<2>();
+    // this block's V/VT (and any row prefetch) have landed; every thread is
+    // past the previous block, so its stage and the row buffer may be reused
+    cp_async_wait<0>();
     __syncthreads();
+    if (more) issue_vt(nga - nwh, nj, stage ^ 1);
+    // first block of step j: prefetch the 64 rows step j+1 brings in
+    bool step_first = true;
+    for (int m = 0; m < wh; ++m)
+      if (j < steps_of(ga - m)) step_first = false;
+    if (step_first && j + 1 < smax_of(ga)) {
+      const int row = B0 + 64 * j + 8 * NT + prr;
+      const bool rok = row >= 0 && row < n;
+      int col = blockIdx.x * kQ2W + pc0;
+      const double* src = Z + (long long)col * ldz + row;
+      double* dst = sZn + pc0 * LDN + prr;
+#pragma unroll 4
+      for (int c = pc0; c < kQ2W; c += kPStep) {
+        const bool ok = rok && col < ncols;
+        cp_async8(dst, ok ? src : Z, ok);
+        src += kPStep * ldz;
+        dst += kPStep * LDN;
+        col += kPStep;
+      }
+      cp_async_commit();
+    }
     const double* sV = sm + stage * STAGE;
     const double* sVT = sV + G * kQ2LDV;
     // group ga - wh's block sits 32 (P - 1 - wh) rows into the window
@@ -266,13 +278,13 @@ __global__ void __launch_bounds__(kQ2Threads, 1) q2_apply_pair_kernel(int n, int
         if (i < nstore) {
 #pragma unroll
           for (int e = 0; e < 2; ++e) {
-            const int row = rbase + 8 * i + 2 * kl + e, col = cw + rl;
-            if (zok(row, col)) *zaddr(row, col) = acc[i][e];
+            const int row = rbase + 8 * i + 2 * kl + e;
+            if (colok && row >= 0 && row < n) zc[row] = acc[i][e];
           }
         }
       }
       if (!pair_end) {
-        cp_async_wait<1>();
+        cp_async_wait<0>();
         __syncthreads();
         const int cl = warp * 8;
 #pragma unroll
@@ -287,7 +299,6 @@ __global__ void __launch_bounds__(kQ2Threads, 1) q2_apply_pair_kernel(int n, int
         pair_start = true;
       }
     }
-    __syncthreads();
     stage ^= 1;
     if (!more) break;
     ga = nga;
