@@ -54,6 +54,7 @@ BSE_DEV void warp_house(const double* x, int len, double* v, double* sc) {
 }
 
 __constant__ int c_sb_flags;  // tuning variants (BSE_SB2ST_VARIANT), default 0
+__constant__ int c_sb_trace_s0;  // first traced sweep (BSE_SB2ST_TRACE)
 
 BSE_DEV void wait_progress(const int* progress, int s, int need) {
   if (s > 0 && threadIdx.x == 0) {
@@ -291,8 +292,8 @@ constexpr int kPairSlots = 34;  // 16-byte row-pair slots per column (33 used)
 constexpr int kBulkWarps = kSbThreads / 32;  // every warp stores part of the bulk
 
 struct SbfSmem {
-  double D[kMaxPanel * kLd2 + 2];
-  double O[kMaxPanel * kLd2 + 2];
+  double D[2][kMaxPanel * kLd2 + 2];  // double-buffered: step j+1 stages while j computes
+  double O[2][kMaxPanel * kLd2 + 2];
   double vbuf[2][kMaxPanel];
   double vnw[kSbThreads / 32][kMaxPanel];
   double w[kMaxPanel];
@@ -325,40 +326,37 @@ BSE_DEV void st_global_v2(double* p, double a, double b) {
   asm volatile("st.global.v2.f64 [%0], {%1, %2};\n" ::"l"(p), "d"(a), "d"(b) : "memory");
 }
 
-BSE_DEV void stage_split(SbfSmem& sm, const double* AB, int ldab, int q0, int lq, int p0, int lp,
-                         const int* full_pred, const int* late_pred, int j, bool has_pred,
-                         unsigned long long* tr) {
-  const int tid = threadIdx.x;
-  if (has_pred && tid == 0) poll_counter(full_pred, kBulkWarps * (j + 1));
-  __syncthreads();  // also: previous step's smem reads are done
-  if (tr && tid == 0) tr[1] = gtimer();
+// Issue the bulk of a step's staging (everything but the late positions, which
+// are loaded stale and overwritten after the late wait) into (Db, Ob), which
+// are already shifted by q0 & 1.  Threads t0, t0 + nt, ... of a 256-slot grid.
+BSE_DEV void stage_bulk(double* Db, double* Ob, const double* AB, int ldab, int q0, int lq, int p0,
+                        int lp, int t0, int nt) {
   const int sh = q0 & 1;
-  double* Db = sm.D + sh;
-  double* Ob = sm.O + sh;
   if (lq == kMaxPanel && lp == kMaxPanel) {
-    // full blocks: 4 threads per column, 16-byte row pairs, no zero fill
-    // (D's strict upper triangle is mirrored below; late rows are reloaded)
-    const int c = tid >> 2, kq = tid & 3;
-    const double* osrc = AB + (long long)(p0 + c) * ldab + (q0 - p0 - c);
-    const double* dsrc = AB + (long long)(q0 + c) * ldab - c;
-    double* od = Ob + c * kLd2;
-    double* dd = Db + c * kLd2;
+    // full blocks: 4 slots per column, 16-byte row pairs, no zero fill (D's
+    // strict upper triangle is mirrored afterwards)
+    for (int t = t0; t < kSbThreads; t += nt) {
+      const int c = t >> 2, kq = t & 3;
+      const double* osrc = AB + (long long)(p0 + c) * ldab + (q0 - p0 - c);
+      const double* dsrc = AB + (long long)(q0 + c) * ldab - c;
+      double* od = Ob + c * kLd2;
+      double* dd = Db + c * kLd2;
 #pragma unroll
-    for (int i = 0; i < 9; ++i) {
-      const int k = kq + 4 * i;
-      if (k <= 32) {
-        const int r0 = 2 * k - sh;
-        const int bytes = k < 32 ? 16 : (sh ? 8 : 0);
-        if (bytes) {
-          cp_async16_n(od + r0, osrc + r0, bytes);
-          if (r0 + 1 >= c) cp_async16_n(dd + r0, dsrc + r0, bytes);
+      for (int i = 0; i < 9; ++i) {
+        const int k = kq + 4 * i;
+        if (k <= 32) {
+          const int r0 = 2 * k - sh;
+          const int bytes = k < 32 ? 16 : (sh ? 8 : 0);
+          if (bytes) {
+            cp_async16_n(od + r0, osrc + r0, bytes);
+            if (r0 + 1 >= c) cp_async16_n(dd + r0, dsrc + r0, bytes);
+          }
         }
       }
     }
   } else {
     constexpr int kTotal = 2 * kMaxPanel * kPairSlots;
-  #pragma unroll 2
-    for (int t = tid; t < kTotal; t += kSbThreads) {
+    for (int t = t0; t < kTotal; t += nt) {
       const bool isO = t >= kMaxPanel * kPairSlots;
       const int u = isO ? t - kMaxPanel * kPairSlots : t;
       const int c = u / kPairSlots, k = u - kPairSlots * c;
@@ -367,8 +365,7 @@ BSE_DEV void stage_split(SbfSmem& sm, const double* AB, int ldab, int q0, int lq
       double* dst = (isO ? Ob : Db) + c * kLd2 + r0;
       const double* src = isO ? AB + (long long)(p0 + c) * ldab + (q0 + r0 - p0 - c)
                               : AB + (long long)(q0 + c) * ldab + (r0 - c);
-      // need: the row must come from this copy (late positions included: they
-      // are overwritten after the late wait); zero: the row must read 0; all
+      // need: the row must come from this copy; zero: the row must read 0;
       // other rows (row -1/64 padding, D's upper triangle) are don't-care.
       const int r1 = r0 + 1;
       bool need0, need1, zero0, zero1;
@@ -384,28 +381,30 @@ BSE_DEV void stage_split(SbfSmem& sm, const double* AB, int ldab, int q0, int lq
         zero1 = r1 < kMaxPanel && r1 >= c && !need1;
       }
       int bytes;
-      if (need1) bytes = 16;            // r0 needed or don't-care
-      else if (need0) bytes = 8;        // r1 zero-filled or don't-care
+      if (need1) bytes = 16;
+      else if (need0) bytes = 8;
       else if (zero0 || zero1) bytes = 0;
       else continue;
       cp_async16_n(dst, bytes ? src : AB, bytes);
     }
   }
-  cp_async_commit();
-  if (tr && tid == 0) tr[2] = gtimer();
-  cp_async_wait<0>();
-  __syncthreads();
-  // mirror D's strict upper triangle from the lower one (except the late row)
+}
+
+// D's strict upper triangle from the lower one (except the late row lq - 1).
+BSE_DEV void mirror_d(double* Db, int lq) {
   const int rl = lq - 1;
 #pragma unroll 4
   for (int k = 0; k < kSlots; ++k) {
-    const int idx = tid + k * kSbThreads;
+    const int idx = threadIdx.x + k * kSbThreads;
     const int r = idx & (kMaxPanel - 1), c = idx >> 6;
     if (r < c && c != rl) Db[c * kLd2 + r] = Db[r * kLd2 + c];
   }
-  if (has_pred && tid == 0) poll_counter(late_pred, j + 2);
-  __syncthreads();
-  if (tr && tid == 0) tr[3] = gtimer();
+}
+
+// The late positions (D's last row and O(lq-1, lp-1)), after the late wait.
+BSE_DEV void late_load(double* Db, double* Ob, const double* AB, int ldab, int q0, int lq, int p0,
+                       int lp) {
+  const int tid = threadIdx.x, rl = lq - 1;
   if (tid < kMaxPanel) {
     const int c = tid;
     const double x = c <= rl ? __ldcg(AB + (long long)(q0 + c) * ldab + (rl - c)) : 0.0;
@@ -414,7 +413,10 @@ BSE_DEV void stage_split(SbfSmem& sm, const double* AB, int ldab, int q0, int lq
   } else if (tid == kMaxPanel) {
     Ob[(lp - 1) * kLd2 + rl] = __ldcg(AB + (long long)(p0 + lp - 1) * ldab + (q0 + rl - p0 - lp + 1));
   }
-  __syncthreads();
+}
+
+BSE_DEV void named_bar(int id, int nthreads) {
+  asm volatile("bar.sync %0, %1;\n" ::"r"(id), "r"(nthreads) : "memory");
 }
 
 __global__ void __launch_bounds__(kSbThreads) sb2st_fused_kernel(double* AB, int ldab, int n,
@@ -427,29 +429,47 @@ __global__ void __launch_bounds__(kSbThreads) sb2st_fused_kernel(double* AB, int
   const int lane = tid & 31, warp = tid >> 5;
   const int mi = warp * 8 + (lane >> 2);  // row (A) / column (C) owned by this quarter-thread
   const int q = lane & 3;
-  const bool tr = trace != nullptr && blockIdx.x < 2 && threadIdx.x == 0;
-  int tcount = 0;
-  auto T = [&](int slot) { trace[(blockIdx.x * (long long)maxsteps + tcount) * 16 + slot] = gtimer(); };
+  const int ts0 = c_sb_trace_s0;
+  int tj = 0, ts = 0;
+  auto T = [&](int slot) { trace[((long long)(ts - ts0) * maxsteps + tj) * 16 + slot] = gtimer(); };
   int* full = progress;
   int* late = progress + n;
   if (tid < kMaxPanel) sm.vbuf[0][tid] = sm.vbuf[1][tid] = 0.0;
 
   for (int s = blockIdx.x; s < n - 2; s += gridDim.x) {
-    const bool trs = tr && s < 2;
-    int p0 = s, p1 = s, lp = 1;
+    const bool trw = trace != nullptr && (s == ts0 || s == ts0 + 1);
+    const bool trs = trw && tid == 0;
+    const bool trs32 = trw && tid == 32;
+    ts = s;
+    const bool has_pred = s > 0;
+    int p0 = s, lp = 1;
     double tau = 0.0;
+    int q0 = s + 1, q1 = min(s + b, n - 1);
+    int lq = q1 - q0 + 1;
+    // prologue: step 0's bulk into buffer 0
+    __syncthreads();  // the previous sweep is done with both buffers
+    if (has_pred && tid == 0) poll_counter(full + s - 1, kBulkWarps);
+    __syncthreads();
+    stage_bulk(sm.D[0] + (q0 & 1), sm.O[0] + (q0 & 1), AB, ldab, q0, lq, p0, lp, tid, kSbThreads);
+    cp_async_commit();
+    cp_async_wait<0>();
+    __syncthreads();
+    mirror_d(sm.D[0] + (q0 & 1), lq);
     for (int j = 0;; ++j) {
-      const int q0 = p1 + 1;
-      if (q0 > n - 1) break;
-      const int q1 = min(p1 + b, n - 1);
-      const int lq = q1 - q0 + 1;
+      const int cur = j & 1;
       const int sh = q0 & 1;
-      const double* Db = sm.D + sh;
-      const double* Ob = sm.O + sh;
+      double* Db = sm.D[cur] + sh;
+      double* Ob = sm.O[cur] + sh;
       const double* v = sm.vbuf[j & 1];
+      tj = j;
       if (trs) T(0);
-      stage_split(sm, AB, ldab, q0, lq, p0, lp, full + s - 1, late + s - 1, j, s > 0, trs ? trace + (blockIdx.x * (long long)maxsteps + tcount) * 16 : nullptr);
-      if (trs) T(4);
+      // late wait (the barrier also publishes the mirror writes)
+      if (has_pred && tid == 0) poll_counter(late + s - 1, j + 2);
+      __syncthreads();
+      if (trs) T(1);
+      late_load(Db, Ob, AB, ldab, q0, lq, p0, lp);
+      __syncthreads();
+      if (trs) T(2);
       // A: w = tau O v
       {
         double a = 0.0;
@@ -465,7 +485,6 @@ __global__ void __launch_bounds__(kSbThreads) sb2st_fused_kernel(double* AB, int
         if (q == 0) sm.w[mi] = tau * a;
       }
       __syncthreads();
-      if (trs) T(5);
       // B: vn = house(O[:, 0] - w), per warp
       double* vn = sm.vnw[warp];
       double taun = 0.0, betan;
@@ -489,7 +508,6 @@ __global__ void __launch_bounds__(kSbThreads) sb2st_fused_kernel(double* AB, int
         swv = warp_sum(sm.w[lane] * vn0 + sm.w[lane + 32] * vn1);
         __syncwarp();
       }
-      if (trs) T(6);
       // C: t = taun D vn, y = taun (O^T vn - v swv)
       {
         double tc = 0.0, gc = 0.0;
@@ -510,116 +528,140 @@ __global__ void __launch_bounds__(kSbThreads) sb2st_fused_kernel(double* AB, int
         }
       }
       __syncthreads();
-      if (trs) T(7);
-      // D: warp 0 publishes row 0 of O'' and D''(0, 0) (the successor's late
-      // data); then every warp stores its share of the rest (16-byte row pairs).
-      {
-        const double gm = warp_sum(sm.tt[lane] * vn[lane] + sm.tt[lane + 32] * vn[lane + 32]);
-        const double al = -0.5 * taun * gm;
-        if (warp == 0) {
+      if (trs) T(3);
+      // next step's geometry
+      const int nq0 = q1 + 1;
+      const bool has_next = nq0 <= n - 1;
+      const int nq1 = min(q1 + b, n - 1);
+      const int nlq = nq1 - nq0 + 1;
+      const double gm = warp_sum(sm.tt[lane] * vn[lane] + sm.tt[lane + 32] * vn[lane + 32]);
+      const double al = -0.5 * taun * gm;
+      if (warp == 0) {
+        // publish the successor's late data: row 0 of O'' and D''(0, 0)
 #pragma unroll
-          for (int h = 0; h < 2; ++h) {
-            const int c = lane + 32 * h;
-            if (c < lp) {
-              const double val = c == 0 ? betan : Ob[c * kLd2] - sm.w[0] * v[c] - sm.y[c];
-              AB[(long long)(p0 + c) * ldab + (q0 - p0 - c)] = val;
-            }
-          }
-          if (lane == 0) AB[(long long)q0 * ldab] = Db[0] - 2.0 * (sm.tt[0] + al);
-          __syncwarp();
-          if (lane == 0) {
-            __threadfence();
-            st_release(late + s, j + 1);
-            if (trs) T(8);
+        for (int h = 0; h < 2; ++h) {
+          const int c = lane + 32 * h;
+          if (c < lp) {
+            const double val = c == 0 ? betan : Ob[c * kLd2] - sm.w[0] * v[c] - sm.y[c];
+            AB[(long long)(p0 + c) * ldab + (q0 - p0 - c)] = val;
           }
         }
-        if (warp == 1) {
-          V2[((long long)s * maxsteps + j) * b + lane] = vn[lane];
-          V2[((long long)s * maxsteps + j) * b + lane + 32] = vn[lane + 32];
-          sm.vbuf[(j + 1) & 1][lane] = vn[lane];
-          sm.vbuf[(j + 1) & 1][lane + 32] = vn[lane + 32];
-          if (lane == 0) tau2[(long long)s * maxsteps + j] = taun;
-        }
-        if (lq == kMaxPanel && lp == kMaxPanel) {
-          // 4 threads per column; warp 0 (late from publishing) gets the
-          // columns with the shortest D segments
-          const int c = kMaxPanel - 1 - (tid >> 2), kq = tid & 3;
-          double* od = AB + (long long)(p0 + c) * ldab + (q0 - p0 - c);
-          double* dd = AB + (long long)(q0 + c) * ldab - c;
-          const double vc = v[c], yc = sm.y[c];
-          const double vnc = vn[c], w2c = sm.tt[c] + al * vnc;
-          const int dlo = c > 1 ? c : 1;
-#pragma unroll
-          for (int i = 0; i < 9; ++i) {
-            const int k = kq + 4 * i;
-            if (k <= 32) {
-              const int r0 = 2 * k - sh, r1 = r0 + 1;
-              const bool in0 = r0 >= 1 && r0 < kMaxPanel, in1 = r1 >= 1 && r1 < kMaxPanel;
-              double o0 = 0.0, o1 = 0.0;
-              if (c > 0) {
-                if (in0) o0 = Ob[c * kLd2 + r0] - sm.w[r0] * vc - vn[r0] * yc;
-                if (in1) o1 = Ob[c * kLd2 + r1] - sm.w[r1] * vc - vn[r1] * yc;
-              }
-              if (in0 && in1) st_global_v2(od + r0, o0, o1);
-              else if (in0) od[r0] = o0;
-              else if (in1) od[r1] = o1;
-              const bool d0 = in0 && r0 >= dlo, d1 = in1 && r1 >= dlo;
-              double e0 = 0.0, e1 = 0.0;
-              if (d0) e0 = Db[c * kLd2 + r0] - (vn[r0] * w2c + (sm.tt[r0] + al * vn[r0]) * vnc);
-              if (d1) e1 = Db[c * kLd2 + r1] - (vn[r1] * w2c + (sm.tt[r1] + al * vn[r1]) * vnc);
-              if (d0 && d1) st_global_v2(dd + r0, e0, e1);
-              else if (d0) dd[r0] = e0;
-              else if (d1) dd[r1] = e1;
-            }
-          }
-        } else {
-          constexpr int kTotal = 2 * kMaxPanel * kPairSlots;
-          for (int t = tid; t < kTotal; t += kSbThreads) {
-            const bool isO = t >= kMaxPanel * kPairSlots;
-            const int u = isO ? t - kMaxPanel * kPairSlots : t;
-            const int c = u / kPairSlots, k = u - kPairSlots * c;
-            const int r0 = 2 * k - sh, r1 = r0 + 1;
-            if (r0 >= lq) continue;
-            double val0 = 0.0, val1 = 0.0;
-            bool ok0, ok1;
-            double* dst;
-            if (isO) {
-              if (c >= lp) continue;
-              ok0 = r0 >= 1;
-              ok1 = r1 >= 1 && r1 < lq;
-              dst = AB + (long long)(p0 + c) * ldab + (q0 + r0 - p0 - c);
-              if (c > 0) {
-                const double vc = v[c], yc = sm.y[c];
-                if (ok0) val0 = Ob[c * kLd2 + r0] - sm.w[r0] * vc - vn[r0] * yc;
-                if (ok1) val1 = Ob[c * kLd2 + r1] - sm.w[r1] * vc - vn[r1] * yc;
-              }
-            } else {
-              ok0 = r0 >= 1 && r0 >= c;
-              ok1 = r1 >= 1 && r1 >= c && r1 < lq;
-              if (!ok0 && !ok1) continue;
-              dst = AB + (long long)(q0 + c) * ldab + (r0 - c);
-              const double vc = vn[c], w2c = sm.tt[c] + al * vc;
-              if (ok0) val0 = Db[c * kLd2 + r0] - (vn[r0] * w2c + (sm.tt[r0] + al * vn[r0]) * vc);
-              if (ok1) val1 = Db[c * kLd2 + r1] - (vn[r1] * w2c + (sm.tt[r1] + al * vn[r1]) * vc);
-            }
-            if (ok0 && ok1) st_global_v2(dst, val0, val1);
-            else if (ok0) dst[0] = val0;
-            else if (ok1) dst[1] = val1;
-          }
-        }
-        // each warp publishes its own bulk stores: full[s] reaches
-        // kBulkWarps * (j + 1) once step j is completely stored
+        if (lane == 0) AB[(long long)q0 * ldab] = Db[0] - 2.0 * (sm.tt[0] + al);
         __syncwarp();
         if (lane == 0) {
           __threadfence();
-          atomicAdd(full + s, 1);
+          st_release(late + s, j + 1);
+          if (trs) T(4);
         }
       }
+      if (warp == 1) {
+        V2[((long long)s * maxsteps + j) * b + lane] = vn[lane];
+        V2[((long long)s * maxsteps + j) * b + lane + 32] = vn[lane + 32];
+        sm.vbuf[(j + 1) & 1][lane] = vn[lane];
+        sm.vbuf[(j + 1) & 1][lane + 32] = vn[lane + 32];
+        if (lane == 0) tau2[(long long)s * maxsteps + j] = taun;
+      }
+      // D: the bulk of O'' and D'' (rows >= 1)
+      if (lq == kMaxPanel && lp == kMaxPanel) {
+        const int c = kMaxPanel - 1 - (tid >> 2), kq = tid & 3;
+        double* od = AB + (long long)(p0 + c) * ldab + (q0 - p0 - c);
+        double* dd = AB + (long long)(q0 + c) * ldab - c;
+        const double vc = v[c], yc = sm.y[c];
+        const double vnc = vn[c], w2c = sm.tt[c] + al * vnc;
+        const int dlo = c > 1 ? c : 1;
+#pragma unroll
+        for (int i = 0; i < 9; ++i) {
+          const int k = kq + 4 * i;
+          if (k <= 32) {
+            const int r0 = 2 * k - sh, r1 = r0 + 1;
+            const bool in0 = r0 >= 1 && r0 < kMaxPanel, in1 = r1 >= 1 && r1 < kMaxPanel;
+            double o0 = 0.0, o1 = 0.0;
+            if (c > 0) {
+              if (in0) o0 = Ob[c * kLd2 + r0] - sm.w[r0] * vc - vn[r0] * yc;
+              if (in1) o1 = Ob[c * kLd2 + r1] - sm.w[r1] * vc - vn[r1] * yc;
+            }
+            if (in0 && in1) st_global_v2(od + r0, o0, o1);
+            else if (in0) od[r0] = o0;
+            else if (in1) od[r1] = o1;
+            const bool d0 = in0 && r0 >= dlo, d1 = in1 && r1 >= dlo;
+            double e0 = 0.0, e1 = 0.0;
+            if (d0) e0 = Db[c * kLd2 + r0] - (vn[r0] * w2c + (sm.tt[r0] + al * vn[r0]) * vnc);
+            if (d1) e1 = Db[c * kLd2 + r1] - (vn[r1] * w2c + (sm.tt[r1] + al * vn[r1]) * vnc);
+            if (d0 && d1) st_global_v2(dd + r0, e0, e1);
+            else if (d0) dd[r0] = e0;
+            else if (d1) dd[r1] = e1;
+          }
+        }
+      } else {
+        constexpr int kTotal = 2 * kMaxPanel * kPairSlots;
+        for (int t = tid; t < kTotal; t += kSbThreads) {
+          const bool isO = t >= kMaxPanel * kPairSlots;
+          const int u = isO ? t - kMaxPanel * kPairSlots : t;
+          const int c = u / kPairSlots, k = u - kPairSlots * c;
+          const int r0 = 2 * k - sh, r1 = r0 + 1;
+          if (r0 >= lq) continue;
+          double val0 = 0.0, val1 = 0.0;
+          bool ok0, ok1;
+          double* dst;
+          if (isO) {
+            if (c >= lp) continue;
+            ok0 = r0 >= 1;
+            ok1 = r1 >= 1 && r1 < lq;
+            dst = AB + (long long)(p0 + c) * ldab + (q0 + r0 - p0 - c);
+            if (c > 0) {
+              const double vc = v[c], yc = sm.y[c];
+              if (ok0) val0 = Ob[c * kLd2 + r0] - sm.w[r0] * vc - vn[r0] * yc;
+              if (ok1) val1 = Ob[c * kLd2 + r1] - sm.w[r1] * vc - vn[r1] * yc;
+            }
+          } else {
+            ok0 = r0 >= 1 && r0 >= c;
+            ok1 = r1 >= 1 && r1 >= c && r1 < lq;
+            if (!ok0 && !ok1) continue;
+            dst = AB + (long long)(q0 + c) * ldab + (r0 - c);
+            const double vc = vn[c], w2c = sm.tt[c] + al * vc;
+            if (ok0) val0 = Db[c * kLd2 + r0] - (vn[r0] * w2c + (sm.tt[r0] + al * vn[r0]) * vc);
+            if (ok1) val1 = Db[c * kLd2 + r1] - (vn[r1] * w2c + (sm.tt[r1] + al * vn[r1]) * vc);
+          }
+          if (ok0 && ok1) st_global_v2(dst, val0, val1);
+          else if (ok0) dst[0] = val0;
+          else if (ok1) dst[1] = val1;
+        }
+      }
+      // each warp publishes its own bulk stores: full[s] reaches
+      // kBulkWarps * (j + 1) once step j is completely stored
+      __syncwarp();
+      if (lane == 0) {
+        __threadfence();
+        atomicAdd(full + s, 1);
+      }
+      if (trs) T(5);
+      if (warp != 0 && has_next) {
+        // warps 1..7: stage step j+1's bulk into the other buffer (needs the
+        // predecessor's step j+1 fully stored) -- after our own bulk, so our
+        // `full` is never held back by our predecessor
+        if (has_pred && tid == 32) poll_counter(full + s - 1, kBulkWarps * (j + 2));
+        if (trs32) T(7);
+        named_bar(1, kSbThreads - 32);
+        const int nsh = nq0 & 1;
+        stage_bulk(sm.D[cur ^ 1] + nsh, sm.O[cur ^ 1] + nsh, AB, ldab, nq0, nlq, q0, lq, tid - 32,
+                   kSbThreads - 32);
+        cp_async_commit();
+        if (trs32) T(8);
+      }
       tau = taun;
-      if (trs) ++tcount;
+      if (!has_next) break;
+      // the next buffer has landed: mirror its D (published by the next late wait's barrier)
+      cp_async_wait<0>();
+      if (trs32) T(9);
+      __syncthreads();
+      if (trs) T(10);
+      mirror_d(sm.D[cur ^ 1] + (nq0 & 1), nlq);
+      if (trs) T(6);
       p0 = q0;
-      p1 = q1;
       lp = lq;
+      q0 = nq0;
+      q1 = nq1;
+      lq = nlq;
     }
     __syncthreads();
     if (tid == 0) {
@@ -670,7 +712,11 @@ cudaError_t sb2st(double* AB, int ldab, int n, int b, double* d, double* e, doub
     int grid = std::max(1, std::min(n - 2, std::max(1, per_sm) * num_sms));
     int maxsteps = sb2st_maxsteps(n, b);
     unsigned long long* trace = nullptr;
-    const bool want_trace = std::getenv("BSE_SB2ST_TRACE") != nullptr;
+    const char* tenv = std::getenv("BSE_SB2ST_TRACE");
+    const bool want_trace = tenv != nullptr;
+    int ts0 = want_trace ? std::atoi(tenv) : 0;
+    ts0 = std::max(0, std::min(ts0, n - 4));
+    cudaMemcpyToSymbolAsync(c_sb_trace_s0, &ts0, sizeof(int), 0, cudaMemcpyHostToDevice, s);
     const size_t tsz = (size_t)2 * maxsteps * 16;
     if (want_trace) {
       cudaMalloc(&trace, sizeof(unsigned long long) * tsz);
@@ -684,26 +730,35 @@ cudaError_t sb2st(double* AB, int ldab, int n, int b, double* d, double* e, doub
       std::vector<unsigned long long> h(tsz);
       cudaMemcpyAsync(h.data(), trace, h.size() * 8, cudaMemcpyDeviceToHost, s);
       cudaStreamSynchronize(s);
-      // per-phase averages for sweep 1 (CTA 1) over steps 8..200, plus the
-      // cross-sweep chain: sweep 0's late publish of step j+1 -> sweep 1's
-      // late-wait exit of step j
-      double acc[16] = {0}, chain = 0.0, period = 0.0;
+      // sweep ts0 + 1 (consumer) against sweep ts0 (producer): per-phase
+      // averages, step period, and the hand-off gap = consumer's late-wait
+      // exit of step j minus the producer's late release of step j + 1
+      double acc[16] = {0}, period = 0.0, gap = 0.0;
       int cnt = 0;
-      for (int j = 8; j < std::min(maxsteps - 2, 200); ++j) {
+      for (int j = 2; j < maxsteps - 2; ++j) {
         const unsigned long long* c = &h[((size_t)maxsteps + j) * 16];
-        const unsigned long long* p = &h[(size_t)(j + 1) * 16];
-        if (!c[8] || !p[8] || !h[((size_t)maxsteps + j + 1) * 16]) break;
-        for (int q = 1; q <= 8; ++q) acc[q] += (double)(c[q] - c[q - 1]);
-        chain += (double)c[3] - (double)p[8];
-        period += (double)(h[((size_t)maxsteps + j + 1) * 16] - c[0]);
+        const unsigned long long* nx = &h[((size_t)maxsteps + j + 1) * 16];
+        const unsigned long long* pr = &h[(size_t)(j + 1) * 16];
+        if (!c[6] || !nx[0] || !pr[4]) break;
+        for (int q = 1; q <= 6; ++q) acc[q] += (double)(c[q] - c[q - 1]);
+        period += (double)(nx[0] - c[0]);
+        gap += (double)c[1] - (double)pr[4];
         ++cnt;
       }
+      double e7 = 0, e8 = 0, e9 = 0, e10 = 0;
+      for (int j = 2; j < 2 + cnt; ++j) {
+        const unsigned long long* c = &h[((size_t)maxsteps + j) * 16];
+        e7 += (double)c[7] - (double)c[5];
+        e8 += (double)c[8] - (double)c[7];
+        e9 += (double)c[9] - (double)c[5];
+        e10 += (double)c[10] - (double)c[9];
+      }
       const double d = std::max(cnt, 1) * 1e3;
-      std::fprintf(stderr, "[sb2st trace] steps=%d us: fullwait %.2f issue %.2f mirror+latewait %.2f "
-                   "lateload %.2f A %.2f B %.2f C %.2f publish %.2f | period %.2f\n",
-                   cnt, acc[1] / d, acc[2] / d, acc[3] / d, acc[4] / d, acc[5] / d, acc[6] / d,
-                   acc[7] / d, acc[8] / d, period / d);
-      (void)chain;
+      std::fprintf(stderr, "[sb2st trace] after bulk(t0): poll %.2f issue %.2f | after own bulk: arrive(t32) %.2f sync %.2f\n",
+                   e7 / d, e8 / d, e9 / d, e10 / d);
+      std::fprintf(stderr, "[sb2st trace] sweep %d steps=%d us: latewait %.2f lateload %.2f ABC %.2f publish %.2f "
+                   "bulk %.2f arrive+mirror %.2f | period %.2f handoff %.2f\n", ts0 + 1, cnt, acc[1] / d,
+                   acc[2] / d, acc[3] / d, acc[4] / d, acc[5] / d, acc[6] / d, period / d, gap / d);
     }
     if (trace) cudaFree(trace);
   }
