@@ -11,58 +11,95 @@ constexpr int kLeaf = 64;
 constexpr int kLds = kLeaf + 1;
 
 // --- POTF2: in-place lower Cholesky of an n x n (n <= 64) diagonal block ---
-__global__ void __launch_bounds__(256) potf2_kernel(double* A, long long lda, int n, int off,
-                                                    DevStatus* st, double* inv) {
+// A single-CTA leaf sits on the critical path of every recursion level, so it
+// is written for latency with a small, rolled instruction stream: two threads
+// per row keep its column halves in registers; the current column is always
+// register 0 (the owning half shifts its registers once per column), so no
+// register array is ever indexed dynamically.  Column j is broadcast through
+// a double-buffered shared vector (one barrier per column) and the
+// elimination runs unscaled (T_rc -= T_rj T_cj / T_jj; L_rc = T_rc / sqrt(T_cc)
+// at the end).  The leaf inverse (cached for every TRSM leaf of the solve) is
+// formed the same way by right-looking elimination of the identity.
+constexpr int kHalf = kLeaf / 2;
+__global__ void __launch_bounds__(2 * kLeaf) potf2_kernel(double* A, long long lda, int n, int off,
+                                                          DevStatus* st, double* inv) {
   extern __shared__ double dyn[];
-  double* T = dyn;                    // column-major, T[c*kLds + r]
-  double* Y = dyn + kLeaf * kLds;     // inverse, column-major
-  if (st->info >= 0) return;          // an earlier block already failed
-  const int tid = threadIdx.x;
-  for (int idx = tid; idx < n * n; idx += blockDim.x) {
-    const int r = idx % n, c = idx / n;
-    T[c * kLds + r] = (r >= c) ? A[r + c * lda] : 0.0;
+  double* Ls = dyn;                    // row-major, Ls[i * kLds + k]
+  __shared__ double colj[2][kLeaf];
+  __shared__ double dsq[kLeaf];
+  if (st->info >= 0) return;           // an earlier block already failed
+  const int r = threadIdx.x & (kLeaf - 1), h = threadIdx.x >> 6;
+  const int cb = h * kHalf;            // this thread's columns: cb .. cb + 31
+  double t[kHalf];
+#pragma unroll
+  for (int q = 0; q < kHalf; ++q) {
+    const int c = cb + q;
+    t[q] = (r < n && c < n && c <= r) ? A[r + c * lda] : 0.0;
   }
   for (int j = 0; j < n; ++j) {
+    const int owner = j / kHalf;
+    double* cj = colj[j & 1];
+    if (h == owner) {
+      cj[r] = t[0];
+      Ls[r * kLds + j] = t[0];
+    }
     __syncthreads();
-    const double piv = T[j * kLds + j];
+    const double piv = cj[j];
     if (!(piv > 0.0)) {  // uniform: every thread read the same value
-      if (tid == 0) { st->info = off + j; st->value = piv; }
+      if (threadIdx.x == 0) { st->info = off + j; st->value = piv; }
       return;
     }
-    const double d = sqrt(piv);
-    const double inv = 1.0 / d;
-    __syncthreads();
-    if (tid == 0) T[j * kLds + j] = d;
-    for (int i = j + 1 + tid; i < n; i += blockDim.x) T[j * kLds + i] *= inv;
-    __syncthreads();
-    const int w = n - j - 1;
-    for (int idx = tid; idx < w * w; idx += blockDim.x) {
-      const int r = j + 1 + idx % w, c = j + 1 + idx / w;
-      if (r >= c) T[c * kLds + r] -= T[j * kLds + r] * T[j * kLds + c];
+    if (threadIdx.x == 0) dsq[j] = sqrt(piv);
+    const double a = (r > j) ? cj[r] * (1.0 / piv) : 0.0;
+    // register q holds column base + q (base advances once per owned column)
+    const int base = cb + (h == 0 ? j : max(0, j - kHalf));
+#pragma unroll
+    for (int q = 0; q < kHalf; ++q) {
+      const int c = base + q;
+      if (c > j && c <= r && c < cb + kHalf) t[q] -= a * cj[c];
+    }
+    if (h == owner) {
+#pragma unroll
+      for (int q = 0; q + 1 < kHalf; ++q) t[q] = t[q + 1];
+      t[kHalf - 1] = 0.0;
     }
   }
   __syncthreads();
-  for (int idx = tid; idx < n * n; idx += blockDim.x) {
-    const int r = idx % n, c = idx / n;
-    A[r + c * lda] = (r >= c) ? T[c * kLds + r] : 0.0;
+  // scale: L_rc = T_rc / sqrt(T_cc), write back
+  for (int idx = threadIdx.x; idx < kLeaf * kLeaf; idx += blockDim.x) {
+    const int i = idx & (kLeaf - 1), c = idx >> 6;  // i fastest: coalesced
+    double l = 0.0;
+    if (i < n && c < n) l = i > c ? Ls[i * kLds + c] / dsq[c] : (i == c ? dsq[c] : 0.0);
+    if (i < n && c < n) A[i + c * lda] = l;
   }
-  if (inv) {
-    // L^{-1} by column-parallel forward substitution (thread j owns column j;
-    // T reads are warp-broadcasts, Y reads/writes stride kLds: conflict-free)
-    const int j = tid;
-    if (j < n) {
-      for (int i = 0; i < n; ++i) {
-        double sacc = (i == j) ? 1.0 : 0.0;
-        if (i > j)
-          for (int k = j; k < i; ++k) sacc -= T[k * kLds + i] * Y[j * kLds + k];
-        Y[j * kLds + i] = (i < j) ? 0.0 : sacc / T[i * kLds + i];
-      }
+  if (!inv) return;
+  __syncthreads();
+  for (int idx = threadIdx.x; idx < kLeaf * kLeaf; idx += blockDim.x) {
+    const int i = idx >> 6, c = idx & (kLeaf - 1);
+    if (i < n && c < n) Ls[i * kLds + c] = i > c ? Ls[i * kLds + c] / dsq[c] : (i == c ? dsq[c] : 0.0);
+  }
+  // Y = L^{-1}: rows kept unscaled, row j broadcast, Y_r -= (L_rj / L_jj) Y_j
+  double y[kHalf];
+#pragma unroll
+  for (int q = 0; q < kHalf; ++q) y[q] = (cb + q == r) ? 1.0 : 0.0;
+  __syncthreads();
+  for (int j = 0; j < n; ++j) {
+    double* yj = colj[j & 1];
+    if (r == j) {
+#pragma unroll
+      for (int q = 0; q < kHalf; ++q) yj[cb + q] = y[q];
     }
     __syncthreads();
-    for (int idx = tid; idx < kLeaf * kLeaf; idx += blockDim.x) {
-      const int r = idx % kLeaf, c = idx / kLeaf;
-      inv[r + c * kLeaf] = (r < n && c < n) ? Y[c * kLds + r] : 0.0;
-    }
+    const double a = (r > j) ? Ls[r * kLds + j] / Ls[j * kLds + j] : 0.0;
+#pragma unroll
+    for (int q = 0; q < kHalf; ++q)
+      if (cb + q <= j) y[q] -= a * yj[cb + q];
+  }
+  const double rd = (r < n) ? 1.0 / Ls[r * kLds + r] : 0.0;
+#pragma unroll
+  for (int q = 0; q < kHalf; ++q) {
+    const int c = cb + q;
+    inv[r + c * kLeaf] = (r < n && c < n) ? y[q] * rd : 0.0;
   }
 }
 
@@ -303,7 +340,7 @@ static cudaError_t potrf_rec(double* A, long long lda, int n, int off, DevStatus
                              cudaStream_t s, double* inv) {
   if (n <= kLeaf) {
     ensure_smem<potf2_kernel>();
-    potf2_kernel<<<1, 256, kLeafSmem, s>>>(A, lda, n, off, st, inv);
+    potf2_kernel<<<1, 2 * kLeaf, kLeafSmem, s>>>(A, lda, n, off, st, inv);
     count_launch();
     return cudaGetLastError();
   }
