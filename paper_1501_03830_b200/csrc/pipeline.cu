@@ -243,9 +243,13 @@ cudaError_t solve_spd_pair(int n, const double* M, long long ldm, const double* 
   g1.ma = Mask::lower();
   g1.mb = Mask::lower();
   if ((e = gemm(false, false, g1, s)) != cudaSuccess) return e;
+  // only T1's lower triangle feeds W = L^T T1 (lower): the strictly-upper
+  // half of M's contribution is needed for rows k >= j only (N^3/3 flops
+  // saved); g1 has already zeroed T1's upper triangle (k-range empty there)
   GemmProblem g2 = make_gemm(n, n, n, 1.0, M, ldm, w.L, ld, 1.0, w.T1, ld);
   g2.ma = Mask::strict_lower();
   g2.mb = Mask::lower();
+  g2.mc = Mask::lower();
   if ((e = gemm(true, false, g2, s)) != cudaSuccess) return e;
   GemmProblem g3 = make_gemm(n, n, n, 1.0, w.L, ld, w.T1, ld, 0.0, w.W, ld);
   g3.ma = Mask::lower();
