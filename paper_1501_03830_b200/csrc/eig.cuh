@@ -12,17 +12,17 @@ namespace bse {
 constexpr int kMaxPanel = 64;  // SY2SB bandwidth b (<= 64)
 
 struct Sy2sbScratch {
-  double* vwv = nullptr;  // m x 3b: [V | W | V]
+  double* vwv = nullptr;  // 8 slots of b columns: V1 W1 V2 W2 | W1c V1c W2c V2c (sy2sb)
   long long ldvwv = 0;
   double* y = nullptr;    // m x b
   long long ldy = 0;
-  double* z = nullptr;    // b x b
+  double* z = nullptr;    // 2b x b
   double* z2 = nullptr;   // b x b
   double* red = nullptr;  // panel-QR grid reduction (2 * 148 * (2 + 2b))
   unsigned* bar = nullptr;
   double* splitk_ws = nullptr;  // 48 * b * b
   double* symm_ws = nullptr;    // kSymmSplits * ld * b
-  GemmProblem* probs = nullptr; // 96 problems
+  GemmProblem* probs = nullptr; // 128 problems (split-K descriptors at +0, +32, +64)
 };
 constexpr int kSymmSplits = 16;
 
@@ -31,7 +31,7 @@ cudaError_t sy2sb(double* A, long long lda, int n, int b, double* Vall, long lon
 cudaError_t extract_band(const double* A, long long lda, int n, int b, double* AB, int ldab,
                          cudaStream_t s);
 
-// Bulge chasing on the band (lower storage, ldab = 2b): d, e out; reflectors
+// Bulge chasing on the band (lower storage, ldab = 2b + 1): d, e out; reflectors
 // of sweep s, step j stored at V2[(s*maxsteps + j) * b], tau2[s*maxsteps + j].
 int sb2st_maxsteps(int n, int b);
 cudaError_t sb2st(double* AB, int ldab, int n, int b, double* d, double* e, double* V2,

@@ -63,16 +63,16 @@ SyevdWork carve_syevd(Arena& a, int n) {
   w.Vall = a.take<double>((size_t)ld * n);
   w.Tall = a.take<double>((size_t)np * b * b);
   w.sc.ldvwv = ld;
-  w.sc.vwv = a.take<double>((size_t)ld * 3 * b);
+  w.sc.vwv = a.take<double>((size_t)ld * 8 * b);  // V1 W1 V2 W2 | W1c V1c W2c V2c
   w.sc.ldy = ld;
   w.sc.y = a.take<double>((size_t)ld * b);
-  w.sc.z = a.take<double>((size_t)b * b);
+  w.sc.z = a.take<double>(2 * (size_t)b * b);
   w.sc.z2 = a.take<double>((size_t)b * b);
   w.sc.red = a.take<double>(2 * 192 * (2 + 2 * (size_t)b));
   w.sc.bar = a.take<unsigned>(4);
   w.sc.splitk_ws = a.take<double>(64 * (size_t)b * b);
   w.sc.symm_ws = a.take<double>((size_t)kSymmSplits * ld * b);
-  w.sc.probs = a.take<GemmProblem>(96);
+  w.sc.probs = a.take<GemmProblem>(128);
   w.ldab = 2 * b + 1;  // element (i, j) at 128 j + i: 2-D tiles with a 1 KB stride
   w.AB = a.take<double>((size_t)w.ldab * n);
   w.d = a.take<double>(n);

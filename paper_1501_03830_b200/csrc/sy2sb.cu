@@ -295,63 +295,134 @@ cudaError_t extract_band(const double* A, long long lda, int n, int b, double* A
   return cudaGetLastError();
 }
 
+namespace {
+
+// Y (m x b, in w.y) = A2 V with A2 symmetric (lower triangle referenced),
+// as two masked split-K GEMMs (the triangular masks give row blocks very
+// different k-ranges; splitting K balances them and fills the GPU).
+cudaError_t symm_panel(const double* A2, long long lda, int m, int bw, const double* V,
+                       long long ldv, const Sy2sbScratch& w, cudaStream_t s) {
+  const int ssplit = (int)std::min<long long>(kSymmSplits, std::max<long long>(1, m / 1024));
+  GemmProblem g1 = make_gemm(m, bw, m, 1.0, A2, lda, V, ldv, 0.0, w.y, w.ldy);
+  g1.ma = Mask::lower();
+  cudaError_t e = gemm_splitk(false, false, g1, ssplit, w.symm_ws, w.probs, s);
+  if (e != cudaSuccess) return e;
+  GemmProblem g2 = make_gemm(m, bw, m, 1.0, A2, lda, V, ldv, 1.0, w.y, w.ldy);
+  g2.ma = Mask::strict_lower();
+  return gemm_splitk(true, false, g2, ssplit, w.symm_ws, w.probs + 32, s);
+}
+
+// W = X - 1/2 V (T^T (V^T X)), X = Y T  (Y in w.y): the two-sided update
+// A - V W^T - W V^T of one panel (compact WY, LAPACK dsytrd's LATRD form).
+cudaError_t panel_w(int m, int bw, const double* V, long long ldv, const double* Tp, double* W,
+                    long long ldw, const Sy2sbScratch& w, cudaStream_t s) {
+  cudaError_t e;
+  GemmProblem g3 = make_gemm(m, bw, bw, 1.0, w.y, w.ldy, Tp, bw, 0.0, W, ldw);
+  g3.mb = Mask::upper();
+  if ((e = gemm(false, false, g3, s)) != cudaSuccess) return e;
+  stage_mark("sy2sb_small", s);
+  GemmProblem g4 = make_gemm(bw, bw, m, 1.0, V, ldv, W, ldw, 0.0, w.z, bw);
+  const int splits = (int)std::min<long long>(48, std::max<long long>(1, m / 256));
+  if ((e = gemm_splitk(true, false, g4, splits, w.splitk_ws, w.probs + 64, s)) != cudaSuccess) return e;
+  GemmProblem g5 = make_gemm(bw, bw, bw, 1.0, Tp, bw, w.z, bw, 0.0, w.z2, bw);
+  g5.ma = Mask::upper();
+  if ((e = gemm(true, false, g5, s)) != cudaSuccess) return e;
+  GemmProblem g6 = make_gemm(m, bw, bw, -0.5, V, ldv, w.z2, bw, 1.0, W, ldw);
+  return gemm(false, false, g6, s);
+}
+
+}  // namespace
+
 // Full -> band.  A (n x n, lower triangle referenced) is overwritten: its
 // lower band holds the band matrix, panel regions hold R, rest is garbage.
 // Vall (ldv): reflectors of panel p at rows k+b.., cols k..k+b-1 (k = p*b);
 // Tall: bw x bw T factors, one per panel.
+//
+// Panels are processed in PAIRS with one aggregated rank-4b trailing update
+// (the band analogue of LAPACK's LATRD look-ahead): after panel p only the
+// next panel's b columns are updated; panel p+1's SYMM runs on the stale
+// trailing matrix and is corrected with two thin products,
+//   A3_true V2 = A3 V2 - V1' (W1'^T V2) - W1' (V1'^T V2),
+// and the trailing matrix is then updated once,
+//   A3 -= [V1' V2 W1' W2] [W1' W2 V1' V2]^T   (lower, K = 4b),
+// halving the read-modify-write passes of the SYR2K and doubling its depth.
+// Scratch slots (ld lw, b columns each): V1 W1 V2 W2 | W1c V1c W2c V2c (the
+// right half copies the left in swapped pairs), the second panel's columns
+// sit b rows down so every slot shares the trailing row index.  Then
+// [V1 W1] [W1c V1c]^T, [W1c V1c]^T V2 and [V1 W1 V2 W2] [W1c V1c W2c V2c]^T
+// are single GEMMs.
 cudaError_t sy2sb(double* A, long long lda, int n, int b, double* Vall, long long ldv,
                   double* Tall, const Sy2sbScratch& w, int num_sms, cudaStream_t s) {
   cudaError_t e = cudaSuccess;
-  for (int p = 0;; ++p) {
+  const int bw = b;
+  const long long lw = w.ldvwv;
+  double* slot[8];
+  for (int i = 0; i < 8; ++i) slot[i] = w.vwv + i * lw * bw;
+  double *sV1 = slot[0], *sW1 = slot[1], *sV2 = slot[2], *sW2 = slot[3];
+  double *sW1c = slot[4], *sV1c = slot[5], *sW2c = slot[6], *sV2c = slot[7];
+  auto copy_cols = [&](double* dst, const double* src, int rows) {
+    return cudaMemcpy2DAsync(dst, lw * sizeof(double), src, lw * sizeof(double),
+                             (size_t)rows * sizeof(double), bw, cudaMemcpyDeviceToDevice, s);
+  };
+  for (int p = 0;; p += 2) {
     const int k = p * b;
     const int m = n - k - b;
     if (m < 2) break;
-    const int bw = b;
-    double* P = A + (k + b) + (long long)k * lda;
+    double* P1 = A + (k + b) + (long long)k * lda;
     double* A2 = A + (k + b) + (long long)(k + b) * lda;
-    double* Vp = Vall + (k + b) + (long long)k * ldv;
-    double* Tp = Tall + (size_t)p * b * b;
-    const long long lw = w.ldvwv;
-    double* slot0 = w.vwv;
-    double* slot1 = w.vwv + lw * bw;
-    double* slot2 = w.vwv + 2 * lw * bw;
+    double* Tp1 = Tall + (size_t)p * b * b;
     stage_mark("sy2sb_panel", s);
-    e = panel_qr(P, lda, m, bw, Vp, ldv, slot0, lw, Tp, w.red, w.bar, num_sms, s);
-    if (e != cudaSuccess) return e;
-    e = cudaMemcpy2DAsync(slot2, lw * sizeof(double), slot0, lw * sizeof(double),
-                          (size_t)m * sizeof(double), bw, cudaMemcpyDeviceToDevice, s);
+    e = panel_qr(P1, lda, m, bw, Vall + (k + b) + (long long)k * ldv, ldv, sV1, lw, Tp1, w.red,
+                 w.bar, num_sms, s);
     if (e != cudaSuccess) return e;
     stage_mark("sy2sb_symm", s);
-    // Y = tril(A2) V + tril(A2,-1)^T V
-    // (split-K: the triangular masks give row blocks very different k-ranges;
-    //  splitting K balances them and fills the GPU with thin m x b outputs)
-    const int ssplit = (int)std::min<long long>(kSymmSplits, std::max<long long>(1, m / 1024));
-    GemmProblem g1 = make_gemm(m, bw, m, 1.0, A2, lda, slot0, lw, 0.0, w.y, w.ldy);
-    g1.ma = Mask::lower();
-    if ((e = gemm_splitk(false, false, g1, ssplit, w.symm_ws, w.probs, s)) != cudaSuccess) return e;
-    GemmProblem g2 = make_gemm(m, bw, m, 1.0, A2, lda, slot0, lw, 1.0, w.y, w.ldy);
-    g2.ma = Mask::strict_lower();
-    if ((e = gemm_splitk(true, false, g2, ssplit, w.symm_ws, w.probs + 32, s)) != cudaSuccess)
-      return e;
-    // X = Y T -> slot1
-    GemmProblem g3 = make_gemm(m, bw, bw, 1.0, w.y, w.ldy, Tp, bw, 0.0, slot1, lw);
-    g3.mb = Mask::upper();
-    if ((e = gemm(false, false, g3, s)) != cudaSuccess) return e;
+    if ((e = symm_panel(A2, lda, m, bw, sV1, lw, w, s)) != cudaSuccess) return e;
+    if ((e = panel_w(m, bw, sV1, lw, Tp1, sW1, lw, w, s)) != cudaSuccess) return e;
+    if ((e = copy_cols(sW1c, sW1, m)) != cudaSuccess) return e;
+    if ((e = copy_cols(sV1c, sV1, m)) != cudaSuccess) return e;
+    const int m2 = m - b;
+    if (m2 < 2) {
+      // last panel: plain rank-2b update A2 -= [V1 W1] [W1 V1]^T
+      stage_mark("sy2sb_syr2k", s);
+      GemmProblem g = make_gemm(m, m, 2 * bw, -1.0, sV1, lw, sW1c, lw, 1.0, A2, lda);
+      g.mc = Mask::lower();
+      if ((e = gemm(false, true, g, s)) != cudaSuccess) return e;
+      break;
+    }
     stage_mark("sy2sb_small", s);
-    // Zs = V^T X (bw x bw), split-K
-    GemmProblem g4 = make_gemm(bw, bw, m, 1.0, slot0, lw, slot1, lw, 0.0, w.z, bw);
-    const int splits = (int)std::min<long long>(48, std::max<long long>(1, m / 256));
-    if ((e = gemm_splitk(true, false, g4, splits, w.splitk_ws, w.probs, s)) != cudaSuccess) return e;
-    // Z2 = T^T Zs
-    GemmProblem g5 = make_gemm(bw, bw, bw, 1.0, Tp, bw, w.z, bw, 0.0, w.z2, bw);
-    g5.ma = Mask::upper();
-    if ((e = gemm(true, false, g5, s)) != cudaSuccess) return e;
-    // W = X - 0.5 V Z2 (in slot1)
-    GemmProblem g6 = make_gemm(m, bw, bw, -0.5, slot0, lw, w.z2, bw, 1.0, slot1, lw);
-    if ((e = gemm(false, false, g6, s)) != cudaSuccess) return e;
+    // next panel block (and the diagonal block above it):
+    // A2[:, 0:b] -= [V1 W1] [W1 V1][0:b, :]^T
+    {
+      GemmProblem g = make_gemm(m, bw, 2 * bw, -1.0, sV1, lw, sW1c, lw, 1.0, A2, lda);
+      g.mc = Mask::lower();
+      if ((e = gemm(false, true, g, s)) != cudaSuccess) return e;
+    }
+    // panel p+1 on the updated columns
+    double* P2 = A2 + b;  // rows k+2b.., cols k+b..k+2b-1
+    double* A3 = A2 + b + (long long)b * lda;
+    double* Tp2 = Tall + (size_t)(p + 1) * b * b;
+    stage_mark("sy2sb_panel", s);
+    e = panel_qr(P2, lda, m2, bw, Vall + (k + 2 * b) + (long long)(k + b) * ldv, ldv, sV2 + b, lw,
+                 Tp2, w.red, w.bar, num_sms, s);
+    if (e != cudaSuccess) return e;
+    stage_mark("sy2sb_symm", s);
+    if ((e = symm_panel(A3, lda, m2, bw, sV2 + b, lw, w, s)) != cudaSuccess) return e;
+    stage_mark("sy2sb_small", s);
+    {
+      // Y2 -= [V1' W1'] S,  S = [W1' V1']^T V2  (2b x b, split-K into z:z2)
+      const int splits = (int)std::min<long long>(48, std::max<long long>(1, m2 / 256));
+      GemmProblem g = make_gemm(2 * bw, bw, m2, 1.0, sW1c + b, lw, sV2 + b, lw, 0.0, w.z, 2 * bw);
+      if ((e = gemm_splitk(true, false, g, splits, w.splitk_ws, w.probs + 64, s)) != cudaSuccess)
+        return e;
+      GemmProblem c = make_gemm(m2, bw, 2 * bw, -1.0, sV1 + b, lw, w.z, 2 * bw, 1.0, w.y, w.ldy);
+      if ((e = gemm(false, false, c, s)) != cudaSuccess) return e;
+    }
+    if ((e = panel_w(m2, bw, sV2 + b, lw, Tp2, sW2 + b, lw, w, s)) != cudaSuccess) return e;
+    if ((e = copy_cols(sW2c + b, sW2 + b, m2)) != cudaSuccess) return e;
+    if ((e = copy_cols(sV2c + b, sV2 + b, m2)) != cudaSuccess) return e;
+    // one rank-4b trailing update: A3 -= [V1' W1' V2 W2] [W1' V1' W2 V2]^T (lower)
     stage_mark("sy2sb_syr2k", s);
-    // A2 -= [V W][W V]^T (lower)
-    GemmProblem g7 = make_gemm(m, m, 2 * bw, -1.0, slot0, lw, slot1, lw, 1.0, A2, lda);
+    GemmProblem g7 = make_gemm(m2, m2, 4 * bw, -1.0, sV1 + b, lw, sW1c + b, lw, 1.0, A3, lda);
     g7.mc = Mask::lower();
     if ((e = gemm(false, true, g7, s)) != cudaSuccess) return e;
   }
