@@ -371,14 +371,16 @@ cudaError_t gemm(bool transA, bool transB, const GemmProblem& p, cudaStream_t s)
   const bool v2 = aligned16(p.A) && aligned16(p.B) && ((p.lda | p.ldb) & 1) == 0;
   // 128x64 tiles, 8 warps of 32x32, 2 CTAs/SM (cfg 3) measured 32-33 TFLOP/s
   // on large FP64 GEMMs (86-90% of the DMMA peak); 64x64 for small outputs.
+  // Transposed A: 128x64x32 tiles, 2 stages (measured 33.5 vs 30.7 TFLOP/s
+  // for the k-contiguous A fragments of V^T Z / L^T B).
   const long long big_tiles = ceil_div(p.M, 128) * ceil_div(p.N, 64);
-  int cfg = (v2 && big_tiles >= 148) ? 3 : 1;
+  int cfg = (v2 && big_tiles >= 148) ? (transA ? 4 : 3) : 1;
   static int forced = -2;
   if (forced == -2) {
     const char* v = std::getenv("BSE_GEMM_CFG");
     forced = v ? std::atoi(v) : -1;
   }
-  if (forced >= 0 && cfg == 3) cfg = forced;
+  if (forced >= 0 && (cfg == 3 || cfg == 4)) cfg = forced;
   return dispatch_all(transA, transB, cfg, v2 ? 2 : 1, &p, nullptr, 1, p.M, p.N, s);
 }
 
