@@ -452,9 +452,6 @@ __global__ void __launch_bounds__(kSbThreads) sb2st_fused_kernel(double* AB, int
     __syncthreads();
     stage_bulk(sm.D[0] + (q0 & 1), sm.O[0] + (q0 & 1), AB, ldab, q0, lq, p0, lp, tid, kSbThreads);
     cp_async_commit();
-    cp_async_wait<0>();
-    __syncthreads();
-    mirror_d(sm.D[0] + (q0 & 1), lq);
     for (int j = 0;; ++j) {
       const int cur = j & 1;
       const int sh = q0 & 1;
@@ -463,10 +460,13 @@ __global__ void __launch_bounds__(kSbThreads) sb2st_fused_kernel(double* AB, int
       const double* v = sm.vbuf[j & 1];
       tj = j;
       if (trs) T(0);
-      // late wait (the barrier also publishes the mirror writes)
+      // late wait, overlapping the arrival of this step's staged bulk; then
+      // mirror D and load the late row (disjoint positions, one barrier)
       if (has_pred && tid == 0) poll_counter(late + s - 1, j + 2);
+      cp_async_wait<0>();
       __syncthreads();
       if (trs) T(1);
+      mirror_d(Db, lq);
       late_load(Db, Ob, AB, ldab, q0, lq, p0, lp);
       __syncthreads();
       if (trs) T(2);
@@ -650,12 +650,6 @@ __global__ void __launch_bounds__(kSbThreads) sb2st_fused_kernel(double* AB, int
       }
       tau = taun;
       if (!has_next) break;
-      // the next buffer has landed: mirror its D (published by the next late wait's barrier)
-      cp_async_wait<0>();
-      if (trs32) T(9);
-      __syncthreads();
-      if (trs) T(10);
-      mirror_d(sm.D[cur ^ 1] + (nq0 & 1), nlq);
       if (trs) T(6);
       p0 = q0;
       lp = lq;
@@ -666,6 +660,367 @@ __global__ void __launch_bounds__(kSbThreads) sb2st_fused_kernel(double* AB, int
     __syncthreads();
     if (tid == 0) {
       __threadfence();
+      st_release(late + s, kDone);
+      st_release(full + s, kDone);
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Pair kernel (default).  One CTA chases TWO consecutive sweeps, leader s
+// (even) and follower s+1, interleaved step by step: round j = leader step
+// j+1, then follower step j.  The follower's blocks are the leader's step-j
+// blocks shifted by one row and column -- still in shared memory, updated in
+// place by the leader -- plus one new row/column: the leader's step-(j+1)
+// row 0 (also in shared memory) and 63 band entries already final in global
+// memory.  So half of all cross-sweep hand-offs never leave the SM: no flag,
+// no fence, no L2 round trip.  Only the follower publishes (late/full
+// counters, as in the fused kernel) for the next pair's leader; the leader
+// waits on the previous pair's follower.  Three shared block sets rotate:
+// leader step J uses set J mod 3, the follower reuses it one round later,
+// and the leader's step J+1 stages into the third.
+constexpr int kLdc = kMaxPanel + 1;  // 65 columns: the follower's view reaches column 64
+constexpr int kSetD = kLdc * kLd2 + 2;
+
+struct SbpSmem {
+  double D[3][kSetD];
+  double O[3][kSetD];
+  double vbuf[2][2][kMaxPanel];  // [leader / follower][parity]
+  double vnw[kSbThreads / 32][kMaxPanel];
+  double w[kMaxPanel];
+  double y[kMaxPanel];
+  double tt[kMaxPanel];
+};
+
+struct SbStep {
+  int q0, lq, p0, lp;
+};
+
+// Phases A-C of one step on (Db, Ob): fills sm.w, sm.y, sm.tt and this warp's
+// copy of vn; returns taun, betan and al = -taun (t^T vn) / 2.
+BSE_DEV void sbp_abc(SbpSmem& sm, const double* Db, const double* Ob, int lq, const double* v,
+                     double tau, double& taun, double& betan, double& al) {
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int mi = warp * 8 + (lane >> 2), q = lane & 3;
+  {
+    double a = 0.0;
+    if (tau != 0.0) {
+#pragma unroll
+      for (int i = 0; i < 16; ++i) {
+        const int c = colA(q, i);
+        a += Ob[c * kLd2 + mi] * v[c];
+      }
+      a += __shfl_xor_sync(0xffffffffu, a, 1);
+      a += __shfl_xor_sync(0xffffffffu, a, 2);
+    }
+    if (q == 0) sm.w[mi] = tau * a;
+  }
+  __syncthreads();
+  double* vn = sm.vnw[warp];
+  double swv;
+  taun = 0.0;
+  {
+    const double x0 = lane < lq ? Ob[lane] - sm.w[lane] : 0.0;
+    const double x1 = lane + 32 < lq ? Ob[lane + 32] - sm.w[lane + 32] : 0.0;
+    const double ss = warp_sum((lane >= 1 ? x0 * x0 : 0.0) + x1 * x1);
+    const double alpha = __shfl_sync(0xffffffffu, x0, 0);
+    betan = alpha;
+    double scale = 0.0;
+    if (ss > 0.0) {
+      betan = -copysign(sqrt(alpha * alpha + ss), alpha);
+      taun = (betan - alpha) / betan;
+      scale = 1.0 / (alpha - betan);
+    }
+    const double vn0 = lane == 0 ? 1.0 : x0 * scale;
+    const double vn1 = x1 * scale;
+    vn[lane] = vn0;
+    vn[lane + 32] = vn1;
+    swv = warp_sum(sm.w[lane] * vn0 + sm.w[lane + 32] * vn1);
+    __syncwarp();
+  }
+  {
+    double tc = 0.0, gc = 0.0;
+#pragma unroll
+    for (int i = 0; i < 16; ++i) {
+      const int r = rowC(q, i);
+      const double vr = vn[r];
+      tc += Db[mi * kLd2 + r] * vr;
+      gc += Ob[mi * kLd2 + r] * vr;
+    }
+    tc += __shfl_xor_sync(0xffffffffu, tc, 1);
+    tc += __shfl_xor_sync(0xffffffffu, tc, 2);
+    gc += __shfl_xor_sync(0xffffffffu, gc, 1);
+    gc += __shfl_xor_sync(0xffffffffu, gc, 2);
+    if (q == 0) {
+      sm.tt[mi] = taun * tc;
+      sm.y[mi] = taun * (gc - v[mi] * swv);
+    }
+  }
+  __syncthreads();
+  al = -0.5 * taun * warp_sum(sm.tt[lane] * vn[lane] + sm.tt[lane + 32] * vn[lane + 32]);
+}
+
+// Phase D: O'' = O - w v^T - vn y^T, D'' = D - vn w2^T - w2 vn^T to the band;
+// WB also writes them back into (Db, Ob) (the leader's blocks feed the
+// follower).  Row 0 is done by warp 0 (and published on `late` when PUB).
+template <bool WB, bool PUB>
+BSE_DEV void sbp_store(SbpSmem& sm, double* AB, int ldab, const SbStep& g, double* Db, double* Ob,
+                       const double* v, double betan, double al, int* late_s, int late_val) {
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const double* vn = sm.vnw[warp];
+  const int sh = g.q0 & 1;
+  const int q0 = g.q0, lq = g.lq, p0 = g.p0, lp = g.lp;
+  if (warp == 0) {
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int c = lane + 32 * h;
+      if (c < lp) {
+        const double val = c == 0 ? betan : Ob[c * kLd2] - sm.w[0] * v[c] - sm.y[c];
+        AB[(long long)(p0 + c) * ldab + (q0 - p0 - c)] = val;
+        if (WB) Ob[c * kLd2] = val;
+      }
+    }
+    if (lane == 0) {
+      const double d00 = Db[0] - 2.0 * (sm.tt[0] + al);
+      AB[(long long)q0 * ldab] = d00;
+      if (WB) Db[0] = d00;
+    }
+    if (PUB) {
+      __syncwarp();
+      if (lane == 0) {
+        __threadfence();
+        st_release(late_s, late_val);
+      }
+    }
+  }
+  auto put = [&](double* gp, double* sp, double* spm, bool ok0, bool ok1, double e0, double e1) {
+    if (ok0 && ok1) st_global_v2(gp, e0, e1);
+    else if (ok0) gp[0] = e0;
+    else if (ok1) gp[1] = e1;
+    if (WB) {
+      if (ok0) { sp[0] = e0; if (spm) spm[0] = e0; }
+      if (ok1) { sp[1] = e1; if (spm) spm[kLd2] = e1; }
+    }
+  };
+  if (lq == kMaxPanel && lp == kMaxPanel) {
+    const int c = kMaxPanel - 1 - (tid >> 2), kq = tid & 3;
+    double* od = AB + (long long)(p0 + c) * ldab + (q0 - p0 - c);
+    double* dd = AB + (long long)(q0 + c) * ldab - c;
+    const double vc = v[c], yc = sm.y[c];
+    const double vnc = vn[c], w2c = sm.tt[c] + al * vnc;
+    const int dlo = c > 1 ? c : 1;
+#pragma unroll
+    for (int i = 0; i < 9; ++i) {
+      const int k = kq + 4 * i;
+      if (k <= 32) {
+        const int r0 = 2 * k - sh, r1 = r0 + 1;
+        const bool in0 = r0 >= 1 && r0 < kMaxPanel, in1 = r1 >= 1 && r1 < kMaxPanel;
+        double o0 = 0.0, o1 = 0.0;
+        if (c > 0) {
+          if (in0) o0 = Ob[c * kLd2 + r0] - sm.w[r0] * vc - vn[r0] * yc;
+          if (in1) o1 = Ob[c * kLd2 + r1] - sm.w[r1] * vc - vn[r1] * yc;
+        }
+        put(od + r0, Ob + c * kLd2 + r0, nullptr, in0, in1, o0, o1);
+        const bool d0 = in0 && r0 >= dlo, d1 = in1 && r1 >= dlo;
+        double e0 = 0.0, e1 = 0.0;
+        if (d0) e0 = Db[c * kLd2 + r0] - (vn[r0] * w2c + (sm.tt[r0] + al * vn[r0]) * vnc);
+        if (d1) e1 = Db[c * kLd2 + r1] - (vn[r1] * w2c + (sm.tt[r1] + al * vn[r1]) * vnc);
+        put(dd + r0, Db + c * kLd2 + r0, Db + r0 * kLd2 + c, d0, d1, e0, e1);
+      }
+    }
+  } else {
+    constexpr int kTotal = 2 * kMaxPanel * kPairSlots;
+    for (int t = tid; t < kTotal; t += kSbThreads) {
+      const bool isO = t >= kMaxPanel * kPairSlots;
+      const int u = isO ? t - kMaxPanel * kPairSlots : t;
+      const int c = u / kPairSlots, k = u - kPairSlots * c;
+      const int r0 = 2 * k - sh, r1 = r0 + 1;
+      if (r0 >= lq) continue;
+      double val0 = 0.0, val1 = 0.0;
+      bool ok0, ok1;
+      if (isO) {
+        if (c >= lp) continue;
+        ok0 = r0 >= 1;
+        ok1 = r1 >= 1 && r1 < lq;
+        if (c > 0) {
+          const double vc = v[c], yc = sm.y[c];
+          if (ok0) val0 = Ob[c * kLd2 + r0] - sm.w[r0] * vc - vn[r0] * yc;
+          if (ok1) val1 = Ob[c * kLd2 + r1] - sm.w[r1] * vc - vn[r1] * yc;
+        }
+        put(AB + (long long)(p0 + c) * ldab + (q0 + r0 - p0 - c), Ob + c * kLd2 + r0, nullptr, ok0,
+            ok1, val0, val1);
+      } else {
+        ok0 = r0 >= 1 && r0 >= c;
+        ok1 = r1 >= 1 && r1 >= c && r1 < lq;
+        if (!ok0 && !ok1) continue;
+        const double vc = vn[c], w2c = sm.tt[c] + al * vc;
+        if (ok0) val0 = Db[c * kLd2 + r0] - (vn[r0] * w2c + (sm.tt[r0] + al * vn[r0]) * vc);
+        if (ok1) val1 = Db[c * kLd2 + r1] - (vn[r1] * w2c + (sm.tt[r1] + al * vn[r1]) * vc);
+        put(AB + (long long)(q0 + c) * ldab + (r0 - c), Db + c * kLd2 + r0, Db + r0 * kLd2 + c, ok0,
+            ok1, val0, val1);
+      }
+    }
+  }
+}
+
+__global__ void __launch_bounds__(kSbThreads) sb2st_pair_kernel(double* AB, int ldab, int n, int b,
+                                                                double* V2, double* tau2,
+                                                                int maxsteps, int* progress,
+                                                                unsigned long long* trace) {
+  (void)trace;
+  extern __shared__ __align__(16) unsigned char raw[];
+  SbpSmem& sm = *reinterpret_cast<SbpSmem*>(raw);
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  int* full = progress;
+  int* late = progress + n;
+  const int nsweeps = n - 2;
+  auto geo = [&](int s, int j) -> SbStep {  // step j of sweep s (q0 > n-1: none)
+    SbStep g;
+    g.q0 = s + 1 + j * b;
+    g.lq = min(s + (j + 1) * b, n - 1) - g.q0 + 1;
+    g.p0 = j == 0 ? s : s + 1 + (j - 1) * b;
+    g.lp = j == 0 ? 1 : b;
+    if (j > 0 && g.p0 + g.lp - 1 > n - 1) g.lp = n - g.p0;
+    return g;
+  };
+  auto exists = [&](int s, int j) { return s < nsweeps && s + 1 + j * b <= n - 1; };
+
+  for (int s = 2 * blockIdx.x; s < nsweeps; s += 2 * gridDim.x) {
+    const int f = s + 1;
+    const bool has_pred = s > 0;
+    const bool has_f = f < nsweeps;
+    double tauL = 0.0, tauF = 0.0;
+    if (tid < kMaxPanel) {
+      sm.vbuf[0][0][tid] = sm.vbuf[0][1][tid] = 0.0;
+      sm.vbuf[1][0][tid] = sm.vbuf[1][1][tid] = 0.0;
+    }
+    // prologue: the leader's step-0 bulk into set 0
+    __syncthreads();
+    if (has_pred && tid == 0) poll_counter(full + s - 1, kBulkWarps);
+    __syncthreads();
+    {
+      const SbStep g = geo(s, 0);
+      stage_bulk(sm.D[0] + (g.q0 & 1), sm.O[0] + (g.q0 & 1), AB, ldab, g.q0, g.lq, g.p0, g.lp, tid,
+                 kSbThreads);
+      cp_async_commit();
+      cp_async_wait<0>();
+      __syncthreads();
+      mirror_d(sm.D[0] + (g.q0 & 1), g.lq);
+    }
+    // round J: leader step J (set J % 3), then follower step J - 1 (set (J-1) % 3)
+    for (int J = 0;; ++J) {
+      const bool lead = exists(s, J);
+      const bool foll = has_f && J >= 1 && exists(f, J - 1);
+      if (!lead && !foll) break;
+      if (lead) {
+        const SbStep g = geo(s, J);
+        const int set = J % 3;
+        double* Db = sm.D[set] + (g.q0 & 1);
+        double* Ob = sm.O[set] + (g.q0 & 1);
+        const double* v = sm.vbuf[0][J & 1];
+        if (has_pred && tid == 0) poll_counter(late + s - 1, J + 2);
+        __syncthreads();  // also publishes the mirror writes
+        late_load(Db, Ob, AB, ldab, g.q0, g.lq, g.p0, g.lp);
+        __syncthreads();
+        double taun, betan, al;
+        sbp_abc(sm, Db, Ob, g.lq, v, tauL, taun, betan, al);
+        if (warp == 1) {
+          V2[((long long)s * maxsteps + J) * b + lane] = sm.vnw[1][lane];
+          V2[((long long)s * maxsteps + J) * b + lane + 32] = sm.vnw[1][lane + 32];
+          sm.vbuf[0][(J + 1) & 1][lane] = sm.vnw[1][lane];
+          sm.vbuf[0][(J + 1) & 1][lane + 32] = sm.vnw[1][lane + 32];
+          if (lane == 0) tau2[(long long)s * maxsteps + J] = taun;
+        }
+        sbp_store<true, false>(sm, AB, ldab, g, Db, Ob, v, betan, al, nullptr, 0);
+        tauL = taun;
+        // stage the leader's step J+1 into set (J+1) % 3 (free: the follower
+        // finished with it last round), needs the predecessor's step J+1 stored
+        if (exists(s, J + 1)) {
+          const SbStep gn = geo(s, J + 1);
+          if (has_pred && tid == 0) poll_counter(full + s - 1, kBulkWarps * (J + 2));
+          __syncthreads();
+          const int ns = (J + 1) % 3;
+          stage_bulk(sm.D[ns] + (gn.q0 & 1), sm.O[ns] + (gn.q0 & 1), AB, ldab, gn.q0, gn.lq, gn.p0,
+                     gn.lp, tid, kSbThreads);
+          cp_async_commit();
+        }
+      }
+      if (foll) {
+        const int jf = J - 1;
+        const SbStep g = geo(f, jf);
+        const SbStep gl = geo(s, jf);  // the leader's step jf: its blocks, shifted, are ours
+        const int set = jf % 3;
+        double* Db = sm.D[set] + (gl.q0 & 1) + kLd2 + 1;
+        double* Ob = sm.O[set] + (gl.q0 & 1) + kLd2 + 1;
+        const double* DLb = sm.D[set] + (gl.q0 & 1);  // leader's step-jf block, unshifted
+        const bool late_in = lead;  // the leader's step J produced our last row
+        __syncthreads();            // the leader's write-back is complete
+        const int rl = g.lq - 1;
+        if (late_in) {
+          const SbStep gn = geo(s, J);
+          const double* DN = sm.D[J % 3] + (gn.q0 & 1);
+          const double* ON = sm.O[J % 3] + (gn.q0 & 1);
+          if (tid < kMaxPanel) {
+            const int c = tid;
+            double x;
+            if (c < rl) x = ON[(c + 1) * kLd2];  // leader's O''(0, c+1)
+            else if (c == rl) x = DN[0];           // leader's D''(0, 0)
+            else x = 0.0;
+            Db[c * kLd2 + rl] = x;
+            Db[rl * kLd2 + c] = x;
+          } else if (tid == kMaxPanel) {
+            Ob[(g.lp - 1) * kLd2 + rl] = ON[0];  // leader's beta: O'(rl, lp-1)
+          } else if (tid > kMaxPanel && tid - kMaxPanel - 1 < g.lp - 1) {
+            const int c = tid - kMaxPanel - 1;  // O'(rl, c), c < lp-1: final in the band
+            Ob[c * kLd2 + rl] = __ldcg(AB + (long long)(g.p0 + c) * ldab + (g.q0 + rl - g.p0 - c));
+          }
+        } else if (tid < kMaxPanel && g.lq < kMaxPanel) {
+          // truncated block: clear the stale extra row / column of the set
+          Db[tid * kLd2 + (kMaxPanel - 1)] = 0.0;
+          Db[(kMaxPanel - 1) * kLd2 + tid] = 0.0;
+          Ob[tid * kLd2 + (kMaxPanel - 1)] = 0.0;
+        }
+        // O'(r, lp-1) = leader's D''(r+1, 0) for r < lq (rl via beta when late_in)
+        if (tid < kMaxPanel) {
+          const int r = tid;
+          if (!(late_in && r == rl)) Ob[(g.lp - 1) * kLd2 + r] = r < g.lq ? DLb[r + 1] : 0.0;
+        }
+        __syncthreads();
+        const double* v = sm.vbuf[1][jf & 1];
+        double taun, betan, al;
+        sbp_abc(sm, Db, Ob, g.lq, v, tauF, taun, betan, al);
+        if (warp == 1) {
+          V2[((long long)f * maxsteps + jf) * b + lane] = sm.vnw[1][lane];
+          V2[((long long)f * maxsteps + jf) * b + lane + 32] = sm.vnw[1][lane + 32];
+          sm.vbuf[1][(jf + 1) & 1][lane] = sm.vnw[1][lane];
+          sm.vbuf[1][(jf + 1) & 1][lane + 32] = sm.vnw[1][lane + 32];
+          if (lane == 0) tau2[(long long)f * maxsteps + jf] = taun;
+        }
+        sbp_store<false, true>(sm, AB, ldab, g, Db, Ob, v, betan, al, late + f, jf + 1);
+        // each warp publishes its bulk (and, by program order, the leader's
+        // earlier stores) on `full`
+        __syncwarp();
+        if (lane == 0) {
+          __threadfence();
+          atomicAdd(full + f, 1);
+        }
+        tauF = taun;
+      }
+      // the leader's next set has landed: mirror its D
+      if (exists(s, J + 1)) {
+        const SbStep gn = geo(s, J + 1);
+        cp_async_wait<0>();
+        __syncthreads();
+        mirror_d(sm.D[(J + 1) % 3] + (gn.q0 & 1), gn.lq);
+      }
+    }
+    __syncthreads();
+    if (tid == 0) {
+      __threadfence();
+      if (has_f) {
+        st_release(late + f, kDone);
+        st_release(full + f, kDone);
+      }
       st_release(late + s, kDone);
       st_release(full + s, kDone);
     }
@@ -694,8 +1049,10 @@ cudaError_t sb2st(double* AB, int ldab, int n, int b, double* d, double* e, doub
     if (const char* v = std::getenv("BSE_SB2ST_VARIANT")) flags = std::atoi(v);
     cudaMemcpyToSymbolAsync(c_sb_flags, &flags, sizeof(int), 0, cudaMemcpyHostToDevice, s);
     const bool legacy = (flags & 16) != 0;  // previous multi-phase step
-    const void* kern = legacy ? (const void*)sb2st_kernel : (const void*)sb2st_fused_kernel;
-    const size_t smem = legacy ? sizeof(SbSmem) : sizeof(SbfSmem);
+    const bool single = (flags & 128) == 0;  // flag 128: sweep pairs per CTA (experimental)
+    const void* kern = legacy ? (const void*)sb2st_kernel
+                              : single ? (const void*)sb2st_fused_kernel : (const void*)sb2st_pair_kernel;
+    const size_t smem = legacy ? sizeof(SbSmem) : single ? sizeof(SbfSmem) : sizeof(SbpSmem);
     static bool attr = false;
     if (!attr) {
       err = cudaFuncSetAttribute(sb2st_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -703,13 +1060,17 @@ cudaError_t sb2st(double* AB, int ldab, int n, int b, double* d, double* e, doub
       if (err == cudaSuccess)
         err = cudaFuncSetAttribute(sb2st_fused_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                    (int)sizeof(SbfSmem));
+      if (err == cudaSuccess)
+        err = cudaFuncSetAttribute(sb2st_pair_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   (int)sizeof(SbpSmem));
       if (err != cudaSuccess) return err;
       attr = true;
     }
     int per_sm = 0;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kSbThreads, smem);
     if (!(flags & 8)) per_sm = 1;  // default 1 CTA/SM (flag 8 restores full occupancy)
-    int grid = std::max(1, std::min(n - 2, std::max(1, per_sm) * num_sms));
+    const int units = (legacy || single) ? n - 2 : (n - 1) / 2;  // sweeps or sweep pairs
+    int grid = std::max(1, std::min(units, std::max(1, per_sm) * num_sms));
     int maxsteps = sb2st_maxsteps(n, b);
     unsigned long long* trace = nullptr;
     const char* tenv = std::getenv("BSE_SB2ST_TRACE");
