@@ -1,9 +1,9 @@
 // Stage 2: band -> tridiagonal by bulge chasing (Schwarz/Lang element
 // annihilation, the task structure of LAPACK's SB2ST kernels), as one
 // persistent cooperative kernel.  Sweep s is owned by CTA s mod G; step j of
-// sweep s may start once sweep s-1 has finished step j+1 (a release/acquire
-// progress counter per sweep), so ~N/(2b) sweeps are in flight at once.  The
-// band (ldab = 2b doubles per column) stays L2-resident; every reflector is
+// sweep s may start once sweep s-1 has published step j+1 (release/acquire
+// counters per sweep), so ~N/(2b) sweeps are in flight at once.  The band
+// (ldab = 2b + 1 doubles per column) stays L2-resident; every reflector is
 // stored for the Q2 back-transform.
 #include <cstdio>
 #include <cstdlib>
@@ -15,252 +15,14 @@ namespace {
 
 constexpr int kSbThreads = 256;
 constexpr int kDone = 0x7fffffff;
-constexpr int kLd = kMaxPanel + 1;
 constexpr int kSlots = kMaxPanel * kMaxPanel / kSbThreads;  // 16 block slots per thread
 
-struct SbSmem {
-  double D[kMaxPanel * kLd];  // symmetric block, full, [c*kLd + r]
-  double O[kMaxPanel * kLd];  // off-diagonal block, [c*kLd + r]
-  double v[kMaxPanel];        // current reflector
-  double vn[kMaxPanel];       // new reflector
-  double w[kMaxPanel];
-  double part[4 * kMaxPanel];
-  double sc[4];
-};
+__constant__ int c_sb_trace_s0;  // first traced sweep (BSE_SB2ST_TRACE)
 
 BSE_DEV unsigned long long gtimer() {
   unsigned long long t;
   asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
   return t;
-}
-
-// Householder of x[0..len) (one warp, LAPACK dlarfg conventions): v (v[0]=1),
-// sc[0] = tau, sc[1] = beta.
-BSE_DEV void warp_house(const double* x, int len, double* v, double* sc) {
-  const int lane = threadIdx.x & 31;
-  double s = 0.0;
-  for (int i = 1 + lane; i < len; i += 32) s += x[i] * x[i];
-  s = warp_sum(s);
-  const double x0 = x[0];
-  double tau = 0.0, beta = x0, scale = 0.0;
-  if (s > 0.0) {
-    beta = -copysign(sqrt(x0 * x0 + s), x0);
-    tau = (beta - x0) / beta;
-    scale = 1.0 / (x0 - beta);
-  }
-  for (int i = lane; i < kMaxPanel; i += 32)
-    v[i] = (i == 0) ? 1.0 : ((i < len && tau != 0.0) ? x[i] * scale : 0.0);
-  if (lane == 0) { sc[0] = tau; sc[1] = beta; }
-}
-
-__constant__ int c_sb_flags;  // tuning variants (BSE_SB2ST_VARIANT), default 0
-__constant__ int c_sb_trace_s0;  // first traced sweep (BSE_SB2ST_TRACE)
-
-BSE_DEV void wait_progress(const int* progress, int s, int need) {
-  if (s > 0 && threadIdx.x == 0) {
-    // relaxed polling (no L1 invalidation per probe), one acquire fence after
-    if (ld_relaxed(progress + s - 1) < need) {
-      const int ns = (c_sb_flags & 1) ? 256 : 0;
-      while (ld_relaxed(progress + s - 1) < need) {
-        if (ns) __nanosleep(ns);
-      }
-    }
-    fence_acquire();
-  }
-  __syncthreads();
-}
-
-BSE_DEV void signal_progress(int* progress, int s, int val) {
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    if (c_sb_flags & 2) fence_acquire();  // acq_rel fence (cheaper than sc)
-    else __threadfence();
-    st_release(progress + s, val);
-  }
-}
-
-// Stage the len x len symmetric block at (q0, q0) (lower triangle in the band)
-// and, optionally, the lq x lp off-diagonal block at (q0, p0) into smem with
-// cp.async: every load of the step is in flight at once (one L2 round trip).
-BSE_DEV void stage_blocks(SbSmem& sm, const double* AB, int ldab, int q0, int len, bool with_o,
-                          int p0, int lp) {
-  const int tid = threadIdx.x;
-#pragma unroll 4
-  for (int k = 0; k < kSlots; ++k) {
-    const int idx = tid + k * kSbThreads;
-    const int r = idx & (kMaxPanel - 1), c = idx >> 6;
-    const bool dv = r < len && c <= r;
-    const double* ds = dv ? AB + (long long)(q0 + c) * ldab + (r - c) : AB;
-    cp_async8(&sm.D[c * kLd + r], ds, dv);
-    if (with_o) {
-      const bool ov = r < len && c < lp;
-      const double* os = ov ? AB + (long long)(p0 + c) * ldab + (q0 + r - p0 - c) : AB;
-      cp_async8(&sm.O[c * kLd + r], os, ov);
-    }
-  }
-  cp_async_commit();
-  cp_async_wait<0>();
-  __syncthreads();
-  // mirror the lower triangle of D into the upper one
-#pragma unroll 4
-  for (int k = 0; k < kSlots; ++k) {
-    const int idx = tid + k * kSbThreads;
-    const int r = idx & (kMaxPanel - 1), c = idx >> 6;
-    if (c > r) sm.D[c * kLd + r] = sm.D[r * kLd + c];
-  }
-  __syncthreads();
-}
-
-// Column-sum matvec out_c = scale * sum_r X[c][r] x[r] (X column-major in smem,
-// 8 columns per warp, lanes over rows: conflict-free, shuffle-reduced).
-BSE_DEV void colsum(const double* X, const double* x, int nrows, double scale, double* out) {
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-#pragma unroll
-  for (int u = 0; u < kMaxPanel / 8; ++u) {
-    const int c = warp + 8 * u;
-    double a = 0.0;
-    if (lane < nrows) a = X[c * kLd + lane] * x[lane];
-    if (lane + 32 < nrows) a += X[c * kLd + lane + 32] * x[lane + 32];
-    a = warp_sum(a);
-    if (lane == 0) out[c] = scale * a;
-  }
-}
-
-// Two-sided D <- H D H (H = I - tau v v^T) on the staged symmetric block; the
-// lower triangle of the result is stored straight to the band.
-BSE_DEV void two_sided_store(SbSmem& sm, int len, const double* v, double tau, double* AB,
-                             int ldab, int q0) {
-  const int tid = threadIdx.x;
-  const int lane = tid & 31;
-  colsum(sm.D, v, len, tau, sm.w);  // D symmetric: column sums == row sums
-  __syncthreads();
-  if (tid < 32) {
-    double a = 0.0;
-    for (int i = lane; i < len; i += 32) a += sm.w[i] * v[i];
-    a = warp_sum(a);
-    if (lane == 0) sm.sc[2] = -0.5 * tau * a;
-  }
-  __syncthreads();
-  const double alpha = sm.sc[2];
-#pragma unroll
-  for (int k = 0; k < kSlots; ++k) {
-    const int idx = tid + k * kSbThreads;
-    const int r = idx & (kMaxPanel - 1), c = idx >> 6;
-    if (r < len && c <= r) {
-      const double wr = sm.w[r] + alpha * v[r], wc = sm.w[c] + alpha * v[c];
-      const double val = sm.D[c * kLd + r] - (v[r] * wc + wr * v[c]);
-      AB[(long long)(q0 + c) * ldab + (r - c)] = val;
-    }
-  }
-}
-
-__global__ void __launch_bounds__(kSbThreads) sb2st_kernel(double* AB, int ldab, int n, int b,
-                                                           double* V2, double* tau2,
-                                                           int maxsteps, int* progress,
-                                                           unsigned long long* trace) {
-  extern __shared__ __align__(16) unsigned char raw[];
-  SbSmem& sm = *reinterpret_cast<SbSmem*>(raw);
-  const int tid = threadIdx.x;
-  const int lane = tid & 31, warp = tid >> 5;
-  const bool tr = trace != nullptr && blockIdx.x == 1 && threadIdx.x == 0;
-  int tcount = 0;
-  auto bidx = [&](int i, int j) -> long long { return (long long)j * ldab + (i - j); };
-
-  for (int s = blockIdx.x; s < n - 2; s += gridDim.x) {
-    const bool trs = tr && s < 1 + 2 * (int)gridDim.x;
-    // ---------------- step 0: annihilate column s ----------------
-    if (trs) trace[8 * tcount] = gtimer();
-    wait_progress(progress, s, 2);
-    if (trs) trace[8 * tcount + 1] = gtimer();
-    int p0 = s + 1, p1 = min(s + b, n - 1);
-    int lp = p1 - p0 + 1;
-    if (tid < kMaxPanel) sm.w[tid] = tid < lp ? __ldcg(AB + bidx(p0 + tid, s)) : 0.0;
-    stage_blocks(sm, AB, ldab, p0, lp, false, 0, 0);
-    if (tid < 32) warp_house(sm.w, lp, sm.v, sm.sc);
-    __syncthreads();
-    double tau = sm.sc[0];
-    if (tid < lp) AB[bidx(p0 + tid, s)] = (tid == 0) ? sm.sc[1] : 0.0;
-    if (tid < b) V2[((long long)s * maxsteps) * b + tid] = sm.v[tid];
-    if (tid == 0) tau2[(long long)s * maxsteps] = tau;
-    if (tau != 0.0) two_sided_store(sm, lp, sm.v, tau, AB, ldab, p0);
-    signal_progress(progress, s, 1);
-    if (trs) { for (int q = 2; q < 8; ++q) trace[8 * tcount + q] = gtimer(); ++tcount; }
-
-    // ---------------- steps j >= 1: chase the bulge ----------------
-    for (int j = 1;; ++j) {
-      const int q0 = p1 + 1;
-      if (q0 > n - 1) break;
-      const int q1 = min(p1 + b, n - 1);
-      const int lq = q1 - q0 + 1;
-      if (trs) trace[8 * tcount] = gtimer();
-      wait_progress(progress, s, j + 2);
-      if (trs) trace[8 * tcount + 1] = gtimer();
-      stage_blocks(sm, AB, ldab, q0, lq, true, p0, lp);
-      if (trs) trace[8 * tcount + 2] = gtimer();
-      if (tau != 0.0) {
-        // right-apply: w = tau O v (row sums: 4 partial sums per row, lanes
-        // over consecutive rows -> conflict-free), O -= w v^T
-        {
-          const int r = tid & (kMaxPanel - 1), q = tid >> 6;
-          double a = 0.0;
-          for (int c = q; c < lp; c += 4) a += sm.O[c * kLd + r] * sm.v[c];
-          sm.part[q * kMaxPanel + r] = a;
-        }
-        __syncthreads();
-        if (tid < kMaxPanel)
-          sm.w[tid] = tau * ((sm.part[tid] + sm.part[kMaxPanel + tid]) +
-                             (sm.part[2 * kMaxPanel + tid] + sm.part[3 * kMaxPanel + tid]));
-        __syncthreads();
-#pragma unroll
-        for (int k = 0; k < kSlots; ++k) {
-          const int idx = tid + k * kSbThreads;
-          const int rr = idx & (kMaxPanel - 1), c = idx >> 6;
-          sm.O[c * kLd + rr] -= sm.w[rr] * sm.v[c];
-        }
-        __syncthreads();
-      }
-      if (trs) trace[8 * tcount + 3] = gtimer();
-      if (tid < 32) warp_house(sm.O, lq, sm.vn, sm.sc);
-      __syncthreads();
-      if (trs) trace[8 * tcount + 4] = gtimer();
-      const double taun = sm.sc[0], betan = sm.sc[1];
-      // left-apply to columns >= 1: y_c = taun * vn^T O[:, c] (column sums)
-      if (taun != 0.0) {
-        colsum(sm.O, sm.vn, lq, taun, sm.w);
-        __syncthreads();
-      }
-      // store O (column 0 = (beta, 0, ...)), reflector, then the two-sided D update
-#pragma unroll
-      for (int k = 0; k < kSlots; ++k) {
-        const int idx = tid + k * kSbThreads;
-        const int r = idx & (kMaxPanel - 1), c = idx >> 6;
-        if (r < lq && c < lp) {
-          double val;
-          if (c == 0) val = (r == 0) ? betan : 0.0;
-          else val = taun != 0.0 ? sm.O[c * kLd + r] - sm.vn[r] * sm.w[c] : sm.O[c * kLd + r];
-          AB[bidx(q0 + r, p0 + c)] = val;
-        }
-      }
-      if (tid < b) V2[((long long)s * maxsteps + j) * b + tid] = sm.vn[tid];
-      if (tid == 0) tau2[(long long)s * maxsteps + j] = taun;
-      __syncthreads();
-      if (trs) trace[8 * tcount + 5] = gtimer();
-      if (taun != 0.0) two_sided_store(sm, lq, sm.vn, taun, AB, ldab, q0);
-      if (trs) trace[8 * tcount + 6] = gtimer();
-      __syncthreads();
-      if (tid < kMaxPanel) sm.v[tid] = sm.vn[tid];
-      tau = taun;
-      signal_progress(progress, s, j + 1);
-      if (trs) { trace[8 * tcount + 7] = gtimer(); ++tcount; }
-      p0 = q0;
-      p1 = q1;
-      lp = lq;
-    }
-    signal_progress(progress, s, kDone);
-    __syncthreads();
-  }
-  (void)lane;
-  (void)warp;
 }
 
 // ---------------------------------------------------------------------------
@@ -312,7 +74,7 @@ BSE_DEV void poll_counter(const int* ctr, int need) {
     while (ld_relaxed(ctr) < need) {
     }
   }
-  if (!(c_sb_flags & 32)) fence_acquire();
+  fence_acquire();
 }
 
 // 16-byte L2-only async copy of `bytes` (0, 8 or 16) with zero fill: band
@@ -666,367 +428,6 @@ __global__ void __launch_bounds__(kSbThreads) sb2st_fused_kernel(double* AB, int
   }
 }
 
-// ---------------------------------------------------------------------------
-// Pair kernel (default).  One CTA chases TWO consecutive sweeps, leader s
-// (even) and follower s+1, interleaved step by step: round j = leader step
-// j+1, then follower step j.  The follower's blocks are the leader's step-j
-// blocks shifted by one row and column -- still in shared memory, updated in
-// place by the leader -- plus one new row/column: the leader's step-(j+1)
-// row 0 (also in shared memory) and 63 band entries already final in global
-// memory.  So half of all cross-sweep hand-offs never leave the SM: no flag,
-// no fence, no L2 round trip.  Only the follower publishes (late/full
-// counters, as in the fused kernel) for the next pair's leader; the leader
-// waits on the previous pair's follower.  Three shared block sets rotate:
-// leader step J uses set J mod 3, the follower reuses it one round later,
-// and the leader's step J+1 stages into the third.
-constexpr int kLdc = kMaxPanel + 1;  // 65 columns: the follower's view reaches column 64
-constexpr int kSetD = kLdc * kLd2 + 2;
-
-struct SbpSmem {
-  double D[3][kSetD];
-  double O[3][kSetD];
-  double vbuf[2][2][kMaxPanel];  // [leader / follower][parity]
-  double vnw[kSbThreads / 32][kMaxPanel];
-  double w[kMaxPanel];
-  double y[kMaxPanel];
-  double tt[kMaxPanel];
-};
-
-struct SbStep {
-  int q0, lq, p0, lp;
-};
-
-// Phases A-C of one step on (Db, Ob): fills sm.w, sm.y, sm.tt and this warp's
-// copy of vn; returns taun, betan and al = -taun (t^T vn) / 2.
-BSE_DEV void sbp_abc(SbpSmem& sm, const double* Db, const double* Ob, int lq, const double* v,
-                     double tau, double& taun, double& betan, double& al) {
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int mi = warp * 8 + (lane >> 2), q = lane & 3;
-  {
-    double a = 0.0;
-    if (tau != 0.0) {
-#pragma unroll
-      for (int i = 0; i < 16; ++i) {
-        const int c = colA(q, i);
-        a += Ob[c * kLd2 + mi] * v[c];
-      }
-      a += __shfl_xor_sync(0xffffffffu, a, 1);
-      a += __shfl_xor_sync(0xffffffffu, a, 2);
-    }
-    if (q == 0) sm.w[mi] = tau * a;
-  }
-  __syncthreads();
-  double* vn = sm.vnw[warp];
-  double swv;
-  taun = 0.0;
-  {
-    const double x0 = lane < lq ? Ob[lane] - sm.w[lane] : 0.0;
-    const double x1 = lane + 32 < lq ? Ob[lane + 32] - sm.w[lane + 32] : 0.0;
-    const double ss = warp_sum((lane >= 1 ? x0 * x0 : 0.0) + x1 * x1);
-    const double alpha = __shfl_sync(0xffffffffu, x0, 0);
-    betan = alpha;
-    double scale = 0.0;
-    if (ss > 0.0) {
-      betan = -copysign(sqrt(alpha * alpha + ss), alpha);
-      taun = (betan - alpha) / betan;
-      scale = 1.0 / (alpha - betan);
-    }
-    const double vn0 = lane == 0 ? 1.0 : x0 * scale;
-    const double vn1 = x1 * scale;
-    vn[lane] = vn0;
-    vn[lane + 32] = vn1;
-    swv = warp_sum(sm.w[lane] * vn0 + sm.w[lane + 32] * vn1);
-    __syncwarp();
-  }
-  {
-    double tc = 0.0, gc = 0.0;
-#pragma unroll
-    for (int i = 0; i < 16; ++i) {
-      const int r = rowC(q, i);
-      const double vr = vn[r];
-      tc += Db[mi * kLd2 + r] * vr;
-      gc += Ob[mi * kLd2 + r] * vr;
-    }
-    tc += __shfl_xor_sync(0xffffffffu, tc, 1);
-    tc += __shfl_xor_sync(0xffffffffu, tc, 2);
-    gc += __shfl_xor_sync(0xffffffffu, gc, 1);
-    gc += __shfl_xor_sync(0xffffffffu, gc, 2);
-    if (q == 0) {
-      sm.tt[mi] = taun * tc;
-      sm.y[mi] = taun * (gc - v[mi] * swv);
-    }
-  }
-  __syncthreads();
-  al = -0.5 * taun * warp_sum(sm.tt[lane] * vn[lane] + sm.tt[lane + 32] * vn[lane + 32]);
-}
-
-// Phase D: O'' = O - w v^T - vn y^T, D'' = D - vn w2^T - w2 vn^T to the band;
-// WB also writes them back into (Db, Ob) (the leader's blocks feed the
-// follower).  Row 0 is done by warp 0 (and published on `late` when PUB).
-template <bool WB, bool PUB>
-BSE_DEV void sbp_store(SbpSmem& sm, double* AB, int ldab, const SbStep& g, double* Db, double* Ob,
-                       const double* v, double betan, double al, int* late_s, int late_val) {
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const double* vn = sm.vnw[warp];
-  const int sh = g.q0 & 1;
-  const int q0 = g.q0, lq = g.lq, p0 = g.p0, lp = g.lp;
-  if (warp == 0) {
-#pragma unroll
-    for (int h = 0; h < 2; ++h) {
-      const int c = lane + 32 * h;
-      if (c < lp) {
-        const double val = c == 0 ? betan : Ob[c * kLd2] - sm.w[0] * v[c] - sm.y[c];
-        AB[(long long)(p0 + c) * ldab + (q0 - p0 - c)] = val;
-        if (WB) Ob[c * kLd2] = val;
-      }
-    }
-    if (lane == 0) {
-      const double d00 = Db[0] - 2.0 * (sm.tt[0] + al);
-      AB[(long long)q0 * ldab] = d00;
-      if (WB) Db[0] = d00;
-    }
-    if (PUB) {
-      __syncwarp();
-      if (lane == 0) {
-        __threadfence();
-        st_release(late_s, late_val);
-      }
-    }
-  }
-  auto put = [&](double* gp, double* sp, double* spm, bool ok0, bool ok1, double e0, double e1) {
-    if (ok0 && ok1) st_global_v2(gp, e0, e1);
-    else if (ok0) gp[0] = e0;
-    else if (ok1) gp[1] = e1;
-    if (WB) {
-      if (ok0) { sp[0] = e0; if (spm) spm[0] = e0; }
-      if (ok1) { sp[1] = e1; if (spm) spm[kLd2] = e1; }
-    }
-  };
-  if (lq == kMaxPanel && lp == kMaxPanel) {
-    const int c = kMaxPanel - 1 - (tid >> 2), kq = tid & 3;
-    double* od = AB + (long long)(p0 + c) * ldab + (q0 - p0 - c);
-    double* dd = AB + (long long)(q0 + c) * ldab - c;
-    const double vc = v[c], yc = sm.y[c];
-    const double vnc = vn[c], w2c = sm.tt[c] + al * vnc;
-    const int dlo = c > 1 ? c : 1;
-#pragma unroll
-    for (int i = 0; i < 9; ++i) {
-      const int k = kq + 4 * i;
-      if (k <= 32) {
-        const int r0 = 2 * k - sh, r1 = r0 + 1;
-        const bool in0 = r0 >= 1 && r0 < kMaxPanel, in1 = r1 >= 1 && r1 < kMaxPanel;
-        double o0 = 0.0, o1 = 0.0;
-        if (c > 0) {
-          if (in0) o0 = Ob[c * kLd2 + r0] - sm.w[r0] * vc - vn[r0] * yc;
-          if (in1) o1 = Ob[c * kLd2 + r1] - sm.w[r1] * vc - vn[r1] * yc;
-        }
-        put(od + r0, Ob + c * kLd2 + r0, nullptr, in0, in1, o0, o1);
-        const bool d0 = in0 && r0 >= dlo, d1 = in1 && r1 >= dlo;
-        double e0 = 0.0, e1 = 0.0;
-        if (d0) e0 = Db[c * kLd2 + r0] - (vn[r0] * w2c + (sm.tt[r0] + al * vn[r0]) * vnc);
-        if (d1) e1 = Db[c * kLd2 + r1] - (vn[r1] * w2c + (sm.tt[r1] + al * vn[r1]) * vnc);
-        put(dd + r0, Db + c * kLd2 + r0, Db + r0 * kLd2 + c, d0, d1, e0, e1);
-      }
-    }
-  } else {
-    constexpr int kTotal = 2 * kMaxPanel * kPairSlots;
-    for (int t = tid; t < kTotal; t += kSbThreads) {
-      const bool isO = t >= kMaxPanel * kPairSlots;
-      const int u = isO ? t - kMaxPanel * kPairSlots : t;
-      const int c = u / kPairSlots, k = u - kPairSlots * c;
-      const int r0 = 2 * k - sh, r1 = r0 + 1;
-      if (r0 >= lq) continue;
-      double val0 = 0.0, val1 = 0.0;
-      bool ok0, ok1;
-      if (isO) {
-        if (c >= lp) continue;
-        ok0 = r0 >= 1;
-        ok1 = r1 >= 1 && r1 < lq;
-        if (c > 0) {
-          const double vc = v[c], yc = sm.y[c];
-          if (ok0) val0 = Ob[c * kLd2 + r0] - sm.w[r0] * vc - vn[r0] * yc;
-          if (ok1) val1 = Ob[c * kLd2 + r1] - sm.w[r1] * vc - vn[r1] * yc;
-        }
-        put(AB + (long long)(p0 + c) * ldab + (q0 + r0 - p0 - c), Ob + c * kLd2 + r0, nullptr, ok0,
-            ok1, val0, val1);
-      } else {
-        ok0 = r0 >= 1 && r0 >= c;
-        ok1 = r1 >= 1 && r1 >= c && r1 < lq;
-        if (!ok0 && !ok1) continue;
-        const double vc = vn[c], w2c = sm.tt[c] + al * vc;
-        if (ok0) val0 = Db[c * kLd2 + r0] - (vn[r0] * w2c + (sm.tt[r0] + al * vn[r0]) * vc);
-        if (ok1) val1 = Db[c * kLd2 + r1] - (vn[r1] * w2c + (sm.tt[r1] + al * vn[r1]) * vc);
-        put(AB + (long long)(q0 + c) * ldab + (r0 - c), Db + c * kLd2 + r0, Db + r0 * kLd2 + c, ok0,
-            ok1, val0, val1);
-      }
-    }
-  }
-}
-
-__global__ void __launch_bounds__(kSbThreads) sb2st_pair_kernel(double* AB, int ldab, int n, int b,
-                                                                double* V2, double* tau2,
-                                                                int maxsteps, int* progress,
-                                                                unsigned long long* trace) {
-  (void)trace;
-  extern __shared__ __align__(16) unsigned char raw[];
-  SbpSmem& sm = *reinterpret_cast<SbpSmem*>(raw);
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  int* full = progress;
-  int* late = progress + n;
-  const int nsweeps = n - 2;
-  auto geo = [&](int s, int j) -> SbStep {  // step j of sweep s (q0 > n-1: none)
-    SbStep g;
-    g.q0 = s + 1 + j * b;
-    g.lq = min(s + (j + 1) * b, n - 1) - g.q0 + 1;
-    g.p0 = j == 0 ? s : s + 1 + (j - 1) * b;
-    g.lp = j == 0 ? 1 : b;
-    if (j > 0 && g.p0 + g.lp - 1 > n - 1) g.lp = n - g.p0;
-    return g;
-  };
-  auto exists = [&](int s, int j) { return s < nsweeps && s + 1 + j * b <= n - 1; };
-
-  for (int s = 2 * blockIdx.x; s < nsweeps; s += 2 * gridDim.x) {
-    const int f = s + 1;
-    const bool has_pred = s > 0;
-    const bool has_f = f < nsweeps;
-    double tauL = 0.0, tauF = 0.0;
-    if (tid < kMaxPanel) {
-      sm.vbuf[0][0][tid] = sm.vbuf[0][1][tid] = 0.0;
-      sm.vbuf[1][0][tid] = sm.vbuf[1][1][tid] = 0.0;
-    }
-    // prologue: the leader's step-0 bulk into set 0
-    __syncthreads();
-    if (has_pred && tid == 0) poll_counter(full + s - 1, kBulkWarps);
-    __syncthreads();
-    {
-      const SbStep g = geo(s, 0);
-      stage_bulk(sm.D[0] + (g.q0 & 1), sm.O[0] + (g.q0 & 1), AB, ldab, g.q0, g.lq, g.p0, g.lp, tid,
-                 kSbThreads);
-      cp_async_commit();
-      cp_async_wait<0>();
-      __syncthreads();
-      mirror_d(sm.D[0] + (g.q0 & 1), g.lq);
-    }
-    // round J: leader step J (set J % 3), then follower step J - 1 (set (J-1) % 3)
-    for (int J = 0;; ++J) {
-      const bool lead = exists(s, J);
-      const bool foll = has_f && J >= 1 && exists(f, J - 1);
-      if (!lead && !foll) break;
-      if (lead) {
-        const SbStep g = geo(s, J);
-        const int set = J % 3;
-        double* Db = sm.D[set] + (g.q0 & 1);
-        double* Ob = sm.O[set] + (g.q0 & 1);
-        const double* v = sm.vbuf[0][J & 1];
-        if (has_pred && tid == 0) poll_counter(late + s - 1, J + 2);
-        __syncthreads();  // also publishes the mirror writes
-        late_load(Db, Ob, AB, ldab, g.q0, g.lq, g.p0, g.lp);
-        __syncthreads();
-        double taun, betan, al;
-        sbp_abc(sm, Db, Ob, g.lq, v, tauL, taun, betan, al);
-        if (warp == 1) {
-          V2[((long long)s * maxsteps + J) * b + lane] = sm.vnw[1][lane];
-          V2[((long long)s * maxsteps + J) * b + lane + 32] = sm.vnw[1][lane + 32];
-          sm.vbuf[0][(J + 1) & 1][lane] = sm.vnw[1][lane];
-          sm.vbuf[0][(J + 1) & 1][lane + 32] = sm.vnw[1][lane + 32];
-          if (lane == 0) tau2[(long long)s * maxsteps + J] = taun;
-        }
-        sbp_store<true, false>(sm, AB, ldab, g, Db, Ob, v, betan, al, nullptr, 0);
-        tauL = taun;
-        // stage the leader's step J+1 into set (J+1) % 3 (free: the follower
-        // finished with it last round), needs the predecessor's step J+1 stored
-        if (exists(s, J + 1)) {
-          const SbStep gn = geo(s, J + 1);
-          if (has_pred && tid == 0) poll_counter(full + s - 1, kBulkWarps * (J + 2));
-          __syncthreads();
-          const int ns = (J + 1) % 3;
-          stage_bulk(sm.D[ns] + (gn.q0 & 1), sm.O[ns] + (gn.q0 & 1), AB, ldab, gn.q0, gn.lq, gn.p0,
-                     gn.lp, tid, kSbThreads);
-          cp_async_commit();
-        }
-      }
-      if (foll) {
-        const int jf = J - 1;
-        const SbStep g = geo(f, jf);
-        const SbStep gl = geo(s, jf);  // the leader's step jf: its blocks, shifted, are ours
-        const int set = jf % 3;
-        double* Db = sm.D[set] + (gl.q0 & 1) + kLd2 + 1;
-        double* Ob = sm.O[set] + (gl.q0 & 1) + kLd2 + 1;
-        const double* DLb = sm.D[set] + (gl.q0 & 1);  // leader's step-jf block, unshifted
-        const bool late_in = lead;  // the leader's step J produced our last row
-        __syncthreads();            // the leader's write-back is complete
-        const int rl = g.lq - 1;
-        if (late_in) {
-          const SbStep gn = geo(s, J);
-          const double* DN = sm.D[J % 3] + (gn.q0 & 1);
-          const double* ON = sm.O[J % 3] + (gn.q0 & 1);
-          if (tid < kMaxPanel) {
-            const int c = tid;
-            double x;
-            if (c < rl) x = ON[(c + 1) * kLd2];  // leader's O''(0, c+1)
-            else if (c == rl) x = DN[0];           // leader's D''(0, 0)
-            else x = 0.0;
-            Db[c * kLd2 + rl] = x;
-            Db[rl * kLd2 + c] = x;
-          } else if (tid == kMaxPanel) {
-            Ob[(g.lp - 1) * kLd2 + rl] = ON[0];  // leader's beta: O'(rl, lp-1)
-          } else if (tid > kMaxPanel && tid - kMaxPanel - 1 < g.lp - 1) {
-            const int c = tid - kMaxPanel - 1;  // O'(rl, c), c < lp-1: final in the band
-            Ob[c * kLd2 + rl] = __ldcg(AB + (long long)(g.p0 + c) * ldab + (g.q0 + rl - g.p0 - c));
-          }
-        } else if (tid < kMaxPanel && g.lq < kMaxPanel) {
-          // truncated block: clear the stale extra row / column of the set
-          Db[tid * kLd2 + (kMaxPanel - 1)] = 0.0;
-          Db[(kMaxPanel - 1) * kLd2 + tid] = 0.0;
-          Ob[tid * kLd2 + (kMaxPanel - 1)] = 0.0;
-        }
-        // O'(r, lp-1) = leader's D''(r+1, 0) for r < lq (rl via beta when late_in)
-        if (tid < kMaxPanel) {
-          const int r = tid;
-          if (!(late_in && r == rl)) Ob[(g.lp - 1) * kLd2 + r] = r < g.lq ? DLb[r + 1] : 0.0;
-        }
-        __syncthreads();
-        const double* v = sm.vbuf[1][jf & 1];
-        double taun, betan, al;
-        sbp_abc(sm, Db, Ob, g.lq, v, tauF, taun, betan, al);
-        if (warp == 1) {
-          V2[((long long)f * maxsteps + jf) * b + lane] = sm.vnw[1][lane];
-          V2[((long long)f * maxsteps + jf) * b + lane + 32] = sm.vnw[1][lane + 32];
-          sm.vbuf[1][(jf + 1) & 1][lane] = sm.vnw[1][lane];
-          sm.vbuf[1][(jf + 1) & 1][lane + 32] = sm.vnw[1][lane + 32];
-          if (lane == 0) tau2[(long long)f * maxsteps + jf] = taun;
-        }
-        sbp_store<false, true>(sm, AB, ldab, g, Db, Ob, v, betan, al, late + f, jf + 1);
-        // each warp publishes its bulk (and, by program order, the leader's
-        // earlier stores) on `full`
-        __syncwarp();
-        if (lane == 0) {
-          __threadfence();
-          atomicAdd(full + f, 1);
-        }
-        tauF = taun;
-      }
-      // the leader's next set has landed: mirror its D
-      if (exists(s, J + 1)) {
-        const SbStep gn = geo(s, J + 1);
-        cp_async_wait<0>();
-        __syncthreads();
-        mirror_d(sm.D[(J + 1) % 3] + (gn.q0 & 1), gn.lq);
-      }
-    }
-    __syncthreads();
-    if (tid == 0) {
-      __threadfence();
-      if (has_f) {
-        st_release(late + f, kDone);
-        st_release(full + f, kDone);
-      }
-      st_release(late + s, kDone);
-      st_release(full + s, kDone);
-    }
-  }
-}
-
 __global__ void band_to_tridiag_kernel(const double* AB, int ldab, int n, double* d, double* e) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i < n) {
@@ -1045,32 +446,17 @@ cudaError_t sb2st(double* AB, int ldab, int n, int b, double* d, double* e, doub
   cudaError_t err;
   if (n > 2) {
     if ((err = cudaMemsetAsync(progress, 0, sizeof(int) * 2 * (size_t)n, s)) != cudaSuccess) return err;
-    int flags = 0;
-    if (const char* v = std::getenv("BSE_SB2ST_VARIANT")) flags = std::atoi(v);
-    cudaMemcpyToSymbolAsync(c_sb_flags, &flags, sizeof(int), 0, cudaMemcpyHostToDevice, s);
-    const bool legacy = (flags & 16) != 0;  // previous multi-phase step
-    const bool single = (flags & 128) == 0;  // flag 128: sweep pairs per CTA (experimental)
-    const void* kern = legacy ? (const void*)sb2st_kernel
-                              : single ? (const void*)sb2st_fused_kernel : (const void*)sb2st_pair_kernel;
-    const size_t smem = legacy ? sizeof(SbSmem) : single ? sizeof(SbfSmem) : sizeof(SbpSmem);
+    const size_t smem = sizeof(SbfSmem);
     static bool attr = false;
     if (!attr) {
-      err = cudaFuncSetAttribute(sb2st_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 (int)sizeof(SbSmem));
-      if (err == cudaSuccess)
-        err = cudaFuncSetAttribute(sb2st_fused_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                   (int)sizeof(SbfSmem));
-      if (err == cudaSuccess)
-        err = cudaFuncSetAttribute(sb2st_pair_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                   (int)sizeof(SbpSmem));
+      err = cudaFuncSetAttribute(sb2st_fused_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)smem);
       if (err != cudaSuccess) return err;
       attr = true;
     }
-    int per_sm = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kSbThreads, smem);
-    if (!(flags & 8)) per_sm = 1;  // default 1 CTA/SM (flag 8 restores full occupancy)
-    const int units = (legacy || single) ? n - 2 : (n - 1) / 2;  // sweeps or sweep pairs
-    int grid = std::max(1, std::min(units, std::max(1, per_sm) * num_sms));
+    // one CTA per SM: the kernel is latency-bound and one resident step per
+    // SM keeps every hand-off on an otherwise idle SM
+    const int grid = std::max(1, std::min(n - 2, num_sms));
     int maxsteps = sb2st_maxsteps(n, b);
     unsigned long long* trace = nullptr;
     const char* tenv = std::getenv("BSE_SB2ST_TRACE");
@@ -1085,9 +471,10 @@ cudaError_t sb2st(double* AB, int ldab, int n, int b, double* d, double* e, doub
     }
     void* args[] = {&AB, &ldab, &n, &b, &V2, &tau2, &maxsteps, &progress, &trace};
     count_launch();
-    err = cudaLaunchCooperativeKernel(kern, dim3(grid), dim3(kSbThreads), args, smem, s);
+    err = cudaLaunchCooperativeKernel((const void*)sb2st_fused_kernel, dim3(grid), dim3(kSbThreads),
+                                      args, smem, s);
     if (err != cudaSuccess) return err;
-    if (want_trace && !legacy) {
+    if (want_trace) {
       std::vector<unsigned long long> h(tsz);
       cudaMemcpyAsync(h.data(), trace, h.size() * 8, cudaMemcpyDeviceToHost, s);
       cudaStreamSynchronize(s);
