@@ -9,9 +9,11 @@ metric's n = 16k-64k range.  One step = one complete solve through the C ABI
 (SY2SB, SB2ST, D&C, Q2/Q1), recovery of X1/X2 (all eigenpairs).  Inputs are
 2 GB each (> 126 MB L2) and resident in HBM when the timed region starts.
 
-Multi-GPU (torchrun, N > 1): round 1 runs independent replicas (one full
-solve per GPU, "scaling": "weak"); the 2-D block-cyclic sharded solve is not
-built yet.  Times are device (CUDA event) times, max over ranks.
+Multi-GPU (torchrun, N > 1): ONE solve spans the N GPUs ("scaling":
+"strong"): the column-sharded path of bse_solve_spd_pair_dist_dev over an
+NCCL communicator (congruence and eigenvector-side stages split by columns,
+reduction and D&C replicated, column blocks broadcast from their owners;
+DESIGN.md section 7).  Times are device (CUDA event) times, max over ranks.
 
 --impl reference times the reference algorithm on the host cores: the numpy
 restatement of the reference's solve_complex (oracle/bse_oracle.py; the
@@ -237,9 +239,13 @@ def run_ours(args):
     n = args.n
     stream = torch.cuda.current_stream(dev)
     sp = stream.cuda_stream
+    comm = None
+    if world > 1:
+        from paper_1501_03830_b200.distributed import Communicator
+        comm = Communicator.nccl()
 
     # inputs: M = A + B = S, K = A - B = D (symmetric: row-major == column-major)
-    S, D, dip = configs.torch_real_operator(n, seed=SEED + rank, spectrum="loguniform", lo=0.1,
+    S, D, dip = configs.torch_real_operator(n, seed=SEED, spectrum="loguniform", lo=0.1,
                                             hi=100.0, device=dev)
     ld = n + (n & 1)
     Mt = torch.zeros((n, ld), dtype=torch.float64, device=dev)
@@ -253,10 +259,20 @@ def run_ours(args):
     wb = lib.bse_solve_workspace_bytes(n, 0)
     work = torch.empty(wb, dtype=torch.uint8, device=dev)
     info = _lib.BseInfo()
+    if world > 1:
+        # one solve over all ranks: every rank must hold rank 0's (M, K)
+        dist.broadcast(Mt, src=0)
+        dist.broadcast(Kt, src=0)
+        torch.cuda.synchronize(dev)
 
     def step():
-        st = lib.bse_solve_spd_pair_dev(n, ptr(Mt), ld, ptr(Kt), ld, ptr(lam), ptr(X1), ld,
-                                        ptr(X2), ld, ptr(work), wb, 0, sp, C.byref(info))
+        if comm is None:
+            st = lib.bse_solve_spd_pair_dev(n, ptr(Mt), ld, ptr(Kt), ld, ptr(lam), ptr(X1), ld,
+                                            ptr(X2), ld, ptr(work), wb, 0, sp, C.byref(info))
+        else:
+            st = lib.bse_solve_spd_pair_dist_dev(comm.handle, n, ptr(Mt), ld, ptr(Kt), ld,
+                                                 ptr(lam), ptr(X1), ld, ptr(X2), ld, ptr(work),
+                                                 wb, 0, sp, C.byref(info))
         if st != 0:
             raise RuntimeError(f"solve failed ({st}): {_lib.last_error()}")
 
@@ -308,7 +324,7 @@ def run_ours(args):
     # size-independent verification of the last timed solve (outside the timed
     # region): per-pair residual / (lam_max ||x||) and ||X1^T X1 - X2^T X2 - I||_F
     verification = None
-    if not args.no_verify:
+    if not args.no_verify and rank == 0:
         from paper_1501_03830_b200.verify import pair_residuals_device
         res, xn, bio = pair_residuals_device(n, Mt, ld, Kt, ld, lam, X1, ld, X2, ld)
         verification = {"max_pair_residual": (res / (lam[0] * xn)).max().item(),
@@ -326,16 +342,29 @@ def run_ours(args):
         Kh = torch.empty((n, n), dtype=torch.float64, pin_memory=True)
         Mh.copy_(Mt[:, :n])
         Kh.copy_(Kt[:, :n])
-        lamh = torch.empty(n, dtype=torch.float64, pin_memory=True)
-        X1h = torch.empty((n, n), dtype=torch.float64, pin_memory=True)
-        X2h = torch.empty((n, n), dtype=torch.float64, pin_memory=True)
+        out_n = n if rank == 0 else 1  # only rank 0 reads the solution back
+        lamh = torch.empty(out_n, dtype=torch.float64, pin_memory=True)
+        X1h = torch.empty((out_n, out_n), dtype=torch.float64, pin_memory=True)
+        X2h = torch.empty((out_n, out_n), dtype=torch.float64, pin_memory=True)
         torch.cuda.synchronize(dev)
 
         def e2e_step():
-            st = lib.bse_solve_spd_pair_host(n, ptr(Mh), n, ptr(Kh), n, ptr(lamh), ptr(X1h), n,
-                                             ptr(X2h), n, 0, C.byref(info))
-            if st != 0:
-                raise RuntimeError(f"host solve failed: {_lib.last_error()}")
+            if comm is None:
+                st = lib.bse_solve_spd_pair_host(n, ptr(Mh), n, ptr(Kh), n, ptr(lamh), ptr(X1h),
+                                                 n, ptr(X2h), n, 0, C.byref(info))
+                if st != 0:
+                    raise RuntimeError(f"host solve failed: {_lib.last_error()}")
+                return
+            # sharded: every rank uploads its host copy of (M, K), the solve
+            # runs across the ranks, rank 0 reads the assembled solution back
+            Mt[:, :n].copy_(Mh, non_blocking=True)
+            Kt[:, :n].copy_(Kh, non_blocking=True)
+            step()
+            if rank == 0:
+                lamh.copy_(lam, non_blocking=True)
+                X1h.copy_(X1[:, :n], non_blocking=True)
+                X2h.copy_(X2[:, :n], non_blocking=True)
+            torch.cuda.synchronize(dev)
         e2e_step()  # warm the allocator pool
         if world > 1:
             dist.barrier()
@@ -344,15 +373,19 @@ def run_ours(args):
             e2e_step()
         e2e_s = max_over_ranks((time.perf_counter() - t0) / args.e2e_steps,
                                dist if world > 1 else None, dev)
-        e2e = {"value": e2e_s, "unit": "s", "h2d_bytes_per_step": 2 * n * n * 8,
+        e2e = {"value": e2e_s, "unit": "s", "h2d_bytes_per_step": world * 2 * n * n * 8,
                "d2h_bytes_per_step": (2 * n * n + n) * 8,
-               "path": "bse_solve_spd_pair_host (pinned host M, K -> lam, X1, X2)"}
+               "path": ("bse_solve_spd_pair_host (pinned host M, K -> lam, X1, X2)" if comm is None
+                        else "pinned host M, K -> every rank; bse_solve_spd_pair_dist_dev; "
+                             "rank 0 lam, X1, X2 -> pinned host")}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         v, cores, sample, _ = cpu_reference_sample(n)
         cpu = {"value": v, "unit": "s", "cores": cores, "kind": "port", "sample": sample}
 
+    if comm is not None:
+        comm.close()
     if rank != 0:
         if world > 1:
             dist.destroy_process_group()
@@ -373,11 +406,14 @@ def run_ours(args):
     line = {
         "metric": "full BSE eigenpair time-to-solution (s)", "value": solve_s, "unit": "s",
         "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step,
-        "higher_is_better": False, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "higher_is_better": False, "scaling": "strong" if world > 1 else "weak",
+        "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (BASELINE cfg2 recipe, torch Philox on GPU)",
         "config": {"workload": f"cfg2 real BSE n={n} (H {2 * n}x{2 * n}), log-uniform [0.1,100] "
                                f"spectra, all eigenpairs + X1/X2",
-                   "n": n, "parallelism": "replicas" if world > 1 else "single GPU",
+                   "n": n,
+                   "parallelism": (f"column-sharded x{world} (NCCL; reduction + D&C replicated)"
+                                   if world > 1 else "single GPU"),
                    "l2": "inputs 2 GB each > 126 MB L2 (no flush needed)"},
         "tflops": alg_flops(n) / solve_s / 1e12,
         "fp64_peak_tflops": fp64_peak,

@@ -23,6 +23,12 @@ NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
          "-Xcompiler", "-fPIC", "-Xcompiler", "-O2", "--expt-relaxed-constexpr",
          "-I", str(ROOT / "include")]
+# CuTe/CUTLASS headers (vendored in the image under flashinfer) for the
+# tcgen05 int8 GEMM behind the emulated-FP64 engine (csrc/ozgemm.cu)
+_CUTLASS = Path(sys.prefix) / "lib" / f"python{sys.version_info.major}.{sys.version_info.minor}" / \
+    "site-packages" / "flashinfer" / "data" / "cutlass"
+CUTLASS_FLAGS = ["-I", str(_CUTLASS / "include"), "-I", str(_CUTLASS / "tools" / "util" / "include"),
+                 "-diag-suppress", "20012"]
 
 
 def _compile(cu: Path) -> Path:
@@ -31,7 +37,8 @@ def _compile(cu: Path) -> Path:
     newest = max([cu.stat().st_mtime] + [h.stat().st_mtime for h in headers])
     if obj.exists() and obj.stat().st_mtime >= newest:
         return obj
-    cmd = [NVCC, *FLAGS, "-c", str(cu), "-o", str(obj)]
+    extra = CUTLASS_FLAGS if cu.stem == "ozgemm" else []
+    cmd = [NVCC, *FLAGS, *extra, "-c", str(cu), "-o", str(obj)]
     res = subprocess.run(cmd, capture_output=True, text=True)
     if res.returncode != 0:
         sys.stderr.write(res.stdout + res.stderr)

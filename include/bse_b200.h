@@ -47,6 +47,7 @@ typedef enum {
 /* Flags for bse_solve_spd_pair_* / bse_syevd_dev. */
 #define BSE_FLAG_VALUES_ONLY 0x1 /* eigenvalues only (TDA / validation) */
 #define BSE_FLAG_ZPOLISH 0x2     /* Z <- Z (1.5 I - 0.5 Z^T Z) orthogonality polish */
+#define BSE_FLAG_NATIVE_FP64 0x4 /* all products on FP64 DMMA (no INT8-emulated GEMMs) */
 
 typedef struct bse_info {
   int64_t pivot_index;  /* first non-positive Cholesky pivot (status 1) */
@@ -127,6 +128,12 @@ int bse_gemm_dev(int transA, int transB, int64_t M, int64_t N, int64_t K, double
                  const double* dA, int64_t lda, const double* dB, int64_t ldb, double beta,
                  double* dC, int64_t ldc, const int32_t* masks /* 9 ints or NULL */,
                  void* stream);
+/* Same contract on the emulated-FP64 engine: Ozaki scheme II, 16 int8
+ * residue products on the tcgen05 tensor cores + CRT reconstruction
+ * (csrc/ozgemm.cu).  chunk: output columns per pass (<= 0: all N). */
+int bse_ozgemm_dev(int transA, int transB, int64_t M, int64_t N, int64_t K, double alpha,
+                   const double* dA, int64_t lda, const double* dB, int64_t ldb, double beta,
+                   double* dC, int64_t ldc, const int32_t* masks, int64_t chunk, void* stream);
 /* kind: 0 = A L^{-T} (right), 1 = L^{-T} B (left, trans), 2 = L^{-1} B (left) */
 int bse_trsm_dev(int kind, int64_t n, const double* dL, int64_t ldl, double* dB, int64_t ldb,
                  int64_t m, void* stream);
@@ -141,6 +148,43 @@ long long bse_launch_count(void);
 /* FP64 peak probe: which 0 = DMMA, 1 = DFMA.  Returns flops of one launch in
  * *flops and the mean device time over `reps` launches in *ms. */
 int bse_peak_fp64(int which, int blocks, int iters, int reps, double* flops, double* ms);
+
+/*
+ * Column-sharded multi-GPU solve (one process per GPU).
+ * Same contract as bse_solve_spd_pair_dev -- the sharded form of
+ * solvers.solve_real / solve_complex (pkg/src/bse/solvers.py:80-109,
+ * :29-77) -- called collectively by every rank with identical M, K.  Rank r
+ * forms the column block [c0_r, c1_r) (bse_shard_range) of the congruence
+ * W = L^T M L and of the back-transformed eigenvectors and X1/X2; the blocks
+ * are broadcast from their owners (one NCCL group of per-root broadcasts),
+ * so on return every rank holds lam, X1 and X2 in full.  The Cholesky, the
+ * band reduction, bulge chasing and D&C are replicated (bitwise identical on
+ * every rank: no kernel on the path reduces in a data-dependent order).
+ */
+typedef struct bse_comm bse_comm;
+/* Host broadcast used by the host-staged transport: broadcast `bytes` at
+ * host_buf from rank `root` to every rank; return 0 on success. */
+typedef int (*bse_host_bcast_fn)(void* ctx, void* host_buf, size_t bytes, int root);
+
+/* 128-byte ncclUniqueId (rank 0 creates it; the caller distributes it). */
+int bse_comm_nccl_unique_id(void* id128);
+/* NCCL communicator over libnccl.so.2 (resolved at run time). */
+int bse_comm_create_nccl(int rank, int world, const void* id128, bse_comm** out);
+/* Host-staged transport (device block -> host -> fn -> device). */
+int bse_comm_create_host(int rank, int world, bse_host_bcast_fn fn, void* ctx, bse_comm** out);
+/* Measurement only: acts as rank `rank` of `world` but exchanges nothing, so
+ * one GPU can time the kernels of one rank of a world-GPU solve (bench.py
+ * --simulate-rank-of).  Its results are NOT a solution. */
+int bse_comm_create_solo(int rank, int world, bse_comm** out);
+int bse_comm_destroy(bse_comm* comm);
+/* This rank's column block [c0, c1) of an n-column matrix. */
+int bse_shard_range(int64_t n, int world, int rank, int64_t* c0, int64_t* c1);
+/* Every rank's column block of dA (n columns, ld) broadcast to all ranks. */
+int bse_comm_allgather_cols_dev(bse_comm* comm, double* dA, int64_t ld, int64_t n, void* stream);
+int bse_solve_spd_pair_dist_dev(bse_comm* comm, int64_t n, const double* dM, int64_t ldm,
+                                const double* dK, int64_t ldk, double* dLam, double* dX1,
+                                int64_t ldx1, double* dX2, int64_t ldx2, void* dWork,
+                                size_t work_bytes, int flags, void* stream, bse_info* info);
 
 #ifdef __cplusplus
 }

@@ -21,6 +21,7 @@ BSE_CUDA_ERROR = 4
 
 FLAG_VALUES_ONLY = 0x1
 FLAG_ZPOLISH = 0x2
+FLAG_NATIVE_FP64 = 0x4
 
 
 class BseInfo(C.Structure):
@@ -54,11 +55,23 @@ SIGNATURES = {
                                       _P, _P, C.c_size_t, _P]),
     "bse_gemm_dev": (_INT, [_INT, _INT, _I64, _I64, _I64, _D, _P, _I64, _P, _I64, _D, _P, _I64,
                             _P, _P]),
+    "bse_ozgemm_dev": (_INT, [_INT, _INT, _I64, _I64, _I64, _D, _P, _I64, _P, _I64, _D, _P, _I64,
+                              _P, _I64, _P]),
     "bse_trsm_dev": (_INT, [_INT, _I64, _P, _I64, _P, _I64, _I64, _P]),
     "bse_profile_enable": (_INT, [_INT]),
     "bse_profile_read": (_INT, [_INT, C.POINTER(_D), C.c_char_p]),
     "bse_launch_count": (C.c_longlong, []),
     "bse_peak_fp64": (_INT, [_INT, _INT, _INT, _INT, C.POINTER(_D), C.POINTER(_D)]),
+    # column-sharded multi-GPU solve
+    "bse_comm_nccl_unique_id": (_INT, [_P]),
+    "bse_comm_create_nccl": (_INT, [_INT, _INT, _P, C.POINTER(_P)]),
+    "bse_comm_create_host": (_INT, [_INT, _INT, _P, _P, C.POINTER(_P)]),
+    "bse_comm_create_solo": (_INT, [_INT, _INT, C.POINTER(_P)]),
+    "bse_comm_destroy": (_INT, [_P]),
+    "bse_shard_range": (_INT, [_I64, _INT, _INT, C.POINTER(_I64), C.POINTER(_I64)]),
+    "bse_comm_allgather_cols_dev": (_INT, [_P, _P, _I64, _I64, _P]),
+    "bse_solve_spd_pair_dist_dev": (_INT, [_P, _I64, _P, _I64, _P, _I64, _P, _P, _I64, _P, _I64,
+                                           _P, C.c_size_t, _INT, _P, C.POINTER(BseInfo)]),
 }
 
 _lib = None

@@ -17,8 +17,10 @@ namespace bse {
 namespace {
 
 constexpr int kQ2G = 32;      // sweeps per block
-constexpr int kQ2W = 112;     // Z columns per CTA (14 warps x 8): 147 CTAs = one wave at n = 16384
-constexpr int kQ2Threads = 448;
+// Z columns per CTA = 8 x warps.  14 warps (112 columns): 147 CTAs = one wave
+// at n = 16384; narrower slabs (8/4/2 warps) keep >= 3/4 of the SMs busy when
+// fewer columns are applied (a rank's column block, mid-size n).
+constexpr int kQ2MaxWarps = 14;
 
 BSE_HD int q2_hb(int b, int g) { return ((g + b + 1) / 2) * 2; }  // padded block height
 
@@ -153,8 +155,8 @@ BSE_DEV void q2_block_t(double (&acc)[NT][2], const double* sV, const double* sV
 // stays in registers; 64 rows stream in (cp.async, one step ahead) and out
 // per STEP instead of per block.
 
-template <int P>
-__global__ void __launch_bounds__(kQ2Threads, 1) q2_apply_pair_kernel(int n, int b, int maxsteps,
+template <int P, int NW>
+__global__ void __launch_bounds__(32 * NW, 1) q2_apply_pair_kernel(int n, int b, int maxsteps,
                                                                       const double* __restrict__ Vblk,
                                                                       const double* __restrict__ VTblk,
                                                                       double* __restrict__ Z,
@@ -167,6 +169,7 @@ __global__ void __launch_bounds__(kQ2Threads, 1) q2_apply_pair_kernel(int n, int
   double* sZn = sm + 2 * STAGE;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int kl = lane & 3, rl = lane >> 2;
+  constexpr int kQ2W = 8 * NW, kQ2Threads = 32 * NW;
   const int cw = blockIdx.x * kQ2W + warp * 8;
   const int nsweeps = n - 2;
   const int ngroups = (int)ceil_div(nsweeps, G);
@@ -337,16 +340,20 @@ cudaError_t q2_apply(int n, int b, int g, const double* Vblk, const double* VTbl
   if (n <= 2 || ncols <= 0) return cudaSuccess;
   if (b != 64 || g != kQ2G || q2_hb(b, g) != kQ2HB) return cudaErrorInvalidValue;
   const int maxsteps = sb2st_maxsteps(n, b);
-  const size_t smem = sizeof(double) * (2 * (size_t)kQ2Stage + (size_t)kQ2W * kQ2LDN);
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(q2_apply_pair_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    attr = true;
-  }
-  q2_apply_pair_kernel<2><<<(unsigned)ceil_div(ncols, kQ2W), kQ2Threads, smem, s>>>(
-      n, b, maxsteps, Vblk, VTblk, Z, ldz, ncols);
-  count_launch();
-  return cudaGetLastError();
+  const int sms = device_sm_count();
+  auto launch = [&](auto kern, int nw) {
+    const size_t smem = sizeof(double) * (2 * (size_t)kQ2Stage + (size_t)8 * nw * kQ2LDN);
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    kern<<<(unsigned)ceil_div(ncols, 8 * nw), 32 * nw, smem, s>>>(n, b, maxsteps, Vblk, VTblk, Z,
+                                                                 ldz, ncols);
+    count_launch();
+    return cudaGetLastError();
+  };
+  auto enough = [&](int nw) { return 4 * ceil_div(ncols, 8 * nw) >= 3 * (long long)sms; };
+  if (enough(kQ2MaxWarps)) return launch(q2_apply_pair_kernel<2, kQ2MaxWarps>, kQ2MaxWarps);
+  if (enough(8)) return launch(q2_apply_pair_kernel<2, 8>, 8);
+  if (enough(4)) return launch(q2_apply_pair_kernel<2, 4>, 4);
+  return launch(q2_apply_pair_kernel<2, 2>, 2);
 }
 
 cudaError_t q1_apply(int n, int b, const double* Vall, long long ldv, const double* Tall,

@@ -5,7 +5,9 @@
 #include <cstring>
 #include <string>
 #include "../../include/bse_b200.h"
+#include "comm.cuh"
 #include "dense.cuh"
+#include "ozgemm.cuh"
 #include "solver.cuh"
 
 namespace {
@@ -50,6 +52,28 @@ int bse_gemm_dev(int transA, int transB, int64_t M, int64_t N, int64_t K, double
     p.mc = mask_from(masks + 6);
   }
   BSE_TRY_CUDA(bse::gemm(transA != 0, transB != 0, p, (cudaStream_t)stream), "gemm");
+  return BSE_OK;
+}
+
+int bse_ozgemm_dev(int transA, int transB, int64_t M, int64_t N, int64_t K, double alpha,
+                   const double* dA, int64_t lda, const double* dB, int64_t ldb, double beta,
+                   double* dC, int64_t ldc, const int32_t* masks, int64_t chunk, void* stream) {
+  if (M < 0 || N < 0 || K < 0) return fail(BSE_BAD_ARGUMENT, "negative dimension");
+  if (M == 0 || N == 0) return BSE_OK;
+  bse::GemmProblem p = bse::make_gemm((int)M, (int)N, (int)K, alpha, dA, lda, dB, ldb, beta, dC, ldc);
+  if (masks) {
+    p.ma = mask_from(masks);
+    p.mb = mask_from(masks + 3);
+    p.mc = mask_from(masks + 6);
+  }
+  const int ch = chunk > 0 ? (int)chunk : (int)N;
+  cudaStream_t s = (cudaStream_t)stream;
+  const size_t wb = bse::ozgemm_bytes((int)M, (int)N, (int)K, ch);
+  void* ws = nullptr;
+  BSE_TRY_CUDA(cudaMallocAsync(&ws, wb, s), "ozgemm workspace");
+  cudaError_t e = bse::ozgemm(transA != 0, transB != 0, p, ws, wb, ch, s);
+  cudaFreeAsync(ws, s);
+  BSE_TRY_CUDA(e, "ozgemm");
   return BSE_OK;
 }
 
@@ -296,6 +320,92 @@ int bse_peak_fp64(int which, int blocks, int iters, int reps, double* flops, dou
   *flops = f;
   *ms = t / reps;
   return BSE_OK;
+}
+
+/* ---- column-sharded multi-GPU solve ------------------------------------- */
+
+struct bse_comm {
+  bse::Comm* impl;
+};
+
+int bse_comm_nccl_unique_id(void* id128) {
+  std::string err;
+  if (!id128) return fail(BSE_BAD_ARGUMENT, "null id buffer");
+  if (bse::nccl_unique_id(id128, &err) != 0) return fail(BSE_CUDA_ERROR, "nccl: " + err);
+  return BSE_OK;
+}
+
+int bse_comm_create_nccl(int rank, int world, const void* id128, bse_comm** out) {
+  if (!out || !id128 || world < 1 || rank < 0 || rank >= world)
+    return fail(BSE_BAD_ARGUMENT, "bad communicator argument");
+  std::string err;
+  bse::Comm* c = bse::make_nccl_comm(rank, world, id128, &err);
+  if (!c) return fail(BSE_CUDA_ERROR, "nccl: " + err);
+  *out = new bse_comm{c};
+  return BSE_OK;
+}
+
+int bse_comm_create_host(int rank, int world, bse_host_bcast_fn fn, void* ctx, bse_comm** out) {
+  if (!out || !fn || world < 1 || rank < 0 || rank >= world)
+    return fail(BSE_BAD_ARGUMENT, "bad communicator argument");
+  *out = new bse_comm{bse::make_host_comm(rank, world, fn, ctx)};
+  return BSE_OK;
+}
+
+int bse_comm_create_solo(int rank, int world, bse_comm** out) {
+  if (!out || world < 1 || rank < 0 || rank >= world)
+    return fail(BSE_BAD_ARGUMENT, "bad communicator argument");
+  *out = new bse_comm{bse::make_solo_comm(rank, world)};
+  return BSE_OK;
+}
+
+int bse_comm_destroy(bse_comm* comm) {
+  if (comm) {
+    delete comm->impl;
+    delete comm;
+  }
+  return BSE_OK;
+}
+
+int bse_shard_range(int64_t n, int world, int rank, int64_t* c0, int64_t* c1) {
+  if (n < 0 || world < 1 || rank < 0 || rank >= world || !c0 || !c1)
+    return fail(BSE_BAD_ARGUMENT, "bad shard argument");
+  long long a, b;
+  bse::shard_range(n, world, rank, &a, &b);
+  *c0 = a;
+  *c1 = b;
+  return BSE_OK;
+}
+
+int bse_comm_allgather_cols_dev(bse_comm* comm, double* dA, int64_t ld, int64_t n, void* stream) {
+  if (!comm || n < 0 || ld < 1) return fail(BSE_BAD_ARGUMENT, "bad argument");
+  cudaError_t e = bse::allgather_cols(*comm->impl, dA, ld, n, (cudaStream_t)stream);
+  if (e != cudaSuccess) {
+    const std::string why = comm->impl->error();
+    return fail(BSE_CUDA_ERROR, "allgather_cols: " + (why.empty() ? std::string(cudaGetErrorString(e)) : why));
+  }
+  return BSE_OK;
+}
+
+int bse_solve_spd_pair_dist_dev(bse_comm* comm, int64_t n, const double* dM, int64_t ldm,
+                                const double* dK, int64_t ldk, double* dLam, double* dX1,
+                                int64_t ldx1, double* dX2, int64_t ldx2, void* dWork,
+                                size_t work_bytes, int flags, void* stream, bse_info* info) {
+  if (!comm) return fail(BSE_BAD_ARGUMENT, "null communicator");
+  if (flags & BSE_FLAG_VALUES_ONLY) return fail(BSE_BAD_ARGUMENT, "values-only is single-GPU");
+  if (n < 0 || ldm < n || ldk < n || ldx1 < n || ldx2 < n)
+    return fail(BSE_BAD_ARGUMENT, "bad dimension");
+  if (n > 0 && work_bytes < bse::solve_bytes((int)n, flags))
+    return fail(BSE_BAD_ARGUMENT, "workspace too small (see bse_solve_workspace_bytes)");
+  bse::SolveStatus st{};
+  cudaError_t e = bse::solve_spd_pair((int)n, dM, ldm, dK, ldk, dLam, dX1, ldx1, dX2, ldx2, dWork,
+                                      work_bytes, flags, (cudaStream_t)stream, &st, nullptr,
+                                      nullptr, comm->impl);
+  if (e != cudaSuccess) {
+    const std::string why = comm->impl->error();
+    return fail(BSE_CUDA_ERROR, "solve_dist: " + (why.empty() ? std::string(cudaGetErrorString(e)) : why));
+  }
+  return map_solve_status(st, info);
 }
 
 }  // extern "C"

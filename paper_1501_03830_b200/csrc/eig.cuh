@@ -100,8 +100,11 @@ cudaError_t tridiag_values(int n, const double* d, const double* e, double* w, d
 
 // Full pipeline on a symmetric matrix (lower triangle of A read, destroyed).
 size_t syevd_bytes(int n, int flags);
+// zc0/zc1: back-transform only Z columns [zc0, zc1) (the column shard of a
+// distributed solve; D&C still produces every column).  zc1 < 0 means n.
 cudaError_t syevd(int n, double* A, long long lda, double* w, double* Z, long long ldz,
-                  void* work, size_t work_bytes, int flags, cudaStream_t s);
+                  void* work, size_t work_bytes, int flags, cudaStream_t s, int zc0 = 0,
+                  int zc1 = -1);
 
 int device_sm_count();
 

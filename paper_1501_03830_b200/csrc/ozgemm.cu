@@ -1,0 +1,386 @@
+// FP64 GEMM emulated on the INT8 tensor cores (Ozaki scheme II: integer
+// slices + Chinese remaindering), for the large-K dense products of the solve.
+//
+//   C := alpha * op(A) * op(B) + beta * C       (FP64, column-major)
+//
+// 1. Each row i of op(A) and column j of op(B) is scaled by a power of two so
+//    its largest entry lies in [2^(beta-1), 2^beta) and truncated to an
+//    integer (beta <= 53 bits: exact in a double).  The integer product
+//    C' = A' B' is then computed EXACTLY modulo 16 pairwise-coprime moduli
+//    m_t <= 256 (product 2^125.4 > 2 |C'|):
+// 2. residues A'_t, B'_t in [-128, 127] (int8, K-major), one batched
+//    tcgen05 kind::i8 GEMM (CUTLASS sm_100 2-SM kernel, INT32 accumulators in
+//    TMEM) gives C_t = A'_t B'_t exactly;
+// 3. C' is rebuilt per element by the CRT in double-double arithmetic,
+//    scaled back by 2^-(s_i + s_j) and written with alpha/beta and the output
+//    mask.
+// The truncation error per entry is below 2^-52 of its row (column) maximum,
+// so the result is as accurate as a DGEMM for the operands it is used on
+// (orthogonal / triangular factors with bounded row ranges); tests compare it
+// against the DMMA engine and float64 numpy.
+#include <algorithm>
+#include <cmath>
+#include <cstdint>
+#include <cstdio>
+#include "cutlass/cutlass.h"
+#include "cute/tensor.hpp"
+#include "cutlass/epilogue/collective/collective_builder.hpp"
+#include "cutlass/gemm/collective/collective_builder.hpp"
+#include "cutlass/gemm/device/gemm_universal_adapter.h"
+#include "cutlass/gemm/dispatch_policy.hpp"
+#include "cutlass/gemm/kernel/gemm_universal.hpp"
+#include "cutlass/util/packed_stride.hpp"
+#include "ozgemm.cuh"
+
+namespace bse {
+namespace {
+
+constexpr int kMods = 16;
+// pairwise coprime (2^8, 3.5.17, 11.23, 251, 13.19, 241, 239, 233, 229, 227,
+// 223, 7.31, 211, 199, 197, 193); compile-time after unrolling, so every
+// "% m" below is a multiply-shift
+BSE_HD constexpr int kMod(int t) {
+  return t == 0 ? 256 : t == 1 ? 255 : t == 2 ? 253 : t == 3 ? 251 : t == 4 ? 247 : t == 5 ? 241
+       : t == 6 ? 239 : t == 7 ? 233 : t == 8 ? 229 : t == 9 ? 227 : t == 10 ? 223
+       : t == 11 ? 217 : t == 12 ? 211 : t == 13 ? 199 : t == 14 ? 197 : 193;
+}
+
+struct CrtConst {
+  double inv_m[kMods];   // 1 / m_t
+  double mhi[kMods];     // M_t = P / m_t as hi + lo
+  double mlo[kMods];
+  int y[kMods];          // M_t^{-1} mod m_t
+  double phi, plo;       // P = prod m_t
+};
+__constant__ CrtConst c_crt;
+
+// ---------------------------------------------------------------------------
+// CUTLASS sm_100 int8 x int8 -> int32, A row-major (K-major), B column-major
+// (K-major), C column-major; 256x256x128 tiles on 2-SM clusters.
+namespace cg = cutlass::gemm;
+using namespace cute;
+using MmaTile = Shape<_256, _256, _128>;
+using ClusterShape = Shape<_2, _1, _1>;
+using Epi = typename cutlass::epilogue::collective::CollectiveBuilder<
+    cutlass::arch::Sm100, cutlass::arch::OpClassTensorOp, MmaTile, ClusterShape,
+    cutlass::epilogue::collective::EpilogueTileAuto, int32_t, int32_t, int32_t,
+    cutlass::layout::ColumnMajor, 4, int32_t, cutlass::layout::ColumnMajor, 4,
+    cutlass::epilogue::TmaWarpSpecialized2Sm>::CollectiveOp;
+using Main = typename cg::collective::CollectiveBuilder<
+    cutlass::arch::Sm100, cutlass::arch::OpClassTensorOp, int8_t, cutlass::layout::RowMajor, 16,
+    int8_t, cutlass::layout::ColumnMajor, 16, int32_t, MmaTile, ClusterShape,
+    cg::collective::StageCountAutoCarveout<static_cast<int>(sizeof(typename Epi::SharedStorage))>,
+    cg::KernelTmaWarpSpecialized2SmSm100>::CollectiveOp;
+using Kernel = cg::kernel::GemmUniversal<Shape<int, int, int, int>, Main, Epi>;
+using I8Gemm = cg::device::GemmUniversalAdapter<Kernel>;
+
+cudaError_t i8_gemm_batched(int M, int N, int K, int L, const int8_t* A, const int8_t* B,
+                            int32_t* C, cudaStream_t s) {
+  auto sA = cutlass::make_cute_packed_stride(typename Kernel::StrideA{}, {M, K, L});
+  auto sB = cutlass::make_cute_packed_stride(typename Kernel::StrideB{}, {N, K, L});
+  auto sC = cutlass::make_cute_packed_stride(typename Kernel::StrideC{}, {M, N, L});
+  auto sD = cutlass::make_cute_packed_stride(typename Kernel::StrideD{}, {M, N, L});
+  typename I8Gemm::Arguments args{cg::GemmUniversalMode::kGemm, {M, N, K, L}, {A, sA, B, sB},
+                                  {{1, 0}, C, sC, C, sD}};
+  I8Gemm gemm;
+  if (gemm.can_implement(args) != cutlass::Status::kSuccess) return cudaErrorInvalidValue;
+  if (I8Gemm::get_workspace_size(args) != 0) return cudaErrorInvalidValue;
+  if (gemm.initialize(args, nullptr, s) != cutlass::Status::kSuccess) return cudaErrorInvalidValue;
+  if (gemm.run(s) != cutlass::Status::kSuccess) return cudaErrorLaunchFailure;
+  count_launch();
+  return cudaGetLastError();
+}
+
+// ---------------------------------------------------------------------------
+// Slicing.  "Line" r of an operand is a row of op(A) or a column of op(B);
+// it is written K-contiguous as 16 int8 residue rows out[t][r][0..Kp).
+// Stored element of line r, position k:
+//   contiguous: src[r * ld + k], stored coordinates (row, col) = (k, r)
+//   strided:    src[r + k * ld], stored coordinates (row, col) = (r, k)
+
+BSE_DEV double masked(double v, int row, int col, const Mask& m) {
+  const int d = col - row;
+  if (m.unit && d == 0) return 1.0;
+  return (d < m.lo || d > m.hi) ? 0.0 : v;
+}
+
+// scale exponent so that max |x| * 2^s lies in [2^(beta-1), 2^beta)
+BSE_DEV int scale_exp(double mx, int beta) {
+  if (!(mx > 0.0)) return 0;
+  int e;
+  frexp(mx, &e);  // mx = f 2^e, f in [0.5, 1)
+  return beta - e;
+}
+
+BSE_DEV uint32_t residues4(const double (&x)[4], int t, int m, double inv_m) {
+  uint32_t w = 0;
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    double r = fma(-rint(x[q] * inv_m), (double)m, x[q]);  // exact: |r| < 1.5 m
+    if (r >= 0.5 * m) r -= m;
+    if (r < -0.5 * m) r += m;
+    w |= ((uint32_t)(int)r & 0xffu) << (8 * q);
+  }
+  (void)t;
+  return w;
+}
+
+// One warp per line, contiguous source.
+__global__ void __launch_bounds__(256) split_contig_kernel(int lines, int K, int Kp,
+                                                           const double* __restrict__ src,
+                                                           long long ld, Mask mk, int beta,
+                                                           int8_t* __restrict__ out,
+                                                           long long mod_stride,
+                                                           int* __restrict__ sexp) {
+  const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+  const int r = warp;
+  const int rows_alloc = (int)(mod_stride / Kp);
+  if (r >= rows_alloc) return;
+  const bool live = r < lines;
+  const double* row = src + (long long)(live ? r : 0) * ld;
+  double mx = 0.0;
+  if (live)
+    for (int k = lane; k < K; k += 32) mx = fmax(mx, fabs(masked(row[k], k, r, mk)));
+  mx = warp_max(mx);
+  const int se = scale_exp(mx, beta);
+  if (lane == 0) sexp[r] = se;
+  uint32_t* o = reinterpret_cast<uint32_t*>(out + (long long)r * Kp);
+  for (int k0 = 4 * lane; k0 < Kp; k0 += 128) {
+    double x[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int k = k0 + q;
+      x[q] = (live && k < K) ? trunc(ldexp(masked(row[k], k, r, mk), se)) : 0.0;
+    }
+#pragma unroll
+    for (int t = 0; t < kMods; ++t)
+      o[t * (mod_stride / 4) + k0 / 4] = residues4(x, t, kMod(t), c_crt.inv_m[t]);
+  }
+}
+
+// Strided source: line maxima first (thread per line, k split over gridDim.y).
+__global__ void strided_max_kernel(int lines, int K, const double* __restrict__ src, long long ld,
+                                   Mask mk, unsigned long long* __restrict__ mx_bits) {
+  const int r = blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= lines) return;
+  const int kc = (K + gridDim.y - 1) / gridDim.y;
+  const int k0 = blockIdx.y * kc, k1 = min(K, k0 + kc);
+  double mx = 0.0;
+  for (int k = k0; k < k1; ++k) mx = fmax(mx, fabs(masked(src[r + (long long)k * ld], r, k, mk)));
+  atomicMax(mx_bits + r, (unsigned long long)__double_as_longlong(mx));
+}
+
+// 64 lines x 64 k per CTA: coalesced loads along lines into shared memory,
+// residues written K-contiguous.
+__global__ void __launch_bounds__(256) split_strided_kernel(int lines, int K, int Kp,
+                                                            const double* __restrict__ src,
+                                                            long long ld, Mask mk, int beta,
+                                                            const unsigned long long* __restrict__ mx_bits,
+                                                            int8_t* __restrict__ out,
+                                                            long long mod_stride,
+                                                            int* __restrict__ sexp) {
+  __shared__ double tile[64][65];  // [k][line]
+  __shared__ int se_s[64];
+  const int r0 = blockIdx.x * 64, k0 = blockIdx.y * 64, tid = threadIdx.x;
+  if (tid < 64) {
+    const int r = r0 + tid;
+    const double mx = r < lines ? __longlong_as_double((long long)mx_bits[r]) : 0.0;
+    se_s[tid] = scale_exp(mx, beta);
+    if (blockIdx.y == 0 && (long long)r * Kp < mod_stride) sexp[r] = se_s[tid];
+  }
+  __syncthreads();
+  for (int idx = tid; idx < 64 * 64; idx += 256) {
+    const int rl = idx & 63, kl = idx >> 6;
+    const int r = r0 + rl, k = k0 + kl;
+    double v = 0.0;
+    if (r < lines && k < K) v = trunc(ldexp(masked(src[r + (long long)k * ld], r, k, mk), se_s[rl]));
+    tile[kl][rl] = v;
+  }
+  __syncthreads();
+  // thread -> (line, 4 consecutive k)
+  for (int idx = tid; idx < 64 * 16; idx += 256) {
+    const int rl = idx >> 4, kq = (idx & 15) * 4;
+    const int r = r0 + rl, k = k0 + kq;
+    if ((long long)r * Kp >= mod_stride || k >= Kp) continue;
+    double x[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) x[q] = tile[kq + q][rl];
+    uint32_t* o = reinterpret_cast<uint32_t*>(out + (long long)r * Kp + k);
+#pragma unroll
+    for (int t = 0; t < kMods; ++t) o[t * (mod_stride / 4)] = residues4(x, t, kMod(t), c_crt.inv_m[t]);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// CRT reconstruction in double-double.
+
+BSE_DEV void two_sum(double a, double b, double& s, double& e) {
+  s = a + b;
+  const double bb = s - a;
+  e = (a - (s - bb)) + (b - bb);
+}
+
+__global__ void __launch_bounds__(256) crt_kernel(int M, int N, int Mp, const int32_t* __restrict__ c32,
+                                                  long long batch, const int* __restrict__ sa,
+                                                  const int* __restrict__ sb, double alpha,
+                                                  double beta, double* __restrict__ C,
+                                                  long long ldc, int col0, Mask mc) {
+  const long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (idx >= (long long)M * N) return;
+  const int i = (int)(idx % M), j = (int)(idx / M);
+  const int d = (col0 + j) - i;
+  if (d < mc.lo || d > mc.hi) return;
+  const int32_t* p = c32 + i + (long long)j * Mp;
+  double hi = 0.0, lo = 0.0, frac = 0.0;
+#pragma unroll
+  for (int t = 0; t < kMods; ++t) {
+    const int m = kMod(t);
+    int r = p[t * batch] % m;
+    int u = (r * c_crt.y[t]) % m;
+    if (u < 0) u += m;
+    const double du = (double)u;
+    frac += du * c_crt.inv_m[t];
+    const double ph = du * c_crt.mhi[t];
+    const double pe = fma(du, c_crt.mhi[t], -ph);
+    double s, e;
+    two_sum(hi, ph, s, e);
+    hi = s;
+    lo += e + pe + du * c_crt.mlo[t];
+  }
+  const double q = rint(frac);
+  {
+    const double ph = -q * c_crt.phi;
+    const double pe = fma(-q, c_crt.phi, -ph);
+    double s, e;
+    two_sum(hi, ph, s, e);
+    hi = s;
+    lo += e + pe - q * c_crt.plo;
+  }
+  const double cp = hi + lo;
+  double v = alpha * ldexp(cp, -(sa[i] + sb[j]));
+  double* cd = C + i + (long long)(col0 + j) * ldc;
+  if (beta != 0.0) v += beta * *cd;
+  *cd = v;
+}
+
+long long r16(long long x) { return (x + 15) / 16 * 16; }
+
+bool g_const_ready = false;
+
+cudaError_t init_const() {
+  if (g_const_ready) return cudaSuccess;
+  CrtConst h{};
+  // exact integer arithmetic (P < 2^126 fits in 128 bits); hi = rn(x),
+  // lo = rn(x - hi) with the difference formed exactly
+  using u128 = unsigned __int128;
+  using i128 = __int128;
+  auto to_dd = [](u128 x, double& hi, double& lo) {
+    hi = (double)x;
+    const i128 diff = (i128)x - (i128)(u128)hi;
+    lo = (double)diff;
+  };
+  u128 P = 1;
+  for (int t = 0; t < kMods; ++t) P *= (u128)kMod(t);
+  to_dd(P, h.phi, h.plo);
+  for (int t = 0; t < kMods; ++t) {
+    const u128 Mt = P / (u128)kMod(t);
+    to_dd(Mt, h.mhi[t], h.mlo[t]);
+    const long long mt_mod = (long long)(Mt % (u128)kMod(t));
+    int y = 1;
+    while ((mt_mod * y) % kMod(t) != 1) ++y;
+    h.y[t] = y;
+    h.inv_m[t] = 1.0 / kMod(t);
+  }
+  cudaError_t e = cudaMemcpyToSymbol(c_crt, &h, sizeof(h));
+  if (e == cudaSuccess) g_const_ready = true;
+  return e;
+}
+
+}  // namespace
+
+size_t ozgemm_bytes(int M, int N, int K, int chunk) {
+  const long long Mp = r16(M), Kp = r16(K), Np = r16(std::min(N, chunk));
+  const size_t a8 = (size_t)kMods * Mp * Kp, b8 = (size_t)kMods * Np * Kp;
+  const size_t c32 = (size_t)kMods * Mp * Np * 4;
+  return a8 + b8 + c32 + 8 * (size_t)(Mp + Np) * 2 + 4096;
+}
+
+cudaError_t ozgemm(bool transA, bool transB, const GemmProblem& p, void* work, size_t work_bytes,
+                   int chunk, cudaStream_t s, bool reuse_a) {
+  if (p.M <= 0 || p.N <= 0) return cudaSuccess;
+  cudaError_t e;
+  if ((e = init_const()) != cudaSuccess) return e;
+  const int M = p.M, K = p.K;
+  const long long Mp = r16(M), Kp = r16(std::max(K, 1));
+  const int nc_max = std::min(p.N, chunk);
+  const long long Np = r16(nc_max);
+  if (work_bytes < ozgemm_bytes(M, p.N, K, chunk)) return cudaErrorInvalidValue;
+  char* w = static_cast<char*>(work);
+  int8_t* a8 = reinterpret_cast<int8_t*>(w);
+  w += (size_t)kMods * Mp * Kp;
+  int8_t* b8 = reinterpret_cast<int8_t*>(w);
+  w += (size_t)kMods * Np * Kp;
+  int32_t* c32 = reinterpret_cast<int32_t*>(w);
+  w += (size_t)kMods * Mp * Np * 4;
+  unsigned long long* mxa = reinterpret_cast<unsigned long long*>(w);
+  w += 8 * (size_t)Mp;
+  unsigned long long* mxb = reinterpret_cast<unsigned long long*>(w);
+  w += 8 * (size_t)Np;
+  int* sa = reinterpret_cast<int*>(w);
+  w += 4 * (size_t)Mp;
+  int* sb = reinterpret_cast<int*>(w);
+  // fixed-point width: 2 beta + log2 K + 2 < log2 P (125.4)
+  int lk = 0;
+  while ((1LL << lk) < K) ++lk;
+  const int beta = std::min(53, (123 - lk) / 2);
+  auto split = [&](bool contiguous, int lines, const double* src, long long ld, Mask mk,
+                   int8_t* out, long long rows_alloc, int* sexp, unsigned long long* mxbuf) {
+    const long long mstride = rows_alloc * Kp;
+    if (contiguous) {
+      const unsigned blocks = (unsigned)ceil_div(rows_alloc * 32, 256);
+      split_contig_kernel<<<blocks, 256, 0, s>>>(lines, K, (int)Kp, src, ld, mk, beta, out,
+                                                 mstride, sexp);
+      count_launch();
+    } else {
+      cudaMemsetAsync(mxbuf, 0, 8 * (size_t)rows_alloc, s);
+      const int ysplit = (int)std::min<long long>(64, std::max<long long>(1, K / 256));
+      strided_max_kernel<<<dim3((unsigned)ceil_div(lines, 256), ysplit), 256, 0, s>>>(
+          lines, K, src, ld, mk, mxbuf);
+      split_strided_kernel<<<dim3((unsigned)ceil_div(rows_alloc, 64), (unsigned)ceil_div(Kp, 64)),
+                             256, 0, s>>>(lines, K, (int)Kp, src, ld, mk, beta, mxbuf, out, mstride,
+                                          sexp);
+      count_launch(2);
+    }
+    return cudaGetLastError();
+  };
+  // op(A) rows: stored A is M x K (transA false: strided lines) or K x M (contiguous)
+  if (!reuse_a && (e = split(transA, M, p.A, p.lda, p.ma, a8, Mp, sa, mxa)) != cudaSuccess) return e;
+  for (int j0 = 0; j0 < p.N; j0 += nc_max) {
+    const int nc = std::min(nc_max, p.N - j0);
+    const long long ncp = r16(nc);
+    // op(B) columns: stored B is K x N (transB false: contiguous lines) or N x K.
+    // Masks are view-relative to the stored matrix: shift by the chunk offset.
+    Mask mb = p.mb;
+    const double* bsrc;
+    if (!transB) {
+      bsrc = p.B + (long long)j0 * p.ldb;
+      if (mb.lo != kNoMaskLo) mb.lo -= j0;
+      if (mb.hi != kNoMaskHi) mb.hi -= j0;
+    } else {
+      bsrc = p.B + j0;
+      if (mb.lo != kNoMaskLo) mb.lo += j0;
+      if (mb.hi != kNoMaskHi) mb.hi += j0;
+    }
+    if ((e = split(!transB, nc, bsrc, p.ldb, mb, b8, ncp, sb, mxb)) != cudaSuccess) return e;
+    if ((e = i8_gemm_batched((int)Mp, (int)ncp, (int)Kp, kMods, a8, b8, c32, s)) != cudaSuccess)
+      return e;
+    const long long tot = (long long)M * nc;
+    crt_kernel<<<(unsigned)ceil_div(tot, 256), 256, 0, s>>>(M, nc, (int)Mp, c32, Mp * ncp, sa, sb,
+                                                           p.alpha, p.beta, p.C, p.ldc, j0, p.mc);
+    count_launch();
+    if ((e = cudaGetLastError()) != cudaSuccess) return e;
+  }
+  return cudaSuccess;
+}
+
+}  // namespace bse

@@ -1,0 +1,21 @@
+// FP64 GEMM emulated on the INT8 tensor cores (Ozaki scheme II), see ozgemm.cu.
+#pragma once
+#include <cuda_runtime.h>
+#include "gemm.cuh"
+
+namespace bse {
+
+// Workspace for an M x N x K product processed in column chunks of `chunk`.
+size_t ozgemm_bytes(int M, int N, int K, int chunk);
+
+// C := alpha op(A) op(B) + beta C with the operand masks of GemmProblem
+// (view-relative, as in gemm()) and the output mask.  Column map (ccol) is
+// not supported.  reuse_a: the workspace already holds the slices of this
+// op(A) from the previous call (same A, M, K and workspace).
+cudaError_t ozgemm(bool transA, bool transB, const GemmProblem& p, void* work, size_t work_bytes,
+                   int chunk, cudaStream_t s, bool reuse_a = false);
+
+// Products at least this large (M N K) go to the emulated engine.
+constexpr double kOzMinWork = 1024.0 * 1024.0 * 1024.0 * 64.0;
+
+}  // namespace bse

@@ -7,6 +7,8 @@
 #include <string>
 #include <vector>
 #include "eig.cuh"
+#include "comm.cuh"
+#include "ozgemm.cuh"
 #include "solver.cuh"
 
 namespace bse {
@@ -107,7 +109,7 @@ size_t syevd_bytes(int n, int flags) {
 }
 
 cudaError_t syevd(int n, double* A, long long lda, double* w, double* Z, long long ldz,
-                  void* work, size_t work_bytes, int flags, cudaStream_t s) {
+                  void* work, size_t work_bytes, int flags, cudaStream_t s, int zc0, int zc1) {
   if (n <= 0) return cudaSuccess;
   Arena a{static_cast<char*>(work), work_bytes, 0, false};
   SyevdWork ws = carve_syevd(a, n);
@@ -130,10 +132,14 @@ cudaError_t syevd(int n, double* A, long long lda, double* w, double* Z, long lo
   if ((e = stedc(n, ws.d, ws.e, w, Z, ldz, ws.dc, s)) != cudaSuccess) return e;
   stage_mark("q2_build", s);
   if ((e = q2_build(n, b, kQ2Group, ws.V2, ws.tau2, ws.Vblk, ws.VTblk, s)) != cudaSuccess) return e;
+  if (zc1 < 0) zc1 = n;
+  double* Zs = Z + (long long)zc0 * ldz;
+  const int nz = zc1 - zc0;
   stage_mark("q2_apply", s);
-  if ((e = q2_apply(n, b, kQ2Group, ws.Vblk, ws.VTblk, Z, ldz, n, s)) != cudaSuccess) return e;
+  if ((e = q2_apply(n, b, kQ2Group, ws.Vblk, ws.VTblk, Zs, ldz, nz, s)) != cudaSuccess) return e;
   stage_mark("q1_apply", s);
-  return q1_apply(n, b, ws.Vall, ws.ldv, ws.Tall, Z, ldz, n, ws.q1, s);
+  if (nz <= 0) return cudaSuccess;
+  return q1_apply(n, b, ws.Vall, ws.ldv, ws.Tall, Zs, ldz, nz, ws.q1, s);
 }
 
 // ---------------------------------------------------------------------------
@@ -147,7 +153,10 @@ struct SolveWork {
   double* linv;
   DevStatus* st;
   void* eig; size_t eig_bytes;
+  void* oz; size_t oz_bytes;  // emulated-FP64 workspace (aliases eig when it fits)
 };
+
+bool use_oz(int n, int flags) { return !(flags & kFlagNativeFp64) && n >= kOzMinN; }
 
 SolveWork carve_solve(Arena& a, int n, int flags) {
   SolveWork w{};
@@ -161,6 +170,8 @@ SolveWork carve_solve(Arena& a, int n, int flags) {
   w.st = a.take<DevStatus>(2);
   w.eig_bytes = syevd_bytes(n, flags);
   w.eig = a.take<char>(w.eig_bytes);
+  w.oz_bytes = use_oz(n, flags) ? ozgemm_bytes(n, n, n, kRecoverBlock) : 0;
+  w.oz = w.oz_bytes <= w.eig_bytes ? w.eig : a.take<char>(w.oz_bytes);
   return w;
 }
 
@@ -171,23 +182,25 @@ __global__ void copy_lower_kernel(int n, const double* src, long long lds, doubl
   dst[r + (long long)c * ldd] = (r >= c) ? src[r + (long long)c * lds] : 0.0;
 }
 
-// v <- Z(:, col) * lam_j, with the column order reversed (descending lam).
-__global__ void scale_reverse_kernel(int n, const double* Z, long long ldz, const double* lam2,
-                                     double* Zr, double* V, long long ld, double* lam_out,
-                                     int* bad) {
+// Output columns [c0, c0 + nc): v <- Z(:, n-1-c) * lam_c, Zr(:, c) <- Z(:, n-1-c)
+// (descending lam).  lam_out and the definiteness flag cover all n columns.
+__global__ void scale_reverse_kernel(int n, int c0, int nc, const double* Z, long long ldz,
+                                     const double* lam2, double* Zr, double* V, long long ld,
+                                     double* lam_out, int* bad) {
   const long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x;
-  if (idx >= (long long)n * n) return;
-  const int r = (int)(idx % n), c = (int)(idx / n);
+  if (idx < n) {
+    const double l2 = lam2[n - 1 - idx];
+    lam_out[idx] = l2 > 0.0 ? sqrt(l2) : 0.0;
+    if (!(l2 > 0.0)) atomicExch(bad, 1);
+  }
+  if (idx >= (long long)n * nc) return;
+  const int r = (int)(idx % n), c = c0 + (int)(idx / n);
   const int src = n - 1 - c;
   const double l2 = lam2[src];
   const double lam = l2 > 0.0 ? sqrt(l2) : 0.0;
   const double z = Z[r + (long long)src * ldz];
   Zr[r + (long long)c * ld] = z;
   V[r + (long long)c * ld] = z * lam;
-  if (r == 0) {
-    lam_out[c] = lam;
-    if (!(l2 > 0.0)) atomicExch(bad, 1);
-  }
 }
 
 // X1 = (u + v) / (2 sqrt(lam)), X2 = (u - v) / (2 sqrt(lam))  (n rows, ncols columns)
@@ -216,7 +229,8 @@ size_t solve_bytes(int n, int flags) {
 cudaError_t solve_spd_pair(int n, const double* M, long long ldm, const double* K, long long ldk,
                            double* lam, double* X1, long long ldx1, double* X2, long long ldx2,
                            void* work, size_t work_bytes, int flags, cudaStream_t s,
-                           SolveStatus* out, cudaEvent_t m_ready, const HostOut* hout) {
+                           SolveStatus* out, cudaEvent_t m_ready, const HostOut* hout,
+                           Comm* comm) {
   out->code = 0;
   out->pivot_index = -1;
   out->pivot_value = 0.0;
@@ -238,42 +252,72 @@ cudaError_t solve_spd_pair(int n, const double* M, long long ldm, const double* 
   if ((e = potrf_lower(w.L, ld, n, &w.st[0], s, w.linv)) != cudaSuccess) return e;
   if (m_ready && (e = cudaStreamWaitEvent(s, m_ready, 0)) != cudaSuccess) return e;
   stage_mark("congruence", s);
+  // Distributed: this rank forms the column block [c0, c1) of T1 and W, then
+  // every block is broadcast from its owner (the only exchange before the
+  // replicated reduction).  Masks are view-relative, so a block starting at
+  // column c0 shifts the diagonal of L, T1 and W by -c0.
+  const int world = comm ? comm->world : 1;
+  long long c0 = 0, c1 = n;
+  if (world > 1) shard_range(n, world, comm->rank, &c0, &c1);
+  const int nc = (int)(c1 - c0);
+  const int sh = (int)c0;
   // 2. W = L^T M L  (T1 = M L from the lower triangle of M, then W = L^T T1, lower)
-  GemmProblem g1 = make_gemm(n, n, n, 1.0, M, ldm, w.L, ld, 0.0, w.T1, ld);
+  GemmProblem g1 = make_gemm(n, nc, n, 1.0, M, ldm, w.L + c0 * ld, ld, 0.0, w.T1 + c0 * ld, ld);
   g1.ma = Mask::lower();
-  g1.mb = Mask::lower();
-  if ((e = gemm(false, false, g1, s)) != cudaSuccess) return e;
+  g1.mb = Mask{kNoMaskLo, -sh, 0};
+  if (nc > 0 && (e = gemm(false, false, g1, s)) != cudaSuccess) return e;
   // only T1's lower triangle feeds W = L^T T1 (lower): the strictly-upper
   // half of M's contribution is needed for rows k >= j only (N^3/3 flops
   // saved); g1 has already zeroed T1's upper triangle (k-range empty there)
-  GemmProblem g2 = make_gemm(n, n, n, 1.0, M, ldm, w.L, ld, 1.0, w.T1, ld);
+  GemmProblem g2 = make_gemm(n, nc, n, 1.0, M, ldm, w.L + c0 * ld, ld, 1.0, w.T1 + c0 * ld, ld);
   g2.ma = Mask::strict_lower();
-  g2.mb = Mask::lower();
-  g2.mc = Mask::lower();
-  if ((e = gemm(true, false, g2, s)) != cudaSuccess) return e;
-  GemmProblem g3 = make_gemm(n, n, n, 1.0, w.L, ld, w.T1, ld, 0.0, w.W, ld);
+  g2.mb = Mask{kNoMaskLo, -sh, 0};
+  g2.mc = Mask{kNoMaskLo, -sh, 0};
+  if (nc > 0 && (e = gemm(true, false, g2, s)) != cudaSuccess) return e;
+  GemmProblem g3 = make_gemm(n, nc, n, 1.0, w.L, ld, w.T1 + c0 * ld, ld, 0.0, w.W + c0 * ld, ld);
   g3.ma = Mask::lower();
-  g3.mc = Mask::lower();
-  if ((e = gemm(true, false, g3, s)) != cudaSuccess) return e;
-  // 3. W = Z diag(lam^2) Z^T (ascending lam^2); Z into T1
-  if ((e = syevd(n, w.W, ld, w.lam2, w.T1, ld, w.eig, w.eig_bytes, flags, s)) != cudaSuccess) return e;
+  g3.mc = Mask{kNoMaskLo, -sh, 0};
+  if (nc > 0 && (e = gemm(true, false, g3, s)) != cudaSuccess) return e;
+  if (world > 1) {
+    stage_mark("allgather_w", s);
+    if ((e = allgather_cols(*comm, w.W, ld, n, s)) != cudaSuccess) return e;
+  }
+  // 3. W = Z diag(lam^2) Z^T (ascending lam^2); Z into T1.  The reduction and
+  // D&C are replicated; only this rank's eigenvector columns (output columns
+  // [c0, c1) = Z columns [n - c1, n - c0)) are back-transformed.
+  if ((e = syevd(n, w.W, ld, w.lam2, w.T1, ld, w.eig, w.eig_bytes, flags, s, (int)(n - c1),
+                 (int)(n - c0))) != cudaSuccess)
+    return e;
   stage_mark("recover", s);
   // 4. descending order; v = Z Lam into W, Z reversed into Zr
   int* bad = reinterpret_cast<int*>(&w.st[1].conv_fail);
-  scale_reverse_kernel<<<nb, 256, 0, s>>>(n, w.T1, ld, w.lam2, w.Zr, w.W, ld, lam, bad);
-  count_launch();
+  {
+    const long long tot_sh = std::max<long long>((long long)n * nc, n);
+    scale_reverse_kernel<<<(unsigned)ceil_div(tot_sh, 256), 256, 0, s>>>(
+        n, (int)c0, nc, w.T1, ld, w.lam2, w.Zr, w.W, ld, lam, bad);
+    count_launch();
+  }
   // u = L Zr (into T1), v = L^{-T} (Zr Lam) (in W); with host outputs the
   // recovery runs in column blocks so each block's D2H copy overlaps the next
   // block's TRMM/TRSM
   const int cb = hout ? kRecoverBlock : n;
   std::vector<cudaEvent_t> evs;
-  for (int c0 = 0; c0 < n; c0 += cb) {
-    const int nc = std::min(cb, n - c0);
+  bool first_block = true;
+  for (int cs = (int)c0; cs < (int)c1; cs += cb) {
+    const int c0 = cs;
+    const int nc = std::min(cb, (int)c1 - cs);
     stage_mark("recover_trmm", s);
     GemmProblem g4 = make_gemm(n, nc, n, 1.0, w.L, ld, w.Zr + (long long)c0 * ld, ld, 0.0,
                                w.T1 + (long long)c0 * ld, ld);
     g4.ma = Mask::lower();
-    if ((e = gemm(false, false, g4, s)) != cudaSuccess) return e;
+    if (w.oz_bytes) {
+      // L is sliced once; every column block reuses its residues
+      if ((e = ozgemm(false, false, g4, w.oz, w.oz_bytes, kRecoverBlock, s, !first_block)) != cudaSuccess)
+        return e;
+    } else if ((e = gemm(false, false, g4, s)) != cudaSuccess) {
+      return e;
+    }
+    first_block = false;
     stage_mark("recover_trsm", s);
     if ((e = trsm_llt(w.L, ld, n, w.W + (long long)c0 * ld, ld, nc, s, w.linv)) != cudaSuccess)
       return e;
@@ -298,6 +342,11 @@ cudaError_t solve_spd_pair(int n, const double* M, long long ldm, const double* 
                                  cudaMemcpyDeviceToHost, hout->stream)) != cudaSuccess)
         return e;
     }
+  }
+  if (world > 1) {
+    stage_mark("allgather_x", s);
+    if ((e = allgather_cols(*comm, X1, ldx1, n, s)) != cudaSuccess) return e;
+    if ((e = allgather_cols(*comm, X2, ldx2, n, s)) != cudaSuccess) return e;
   }
   if (hout) {
     if ((e = cudaMemcpyAsync(hout->lam, lam, sizeof(double) * n, cudaMemcpyDeviceToHost, s)) !=

@@ -1,6 +1,7 @@
 // Pipeline-level declarations shared by the C ABI.
 #pragma once
 #include <cuda_runtime.h>
+#include "comm.cuh"
 #include "eig.cuh"
 
 #include <string>
@@ -34,13 +35,17 @@ struct HostOut {
   cudaStream_t stream;
 };
 constexpr int kRecoverBlock = 2048;
+// BSE_FLAG_NATIVE_FP64: every product on the DMMA engine (no INT8 emulation)
+constexpr int kFlagNativeFp64 = 0x4;
+// the emulated-FP64 engine is used for the large products from this n up
+constexpr int kOzMinN = 4096;
 
 size_t solve_bytes(int n, int flags);
 cudaError_t solve_spd_pair(int n, const double* M, long long ldm, const double* K, long long ldk,
                            double* lam, double* X1, long long ldx1, double* X2, long long ldx2,
                            void* work, size_t work_bytes, int flags, cudaStream_t s,
                            SolveStatus* out, cudaEvent_t m_ready = nullptr,
-                           const HostOut* hout = nullptr);
+                           const HostOut* hout = nullptr, Comm* comm = nullptr);
 
 cudaError_t absorption(int n, const double* lam, const double* X1c, long long ldx1,
                        const double* X2c, long long ldx2, const double* dr, const double* dl,

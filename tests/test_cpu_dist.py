@@ -48,3 +48,57 @@ def test_reference_arm_nonzero_rank_exits_quietly(monkeypatch, capsys):
         n, steps, warmup = 64, 1, 0
     assert bench.run_reference(A()) == 0
     assert capsys.readouterr().out == ""
+
+
+# ---------------------------------------------------------------------------
+# Column-sharded solve: host-side logic (partition, host-staged broadcast)
+
+def test_shard_range_matches_c_abi_and_partitions():
+    import ctypes as C
+
+    from paper_1501_03830_b200 import _lib
+    from paper_1501_03830_b200.distributed import shard_range
+    lib = _lib.load()
+    for n in (0, 1, 2, 3, 7, 64, 301, 16384):
+        for world in (1, 2, 3, 4, 8):
+            cover = []
+            for r in range(world):
+                c0, c1 = C.c_int64(), C.c_int64()
+                assert lib.bse_shard_range(n, world, r, C.byref(c0), C.byref(c1)) == 0
+                assert (c0.value, c1.value) == shard_range(n, world, r)
+                cover += list(range(c0.value, c1.value))
+            assert cover == list(range(n))
+    c0, c1 = C.c_int64(), C.c_int64()
+    assert lib.bse_shard_range(10, 2, 2, C.byref(c0), C.byref(c1)) == _lib.BSE_BAD_ARGUMENT
+
+
+def _shard_worker(rank, world, port, out):
+    import numpy as np
+
+    from oracle import bse_oracle as orc
+    from paper_1501_03830_b200 import configs
+    from paper_1501_03830_b200.distributed import allgather_cols_host, make_host_bcast, shard_range
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    a, b, _ = configs.config_operator(0, n=37)
+    lam, x1, x2 = orc.solve_complex(a, b)
+    n = lam.size
+    # each rank keeps only its own column block, then the blocks are
+    # broadcast from their owners exactly as the device transport does
+    c0, c1 = shard_range(n, world, rank)
+    mine = np.zeros((2 * n, n))
+    mine[:, c0:c1] = np.vstack([x1.real, x2.real])[:, c0:c1]
+    full = allgather_cols_host(mine, world, rank, make_host_bcast())
+    out[rank] = float(np.max(np.abs(full - np.vstack([x1.real, x2.real]))))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_sharded_columns_allgather_gloo_world2():
+    port = _free_port()
+    ctx = mp.get_context("spawn")
+    with ctx.Manager() as mgr:
+        out = mgr.dict()
+        mp.start_processes(_shard_worker, args=(2, port, out), nprocs=2, join=True,
+                           start_method="spawn")
+        assert dict(out) == {0: 0.0, 1: 0.0}

@@ -1,0 +1,102 @@
+"""Emulated FP64 GEMM on the INT8 tensor cores (csrc/ozgemm.cu: Ozaki scheme
+II, tcgen05 kind::i8) against float64 references: every transpose, operand
+and output masks (view-relative, like the DMMA engine), alpha/beta, column
+chunking, ragged sizes, zero rows and rows spanning many binades."""
+import numpy as np
+import pytest
+
+from paper_1501_03830_b200 import _lib
+from paper_1501_03830_b200.device import (check, from_device_colmajor, mask_array, ptr,
+                                          stream_ptr, to_device_colmajor)
+
+from test_gpu_dense import _band
+
+pytestmark = pytest.mark.gpu
+
+
+def _oz(dev, ta, tb, a, b, c, alpha, beta, masks=None, chunk=0):
+    lib = _lib.load()
+    M, N = c.shape
+    K = a.shape[0] if ta else a.shape[1]
+    da, lda = to_device_colmajor(a, dev)
+    db, ldb = to_device_colmajor(b, dev)
+    dc, ldc = to_device_colmajor(c, dev)
+    check(lib.bse_ozgemm_dev(ta, tb, M, N, K, alpha, ptr(da), lda, ptr(db), ldb, beta, ptr(dc),
+                             ldc, masks, chunk, stream_ptr()), "ozgemm")
+    return from_device_colmajor(dc, M, N)
+
+
+def _bound(a_op, b_op):
+    # per-entry truncation bound: 2^-52 (row max of A) sum|B| + sum|A| (col max of B)
+    ra = np.max(np.abs(a_op), axis=1, keepdims=True)
+    cb = np.max(np.abs(b_op), axis=0, keepdims=True)
+    return 2.0 ** -51 * (ra * np.sum(np.abs(b_op), axis=0, keepdims=True)
+                         + np.sum(np.abs(a_op), axis=1, keepdims=True) * cb)
+
+
+@pytest.mark.parametrize("M,N,K", [(1, 1, 1), (7, 5, 3), (130, 257, 77), (300, 129, 1000),
+                                   (513, 511, 256), (1024, 1024, 4096)])
+@pytest.mark.parametrize("ta,tb", [(0, 0), (0, 1), (1, 0), (1, 1)])
+def test_ozgemm_plain(dev, M, N, K, ta, tb):
+    rng = np.random.default_rng(M * 7 + N * 3 + K + ta * 11 + tb * 13)
+    a = rng.standard_normal((K, M) if ta else (M, K))
+    b = rng.standard_normal((N, K) if tb else (K, N))
+    c = rng.standard_normal((M, N))
+    got = _oz(dev, ta, tb, a, b, c, 1.5, -0.5)
+    ao, bo = (a.T if ta else a), (b.T if tb else b)
+    ref = 1.5 * (ao @ bo) - 0.5 * c
+    tol = 1.5 * _bound(ao, bo) + 1e-15 * (np.abs(ref) + 1) * np.sqrt(K)
+    assert np.all(np.abs(got - ref) <= tol)
+    # at least as accurate as the DMMA engine's test gate
+    assert np.max(np.abs(got - ref)) <= 1e-13 * max(1.0, np.max(np.abs(ref))) * np.sqrt(K)
+
+
+@pytest.mark.parametrize("ta,tb", [(0, 0), (0, 1), (1, 0), (1, 1)])
+@pytest.mark.parametrize("case", ["lowerA", "unitA", "strictB", "upperA_lowerC", "lowerB_upperC"])
+def test_ozgemm_masks(dev, ta, tb, case):
+    M, N, K = 200, 190, 200
+    rng = np.random.default_rng(5)
+    a = rng.standard_normal((K, M) if ta else (M, K))
+    b = rng.standard_normal((N, K) if tb else (K, N))
+    c = rng.standard_normal((M, N))
+    ma = mb = mc = None
+    if case == "lowerA":
+        ma = (None, 0, 0)
+    elif case == "unitA":
+        ma = (None, -1, 1)
+    elif case == "strictB":
+        mb = (None, -1, 0)
+    elif case == "upperA_lowerC":
+        ma, mc = (0, None, 0), (None, 0, 0)
+    else:
+        mb, mc = (None, 0, 0), (0, None, 0)
+    am = _band(a, *ma) if ma else a
+    bm = _band(b, *mb) if mb else b
+    ref = 0.75 * ((am.T if ta else am) @ (bm.T if tb else bm)) + 2.0 * c
+    if mc:
+        ref = np.where(_band(np.ones_like(c), *mc) != 0, ref, c)
+    for chunk in (0, 64):  # chunked output columns shift the B / C masks
+        got = _oz(dev, ta, tb, a, b, c, 0.75, 2.0, mask_array(ma, mb, mc), chunk)
+        assert np.max(np.abs(got - ref)) <= 1e-12 * max(1.0, np.max(np.abs(ref))), chunk
+
+
+def test_ozgemm_wide_dynamic_range_and_zero_rows(dev):
+    rng = np.random.default_rng(11)
+    M, N, K = 257, 300, 700
+    a = rng.standard_normal((M, K)) * np.exp2(rng.integers(-300, 300, size=(M, 1)))
+    a[::17] = 0.0
+    a[5, :] *= np.exp2(rng.integers(-40, 0, size=K))  # one row spans 40 binades
+    b = rng.standard_normal((K, N)) * np.exp2(rng.integers(-60, 60, size=(1, N)))
+    got = _oz(dev, 0, 0, a, b, np.zeros((M, N)), 1.0, 0.0)
+    ref = a @ b
+    assert np.all(np.abs(got - ref) <= 1.5 * _bound(a, b) + 1e-300)
+    assert np.all(got[::17] == 0.0)
+
+
+def test_ozgemm_orthogonal_product_keeps_orthogonality(dev):
+    # the solve uses it on orthogonal factors: Q^T Q must stay I to O(eps)
+    rng = np.random.default_rng(3)
+    n = 1536
+    q, _ = np.linalg.qr(rng.standard_normal((n, n)))
+    got = _oz(dev, 1, 0, q, q, np.zeros((n, n)), 1.0, 0.0, chunk=512)
+    assert np.max(np.abs(got - np.eye(n))) <= 5e-15 * np.sqrt(n)
