@@ -6,7 +6,7 @@ types, the structural transforms and the solvers, with the numerical core in
 the CUDA library libbse_b200.so (C ABI: include/bse_b200.h).
 """
 from .solvers import (hermitian_eigvals, polish, real_embedding, solve_complex, solve_pair_device,
-                      solve_real, syevd_values_device, tda_gap_report)
+                      solve_real, syevd_values_device, tda_gap_report, validate)
 from .spectra import absorption_device, absorption_spectrum
 from .verify import PairResidualReport, pair_residual_report, pair_residuals_device
 from .types import (BseOperator, ConvergenceError, DipoleData, FullEigensystem,
@@ -25,5 +25,5 @@ __all__ = [
     "conditioning_warnings", "real_embedding", "polish", "solve_pair_device",
     "absorption_device", "hermitian_eigvals", "tda_gap_report", "TdaGapReport",
     "syevd_values_device", "PairResidualReport", "pair_residual_report",
-    "pair_residuals_device", "__version__",
+    "pair_residuals_device", "validate", "__version__",
 ]

@@ -315,19 +315,21 @@ cudaError_t ozgemm(bool transA, bool transB, const GemmProblem& p, void* work, s
   const int nc_max = std::min(p.N, chunk);
   const long long Np = r16(nc_max);
   if (work_bytes < ozgemm_bytes(M, p.N, K, chunk)) return cudaErrorInvalidValue;
+  // op(A)'s residues and row exponents first: their offsets depend on M and K
+  // only, so a reuse_a call with a narrower last column chunk finds them
   char* w = static_cast<char*>(work);
   int8_t* a8 = reinterpret_cast<int8_t*>(w);
   w += (size_t)kMods * Mp * Kp;
+  unsigned long long* mxa = reinterpret_cast<unsigned long long*>(w);
+  w += 8 * (size_t)Mp;
+  int* sa = reinterpret_cast<int*>(w);
+  w += 8 * (size_t)Mp;
   int8_t* b8 = reinterpret_cast<int8_t*>(w);
   w += (size_t)kMods * Np * Kp;
   int32_t* c32 = reinterpret_cast<int32_t*>(w);
   w += (size_t)kMods * Mp * Np * 4;
-  unsigned long long* mxa = reinterpret_cast<unsigned long long*>(w);
-  w += 8 * (size_t)Mp;
   unsigned long long* mxb = reinterpret_cast<unsigned long long*>(w);
   w += 8 * (size_t)Np;
-  int* sa = reinterpret_cast<int*>(w);
-  w += 4 * (size_t)Mp;
   int* sb = reinterpret_cast<int*>(w);
   // fixed-point width: 2 beta + log2 K + 2 < log2 P (125.4)
   int lk = 0;

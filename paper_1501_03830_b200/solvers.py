@@ -316,3 +316,55 @@ def solve_complex(op: BseOperator, workers: int = 1) -> PositiveEigensystem:
     lam, X1c, X2c = _select_and_polish(lam2, X1, X2, ld, n, dev)
     return PositiveEigensystem(lambda_plus=lam, x1=X1c.cpu().numpy(), x2=X2c.cpu().numpy(),
                                warnings=conditioning_warnings(lam))
+
+
+def _potrf_margin(m: np.ndarray, dev):
+    """GPU Cholesky probe of one symmetric block: (ok, margin, pivot_index)
+    with margin = min(diag L)^2 or the failing pivot value."""
+    n = m.shape[0]
+    At, lda = to_device_colmajor(m, dev)
+    info = _lib.BseInfo()
+    st = _lib.load().bse_potrf_dev(n, ptr(At), lda, stream_ptr(dev), C.byref(info))
+    if st == _lib.BSE_NOT_POSITIVE_DEFINITE:
+        return False, float(info.pivot_value), int(info.pivot_index)
+    if st != _lib.BSE_OK:
+        raise RuntimeError(f"bse_potrf_dev failed ({st}): {_lib.last_error()}")
+    d = view_colmajor(At, n, n).diagonal()
+    return True, float(d.min().item()) ** 2, -1
+
+
+def validate(op: BseOperator, tol: float | None = None):
+    """Structural pre-check (reference: core.validate, core.py:203-232):
+    (A Hermitian, B symmetric) within ``tol`` (default SYM_RTOL) and positive
+    definiteness of the real embedding build_m, probed by the GPU Cholesky.
+    ``margin`` is min(diag L)^2 on success, else the failing pivot value.
+    For a real operator build_m = diag(A+B, A-B) exactly, so the two blocks
+    are factored separately (A+B first, as the reference's column order)."""
+    from .types import SYM_RTOL, ValidationReport, _frob, build_m
+    rtol = SYM_RTOL if tol is None else float(tol)
+
+    def defect(x, conj):
+        nrm = _frob(x)
+        return 0.0 if nrm == 0.0 else _frob(x - (x.conj().T if conj else x.T)) / nrm
+
+    defects = (defect(op.a, True), defect(op.b, False))
+    sym_ok = (_frob(op.a - op.a.conj().T) <= rtol * max(1.0, _frob(op.a))
+              and _frob(op.b - op.b.T) <= rtol * max(1.0, _frob(op.b)))
+    m = build_m(op)
+    N = m.shape[0]
+    if N == 0:
+        return ValidationReport(symmetry_ok=bool(sym_ok), definiteness_ok=True,
+                                sym_defects=defects, margin=0.0)
+    dev = _device()
+    n = op.n
+    blocks = [m[:n, :n], m[n:, n:]] if op.kind == "real" else [m]
+    margin = np.inf
+    pd_ok = True
+    for blk in blocks:
+        ok, mg, _ = _potrf_margin(np.ascontiguousarray(blk), dev)
+        if not ok:
+            pd_ok, margin = False, mg
+            break
+        margin = min(margin, mg)
+    return ValidationReport(symmetry_ok=bool(sym_ok), definiteness_ok=pd_ok,
+                            sym_defects=defects, margin=float(margin))
