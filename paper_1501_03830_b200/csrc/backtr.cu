@@ -12,6 +12,7 @@
 #include <cstdlib>
 #include <vector>
 #include "eig.cuh"
+#include "ozgemm.cuh"
 
 namespace bse {
 namespace {
@@ -356,23 +357,40 @@ cudaError_t q2_apply(int n, int b, int g, const double* Vblk, const double* VTbl
   return launch(q2_apply_pair_kernel<2, 2>, 2);
 }
 
+size_t q1_oz_bytes(int n, int b, int ncols) {
+  const int kb = kQ1GroupOz * b, c = std::min(ncols, kQ1OzChunk);
+  // Y = V^T Zs (kb x c chunks, K = m <= n); Zs -= V Y2 (n x c chunks, K = kb)
+  return std::max({ozgemm_bytes(kb, ncols, n, c), ozgemm_bytes(n, ncols, kb, c),
+                   ozgemm_bytes(kb, ncols, kb, c)});
+}
+
 cudaError_t q1_apply(int n, int b, const double* Vall, long long ldv, const double* Tall,
                      double* Z, long long ldz, int ncols, const Q1Scratch& w, cudaStream_t s) {
-  // Panels are merged in groups of kQ1Group (compact-WY of the product,
+  // Panels are merged in groups of w.group (compact-WY of the product,
   // T_g = [[T_A, -T_A (V_A^T V_B) T_B], [0, T_B]]) so the applying GEMMs run
-  // with K = kQ1Group*b instead of b.  Vall must be zero outside the
+  // with K = group*b instead of b.  Vall must be zero outside the
   // reflectors (syevd memsets it before SY2SB).
   int np = 0;
   while (n - np * b - b >= 2) ++np;
   cudaError_t e = cudaSuccess;
-  const int G = kQ1Group;
+  const int G = w.group;
+  // one product on the INT8 engine when it is large enough to pay for the
+  // slicing and reconstruction passes
+  auto mul = [&](bool ta, const GemmProblem& g) {
+    if (w.oz && (double)g.M * g.N * g.K >= kOzMinWork)
+      return ozgemm(ta, false, g, w.oz, w.oz_bytes, kQ1OzChunk, s);
+    return gemm(ta, false, g, s);
+  };
   for (int pend = np; pend > 0; pend -= G) {
     const int p0 = std::max(0, pend - G), k = pend - p0, kb = k * b;
     const int r0 = (p0 + 1) * b, m = n - r0;
     const double* V = Vall + r0 + (long long)(p0 * b) * ldv;  // m x kb
     double* Tg = w.tg;                                        // kb x kb (ld kb)
     stage_mark("q1_tg", s);
-    // block-diagonal T_p, then the off-diagonal blocks column by column
+    // T_g by pairwise merging, bottom-up: blocks A = [a0, a0+h), B = [a0+h,
+    // a0+h+hb) of an already merged level combine as T_AB = -T_A X_AB T_B with
+    // X = V^T V (strict block-upper part, one product per group), so the
+    // work sits in a few large products instead of k thin ones.
     if ((e = cudaMemsetAsync(Tg, 0, sizeof(double) * kb * kb, s)) != cudaSuccess) return e;
     for (int j = 0; j < k; ++j) {
       if ((e = cudaMemcpy2DAsync(Tg + (long long)j * b + (long long)j * b * kb, kb * sizeof(double),
@@ -380,32 +398,38 @@ cudaError_t q1_apply(int n, int b, const double* Vall, long long ldv, const doub
                                  b * sizeof(double), b, cudaMemcpyDeviceToDevice, s)) != cudaSuccess)
         return e;
     }
-    for (int j = 1; j < k; ++j) {
-      const int jb = j * b;
-      // X = V[:, :jb]^T V[:, jb:jb+b]   (jb x b, K = m)
-      GemmProblem gx = make_gemm(jb, b, m, 1.0, V, ldv, V + (long long)jb * ldv, ldv, 0.0, w.x, jb);
-      if ((e = gemm_splitk(true, false, gx, 16, w.splitk_ws, w.probs, s)) != cudaSuccess) return e;
-      // tmp = T_g[:jb,:jb] X ; T_g[:jb, jb:jb+b] = -tmp T_j
-      GemmProblem g1 = make_gemm(jb, b, jb, 1.0, Tg, kb, w.x, jb, 0.0, w.tmp, jb);
-      g1.ma = Mask::upper();
-      if ((e = gemm(false, false, g1, s)) != cudaSuccess) return e;
-      GemmProblem g2 = make_gemm(jb, b, b, -1.0, w.tmp, jb, Tg + jb + (long long)jb * kb, kb, 0.0,
-                                 Tg + (long long)jb * kb, kb);
-      g2.mb = Mask::upper();
-      if ((e = gemm(false, false, g2, s)) != cudaSuccess) return e;
+    if (k > 1) {
+      GemmProblem gx = make_gemm(kb, kb, m, 1.0, V, ldv, V, ldv, 0.0, w.x, kb);
+      gx.mc = Mask::strict_upper();  // covers every block above the diagonal blocks
+      if ((e = mul(true, gx)) != cudaSuccess) return e;
+    }
+    for (int h = b; h < kb; h *= 2) {
+      for (int a0 = 0; a0 + h < kb; a0 += 2 * h) {
+        const int c0 = a0 + h, hb = std::min(h, kb - c0);
+        // tmp = T_A X_AB   (h x hb)
+        GemmProblem g1 = make_gemm(h, hb, h, 1.0, Tg + a0 + (long long)a0 * kb, kb,
+                                   w.x + a0 + (long long)c0 * kb, kb, 0.0, w.tmp, h);
+        g1.ma = Mask::upper();
+        if ((e = gemm(false, false, g1, s)) != cudaSuccess) return e;
+        // T_g[A, B] = -tmp T_B
+        GemmProblem g2 = make_gemm(h, hb, hb, -1.0, w.tmp, h, Tg + c0 + (long long)c0 * kb, kb,
+                                   0.0, Tg + a0 + (long long)c0 * kb, kb);
+        g2.mb = Mask::upper();
+        if ((e = gemm(false, false, g2, s)) != cudaSuccess) return e;
+      }
     }
     double* Zs = Z + r0;
     stage_mark("q1_gemm", s);
     // Y = V^T Zs (kb x ncols)
     GemmProblem g3 = make_gemm(kb, ncols, m, 1.0, V, ldv, Zs, ldz, 0.0, w.y, kb);
-    if ((e = gemm(true, false, g3, s)) != cudaSuccess) return e;
+    if ((e = mul(true, g3)) != cudaSuccess) return e;
     // Y2 = T_g Y
     GemmProblem g4 = make_gemm(kb, ncols, kb, 1.0, Tg, kb, w.y, kb, 0.0, w.y2, kb);
     g4.ma = Mask::upper();
-    if ((e = gemm(false, false, g4, s)) != cudaSuccess) return e;
+    if ((e = mul(false, g4)) != cudaSuccess) return e;
     // Zs -= V Y2
     GemmProblem g5 = make_gemm(m, ncols, kb, -1.0, V, ldv, w.y2, kb, 1.0, Zs, ldz);
-    if ((e = gemm(false, false, g5, s)) != cudaSuccess) return e;
+    if ((e = mul(false, g5)) != cudaSuccess) return e;
   }
   return e;
 }

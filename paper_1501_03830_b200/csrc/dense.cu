@@ -3,6 +3,7 @@
 // large GEMM (the blocked right-looking counterpart of the reference's
 // left-looking GEMV loop, kernels.py:43-65).
 #include "dense.cuh"
+#include "ozgemm.cuh"
 
 namespace bse {
 namespace {
@@ -289,8 +290,15 @@ cudaError_t trsm_rlt(const double* L, long long ldl, int n, double* A, long long
                   inv ? inv + (size_t)(n1 / kLeaf) * kLeaf * kLeaf : nullptr);
 }
 
+size_t trsm_llt_oz_bytes(int n, int ncols, int chunk) {
+  if (n <= kLeaf) return 0;
+  const int n1 = split_point(n), n2 = n - n1;
+  // the top-level update is the largest; deeper ones fit in its workspace
+  return ozgemm_bytes(n1, ncols, n2, std::min(ncols, chunk));
+}
+
 cudaError_t trsm_llt(const double* L, long long ldl, int n, double* B, long long ldb, int ncols,
-                     cudaStream_t s, const double* inv) {
+                     cudaStream_t s, const double* inv, const OzWork* oz) {
   if (n <= 0 || ncols <= 0) return cudaSuccess;
   if (n <= kLeaf) {
     const double* Y = inv;
@@ -306,13 +314,16 @@ cudaError_t trsm_llt(const double* L, long long ldl, int n, double* B, long long
   }
   const int n1 = split_point(n), n2 = n - n1;
   cudaError_t e = trsm_llt(L + n1 + n1 * ldl, ldl, n2, B + n1, ldb, ncols, s,
-                           inv ? inv + (size_t)(n1 / kLeaf) * kLeaf * kLeaf : nullptr);
+                           inv ? inv + (size_t)(n1 / kLeaf) * kLeaf * kLeaf : nullptr, oz);
   if (e != cudaSuccess) return e;
   // B1 -= L21^T X2
   GemmProblem p = make_gemm(n1, ncols, n2, -1.0, L + n1, ldl, B + n1, ldb, 1.0, B, ldb);
-  e = gemm(true, false, p, s);
+  if (oz && oz->p && (double)n1 * ncols * n2 >= kOzMinWork)
+    e = ozgemm(true, false, p, oz->p, oz->bytes, oz->chunk, s);
+  else
+    e = gemm(true, false, p, s);
   if (e != cudaSuccess) return e;
-  return trsm_llt(L, ldl, n1, B, ldb, ncols, s, inv);
+  return trsm_llt(L, ldl, n1, B, ldb, ncols, s, inv, oz);
 }
 
 cudaError_t trsm_lln(const double* L, long long ldl, int n, double* B, long long ldb, int ncols,

@@ -29,9 +29,18 @@ cudaError_t potrf_lower(double* A, long long lda, int n, DevStatus* st, cudaStre
 cudaError_t trsm_rlt(const double* L, long long ldl, int n, double* A, long long lda, int m,
                      cudaStream_t s, const double* inv = nullptr);
 
+// Workspace for the emulated-FP64 (INT8 tensor core) engine: large
+// off-diagonal updates of the recursive TRSM run there when it is given.
+struct OzWork {
+  void* p = nullptr;
+  size_t bytes = 0;
+  int chunk = 2048;
+};
+size_t trsm_llt_oz_bytes(int n, int ncols, int chunk);
+
 // B (n x ncols) <- L^{-T} * B (left, lower, transposed: solves L^T X = B).
 cudaError_t trsm_llt(const double* L, long long ldl, int n, double* B, long long ldb, int ncols,
-                     cudaStream_t s, const double* inv = nullptr);
+                     cudaStream_t s, const double* inv = nullptr, const OzWork* oz = nullptr);
 
 // B (n x ncols) <- L^{-1} * B (left, lower, no transpose).
 cudaError_t trsm_lln(const double* L, long long ldl, int n, double* B, long long ldb, int ncols,

@@ -45,17 +45,26 @@ cudaError_t q2_build(int n, int b, int g, const double* V2, const double* tau2, 
 cudaError_t q2_apply(int n, int b, int g, const double* Vblk, const double* VTblk, double* Z,
                      long long ldz, int ncols, cudaStream_t s);
 
-// Q1 back-transform: Z <- Q1 Z using the SY2SB panels (merged kQ1Group at a time).
+// Q1 back-transform: Z <- Q1 Z using the SY2SB panels, merged `group` at a
+// time into one compact-WY block (kQ1Group on the DMMA engine; kQ1GroupOz
+// when the large products run on the emulated-FP64 INT8 engine, whose
+// efficiency needs K = group * b in the thousands).
 constexpr int kQ1Group = 8;
+constexpr int kQ1GroupOz = 32;
+constexpr int kQ1OzChunk = 2048;
 struct Q1Scratch {
+  int group = kQ1Group;
   double* tg = nullptr;    // (G b)^2
-  double* x = nullptr;     // (G b) x b
-  double* tmp = nullptr;   // (G b) x b
+  double* x = nullptr;     // (G b) x (G b): V^T V of the group
+  double* tmp = nullptr;   // (G b)^2 / 2
   double* y = nullptr;     // (G b) x ncols
   double* y2 = nullptr;    // (G b) x ncols
   double* splitk_ws = nullptr;  // 16 * (G b) * b
   GemmProblem* probs = nullptr; // 64
+  void* oz = nullptr;      // emulated-FP64 workspace (null: DMMA only)
+  size_t oz_bytes = 0;
 };
+size_t q1_oz_bytes(int n, int b, int ncols);
 cudaError_t q1_apply(int n, int b, const double* Vall, long long ldv, const double* Tall,
                      double* Z, long long ldz, int ncols, const Q1Scratch& w, cudaStream_t s);
 
@@ -86,6 +95,8 @@ struct StedcWork {
   double* rots = nullptr;
   int* counts = nullptr;  // per node: K, ndefl, nrot (3 * n)
   GemmProblem* probs = nullptr;  // 2 * n
+  void* oz = nullptr;            // emulated-FP64 workspace for the top merges (optional)
+  size_t oz_bytes = 0;
   double* scal = nullptr;  // scaling scalar(s)
 };
 size_t stedc_bytes(int n);

@@ -224,7 +224,8 @@ __global__ void __launch_bounds__(256) crt_kernel(int M, int N, int Mp, const in
                                                   long long batch, const int* __restrict__ sa,
                                                   const int* __restrict__ sb, double alpha,
                                                   double beta, double* __restrict__ C,
-                                                  long long ldc, int col0, Mask mc) {
+                                                  long long ldc, int col0, Mask mc,
+                                                  const int* __restrict__ ccol) {
   const long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x;
   if (idx >= (long long)M * N) return;
   const int i = (int)(idx % M), j = (int)(idx / M);
@@ -258,7 +259,7 @@ __global__ void __launch_bounds__(256) crt_kernel(int M, int N, int Mp, const in
   }
   const double cp = hi + lo;
   double v = alpha * ldexp(cp, -(sa[i] + sb[j]));
-  double* cd = C + i + (long long)(col0 + j) * ldc;
+  double* cd = C + i + (long long)(ccol ? ccol[col0 + j] : col0 + j) * ldc;
   if (beta != 0.0) v += beta * *cd;
   *cd = v;
 }
@@ -378,7 +379,8 @@ cudaError_t ozgemm(bool transA, bool transB, const GemmProblem& p, void* work, s
       return e;
     const long long tot = (long long)M * nc;
     crt_kernel<<<(unsigned)ceil_div(tot, 256), 256, 0, s>>>(M, nc, (int)Mp, c32, Mp * ncp, sa, sb,
-                                                           p.alpha, p.beta, p.C, p.ldc, j0, p.mc);
+                                                           p.alpha, p.beta, p.C, p.ldc, j0, p.mc,
+                                                           p.ccol);
     count_launch();
     if ((e = cudaGetLastError()) != cudaSuccess) return e;
   }

@@ -9,8 +9,8 @@ namespace bse {
 size_t ozgemm_bytes(int M, int N, int K, int chunk);
 
 // C := alpha op(A) op(B) + beta C with the operand masks of GemmProblem
-// (view-relative, as in gemm()) and the output mask.  Column map (ccol) is
-// not supported.  reuse_a: the workspace already holds the slices of this
+// (view-relative, as in gemm()), the output mask (relative to the unmapped
+// column) and the optional output column map p.ccol (device array).  reuse_a: the workspace already holds the slices of this
 // op(A) from the previous call (same A, M, K and workspace).
 cudaError_t ozgemm(bool transA, bool transB, const GemmProblem& p, void* work, size_t work_bytes,
                    int chunk, cudaStream_t s, bool reuse_a = false);

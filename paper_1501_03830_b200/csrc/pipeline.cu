@@ -56,7 +56,7 @@ struct SyevdWork {
   StedcWork dc;
 };
 
-SyevdWork carve_syevd(Arena& a, int n) {
+SyevdWork carve_syevd(Arena& a, int n, int flags) {
   SyevdWork w{};
   const int b = kBand;
   const long long ld = pad_ld(n);
@@ -86,25 +86,34 @@ SyevdWork carve_syevd(Arena& a, int n) {
   const size_t qb = q2_block_doubles(n, b, kQ2Group);
   w.Vblk = a.take<double>(qb);
   w.VTblk = a.take<double>(qb);
-  const size_t gb = (size_t)kQ1Group * b;
+  const bool oz = !(flags & kFlagNativeFp64) && !(flags & 0x1) && n >= kOzMinN;
+  w.q1.group = oz ? kQ1GroupOz : kQ1Group;
+  const size_t gb = (size_t)w.q1.group * b;
   w.q1.tg = a.take<double>(gb * gb);
-  w.q1.x = a.take<double>(gb * b);
-  w.q1.tmp = a.take<double>(gb * b);
+  w.q1.x = a.take<double>(gb * gb);
+  w.q1.tmp = a.take<double>(gb * gb / 2 + gb * b);
   w.q1.y = a.take<double>(gb * n);
   w.q1.y2 = a.take<double>(gb * n);
   w.q1.splitk_ws = a.take<double>(16 * gb * b);
   w.q1.probs = a.take<GemmProblem>(64);
   w.dc = stedc_carve(a, n);
+  if (oz) {
+    // shared by the top D&C merges and Q1 (never live at the same time)
+    const int h = (n + 1) / 2;
+    w.q1.oz_bytes = std::max(q1_oz_bytes(n, b, n), ozgemm_bytes(h, n, h, 2048));
+    w.q1.oz = a.take<char>(w.q1.oz_bytes);
+    w.dc.oz = w.q1.oz;
+    w.dc.oz_bytes = w.q1.oz_bytes;
+  }
   return w;
 }
 
 }  // namespace
 
 size_t syevd_bytes(int n, int flags) {
-  (void)flags;
   Arena a;
   a.dry = true;
-  carve_syevd(a, n);
+  carve_syevd(a, n, flags);
   return a.used + 4096;
 }
 
@@ -112,7 +121,7 @@ cudaError_t syevd(int n, double* A, long long lda, double* w, double* Z, long lo
                   void* work, size_t work_bytes, int flags, cudaStream_t s, int zc0, int zc1) {
   if (n <= 0) return cudaSuccess;
   Arena a{static_cast<char*>(work), work_bytes, 0, false};
-  SyevdWork ws = carve_syevd(a, n);
+  SyevdWork ws = carve_syevd(a, n, flags);
   if (!ws.dc.scal) return cudaErrorMemoryAllocation;
   const int b = kBand;
   const int sms = device_sm_count();
@@ -154,6 +163,7 @@ struct SolveWork {
   DevStatus* st;
   void* eig; size_t eig_bytes;
   void* oz; size_t oz_bytes;  // emulated-FP64 workspace (aliases eig when it fits)
+  OzWork oz_trsm;             // separate: the TRMM's L slices stay live across blocks
 };
 
 bool use_oz(int n, int flags) { return !(flags & kFlagNativeFp64) && n >= kOzMinN; }
@@ -172,6 +182,11 @@ SolveWork carve_solve(Arena& a, int n, int flags) {
   w.eig = a.take<char>(w.eig_bytes);
   w.oz_bytes = use_oz(n, flags) ? ozgemm_bytes(n, n, n, kRecoverBlock) : 0;
   w.oz = w.oz_bytes <= w.eig_bytes ? w.eig : a.take<char>(w.oz_bytes);
+  if (use_oz(n, flags)) {
+    w.oz_trsm.chunk = kRecoverBlock;
+    w.oz_trsm.bytes = trsm_llt_oz_bytes(n, n, kRecoverBlock);
+    w.oz_trsm.p = a.take<char>(w.oz_trsm.bytes);
+  }
   return w;
 }
 
@@ -215,6 +230,8 @@ __global__ void recover_kernel(int n, int ncols, const double* U, const double* 
   X1[r + (long long)c * ldx1] = (u + v) * sc;
   X2[r + (long long)c * ldx2] = (u - v) * sc;
 }
+
+unsigned nb_all(int n) { return (unsigned)ceil_div((long long)n * n, 256); }
 
 }  // namespace
 
@@ -262,22 +279,45 @@ cudaError_t solve_spd_pair(int n, const double* M, long long ldm, const double* 
   const int nc = (int)(c1 - c0);
   const int sh = (int)c0;
   // 2. W = L^T M L  (T1 = M L from the lower triangle of M, then W = L^T T1, lower)
-  GemmProblem g1 = make_gemm(n, nc, n, 1.0, M, ldm, w.L + c0 * ld, ld, 0.0, w.T1 + c0 * ld, ld);
-  g1.ma = Mask::lower();
-  g1.mb = Mask{kNoMaskLo, -sh, 0};
-  if (nc > 0 && (e = gemm(false, false, g1, s)) != cudaSuccess) return e;
-  // only T1's lower triangle feeds W = L^T T1 (lower): the strictly-upper
-  // half of M's contribution is needed for rows k >= j only (N^3/3 flops
-  // saved); g1 has already zeroed T1's upper triangle (k-range empty there)
-  GemmProblem g2 = make_gemm(n, nc, n, 1.0, M, ldm, w.L + c0 * ld, ld, 1.0, w.T1 + c0 * ld, ld);
-  g2.ma = Mask::strict_lower();
-  g2.mb = Mask{kNoMaskLo, -sh, 0};
-  g2.mc = Mask{kNoMaskLo, -sh, 0};
-  if (nc > 0 && (e = gemm(true, false, g2, s)) != cudaSuccess) return e;
-  GemmProblem g3 = make_gemm(n, nc, n, 1.0, w.L, ld, w.T1 + c0 * ld, ld, 0.0, w.W + c0 * ld, ld);
-  g3.ma = Mask::lower();
-  g3.mc = Mask{kNoMaskLo, -sh, 0};
-  if (nc > 0 && (e = gemm(true, false, g3, s)) != cudaSuccess) return e;
+  if (w.oz_bytes) {
+    // Emulated-FP64 engine: column blocks [j0, j1) of W need only rows >= j0
+    // of T1 and of L^T, so each block is two dense products on the trailing
+    // square: T1_j = Msym[j0:, j0:] L[j0:, j0:j1], W[j0:, j0:j1] =
+    // L[j0:, j0:]^T T1_j (lower part).  Msym (full symmetric M) lives in Zr
+    // until the recovery needs it.
+    const int nb = kRecoverBlock;
+    copy_lower_kernel<<<nb_all(n), 256, 0, s>>>(n, M, ldm, w.Zr, ld);
+    count_launch();
+    if ((e = symmetrize_from_lower(w.Zr, ld, n, s)) != cudaSuccess) return e;
+    for (int j0 = (int)c0; j0 < (int)c1; j0 += nb) {
+      const int wj = std::min(nb, (int)c1 - j0), mt = n - j0;
+      const long long o = j0 + (long long)j0 * ld;
+      GemmProblem t1 = make_gemm(mt, wj, mt, 1.0, w.Zr + o, ld, w.L + o, ld, 0.0, w.T1 + o, ld);
+      t1.mb = Mask::lower();
+      if ((e = ozgemm(false, false, t1, w.oz, w.oz_bytes, nb, s)) != cudaSuccess) return e;
+      GemmProblem t2 = make_gemm(mt, wj, mt, 1.0, w.L + o, ld, w.T1 + o, ld, 0.0, w.W + o, ld);
+      t2.ma = Mask::lower();
+      t2.mc = Mask::lower();
+      if ((e = ozgemm(true, false, t2, w.oz, w.oz_bytes, nb, s)) != cudaSuccess) return e;
+    }
+  } else {
+    GemmProblem g1 = make_gemm(n, nc, n, 1.0, M, ldm, w.L + c0 * ld, ld, 0.0, w.T1 + c0 * ld, ld);
+    g1.ma = Mask::lower();
+    g1.mb = Mask{kNoMaskLo, -sh, 0};
+    if (nc > 0 && (e = gemm(false, false, g1, s)) != cudaSuccess) return e;
+    // only T1's lower triangle feeds W = L^T T1 (lower): the strictly-upper
+    // half of M's contribution is needed for rows k >= j only (N^3/3 flops
+    // saved); g1 has already zeroed T1's upper triangle (k-range empty there)
+    GemmProblem g2 = make_gemm(n, nc, n, 1.0, M, ldm, w.L + c0 * ld, ld, 1.0, w.T1 + c0 * ld, ld);
+    g2.ma = Mask::strict_lower();
+    g2.mb = Mask{kNoMaskLo, -sh, 0};
+    g2.mc = Mask{kNoMaskLo, -sh, 0};
+    if (nc > 0 && (e = gemm(true, false, g2, s)) != cudaSuccess) return e;
+    GemmProblem g3 = make_gemm(n, nc, n, 1.0, w.L, ld, w.T1 + c0 * ld, ld, 0.0, w.W + c0 * ld, ld);
+    g3.ma = Mask::lower();
+    g3.mc = Mask{kNoMaskLo, -sh, 0};
+    if (nc > 0 && (e = gemm(true, false, g3, s)) != cudaSuccess) return e;
+  }
   if (world > 1) {
     stage_mark("allgather_w", s);
     if ((e = allgather_cols(*comm, w.W, ld, n, s)) != cudaSuccess) return e;
@@ -319,7 +359,8 @@ cudaError_t solve_spd_pair(int n, const double* M, long long ldm, const double* 
     }
     first_block = false;
     stage_mark("recover_trsm", s);
-    if ((e = trsm_llt(w.L, ld, n, w.W + (long long)c0 * ld, ld, nc, s, w.linv)) != cudaSuccess)
+    if ((e = trsm_llt(w.L, ld, n, w.W + (long long)c0 * ld, ld, nc, s, w.linv,
+                      w.oz_trsm.p ? &w.oz_trsm : nullptr)) != cudaSuccess)
       return e;
     const long long tb = (long long)n * nc;
     recover_kernel<<<(unsigned)ceil_div(tb, 256), 256, 0, s>>>(

@@ -13,6 +13,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include "eig.cuh"
+#include "ozgemm.cuh"
 
 namespace bse {
 namespace {
@@ -578,9 +579,27 @@ cudaError_t stedc(int n, double* d, double* e, double* wout, double* Q, long lon
         std::fprintf(stderr, "[dc] level size %d node %d: K=%d deflated=%d rotations=%d\n", size, q,
                      hc[3 * q], hc[3 * q + 1], hc[3 * q + 2]);
     }
-    err = gemm_grouped(false, false, ws.probs, 2 * L.nnodes, L.half, maxm, s, L.half >= 2,
-                       L.half >= 512 ? 3 : 1);
-    if (err != cudaSuccess) return err;
+    if (ws.oz && L.nnodes <= 2 && (double)L.half * L.half * maxm >= kOzMinWork) {
+      // top merges: the problem shapes come back to the host (one sync per
+      // level) and the large products run on the emulated-FP64 engine
+      GemmProblem hp[4];
+      if ((err = cudaMemcpyAsync(hp, ws.probs, sizeof(GemmProblem) * 2 * L.nnodes,
+                                 cudaMemcpyDeviceToHost, s)) != cudaSuccess)
+        return err;
+      if ((err = cudaStreamSynchronize(s)) != cudaSuccess) return err;
+      for (int q = 0; q < 2 * L.nnodes; ++q) {
+        const GemmProblem& p = hp[q];
+        if (p.M <= 0 || p.N <= 0) continue;
+        err = (double)p.M * p.N * p.K >= kOzMinWork
+                  ? ozgemm(false, false, p, ws.oz, ws.oz_bytes, 2048, s)
+                  : gemm(false, false, p, s);
+        if (err != cudaSuccess) return err;
+      }
+    } else {
+      err = gemm_grouped(false, false, ws.probs, 2 * L.nnodes, L.half, maxm, s, L.half >= 2,
+                         L.half >= 512 ? 3 : 1);
+      if (err != cudaSuccess) return err;
+    }
     dc_copy_deflated_kernel<<<g2, kDcThreads, 0, s>>>(L, n, ws, Qin, Qout, ld);
     count_launch();
     std::swap(Din, Dout);
