@@ -397,8 +397,15 @@ def run_ours(args):
     roof = None
     if dom:
         ach = STAGE_FLOPS[dom](n) / (tens[dom] * 1e-3) / 1e12
+        traffic = None
+        try:
+            tr = json.loads((ROOT / "profiles" / "ncu_traffic.json").read_text()).get(dom)
+            if tr and int(tr["n"]) == n:
+                traffic = {"bytes": tr["dram_bytes"], "unit": "B", "source": tr["source"]}
+        except (OSError, ValueError, KeyError):
+            traffic = None
         roof = {"bound": "tensor", "kernel": dom, "achieved": ach, "peak": fp64_peak,
-                "unit": "TFLOP/s", "frac": ach / fp64_peak, "traffic": None,
+                "unit": "TFLOP/s", "frac": ach / fp64_peak, "traffic": traffic,
                 "peak_source": "measured in-run FP64 DMMA probe (mma.sync m8n8k4 f64); "
                                "MEASURED_PEAKS.json has no FP64 entry",
                 "flops_per_launch": STAGE_FLOPS[dom](n)}

@@ -104,3 +104,35 @@ def test_tda_gap_1x1_analytic(dev):
     rep = bg.tda_gap_report(bg.make_operator([[2.0]], [[1j]]))
     assert rep.gaps[0] == pytest.approx(2.0 - np.sqrt(3.0), abs=1e-14)
     assert rep.certified
+
+
+def test_emulated_fp64_path_n4608(dev):
+    """n >= 4096 routes the congruence, the top D&C merges, Q1, the recovery
+    TRMM and the top TRSM updates through the emulated-FP64 INT8 engine:
+    the solve must meet the same gates as the all-DMMA path
+    (BSE_FLAG_NATIVE_FP64) and agree with it and with LAPACK."""
+    import torch
+    from paper_1501_03830_b200 import _lib
+    from paper_1501_03830_b200.device import from_device_colmajor, to_device_colmajor
+    n = 4608
+    a, b, _ = configs.config_operator(2, n=n)
+    op = bg.make_operator(a, b, kind="real")
+    pos = bg.solve_real(op)
+    lam_ref = lapack_lambda(a + b, a - b)
+    assert np.max(np.abs(pos.lambda_plus - lam_ref) / lam_ref) <= 1e-10
+    check_properties(op, pos, n)
+    Mt, ldm = to_device_colmajor(a + b, dev)
+    Kt, ldk = to_device_colmajor(a - b, dev)
+    lam_n, X1n, _, _ = bg.solve_pair_device(Mt, ldm, Kt, ldk, n, flags=_lib.FLAG_NATIVE_FP64)
+    lam_n = lam_n.cpu().numpy()
+    assert np.max(np.abs(lam_n - pos.lambda_plus) / lam_n) <= 1e-12
+    x1n = from_device_colmajor(X1n, n, n)
+    x1 = pos.x1.real
+    # columns equal up to sign, tolerance n eps |W| / gap(lambda^2) (SURVEY 8c(4))
+    l2 = lam_n ** 2
+    d = -np.diff(l2)
+    gap = np.minimum(np.r_[np.inf, d], np.r_[d, np.inf]) / l2[0]
+    sgn = np.sign(np.sum(x1 * x1n, axis=0))
+    err = np.linalg.norm(x1 * sgn - x1n, axis=0) / np.linalg.norm(x1n, axis=0)
+    assert np.all(err <= n * np.finfo(float).eps / gap + 1e-12)
+    torch.cuda.synchronize()
