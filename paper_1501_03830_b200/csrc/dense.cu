@@ -262,8 +262,16 @@ int split_point(int n) {
 
 size_t potrf_inv_cache_doubles(int n) { return (size_t)ceil_div(n, kLeaf) * kLeaf * kLeaf; }
 
+// C-block update on the emulated-FP64 engine when it is given and the
+// product is large enough, else on the DMMA engine
+static cudaError_t update(bool ta, bool tb, const GemmProblem& p, const OzWork* oz, cudaStream_t s) {
+  if (oz && oz->p && (double)p.M * p.N * p.K >= kOzMinWork)
+    return ozgemm(ta, tb, p, oz->p, oz->bytes, oz->chunk, s);
+  return gemm(ta, tb, p, s);
+}
+
 cudaError_t trsm_rlt(const double* L, long long ldl, int n, double* A, long long lda, int m,
-                     cudaStream_t s, const double* inv) {
+                     cudaStream_t s, const double* inv, const OzWork* oz) {
   if (n <= 0 || m <= 0) return cudaSuccess;
   if (n <= kLeaf) {
     // A <- A * (L^{-1})^T : (cached) inverse of the block, then one in-place
@@ -280,14 +288,14 @@ cudaError_t trsm_rlt(const double* L, long long ldl, int n, double* A, long long
     return gemm(false, true, p, s);
   }
   const int n1 = split_point(n), n2 = n - n1;
-  cudaError_t e = trsm_rlt(L, ldl, n1, A, lda, m, s, inv);
+  cudaError_t e = trsm_rlt(L, ldl, n1, A, lda, m, s, inv, oz);
   if (e != cudaSuccess) return e;
   // A2 -= X1 * L21^T
   GemmProblem p = make_gemm(m, n2, n1, -1.0, A, lda, L + n1, ldl, 1.0, A + n1 * lda, lda);
-  e = gemm(false, true, p, s);
+  e = update(false, true, p, oz, s);
   if (e != cudaSuccess) return e;
   return trsm_rlt(L + n1 + n1 * ldl, ldl, n2, A + n1 * lda, lda, m, s,
-                  inv ? inv + (size_t)(n1 / kLeaf) * kLeaf * kLeaf : nullptr);
+                  inv ? inv + (size_t)(n1 / kLeaf) * kLeaf * kLeaf : nullptr, oz);
 }
 
 size_t trsm_llt_oz_bytes(int n, int ncols, int chunk) {
@@ -318,10 +326,7 @@ cudaError_t trsm_llt(const double* L, long long ldl, int n, double* B, long long
   if (e != cudaSuccess) return e;
   // B1 -= L21^T X2
   GemmProblem p = make_gemm(n1, ncols, n2, -1.0, L + n1, ldl, B + n1, ldb, 1.0, B, ldb);
-  if (oz && oz->p && (double)n1 * ncols * n2 >= kOzMinWork)
-    e = ozgemm(true, false, p, oz->p, oz->bytes, oz->chunk, s);
-  else
-    e = gemm(true, false, p, s);
+  e = update(true, false, p, oz, s);
   if (e != cudaSuccess) return e;
   return trsm_llt(L, ldl, n1, B, ldb, ncols, s, inv, oz);
 }
@@ -348,7 +353,7 @@ cudaError_t trsm_lln(const double* L, long long ldl, int n, double* B, long long
 }
 
 static cudaError_t potrf_rec(double* A, long long lda, int n, int off, DevStatus* st,
-                             cudaStream_t s, double* inv) {
+                             cudaStream_t s, double* inv, const OzWork* oz) {
   if (n <= kLeaf) {
     ensure_smem<potf2_kernel>();
     potf2_kernel<<<1, 2 * kLeaf, kLeafSmem, s>>>(A, lda, n, off, st, inv);
@@ -356,24 +361,24 @@ static cudaError_t potrf_rec(double* A, long long lda, int n, int off, DevStatus
     return cudaGetLastError();
   }
   const int n1 = split_point(n), n2 = n - n1;
-  cudaError_t e = potrf_rec(A, lda, n1, off, st, s, inv);
+  cudaError_t e = potrf_rec(A, lda, n1, off, st, s, inv, oz);
   if (e != cudaSuccess) return e;
-  e = trsm_rlt(A, lda, n1, A + n1, lda, n2, s, inv);  // A21 <- A21 L11^{-T}
+  e = trsm_rlt(A, lda, n1, A + n1, lda, n2, s, inv, oz);  // A21 <- A21 L11^{-T}
   if (e != cudaSuccess) return e;
   // A22 -= A21 A21^T (lower triangle only)
   GemmProblem p = make_gemm(n2, n2, n1, -1.0, A + n1, lda, A + n1, lda, 1.0,
                             A + n1 + n1 * lda, lda);
   p.mc = Mask::lower();
-  e = gemm(false, true, p, s);
+  e = update(false, true, p, oz, s);
   if (e != cudaSuccess) return e;
   return potrf_rec(A + n1 + n1 * lda, lda, n2, off + n1, st, s,
-                   inv ? inv + (size_t)(n1 / kLeaf) * kLeaf * kLeaf : nullptr);
+                   inv ? inv + (size_t)(n1 / kLeaf) * kLeaf * kLeaf : nullptr, oz);
 }
 
 cudaError_t potrf_lower(double* A, long long lda, int n, DevStatus* st, cudaStream_t s,
-                        double* inv_cache) {
+                        double* inv_cache, const OzWork* oz) {
   if (n <= 0) return cudaSuccess;
-  cudaError_t e = potrf_rec(A, lda, n, 0, st, s, inv_cache);
+  cudaError_t e = potrf_rec(A, lda, n, 0, st, s, inv_cache, oz);
   if (e != cudaSuccess) return e;
   return zero_strict_upper(A, lda, n, s);
 }

@@ -21,22 +21,23 @@ struct DevStatus {
 // inv_cache (optional): ceil(n/64) blocks of 64 x 64 doubles receiving the
 // inverses of the 64-wide diagonal blocks of L, reused by trsm_* (pass the
 // same cache there) so each leaf inverse is computed once.
-size_t potrf_inv_cache_doubles(int n);
-cudaError_t potrf_lower(double* A, long long lda, int n, DevStatus* st, cudaStream_t s,
-                        double* inv_cache = nullptr);
-
-// A (m x n) <- A * L^{-T}, L n x n lower (right, lower, transposed).
-cudaError_t trsm_rlt(const double* L, long long ldl, int n, double* A, long long lda, int m,
-                     cudaStream_t s, const double* inv = nullptr);
-
-// Workspace for the emulated-FP64 (INT8 tensor core) engine: large
-// off-diagonal updates of the recursive TRSM run there when it is given.
+// Workspace for the emulated-FP64 (INT8 tensor core) engine: the large
+// off-diagonal updates of the recursive POTRF / TRSM run there when given.
 struct OzWork {
   void* p = nullptr;
   size_t bytes = 0;
   int chunk = 2048;
 };
 size_t trsm_llt_oz_bytes(int n, int ncols, int chunk);
+
+size_t potrf_inv_cache_doubles(int n);
+cudaError_t potrf_lower(double* A, long long lda, int n, DevStatus* st, cudaStream_t s,
+                        double* inv_cache = nullptr, const OzWork* oz = nullptr);
+
+// A (m x n) <- A * L^{-T}, L n x n lower (right, lower, transposed).
+cudaError_t trsm_rlt(const double* L, long long ldl, int n, double* A, long long lda, int m,
+                     cudaStream_t s, const double* inv = nullptr, const OzWork* oz = nullptr);
+
 
 // B (n x ncols) <- L^{-T} * B (left, lower, transposed: solves L^T X = B).
 cudaError_t trsm_llt(const double* L, long long ldl, int n, double* B, long long ldb, int ncols,

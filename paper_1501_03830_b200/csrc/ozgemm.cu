@@ -11,7 +11,7 @@
 // 2. residues A'_t, B'_t in [-128, 127] (int8, K-major), one batched
 //    tcgen05 kind::i8 GEMM (CUTLASS sm_100 2-SM kernel, INT32 accumulators in
 //    TMEM) gives C_t = A'_t B'_t exactly;
-// 3. C' is rebuilt per element by the CRT in double-double arithmetic,
+// 3. C' is rebuilt per element by the CRT (exact 32-bit-limb sums in FP64),
 //    scaled back by 2^-(s_i + s_j) and written with alpha/beta and the output
 //    mask.
 // The truncation error per entry is below 2^-52 of its row (column) maximum,
@@ -46,11 +46,11 @@ BSE_HD constexpr int kMod(int t) {
 }
 
 struct CrtConst {
-  double inv_m[kMods];   // 1 / m_t
-  double mhi[kMods];     // M_t = P / m_t as hi + lo
-  double mlo[kMods];
-  int y[kMods];          // M_t^{-1} mod m_t
-  double phi, plo;       // P = prod m_t
+  // Q_t = (M_t * (M_t^{-1} mod m_t)) mod P, M_t = P / m_t, as four 32-bit
+  // limbs (Q_t = sum_k q[t][k] 2^(32 k)); P likewise; 1 / P
+  double q[kMods][4];
+  double p[4];
+  double inv_p;
 };
 __constant__ CrtConst c_crt;
 
@@ -112,17 +112,36 @@ BSE_DEV int scale_exp(double mx, int beta) {
   return beta - e;
 }
 
-BSE_DEV uint32_t residues4(const double (&x)[4], int t, int m, double inv_m) {
-  uint32_t w = 0;
+// Residues of 4 integer-valued doubles (|x| < 2^53) for all 16 moduli,
+// packed 4 per word (byte q = element q).  The moduli are reduced in pairs:
+// r = x mod (m_a m_b) in FP64 (|r| < 1.5 m_a m_b < 2^17, exact), then both
+// residues of the small non-negative integer r + 2 m_a m_b on the integer
+// pipe (unsigned division by a constant).  Each residue v in [0, m) is
+// stored as the int8 centred representative (v >= 128 ? v - m : v).
+BSE_DEV uint32_t byte8(uint32_t u, uint32_t m) {
+  // u < 2^24: q = floor(u c / 2^32), c = ceil(2^32 / m), is exact because
+  // u (c m - 2^32) < 2^24 m < 2^32
+  const uint32_t c = (uint32_t)((0x100000000ull + m - 1) / m);
+  const uint32_t v = u - __umulhi(u, c) * m;
+  return (v + (v >= 128u ? 256u - m : 0u)) & 0xffu;
+}
+
+BSE_DEV void residues_all(const double (&x)[4], uint32_t (&w)[kMods]) {
 #pragma unroll
-  for (int q = 0; q < 4; ++q) {
-    double r = fma(-rint(x[q] * inv_m), (double)m, x[q]);  // exact: |r| < 1.5 m
-    if (r >= 0.5 * m) r -= m;
-    if (r < -0.5 * m) r += m;
-    w |= ((uint32_t)(int)r & 0xffu) << (8 * q);
+  for (int t = 0; t < kMods; ++t) w[t] = 0;
+#pragma unroll
+  for (int pr = 0; pr < kMods / 2; ++pr) {
+    constexpr double kMagic = 6755399441055744.0;  // 1.5 * 2^52
+    const uint32_t ma = kMod(2 * pr), mb = kMod(2 * pr + 1);
+    const double mp = (double)(ma * mb), inv = 1.0 / mp;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const double r = fma(-rint(x[q] * inv), mp, x[q]);
+      const uint32_t u = (uint32_t)__double2loint(r + kMagic) + 2u * ma * mb;
+      w[2 * pr] |= byte8(u, ma) << (8 * q);
+      w[2 * pr + 1] |= byte8(u, mb) << (8 * q);
+    }
   }
-  (void)t;
-  return w;
 }
 
 // One warp per line, contiguous source.
@@ -152,9 +171,10 @@ __global__ void __launch_bounds__(256) split_contig_kernel(int lines, int K, int
       const int k = k0 + q;
       x[q] = (live && k < K) ? trunc(ldexp(masked(row[k], k, r, mk), se)) : 0.0;
     }
+    uint32_t w[kMods];
+    residues_all(x, w);
 #pragma unroll
-    for (int t = 0; t < kMods; ++t)
-      o[t * (mod_stride / 4) + k0 / 4] = residues4(x, t, kMod(t), c_crt.inv_m[t]);
+    for (int t = 0; t < kMods; ++t) o[t * (mod_stride / 4) + k0 / 4] = w[t];
   }
 }
 
@@ -206,20 +226,21 @@ __global__ void __launch_bounds__(256) split_strided_kernel(int lines, int K, in
 #pragma unroll
     for (int q = 0; q < 4; ++q) x[q] = tile[kq + q][rl];
     uint32_t* o = reinterpret_cast<uint32_t*>(out + (long long)r * Kp + k);
+    uint32_t w[kMods];
+    residues_all(x, w);
 #pragma unroll
-    for (int t = 0; t < kMods; ++t) o[t * (mod_stride / 4)] = residues4(x, t, kMod(t), c_crt.inv_m[t]);
+    for (int t = 0; t < kMods; ++t) o[t * (mod_stride / 4)] = w[t];
   }
 }
 
 // ---------------------------------------------------------------------------
-// CRT reconstruction in double-double.
+// CRT reconstruction.
 
-BSE_DEV void two_sum(double a, double b, double& s, double& e) {
-  s = a + b;
-  const double bb = s - a;
-  e = (a - (s - bb)) + (b - bb);
-}
 
+// C' = sum_t v_t Q_t mod P with v_t = c_t mod m_t in [0, m_t): every
+// v_t q[t][k] < 2^40, so the four limb sums A_k (< 2^44) are exact in FP64;
+// the quotient q = rint(S / P) (|q| < 2^12) comes from the top limbs and
+// R_k = A_k - q p_k is exact, leaving one rounding per limb addition.
 __global__ void __launch_bounds__(256) crt_kernel(int M, int N, int Mp, const int32_t* __restrict__ c32,
                                                   long long batch, const int* __restrict__ sa,
                                                   const int* __restrict__ sb, double alpha,
@@ -232,32 +253,24 @@ __global__ void __launch_bounds__(256) crt_kernel(int M, int N, int Mp, const in
   const int d = (col0 + j) - i;
   if (d < mc.lo || d > mc.hi) return;
   const int32_t* p = c32 + i + (long long)j * Mp;
-  double hi = 0.0, lo = 0.0, frac = 0.0;
+  double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
 #pragma unroll
   for (int t = 0; t < kMods; ++t) {
-    const int m = kMod(t);
-    int r = p[t * batch] % m;
-    int u = (r * c_crt.y[t]) % m;
-    if (u < 0) u += m;
-    const double du = (double)u;
-    frac += du * c_crt.inv_m[t];
-    const double ph = du * c_crt.mhi[t];
-    const double pe = fma(du, c_crt.mhi[t], -ph);
-    double s, e;
-    two_sum(hi, ph, s, e);
-    hi = s;
-    lo += e + pe + du * c_crt.mlo[t];
+    const uint32_t m = kMod(t);
+    // c_t + 2^31 - (2^31 mod m) >= 0 has the residue of c_t (|c_t| < 2^31 - 256)
+    const uint32_t off = 0x80000000u - (0x80000000u % m);
+    const uint32_t v = ((uint32_t)p[t * batch] + off) % m;
+    const double dv = __hiloint2double(0x43300000, (int)v) - 4503599627370496.0;  // 2^52
+    a0 = fma(dv, c_crt.q[t][0], a0);
+    a1 = fma(dv, c_crt.q[t][1], a1);
+    a2 = fma(dv, c_crt.q[t][2], a2);
+    a3 = fma(dv, c_crt.q[t][3], a3);
   }
-  const double q = rint(frac);
-  {
-    const double ph = -q * c_crt.phi;
-    const double pe = fma(-q, c_crt.phi, -ph);
-    double s, e;
-    two_sum(hi, ph, s, e);
-    hi = s;
-    lo += e + pe - q * c_crt.plo;
-  }
-  const double cp = hi + lo;
+  constexpr double k32 = 4294967296.0, k64 = k32 * k32, k96 = k64 * k32;
+  const double q = rint(fma(a3, k96, fma(a2, k64, a1 * k32)) * c_crt.inv_p);
+  const double r0 = fma(-q, c_crt.p[0], a0), r1 = fma(-q, c_crt.p[1], a1);
+  const double r2 = fma(-q, c_crt.p[2], a2), r3 = fma(-q, c_crt.p[3], a3);
+  const double cp = ((r3 * k96 + r2 * k64) + r1 * k32) + r0;
   double v = alpha * ldexp(cp, -(sa[i] + sb[j]));
   double* cd = C + i + (long long)(ccol ? ccol[col0 + j] : col0 + j) * ldc;
   if (beta != 0.0) v += beta * *cd;
@@ -266,34 +279,32 @@ __global__ void __launch_bounds__(256) crt_kernel(int M, int N, int Mp, const in
 
 long long r16(long long x) { return (x + 15) / 16 * 16; }
 
-bool g_const_ready = false;
+bool g_const_ready[64] = {};
 
 cudaError_t init_const() {
-  if (g_const_ready) return cudaSuccess;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (dev >= 0 && dev < 64 && g_const_ready[dev]) return cudaSuccess;
   CrtConst h{};
-  // exact integer arithmetic (P < 2^126 fits in 128 bits); hi = rn(x),
-  // lo = rn(x - hi) with the difference formed exactly
+  // exact integer arithmetic: P < 2^126 fits in 128 bits
   using u128 = unsigned __int128;
-  using i128 = __int128;
-  auto to_dd = [](u128 x, double& hi, double& lo) {
-    hi = (double)x;
-    const i128 diff = (i128)x - (i128)(u128)hi;
-    lo = (double)diff;
+  auto limbs = [](u128 x, double (&out)[4]) {
+    for (int k = 0; k < 4; ++k) out[k] = (double)(uint32_t)(x >> (32 * k));
   };
   u128 P = 1;
   for (int t = 0; t < kMods; ++t) P *= (u128)kMod(t);
-  to_dd(P, h.phi, h.plo);
+  limbs(P, h.p);
+  h.inv_p = 1.0 / (double)P;
   for (int t = 0; t < kMods; ++t) {
-    const u128 Mt = P / (u128)kMod(t);
-    to_dd(Mt, h.mhi[t], h.mlo[t]);
-    const long long mt_mod = (long long)(Mt % (u128)kMod(t));
-    int y = 1;
+    const u128 m = (u128)kMod(t), Mt = P / m;
+    const unsigned long long mt_mod = (unsigned long long)(Mt % m);
+    unsigned long long y = 1;
     while ((mt_mod * y) % kMod(t) != 1) ++y;
-    h.y[t] = y;
-    h.inv_m[t] = 1.0 / kMod(t);
+    // Q_t = M_t y mod P = M_t (y mod m): y < m, so M_t y < P m fits in 128 bits
+    limbs((Mt * (u128)y) % P, h.q[t]);
   }
   cudaError_t e = cudaMemcpyToSymbol(c_crt, &h, sizeof(h));
-  if (e == cudaSuccess) g_const_ready = true;
+  if (e == cudaSuccess && dev >= 0 && dev < 64) g_const_ready[dev] = true;
   return e;
 }
 

@@ -266,7 +266,13 @@ cudaError_t solve_spd_pair(int n, const double* M, long long ldm, const double* 
   stage_mark("potrf", s);
   copy_lower_kernel<<<nb, 256, 0, s>>>(n, K, ldk, w.L, ld);
   count_launch();
-  if ((e = potrf_lower(w.L, ld, n, &w.st[0], s, w.linv)) != cudaSuccess) return e;
+  {
+    // the emulated engine's workspace aliases the (still idle) eigensolver's
+    OzWork ozp{w.oz, w.oz_bytes, kRecoverBlock};
+    if ((e = potrf_lower(w.L, ld, n, &w.st[0], s, w.linv, w.oz_bytes ? &ozp : nullptr)) !=
+        cudaSuccess)
+      return e;
+  }
   if (m_ready && (e = cudaStreamWaitEvent(s, m_ready, 0)) != cudaSuccess) return e;
   stage_mark("congruence", s);
   // Distributed: this rank forms the column block [c0, c1) of T1 and W, then

@@ -63,7 +63,7 @@ def _run(world, sizes, transport="host"):
         return dict(out)
 
 
-def _check_against_single(dev, res, sizes, exact=False):
+def _check_against_single(dev, res, sizes, exact=False, vec_tol=1e-10):
     import paper_1501_03830_b200 as bg
     from oracle import bse_oracle as orc
     for n, seed in sizes:
@@ -78,8 +78,9 @@ def _check_against_single(dev, res, sizes, exact=False):
         # same Cholesky, reduction and D&C on every rank: columns agree with the
         # single-GPU solve to rounding, without sign flips
         scale = max(np.abs(ref.x1).max(), 1.0)
-        assert np.max(np.abs(x1 - ref.x1.real)) <= 1e-10 * scale, n
-        assert np.max(np.abs(x2 - ref.x2.real)) <= 1e-10 * scale, n
+        if vec_tol is not None:
+            assert np.max(np.abs(x1 - ref.x1.real)) <= vec_tol * scale, n
+            assert np.max(np.abs(x2 - ref.x2.real)) <= vec_tol * scale, n
         # north-star gates on the assembled solution
         G = x1.T @ x1 - x2.T @ x2
         assert np.linalg.norm(G - np.eye(n)) <= 1e-12 * n
@@ -117,3 +118,17 @@ def test_host_transport_world3_ragged_blocks(dev):
             for u, v in zip(res[0][key], res[r][key]):
                 assert np.array_equal(u, v), key
     _check_against_single(dev, res[0], sizes)
+
+
+def test_host_transport_world2_emulated_engine(dev):
+    """n >= 4096: the sharded congruence blocks, Q1 and recovery run on the
+    emulated-FP64 engine over each rank's column range."""
+    sizes = [(4500, 11)]
+    res = _run(2, sizes)
+    for key in res[0]:
+        for u, v in zip(res[0][key], res[1][key]):
+            assert np.array_equal(u, v), key
+    # the emulated products' row scaling depends on the column-block origin,
+    # so W matches the single-GPU W to rounding only (eigenvectors to eps/gap,
+    # up to sign): lambda and the north-star gates are checked, not columns
+    _check_against_single(dev, res[0], sizes, vec_tol=None)
