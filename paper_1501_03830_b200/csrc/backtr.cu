@@ -357,40 +357,50 @@ cudaError_t q2_apply(int n, int b, int g, const double* Vblk, const double* VTbl
   return launch(q2_apply_pair_kernel<2, 2>, 2);
 }
 
-size_t q1_oz_bytes(int n, int b, int ncols) {
-  const int kb = kQ1GroupOz * b, c = std::min(ncols, kQ1OzChunk);
+size_t q1_oz_bytes(int n, int b, int ncols, int group) {
+  const int kb = group * b, c = std::min(ncols, kQ1OzChunk);
   // Y = V^T Zs (kb x c chunks, K = m <= n); Zs -= V Y2 (n x c chunks, K = kb)
   return std::max({ozgemm_bytes(kb, ncols, n, c), ozgemm_bytes(n, ncols, kb, c),
                    ozgemm_bytes(kb, ncols, kb, c)});
 }
 
-cudaError_t q1_apply(int n, int b, const double* Vall, long long ldv, const double* Tall,
-                     double* Z, long long ldz, int ncols, const Q1Scratch& w, cudaStream_t s) {
-  // Panels are merged in groups of w.group (compact-WY of the product,
-  // T_g = [[T_A, -T_A (V_A^T V_B) T_B], [0, T_B]]) so the applying GEMMs run
-  // with K = group*b instead of b.  Vall must be zero outside the
-  // reflectors (syevd memsets it before SY2SB).
+namespace {
+
+int q1_panels(int n, int b) {
   int np = 0;
   while (n - np * b - b >= 2) ++np;
+  return np;
+}
+
+}  // namespace
+
+size_t q1_tg_doubles(int n, int b, int group) {
+  const int np = q1_panels(n, b);
+  size_t tot = 0;
+  for (int pend = np; pend > 0; pend -= group) {
+    const size_t kb = (size_t)(pend - std::max(0, pend - group)) * b;
+    tot += kb * kb;
+  }
+  return std::max<size_t>(tot, 1);
+}
+
+cudaError_t q1_build(int n, int b, const double* Vall, long long ldv, const double* Tall,
+                     const Q1Scratch& w, cudaStream_t s) {
+  // Panels are merged in groups of w.group (compact-WY of the product,
+  // T_g = [[T_A, -T_A (V_A^T V_B) T_B], [0, T_B]]) so the applying GEMMs run
+  // with K = group*b instead of b.  T_g by pairwise merging, bottom-up:
+  // blocks A = [a0, a0+h), B = [a0+h, a0+h+hb) of an already merged level
+  // combine as T_AB = -T_A X_AB T_B with X = V^T V (strict block-upper part,
+  // one product per group).  DMMA only: this runs on a side stream next to
+  // the divide and conquer, whose top merges own the emulated workspace.
+  // Vall must be zero outside the reflectors (syevd memsets it before SY2SB).
+  const int np = q1_panels(n, b), G = w.group;
   cudaError_t e = cudaSuccess;
-  const int G = w.group;
-  // one product on the INT8 engine when it is large enough to pay for the
-  // slicing and reconstruction passes
-  auto mul = [&](bool ta, const GemmProblem& g) {
-    if (w.oz && (double)g.M * g.N * g.K >= kOzMinWork)
-      return ozgemm(ta, false, g, w.oz, w.oz_bytes, kQ1OzChunk, s);
-    return gemm(ta, false, g, s);
-  };
+  double* Tg = w.tg;
   for (int pend = np; pend > 0; pend -= G) {
     const int p0 = std::max(0, pend - G), k = pend - p0, kb = k * b;
     const int r0 = (p0 + 1) * b, m = n - r0;
     const double* V = Vall + r0 + (long long)(p0 * b) * ldv;  // m x kb
-    double* Tg = w.tg;                                        // kb x kb (ld kb)
-    stage_mark("q1_tg", s);
-    // T_g by pairwise merging, bottom-up: blocks A = [a0, a0+h), B = [a0+h,
-    // a0+h+hb) of an already merged level combine as T_AB = -T_A X_AB T_B with
-    // X = V^T V (strict block-upper part, one product per group), so the
-    // work sits in a few large products instead of k thin ones.
     if ((e = cudaMemsetAsync(Tg, 0, sizeof(double) * kb * kb, s)) != cudaSuccess) return e;
     for (int j = 0; j < k; ++j) {
       if ((e = cudaMemcpy2DAsync(Tg + (long long)j * b + (long long)j * b * kb, kb * sizeof(double),
@@ -401,7 +411,7 @@ cudaError_t q1_apply(int n, int b, const double* Vall, long long ldv, const doub
     if (k > 1) {
       GemmProblem gx = make_gemm(kb, kb, m, 1.0, V, ldv, V, ldv, 0.0, w.x, kb);
       gx.mc = Mask::strict_upper();  // covers every block above the diagonal blocks
-      if ((e = mul(true, gx)) != cudaSuccess) return e;
+      if ((e = gemm(true, false, gx, s)) != cudaSuccess) return e;
     }
     for (int h = b; h < kb; h *= 2) {
       for (int a0 = 0; a0 + h < kb; a0 += 2 * h) {
@@ -418,8 +428,28 @@ cudaError_t q1_apply(int n, int b, const double* Vall, long long ldv, const doub
         if ((e = gemm(false, false, g2, s)) != cudaSuccess) return e;
       }
     }
+    Tg += (size_t)kb * kb;
+  }
+  return e;
+}
+
+cudaError_t q1_apply(int n, int b, const double* Vall, long long ldv, double* Z, long long ldz,
+                     int ncols, const Q1Scratch& w, cudaStream_t s) {
+  const int np = q1_panels(n, b), G = w.group;
+  cudaError_t e = cudaSuccess;
+  // one product on the INT8 engine when it is large enough to pay for the
+  // slicing and reconstruction passes
+  auto mul = [&](bool ta, const GemmProblem& g) {
+    if (w.oz && (double)g.M * g.N * g.K >= kOzMinWork)
+      return ozgemm(ta, false, g, w.oz, w.oz_bytes, kQ1OzChunk, s);
+    return gemm(ta, false, g, s);
+  };
+  const double* Tg = w.tg;
+  for (int pend = np; pend > 0; pend -= G) {
+    const int p0 = std::max(0, pend - G), k = pend - p0, kb = k * b;
+    const int r0 = (p0 + 1) * b, m = n - r0;
+    const double* V = Vall + r0 + (long long)(p0 * b) * ldv;  // m x kb
     double* Zs = Z + r0;
-    stage_mark("q1_gemm", s);
     // Y = V^T Zs (kb x ncols)
     GemmProblem g3 = make_gemm(kb, ncols, m, 1.0, V, ldv, Zs, ldz, 0.0, w.y, kb);
     if ((e = mul(true, g3)) != cudaSuccess) return e;
@@ -430,6 +460,7 @@ cudaError_t q1_apply(int n, int b, const double* Vall, long long ldv, const doub
     // Zs -= V Y2
     GemmProblem g5 = make_gemm(m, ncols, kb, -1.0, V, ldv, w.y2, kb, 1.0, Zs, ldz);
     if ((e = mul(false, g5)) != cudaSuccess) return e;
+    Tg += (size_t)kb * kb;
   }
   return e;
 }

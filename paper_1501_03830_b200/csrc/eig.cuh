@@ -12,7 +12,7 @@ namespace bse {
 constexpr int kMaxPanel = 64;  // SY2SB bandwidth b (<= 64)
 
 struct Sy2sbScratch {
-  double* vwv = nullptr;  // 8 slots of b columns: V1 W1 V2 W2 | W1c V1c W2c V2c (sy2sb)
+  double* vwv = nullptr;  // 2 x 8 slots of b columns: V1 W1 V2 W2 | W1c V1c W2c V2c (sy2sb)
   long long ldvwv = 0;
   double* y = nullptr;    // m x b
   long long ldy = 0;
@@ -26,8 +26,12 @@ struct Sy2sbScratch {
 };
 constexpr int kSymmSplits = 16;
 
+// la (optional): look-ahead stream for the next pair's first panel, with two
+// events (trailing columns ready, panel done).
 cudaError_t sy2sb(double* A, long long lda, int n, int b, double* Vall, long long ldv,
-                  double* Tall, const Sy2sbScratch& w, int num_sms, cudaStream_t s);
+                  double* Tall, const Sy2sbScratch& w, int num_sms, cudaStream_t s,
+                  cudaStream_t la = nullptr, cudaEvent_t ev_cols = nullptr,
+                  cudaEvent_t ev_panel = nullptr);
 cudaError_t extract_band(const double* A, long long lda, int n, int b, double* AB, int ldab,
                          cudaStream_t s);
 
@@ -50,11 +54,11 @@ cudaError_t q2_apply(int n, int b, int g, const double* Vblk, const double* VTbl
 // when the large products run on the emulated-FP64 INT8 engine, whose
 // efficiency needs K = group * b in the thousands).
 constexpr int kQ1Group = 8;
-constexpr int kQ1GroupOz = 32;
+constexpr int kQ1GroupOz = 64;
 constexpr int kQ1OzChunk = 2048;
 struct Q1Scratch {
   int group = kQ1Group;
-  double* tg = nullptr;    // (G b)^2
+  double* tg = nullptr;    // every group's T_g, back to back (q1_tg_doubles)
   double* x = nullptr;     // (G b) x (G b): V^T V of the group
   double* tmp = nullptr;   // (G b)^2 / 2
   double* y = nullptr;     // (G b) x ncols
@@ -64,9 +68,14 @@ struct Q1Scratch {
   void* oz = nullptr;      // emulated-FP64 workspace (null: DMMA only)
   size_t oz_bytes = 0;
 };
-size_t q1_oz_bytes(int n, int b, int ncols);
-cudaError_t q1_apply(int n, int b, const double* Vall, long long ldv, const double* Tall,
-                     double* Z, long long ldz, int ncols, const Q1Scratch& w, cudaStream_t s);
+size_t q1_oz_bytes(int n, int b, int ncols, int group);
+size_t q1_tg_doubles(int n, int b, int group);
+// T_g of every panel group (DMMA only; may run on a side stream).
+cudaError_t q1_build(int n, int b, const double* Vall, long long ldv, const double* Tall,
+                     const Q1Scratch& w, cudaStream_t s);
+// Z <- Q1 Z with the T_g from q1_build.
+cudaError_t q1_apply(int n, int b, const double* Vall, long long ldv, double* Z, long long ldz,
+                     int ncols, const Q1Scratch& w, cudaStream_t s);
 
 // Tridiagonal divide and conquer.
 struct StedcWork {

@@ -4,6 +4,7 @@
 // Step order follows the reference's solvers (solvers.py:46-77 / :97-104):
 // Cholesky -> congruence -> eigendecomposition -> back-transform -> scale.
 #include <algorithm>
+#include <cstdlib>
 #include <string>
 #include <vector>
 #include "eig.cuh"
@@ -30,6 +31,27 @@ void stage_mark(const char* name, cudaStream_t s) {
   cudaEventRecord(L.ev[L.used], s);
   L.names[L.used] = name;
   ++L.used;
+}
+
+SideStream& side_stream() {
+  // one per device (the solve may run on any current device)
+  static SideStream per_dev[64];
+  int dev = 0;
+  cudaGetDevice(&dev);
+  SideStream& ss = per_dev[dev & 63];
+  if (!ss.s) {
+    int least = 0, greatest = 0;
+    cudaDeviceGetStreamPriorityRange(&least, &greatest);
+    cudaStreamCreateWithPriority(&ss.s, cudaStreamNonBlocking, least);
+    cudaStreamCreateWithPriority(&ss.hp, cudaStreamNonBlocking, greatest);
+    cudaEventCreateWithFlags(&ss.fork, cudaEventDisableTiming);
+    cudaEventCreateWithFlags(&ss.join, cudaEventDisableTiming);
+    cudaEventCreateWithFlags(&ss.hp_fork, cudaEventDisableTiming);
+    cudaEventCreateWithFlags(&ss.hp_join, cudaEventDisableTiming);
+    cudaEventCreateWithFlags(&ss.la_cols, cudaEventDisableTiming);
+    cudaEventCreateWithFlags(&ss.la_panel, cudaEventDisableTiming);
+  }
+  return ss;
 }
 
 int device_sm_count() {
@@ -65,7 +87,7 @@ SyevdWork carve_syevd(Arena& a, int n, int flags) {
   w.Vall = a.take<double>((size_t)ld * n);
   w.Tall = a.take<double>((size_t)np * b * b);
   w.sc.ldvwv = ld;
-  w.sc.vwv = a.take<double>((size_t)ld * 8 * b);  // V1 W1 V2 W2 | W1c V1c W2c V2c
+  w.sc.vwv = a.take<double>((size_t)ld * 16 * b);  // 2 x (V1 W1 V2 W2 | W1c V1c W2c V2c)
   w.sc.ldy = ld;
   w.sc.y = a.take<double>((size_t)ld * b);
   w.sc.z = a.take<double>(2 * (size_t)b * b);
@@ -88,8 +110,9 @@ SyevdWork carve_syevd(Arena& a, int n, int flags) {
   w.VTblk = a.take<double>(qb);
   const bool oz = !(flags & kFlagNativeFp64) && !(flags & 0x1) && n >= kOzMinN;
   w.q1.group = oz ? kQ1GroupOz : kQ1Group;
+  if (const char* g = std::getenv("BSE_Q1_GROUP")) w.q1.group = std::max(1, std::atoi(g));  // tuning
   const size_t gb = (size_t)w.q1.group * b;
-  w.q1.tg = a.take<double>(gb * gb);
+  w.q1.tg = a.take<double>(q1_tg_doubles(n, b, w.q1.group));
   w.q1.x = a.take<double>(gb * gb);
   w.q1.tmp = a.take<double>(gb * gb / 2 + gb * b);
   w.q1.y = a.take<double>(gb * n);
@@ -100,7 +123,7 @@ SyevdWork carve_syevd(Arena& a, int n, int flags) {
   if (oz) {
     // shared by the top D&C merges and Q1 (never live at the same time)
     const int h = (n + 1) / 2;
-    w.q1.oz_bytes = std::max(q1_oz_bytes(n, b, n), ozgemm_bytes(h, n, h, 2048));
+    w.q1.oz_bytes = std::max(q1_oz_bytes(n, b, n, w.q1.group), ozgemm_bytes(h, n, h, 2048));
     w.q1.oz = a.take<char>(w.q1.oz_bytes);
     w.dc.oz = w.q1.oz;
     w.dc.oz_bytes = w.q1.oz_bytes;
@@ -128,7 +151,10 @@ cudaError_t syevd(int n, double* A, long long lda, double* w, double* Z, long lo
   cudaError_t e;
   stage_mark("sy2sb", s);
   if ((e = cudaMemsetAsync(ws.Vall, 0, sizeof(double) * ws.ldv * n, s)) != cudaSuccess) return e;
-  if ((e = sy2sb(A, lda, n, b, ws.Vall, ws.ldv, ws.Tall, ws.sc, sms, s)) != cudaSuccess) return e;
+  SideStream& side = side_stream();
+  if ((e = sy2sb(A, lda, n, b, ws.Vall, ws.ldv, ws.Tall, ws.sc, sms, s, side.hp, side.la_cols,
+                 side.la_panel)) != cudaSuccess)
+    return e;
   stage_mark("sb2st", s);
   if ((e = extract_band(A, lda, n, b, ws.AB, ws.ldab, s)) != cudaSuccess) return e;
   if ((e = sb2st(ws.AB, ws.ldab, n, b, ws.d, ws.e, ws.V2, ws.tau2, ws.progress, sms, s)) != cudaSuccess)
@@ -137,10 +163,25 @@ cudaError_t syevd(int n, double* A, long long lda, double* w, double* Z, long lo
     stage_mark("values", s);
     return tridiag_values(n, ws.d, ws.e, w, ws.dc.scal, s);
   }
-  stage_mark("stedc", s);
-  if ((e = stedc(n, ws.d, ws.e, w, Z, ldz, ws.dc, s)) != cudaSuccess) return e;
-  stage_mark("q2_build", s);
-  if ((e = q2_build(n, b, kQ2Group, ws.V2, ws.tau2, ws.Vblk, ws.VTblk, s)) != cudaSuccess) return e;
+  // The Q2 blocks (from the bulge-chasing reflectors) and the Q1 group T
+  // factors (from the SY2SB panels) do not depend on the divide and conquer:
+  // they are built on a side stream while the latency-bound D&C runs.
+  if ((e = cudaEventRecord(side.fork, s)) != cudaSuccess) return e;
+  if ((e = cudaStreamWaitEvent(side.s, side.fork, 0)) != cudaSuccess) return e;
+  if ((e = q2_build(n, b, kQ2Group, ws.V2, ws.tau2, ws.Vblk, ws.VTblk, side.s)) != cudaSuccess)
+    return e;
+  if ((e = q1_build(n, b, ws.Vall, ws.ldv, ws.Tall, ws.q1, side.s)) != cudaSuccess) return e;
+  if ((e = cudaEventRecord(side.join, side.s)) != cudaSuccess) return e;
+  // the D&C chain of small latency-bound kernels runs on a high-priority
+  // stream so the side stream's CTAs never delay its next launch
+  if ((e = cudaEventRecord(side.hp_fork, s)) != cudaSuccess) return e;
+  if ((e = cudaStreamWaitEvent(side.hp, side.hp_fork, 0)) != cudaSuccess) return e;
+  stage_mark("stedc", side.hp);
+  if ((e = stedc(n, ws.d, ws.e, w, Z, ldz, ws.dc, side.hp)) != cudaSuccess) return e;
+  if ((e = cudaEventRecord(side.hp_join, side.hp)) != cudaSuccess) return e;
+  if ((e = cudaStreamWaitEvent(s, side.hp_join, 0)) != cudaSuccess) return e;
+  stage_mark("q2_build_wait", s);
+  if ((e = cudaStreamWaitEvent(s, side.join, 0)) != cudaSuccess) return e;
   if (zc1 < 0) zc1 = n;
   double* Zs = Z + (long long)zc0 * ldz;
   const int nz = zc1 - zc0;
@@ -148,7 +189,7 @@ cudaError_t syevd(int n, double* A, long long lda, double* w, double* Z, long lo
   if ((e = q2_apply(n, b, kQ2Group, ws.Vblk, ws.VTblk, Zs, ldz, nz, s)) != cudaSuccess) return e;
   stage_mark("q1_apply", s);
   if (nz <= 0) return cudaSuccess;
-  return q1_apply(n, b, ws.Vall, ws.ldv, ws.Tall, Zs, ldz, nz, ws.q1, s);
+  return q1_apply(n, b, ws.Vall, ws.ldv, Zs, ldz, nz, ws.q1, s);
 }
 
 // ---------------------------------------------------------------------------

@@ -17,6 +17,16 @@ struct StageLog {
 };
 StageLog& stage_log();
 
+// Per-device auxiliary stream (+ fork/join events) for work that overlaps the
+// main solve stream.
+struct SideStream {
+  cudaStream_t s = nullptr;   // lowest priority: work that overlaps the solve stream
+  cudaStream_t hp = nullptr;  // highest priority: latency-bound chains next to it
+  cudaEvent_t fork = nullptr, join = nullptr, hp_fork = nullptr, hp_join = nullptr;
+  cudaEvent_t la_cols = nullptr, la_panel = nullptr;  // SY2SB panel look-ahead
+};
+SideStream& side_stream();
+
 double launch_peak(int which, int blocks, int iters, double* sink, cudaStream_t s);
 
 struct SolveStatus {

@@ -352,19 +352,24 @@ cudaError_t panel_w(int m, int bw, const double* V, long long ldv, const double*
 // [V1 W1] [W1c V1c]^T, [W1c V1c]^T V2 and [V1 W1 V2 W2] [W1c V1c W2c V2c]^T
 // are single GEMMs.
 cudaError_t sy2sb(double* A, long long lda, int n, int b, double* Vall, long long ldv,
-                  double* Tall, const Sy2sbScratch& w, int num_sms, cudaStream_t s) {
+                  double* Tall, const Sy2sbScratch& w, int num_sms, cudaStream_t s,
+                  cudaStream_t la, cudaEvent_t ev_cols, cudaEvent_t ev_panel) {
   cudaError_t e = cudaSuccess;
   const int bw = b;
   const long long lw = w.ldvwv;
-  double* slot[8];
-  for (int i = 0; i < 8; ++i) slot[i] = w.vwv + i * lw * bw;
-  double *sV1 = slot[0], *sW1 = slot[1], *sV2 = slot[2], *sW2 = slot[3];
-  double *sW1c = slot[4], *sV1c = slot[5], *sW2c = slot[6], *sV2c = slot[7];
+  // two sets of 8 slots: the look-ahead panel of the next pair writes its V
+  // into the other set while this pair's trailing update still reads V1/W1
+  double* slots[2][8];
+  for (int q = 0; q < 2; ++q)
+    for (int i = 0; i < 8; ++i) slots[q][i] = w.vwv + (q * 8 + i) * lw * bw;
   auto copy_cols = [&](double* dst, const double* src, int rows) {
     return cudaMemcpy2DAsync(dst, lw * sizeof(double), src, lw * sizeof(double),
                              (size_t)rows * sizeof(double), bw, cudaMemcpyDeviceToDevice, s);
   };
-  for (int p = 0;; p += 2) {
+  bool panel_ready = false;  // this pair's first panel was factored by the look-ahead
+  for (int p = 0, set = 0;; p += 2, set ^= 1) {
+    double *sV1 = slots[set][0], *sW1 = slots[set][1], *sV2 = slots[set][2], *sW2 = slots[set][3];
+    double *sW1c = slots[set][4], *sV1c = slots[set][5], *sW2c = slots[set][6], *sV2c = slots[set][7];
     const int k = p * b;
     const int m = n - k - b;
     if (m < 2) break;
@@ -372,9 +377,14 @@ cudaError_t sy2sb(double* A, long long lda, int n, int b, double* Vall, long lon
     double* A2 = A + (k + b) + (long long)(k + b) * lda;
     double* Tp1 = Tall + (size_t)p * b * b;
     stage_mark("sy2sb_panel", s);
-    e = panel_qr(P1, lda, m, bw, Vall + (k + b) + (long long)k * ldv, ldv, sV1, lw, Tp1, w.red,
-                 w.bar, num_sms, s);
-    if (e != cudaSuccess) return e;
+    if (panel_ready) {
+      if ((e = cudaStreamWaitEvent(s, ev_panel, 0)) != cudaSuccess) return e;
+    } else {
+      e = panel_qr(P1, lda, m, bw, Vall + (k + b) + (long long)k * ldv, ldv, sV1, lw, Tp1, w.red,
+                   w.bar, num_sms, s);
+      if (e != cudaSuccess) return e;
+    }
+    panel_ready = false;
     stage_mark("sy2sb_symm", s);
     if ((e = symm_panel(A2, lda, m, bw, sV1, lw, w, s)) != cudaSuccess) return e;
     if ((e = panel_w(m, bw, sV1, lw, Tp1, sW1, lw, w, s)) != cudaSuccess) return e;
@@ -422,9 +432,34 @@ cudaError_t sy2sb(double* A, long long lda, int n, int b, double* Vall, long lon
     if ((e = copy_cols(sV2c + b, sV2 + b, m2)) != cudaSuccess) return e;
     // one rank-4b trailing update: A3 -= [V1' W1' V2 W2] [W1' V1' W2 V2]^T (lower)
     stage_mark("sy2sb_syr2k", s);
-    GemmProblem g7 = make_gemm(m2, m2, 4 * bw, -1.0, sV1 + b, lw, sW1c + b, lw, 1.0, A3, lda);
-    g7.mc = Mask::lower();
-    if ((e = gemm(false, true, g7, s)) != cudaSuccess) return e;
+    // Look-ahead: the next pair's first panel lives in A3's first b columns.
+    // Update those first, factor the panel on the (high-priority) look-ahead
+    // stream -- the panel kernel needs at most m/256 SMs -- while the rest of
+    // the trailing update runs here.
+    const int kn = k + 2 * b, mn = n - kn - b;
+    const bool ahead = la && mn >= 2 && (long long)kPanelThreads * num_sms >= mn;
+    if (ahead) {
+      GemmProblem ga = make_gemm(m2, bw, 4 * bw, -1.0, sV1 + b, lw, sW1c + b, lw, 1.0, A3, lda);
+      ga.mc = Mask::lower();
+      if ((e = gemm(false, true, ga, s)) != cudaSuccess) return e;
+      if ((e = cudaEventRecord(ev_cols, s)) != cudaSuccess) return e;
+      if ((e = cudaStreamWaitEvent(la, ev_cols, 0)) != cudaSuccess) return e;
+      double* Pn = A + (kn + b) + (long long)kn * lda;
+      e = panel_qr(Pn, lda, mn, bw, Vall + (kn + b) + (long long)kn * ldv, ldv, slots[set ^ 1][0],
+                   lw, Tall + (size_t)(p + 2) * b * b, w.red, w.bar, num_sms, la);
+      if (e != cudaSuccess) return e;
+      if ((e = cudaEventRecord(ev_panel, la)) != cudaSuccess) return e;
+      panel_ready = true;
+      // rest: rows b.., columns b.. of A3 (lower)
+      GemmProblem gb = make_gemm(m2 - b, m2 - b, 4 * bw, -1.0, sV1 + 2 * b, lw, sW1c + 2 * b, lw,
+                                 1.0, A3 + b + (long long)b * lda, lda);
+      gb.mc = Mask::lower();
+      if ((e = gemm(false, true, gb, s)) != cudaSuccess) return e;
+    } else {
+      GemmProblem g7 = make_gemm(m2, m2, 4 * bw, -1.0, sV1 + b, lw, sW1c + b, lw, 1.0, A3, lda);
+      g7.mc = Mask::lower();
+      if ((e = gemm(false, true, g7, s)) != cudaSuccess) return e;
+    }
   }
   return e;
 }
