@@ -216,10 +216,11 @@ __global__ void __launch_bounds__(32 * NW, 1) q2_apply_pair_kernel(int n, int b,
   // this lane's column of Z (rows added per access); prefetch thread's column
   const bool colok = cw + rl < ncols;
   double* const zc = Z + (long long)(colok ? cw + rl : 0) * ldz;
-  const int prr = tid & 63;           // prefetch row (kQ2Threads % 64 == 0)
-  const int pc0 = tid >> 6;           // first prefetch column, step 7
-  static_assert(kQ2Threads % 64 == 0, "prefetch mapping");
-  constexpr int kPStep = kQ2Threads / 64;
+  // row prefetch: every warp streams in its own 8 columns (lanes 4c..4c+3
+  // cover column c's 64 rows, 16 each), so only a warp-level sync guards sZn
+  const int pcol = lane >> 2;         // column within the warp's 8
+  const int prow0 = (lane & 3) * 16;  // first of this lane's 16 rows
+  static_assert(kQ2Threads % 32 == 0, "prefetch mapping");
 
   double acc[NT][2];
   int ga = ngroups - 1, j = 0, wh = 0, stage = 0;
@@ -252,18 +253,16 @@ __global__ void __launch_bounds__(32 * NW, 1) q2_apply_pair_kernel(int n, int b,
     for (int m = 0; m < wh; ++m)
       if (j < steps_of(ga - m)) step_first = false;
     if (step_first && j + 1 < smax_of(ga)) {
-      const int row = B0 + 64 * j + 8 * NT + prr;
-      const bool rok = row >= 0 && row < n;
-      int col = blockIdx.x * kQ2W + pc0;
-      const double* src = Z + (long long)col * ldz + row;
-      double* dst = sZn + pc0 * LDN + prr;
-#pragma unroll 4
-      for (int c = pc0; c < kQ2W; c += kPStep) {
-        const bool ok = rok && col < ncols;
-        cp_async8(dst, ok ? src : Z, ok);
-        src += kPStep * ldz;
-        dst += kPStep * LDN;
-        col += kPStep;
+      const int row0 = B0 + 64 * j + 8 * NT + prow0;
+      const int col = cw + pcol;
+      const bool cok = col < ncols;
+      const double* src = Z + (long long)(cok ? col : 0) * ldz;
+      double* dst = sZn + (warp * 8 + pcol) * LDN + prow0;
+#pragma unroll
+      for (int r = 0; r < 16; ++r) {
+        const int row = row0 + r;
+        const bool ok = cok && row >= 0 && row < n;
+        cp_async8(dst + r, ok ? src + row : Z, ok);
       }
       cp_async_commit();
     }
@@ -288,8 +287,9 @@ __global__ void __launch_bounds__(32 * NW, 1) q2_apply_pair_kernel(int n, int b,
         }
       }
       if (!pair_end) {
+        // the rows were streamed in by this warp only
         cp_async_wait<0>();
-        __syncthreads();
+        __syncwarp();
         const int cl = warp * 8;
 #pragma unroll
         for (int i = 0; i < NT - 8; ++i) { acc[i][0] = acc[8 + i][0]; acc[i][1] = acc[8 + i][1]; }

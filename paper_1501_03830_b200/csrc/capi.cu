@@ -186,13 +186,21 @@ int bse_solve_spd_pair_host(int64_t n, const double* M, int64_t ldm, const doubl
   void* dW = buf + 4 * mat + lam_bytes;
   bse::SolveStatus st{};
   const size_t row = sizeof(double) * (size_t)n;
-  // K first (Cholesky starts as soon as it lands); M on a second stream,
-  // joined before the congruence
-  e = cudaMemcpy2DAsync(dK, ld * 8, K, ldk * 8, row, n, cudaMemcpyHostToDevice, s);
-  cudaEvent_t evAlloc;
+  // K's first column half first (the Cholesky starts on it as soon as it
+  // lands), then its second half and M on a second stream: the copies share
+  // the host link in that order, overlapping the factorization; joined
+  // before the first trailing update and before the congruence.
+  const int n1 = bse::potrf_top_split((int)n);
+  e = cudaMemcpy2DAsync(dK, ld * 8, K, ldk * 8, row, n1, cudaMemcpyHostToDevice, s);
+  cudaEvent_t evAlloc, evK2;
   cudaEventCreateWithFlags(&evAlloc, cudaEventDisableTiming);
+  cudaEventCreateWithFlags(&evK2, cudaEventDisableTiming);
   cudaEventRecord(evAlloc, s);
   cudaStreamWaitEvent(s2, evAlloc, 0);
+  if (e == cudaSuccess && n1 < n)
+    e = cudaMemcpy2DAsync(dK + (long long)n1 * ld, ld * 8, K + (long long)n1 * ldk, ldk * 8, row,
+                          n - n1, cudaMemcpyHostToDevice, s2);
+  if (e == cudaSuccess) e = cudaEventRecord(evK2, s2);
   if (e == cudaSuccess)
     e = cudaMemcpy2DAsync(dM, ld * 8, M, ldm * 8, row, n, cudaMemcpyHostToDevice, s2);
   if (e == cudaSuccess) e = cudaEventRecord(evM, s2);
@@ -200,7 +208,7 @@ int bse_solve_spd_pair_host(int64_t n, const double* M, int64_t ldm, const doubl
   bse::HostOut hout{X1, ldx1, X2, ldx2, lam, s2};
   if (e == cudaSuccess)
     e = bse::solve_spd_pair((int)n, dM, ld, dK, ld, dLam, dX1, ld, dX2, ld, dW, wb, flags, s, &st,
-                            evM, &hout);
+                            evM, &hout, nullptr, evK2);
   cudaEvent_t evDone;
   cudaEventCreateWithFlags(&evDone, cudaEventDisableTiming);
   cudaEventRecord(evDone, s2);
@@ -212,6 +220,7 @@ int bse_solve_spd_pair_host(int64_t n, const double* M, int64_t ldm, const doubl
   cudaStreamDestroy(s2);
   cudaEventDestroy(evM);
   cudaEventDestroy(evAlloc);
+  cudaEventDestroy(evK2);
   BSE_TRY_CUDA(e, "solve_host");
   BSE_TRY_CUDA(e2, "solve_host sync");
   return map_solve_status(st, info);

@@ -352,8 +352,11 @@ cudaError_t trsm_lln(const double* L, long long ldl, int n, double* B, long long
   return trsm_lln(L + n1 + n1 * ldl, ldl, n2, B + n1, ldb, ncols, s);
 }
 
+int potrf_top_split(int n) { return n <= kLeaf ? n : split_point(n); }
+
 static cudaError_t potrf_rec(double* A, long long lda, int n, int off, DevStatus* st,
-                             cudaStream_t s, double* inv, const OzWork* oz) {
+                             cudaStream_t s, double* inv, const OzWork* oz,
+                             const PotrfHook* hook = nullptr) {
   if (n <= kLeaf) {
     ensure_smem<potf2_kernel>();
     potf2_kernel<<<1, 2 * kLeaf, kLeafSmem, s>>>(A, lda, n, off, st, inv);
@@ -365,6 +368,8 @@ static cudaError_t potrf_rec(double* A, long long lda, int n, int off, DevStatus
   if (e != cudaSuccess) return e;
   e = trsm_rlt(A, lda, n1, A + n1, lda, n2, s, inv, oz);  // A21 <- A21 L11^{-T}
   if (e != cudaSuccess) return e;
+  // columns [n1, n) are first touched here (the host entry streams them in)
+  if (hook && (e = hook->fn(hook->ctx, s)) != cudaSuccess) return e;
   // A22 -= A21 A21^T (lower triangle only)
   GemmProblem p = make_gemm(n2, n2, n1, -1.0, A + n1, lda, A + n1, lda, 1.0,
                             A + n1 + n1 * lda, lda);
@@ -376,9 +381,14 @@ static cudaError_t potrf_rec(double* A, long long lda, int n, int off, DevStatus
 }
 
 cudaError_t potrf_lower(double* A, long long lda, int n, DevStatus* st, cudaStream_t s,
-                        double* inv_cache, const OzWork* oz) {
+                        double* inv_cache, const OzWork* oz, const PotrfHook* hook) {
   if (n <= 0) return cudaSuccess;
-  cudaError_t e = potrf_rec(A, lda, n, 0, st, s, inv_cache, oz);
+  if (hook && n <= kLeaf) {
+    cudaError_t e = hook->fn(hook->ctx, s);
+    if (e != cudaSuccess) return e;
+    hook = nullptr;
+  }
+  cudaError_t e = potrf_rec(A, lda, n, 0, st, s, inv_cache, oz, hook);
   if (e != cudaSuccess) return e;
   return zero_strict_upper(A, lda, n, s);
 }

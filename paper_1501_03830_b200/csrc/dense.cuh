@@ -31,8 +31,17 @@ struct OzWork {
 size_t trsm_llt_oz_bytes(int n, int ncols, int chunk);
 
 size_t potrf_inv_cache_doubles(int n);
+// hook (optional): called on the stream once, at the top level, before
+// columns [potrf_top_split(n), n) are first read (lets a caller stream that
+// half of the matrix in while the first half is factored).
+struct PotrfHook {
+  cudaError_t (*fn)(void* ctx, cudaStream_t s);
+  void* ctx;
+};
+int potrf_top_split(int n);
 cudaError_t potrf_lower(double* A, long long lda, int n, DevStatus* st, cudaStream_t s,
-                        double* inv_cache = nullptr, const OzWork* oz = nullptr);
+                        double* inv_cache = nullptr, const OzWork* oz = nullptr,
+                        const PotrfHook* hook = nullptr);
 
 // A (m x n) <- A * L^{-T}, L n x n lower (right, lower, transposed).
 cudaError_t trsm_rlt(const double* L, long long ldl, int n, double* A, long long lda, int m,

@@ -231,11 +231,35 @@ SolveWork carve_solve(Arena& a, int n, int flags) {
   return w;
 }
 
-__global__ void copy_lower_kernel(int n, const double* src, long long lds, double* dst, long long ldd) {
+// dst(:, c0:c1) = tril(src)(:, c0:c1)  (n rows)
+__global__ void copy_lower_kernel(int n, const double* src, long long lds, double* dst, long long ldd,
+                                  int c0 = 0, int c1 = -1) {
+  if (c1 < 0) c1 = n;
   const long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x;
-  if (idx >= (long long)n * n) return;
-  const int r = (int)(idx % n), c = (int)(idx / n);
+  if (idx >= (long long)n * (c1 - c0)) return;
+  const int r = (int)(idx % n), c = c0 + (int)(idx / n);
   dst[r + (long long)c * ldd] = (r >= c) ? src[r + (long long)c * lds] : 0.0;
+}
+
+// Second half of the host entry's K upload: wait for it, then copy it into L.
+struct KTail {
+  int n, c0;
+  const double* K; long long ldk;
+  double* L; long long ld;
+  cudaEvent_t ready;
+};
+
+cudaError_t k_tail_hook(void* ctx, cudaStream_t s) {
+  const KTail& t = *static_cast<const KTail*>(ctx);
+  cudaError_t e = cudaStreamWaitEvent(s, t.ready, 0);
+  if (e != cudaSuccess) return e;
+  const long long cnt = (long long)t.n * (t.n - t.c0);
+  if (cnt > 0) {
+    copy_lower_kernel<<<(unsigned)ceil_div(cnt, 256), 256, 0, s>>>(t.n, t.K, t.ldk, t.L, t.ld, t.c0,
+                                                                   t.n);
+    count_launch();
+  }
+  return cudaGetLastError();
 }
 
 // Output columns [c0, c0 + nc): v <- Z(:, n-1-c) * lam_c, Zr(:, c) <- Z(:, n-1-c)
@@ -288,7 +312,7 @@ cudaError_t solve_spd_pair(int n, const double* M, long long ldm, const double* 
                            double* lam, double* X1, long long ldx1, double* X2, long long ldx2,
                            void* work, size_t work_bytes, int flags, cudaStream_t s,
                            SolveStatus* out, cudaEvent_t m_ready, const HostOut* hout,
-                           Comm* comm) {
+                           Comm* comm, cudaEvent_t k_tail_ready) {
   out->code = 0;
   out->pivot_index = -1;
   out->pivot_value = 0.0;
@@ -305,13 +329,19 @@ cudaError_t solve_spd_pair(int n, const double* M, long long ldm, const double* 
   if ((e = cudaMemcpyAsync(w.st, h0, sizeof(h0), cudaMemcpyHostToDevice, s)) != cudaSuccess) return e;
   // 1. K = L L^T
   stage_mark("potrf", s);
-  copy_lower_kernel<<<nb, 256, 0, s>>>(n, K, ldk, w.L, ld);
-  count_launch();
   {
+    // with k_tail_ready (host entry), only columns [0, n1) of K have landed:
+    // the Cholesky factors them while the rest streams in
+    const int n1 = k_tail_ready ? potrf_top_split(n) : n;
+    const long long cnt = (long long)n * n1;
+    copy_lower_kernel<<<(unsigned)ceil_div(cnt, 256), 256, 0, s>>>(n, K, ldk, w.L, ld, 0, n1);
+    count_launch();
+    KTail tail{n, n1, K, ldk, w.L, ld, k_tail_ready};
+    PotrfHook hook{k_tail_hook, &tail};
     // the emulated engine's workspace aliases the (still idle) eigensolver's
     OzWork ozp{w.oz, w.oz_bytes, kRecoverBlock};
-    if ((e = potrf_lower(w.L, ld, n, &w.st[0], s, w.linv, w.oz_bytes ? &ozp : nullptr)) !=
-        cudaSuccess)
+    if ((e = potrf_lower(w.L, ld, n, &w.st[0], s, w.linv, w.oz_bytes ? &ozp : nullptr,
+                         k_tail_ready ? &hook : nullptr)) != cudaSuccess)
       return e;
   }
   if (m_ready && (e = cudaStreamWaitEvent(s, m_ready, 0)) != cudaSuccess) return e;
@@ -387,7 +417,7 @@ cudaError_t solve_spd_pair(int n, const double* M, long long ldm, const double* 
   // u = L Zr (into T1), v = L^{-T} (Zr Lam) (in W); with host outputs the
   // recovery runs in column blocks so each block's D2H copy overlaps the next
   // block's TRMM/TRSM
-  const int cb = hout ? kRecoverBlock : n;
+  const int cb = hout ? kRecoverBlockHost : n;
   std::vector<cudaEvent_t> evs;
   bool first_block = true;
   for (int cs = (int)c0; cs < (int)c1; cs += cb) {

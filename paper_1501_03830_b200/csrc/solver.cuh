@@ -36,6 +36,8 @@ struct SolveStatus {
   int failed_factor;   // 0: K (A-B), 1: M (A+B)
 };
 
+// k_tail_ready (host entry): only K's columns [0, potrf_top_split(n)) are on
+// the device at the call; the rest lands when the event fires.
 // Optional host destination for the e2e path: X1/X2 column blocks are copied
 // on `stream` as soon as they are recovered.
 struct HostOut {
@@ -44,7 +46,11 @@ struct HostOut {
   double* lam;
   cudaStream_t stream;
 };
-constexpr int kRecoverBlock = 2048;
+constexpr int kRecoverBlock = 2048;      // emulated-engine column chunk
+// host entry: X columns recovered per block (its D2H overlaps the next
+// block's TRMM/TRSM; wide enough that the per-block TRSM keeps its large
+// updates on the emulated engine)
+constexpr int kRecoverBlockHost = 4096;
 // BSE_FLAG_NATIVE_FP64: every product on the DMMA engine (no INT8 emulation)
 constexpr int kFlagNativeFp64 = 0x4;
 // the emulated-FP64 engine is used for the large products from this n up
@@ -55,7 +61,8 @@ cudaError_t solve_spd_pair(int n, const double* M, long long ldm, const double* 
                            double* lam, double* X1, long long ldx1, double* X2, long long ldx2,
                            void* work, size_t work_bytes, int flags, cudaStream_t s,
                            SolveStatus* out, cudaEvent_t m_ready = nullptr,
-                           const HostOut* hout = nullptr, Comm* comm = nullptr);
+                           const HostOut* hout = nullptr, Comm* comm = nullptr,
+                           cudaEvent_t k_tail_ready = nullptr);
 
 cudaError_t absorption(int n, const double* lam, const double* X1c, long long ldx1,
                        const double* X2c, long long ldx2, const double* dr, const double* dl,

@@ -136,3 +136,23 @@ def test_emulated_fp64_path_n4608(dev):
     err = np.linalg.norm(x1 * sgn - x1n, axis=0) / np.linalg.norm(x1n, axis=0)
     assert np.all(err <= n * np.finfo(float).eps / gap + 1e-12)
     torch.cuda.synchronize()
+
+
+def test_repeat_solves_bitwise_identical(dev):
+    """The solve overlaps work on auxiliary streams (SY2SB panel look-ahead,
+    Q2/Q1 block builds under the D&C): repeated solves must be bitwise
+    identical (no race, no order-dependent reduction)."""
+    import torch
+    from paper_1501_03830_b200.device import to_device_colmajor, view_colmajor
+    n = 5000
+    a, b, _ = configs.config_operator(2, n=n, seed=7)
+    Mt, ldm = to_device_colmajor(a + b, dev)
+    Kt, ldk = to_device_colmajor(a - b, dev)
+    outs = []
+    for _ in range(3):
+        lam, X1, X2, _ = bg.solve_pair_device(Mt, ldm, Kt, ldk, n)
+        outs.append((lam.clone(), view_colmajor(X1, n, n).clone(), view_colmajor(X2, n, n).clone()))
+    torch.cuda.synchronize()
+    for lam, X1, X2 in outs[1:]:
+        assert torch.equal(lam, outs[0][0])
+        assert torch.equal(X1, outs[0][1]) and torch.equal(X2, outs[0][2])

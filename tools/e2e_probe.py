@@ -55,12 +55,17 @@ lib.bse_profile_enable(1)
 t0 = time.perf_counter()
 host()
 dt = time.perf_counter() - t0
-ms = (C.c_double * 256)()
-names = C.create_string_buffer(256 * 32)
-k = lib.bse_profile_read(256, ms, names)
-print(f"host entry: {dt * 1e3:.1f} ms wall")
+cap = 4096
+ms = (C.c_double * cap)()
+names = C.create_string_buffer(cap * 32)
+k = lib.bse_profile_read(cap, ms, names)
+print(f"host entry: {dt * 1e3:.1f} ms wall; {k} stage intervals")
 raw = names.raw
+agg = {}
 for i in range(k):
     nm = raw[i * 32:(i + 1) * 32].split(b"\0")[0].decode()
-    print(f"  {nm:16s} {ms[i]:8.2f} ms")
+    agg[nm] = agg.get(nm, 0.0) + ms[i]
+for nm, v in agg.items():
+    print(f"  {nm:16s} {v:8.2f} ms")
+print(f"  {'sum':16s} {sum(agg.values()):8.2f} ms")
 lib.bse_profile_enable(0)
