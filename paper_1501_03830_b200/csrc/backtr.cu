@@ -25,6 +25,15 @@ constexpr int kQ2MaxWarps = 14;
 
 BSE_HD int q2_hb(int b, int g) { return ((g + b + 1) / 2) * 2; }  // padded block height
 
+// Stored block = the apply kernel's shared-memory stage, byte for byte, so one
+// bulk copy moves it: V column-major (ld LDV = 104), then VT = V*T row-major
+// (ld LDT = 40); both strides are == 8 mod 16 doubles (conflict-free 128-bit
+// fragment loads).  Padding entries are zero.
+constexpr int kQ2HB = 96;
+constexpr int kQ2LDV = kQ2HB + 8;  // sV[c * LDV + r]
+constexpr int kQ2LDT = kQ2G + 8;   // sVT[r * LDT + c]
+constexpr int kQ2Stage = kQ2G * kQ2LDV + kQ2HB * kQ2LDT;
+
 BSE_DEV int refl_len(int n, int b, int s, int j) {
   const int r0 = s + 1 + j * b;
   if (s > n - 3 || r0 > n - 1) return 0;
@@ -47,8 +56,7 @@ __global__ void __launch_bounds__(256) q2_build_kernel(int n, int b, int g, int 
   const int s0 = gi * g;
   const int tid = threadIdx.x;
   const size_t blk = (size_t)gi * maxsteps + j;
-  double* Vout = Vblk + blk * HB * g;
-  double* VTout = VTblk + blk * HB * g;
+  double* Vout = Vblk + blk * kQ2Stage;
   for (int idx = tid; idx < HB * g; idx += blockDim.x) {
     const int r = idx % HB, c = idx / HB;
     const int s = s0 + c;
@@ -80,12 +88,18 @@ __global__ void __launch_bounds__(256) q2_build_kernel(int n, int b, int g, int 
     }
     __syncthreads();
   }
-  for (int idx = tid; idx < HB * g; idx += blockDim.x) {
-    const int r = idx % HB, c = idx / HB;
+  (void)VTblk;
+  double* VTo = Vout + (size_t)g * kQ2LDV;
+  for (int idx = tid; idx < kQ2LDV * g; idx += blockDim.x) {
+    const int r = idx % kQ2LDV, c = idx / kQ2LDV;
+    Vout[idx] = r < HB ? V[c * HB + r] : 0.0;
+  }
+  for (int idx = tid; idx < HB * kQ2LDT; idx += blockDim.x) {
+    const int r = idx / kQ2LDT, c = idx % kQ2LDT;
     double acc = 0.0;
-    for (int k = 0; k <= c; ++k) acc += V[k * HB + r] * T[c * g + k];
-    Vout[idx] = V[idx];
-    VTout[r * g + c] = acc;  // VT row-major (q2_apply's B-operand layout)
+    if (c < g)
+      for (int k = 0; k <= c; ++k) acc += V[k * HB + r] * T[c * g + k];
+    VTo[idx] = acc;  // VT row-major (q2_apply's B-operand layout)
   }
 }
 
@@ -99,10 +113,6 @@ __global__ void __launch_bounds__(256) q2_build_kernel(int n, int b, int g, int 
 // every shared-memory fragment pair is one conflict-free 128-bit load (V
 // column-major with LDV = 104, VT row-major with LDT = 40: both == 8 mod 16).
 // The zero corners of the staircase V (and of VT) are skipped at compile time.
-constexpr int kQ2HB = 96;
-constexpr int kQ2LDV = kQ2HB + 8;  // sV[c * LDV + r]
-constexpr int kQ2LDT = kQ2G + 8;   // sVT[r * LDT + c]
-constexpr int kQ2Stage = kQ2G * kQ2LDV + kQ2HB * kQ2LDT;
 constexpr int kQ2LDN = 64 + 8;     // prefetched rows, [col * LDN + row]
 
 BSE_DEV double2 lds2(const double* p) { return *reinterpret_cast<const double2*>(p); }
@@ -156,21 +166,29 @@ BSE_DEV void q2_block_t(double (&acc)[NT][2], const double* sV, const double* sV
 // stays in registers; 64 rows stream in (cp.async, one step ahead) and out
 // per STEP instead of per block.
 
+// V/VT blocks arrive by bulk async copy (TMA engine) into a 2-stage ring
+// driven by mbarriers: a producer warp walks the same block order and issues
+// each block's copy as soon as every consumer warp has released the stage
+// (empty barrier, one arrival per warp); consumer warps wait only on the
+// stage's full barrier.  No CTA-wide barrier in the loop: warps may drift up
+// to one block apart.
 template <int P, int NW>
-__global__ void __launch_bounds__(32 * NW, 1) q2_apply_pair_kernel(int n, int b, int maxsteps,
-                                                                      const double* __restrict__ Vblk,
-                                                                      const double* __restrict__ VTblk,
-                                                                      double* __restrict__ Z,
-                                                                      long long ldz, int ncols) {
-  constexpr int HB = kQ2HB, G = kQ2G;
+__global__ void __launch_bounds__(32 * (NW + 1), 1) q2_apply_pair_kernel(
+    int n, int b, int maxsteps, const double* __restrict__ Vblk, double* __restrict__ Z,
+    long long ldz, int ncols) {
+  constexpr int G = kQ2G;
   constexpr int STAGE = kQ2Stage;
   constexpr int LDN = kQ2LDN;
   constexpr int NT = 4 * P + 8;  // 8-row tiles in the window
+  constexpr unsigned kStageBytes = STAGE * sizeof(double);
   extern __shared__ __align__(16) double sm[];
   double* sZn = sm + 2 * STAGE;
+  unsigned long long* bars = reinterpret_cast<unsigned long long*>(sZn + 8 * NW * LDN);
+  unsigned long long* full = bars;       // [2]
+  unsigned long long* empty = bars + 2;  // [2]
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int kl = lane & 3, rl = lane >> 2;
-  constexpr int kQ2W = 8 * NW, kQ2Threads = 32 * NW;
+  constexpr int kQ2W = 8 * NW;
   const int cw = blockIdx.x * kQ2W + warp * 8;
   const int nsweeps = n - 2;
   const int ngroups = (int)ceil_div(nsweeps, G);
@@ -198,36 +216,42 @@ __global__ void __launch_bounds__(32 * NW, 1) q2_apply_pair_kernel(int n, int b,
       if (ga - wh >= 0 && j < steps_of(ga - wh)) return true;
     }
   };
-  auto issue_vt = [&](int gi, int j, int stage) {
-    const size_t blk = (size_t)gi * maxsteps + j;
-    const double* gV = Vblk + blk * HB * G;
-    const double* gVT = VTblk + blk * HB * G;
-    double* sV = sm + stage * STAGE;
-    double* sVT = sV + G * kQ2LDV;
-    for (int idx = tid; idx < HB * G / 2; idx += blockDim.x) {
-      const int e = idx * 2;
-      const int r = e % HB, c = e / HB;   // V: column-major
-      cp_async16(sV + c * kQ2LDV + r, gV + e, true);
-      const int rt = e / G, ct = e % G;   // VT: row-major
-      cp_async16(sVT + rt * kQ2LDT + ct, gVT + e, true);
+  if (tid == 0) {
+    mbar_init(&full[0], 1);
+    mbar_init(&full[1], 1);
+    mbar_init(&empty[0], NW);
+    mbar_init(&empty[1], NW);
+    mbar_fence_init();
+  }
+  __syncthreads();
+  if (ngroups <= 0) return;
+  if (warp == NW) {
+    // producer: one bulk copy per block, in the consumers' order
+    if (lane == 0) {
+      int ga = ngroups - 1, j = 0, wh = 0;
+      for (unsigned blkno = 0;; ++blkno) {
+        const int st = blkno & 1;
+        if (blkno >= 2) mbar_wait(&empty[st], ((blkno - 2) >> 1) & 1);
+        const size_t blk = (size_t)(ga - wh) * maxsteps + j;
+        mbar_arrive_expect_tx(&full[st], kStageBytes);
+        bulk_g2s(sm + st * STAGE, Vblk + blk * STAGE, kStageBytes, &full[st]);
+        if (!advance(ga, j, wh)) break;
+      }
     }
-    cp_async_commit();
-  };
-  // this lane's column of Z (rows added per access); prefetch thread's column
+    return;
+  }
+  // this lane's column of Z (rows added per access)
   const bool colok = cw + rl < ncols;
   double* const zc = Z + (long long)(colok ? cw + rl : 0) * ldz;
-  // row prefetch: every warp streams in its own 8 columns (lanes 4c..4c+3
-  // cover column c's 64 rows, 16 each), so only a warp-level sync guards sZn
-  const int pcol = lane >> 2;         // column within the warp's 8
-  const int prow0 = (lane & 3) * 16;  // first of this lane's 16 rows
-  static_assert(kQ2Threads % 32 == 0, "prefetch mapping");
+  // row prefetch: every warp streams in its own 8 columns (lane l: rows l
+  // and l + 32 of each column, so every copy instruction moves 256
+  // contiguous bytes), and only a warp-level sync guards sZn
 
   double acc[NT][2];
   int ga = ngroups - 1, j = 0, wh = 0, stage = 0;
-  if (ga < 0) return;
-  issue_vt(ga, 0, 0);
+  unsigned blkno = 0;
   bool pair_start = true;
-  for (;;) {
+  for (;; ++blkno) {
     const int B0 = (ga - P + 1) * G + 1;
     int nga = ga, nj = j, nwh = wh;
     const bool more = advance(nga, nj, nwh);
@@ -243,26 +267,26 @@ __global__ void __launch_bounds__(32 * NW, 1) q2_apply_pair_kernel(int n, int b,
         }
       pair_start = false;
     }
-    // this block's V/VT (and any row prefetch) have landed; every thread is
-    // past the previous block, so its stage and the row buffer may be reused
-    cp_async_wait<0>();
-    __syncthreads();
-    if (more) issue_vt(nga - nwh, nj, stage ^ 1);
+    // this block's V/VT have landed
+    mbar_wait(&full[stage], (blkno >> 1) & 1);
     // first block of step j: prefetch the 64 rows step j+1 brings in
     bool step_first = true;
     for (int m = 0; m < wh; ++m)
       if (j < steps_of(ga - m)) step_first = false;
     if (step_first && j + 1 < smax_of(ga)) {
-      const int row0 = B0 + 64 * j + 8 * NT + prow0;
-      const int col = cw + pcol;
-      const bool cok = col < ncols;
-      const double* src = Z + (long long)(cok ? col : 0) * ldz;
-      double* dst = sZn + (warp * 8 + pcol) * LDN + prow0;
+      const int row0 = B0 + 64 * j + 8 * NT;
 #pragma unroll
-      for (int r = 0; r < 16; ++r) {
-        const int row = row0 + r;
-        const bool ok = cok && row >= 0 && row < n;
-        cp_async8(dst + r, ok ? src + row : Z, ok);
+      for (int c = 0; c < 8; ++c) {
+        const int col = cw + c;
+        const bool cok = col < ncols;
+        const double* src = Z + (long long)(cok ? col : 0) * ldz;
+        double* dst = sZn + (warp * 8 + c) * LDN;
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const int row = row0 + lane + 32 * h;
+          const bool ok = cok && row >= 0 && row < n;
+          cp_async8(dst + lane + 32 * h, ok ? src + row : Z, ok);
+        }
       }
       cp_async_commit();
     }
@@ -273,6 +297,9 @@ __global__ void __launch_bounds__(32 * NW, 1) q2_apply_pair_kernel(int n, int b,
     else if (P == 2 || wh == 1) q2_block_t<4 * (P > 1 ? P - 2 : 0), NT>(acc, sV, sVT, lane);
     else if (P == 3 || wh == 2) q2_block_t<4 * (P > 2 ? P - 3 : 0), NT>(acc, sV, sVT, lane);
     else q2_block_t<4 * (P > 3 ? P - 4 : 0), NT>(acc, sV, sVT, lane);
+    // this warp is done with the stage
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty[stage]);
     if (step_end) {
       const int nstore = pair_end ? NT : 8;
       const int rbase = B0 + 64 * j;
@@ -300,6 +327,8 @@ __global__ void __launch_bounds__(32 * NW, 1) q2_apply_pair_kernel(int n, int b,
           acc[NT - 8 + i][1] = z.y;
         }
       } else {
+        // the next pair's row prefetches (other lanes) read rows stored here
+        __syncwarp();
         pair_start = true;
       }
     }
@@ -316,12 +345,14 @@ __global__ void __launch_bounds__(32 * NW, 1) q2_apply_pair_kernel(int n, int b,
 size_t q2_block_doubles(int n, int b, int g) {
   const int maxsteps = sb2st_maxsteps(n, b);
   const int ngroups = (int)ceil_div(std::max(n - 2, 1), g);
-  return (size_t)ngroups * maxsteps * q2_hb(b, g) * g;
+  (void)b;
+  return (size_t)ngroups * maxsteps * kQ2Stage;
 }
 
 cudaError_t q2_build(int n, int b, int g, const double* V2, const double* tau2, double* Vblk,
                      double* VTblk, cudaStream_t s) {
   if (n <= 2) return cudaSuccess;
+  if (b != 64 || g != kQ2G || q2_hb(b, g) != kQ2HB) return cudaErrorInvalidValue;
   const int maxsteps = sb2st_maxsteps(n, b);
   const int ngroups = (int)ceil_div(n - 2, g);
   const int HB = q2_hb(b, g);
@@ -342,11 +373,13 @@ cudaError_t q2_apply(int n, int b, int g, const double* Vblk, const double* VTbl
   if (b != 64 || g != kQ2G || q2_hb(b, g) != kQ2HB) return cudaErrorInvalidValue;
   const int maxsteps = sb2st_maxsteps(n, b);
   const int sms = device_sm_count();
+  (void)VTblk;
   auto launch = [&](auto kern, int nw) {
-    const size_t smem = sizeof(double) * (2 * (size_t)kQ2Stage + (size_t)8 * nw * kQ2LDN);
+    const size_t smem =
+        sizeof(double) * (2 * (size_t)kQ2Stage + (size_t)8 * nw * kQ2LDN) + 4 * sizeof(unsigned long long);
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    kern<<<(unsigned)ceil_div(ncols, 8 * nw), 32 * nw, smem, s>>>(n, b, maxsteps, Vblk, VTblk, Z,
-                                                                 ldz, ncols);
+    kern<<<(unsigned)ceil_div(ncols, 8 * nw), 32 * (nw + 1), smem, s>>>(n, b, maxsteps, Vblk, Z,
+                                                                       ldz, ncols);
     count_launch();
     return cudaGetLastError();
   };
