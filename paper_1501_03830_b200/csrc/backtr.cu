@@ -26,13 +26,17 @@ constexpr int kQ2MaxWarps = 14;
 BSE_HD int q2_hb(int b, int g) { return ((g + b + 1) / 2) * 2; }  // padded block height
 
 // Stored block = the apply kernel's shared-memory stage, byte for byte, so one
-// bulk copy moves it: V column-major (ld LDV = 104), then VT = V*T row-major
-// (ld LDT = 40); both strides are == 8 mod 16 doubles (conflict-free 128-bit
-// fragment loads).  Padding entries are zero.
+// bulk copy moves it: V column-major (ld 96), then VT = V*T row-major (ld
+// 32), both with the 16-byte units of odd columns (V) / odd rows (VT) XOR-ed
+// by 4: the 128-bit fragment loads of a quarter warp (two consecutive
+// columns / rows) then hit 8 distinct bank groups without padding.
 constexpr int kQ2HB = 96;
-constexpr int kQ2LDV = kQ2HB + 8;  // sV[c * LDV + r]
-constexpr int kQ2LDT = kQ2G + 8;   // sVT[r * LDT + c]
+constexpr int kQ2LDV = kQ2HB;  // sV[c * LDV + swz(r)]
+constexpr int kQ2LDT = kQ2G;   // sVT[r * LDT + swz(c)]
 constexpr int kQ2Stage = kQ2G * kQ2LDV + kQ2HB * kQ2LDT;
+constexpr int kQ2Stages = 2;
+// position of element k (row of V / column of VT) inside line `line`
+BSE_HD int q2_swz(int k, int line) { return ((((k >> 1) ^ ((line & 1) << 2))) << 1) | (k & 1); }
 
 BSE_DEV int refl_len(int n, int b, int s, int j) {
   const int r0 = s + 1 + j * b;
@@ -40,7 +44,9 @@ BSE_DEV int refl_len(int n, int b, int s, int j) {
   return min(b, n - r0);
 }
 
-// One CTA per (group, step): staircase V, T = larft(V), VT = V*T.
+// One CTA per (group, step): staircase V, T = larft(V), VT = V*T.  Shared
+// arrays use odd strides (HB + 1, g + 1) so the column-indexed dot products
+// are bank-conflict free; reflector c is nonzero only in rows [c, c + b).
 __global__ void __launch_bounds__(256) q2_build_kernel(int n, int b, int g, int maxsteps,
                                                        const double* __restrict__ V2,
                                                        const double* __restrict__ tau2,
@@ -48,10 +54,11 @@ __global__ void __launch_bounds__(256) q2_build_kernel(int n, int b, int g, int 
                                                        double* __restrict__ VTblk) {
   extern __shared__ double sm[];
   const int HB = q2_hb(b, g);
-  double* V = sm;                 // HB x g, [c*HB + r]
-  double* G = V + HB * g;         // g x g gram
-  double* T = G + g * g;          // g x g
-  double* tau = T + g * g;        // g
+  const int LV = HB + 1, LG = g + 1;
+  double* V = sm;                 // HB x g, [c*LV + r]
+  double* G = V + LV * g;         // g x g gram, [c*LG + a]
+  double* T = G + LG * g;         // g x g, [c*LG + k]
+  double* tau = T + LG * g;       // g
   const int j = blockIdx.x, gi = blockIdx.y;
   const int s0 = gi * g;
   const int tid = threadIdx.x;
@@ -63,43 +70,48 @@ __global__ void __launch_bounds__(256) q2_build_kernel(int n, int b, int g, int 
     const int len = refl_len(n, b, s, j);
     double v = 0.0;
     if (len > 0 && r >= c && r < c + len) v = V2[((size_t)s * maxsteps + j) * b + (r - c)];
-    V[idx] = v;
+    V[c * LV + r] = v;
   }
   for (int c = tid; c < g; c += blockDim.x) {
     const int s = s0 + c;
     tau[c] = refl_len(n, b, s, j) > 0 ? tau2[(size_t)s * maxsteps + j] : 0.0;
   }
   __syncthreads();
+  // G[c][a] = v_a . v_c for a < c (rows where both are nonzero: [c, a + b))
   for (int idx = tid; idx < g * g; idx += blockDim.x) {
     const int a = idx % g, c = idx / g;
     double acc = 0.0;
-    for (int r = 0; r < HB; ++r) acc += V[a * HB + r] * V[c * HB + r];
-    G[idx] = acc;  // G[c*g + a] = v_a . v_c
-    T[idx] = 0.0;
+    if (a < c) {
+      const int r1 = min(a + b, HB);
+      for (int r = c; r < r1; ++r) acc += V[a * LV + r] * V[c * LV + r];
+    }
+    G[c * LG + a] = acc;
+    T[c * LG + a] = 0.0;
   }
   __syncthreads();
   for (int c = 0; c < g; ++c) {
     if (tid < c) {
       double acc = 0.0;
-      for (int k = tid; k < c; ++k) acc += T[k * g + tid] * G[c * g + k];
-      T[c * g + tid] = -tau[c] * acc;
+      for (int k = tid; k < c; ++k) acc += T[k * LG + tid] * G[c * LG + k];
+      T[c * LG + tid] = -tau[c] * acc;
     } else if (tid == c) {
-      T[c * g + c] = tau[c];
+      T[c * LG + c] = tau[c];
     }
     __syncthreads();
   }
   (void)VTblk;
   double* VTo = Vout + (size_t)g * kQ2LDV;
-  for (int idx = tid; idx < kQ2LDV * g; idx += blockDim.x) {
-    const int r = idx % kQ2LDV, c = idx / kQ2LDV;
-    Vout[idx] = r < HB ? V[c * HB + r] : 0.0;
+  for (int idx = tid; idx < HB * g; idx += blockDim.x) {
+    const int r = idx % HB, c = idx / HB;
+    Vout[c * kQ2LDV + q2_swz(r, c)] = V[c * LV + r];
   }
-  for (int idx = tid; idx < HB * kQ2LDT; idx += blockDim.x) {
-    const int r = idx / kQ2LDT, c = idx % kQ2LDT;
+  // VT[r][c] = sum_{k <= c} V[r][k] T[k][c], V[r][k] != 0 only for r - b < k <= r
+  for (int idx = tid; idx < HB * g; idx += blockDim.x) {
+    const int r = idx / g, c = idx % g;
     double acc = 0.0;
-    if (c < g)
-      for (int k = 0; k <= c; ++k) acc += V[k * HB + r] * T[c * g + k];
-    VTo[idx] = acc;  // VT row-major (q2_apply's B-operand layout)
+    const int k1 = min(c, r);
+    for (int k = max(0, r - b + 1); k <= k1; ++k) acc += V[k * LV + r] * T[c * LG + k];
+    VTo[r * kQ2LDT + q2_swz(c, r)] = acc;  // VT row-major (q2_apply's B-operand layout)
   }
 }
 
@@ -120,6 +132,14 @@ BSE_DEV double2 lds2(const double* p) { return *reinterpret_cast<const double2*>
 template <int OFF, int NT>
 BSE_DEV void q2_block_t(double (&acc)[NT][2], const double* sV, const double* sVT, int lane) {
   const int kl = lane & 3, rl = lane >> 2;
+  // swizzle: this lane's line (column c = 8q + rl of V, row 8i + rl of VT)
+  // has parity rl & 1, so 16-byte unit u moves to u ^ 4 on odd lines; with u
+  // = 4t + kl (t a compile-time tile index) that is +-8 doubles by t's parity
+  const int sw = (rl & 1) * 8;
+  const double* pV0 = sV + rl * kQ2LDV + 2 * kl + sw;   // even tile
+  const double* pV1 = sV + rl * kQ2LDV + 2 * kl - sw;   // odd tile
+  const double* pT0 = sVT + rl * kQ2LDT + 2 * kl + sw;
+  const double* pT1 = sVT + rl * kQ2LDT + 2 * kl - sw;
   double yt[4][2];
 #pragma unroll
   for (int q = 0; q < 4; ++q) yt[q][0] = yt[q][1] = 0.0;
@@ -129,7 +149,7 @@ BSE_DEV void q2_block_t(double (&acc)[NT][2], const double* sV, const double* sV
     double2 bv[4];
 #pragma unroll
     for (int q = 0; q < 4; ++q)
-      if (i >= q && i <= q + 8) bv[q] = lds2(sV + (8 * q + rl) * kQ2LDV + 8 * i + 2 * kl);
+      if (i >= q && i <= q + 8) bv[q] = lds2((i & 1 ? pV1 : pV0) + 8 * q * kQ2LDV + 8 * i);
 #pragma unroll
     for (int q = 0; q < 4; ++q)
       if (i >= q && i <= q + 8) dmma8x8x4(yt[q], acc[OFF + i][0], bv[q].x);
@@ -147,7 +167,7 @@ BSE_DEV void q2_block_t(double (&acc)[NT][2], const double* sV, const double* sV
       double2 bv[6];
 #pragma unroll
       for (int i = h; i < h + 6; ++i)
-        if (q >= i - 8) bv[i - h] = lds2(sVT + (8 * i + rl) * kQ2LDT + 8 * q + 2 * kl);
+        if (q >= i - 8) bv[i - h] = lds2((q & 1 ? pT1 : pT0) + 8 * i * kQ2LDT + 8 * q);
 #pragma unroll
       for (int i = h; i < h + 6; ++i)
         if (q >= i - 8) dmma8x8x4(acc[OFF + i], yt[q][0], bv[i - h].x);
@@ -182,10 +202,11 @@ __global__ void __launch_bounds__(32 * (NW + 1), 1) q2_apply_pair_kernel(
   constexpr int NT = 4 * P + 8;  // 8-row tiles in the window
   constexpr unsigned kStageBytes = STAGE * sizeof(double);
   extern __shared__ __align__(16) double sm[];
-  double* sZn = sm + 2 * STAGE;
+  constexpr int NS = kQ2Stages;
+  double* sZn = sm + NS * STAGE;
   unsigned long long* bars = reinterpret_cast<unsigned long long*>(sZn + 8 * NW * LDN);
-  unsigned long long* full = bars;       // [2]
-  unsigned long long* empty = bars + 2;  // [2]
+  unsigned long long* full = bars;        // [NS]
+  unsigned long long* empty = bars + NS;  // [NS]
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int kl = lane & 3, rl = lane >> 2;
   constexpr int kQ2W = 8 * NW;
@@ -217,10 +238,11 @@ __global__ void __launch_bounds__(32 * (NW + 1), 1) q2_apply_pair_kernel(
     }
   };
   if (tid == 0) {
-    mbar_init(&full[0], 1);
-    mbar_init(&full[1], 1);
-    mbar_init(&empty[0], NW);
-    mbar_init(&empty[1], NW);
+#pragma unroll
+    for (int q = 0; q < NS; ++q) {
+      mbar_init(&full[q], 1);
+      mbar_init(&empty[q], NW);
+    }
     mbar_fence_init();
   }
   __syncthreads();
@@ -229,13 +251,15 @@ __global__ void __launch_bounds__(32 * (NW + 1), 1) q2_apply_pair_kernel(
     // producer: one bulk copy per block, in the consumers' order
     if (lane == 0) {
       int ga = ngroups - 1, j = 0, wh = 0;
-      for (unsigned blkno = 0;; ++blkno) {
-        const int st = blkno & 1;
-        if (blkno >= 2) mbar_wait(&empty[st], ((blkno - 2) >> 1) & 1);
+      for (unsigned blkno = 0, st = 0, use = 0;; ++blkno) {
+        // stage st is being filled for the use-th time: wait for the
+        // consumers' release of its (use-1)-th fill
+        if (use > 0) mbar_wait(&empty[st], (use - 1) & 1);
         const size_t blk = (size_t)(ga - wh) * maxsteps + j;
         mbar_arrive_expect_tx(&full[st], kStageBytes);
         bulk_g2s(sm + st * STAGE, Vblk + blk * STAGE, kStageBytes, &full[st]);
         if (!advance(ga, j, wh)) break;
+        if (++st == NS) { st = 0; ++use; }
       }
     }
     return;
@@ -249,9 +273,9 @@ __global__ void __launch_bounds__(32 * (NW + 1), 1) q2_apply_pair_kernel(
 
   double acc[NT][2];
   int ga = ngroups - 1, j = 0, wh = 0, stage = 0;
-  unsigned blkno = 0;
+  unsigned use = 0;  // fills of `stage` consumed so far
   bool pair_start = true;
-  for (;; ++blkno) {
+  for (;;) {
     const int B0 = (ga - P + 1) * G + 1;
     int nga = ga, nj = j, nwh = wh;
     const bool more = advance(nga, nj, nwh);
@@ -268,7 +292,7 @@ __global__ void __launch_bounds__(32 * (NW + 1), 1) q2_apply_pair_kernel(
       pair_start = false;
     }
     // this block's V/VT have landed
-    mbar_wait(&full[stage], (blkno >> 1) & 1);
+    mbar_wait(&full[stage], use & 1);
     // first block of step j: prefetch the 64 rows step j+1 brings in
     bool step_first = true;
     for (int m = 0; m < wh; ++m)
@@ -332,7 +356,7 @@ __global__ void __launch_bounds__(32 * (NW + 1), 1) q2_apply_pair_kernel(
         pair_start = true;
       }
     }
-    stage ^= 1;
+    if (++stage == NS) { stage = 0; ++use; }
     if (!more) break;
     ga = nga;
     j = nj;
@@ -356,7 +380,7 @@ cudaError_t q2_build(int n, int b, int g, const double* V2, const double* tau2, 
   const int maxsteps = sb2st_maxsteps(n, b);
   const int ngroups = (int)ceil_div(n - 2, g);
   const int HB = q2_hb(b, g);
-  const size_t smem = sizeof(double) * ((size_t)HB * g + 2 * (size_t)g * g + g);
+  const size_t smem = sizeof(double) * ((size_t)(HB + 1) * g + 2 * (size_t)(g + 1) * g + g);
   static bool attr = false;
   if (!attr) {
     cudaFuncSetAttribute(q2_build_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
@@ -376,7 +400,8 @@ cudaError_t q2_apply(int n, int b, int g, const double* Vblk, const double* VTbl
   (void)VTblk;
   auto launch = [&](auto kern, int nw) {
     const size_t smem =
-        sizeof(double) * (2 * (size_t)kQ2Stage + (size_t)8 * nw * kQ2LDN) + 4 * sizeof(unsigned long long);
+        sizeof(double) * (kQ2Stages * (size_t)kQ2Stage + (size_t)8 * nw * kQ2LDN) +
+        2 * kQ2Stages * sizeof(unsigned long long);
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     kern<<<(unsigned)ceil_div(ncols, 8 * nw), 32 * (nw + 1), smem, s>>>(n, b, maxsteps, Vblk, Z,
                                                                        ldz, ncols);
@@ -424,8 +449,9 @@ cudaError_t q1_build(int n, int b, const double* Vall, long long ldv, const doub
   // with K = group*b instead of b.  T_g by pairwise merging, bottom-up:
   // blocks A = [a0, a0+h), B = [a0+h, a0+h+hb) of an already merged level
   // combine as T_AB = -T_A X_AB T_B with X = V^T V (strict block-upper part,
-  // one product per group).  DMMA only: this runs on a side stream next to
-  // the divide and conquer, whose top merges own the emulated workspace.
+  // one product per group, on the emulated engine with its own workspace:
+  // this runs on a side stream next to the divide and conquer, whose top
+  // merges use the shared one).
   // Vall must be zero outside the reflectors (syevd memsets it before SY2SB).
   const int np = q1_panels(n, b), G = w.group;
   cudaError_t e = cudaSuccess;
@@ -444,7 +470,11 @@ cudaError_t q1_build(int n, int b, const double* Vall, long long ldv, const doub
     if (k > 1) {
       GemmProblem gx = make_gemm(kb, kb, m, 1.0, V, ldv, V, ldv, 0.0, w.x, kb);
       gx.mc = Mask::strict_upper();  // covers every block above the diagonal blocks
-      if ((e = gemm(true, false, gx, s)) != cudaSuccess) return e;
+      if (w.oz_side && (double)kb * kb * m >= kOzMinWork)
+        e = ozgemm(true, false, gx, w.oz_side, w.oz_side_bytes, kQ1OzChunk, s);
+      else
+        e = gemm(true, false, gx, s);
+      if (e != cudaSuccess) return e;
     }
     for (int h = b; h < kb; h *= 2) {
       for (int a0 = 0; a0 + h < kb; a0 += 2 * h) {

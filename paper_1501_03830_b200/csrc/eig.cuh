@@ -67,10 +67,12 @@ struct Q1Scratch {
   GemmProblem* probs = nullptr; // 64
   void* oz = nullptr;      // emulated-FP64 workspace (null: DMMA only)
   size_t oz_bytes = 0;
+  void* oz_side = nullptr; // q1_build's own emulated workspace (it overlaps the D&C)
+  size_t oz_side_bytes = 0;
 };
 size_t q1_oz_bytes(int n, int b, int ncols, int group);
 size_t q1_tg_doubles(int n, int b, int group);
-// T_g of every panel group (DMMA only; may run on a side stream).
+// T_g of every panel group (may run on a side stream; own emulated workspace).
 cudaError_t q1_build(int n, int b, const double* Vall, long long ldv, const double* Tall,
                      const Q1Scratch& w, cudaStream_t s);
 // Z <- Q1 Z with the T_g from q1_build.

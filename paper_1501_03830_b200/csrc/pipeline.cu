@@ -127,6 +127,9 @@ SyevdWork carve_syevd(Arena& a, int n, int flags) {
     w.q1.oz = a.take<char>(w.q1.oz_bytes);
     w.dc.oz = w.q1.oz;
     w.dc.oz_bytes = w.q1.oz_bytes;
+    const int kb = w.q1.group * b;
+    w.q1.oz_side_bytes = ozgemm_bytes(kb, kb, n, kQ1OzChunk);
+    w.q1.oz_side = a.take<char>(w.q1.oz_side_bytes);
   }
   return w;
 }
@@ -166,12 +169,15 @@ cudaError_t syevd(int n, double* A, long long lda, double* w, double* Z, long lo
   // The Q2 blocks (from the bulge-chasing reflectors) and the Q1 group T
   // factors (from the SY2SB panels) do not depend on the divide and conquer:
   // they are built on a side stream while the latency-bound D&C runs.
+  static const bool serial = std::getenv("BSE_SERIAL_BUILDS") != nullptr;  // A/B timing switch
+  cudaStream_t sb = serial ? s : side.s;
+  if (serial) stage_mark("q_builds", s);
   if ((e = cudaEventRecord(side.fork, s)) != cudaSuccess) return e;
-  if ((e = cudaStreamWaitEvent(side.s, side.fork, 0)) != cudaSuccess) return e;
-  if ((e = q2_build(n, b, kQ2Group, ws.V2, ws.tau2, ws.Vblk, ws.VTblk, side.s)) != cudaSuccess)
+  if ((e = cudaStreamWaitEvent(sb, side.fork, 0)) != cudaSuccess) return e;
+  if ((e = q2_build(n, b, kQ2Group, ws.V2, ws.tau2, ws.Vblk, ws.VTblk, sb)) != cudaSuccess)
     return e;
-  if ((e = q1_build(n, b, ws.Vall, ws.ldv, ws.Tall, ws.q1, side.s)) != cudaSuccess) return e;
-  if ((e = cudaEventRecord(side.join, side.s)) != cudaSuccess) return e;
+  if ((e = q1_build(n, b, ws.Vall, ws.ldv, ws.Tall, ws.q1, sb)) != cudaSuccess) return e;
+  if ((e = cudaEventRecord(side.join, sb)) != cudaSuccess) return e;
   // the D&C chain of small latency-bound kernels runs on a high-priority
   // stream so the side stream's CTAs never delay its next launch
   if ((e = cudaEventRecord(side.hp_fork, s)) != cudaSuccess) return e;
