@@ -306,8 +306,14 @@ size_t trsm_llt_oz_bytes(int n, int ncols, int chunk) {
 }
 
 cudaError_t trsm_llt(const double* L, long long ldl, int n, double* B, long long ldb, int ncols,
-                     cudaStream_t s, const double* inv, const OzWork* oz) {
+                     cudaStream_t s, const double* inv, const OzWork* oz, const RowHook* hook) {
   if (n <= 0 || ncols <= 0) return cudaSuccess;
+  cudaError_t e;
+  if (hook && (hook->depth <= 0 || n <= kLeaf)) {
+    // report this whole row range once it is solved
+    if ((e = trsm_llt(L, ldl, n, B, ldb, ncols, s, inv, oz, nullptr)) != cudaSuccess) return e;
+    return hook->fn(hook->ctx, hook->base, hook->base + n, s);
+  }
   if (n <= kLeaf) {
     const double* Y = inv;
     if (!Y) {
@@ -321,14 +327,20 @@ cudaError_t trsm_llt(const double* L, long long ldl, int n, double* B, long long
     return gemm(true, false, p, s);
   }
   const int n1 = split_point(n), n2 = n - n1;
-  cudaError_t e = trsm_llt(L + n1 + n1 * ldl, ldl, n2, B + n1, ldb, ncols, s,
-                           inv ? inv + (size_t)(n1 / kLeaf) * kLeaf * kLeaf : nullptr, oz);
+  // rows [n1, n) are final after the first call (L^T is upper triangular)
+  RowHook hb{}, ht{};
+  if (hook) {
+    hb = *hook; hb.depth -= 1; hb.base = hook->base + n1;
+    ht = *hook; ht.depth -= 1;
+  }
+  e = trsm_llt(L + n1 + n1 * ldl, ldl, n2, B + n1, ldb, ncols, s,
+               inv ? inv + (size_t)(n1 / kLeaf) * kLeaf * kLeaf : nullptr, oz, hook ? &hb : nullptr);
   if (e != cudaSuccess) return e;
   // B1 -= L21^T X2
   GemmProblem p = make_gemm(n1, ncols, n2, -1.0, L + n1, ldl, B + n1, ldb, 1.0, B, ldb);
   e = update(true, false, p, oz, s);
   if (e != cudaSuccess) return e;
-  return trsm_llt(L, ldl, n1, B, ldb, ncols, s, inv, oz);
+  return trsm_llt(L, ldl, n1, B, ldb, ncols, s, inv, oz, hook ? &ht : nullptr);
 }
 
 cudaError_t trsm_lln(const double* L, long long ldl, int n, double* B, long long ldb, int ncols,

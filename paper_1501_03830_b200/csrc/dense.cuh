@@ -48,9 +48,20 @@ cudaError_t trsm_rlt(const double* L, long long ldl, int n, double* A, long long
                      cudaStream_t s, const double* inv = nullptr, const OzWork* oz = nullptr);
 
 
+// Called on the stream as soon as rows [r0, r1) of a TRSM solution are final
+// (bottom-up: L^T is upper triangular); `depth` levels of the recursion
+// report separately (2^depth row pieces), `base` offsets the row indices.
+struct RowHook {
+  cudaError_t (*fn)(void* ctx, int r0, int r1, cudaStream_t s);
+  void* ctx;
+  int depth;
+  int base;
+};
+
 // B (n x ncols) <- L^{-T} * B (left, lower, transposed: solves L^T X = B).
 cudaError_t trsm_llt(const double* L, long long ldl, int n, double* B, long long ldb, int ncols,
-                     cudaStream_t s, const double* inv = nullptr, const OzWork* oz = nullptr);
+                     cudaStream_t s, const double* inv = nullptr, const OzWork* oz = nullptr,
+                     const RowHook* hook = nullptr);
 
 // B (n x ncols) <- L^{-1} * B (left, lower, no transpose).
 cudaError_t trsm_lln(const double* L, long long ldl, int n, double* B, long long ldb, int ncols,

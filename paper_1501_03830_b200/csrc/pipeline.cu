@@ -304,6 +304,54 @@ __global__ void recover_kernel(int n, int ncols, const double* U, const double* 
 
 unsigned nb_all(int n) { return (unsigned)ceil_div((long long)n * n, 256); }
 
+// Rows [r0, r1) of X1, X2 (all ncols columns) from u (U) and v (V).
+__global__ void recover_rows_kernel(int r0, int r1, int ncols, const double* U, const double* V,
+                                    long long ld, const double* lam, double* X1, long long ldx1,
+                                    double* X2, long long ldx2) {
+  const int h = r1 - r0;
+  const long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (idx >= (long long)h * ncols) return;
+  const int r = r0 + (int)(idx % h), c = (int)(idx / h);
+  const double sc = 0.5 / sqrt(lam[c]);
+  const double u = U[r + (long long)c * ld], v = V[r + (long long)c * ld];
+  X1[r + (long long)c * ldx1] = (u + v) * sc;
+  X2[r + (long long)c * ldx2] = (u - v) * sc;
+}
+
+// Host-entry recovery: as each row range of v = L^{-T} Z Lam is final, its
+// rows of X1, X2 are formed and copied back on the copy stream.
+struct RowsOut {
+  int ncols;
+  const double* U; const double* V; long long ld;
+  const double* lam;
+  double* X1; long long ldx1;
+  double* X2; long long ldx2;
+  const HostOut* hout;
+  std::vector<cudaEvent_t>* evs;
+};
+
+cudaError_t rows_out_hook(void* ctx, int r0, int r1, cudaStream_t s) {
+  const RowsOut& o = *static_cast<const RowsOut*>(ctx);
+  if (r1 <= r0) return cudaSuccess;
+  const long long tot = (long long)(r1 - r0) * o.ncols;
+  recover_rows_kernel<<<(unsigned)ceil_div(tot, 256), 256, 0, s>>>(
+      r0, r1, o.ncols, o.U, o.V, o.ld, o.lam, o.X1, o.ldx1, o.X2, o.ldx2);
+  count_launch();
+  cudaError_t e;
+  if ((e = cudaGetLastError()) != cudaSuccess) return e;
+  cudaEvent_t ev;
+  if ((e = cudaEventCreateWithFlags(&ev, cudaEventDisableTiming)) != cudaSuccess) return e;
+  o.evs->push_back(ev);
+  if ((e = cudaEventRecord(ev, s)) != cudaSuccess) return e;
+  if ((e = cudaStreamWaitEvent(o.hout->stream, ev, 0)) != cudaSuccess) return e;
+  const size_t w = sizeof(double) * (size_t)(r1 - r0);
+  if ((e = cudaMemcpy2DAsync(o.hout->X1 + r0, o.hout->ldx1 * 8, o.X1 + r0, o.ldx1 * 8, w, o.ncols,
+                             cudaMemcpyDeviceToHost, o.hout->stream)) != cudaSuccess)
+    return e;
+  return cudaMemcpy2DAsync(o.hout->X2 + r0, o.hout->ldx2 * 8, o.X2 + r0, o.ldx2 * 8, w, o.ncols,
+                           cudaMemcpyDeviceToHost, o.hout->stream);
+}
+
 }  // namespace
 
 size_t solve_bytes(int n, int flags) {
@@ -420,51 +468,35 @@ cudaError_t solve_spd_pair(int n, const double* M, long long ldm, const double* 
         n, (int)c0, nc, w.T1, ld, w.lam2, w.Zr, w.W, ld, lam, bad);
     count_launch();
   }
-  // u = L Zr (into T1), v = L^{-T} (Zr Lam) (in W); with host outputs the
-  // recovery runs in column blocks so each block's D2H copy overlaps the next
-  // block's TRMM/TRSM
-  const int cb = hout ? kRecoverBlockHost : n;
+  // u = L Zr (into T1), v = L^{-T} (Zr Lam) (in W).  With host outputs, v's
+  // rows finalise bottom-up inside the TRSM recursion: each quarter's rows of
+  // X1, X2 are formed and their D2H copy overlaps the rest of the solve.
   std::vector<cudaEvent_t> evs;
-  bool first_block = true;
-  for (int cs = (int)c0; cs < (int)c1; cs += cb) {
-    const int c0 = cs;
-    const int nc = std::min(cb, (int)c1 - cs);
+  const int nc_all = (int)(c1 - c0);
+  if (nc_all > 0) {
     stage_mark("recover_trmm", s);
-    GemmProblem g4 = make_gemm(n, nc, n, 1.0, w.L, ld, w.Zr + (long long)c0 * ld, ld, 0.0,
-                               w.T1 + (long long)c0 * ld, ld);
+    GemmProblem g4 = make_gemm(n, nc_all, n, 1.0, w.L, ld, w.Zr + c0 * ld, ld, 0.0, w.T1 + c0 * ld,
+                               ld);
     g4.ma = Mask::lower();
     if (w.oz_bytes) {
-      // L is sliced once; every column block reuses its residues
-      if ((e = ozgemm(false, false, g4, w.oz, w.oz_bytes, kRecoverBlock, s, !first_block)) != cudaSuccess)
-        return e;
+      if ((e = ozgemm(false, false, g4, w.oz, w.oz_bytes, kRecoverBlock, s)) != cudaSuccess) return e;
     } else if ((e = gemm(false, false, g4, s)) != cudaSuccess) {
       return e;
     }
-    first_block = false;
     stage_mark("recover_trsm", s);
-    if ((e = trsm_llt(w.L, ld, n, w.W + (long long)c0 * ld, ld, nc, s, w.linv,
-                      w.oz_trsm.p ? &w.oz_trsm : nullptr)) != cudaSuccess)
+    const bool host_rows = hout && world == 1;
+    RowsOut ro{nc_all, w.T1 + c0 * ld, w.W + c0 * ld, ld, lam + c0, X1 + c0 * ldx1, ldx1,
+               X2 + c0 * ldx2, ldx2, hout, &evs};
+    RowHook hk{rows_out_hook, &ro, 2, 0};
+    if ((e = trsm_llt(w.L, ld, n, w.W + c0 * ld, ld, nc_all, s, w.linv,
+                      w.oz_trsm.p ? &w.oz_trsm : nullptr, host_rows ? &hk : nullptr)) != cudaSuccess)
       return e;
-    const long long tb = (long long)n * nc;
-    recover_kernel<<<(unsigned)ceil_div(tb, 256), 256, 0, s>>>(
-        n, nc, w.T1 + (long long)c0 * ld, w.W + (long long)c0 * ld, ld, lam + c0,
-        X1 + (long long)c0 * ldx1, ldx1, X2 + (long long)c0 * ldx2, ldx2);
-    count_launch();
-    if (hout) {
-      cudaEvent_t ev;
-      cudaEventCreateWithFlags(&ev, cudaEventDisableTiming);
-      evs.push_back(ev);
-      cudaEventRecord(ev, s);
-      cudaStreamWaitEvent(hout->stream, ev, 0);
-      const size_t row = sizeof(double) * (size_t)n;
-      if ((e = cudaMemcpy2DAsync(hout->X1 + (long long)c0 * hout->ldx1, hout->ldx1 * 8,
-                                 X1 + (long long)c0 * ldx1, ldx1 * 8, row, nc,
-                                 cudaMemcpyDeviceToHost, hout->stream)) != cudaSuccess)
-        return e;
-      if ((e = cudaMemcpy2DAsync(hout->X2 + (long long)c0 * hout->ldx2, hout->ldx2 * 8,
-                                 X2 + (long long)c0 * ldx2, ldx2 * 8, row, nc,
-                                 cudaMemcpyDeviceToHost, hout->stream)) != cudaSuccess)
-        return e;
+    if (!host_rows) {
+      const long long tb = (long long)n * nc_all;
+      recover_kernel<<<(unsigned)ceil_div(tb, 256), 256, 0, s>>>(
+          n, nc_all, w.T1 + c0 * ld, w.W + c0 * ld, ld, lam + c0, X1 + c0 * ldx1, ldx1,
+          X2 + c0 * ldx2, ldx2);
+      count_launch();
     }
   }
   if (world > 1) {

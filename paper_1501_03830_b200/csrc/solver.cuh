@@ -47,10 +47,6 @@ struct HostOut {
   cudaStream_t stream;
 };
 constexpr int kRecoverBlock = 2048;      // emulated-engine column chunk
-// host entry: X columns recovered per block (its D2H overlaps the next
-// block's TRMM/TRSM; wide enough that the per-block TRSM keeps its large
-// updates on the emulated engine)
-constexpr int kRecoverBlockHost = 4096;
 // BSE_FLAG_NATIVE_FP64: every product on the DMMA engine (no INT8 emulation)
 constexpr int kFlagNativeFp64 = 0x4;
 // the emulated-FP64 engine is used for the large products from this n up

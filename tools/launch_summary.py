@@ -14,7 +14,7 @@ ap.add_argument("--top", type=int, default=30)
 a = ap.parse_args()
 lines = [ln for ln in open(a.csv) if not ln.startswith("==")]
 rows = list(csv.DictReader(lines))
-rows = [r for r in rows if "bse" in r["Kernel Name"]]
+rows = [r for r in rows if "bse" in r["Kernel Name"] or "cutlass::device_kernel" in r["Kernel Name"]]
 rows = rows[int(len(rows) * (1 - a.last_fraction)):]
 tot = collections.defaultdict(float)
 cnt = collections.Counter()
@@ -24,6 +24,8 @@ for r in rows:
     name = re.sub(r"^void ", "", name)
     name = re.sub(r"bse::\(anonymous namespace\)::", "", name)
     name = re.sub(r"\(.*$", "", name)
+    if name.startswith("cutlass::device_kernel"):
+        name = "cutlass::device_kernel<int8 tcgen05 GEMM (emulated FP64)>"
     v = float(r["Metric Value"].replace(",", "")) * scale[r["Metric Unit"]]
     tot[name] += v
     cnt[name] += 1
