@@ -50,8 +50,7 @@ BSE_DEV int refl_len(int n, int b, int s, int j) {
 __global__ void __launch_bounds__(256) q2_build_kernel(int n, int b, int g, int maxsteps,
                                                        const double* __restrict__ V2,
                                                        const double* __restrict__ tau2,
-                                                       double* __restrict__ Vblk,
-                                                       double* __restrict__ VTblk) {
+                                                       double* __restrict__ Vblk) {
   extern __shared__ double sm[];
   const int HB = q2_hb(b, g);
   const int LV = HB + 1, LG = g + 1;
@@ -99,7 +98,6 @@ __global__ void __launch_bounds__(256) q2_build_kernel(int n, int b, int g, int 
     }
     __syncthreads();
   }
-  (void)VTblk;
   double* VTo = Vout + (size_t)g * kQ2LDV;
   for (int idx = tid; idx < HB * g; idx += blockDim.x) {
     const int r = idx % HB, c = idx / HB;
@@ -374,7 +372,7 @@ size_t q2_block_doubles(int n, int b, int g) {
 }
 
 cudaError_t q2_build(int n, int b, int g, const double* V2, const double* tau2, double* Vblk,
-                     double* VTblk, cudaStream_t s) {
+                     cudaStream_t s) {
   if (n <= 2) return cudaSuccess;
   if (b != 64 || g != kQ2G || q2_hb(b, g) != kQ2HB) return cudaErrorInvalidValue;
   const int maxsteps = sb2st_maxsteps(n, b);
@@ -386,18 +384,17 @@ cudaError_t q2_build(int n, int b, int g, const double* V2, const double* tau2, 
     cudaFuncSetAttribute(q2_build_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
     attr = true;
   }
-  q2_build_kernel<<<dim3(maxsteps, ngroups), 256, smem, s>>>(n, b, g, maxsteps, V2, tau2, Vblk, VTblk);
+  q2_build_kernel<<<dim3(maxsteps, ngroups), 256, smem, s>>>(n, b, g, maxsteps, V2, tau2, Vblk);
   count_launch();
   return cudaGetLastError();
 }
 
-cudaError_t q2_apply(int n, int b, int g, const double* Vblk, const double* VTblk, double* Z,
-                     long long ldz, int ncols, cudaStream_t s) {
+cudaError_t q2_apply(int n, int b, int g, const double* Vblk, double* Z, long long ldz, int ncols,
+                     cudaStream_t s) {
   if (n <= 2 || ncols <= 0) return cudaSuccess;
   if (b != 64 || g != kQ2G || q2_hb(b, g) != kQ2HB) return cudaErrorInvalidValue;
   const int maxsteps = sb2st_maxsteps(n, b);
   const int sms = device_sm_count();
-  (void)VTblk;
   auto launch = [&](auto kern, int nw) {
     const size_t smem =
         sizeof(double) * (kQ2Stages * (size_t)kQ2Stage + (size_t)8 * nw * kQ2LDN) +

@@ -42,12 +42,13 @@ cudaError_t sb2st(double* AB, int ldab, int n, int b, double* d, double* e, doub
                   double* tau2, int* progress, int num_sms, cudaStream_t s);
 
 // Q2 back-transform: Z <- Q2 Z (Z n x ncols).  Groups of g sweeps form
-// compact-WY blocks; Vblk/VTblk sized by q2_block_bytes().
+// compact-WY blocks (V and V*T, stored in q2_apply's shared-memory stage
+// layout); Vblk sized by q2_block_doubles().
 size_t q2_block_doubles(int n, int b, int g);
 cudaError_t q2_build(int n, int b, int g, const double* V2, const double* tau2, double* Vblk,
-                     double* VTblk, cudaStream_t s);
-cudaError_t q2_apply(int n, int b, int g, const double* Vblk, const double* VTblk, double* Z,
-                     long long ldz, int ncols, cudaStream_t s);
+                     cudaStream_t s);
+cudaError_t q2_apply(int n, int b, int g, const double* Vblk, double* Z, long long ldz, int ncols,
+                     cudaStream_t s);
 
 // Q1 back-transform: Z <- Q1 Z using the SY2SB panels, merged `group` at a
 // time into one compact-WY block (kQ1Group on the DMMA engine; kQ1GroupOz

@@ -73,7 +73,7 @@ struct SyevdWork {
   double* AB; int ldab;
   double* d; double* e;
   double* V2; double* tau2; int* progress;
-  double* Vblk; double* VTblk;
+  double* Vblk;  // Q2 blocks in the apply kernel's stage layout
   Q1Scratch q1;
   StedcWork dc;
 };
@@ -107,7 +107,6 @@ SyevdWork carve_syevd(Arena& a, int n, int flags) {
   w.progress = a.take<int>(2 * (size_t)n);  // full + late counters (sb2st)
   const size_t qb = q2_block_doubles(n, b, kQ2Group);
   w.Vblk = a.take<double>(qb);
-  w.VTblk = a.take<double>(qb);
   const bool oz = !(flags & kFlagNativeFp64) && !(flags & 0x1) && n >= kOzMinN;
   w.q1.group = oz ? kQ1GroupOz : kQ1Group;
   if (const char* g = std::getenv("BSE_Q1_GROUP")) w.q1.group = std::max(1, std::atoi(g));  // tuning
@@ -174,7 +173,7 @@ cudaError_t syevd(int n, double* A, long long lda, double* w, double* Z, long lo
   if (serial) stage_mark("q_builds", s);
   if ((e = cudaEventRecord(side.fork, s)) != cudaSuccess) return e;
   if ((e = cudaStreamWaitEvent(sb, side.fork, 0)) != cudaSuccess) return e;
-  if ((e = q2_build(n, b, kQ2Group, ws.V2, ws.tau2, ws.Vblk, ws.VTblk, sb)) != cudaSuccess)
+  if ((e = q2_build(n, b, kQ2Group, ws.V2, ws.tau2, ws.Vblk, sb)) != cudaSuccess)
     return e;
   if ((e = q1_build(n, b, ws.Vall, ws.ldv, ws.Tall, ws.q1, sb)) != cudaSuccess) return e;
   if ((e = cudaEventRecord(side.join, sb)) != cudaSuccess) return e;
@@ -192,7 +191,7 @@ cudaError_t syevd(int n, double* A, long long lda, double* w, double* Z, long lo
   double* Zs = Z + (long long)zc0 * ldz;
   const int nz = zc1 - zc0;
   stage_mark("q2_apply", s);
-  if ((e = q2_apply(n, b, kQ2Group, ws.Vblk, ws.VTblk, Zs, ldz, nz, s)) != cudaSuccess) return e;
+  if ((e = q2_apply(n, b, kQ2Group, ws.Vblk, Zs, ldz, nz, s)) != cudaSuccess) return e;
   stage_mark("q1_apply", s);
   if (nz <= 0) return cudaSuccess;
   return q1_apply(n, b, ws.Vall, ws.ldv, Zs, ldz, nz, ws.q1, s);
