@@ -104,6 +104,13 @@ BSE_DEV double masked(double v, int row, int col, const Mask& m) {
   return (d < m.lo || d > m.hi) ? 0.0 : v;
 }
 
+// x * 2^k: one multiply by an exactly built power of two in the normal range
+// (the common case), ldexp otherwise
+BSE_DEV double scale2(double x, int k) {
+  if (k >= -1020 && k <= 1020) return x * __longlong_as_double((long long)(k + 1023) << 52);
+  return ldexp(x, k);
+}
+
 // scale exponent so that max |x| * 2^s lies in [2^(beta-1), 2^beta)
 BSE_DEV int scale_exp(double mx, int beta) {
   if (!(mx > 0.0)) return 0;
@@ -116,14 +123,15 @@ BSE_DEV int scale_exp(double mx, int beta) {
 // packed 4 per word (byte q = element q).  The moduli are reduced in pairs:
 // r = x mod (m_a m_b) in FP64 (|r| < 1.5 m_a m_b < 2^17, exact), then both
 // residues of the small non-negative integer r + 2 m_a m_b on the integer
-// pipe (unsigned division by a constant).  Each residue v in [0, m) is
-// stored as the int8 centred representative (v >= 128 ? v - m : v).
-BSE_DEV uint32_t byte8(uint32_t u, uint32_t m) {
-  // u < 2^24: q = floor(u c / 2^32), c = ceil(2^32 / m), is exact because
-  // u (c m - 2^32) < 2^24 m < 2^32
+// pipe (unsigned division by a constant), stored as int8 representatives
+// centred in [-128, m - 128).
+BSE_DEV uint32_t byte8(uint32_t u1, uint32_t m) {
+  // u1 = u + 128 < 2^24: q = floor(u1 c / 2^32), c = ceil(2^32 / m), is exact
+  // because u1 (c m - 2^32) < 2^24 m < 2^32.  (u1 mod m) - 128 is the
+  // residue of u centred in [-128, m - 128) (no compare); as a byte that is
+  // (u1 mod m) ^ 0x80.
   const uint32_t c = (uint32_t)((0x100000000ull + m - 1) / m);
-  const uint32_t v = u - __umulhi(u, c) * m;
-  return (v + (v >= 128u ? 256u - m : 0u)) & 0xffu;
+  return (u1 - __umulhi(u1, c) * m) ^ 0x80u;
 }
 
 BSE_DEV void residues_all(const double (&x)[4], uint32_t (&w)[kMods]) {
@@ -137,39 +145,54 @@ BSE_DEV void residues_all(const double (&x)[4], uint32_t (&w)[kMods]) {
 #pragma unroll
     for (int q = 0; q < 4; ++q) {
       const double r = fma(-rint(x[q] * inv), mp, x[q]);
-      const uint32_t u = (uint32_t)__double2loint(r + kMagic) + 2u * ma * mb;
-      w[2 * pr] |= byte8(u, ma) << (8 * q);
-      w[2 * pr + 1] |= byte8(u, mb) << (8 * q);
+      const uint32_t u1 = (uint32_t)__double2loint(r + kMagic) + 2u * ma * mb + 128u;
+      w[2 * pr] |= byte8(u1, ma) << (8 * q);
+      w[2 * pr + 1] |= byte8(u1, mb) << (8 * q);
     }
   }
 }
 
-// One warp per line, contiguous source.
+// Contiguous source: kSplitWPL warps per line (each a contiguous K range,
+// so a line's loads are spread over several warps in flight), 256 / (32 *
+// kSplitWPL) lines per CTA; the line maximum is combined in shared memory.
+constexpr int kSplitWPL = 4;
+constexpr int kSplitLPC = 256 / (32 * kSplitWPL);
 __global__ void __launch_bounds__(256) split_contig_kernel(int lines, int K, int Kp,
                                                            const double* __restrict__ src,
                                                            long long ld, Mask mk, int beta,
                                                            int8_t* __restrict__ out,
                                                            long long mod_stride,
                                                            int* __restrict__ sexp) {
-  const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
-  const int r = warp;
+  __shared__ double smx[kSplitLPC][kSplitWPL];
+  const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int ll = wid / kSplitWPL, part = wid % kSplitWPL;
+  const int r = blockIdx.x * kSplitLPC + ll;
   const int rows_alloc = (int)(mod_stride / Kp);
-  if (r >= rows_alloc) return;
+  const bool alloc = r < rows_alloc;
   const bool live = r < lines;
   const double* row = src + (long long)(live ? r : 0) * ld;
+  // this warp's K range: a multiple of 128 elements
+  const int span = ((Kp + 128 * kSplitWPL - 1) / (128 * kSplitWPL)) * 128;
+  const int kb = part * span, ke = min(Kp, kb + span);
   double mx = 0.0;
   if (live)
-    for (int k = lane; k < K; k += 32) mx = fmax(mx, fabs(masked(row[k], k, r, mk)));
+    for (int k = kb + lane; k < min(K, ke); k += 32) mx = fmax(mx, fabs(masked(row[k], k, r, mk)));
   mx = warp_max(mx);
+  if (lane == 0) smx[ll][part] = mx;
+  __syncthreads();
+  if (!alloc) return;
+  mx = smx[ll][0];
+#pragma unroll
+  for (int q = 1; q < kSplitWPL; ++q) mx = fmax(mx, smx[ll][q]);
   const int se = scale_exp(mx, beta);
-  if (lane == 0) sexp[r] = se;
+  if (lane == 0 && part == 0) sexp[r] = se;
   uint32_t* o = reinterpret_cast<uint32_t*>(out + (long long)r * Kp);
-  for (int k0 = 4 * lane; k0 < Kp; k0 += 128) {
+  for (int k0 = kb + 4 * lane; k0 < ke; k0 += 128) {
     double x[4];
 #pragma unroll
     for (int q = 0; q < 4; ++q) {
       const int k = k0 + q;
-      x[q] = (live && k < K) ? trunc(ldexp(masked(row[k], k, r, mk), se)) : 0.0;
+      x[q] = (live && k < K) ? trunc(scale2(masked(row[k], k, r, mk), se)) : 0.0;
     }
     uint32_t w[kMods];
     residues_all(x, w);
@@ -213,7 +236,7 @@ __global__ void __launch_bounds__(256) split_strided_kernel(int lines, int K, in
     const int rl = idx & 63, kl = idx >> 6;
     const int r = r0 + rl, k = k0 + kl;
     double v = 0.0;
-    if (r < lines && k < K) v = trunc(ldexp(masked(src[r + (long long)k * ld], r, k, mk), se_s[rl]));
+    if (r < lines && k < K) v = trunc(scale2(masked(src[r + (long long)k * ld], r, k, mk), se_s[rl]));
     tile[kl][rl] = v;
   }
   __syncthreads();
@@ -241,40 +264,59 @@ __global__ void __launch_bounds__(256) split_strided_kernel(int lines, int K, in
 // v_t q[t][k] < 2^40, so the four limb sums A_k (< 2^44) are exact in FP64;
 // the quotient q = rint(S / P) (|q| < 2^12) comes from the top limbs and
 // R_k = A_k - q p_k is exact, leaving one rounding per limb addition.
+// One thread per 4 consecutive rows of one column: 16-byte loads of every
+// residue plane (Mp % 16 == 0 keeps them aligned), 4 independent CRTs.
 __global__ void __launch_bounds__(256) crt_kernel(int M, int N, int Mp, const int32_t* __restrict__ c32,
                                                   long long batch, const int* __restrict__ sa,
                                                   const int* __restrict__ sb, double alpha,
                                                   double beta, double* __restrict__ C,
                                                   long long ldc, int col0, Mask mc,
                                                   const int* __restrict__ ccol) {
+  const int M4 = (M + 3) >> 2;
   const long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x;
-  if (idx >= (long long)M * N) return;
-  const int i = (int)(idx % M), j = (int)(idx / M);
-  const int d = (col0 + j) - i;
-  if (d < mc.lo || d > mc.hi) return;
-  const int32_t* p = c32 + i + (long long)j * Mp;
-  double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+  if (idx >= (long long)M4 * N) return;
+  const int i0 = (int)(idx % M4) * 4, j = (int)(idx / M4);
+  const int dj = col0 + j;
+  // rows i0..i0+3 all outside the output band: nothing to do
+  if (dj - (i0 + 3) > mc.hi || dj - i0 < mc.lo) return;
+  const int4* p = reinterpret_cast<const int4*>(c32 + i0 + (long long)j * Mp);
+  const long long b4 = batch >> 2;
+  double a[4][4];
+#pragma unroll
+  for (int e = 0; e < 4; ++e) a[e][0] = a[e][1] = a[e][2] = a[e][3] = 0.0;
 #pragma unroll
   for (int t = 0; t < kMods; ++t) {
     const uint32_t m = kMod(t);
     // c_t + 2^31 - (2^31 mod m) >= 0 has the residue of c_t (|c_t| < 2^31 - 256)
     const uint32_t off = 0x80000000u - (0x80000000u % m);
-    const uint32_t v = ((uint32_t)p[t * batch] + off) % m;
-    const double dv = __hiloint2double(0x43300000, (int)v) - 4503599627370496.0;  // 2^52
-    a0 = fma(dv, c_crt.q[t][0], a0);
-    a1 = fma(dv, c_crt.q[t][1], a1);
-    a2 = fma(dv, c_crt.q[t][2], a2);
-    a3 = fma(dv, c_crt.q[t][3], a3);
+    const int4 c4 = __ldcs(p + t * b4);
+    const int cv[4] = {c4.x, c4.y, c4.z, c4.w};
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      const uint32_t v = ((uint32_t)cv[e] + off) % m;
+      const double dv = __hiloint2double(0x43300000, (int)v) - 4503599627370496.0;  // 2^52
+      a[e][0] = fma(dv, c_crt.q[t][0], a[e][0]);
+      a[e][1] = fma(dv, c_crt.q[t][1], a[e][1]);
+      a[e][2] = fma(dv, c_crt.q[t][2], a[e][2]);
+      a[e][3] = fma(dv, c_crt.q[t][3], a[e][3]);
+    }
   }
   constexpr double k32 = 4294967296.0, k64 = k32 * k32, k96 = k64 * k32;
-  const double q = rint(fma(a3, k96, fma(a2, k64, a1 * k32)) * c_crt.inv_p);
-  const double r0 = fma(-q, c_crt.p[0], a0), r1 = fma(-q, c_crt.p[1], a1);
-  const double r2 = fma(-q, c_crt.p[2], a2), r3 = fma(-q, c_crt.p[3], a3);
-  const double cp = ((r3 * k96 + r2 * k64) + r1 * k32) + r0;
-  double v = alpha * ldexp(cp, -(sa[i] + sb[j]));
-  double* cd = C + i + (long long)(ccol ? ccol[col0 + j] : col0 + j) * ldc;
-  if (beta != 0.0) v += beta * *cd;
-  *cd = v;
+  double* cd = C + (long long)(ccol ? ccol[dj] : dj) * ldc;
+  const int sj = sb[j];
+#pragma unroll
+  for (int e = 0; e < 4; ++e) {
+    const int i = i0 + e;
+    const int d = dj - i;
+    if (i >= M || d < mc.lo || d > mc.hi) continue;
+    const double q = rint(fma(a[e][3], k96, fma(a[e][2], k64, a[e][1] * k32)) * c_crt.inv_p);
+    const double r0 = fma(-q, c_crt.p[0], a[e][0]), r1 = fma(-q, c_crt.p[1], a[e][1]);
+    const double r2 = fma(-q, c_crt.p[2], a[e][2]), r3 = fma(-q, c_crt.p[3], a[e][3]);
+    const double cp = ((r3 * k96 + r2 * k64) + r1 * k32) + r0;
+    double v = alpha * scale2(cp, -(sa[i] + sj));
+    if (beta != 0.0) v += beta * cd[i];
+    cd[i] = v;
+  }
 }
 
 long long r16(long long x) { return (x + 15) / 16 * 16; }
@@ -351,7 +393,7 @@ cudaError_t ozgemm(bool transA, bool transB, const GemmProblem& p, void* work, s
                    int8_t* out, long long rows_alloc, int* sexp, unsigned long long* mxbuf) {
     const long long mstride = rows_alloc * Kp;
     if (contiguous) {
-      const unsigned blocks = (unsigned)ceil_div(rows_alloc * 32, 256);
+      const unsigned blocks = (unsigned)ceil_div(rows_alloc, kSplitLPC);
       split_contig_kernel<<<blocks, 256, 0, s>>>(lines, K, (int)Kp, src, ld, mk, beta, out,
                                                  mstride, sexp);
       count_launch();
@@ -388,7 +430,7 @@ cudaError_t ozgemm(bool transA, bool transB, const GemmProblem& p, void* work, s
     if ((e = split(!transB, nc, bsrc, p.ldb, mb, b8, ncp, sb, mxb)) != cudaSuccess) return e;
     if ((e = i8_gemm_batched((int)Mp, (int)ncp, (int)Kp, kMods, a8, b8, c32, s)) != cudaSuccess)
       return e;
-    const long long tot = (long long)M * nc;
+    const long long tot = (long long)((M + 3) / 4) * nc;
     crt_kernel<<<(unsigned)ceil_div(tot, 256), 256, 0, s>>>(M, nc, (int)Mp, c32, Mp * ncp, sa, sb,
                                                            p.alpha, p.beta, p.C, p.ldc, j0, p.mc,
                                                            p.ccol);

@@ -72,14 +72,16 @@ def test_real_n2048(dev, cfg):
     check_properties(op, pos, 2048)
 
 
-def test_clustered_cfg4_recipe(dev):
-    """cfg4 recipe (clusters of 1e-6 relative spread) at n = 1024."""
-    a, b, _ = configs.config_operator(4, n=1024)
+@pytest.mark.parametrize("n", [1024, 6144])
+def test_clustered_cfg4_recipe(dev, n):
+    """cfg4 recipe (256 clusters of 1e-6 relative spread): heavy D&C
+    deflation; n = 6144 runs the emulated-FP64 path (top merges, Q1, ...)."""
+    a, b, _ = configs.config_operator(4, n=n)
     op = bg.make_operator(a, b, kind="real")
     pos = bg.solve_real(op)
     lam_ref = lapack_lambda(a + b, a - b)
     assert np.max(np.abs(pos.lambda_plus - lam_ref) / lam_ref) <= 1e-10
-    check_properties(op, pos, 1024)
+    check_properties(op, pos, n)
 
 
 @pytest.mark.parametrize("n", [1, 2, 7, 64, 65, 1000, 2049])
