@@ -301,8 +301,13 @@ namespace {
 // as two masked split-K GEMMs (the triangular masks give row blocks very
 // different k-ranges; splitting K balances them and fills the GPU).
 cudaError_t symm_panel(const double* A2, long long lda, int m, int bw, const double* V,
-                       long long ldv, const Sy2sbScratch& w, cudaStream_t s) {
+                       long long ldv, const Sy2sbScratch& w, cudaStream_t s, bool full = false) {
   const int ssplit = (int)std::min<long long>(kSymmSplits, std::max<long long>(1, m / 1024));
+  if (full) {
+    // A2 holds both triangles (symmetrised once per pair): one unmasked product
+    GemmProblem g = make_gemm(m, bw, m, 1.0, A2, lda, V, ldv, 0.0, w.y, w.ldy);
+    return gemm_splitk(false, false, g, ssplit, w.symm_ws, w.probs, s);
+  }
   GemmProblem g1 = make_gemm(m, bw, m, 1.0, A2, lda, V, ldv, 0.0, w.y, w.ldy);
   g1.ma = Mask::lower();
   cudaError_t e = gemm_splitk(false, false, g1, ssplit, w.symm_ws, w.probs, s);
@@ -351,6 +356,11 @@ cudaError_t panel_w(int m, int bw, const double* V, long long ldv, const double*
 // sit b rows down so every slot shares the trailing row index.  Then
 // [V1 W1] [W1c V1c]^T, [W1c V1c]^T V2 and [V1 W1 V2 W2] [W1c V1c W2c V2c]^T
 // are single GEMMs.
+bool sy2sb_full_symm() {
+  static const bool off = std::getenv("BSE_SY2SB_TRI_SYMM") != nullptr;  // A/B timing switch
+  return !off;
+}
+
 cudaError_t sy2sb(double* A, long long lda, int n, int b, double* Vall, long long ldv,
                   double* Tall, const Sy2sbScratch& w, int num_sms, cudaStream_t s,
                   cudaStream_t la, cudaEvent_t ev_cols, cudaEvent_t ev_panel) {
@@ -386,7 +396,11 @@ cudaError_t sy2sb(double* A, long long lda, int n, int b, double* Vall, long lon
     }
     panel_ready = false;
     stage_mark("sy2sb_symm", s);
-    if ((e = symm_panel(A2, lda, m, bw, sV1, lw, w, s)) != cudaSuccess) return e;
+    // both SYMMs of the pair read the trailing matrix as it stands now (the
+    // second one on its stale sub-block A3): mirror its lower triangle once
+    const bool full = sy2sb_full_symm();
+    if (full && (e = symmetrize_from_lower(A2, lda, m, s)) != cudaSuccess) return e;
+    if ((e = symm_panel(A2, lda, m, bw, sV1, lw, w, s, full)) != cudaSuccess) return e;
     if ((e = panel_w(m, bw, sV1, lw, Tp1, sW1, lw, w, s)) != cudaSuccess) return e;
     if ((e = copy_cols(sW1c, sW1, m)) != cudaSuccess) return e;
     if ((e = copy_cols(sV1c, sV1, m)) != cudaSuccess) return e;
@@ -416,7 +430,7 @@ cudaError_t sy2sb(double* A, long long lda, int n, int b, double* Vall, long lon
                  Tp2, w.red, w.bar, num_sms, s);
     if (e != cudaSuccess) return e;
     stage_mark("sy2sb_symm", s);
-    if ((e = symm_panel(A3, lda, m2, bw, sV2 + b, lw, w, s)) != cudaSuccess) return e;
+    if ((e = symm_panel(A3, lda, m2, bw, sV2 + b, lw, w, s, full)) != cudaSuccess) return e;
     stage_mark("sy2sb_small", s);
     {
       // Y2 -= [V1' W1'] S,  S = [W1' V1']^T V2  (2b x b, split-K into z:z2)
