@@ -357,7 +357,12 @@ cudaError_t gemm_splitk(bool transA, bool transB, const GemmProblem& p, int spli
   count_launch();
   const bool v2 = aligned16(p.A) && aligned16(p.B) && ((p.lda | p.ldb) & 1) == 0;
   // (64 x 64 tiles: measured faster than 128 x 64 for the thin split-K SYMM)
-  cudaError_t e = gemm_grouped(transA, transB, probs_dev_scratch, splits, p.M, p.N, s, v2, 1);
+  static int cfg = -1;
+  if (cfg < 0) {
+    const char* v = std::getenv("BSE_SPLITK_CFG");  // tuning switch
+    cfg = v ? std::atoi(v) : 1;
+  }
+  cudaError_t e = gemm_grouped(transA, transB, probs_dev_scratch, splits, p.M, p.N, s, v2, cfg);
   if (e != cudaSuccess) return e;
   const long long tot = (long long)p.M * p.N;
   splitk_reduce_kernel<<<(unsigned)ceil_div(tot, 256), 256, 0, s>>>(ws, splits, p.M, p.N, p.alpha,
