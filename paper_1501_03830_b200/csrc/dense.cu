@@ -20,29 +20,40 @@ constexpr int kLds = kLeaf + 1;
 // a double-buffered shared vector (one barrier per column) and the
 // elimination runs unscaled (T_rc -= T_rj T_cj / T_jj; L_rc = T_rc / sqrt(T_cc)
 // at the end).  The leaf inverse (cached for every TRSM leaf of the solve) is
-// formed the same way by right-looking elimination of the identity.
+// formed in the same loop by elimination of the identity.
 constexpr int kHalf = kLeaf / 2;
 __global__ void __launch_bounds__(2 * kLeaf) potf2_kernel(double* A, long long lda, int n, int off,
                                                           DevStatus* st, double* inv) {
   extern __shared__ double dyn[];
   double* Ls = dyn;                    // row-major, Ls[i * kLds + k]
   __shared__ double colj[2][kLeaf];
+  __shared__ double rowj[2][kLeaf];    // row j of the unit-lower inverse
   __shared__ double dsq[kLeaf];
   if (st->info >= 0) return;           // an earlier block already failed
   const int r = threadIdx.x & (kLeaf - 1), h = threadIdx.x >> 6;
   const int cb = h * kHalf;            // this thread's columns: cb .. cb + 31
   double t[kHalf];
+  // Y = (L diag(L)^-1)^-1 by forward elimination of the identity, in the same
+  // column loop (row j of Y is final once column j is eliminated), so the
+  // leaf inverse costs no extra barriers: L^-1 = diag(1/L_rr) Y.
+  double y[kHalf];
 #pragma unroll
   for (int q = 0; q < kHalf; ++q) {
     const int c = cb + q;
     t[q] = (r < n && c < n && c <= r) ? A[r + c * lda] : 0.0;
+    y[q] = (c == r) ? 1.0 : 0.0;
   }
   for (int j = 0; j < n; ++j) {
     const int owner = j / kHalf;
     double* cj = colj[j & 1];
+    double* yj = rowj[j & 1];
     if (h == owner) {
       cj[r] = t[0];
       Ls[r * kLds + j] = t[0];
+    }
+    if (inv && r == j) {
+#pragma unroll
+      for (int q = 0; q < kHalf; ++q) yj[cb + q] = y[q];
     }
     __syncthreads();
     const double piv = cj[j];
@@ -51,6 +62,7 @@ __global__ void __launch_bounds__(2 * kLeaf) potf2_kernel(double* A, long long l
       return;
     }
     if (threadIdx.x == 0) dsq[j] = sqrt(piv);
+    // T_rj / T_jj = L_rj / L_jj
     const double a = (r > j) ? cj[r] * (1.0 / piv) : 0.0;
     // register q holds column base + q (base advances once per owned column)
     const int base = cb + (h == 0 ? j : max(0, j - kHalf));
@@ -58,6 +70,11 @@ __global__ void __launch_bounds__(2 * kLeaf) potf2_kernel(double* A, long long l
     for (int q = 0; q < kHalf; ++q) {
       const int c = base + q;
       if (c > j && c <= r && c < cb + kHalf) t[q] -= a * cj[c];
+    }
+    if (inv) {
+#pragma unroll
+      for (int q = 0; q < kHalf; ++q)
+        if (cb + q <= j) y[q] -= a * yj[cb + q];
     }
     if (h == owner) {
 #pragma unroll
@@ -74,29 +91,7 @@ __global__ void __launch_bounds__(2 * kLeaf) potf2_kernel(double* A, long long l
     if (i < n && c < n) A[i + c * lda] = l;
   }
   if (!inv) return;
-  __syncthreads();
-  for (int idx = threadIdx.x; idx < kLeaf * kLeaf; idx += blockDim.x) {
-    const int i = idx >> 6, c = idx & (kLeaf - 1);
-    if (i < n && c < n) Ls[i * kLds + c] = i > c ? Ls[i * kLds + c] / dsq[c] : (i == c ? dsq[c] : 0.0);
-  }
-  // Y = L^{-1}: rows kept unscaled, row j broadcast, Y_r -= (L_rj / L_jj) Y_j
-  double y[kHalf];
-#pragma unroll
-  for (int q = 0; q < kHalf; ++q) y[q] = (cb + q == r) ? 1.0 : 0.0;
-  __syncthreads();
-  for (int j = 0; j < n; ++j) {
-    double* yj = colj[j & 1];
-    if (r == j) {
-#pragma unroll
-      for (int q = 0; q < kHalf; ++q) yj[cb + q] = y[q];
-    }
-    __syncthreads();
-    const double a = (r > j) ? Ls[r * kLds + j] / Ls[j * kLds + j] : 0.0;
-#pragma unroll
-    for (int q = 0; q < kHalf; ++q)
-      if (cb + q <= j) y[q] -= a * yj[cb + q];
-  }
-  const double rd = (r < n) ? 1.0 / Ls[r * kLds + r] : 0.0;
+  const double rd = (r < n) ? 1.0 / dsq[r] : 0.0;
 #pragma unroll
   for (int q = 0; q < kHalf; ++q) {
     const int c = cb + q;
