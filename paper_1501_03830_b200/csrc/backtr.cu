@@ -439,6 +439,17 @@ size_t q1_tg_doubles(int n, int b, int group) {
   return std::max<size_t>(tot, 1);
 }
 
+size_t q1_vt_doubles(int n, int b, int group) {
+  const int np = q1_panels(n, b);
+  size_t tot = 0;
+  for (int pend = np; pend > 0; pend -= group) {
+    const int p0 = std::max(0, pend - group);
+    const size_t kb = (size_t)(pend - p0) * b, m = (size_t)(n - (p0 + 1) * b);
+    tot += m * kb;
+  }
+  return std::max<size_t>(tot, 1);
+}
+
 cudaError_t q1_build(int n, int b, const double* Vall, long long ldv, const double* Tall,
                      const Q1Scratch& w, cudaStream_t s) {
   // Panels are merged in groups of w.group (compact-WY of the product,
@@ -453,6 +464,7 @@ cudaError_t q1_build(int n, int b, const double* Vall, long long ldv, const doub
   const int np = q1_panels(n, b), G = w.group;
   cudaError_t e = cudaSuccess;
   double* Tg = w.tg;
+  double* VT = w.vt;
   for (int pend = np; pend > 0; pend -= G) {
     const int p0 = std::max(0, pend - G), k = pend - p0, kb = k * b;
     const int r0 = (p0 + 1) * b, m = n - r0;
@@ -488,6 +500,18 @@ cudaError_t q1_build(int n, int b, const double* Vall, long long ldv, const doub
         if ((e = gemm(false, false, g2, s)) != cudaSuccess) return e;
       }
     }
+    if (w.vt) {
+      // V T_g once per group here (off the critical path), so the apply is two
+      // products instead of three
+      GemmProblem gv = make_gemm(m, kb, kb, 1.0, V, ldv, Tg, kb, 0.0, VT, m);
+      gv.mb = Mask::upper();
+      if (w.oz_side && (double)m * kb * kb >= kOzMinWork)
+        e = ozgemm(false, false, gv, w.oz_side, w.oz_side_bytes, kQ1OzChunk, s);
+      else
+        e = gemm(false, false, gv, s);
+      if (e != cudaSuccess) return e;
+      VT += (size_t)m * kb;
+    }
     Tg += (size_t)kb * kb;
   }
   return e;
@@ -505,6 +529,7 @@ cudaError_t q1_apply(int n, int b, const double* Vall, long long ldv, double* Z,
     return gemm(ta, false, g, s);
   };
   const double* Tg = w.tg;
+  const double* VT = w.vt;
   for (int pend = np; pend > 0; pend -= G) {
     const int p0 = std::max(0, pend - G), k = pend - p0, kb = k * b;
     const int r0 = (p0 + 1) * b, m = n - r0;
@@ -513,13 +538,19 @@ cudaError_t q1_apply(int n, int b, const double* Vall, long long ldv, double* Z,
     // Y = V^T Zs (kb x ncols)
     GemmProblem g3 = make_gemm(kb, ncols, m, 1.0, V, ldv, Zs, ldz, 0.0, w.y, kb);
     if ((e = mul(true, g3)) != cudaSuccess) return e;
-    // Y2 = T_g Y
-    GemmProblem g4 = make_gemm(kb, ncols, kb, 1.0, Tg, kb, w.y, kb, 0.0, w.y2, kb);
-    g4.ma = Mask::upper();
-    if ((e = mul(false, g4)) != cudaSuccess) return e;
-    // Zs -= V Y2
-    GemmProblem g5 = make_gemm(m, ncols, kb, -1.0, V, ldv, w.y2, kb, 1.0, Zs, ldz);
-    if ((e = mul(false, g5)) != cudaSuccess) return e;
+    if (w.vt) {
+      // Zs -= (V T_g) Y
+      GemmProblem g5 = make_gemm(m, ncols, kb, -1.0, VT, m, w.y, kb, 1.0, Zs, ldz);
+      if ((e = mul(false, g5)) != cudaSuccess) return e;
+      VT += (size_t)m * kb;
+    } else {
+      // Y2 = T_g Y; Zs -= V Y2
+      GemmProblem g4 = make_gemm(kb, ncols, kb, 1.0, Tg, kb, w.y, kb, 0.0, w.y2, kb);
+      g4.ma = Mask::upper();
+      if ((e = mul(false, g4)) != cudaSuccess) return e;
+      GemmProblem g5 = make_gemm(m, ncols, kb, -1.0, V, ldv, w.y2, kb, 1.0, Zs, ldz);
+      if ((e = mul(false, g5)) != cudaSuccess) return e;
+    }
     Tg += (size_t)kb * kb;
   }
   return e;

@@ -60,6 +60,7 @@ constexpr int kQ1OzChunk = 2048;
 struct Q1Scratch {
   int group = kQ1Group;
   double* tg = nullptr;    // every group's T_g, back to back (q1_tg_doubles)
+  double* vt = nullptr;    // every group's V_g T_g (m_g x kb), back to back (q1_vt_doubles)
   double* x = nullptr;     // (G b) x (G b): V^T V of the group
   double* tmp = nullptr;   // (G b)^2 / 2
   double* y = nullptr;     // (G b) x ncols
@@ -73,6 +74,7 @@ struct Q1Scratch {
 };
 size_t q1_oz_bytes(int n, int b, int ncols, int group);
 size_t q1_tg_doubles(int n, int b, int group);
+size_t q1_vt_doubles(int n, int b, int group);
 // T_g of every panel group (may run on a side stream; own emulated workspace).
 cudaError_t q1_build(int n, int b, const double* Vall, long long ldv, const double* Tall,
                      const Q1Scratch& w, cudaStream_t s);

@@ -127,8 +127,11 @@ SyevdWork carve_syevd(Arena& a, int n, int flags) {
     w.dc.oz = w.q1.oz;
     w.dc.oz_bytes = w.q1.oz_bytes;
     const int kb = w.q1.group * b;
-    w.q1.oz_side_bytes = ozgemm_bytes(kb, kb, n, kQ1OzChunk);
+    // V^T V (kb x kb, K = m) and V T_g (m x kb, K = kb) of q1_build
+    w.q1.oz_side_bytes = std::max(ozgemm_bytes(kb, kb, n, kQ1OzChunk),
+                                  ozgemm_bytes(n, kb, kb, kQ1OzChunk));
     w.q1.oz_side = a.take<char>(w.q1.oz_side_bytes);
+    w.q1.vt = a.take<double>(q1_vt_doubles(n, b, w.q1.group));
   }
   return w;
 }
@@ -474,13 +477,24 @@ cudaError_t solve_spd_pair(int n, const double* M, long long ldm, const double* 
   const int nc_all = (int)(c1 - c0);
   if (nc_all > 0) {
     stage_mark("recover_trmm", s);
-    GemmProblem g4 = make_gemm(n, nc_all, n, 1.0, w.L, ld, w.Zr + c0 * ld, ld, 0.0, w.T1 + c0 * ld,
-                               ld);
-    g4.ma = Mask::lower();
     if (w.oz_bytes) {
-      if ((e = ozgemm(false, false, g4, w.oz, w.oz_bytes, kRecoverBlock, s)) != cudaSuccess) return e;
-    } else if ((e = gemm(false, false, g4, s)) != cudaSuccess) {
-      return e;
+      // row blocks: u[r0:r1, :] = L[r0:r1, 0:r1] Zr[0:r1, :] -- the emulated
+      // engine cannot skip L's zero triangle, so trim K per block (1.25 N^3
+      // executed instead of 2 N^3 with four blocks)
+      const int rb = (int)((ceil_div(n, 4) + 63) / 64 * 64);
+      for (int r0 = 0; r0 < n; r0 += rb) {
+        const int r1 = std::min(n, r0 + rb);
+        GemmProblem g4 = make_gemm(r1 - r0, nc_all, r1, 1.0, w.L + r0, ld, w.Zr + c0 * ld, ld, 0.0,
+                                   w.T1 + r0 + c0 * ld, ld);
+        g4.ma = Mask{kNoMaskLo, r0, 0};  // view-relative: L[r0 + i][k] for k <= r0 + i
+        if ((e = ozgemm(false, false, g4, w.oz, w.oz_bytes, kRecoverBlock, s)) != cudaSuccess)
+          return e;
+      }
+    } else {
+      GemmProblem g4 = make_gemm(n, nc_all, n, 1.0, w.L, ld, w.Zr + c0 * ld, ld, 0.0,
+                                 w.T1 + c0 * ld, ld);
+      g4.ma = Mask::lower();
+      if ((e = gemm(false, false, g4, s)) != cudaSuccess) return e;
     }
     stage_mark("recover_trsm", s);
     const bool host_rows = hout && world == 1;
