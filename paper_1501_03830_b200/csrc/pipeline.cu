@@ -171,14 +171,16 @@ cudaError_t syevd(int n, double* A, long long lda, double* w, double* Z, long lo
   // The Q2 blocks (from the bulge-chasing reflectors) and the Q1 group T
   // factors (from the SY2SB panels) do not depend on the divide and conquer:
   // they are built on a side stream while the latency-bound D&C runs.
-  static const bool serial = std::getenv("BSE_SERIAL_BUILDS") != nullptr;  // A/B timing switch
-  cudaStream_t sb = serial ? s : side.s;
-  if (serial) stage_mark("q_builds", s);
+  // A/B timing switch: 0 both builds on the side stream, 1 both serial before
+  // the D&C, 2 Q2 build on the side stream and the Q1 build after the D&C
+  static const int mode = std::getenv("BSE_BUILD_MODE") ? std::atoi(std::getenv("BSE_BUILD_MODE")) : 0;
+  cudaStream_t sb = mode == 1 ? s : side.s;
+  if (mode == 1) stage_mark("q_builds", s);
   if ((e = cudaEventRecord(side.fork, s)) != cudaSuccess) return e;
   if ((e = cudaStreamWaitEvent(sb, side.fork, 0)) != cudaSuccess) return e;
   if ((e = q2_build(n, b, kQ2Group, ws.V2, ws.tau2, ws.Vblk, sb)) != cudaSuccess)
     return e;
-  if ((e = q1_build(n, b, ws.Vall, ws.ldv, ws.Tall, ws.q1, sb)) != cudaSuccess) return e;
+  if (mode != 2 && (e = q1_build(n, b, ws.Vall, ws.ldv, ws.Tall, ws.q1, sb)) != cudaSuccess) return e;
   if ((e = cudaEventRecord(side.join, sb)) != cudaSuccess) return e;
   // the D&C chain of small latency-bound kernels runs on a high-priority
   // stream so the side stream's CTAs never delay its next launch
@@ -188,6 +190,10 @@ cudaError_t syevd(int n, double* A, long long lda, double* w, double* Z, long lo
   if ((e = stedc(n, ws.d, ws.e, w, Z, ldz, ws.dc, side.hp)) != cudaSuccess) return e;
   if ((e = cudaEventRecord(side.hp_join, side.hp)) != cudaSuccess) return e;
   if ((e = cudaStreamWaitEvent(s, side.hp_join, 0)) != cudaSuccess) return e;
+  if (mode == 2) {
+    stage_mark("q1_build", s);
+    if ((e = q1_build(n, b, ws.Vall, ws.ldv, ws.Tall, ws.q1, s)) != cudaSuccess) return e;
+  }
   stage_mark("q2_build_wait", s);
   if ((e = cudaStreamWaitEvent(s, side.join, 0)) != cudaSuccess) return e;
   if (zc1 < 0) zc1 = n;
