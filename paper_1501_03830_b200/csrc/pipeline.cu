@@ -477,7 +477,7 @@ cudaError_t solve_spd_pair(int n, const double* M, long long ldm, const double* 
     count_launch();
   }
   // u = L Zr (into T1), v = L^{-T} (Zr Lam) (in W).  With host outputs, v's
-  // rows finalise bottom-up inside the TRSM recursion: each quarter's rows of
+  // rows finalise bottom-up inside the TRSM recursion: each eighth of the rows of
   // X1, X2 are formed and their D2H copy overlaps the rest of the solve.
   std::vector<cudaEvent_t> evs;
   const int nc_all = (int)(c1 - c0);
@@ -506,7 +506,7 @@ cudaError_t solve_spd_pair(int n, const double* M, long long ldm, const double* 
     const bool host_rows = hout && world == 1;
     RowsOut ro{nc_all, w.T1 + c0 * ld, w.W + c0 * ld, ld, lam + c0, X1 + c0 * ldx1, ldx1,
                X2 + c0 * ldx2, ldx2, hout, &evs};
-    RowHook hk{rows_out_hook, &ro, 2, 0};
+    RowHook hk{rows_out_hook, &ro, 3, 0};  // eighths: the last D2H is rows [0, n/8)
     if ((e = trsm_llt(w.L, ld, n, w.W + c0 * ld, ld, nc_all, s, w.linv,
                       w.oz_trsm.p ? &w.oz_trsm : nullptr, host_rows ? &hk : nullptr)) != cudaSuccess)
       return e;
