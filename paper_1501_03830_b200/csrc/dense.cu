@@ -378,11 +378,26 @@ static cudaError_t potrf_rec(double* A, long long lda, int n, int off, DevStatus
   // columns [n1, n) are first touched here (the host entry streams them in)
   if (hook && (e = hook->fn(hook->ctx, s)) != cudaSuccess) return e;
   // A22 -= A21 A21^T (lower triangle only)
-  GemmProblem p = make_gemm(n2, n2, n1, -1.0, A + n1, lda, A + n1, lda, 1.0,
-                            A + n1 + n1 * lda, lda);
-  p.mc = Mask::lower();
-  e = update(false, true, p, oz, s);
-  if (e != cudaSuccess) return e;
+  double* A21 = A + n1;
+  double* A22 = A + n1 + n1 * lda;
+  if (oz && oz->p && (double)n2 * n2 * n1 >= 4.0 * kOzMinWork) {
+    // the emulated engine cannot skip the upper triangle: 2 x 2 output blocks
+    // (two lower-masked diagonal blocks + one full block) do 3/4 of the work
+    const int h = ((n2 / 2 + kLeaf - 1) / kLeaf) * kLeaf, h2 = n2 - h;
+    GemmProblem c11 = make_gemm(h, h, n1, -1.0, A21, lda, A21, lda, 1.0, A22, lda);
+    c11.mc = Mask::lower();
+    GemmProblem c21 = make_gemm(h2, h, n1, -1.0, A21 + h, lda, A21, lda, 1.0, A22 + h, lda);
+    GemmProblem c22 = make_gemm(h2, h2, n1, -1.0, A21 + h, lda, A21 + h, lda, 1.0,
+                                A22 + h + (long long)h * lda, lda);
+    c22.mc = Mask::lower();
+    if ((e = update(false, true, c11, oz, s)) != cudaSuccess) return e;
+    if ((e = update(false, true, c21, oz, s)) != cudaSuccess) return e;
+    if ((e = update(false, true, c22, oz, s)) != cudaSuccess) return e;
+  } else {
+    GemmProblem p = make_gemm(n2, n2, n1, -1.0, A21, lda, A21, lda, 1.0, A22, lda);
+    p.mc = Mask::lower();
+    if ((e = update(false, true, p, oz, s)) != cudaSuccess) return e;
+  }
   return potrf_rec(A + n1 + n1 * lda, lda, n2, off + n1, st, s,
                    inv ? inv + (size_t)(n1 / kLeaf) * kLeaf * kLeaf : nullptr, oz);
 }
