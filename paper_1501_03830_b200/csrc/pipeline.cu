@@ -480,6 +480,12 @@ cudaError_t solve_spd_pair(int n, const double* M, long long ldm, const double* 
   // rows finalise bottom-up inside the TRSM recursion: each eighth of the rows of
   // X1, X2 are formed and their D2H copy overlaps the rest of the solve.
   std::vector<cudaEvent_t> evs;
+  // destroyed on every exit path (the copies they gate are on hout->stream;
+  // destroying a recorded event is safe)
+  struct EvGuard {
+    std::vector<cudaEvent_t>& v;
+    ~EvGuard() { for (auto ev : v) cudaEventDestroy(ev); }
+  } guard{evs};
   const int nc_all = (int)(c1 - c0);
   if (nc_all > 0) {
     stage_mark("recover_trmm", s);
@@ -532,10 +538,7 @@ cudaError_t solve_spd_pair(int n, const double* M, long long ldm, const double* 
   if ((e = cudaGetLastError()) != cudaSuccess) return e;
   // status
   DevStatus hs[2];
-  struct EvGuard {
-    std::vector<cudaEvent_t>& v;
-    ~EvGuard() { for (auto ev : v) cudaEventDestroy(ev); }
-  } guard{evs};
+
   if ((e = cudaMemcpyAsync(hs, w.st, sizeof(hs), cudaMemcpyDeviceToHost, s)) != cudaSuccess) return e;
   if ((e = cudaStreamSynchronize(s)) != cudaSuccess) return e;
   if (hs[0].info >= 0 || hs[1].conv_fail) {
