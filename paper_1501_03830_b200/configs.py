@@ -144,6 +144,12 @@ def torch_real_operator(n, seed=2, spectrum="loguniform", lo=0.1, hi=100.0, devi
             return lo + (hi - lo) * u
         if spectrum == "loguniform":
             return torch.exp(np.log(lo) + (np.log(hi) - np.log(lo)) * u)
+        if spectrum == "clustered":  # cfg4 recipe: 256 clusters, 1e-6 relative spread
+            per = max(1, n // 256)
+            nc = -(-n // per)
+            centres = lo + (hi - lo) * torch.rand(nc, dtype=torch.float64, device=device, generator=g)
+            vals = centres.repeat_interleave(per)[:n]
+            return vals * (1.0 + 1e-6 * (2.0 * u - 1.0))
         raise ValueError(spectrum)
 
     u1 = haar()

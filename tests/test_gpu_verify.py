@@ -80,3 +80,27 @@ def test_cfg2_full_size_properties(dev):
     l2 = lam.double() ** 2
     assert abs(torch.sum(l2).item() - m2) <= 1e-12 * n * m2
     assert abs(torch.sum(l2 * l2).item() - m4) <= 1e-12 * n * m4
+
+
+def test_cfg4_recipe_n16384_properties(dev):
+    """BASELINE config 4's clustered spectrum (256 clusters, 1e-6 relative
+    spread: heavy D&C deflation, near-degenerate eigenvectors) at n = 16384
+    on one GPU: positivity/order, per-pair residual and biorthogonality
+    gates, and the spectral moments tr(MK), tr((MK)^2)."""
+    import torch
+    n = 16384
+    S, D, _ = configs.torch_real_operator(n, seed=4, spectrum="clustered", lo=1.0, hi=10.0,
+                                          device=dev)
+    lam, X1, X2, ld = bg.solve_pair_device(S, n, D, n, n)
+    lam_h = lam.cpu().numpy()
+    assert np.all(lam_h > 0) and np.all(np.diff(lam_h) <= 0)
+    res, xn, bio = bg.pair_residuals_device(n, S, n, D, n, lam, X1, ld, X2, ld)
+    ratio = (res / (lam[0] * xn)).max().item()
+    assert ratio <= 1e-13 * n, ratio
+    assert bio.item() <= 1e-12 * n, bio.item()
+    G = S @ D
+    m2 = torch.sum(S * D).item()
+    m4 = torch.sum(G * G.T).item()
+    l2 = lam.double() ** 2
+    assert abs(torch.sum(l2).item() - m2) <= 1e-12 * n * m2
+    assert abs(torch.sum(l2 * l2).item() - m4) <= 1e-12 * n * m4
