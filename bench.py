@@ -431,7 +431,7 @@ def run_ours(args):
                    "n": n,
                    "parallelism": (f"column-sharded x{world} (NCCL; reduction + D&C replicated)"
                                    if world > 1 else "single GPU"),
-                   "l2": "inputs 2 GB each > 126 MB L2 (no flush needed)"},
+                   "l2": f"inputs {n * n * 8 / 2**30:.0f} GiB each > 126 MB L2 (no flush needed)"},
         "tflops": alg_flops(n) / solve_s / 1e12,
         "fp64_peak_tflops": fp64_peak,
         "frac_of_fp64_peak": alg_flops(n) / solve_s / 1e12 / fp64_peak,
