@@ -45,7 +45,12 @@ def to_device_colmajor(a: np.ndarray, device, ld: int | None = None):
     rows, cols = a.shape
     t, ld = colmajor_empty(rows, cols, device, ld, zero=True)
     if rows and cols:
-        t[:cols, :rows].copy_(torch.from_numpy(np.ascontiguousarray(a.T)))
+        # upload as stored, transpose on the device (a host transpose of a
+        # multi-GB array costs seconds)
+        src = np.ascontiguousarray(a)
+        if not src.flags.writeable:
+            src = src.copy()
+        t[:cols, :rows].copy_(torch.from_numpy(src).to(t.device).T)
     return t, ld
 
 

@@ -103,6 +103,38 @@ def real_embedding(op: BseOperator):
     return 0.5 * (m + m.T), 0.5 * (k + k.T)
 
 
+def _real_embedding_device(op: BseOperator, dev):
+    """real_embedding() formed on the device from one upload of A and B:
+    the same IEEE operations as the host version (bitwise equal), without
+    host-side block assembly and transposes of 2n x 2n arrays.  M', K' are
+    exactly symmetric, so their row-major tensors are their column-major
+    buffers."""
+    torch = require_cuda()
+    n = op.n
+    N = 2 * n
+
+    def up(x):
+        x = np.asarray(x)
+        return torch.from_numpy(x if x.flags.writeable else x.copy()).to(dev)
+
+    A, B = up(op.a), up(op.b)
+    ar, ai, br, bi = A.real, A.imag, B.real, B.imag
+    out = []
+    for sgn in (1.0, -1.0):  # M' = A' + B', K' = A' - B'
+        T = torch.empty((N, N), dtype=torch.float64, device=dev)
+        T[:n, :n] = ar + sgn * br
+        T[:n, n:] = -ai + sgn * bi
+        T[n:, :n] = ai + sgn * bi
+        T[n:, n:] = ar - sgn * br
+        T = 0.5 * (T + T.T)
+        buf, ld = colmajor_empty(N, N, dev)
+        buf[:N, :N].copy_(T)
+        del T
+        out.append((buf, ld))
+    del A, B
+    return out
+
+
 def _select_and_polish(lam2, X1, X2, ld, n, dev):
     """Complex eigenvectors from the doubled real spectrum of the 2n-embedding.
 
@@ -305,10 +337,8 @@ def solve_complex(op: BseOperator, workers: int = 1) -> PositiveEigensystem:
         return PositiveEigensystem(lambda_plus=lam_h, x1=x1.astype(np.complex128),
                                    x2=x2.astype(np.complex128),
                                    warnings=conditioning_warnings(lam_h))
-    m, k = real_embedding(op)
     N = 2 * n
-    Mt, ldm = to_device_colmajor(m, dev)
-    Kt, ldk = to_device_colmajor(k, dev)
+    (Mt, ldm), (Kt, ldk) = _real_embedding_device(op, dev)
     try:
         lam2, X1, X2, ld = solve_pair_device(Mt, ldm, Kt, ldk, N)
     except NotPositiveDefinite as err:
