@@ -127,8 +127,8 @@ constexpr int kQ2LDN = 64 + 8;     // prefetched rows, [col * LDN + row]
 
 BSE_DEV double2 lds2(const double* p) { return *reinterpret_cast<const double2*>(p); }
 
-template <int OFF, int NT>
-BSE_DEV void q2_block_t(double (&acc)[NT][2], const double* sV, const double* sVT, int lane) {
+template <int OFF, int NT, int CG>
+BSE_DEV void q2_block_t(double (&acc)[CG][NT][2], const double* sV, const double* sVT, int lane) {
   const int kl = lane & 3, rl = lane >> 2;
   // swizzle: this lane's line (column c = 8q + rl of V, row 8i + rl of VT)
   // has parity rl & 1, so 16-byte unit u moves to u ^ 4 on odd lines; with u
@@ -138,9 +138,12 @@ BSE_DEV void q2_block_t(double (&acc)[NT][2], const double* sV, const double* sV
   const double* pV1 = sV + rl * kQ2LDV + 2 * kl - sw;   // odd tile
   const double* pT0 = sVT + rl * kQ2LDT + 2 * kl + sw;
   const double* pT1 = sVT + rl * kQ2LDT + 2 * kl - sw;
-  double yt[4][2];
+  // CG groups of 8 columns share every V / VT fragment load
+  double yt[CG][4][2];
 #pragma unroll
-  for (int q = 0; q < 4; ++q) yt[q][0] = yt[q][1] = 0.0;
+  for (int g = 0; g < CG; ++g)
+#pragma unroll
+    for (int q = 0; q < 4; ++q) yt[g][q][0] = yt[g][q][1] = 0.0;
   // Y^T (8 cols x 32 reflectors): reflector tile q meets row tiles q .. q+8
 #pragma unroll
   for (int i = 0; i < 12; ++i) {
@@ -149,14 +152,20 @@ BSE_DEV void q2_block_t(double (&acc)[NT][2], const double* sV, const double* sV
     for (int q = 0; q < 4; ++q)
       if (i >= q && i <= q + 8) bv[q] = lds2((i & 1 ? pV1 : pV0) + 8 * q * kQ2LDV + 8 * i);
 #pragma unroll
-    for (int q = 0; q < 4; ++q)
-      if (i >= q && i <= q + 8) dmma8x8x4(yt[q], acc[OFF + i][0], bv[q].x);
+    for (int g = 0; g < CG; ++g)
 #pragma unroll
-    for (int q = 0; q < 4; ++q)
-      if (i >= q && i <= q + 8) dmma8x8x4(yt[q], acc[OFF + i][1], bv[q].y);
+      for (int q = 0; q < 4; ++q)
+        if (i >= q && i <= q + 8) dmma8x8x4(yt[g][q], acc[g][OFF + i][0], bv[q].x);
+#pragma unroll
+    for (int g = 0; g < CG; ++g)
+#pragma unroll
+      for (int q = 0; q < 4; ++q)
+        if (i >= q && i <= q + 8) dmma8x8x4(yt[g][q], acc[g][OFF + i][1], bv[q].y);
   }
 #pragma unroll
-  for (int q = 0; q < 4; ++q) { yt[q][0] = -yt[q][0]; yt[q][1] = -yt[q][1]; }
+  for (int g = 0; g < CG; ++g)
+#pragma unroll
+    for (int q = 0; q < 4; ++q) { yt[g][q][0] = -yt[g][q][0]; yt[g][q][1] = -yt[g][q][1]; }
   // Z^T -= Y^T VT^T: VT[r][c] = 0 for c < r - 63 (row tile i needs q >= i - 8)
 #pragma unroll
   for (int q = 0; q < 4; ++q) {
@@ -167,11 +176,15 @@ BSE_DEV void q2_block_t(double (&acc)[NT][2], const double* sV, const double* sV
       for (int i = h; i < h + 6; ++i)
         if (q >= i - 8) bv[i - h] = lds2((q & 1 ? pT1 : pT0) + 8 * i * kQ2LDT + 8 * q);
 #pragma unroll
-      for (int i = h; i < h + 6; ++i)
-        if (q >= i - 8) dmma8x8x4(acc[OFF + i], yt[q][0], bv[i - h].x);
+      for (int g = 0; g < CG; ++g)
 #pragma unroll
-      for (int i = h; i < h + 6; ++i)
-        if (q >= i - 8) dmma8x8x4(acc[OFF + i], yt[q][1], bv[i - h].y);
+        for (int i = h; i < h + 6; ++i)
+          if (q >= i - 8) dmma8x8x4(acc[g][OFF + i], yt[g][q][0], bv[i - h].x);
+#pragma unroll
+      for (int g = 0; g < CG; ++g)
+#pragma unroll
+        for (int i = h; i < h + 6; ++i)
+          if (q >= i - 8) dmma8x8x4(acc[g][OFF + i], yt[g][q][1], bv[i - h].y);
     }
   }
 }
@@ -190,7 +203,7 @@ BSE_DEV void q2_block_t(double (&acc)[NT][2], const double* sV, const double* sV
 // (empty barrier, one arrival per warp); consumer warps wait only on the
 // stage's full barrier.  No CTA-wide barrier in the loop: warps may drift up
 // to one block apart.
-template <int P, int NW>
+template <int P, int NW, int CG>
 __global__ void __launch_bounds__(32 * (NW + 1), 1) q2_apply_pair_kernel(
     int n, int b, int maxsteps, const double* __restrict__ Vblk, double* __restrict__ Z,
     long long ldz, int ncols) {
@@ -202,13 +215,13 @@ __global__ void __launch_bounds__(32 * (NW + 1), 1) q2_apply_pair_kernel(
   extern __shared__ __align__(16) double sm[];
   constexpr int NS = kQ2Stages;
   double* sZn = sm + NS * STAGE;
-  unsigned long long* bars = reinterpret_cast<unsigned long long*>(sZn + 8 * NW * LDN);
+  unsigned long long* bars = reinterpret_cast<unsigned long long*>(sZn + 8 * CG * NW * LDN);
   unsigned long long* full = bars;        // [NS]
   unsigned long long* empty = bars + NS;  // [NS]
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int kl = lane & 3, rl = lane >> 2;
-  constexpr int kQ2W = 8 * NW;
-  const int cw = blockIdx.x * kQ2W + warp * 8;
+  constexpr int kQ2W = 8 * CG * NW;           // columns per CTA
+  const int cw = blockIdx.x * kQ2W + warp * 8 * CG;  // this warp's first column
   const int nsweeps = n - 2;
   const int ngroups = (int)ceil_div(nsweeps, G);
 
@@ -262,14 +275,19 @@ __global__ void __launch_bounds__(32 * (NW + 1), 1) q2_apply_pair_kernel(
     }
     return;
   }
-  // this lane's column of Z (rows added per access)
-  const bool colok = cw + rl < ncols;
-  double* const zc = Z + (long long)(colok ? cw + rl : 0) * ldz;
+  // this lane's columns of Z (one per group of 8; rows added per access)
+  bool colok[CG];
+  double* zc[CG];
+#pragma unroll
+  for (int g = 0; g < CG; ++g) {
+    colok[g] = cw + 8 * g + rl < ncols;
+    zc[g] = Z + (long long)(colok[g] ? cw + 8 * g + rl : 0) * ldz;
+  }
   // row prefetch: every warp streams in its own 8 columns (lane l: rows l
   // and l + 32 of each column, so every copy instruction moves 256
   // contiguous bytes), and only a warp-level sync guards sZn
 
-  double acc[NT][2];
+  double acc[CG][NT][2];
   int ga = ngroups - 1, j = 0, wh = 0, stage = 0;
   unsigned use = 0;  // fills of `stage` consumed so far
   bool pair_start = true;
@@ -281,12 +299,14 @@ __global__ void __launch_bounds__(32 * (NW + 1), 1) q2_apply_pair_kernel(
     const bool pair_end = !more || nga != ga;
     if (pair_start) {
 #pragma unroll
-      for (int i = 0; i < NT; ++i)
+      for (int g = 0; g < CG; ++g)
 #pragma unroll
-        for (int e = 0; e < 2; ++e) {
-          const int row = B0 + 8 * i + 2 * kl + e;
-          acc[i][e] = (colok && row >= 0 && row < n) ? __ldcg(zc + row) : 0.0;
-        }
+        for (int i = 0; i < NT; ++i)
+#pragma unroll
+          for (int e = 0; e < 2; ++e) {
+            const int row = B0 + 8 * i + 2 * kl + e;
+            acc[g][i][e] = (colok[g] && row >= 0 && row < n) ? __ldcg(zc[g] + row) : 0.0;
+          }
       pair_start = false;
     }
     // this block's V/VT have landed
@@ -298,11 +318,11 @@ __global__ void __launch_bounds__(32 * (NW + 1), 1) q2_apply_pair_kernel(
     if (step_first && j + 1 < smax_of(ga)) {
       const int row0 = B0 + 64 * j + 8 * NT;
 #pragma unroll
-      for (int c = 0; c < 8; ++c) {
+      for (int c = 0; c < 8 * CG; ++c) {
         const int col = cw + c;
         const bool cok = col < ncols;
         const double* src = Z + (long long)(cok ? col : 0) * ldz;
-        double* dst = sZn + (warp * 8 + c) * LDN;
+        double* dst = sZn + (warp * 8 * CG + c) * LDN;
 #pragma unroll
         for (int h = 0; h < 2; ++h) {
           const int row = row0 + lane + 32 * h;
@@ -315,10 +335,10 @@ __global__ void __launch_bounds__(32 * (NW + 1), 1) q2_apply_pair_kernel(
     const double* sV = sm + stage * STAGE;
     const double* sVT = sV + G * kQ2LDV;
     // group ga - wh's block sits 32 (P - 1 - wh) rows into the window
-    if (P == 1 || wh == 0) q2_block_t<4 * (P - 1), NT>(acc, sV, sVT, lane);
-    else if (P == 2 || wh == 1) q2_block_t<4 * (P > 1 ? P - 2 : 0), NT>(acc, sV, sVT, lane);
-    else if (P == 3 || wh == 2) q2_block_t<4 * (P > 2 ? P - 3 : 0), NT>(acc, sV, sVT, lane);
-    else q2_block_t<4 * (P > 3 ? P - 4 : 0), NT>(acc, sV, sVT, lane);
+    if (P == 1 || wh == 0) q2_block_t<4 * (P - 1), NT, CG>(acc, sV, sVT, lane);
+    else if (P == 2 || wh == 1) q2_block_t<4 * (P > 1 ? P - 2 : 0), NT, CG>(acc, sV, sVT, lane);
+    else if (P == 3 || wh == 2) q2_block_t<4 * (P > 2 ? P - 3 : 0), NT, CG>(acc, sV, sVT, lane);
+    else q2_block_t<4 * (P > 3 ? P - 4 : 0), NT, CG>(acc, sV, sVT, lane);
     // this warp is done with the stage
     __syncwarp();
     if (lane == 0) mbar_arrive(&empty[stage]);
@@ -326,27 +346,35 @@ __global__ void __launch_bounds__(32 * (NW + 1), 1) q2_apply_pair_kernel(
       const int nstore = pair_end ? NT : 8;
       const int rbase = B0 + 64 * j;
 #pragma unroll
-      for (int i = 0; i < NT; ++i) {
-        if (i < nstore) {
+      for (int g = 0; g < CG; ++g)
 #pragma unroll
-          for (int e = 0; e < 2; ++e) {
-            const int row = rbase + 8 * i + 2 * kl + e;
-            if (colok && row >= 0 && row < n) zc[row] = acc[i][e];
+        for (int i = 0; i < NT; ++i) {
+          if (i < nstore) {
+#pragma unroll
+            for (int e = 0; e < 2; ++e) {
+              const int row = rbase + 8 * i + 2 * kl + e;
+              if (colok[g] && row >= 0 && row < n) zc[g][row] = acc[g][i][e];
+            }
           }
         }
-      }
       if (!pair_end) {
         // the rows were streamed in by this warp only
         cp_async_wait<0>();
         __syncwarp();
-        const int cl = warp * 8;
 #pragma unroll
-        for (int i = 0; i < NT - 8; ++i) { acc[i][0] = acc[8 + i][0]; acc[i][1] = acc[8 + i][1]; }
+        for (int g = 0; g < CG; ++g) {
+          const int cl = warp * 8 * CG + 8 * g;
 #pragma unroll
-        for (int i = 0; i < 8; ++i) {
-          const double2 z = lds2(sZn + (cl + rl) * LDN + 8 * i + 2 * kl);
-          acc[NT - 8 + i][0] = z.x;
-          acc[NT - 8 + i][1] = z.y;
+          for (int i = 0; i < NT - 8; ++i) {
+            acc[g][i][0] = acc[g][8 + i][0];
+            acc[g][i][1] = acc[g][8 + i][1];
+          }
+#pragma unroll
+          for (int i = 0; i < 8; ++i) {
+            const double2 z = lds2(sZn + (cl + rl) * LDN + 8 * i + 2 * kl);
+            acc[g][NT - 8 + i][0] = z.x;
+            acc[g][NT - 8 + i][1] = z.y;
+          }
         }
       } else {
         // the next pair's row prefetches (other lanes) read rows stored here
@@ -395,21 +423,24 @@ cudaError_t q2_apply(int n, int b, int g, const double* Vblk, double* Z, long lo
   if (b != 64 || g != kQ2G || q2_hb(b, g) != kQ2HB) return cudaErrorInvalidValue;
   const int maxsteps = sb2st_maxsteps(n, b);
   const int sms = device_sm_count();
-  auto launch = [&](auto kern, int nw) {
-    const size_t smem =
-        sizeof(double) * (kQ2Stages * (size_t)kQ2Stage + (size_t)8 * nw * kQ2LDN) +
-        2 * kQ2Stages * sizeof(unsigned long long);
+  auto launch = [&](auto kern, int nw, int cg) {
+    const size_t smem = sizeof(double) * (kQ2Stages * (size_t)kQ2Stage +
+                                          (size_t)8 * cg * nw * kQ2LDN) +
+                        2 * kQ2Stages * sizeof(unsigned long long);
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    kern<<<(unsigned)ceil_div(ncols, 8 * nw), 32 * (nw + 1), smem, s>>>(n, b, maxsteps, Vblk, Z,
-                                                                       ldz, ncols);
+    kern<<<(unsigned)ceil_div(ncols, 8 * cg * nw), 32 * (nw + 1), smem, s>>>(n, b, maxsteps, Vblk,
+                                                                            Z, ldz, ncols);
     count_launch();
     return cudaGetLastError();
   };
   auto enough = [&](int nw) { return 4 * ceil_div(ncols, 8 * nw) >= 3 * (long long)sms; };
-  if (enough(kQ2MaxWarps)) return launch(q2_apply_pair_kernel<2, kQ2MaxWarps>, kQ2MaxWarps);
-  if (enough(8)) return launch(q2_apply_pair_kernel<2, 8>, 8);
-  if (enough(4)) return launch(q2_apply_pair_kernel<2, 4>, 4);
-  return launch(q2_apply_pair_kernel<2, 2>, 2);
+  static const int cg2 = std::getenv("BSE_Q2_CG") ? std::atoi(std::getenv("BSE_Q2_CG")) : 1;
+  if (cg2 == 2 && enough(kQ2MaxWarps))
+    return launch(q2_apply_pair_kernel<2, kQ2MaxWarps / 2, 2>, kQ2MaxWarps / 2, 2);
+  if (enough(kQ2MaxWarps)) return launch(q2_apply_pair_kernel<2, kQ2MaxWarps, 1>, kQ2MaxWarps, 1);
+  if (enough(8)) return launch(q2_apply_pair_kernel<2, 8, 1>, 8, 1);
+  if (enough(4)) return launch(q2_apply_pair_kernel<2, 4, 1>, 4, 1);
+  return launch(q2_apply_pair_kernel<2, 2, 1>, 2, 1);
 }
 
 size_t q1_oz_bytes(int n, int b, int ncols, int group) {
