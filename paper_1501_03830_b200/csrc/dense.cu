@@ -209,21 +209,25 @@ __global__ void zero_upper_kernel(double* A, long long lda, int n) {
 }
 
 __global__ void symmetrize_kernel(double* A, long long lda, int n) {
-  // tile transpose of the lower triangle into the upper one
+  // tile transpose of the lower triangle into the upper one; one CTA per
+  // lower tile (bi >= bj), linear index k = bi (bi + 1) / 2 + bj
   __shared__ double t[32][33];
-  const int bi = blockIdx.x, bj = blockIdx.y;  // tile (row block bi, col block bj), want bi > bj or ==
-  if (bi < bj) return;
+  const long long k = blockIdx.x;
+  int bi = (int)((sqrt(8.0 * (double)k + 1.0) - 1.0) * 0.5);
+  while ((long long)(bi + 1) * (bi + 2) / 2 <= k) ++bi;
+  while ((long long)bi * (bi + 1) / 2 > k) --bi;
+  const int bj = (int)(k - (long long)bi * (bi + 1) / 2);
   const int tx = threadIdx.x, ty = threadIdx.y;  // 32 x 8
-  for (int k = ty; k < 32; k += 8) {
-    const int r = bi * 32 + tx, c = bj * 32 + k;
-    t[k][tx] = (r < n && c < n) ? A[r + (long long)c * lda] : 0.0;
+  for (int q = ty; q < 32; q += 8) {
+    const int r = bi * 32 + tx, c = bj * 32 + q;
+    t[q][tx] = (r < n && c < n) ? A[r + (long long)c * lda] : 0.0;
   }
   __syncthreads();
   // write A[c][r] = A[r][c] for r > c
-  for (int k = ty; k < 32; k += 8) {
+  for (int q = ty; q < 32; q += 8) {
     const int rr = bj * 32 + tx;  // destination row (= source col)
-    const int cc = bi * 32 + k;   // destination col (= source row)
-    if (rr < n && cc < n && cc > rr) A[rr + (long long)cc * lda] = t[tx][k];
+    const int cc = bi * 32 + q;   // destination col (= source row)
+    if (rr < n && cc < n && cc > rr) A[rr + (long long)cc * lda] = t[tx][q];
   }
 }
 
@@ -425,7 +429,7 @@ cudaError_t zero_strict_upper(double* A, long long lda, int n, cudaStream_t s) {
 cudaError_t symmetrize_from_lower(double* A, long long lda, int n, cudaStream_t s) {
   if (n <= 0) return cudaSuccess;
   const unsigned t = (unsigned)ceil_div(n, 32);
-  symmetrize_kernel<<<dim3(t, t), dim3(32, 8), 0, s>>>(A, lda, n);
+  symmetrize_kernel<<<(unsigned)((long long)t * (t + 1) / 2), dim3(32, 8), 0, s>>>(A, lda, n);
   count_launch();
   return cudaGetLastError();
 }
