@@ -186,21 +186,25 @@ int bse_solve_spd_pair_host(int64_t n, const double* M, int64_t ldm, const doubl
   void* dW = buf + 4 * mat + lam_bytes;
   bse::SolveStatus st{};
   const size_t row = sizeof(double) * (size_t)n;
-  // K's first column half first (the Cholesky starts on it as soon as it
-  // lands), then its second half and M on a second stream: the copies share
-  // the host link in that order, overlapping the factorization; joined
-  // before the first trailing update and before the congruence.
-  const int n1 = bse::potrf_top_split((int)n);
-  e = cudaMemcpy2DAsync(dK, ld * 8, K, ldk * 8, row, n1, cudaMemcpyHostToDevice, s);
-  cudaEvent_t evAlloc, evK2;
+  // K by column pieces (the Cholesky starts on piece 0 as soon as it lands
+  // and waits for each later piece just before first reading it), then M, on
+  // a second stream after piece 0: the copies share the host link in that
+  // order, overlapping the factorization; M is joined before the congruence.
+  bse::KPieces kp{};
+  bse::kpieces_plan((int)n, 2, &kp);
+  e = cudaMemcpy2DAsync(dK, ld * 8, K, ldk * 8, row, kp.c1[0], cudaMemcpyHostToDevice, s);
+  cudaEvent_t evAlloc;
   cudaEventCreateWithFlags(&evAlloc, cudaEventDisableTiming);
-  cudaEventCreateWithFlags(&evK2, cudaEventDisableTiming);
   cudaEventRecord(evAlloc, s);
   cudaStreamWaitEvent(s2, evAlloc, 0);
-  if (e == cudaSuccess && n1 < n)
-    e = cudaMemcpy2DAsync(dK + (long long)n1 * ld, ld * 8, K + (long long)n1 * ldk, ldk * 8, row,
-                          n - n1, cudaMemcpyHostToDevice, s2);
-  if (e == cudaSuccess) e = cudaEventRecord(evK2, s2);
+  for (int L = 1; L <= kp.depth; ++L) {
+    cudaEventCreateWithFlags(&kp.ready[L], cudaEventDisableTiming);
+    const int c0 = kp.c0[L], c1 = kp.c1[L];
+    if (e == cudaSuccess && c1 > c0)
+      e = cudaMemcpy2DAsync(dK + (long long)c0 * ld, ld * 8, K + (long long)c0 * ldk, ldk * 8, row,
+                            c1 - c0, cudaMemcpyHostToDevice, s2);
+    if (e == cudaSuccess) e = cudaEventRecord(kp.ready[L], s2);
+  }
   if (e == cudaSuccess)
     e = cudaMemcpy2DAsync(dM, ld * 8, M, ldm * 8, row, n, cudaMemcpyHostToDevice, s2);
   if (e == cudaSuccess) e = cudaEventRecord(evM, s2);
@@ -208,7 +212,7 @@ int bse_solve_spd_pair_host(int64_t n, const double* M, int64_t ldm, const doubl
   bse::HostOut hout{X1, ldx1, X2, ldx2, lam, s2};
   if (e == cudaSuccess)
     e = bse::solve_spd_pair((int)n, dM, ld, dK, ld, dLam, dX1, ld, dX2, ld, dW, wb, flags, s, &st,
-                            evM, &hout, nullptr, evK2);
+                            evM, &hout, nullptr, &kp);
   cudaEvent_t evDone;
   cudaEventCreateWithFlags(&evDone, cudaEventDisableTiming);
   cudaEventRecord(evDone, s2);
@@ -220,7 +224,8 @@ int bse_solve_spd_pair_host(int64_t n, const double* M, int64_t ldm, const doubl
   cudaStreamDestroy(s2);
   cudaEventDestroy(evM);
   cudaEventDestroy(evAlloc);
-  cudaEventDestroy(evK2);
+  for (int L = 1; L <= kp.depth; ++L)
+    if (kp.ready[L]) cudaEventDestroy(kp.ready[L]);
   BSE_TRY_CUDA(e, "solve_host");
   BSE_TRY_CUDA(e2, "solve_host sync");
   return map_solve_status(st, info);

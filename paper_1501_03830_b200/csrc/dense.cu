@@ -368,19 +368,31 @@ int potrf_top_split(int n) { return n <= kLeaf ? n : split_point(n); }
 static cudaError_t potrf_rec(double* A, long long lda, int n, int off, DevStatus* st,
                              cudaStream_t s, double* inv, const OzWork* oz,
                              const PotrfHook* hook = nullptr) {
+  cudaError_t e;
   if (n <= kLeaf) {
+    // a leaf still owing pieces: deliver them (in column order) first
+    for (int L = 1; hook && L <= hook->depth; ++L)
+      if ((e = hook->fn(hook->ctx, L, s)) != cudaSuccess) return e;
     ensure_smem<potf2_kernel>();
     potf2_kernel<<<1, 2 * kLeaf, kLeafSmem, s>>>(A, lda, n, off, st, inv);
     count_launch();
     return cudaGetLastError();
   }
   const int n1 = split_point(n), n2 = n - n1;
-  cudaError_t e = potrf_rec(A, lda, n1, off, st, s, inv, oz);
+  // the top-left recursion owes the pieces below this level's
+  PotrfHook inner{};
+  const PotrfHook* ih = nullptr;
+  if (hook && hook->depth > 1) {
+    inner = *hook;
+    inner.depth -= 1;
+    ih = &inner;
+  }
+  e = potrf_rec(A, lda, n1, off, st, s, inv, oz, ih);
   if (e != cudaSuccess) return e;
   e = trsm_rlt(A, lda, n1, A + n1, lda, n2, s, inv, oz);  // A21 <- A21 L11^{-T}
   if (e != cudaSuccess) return e;
   // columns [n1, n) are first touched here (the host entry streams them in)
-  if (hook && (e = hook->fn(hook->ctx, s)) != cudaSuccess) return e;
+  if (hook && (e = hook->fn(hook->ctx, hook->depth, s)) != cudaSuccess) return e;
   // A22 -= A21 A21^T (lower triangle only)
   double* A21 = A + n1;
   double* A22 = A + n1 + n1 * lda;
@@ -409,11 +421,6 @@ static cudaError_t potrf_rec(double* A, long long lda, int n, int off, DevStatus
 cudaError_t potrf_lower(double* A, long long lda, int n, DevStatus* st, cudaStream_t s,
                         double* inv_cache, const OzWork* oz, const PotrfHook* hook) {
   if (n <= 0) return cudaSuccess;
-  if (hook && n <= kLeaf) {
-    cudaError_t e = hook->fn(hook->ctx, s);
-    if (e != cudaSuccess) return e;
-    hook = nullptr;
-  }
   cudaError_t e = potrf_rec(A, lda, n, 0, st, s, inv_cache, oz, hook);
   if (e != cudaSuccess) return e;
   return zero_strict_upper(A, lda, n, s);

@@ -31,12 +31,15 @@ struct OzWork {
 size_t trsm_llt_oz_bytes(int n, int ncols, int chunk);
 
 size_t potrf_inv_cache_doubles(int n);
-// hook (optional): called on the stream once, at the top level, before
-// columns [potrf_top_split(n), n) are first read (lets a caller stream that
-// half of the matrix in while the first half is factored).
+// hook (optional): lets a caller stream the matrix in by column pieces while
+// the Cholesky runs.  Piece 0 = columns [0, s_depth) must be present at the
+// call; piece L (1 <= L <= depth) = columns [s_{depth-L+1}, s_{depth-L}) with
+// s_0 = n and s_{k+1} = potrf_top_split(s_k), i.e. the top-left recursion
+// chain.  fn(ctx, L, s) is called on the stream before piece L is first read.
 struct PotrfHook {
-  cudaError_t (*fn)(void* ctx, cudaStream_t s);
+  cudaError_t (*fn)(void* ctx, int level, cudaStream_t s);
   void* ctx;
+  int depth;
 };
 int potrf_top_split(int n);
 cudaError_t potrf_lower(double* A, long long lda, int n, DevStatus* st, cudaStream_t s,

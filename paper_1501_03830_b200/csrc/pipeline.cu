@@ -255,22 +255,26 @@ __global__ void copy_lower_kernel(int n, const double* src, long long lds, doubl
   dst[r + (long long)c * ldd] = (r >= c) ? src[r + (long long)c * lds] : 0.0;
 }
 
-// Second half of the host entry's K upload: wait for it, then copy it into L.
+// Later column pieces of the host entry's K upload: wait for piece L, then
+// copy it into L's buffer (potrf hook, see PotrfHook).
 struct KTail {
-  int n, c0;
+  int n;
   const double* K; long long ldk;
   double* L; long long ld;
-  cudaEvent_t ready;
+  int depth;
+  int c0[kKPieces], c1[kKPieces];
+  cudaEvent_t ready[kKPieces];
 };
 
-cudaError_t k_tail_hook(void* ctx, cudaStream_t s) {
+cudaError_t k_tail_hook(void* ctx, int level, cudaStream_t s) {
   const KTail& t = *static_cast<const KTail*>(ctx);
-  cudaError_t e = cudaStreamWaitEvent(s, t.ready, 0);
+  if (level < 1 || level > t.depth) return cudaSuccess;
+  cudaError_t e = cudaStreamWaitEvent(s, t.ready[level], 0);
   if (e != cudaSuccess) return e;
-  const long long cnt = (long long)t.n * (t.n - t.c0);
+  const long long cnt = (long long)t.n * (t.c1[level] - t.c0[level]);
   if (cnt > 0) {
-    copy_lower_kernel<<<(unsigned)ceil_div(cnt, 256), 256, 0, s>>>(t.n, t.K, t.ldk, t.L, t.ld, t.c0,
-                                                                   t.n);
+    copy_lower_kernel<<<(unsigned)ceil_div(cnt, 256), 256, 0, s>>>(t.n, t.K, t.ldk, t.L, t.ld,
+                                                                   t.c0[level], t.c1[level]);
     count_launch();
   }
   return cudaGetLastError();
@@ -362,6 +366,25 @@ cudaError_t rows_out_hook(void* ctx, int r0, int r1, cudaStream_t s) {
 
 }  // namespace
 
+void kpieces_plan(int n, int depth, KPieces* kp) {
+  int sp[kKPieces + 1];
+  sp[0] = n;
+  int d = 0;
+  while (d < depth && d + 1 < kKPieces && sp[d] > 64) {
+    sp[d + 1] = potrf_top_split(sp[d]);
+    ++d;
+  }
+  kp->depth = d;
+  // piece L = [s_{d-L+1}, s_{d-L}), piece 0 = [0, s_d)
+  kp->c0[0] = 0;
+  kp->c1[0] = sp[d];
+  for (int L = 1; L <= d; ++L) {
+    kp->c0[L] = sp[d - L + 1];
+    kp->c1[L] = sp[d - L];
+    kp->ready[L] = nullptr;
+  }
+}
+
 size_t solve_bytes(int n, int flags) {
   Arena a;
   a.dry = true;
@@ -374,7 +397,7 @@ cudaError_t solve_spd_pair(int n, const double* M, long long ldm, const double* 
                            double* lam, double* X1, long long ldx1, double* X2, long long ldx2,
                            void* work, size_t work_bytes, int flags, cudaStream_t s,
                            SolveStatus* out, cudaEvent_t m_ready, const HostOut* hout,
-                           Comm* comm, cudaEvent_t k_tail_ready) {
+                           Comm* comm, const KPieces* k_pieces) {
   out->code = 0;
   out->pivot_index = -1;
   out->pivot_value = 0.0;
@@ -392,18 +415,28 @@ cudaError_t solve_spd_pair(int n, const double* M, long long ldm, const double* 
   // 1. K = L L^T
   stage_mark("potrf", s);
   {
-    // with k_tail_ready (host entry), only columns [0, n1) of K have landed:
-    // the Cholesky factors them while the rest streams in
-    const int n1 = k_tail_ready ? potrf_top_split(n) : n;
-    const long long cnt = (long long)n * n1;
-    copy_lower_kernel<<<(unsigned)ceil_div(cnt, 256), 256, 0, s>>>(n, K, ldk, w.L, ld, 0, n1);
+    // with k_pieces (host entry), only K's piece 0 has landed: the Cholesky
+    // factors it while the later pieces stream in
+    KTail tail{};
+    tail.n = n; tail.K = K; tail.ldk = ldk; tail.L = w.L; tail.ld = ld;
+    int p0 = n;
+    if (k_pieces) {
+      tail.depth = k_pieces->depth;
+      for (int L = 1; L <= tail.depth; ++L) {
+        tail.c0[L] = k_pieces->c0[L];
+        tail.c1[L] = k_pieces->c1[L];
+        tail.ready[L] = k_pieces->ready[L];
+      }
+      p0 = k_pieces->c1[0];
+    }
+    const long long cnt = (long long)n * p0;
+    copy_lower_kernel<<<(unsigned)ceil_div(cnt, 256), 256, 0, s>>>(n, K, ldk, w.L, ld, 0, p0);
     count_launch();
-    KTail tail{n, n1, K, ldk, w.L, ld, k_tail_ready};
-    PotrfHook hook{k_tail_hook, &tail};
+    PotrfHook hook{k_tail_hook, &tail, tail.depth};
     // the emulated engine's workspace aliases the (still idle) eigensolver's
     OzWork ozp{w.oz, w.oz_bytes, kRecoverBlock};
     if ((e = potrf_lower(w.L, ld, n, &w.st[0], s, w.linv, w.oz_bytes ? &ozp : nullptr,
-                         k_tail_ready ? &hook : nullptr)) != cudaSuccess)
+                         k_pieces ? &hook : nullptr)) != cudaSuccess)
       return e;
   }
   if (m_ready && (e = cudaStreamWaitEvent(s, m_ready, 0)) != cudaSuccess) return e;

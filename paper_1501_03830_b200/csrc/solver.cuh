@@ -36,8 +36,16 @@ struct SolveStatus {
   int failed_factor;   // 0: K (A-B), 1: M (A+B)
 };
 
-// k_tail_ready (host entry): only K's columns [0, potrf_top_split(n)) are on
-// the device at the call; the rest lands when the event fires.
+// Host-entry upload of K by column pieces (see PotrfHook): piece 0 =
+// [c0[0], c1[0]) is on the device at the call, piece L lands when ready[L]
+// fires.  kpieces_plan() fills the boundaries for n.
+constexpr int kKPieces = 4;  // pieces 0..3 (depth <= 3)
+struct KPieces {
+  int depth;
+  int c0[kKPieces], c1[kKPieces];
+  cudaEvent_t ready[kKPieces];
+};
+void kpieces_plan(int n, int depth, KPieces* kp);
 // Optional host destination for the e2e path: X1/X2 column blocks are copied
 // on `stream` as soon as they are recovered.
 struct HostOut {
@@ -58,7 +66,7 @@ cudaError_t solve_spd_pair(int n, const double* M, long long ldm, const double* 
                            void* work, size_t work_bytes, int flags, cudaStream_t s,
                            SolveStatus* out, cudaEvent_t m_ready = nullptr,
                            const HostOut* hout = nullptr, Comm* comm = nullptr,
-                           cudaEvent_t k_tail_ready = nullptr);
+                           const KPieces* k_pieces = nullptr);
 
 cudaError_t absorption(int n, const double* lam, const double* X1c, long long ldx1,
                        const double* X2c, long long ldx2, const double* dr, const double* dl,
