@@ -69,6 +69,11 @@ size_t bse_solve_workspace_bytes(int64_t n, int flags);
  *   X1 = (L Z + L^{-T} Z Lam) Lam^{-1/2} / 2,  X2 = (L Z - L^{-T} Z Lam) Lam^{-1/2} / 2
  * lam is returned DESCENDING and strictly positive (core.py:159-162).
  * M and K are read-only; only their lower triangles are referenced.
+ * Work is ordered on `stream`; internally the solve forks per-device
+ * auxiliary streams (panel look-ahead, block builds under the divide and
+ * conquer) and joins them back into `stream` before the last kernel, so
+ * events recorded on `stream` bracket the whole solve.  One solve at a time
+ * per device and process (the auxiliary streams are shared).
  */
 int bse_solve_spd_pair_dev(int64_t n, const double* dM, int64_t ldm, const double* dK,
                            int64_t ldk, double* dLam, double* dX1, int64_t ldx1, double* dX2,
