@@ -63,6 +63,7 @@ __global__ void absmax_kernel(int n, const double* d, const double* e, double* o
 }
 
 // ---- 1. z vector, merge-sort of the children's eigenvalues, deflation ----
+constexpr int kDcScanChunk = 2048;
 __global__ void __launch_bounds__(kDcThreads) dc_prepare_kernel(
     Level L, int n, const double* __restrict__ e, const double* __restrict__ scal,
     const double* __restrict__ Din, double* __restrict__ Dout, const double* __restrict__ Qin,
@@ -116,47 +117,58 @@ __global__ void __launch_bounds__(kDcThreads) dc_prepare_kernel(
   amax = warp_max(amax);
   if ((tid & 31) == 0) red[tid >> 5] = amax;
   __syncthreads();
-  if (tid != 0) return;
   double tol = 0.0;
   for (int i = 0; i < (int)(blockDim.x >> 5); ++i) tol = fmax(tol, red[i]);
   tol *= 8.0 * kEps;
-  // sequential deflation scan (dlaed2 logic) in sorted order
-  double* ds = w.ds + lo;
-  double* zs = w.zs + lo;
+  // sequential deflation scan (dlaed2 logic) in sorted order.  The scan only
+  // ever rewrites the entries of the current candidate pj and of j, so pj's
+  // (possibly rotated) d and z live in registers and every j is a fresh read
+  // of the sorted arrays, staged chunk-wise into shared memory by the whole
+  // block: the serial loop then runs at shared-memory instead of L2 latency.
+  __shared__ double sd[kDcScanChunk], sz[kDcScanChunk];
+  const double* ds = w.ds + lo;
+  const double* zs = w.zs + lo;
   int K = 0, nd = 0, nr = 0, pj = -1;
-  for (int j = 0; j < m; ++j) {
-    const double zj = zs[j];
-    if (rho * fabs(zj) <= tol) {
-      w.defl[lo + nd] = j;
-      w.val[lo + (m - 1 - nd)] = ds[j];  // deflated values fill from the back
-      ++nd;
-      continue;
-    }
-    if (pj < 0) { pj = j; continue; }
-    double s = zs[pj], c = zj;
-    const double tau = hypot(c, s);
-    const double t = ds[j] - ds[pj];
-    c /= tau;
-    s = -s / tau;
-    if (fabs(t * c * s) <= tol) {
-      zs[j] = tau;
-      zs[pj] = 0.0;
-      w.rotp[lo + nr] = pj; w.rotq[lo + nr] = j; w.rotc[lo + nr] = c; w.rots[lo + nr] = s;
-      ++nr;
-      const double tt = ds[pj] * c * c + ds[j] * s * s;
-      ds[j] = ds[pj] * s * s + ds[j] * c * c;
-      ds[pj] = tt;
-      w.defl[lo + nd] = pj;
-      w.val[lo + (m - 1 - nd)] = tt;
-      ++nd;
-      pj = j;
-    } else {
-      w.keep[lo + K] = pj; w.dk[lo + K] = ds[pj]; w.zk[lo + K] = zs[pj];
-      ++K;
-      pj = j;
+  double dpj = 0.0, zpj = 0.0;
+  for (int c0 = 0; c0 < m; c0 += kDcScanChunk) {
+    const int cl = min(kDcScanChunk, m - c0);
+    __syncthreads();
+    for (int t = tid; t < cl; t += blockDim.x) { sd[t] = ds[c0 + t]; sz[t] = zs[c0 + t]; }
+    __syncthreads();
+    if (tid != 0) continue;
+    for (int jj = 0; jj < cl; ++jj) {
+      const int j = c0 + jj;
+      const double zj = sz[jj], dj = sd[jj];
+      if (rho * fabs(zj) <= tol) {
+        w.defl[lo + nd] = j;
+        w.val[lo + (m - 1 - nd)] = dj;  // deflated values fill from the back
+        ++nd;
+        continue;
+      }
+      if (pj < 0) { pj = j; dpj = dj; zpj = zj; continue; }
+      double s = zpj, c = zj;
+      const double tau = hypot(c, s);
+      const double t = dj - dpj;
+      c /= tau;
+      s = -s / tau;
+      if (fabs(t * c * s) <= tol) {
+        w.rotp[lo + nr] = pj; w.rotq[lo + nr] = j; w.rotc[lo + nr] = c; w.rots[lo + nr] = s;
+        ++nr;
+        const double tt = dpj * c * c + dj * s * s;
+        const double dnew = dpj * s * s + dj * c * c;
+        w.defl[lo + nd] = pj;
+        w.val[lo + (m - 1 - nd)] = tt;
+        ++nd;
+        pj = j; dpj = dnew; zpj = tau;
+      } else {
+        w.keep[lo + K] = pj; w.dk[lo + K] = dpj; w.zk[lo + K] = zpj;
+        ++K;
+        pj = j; dpj = dj; zpj = zj;
+      }
     }
   }
-  if (pj >= 0) { w.keep[lo + K] = pj; w.dk[lo + K] = ds[pj]; w.zk[lo + K] = zs[pj]; ++K; }
+  if (tid != 0) return;
+  if (pj >= 0) { w.keep[lo + K] = pj; w.dk[lo + K] = dpj; w.zk[lo + K] = zpj; ++K; }
   cnt[0] = K; cnt[1] = nd; cnt[2] = nr;
   w.zh[lo] = rho;  // stash rho for the secular / z-hat kernels
 }
@@ -169,17 +181,34 @@ __global__ void __launch_bounds__(kDcThreads) dc_prepare_kernel(
 // c + rho b1/(d_l - x) + rho b2/(d_r - x), fitted to f and f' at the current
 // iterate (the "middle way" of Li / LAPACK dlaed4), with bisection whenever
 // the model step leaves the bracket.  Converges in a handful of sweeps.
+// kSecLanes lanes share one root: each sums a strided slice of the K poles
+// and a butterfly (xor) reduction gives every lane of the group the same
+// bitwise sum (a + b == b + a), so the group's control flow stays uniform.
+// One thread per root left the top merges at ~3 warps per SM, latency-bound
+// on the dependent FP64 reciprocals.
+constexpr int kSecLanes = 8;
+
+__device__ __forceinline__ double group_sum(double v, unsigned mask) {
+#pragma unroll
+  for (int o = kSecLanes / 2; o > 0; o >>= 1) v += __shfl_xor_sync(mask, v, o, kSecLanes);
+  return v;
+}
+
 __global__ void dc_secular_kernel(Level L, int n, StedcWork w) {
   int lo, mid, hi;
   node_range(L, n, blockIdx.y, lo, mid, hi);
   const int* cnt = w.counts + 3 * blockIdx.y;
   const int K = cnt[0];
-  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  const int gt = blockIdx.x * blockDim.x + threadIdx.x;
+  const int i = gt / kSecLanes;
+  const int lane = gt % kSecLanes;
+  const unsigned mask = ((1u << kSecLanes) - 1u) << ((threadIdx.x & 31) & ~(kSecLanes - 1));
   if (K <= 0 || i >= K) return;
   const double rho = w.zh[lo];
   const double* dk = w.dk + lo;
   const double* zk = w.zk + lo;
   if (K == 1) {
+    if (lane != 0) return;
     const double t = rho * zk[0] * zk[0];
     w.org[lo] = 0;
     w.tau[lo] = t;
@@ -191,15 +220,15 @@ __global__ void dc_secular_kernel(Level L, int n, StedcWork w) {
   if (i < K - 1) {
     const double half = 0.5 * (dk[i + 1] - dk[i]);
     double f = 0.0;
-    for (int j = 0; j < K; ++j) f += zk[j] * zk[j] / ((dk[j] - dk[i]) - half);
-    f = 1.0 + rho * f;
+    for (int j = lane; j < K; j += kSecLanes) f += zk[j] * zk[j] / ((dk[j] - dk[i]) - half);
+    f = 1.0 + rho * group_sum(f, mask);
     if (f >= 0.0) { org = i; a = 0.0; b = half; }
     else { org = i + 1; a = -half; b = 0.0; }
     pl = i; pr = i + 1;
   } else {
     double s = 0.0;
-    for (int j = 0; j < K; ++j) s += zk[j] * zk[j];
-    org = K - 1; a = 0.0; b = rho * s;
+    for (int j = lane; j < K; j += kSecLanes) s += zk[j] * zk[j];
+    org = K - 1; a = 0.0; b = rho * group_sum(s, mask);
     pl = K - 2; pr = K - 1;
   }
   const double d0 = dk[org];
@@ -207,18 +236,22 @@ __global__ void dc_secular_kernel(Level L, int n, StedcWork w) {
   double t = 0.5 * (a + b);
   for (int it = 0; it < 60; ++it) {
     double psi = 0.0, dpsi = 0.0, phi = 0.0, dphi = 0.0;
-    for (int j = 0; j <= pl; ++j) {
+    for (int j = lane; j <= pl; j += kSecLanes) {
       const double inv = 1.0 / ((dk[j] - d0) - t);
       const double q = zk[j] * zk[j] * inv;
       psi += q;
       dpsi += q * inv;
     }
-    for (int j = pr; j < K; ++j) {
+    for (int j = pr + lane; j < K; j += kSecLanes) {
       const double inv = 1.0 / ((dk[j] - d0) - t);
       const double q = zk[j] * zk[j] * inv;
       phi += q;
       dphi += q * inv;
     }
+    psi = group_sum(psi, mask);
+    dpsi = group_sum(dpsi, mask);
+    phi = group_sum(phi, mask);
+    dphi = group_sum(dphi, mask);
     const double f = 1.0 + rho * (psi + phi);
     // rounding-error bound of the computed f (cf. dlaed4's ERRETM): once |f|
     // is below it the iterate is a root to working accuracy
@@ -245,6 +278,7 @@ __global__ void dc_secular_kernel(Level L, int n, StedcWork w) {
     t = tn;
     if (done) break;
   }
+  if (lane != 0) return;
   w.org[lo + i] = org;
   w.tau[lo + i] = t;
   w.val[lo + i] = d0 + t;
@@ -255,19 +289,27 @@ __global__ void dc_zhat_kernel(Level L, int n, StedcWork w, const double* rho_sr
   int lo, mid, hi;
   node_range(L, n, blockIdx.y, lo, mid, hi);
   const int K = w.counts[3 * blockIdx.y];
-  const int j = blockIdx.x * blockDim.x + threadIdx.x;
+  const int gt = blockIdx.x * blockDim.x + threadIdx.x;
+  const int j = gt / kSecLanes;
+  const int lane = gt % kSecLanes;
+  const unsigned mask = ((1u << kSecLanes) - 1u) << ((threadIdx.x & 31) & ~(kSecLanes - 1));
   if (K <= 0 || j >= K) return;
   const double rho = rho_src[lo];
   const double* dk = w.dk + lo;
   const int* org = w.org + lo;
   const double* tau = w.tau + lo;
   const double dj = dk[j];
+  // each factor is a ratio of neighbouring pole/root gaps (O(1)), so the
+  // per-lane partial products stay in range
   double p = 1.0;
-  for (int i = 0; i < K; ++i) {
+  for (int i = lane; i < K; i += kSecLanes) {
     const double li = (dk[org[i]] - dj) + tau[i];
     if (i < K - 1) p *= li / (i < j ? (dk[i] - dj) : (dk[i + 1] - dj));
     else p *= li;
   }
+#pragma unroll
+  for (int o = kSecLanes / 2; o > 0; o >>= 1) p *= __shfl_xor_sync(mask, p, o, kSecLanes);
+  if (lane != 0) return;
   w.zh2[lo + j] = copysign(sqrt(fmax(p, 0.0) / rho), w.zk[lo + j]);
 }
 
@@ -555,10 +597,11 @@ cudaError_t stedc(int n, double* d, double* e, double* wout, double* Q, long lon
     count_launch();
     const dim3 g1((unsigned)ceil_div(maxm, 128), (unsigned)L.nnodes);
     stage_mark("dc_secular", s);
-    dc_secular_kernel<<<g1, 128, 0, s>>>(L, n, ws);
+    const dim3 gs((unsigned)ceil_div((long long)maxm * kSecLanes, 128), (unsigned)L.nnodes);
+    dc_secular_kernel<<<gs, 128, 0, s>>>(L, n, ws);
     count_launch();
     stage_mark("dc_vectors", s);
-    dc_zhat_kernel<<<g1, 128, 0, s>>>(L, n, ws, ws.zh);
+    dc_zhat_kernel<<<gs, 128, 0, s>>>(L, n, ws, ws.zh);
     count_launch();
     dc_order_kernel<<<g1, 128, 0, s>>>(L, n, ws, Dout);
     count_launch();
