@@ -17,9 +17,16 @@ DESIGN.md section 7).  Times are device (CUDA event) times, max over ranks.
 
 --impl reference times the reference algorithm on the host cores: the numpy
 restatement of the reference's solve_complex (oracle/bse_oracle.py; the
-reference itself is pure Python and not installed on the GPU box), on a
-bounded sample (cfg2 recipe at n = 256 and 512) extrapolated to the workload n
-with the fitted power law.
+reference itself is pure Python and cannot travel to the GPU box), priced at
+the FULL workload size by oracle/cost_model.py: each bench step runs a
+bounded sample of the reference's own loop steps on full-size arrays, and the
+time-to-solution is the measured time per unit of work x the exact work of
+every loop (validated against complete runs: tools/validate_cost_model.py).
+The GPU arm's cpu_baseline leg is one such sample (~20-40 s on the host).
+
+Stage breakdown: CUDA events for ONE designated timed step (the last), read
+back in full; stage_log_check asserts their sum matches that step's own
+event time and ms_per_step within 2 %.
 """
 from __future__ import annotations
 
@@ -55,6 +62,16 @@ STAGE_FLOPS = {  # per-stage algorithmic flops, N = n
 }
 
 
+def hbm_peak():
+    """(GB/s, source): MEASURED_PEAKS.json (driver-written) or the profiling
+    guide's fallback."""
+    try:
+        v = float(json.loads((ROOT / "MEASURED_PEAKS.json").read_text())["hbm_gbs"])
+        return v, "MEASURED_PEAKS.json hbm_gbs"
+    except (OSError, ValueError, KeyError):
+        return 6465.0, "fallback (SURVEY 8d)"
+
+
 def env_rank():
     return (int(os.environ.get("RANK", 0)), int(os.environ.get("LOCAL_RANK", 0)),
             int(os.environ.get("WORLD_SIZE", 1)))
@@ -71,52 +88,133 @@ def max_over_ranks(value: float, dist=None, device=None) -> float:
 
 
 # ---------------------------------------------------------------------------
-# CPU baseline: the reference algorithm (numpy restatement) on host cores
+# CPU baseline: the reference algorithm on host cores, priced at FULL size by
+# oracle/cost_model.py (the reference's own step bodies timed on full-size
+# arrays at stratified step indices x exact per-loop work counts).
 
-def cpu_reference_sample(n_target: int, sizes=(256, 512)):
+def _host_threads():
+    t = os.environ.get("OPENBLAS_NUM_THREADS") or os.environ.get("OMP_NUM_THREADS")
+    return int(t) if t else (os.cpu_count() or 1)
+
+
+def _host_ram_ok(n: int) -> bool:
+    """The sampler holds a, b (2 x 16 n^2 B), one m x m and one m x n float64
+    buffer (m = 2n) and transient m x m temporaries of the reduction step."""
+    try:
+        import psutil
+        need = 16 * n * n * 2 + 8 * (2 * n) ** 2 * 3 + 8 * 2 * n * n
+        return psutil.virtual_memory().available > 1.2 * need
+    except Exception:
+        return True
+
+
+def reference_inputs(n: int, config: int = CFG, seed: int = SEED):
+    """(a, b, lam_bounds) of the bench workload as the reference receives them
+    (complex128 n x n, BseOperator's storage, core.py:45-75)."""
     import numpy as np
-    from oracle import bse_oracle as orc
     from paper_1501_03830_b200 import configs
-    times = []
-    for n in sizes:
-        a, b, _ = configs.config_operator(CFG, n=n, seed=SEED)
-        t0 = time.perf_counter()
-        orc.solve_complex(a, b)
-        times.append(time.perf_counter() - t0)
-    expo = float(np.log(times[-1] / times[0]) / np.log(sizes[-1] / sizes[0]))
-    expo = min(max(expo, 2.5), 3.3)
-    value = times[-1] * (n_target / sizes[-1]) ** expo
-    threads = os.environ.get("OPENBLAS_NUM_THREADS") or os.environ.get("OMP_NUM_THREADS")
-    cores = int(threads) if threads else (os.cpu_count() or 1)
-    sample = (f"reference algorithm (oracle/bse_oracle.solve_complex: skew Householder "
-              f"tridiagonalization + bisection/inverse iteration, numpy) on the cfg2 recipe at "
-              f"n={sizes} took {[round(t, 2) for t in times]} s; extrapolated to n={n_target} "
-              f"with fitted exponent {expo:.2f} (effectively single-core Python loops; "
-              f"BLAS threads {cores})")
-    return value, cores, sample, times
+    c = configs.CONFIGS[config]
+    if c["kind"] == "real":
+        bounds = (c["lo"], c["hi"])  # lam^2 in [min s min d, max s max d]
+        try:
+            import torch
+            if torch.cuda.is_available() and n >= 2048:
+                S, D, _ = configs.torch_real_operator(n, seed=seed, spectrum=c["spectrum"],
+                                                      lo=c["lo"], hi=c["hi"], device="cuda")
+                a = (0.5 * (S + D)).cpu().numpy().astype(np.complex128)
+                b = (0.5 * (S - D)).cpu().numpy().astype(np.complex128)
+                del S, D
+                torch.cuda.empty_cache()
+                return a, b, bounds
+        except ImportError:
+            pass
+        a, b, _ = configs.config_operator(config, n=n, seed=seed)
+        return a, b, bounds
+    a, b, _, a_vals = configs.complex_operator(n, seed=seed, lo=c["lo"], hi=c["hi"],
+                                              bnorm=c["bnorm"])
+    bn = 1.0 if c["bnorm"] == "one" else 0.9 * float(np.min(a_vals))
+    return a, b, (max(c["lo"] - bn, 1e-3), c["hi"] + bn)
+
+
+def cpu_reference_sample(n: int, rounds: int = 1, points: int = 2, inputs=None):
+    """Bounded full-size sample of the reference solve_complex on host cores
+    (GPU arm's cpu_baseline leg).  Returns (estimate_s, cores, sample_text,
+    phases)."""
+    from oracle import cost_model as cm
+    if not _host_ram_ok(n):
+        return None, _host_threads(), "skipped: not enough host RAM for a full-size sample", {}
+    a, b, bounds = inputs if inputs is not None else reference_inputs(n)
+    smp = cm.SolveComplexCost(a, b, bounds)
+    spent = 0.0
+    for u in cm.offsets(rounds):
+        spent += smp.round(points=points, u=u)
+    est = smp.estimate()
+    sample = (f"{smp.notes()}; {spent:.1f} s of reference code measured; phases (s): "
+              + ", ".join(f"{k} {v:.0f}" for k, v in smp.phases().items())
+              + f"; OpenBLAS threads {_host_threads()} (the Python loops run on one core)")
+    return est, _host_threads(), sample, smp.phases()
 
 
 def run_reference(args):
+    """--impl reference: the reference algorithm (oracle port of solve_complex)
+    on the host cores for the bench workload.  Each step is one bounded sample:
+    one reference loop (Cholesky columns, reduction steps, reorthogonalisation
+    columns, reflector applications, in rotation) sampled at full size; the
+    single-shot stages (BLAS-3 blocks, vectorised sweeps) are measured in the
+    first step.  value = the full-size time-to-solution priced from all
+    samples (oracle/cost_model.py); ms_per_step = the wall time of a sample
+    step (what actually ran)."""
     rank, _, world = env_rank()
     if rank != 0:
         return 0
-    vals = []
-    info = None
+    from oracle import cost_model as cm
+    n = args.n if args.config == 2 else 16384
+    if not _host_ram_ok(n):
+        print(json.dumps({"impl": "reference", "unavailable":
+                          f"host RAM below the full-size sample's need at n={n}"}), flush=True)
+        return 0
+    t_setup = time.perf_counter()
+    a, b, bounds = reference_inputs(n, config=args.config, seed=SEED if args.config == 2 else 3)
+    smp = cm.SolveComplexCost(a, b, bounds)
+    t_setup = time.perf_counter() - t_setup
+    names = list(smp.loops)
+    offs = cm.offsets(args.warmup + args.steps + len(names))
+    walls = []
     for i in range(args.warmup + args.steps):
-        v, cores, sample, _ = cpu_reference_sample(args.n)
+        t0 = time.perf_counter()
+        smp._fill_f()
+        smp._fill_v()
+        if smp.fixed is None:
+            smp.fixed = smp._fixed_phases()
+        smp.loops[names[i % len(names)]].sample(1, offs[i // len(names)])
         if i >= args.warmup:
-            vals.append(v)
-        info = (cores, sample)
-    value = statistics.median(vals)
+            walls.append(time.perf_counter() - t0)
+    for nm in names:  # every loop priced by >= 1 sample even for tiny --steps
+        if smp.loops[nm].samples == 0:
+            smp._fill_f()
+            smp._fill_v()
+            smp.loops[nm].sample(1, 0.5)
+    smp.rounds = args.warmup + args.steps
+    value = smp.estimate()
+    wall = statistics.mean(walls)
+    ph = smp.phases()
+    sample = (f"{smp.notes()}; phases (s): " + ", ".join(f"{k} {v:.0f}" for k, v in ph.items())
+              + f"; OpenBLAS threads {_host_threads()} (the Python loops run on one core); "
+              f"input generation + buffers {t_setup:.0f} s untimed")
+    wl = (f"cfg2 real BSE n={n}, log-uniform [0.1,100] spectra" if args.config == 2 else
+          "cfg3 complex BSE n=16384 (real embedding 32768)")
     line = {
         "impl": "reference", "metric": "full BSE eigenpair time-to-solution (s)", "value": value,
         "unit": "s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": value * 1e3, "higher_is_better": False, "scaling": "weak",
-        "vs_baseline": None, "dtype": "f64", "data": "synthetic (BASELINE cfg2 recipe)",
-        "config": {"workload": f"cfg2 real BSE n={args.n}, log-uniform [0.1,100] spectra",
-                   "n": args.n, "parallelism": "host cpu"},
-        "cpu_baseline": {"value": value, "unit": "s", "cores": info[0], "kind": "port",
-                         "sample": info[1]},
+        "ms_per_step": wall * 1e3, "higher_is_better": False, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64",
+        "data": f"synthetic (BASELINE cfg{args.config} recipe)",
+        "config": {"workload": wl, "n": n, "parallelism": "host cpu"},
+        "value_kind": "full-size time-to-solution priced from measured full-size step samples "
+                      "(oracle/cost_model.py); ms_per_step is the wall time of one sample step",
+        "cpu_baseline": {"value": value, "unit": "s", "cores": _host_threads(), "kind": "port",
+                         "sample": sample},
+        "phases_s": {k: round(v, 1) for k, v in ph.items()},
         "e2e": {"value": value, "unit": "s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -287,36 +385,77 @@ def run_ours(args):
     torch.cuda.synchronize(dev)
 
     # ---- timed region ----
+    # Stage events are recorded for ONE designated timed step (the last), with
+    # the log read back in full (bse_profile_count), so stages_ms is that
+    # step's breakdown; per-step CUDA events bracket every step.
     clocks = ClockSampler(local_rank)
     time.sleep(0.3)
-    lib.bse_profile_enable(1)
     launches0 = lib.bse_launch_count()
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize(dev)
-    ev0 = torch.cuda.Event(enable_timing=True)
-    ev1 = torch.cuda.Event(enable_timing=True)
-    ev0.record(stream)
-    for _ in range(args.steps):
+    evs = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps + 1)]
+    evs[0].record(stream)
+    for i in range(args.steps):
+        if i == args.steps - 1:
+            lib.bse_profile_enable(1)
         step()
-    ev1.record(stream)
+        evs[i + 1].record(stream)
     torch.cuda.synchronize(dev)
     if world > 1:
         dist.barrier()
     launches = lib.bse_launch_count() - launches0
     clk = clocks.stop()
-    total_ms = ev0.elapsed_time(ev1)
-    msarr = (C.c_double * 4096)()
-    names = C.create_string_buffer(32 * 4096)
-    cnt = lib.bse_profile_read(4096, msarr, names)
+    total_ms = evs[0].elapsed_time(evs[-1])
+    step_ms = [evs[i].elapsed_time(evs[i + 1]) for i in range(args.steps)]
+    cnt = lib.bse_profile_count()
+    msarr = (C.c_double * max(cnt, 1))()
+    names = C.create_string_buffer(32 * max(cnt, 1))
+    got = lib.bse_profile_read(cnt, msarr, names)
     lib.bse_profile_enable(0)
     stages = {}
-    for i in range(cnt):
+    for i in range(got):
         nm = names.raw[32 * i:32 * (i + 1)].split(b"\0")[0].decode()
         if nm == "end":
             continue
-        stages[nm] = stages.get(nm, 0.0) + msarr[i] / args.steps
+        stages[nm] = stages.get(nm, 0.0) + msarr[i]
     ms_step = max_over_ranks(total_ms / args.steps, dist if world > 1 else None, dev)
+    stage_sum = sum(stages.values())
+    stage_check = {"designated_step": args.steps, "events": got, "sum_stages_ms": stage_sum,
+                   "designated_step_ms": step_ms[-1], "ms_per_step": ms_step,
+                   "rel_vs_step": abs(stage_sum - step_ms[-1]) / step_ms[-1],
+                   "rel_vs_ms_per_step": abs(stage_sum - ms_step) / ms_step}
+    stage_check["pass"] = bool(got == cnt and stage_check["rel_vs_step"] <= 0.02 and
+                               stage_check["rel_vs_ms_per_step"] <= 0.02)
+    if not stage_check["pass"]:
+        print(f"bench.py: STAGE LOG CHECK FAILED {stage_check}", file=sys.stderr, flush=True)
+
+    # all-DMMA comparison (BSE_FLAG_NATIVE_FP64: no INT8-emulated products),
+    # one solve outside the timed region into separate output buffers
+    native = None
+    if comm is None and not args.no_native:
+        wbn = lib.bse_solve_workspace_bytes(n, _lib.FLAG_NATIVE_FP64)
+        if wbn <= wb:
+            X1n = torch.empty_like(X1)
+            X2n = torch.empty_like(X2)
+            lamn = torch.empty_like(lam)
+            ea, eb = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            torch.cuda.synchronize(dev)
+            ea.record(stream)
+            st = lib.bse_solve_spd_pair_dev(n, ptr(Mt), ld, ptr(Kt), ld, ptr(lamn), ptr(X1n), ld,
+                                            ptr(X2n), ld, ptr(work), wb, _lib.FLAG_NATIVE_FP64,
+                                            sp, C.byref(info))
+            eb.record(stream)
+            torch.cuda.synchronize(dev)
+            if st == 0:
+                t = ea.elapsed_time(eb) / 1e3
+                native = {"value": t, "unit": "s", "tflops": alg_flops(n) / t / 1e12,
+                          "frac_of_fp64_peak": alg_flops(n) / t / 1e12 / fp64_peak,
+                          "max_rel_lambda_diff_vs_timed": float(
+                              ((lamn - lam).abs() / lam).max().item()),
+                          "note": "one solve with every product on the FP64 DMMA engine"}
+            del X1n, X2n, lamn
+            torch.cuda.empty_cache()
 
     # sanity: eigenvalues positive, descending
     lam_h = lam.cpu().numpy()
@@ -401,6 +540,28 @@ def run_ours(args):
             dist.destroy_process_group()
         return 0
 
+    # bandwidth / latency-bound stages of the designated step (north star:
+    # "achieved HBM GB/s for bulge chasing and tridiagonal work")
+    band = 64
+    bw_stages = {}
+    hbm = hbm_peak()
+    sb_ms = stages.get("sb2st", 0.0)
+    if sb_ms > 0:
+        by = 8.0 * (band + 1) * n * n  # each of N-1 sweeps reads+writes the band once
+        bw_stages["sb2st"] = {"bytes": by, "ms": sb_ms, "gbs": by / (sb_ms * 1e-3) / 1e9,
+                              "frac_of_hbm": by / (sb_ms * 1e-3) / 1e9 / hbm[0],
+                              "model": "8 (b+1) N^2 B, b = 64"}
+    dc_ms = sum(v for k, v in stages.items() if k.startswith("dc_") or k == "stedc")
+    if dc_ms > 0:
+        by = 40.0 * n * n  # dense merge traffic, no deflation: sum over levels of 20 N m_l B
+        bw_stages["stedc"] = {"bytes": by, "ms": dc_ms, "gbs": by / (dc_ms * 1e-3) / 1e9,
+                              "frac_of_hbm": by / (dc_ms * 1e-3) / 1e9 / hbm[0],
+                              "model": "40 N^2 B: per merge level read Q children (N m/2) + U "
+                                       "(N m), write Q (N m) doubles; latency-bound stage"}
+    for v in bw_stages.values():
+        v["peak_gbs"] = hbm[0]
+        v["peak_source"] = hbm[1]
+
     # roofline of the dominant FP64-tensor stage (algorithmic flops / live event time)
     tens = {k: v for k, v in stages.items() if k in STAGE_FLOPS}
     dom = max(tens, key=tens.get) if tens else None
@@ -436,7 +597,10 @@ def run_ours(args):
         "fp64_peak_tflops": fp64_peak,
         "frac_of_fp64_peak": alg_flops(n) / solve_s / 1e12 / fp64_peak,
         "stages_ms": {k: round(v, 3) for k, v in stages.items()},
+        "stage_log_check": stage_check,
         "roofline": roof,
+        "bandwidth_stages": bw_stages,
+        "native_fp64_solve": native,
         "cpu_baseline": cpu,
         "e2e": e2e,
         "gpu_launches": int(launches),
@@ -460,6 +624,8 @@ def main():
     ap.add_argument("--e2e-steps", type=int, default=1)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-verify", action="store_true")
+    ap.add_argument("--no-native", action="store_true",
+                    help="skip the all-DMMA (BSE_FLAG_NATIVE_FP64) comparison solve")
     ap.add_argument("--config", type=int, default=2, choices=[1, 2],
                     help="2 (default): real n=16384 headline; 1: complex n=2048 side line")
     args = ap.parse_args()

@@ -41,20 +41,23 @@ typedef enum {
   BSE_NOT_POSITIVE_DEFINITE = 1, /* maps to kernels.NotPositiveDefinite */
   BSE_NO_CONVERGENCE = 2,        /* maps to kernels.ConvergenceError */
   BSE_BAD_ARGUMENT = 3,          /* maps to ValueError */
-  BSE_CUDA_ERROR = 4             /* message in bse_last_error() */
+  BSE_CUDA_ERROR = 4,            /* message in bse_last_error() */
+  BSE_SPECTRUM_NOT_POSITIVE = 5  /* A+B, A-B definite but some lambda^2 <= 0 in floating
+                                    point: maps to the ValueError the reference's
+                                    PositiveEigensystem raises (core.py:159-160) */
 } bse_status;
 
-/* Flags for bse_solve_spd_pair_* / bse_syevd_dev. */
-#define BSE_FLAG_VALUES_ONLY 0x1 /* eigenvalues only (TDA / validation) */
-#define BSE_FLAG_ZPOLISH 0x2     /* Z <- Z (1.5 I - 0.5 Z^T Z) orthogonality polish */
+/* Flags.  Solve entries accept BSE_FLAG_NATIVE_FP64 only (any other bit is
+ * BSE_BAD_ARGUMENT); bse_syevd_dev also accepts BSE_FLAG_VALUES_ONLY. */
+#define BSE_FLAG_VALUES_ONLY 0x1 /* bse_syevd_dev: eigenvalues only (TDA / validation); Z untouched */
 #define BSE_FLAG_NATIVE_FP64 0x4 /* all products on FP64 DMMA (no INT8-emulated GEMMs) */
 
 typedef struct bse_info {
-  int64_t pivot_index;  /* first non-positive Cholesky pivot (status 1) */
+  int64_t pivot_index;  /* first non-positive Cholesky pivot (status 1), else -1 */
   double pivot_value;   /* its value */
-  int32_t failed_factor;/* 0: K = A - B, 1: M = A + B */
+  int32_t failed_factor;/* 0: K = A - B, 1: M = A + B, -1: none */
   int32_t reserved;
-  double min_pivot;     /* min_j L_jj^2 of the last successful factor */
+  double min_pivot;     /* status 0: min_j L_jj^2 of the factor of K (bse_potrf_dev: of A) */
 } bse_info;
 
 int bse_version(void);
@@ -146,9 +149,16 @@ int bse_trsm_dev(int kind, int64_t n, const double* dL, int64_t ldl, double* dB,
 /* Instrumentation (bench/profiling): stage timing with CUDA events recorded
  * on the solve stream, and the number of kernels this library has launched. */
 int bse_profile_enable(int on);
-/* Fills up to max_stages durations (ms) and 32-byte names; returns the count. */
+/* Number of stage intervals recorded since bse_profile_enable (size the
+ * buffers of bse_profile_read with it: one solve records ~1300). */
+int bse_profile_count(void);
+/* Fills up to max_stages durations (ms) and 32-byte names; returns the count
+ * and resets the log. */
 int bse_profile_read(int max_stages, double* ms, char* names);
 long long bse_launch_count(void);
+/* Returns the host entries' cached device memory (library-owned pool; the
+ * device's default pool is never modified) to the driver. */
+int bse_release_cached_memory(void);
 
 /* FP64 peak probe: which 0 = DMMA, 1 = DFMA.  Returns flops of one launch in
  * *flops and the mean device time over `reps` launches in *ms. */
@@ -178,8 +188,8 @@ int bse_comm_create_nccl(int rank, int world, const void* id128, bse_comm** out)
 /* Host-staged transport (device block -> host -> fn -> device). */
 int bse_comm_create_host(int rank, int world, bse_host_bcast_fn fn, void* ctx, bse_comm** out);
 /* Measurement only: acts as rank `rank` of `world` but exchanges nothing, so
- * one GPU can time the kernels of one rank of a world-GPU solve (bench.py
- * --simulate-rank-of).  Its results are NOT a solution. */
+ * one GPU can time the kernels of one rank of a world-GPU solve
+ * (tools/dist_projection.py).  Its results are NOT a solution. */
 int bse_comm_create_solo(int rank, int world, bse_comm** out);
 int bse_comm_destroy(bse_comm* comm);
 /* This rank's column block [c0, c1) of an n-column matrix. */

@@ -18,9 +18,9 @@ BSE_NOT_POSITIVE_DEFINITE = 1
 BSE_NO_CONVERGENCE = 2
 BSE_BAD_ARGUMENT = 3
 BSE_CUDA_ERROR = 4
+BSE_SPECTRUM_NOT_POSITIVE = 5
 
 FLAG_VALUES_ONLY = 0x1
-FLAG_ZPOLISH = 0x2
 FLAG_NATIVE_FP64 = 0x4
 
 
@@ -60,7 +60,9 @@ SIGNATURES = {
     "bse_trsm_dev": (_INT, [_INT, _I64, _P, _I64, _P, _I64, _I64, _P]),
     "bse_profile_enable": (_INT, [_INT]),
     "bse_profile_read": (_INT, [_INT, C.POINTER(_D), C.c_char_p]),
+    "bse_profile_count": (_INT, []),
     "bse_launch_count": (C.c_longlong, []),
+    "bse_release_cached_memory": (_INT, []),
     "bse_peak_fp64": (_INT, [_INT, _INT, _INT, _INT, C.POINTER(_D), C.POINTER(_D)]),
     # column-sharded multi-GPU solve
     "bse_comm_nccl_unique_id": (_INT, [_P]),

@@ -407,11 +407,9 @@ cudaError_t q2_build(int n, int b, int g, const double* V2, const double* tau2, 
   const int ngroups = (int)ceil_div(n - 2, g);
   const int HB = q2_hb(b, g);
   const size_t smem = sizeof(double) * ((size_t)(HB + 1) * g + 2 * (size_t)(g + 1) * g + g);
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(q2_build_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-    attr = true;
-  }
+  static PerDeviceOnce attr;
+  cudaError_t ae = set_smem_limit(attr, q2_build_kernel, 200 * 1024);
+  if (ae != cudaSuccess) return ae;
   q2_build_kernel<<<dim3(maxsteps, ngroups), 256, smem, s>>>(n, b, g, maxsteps, V2, tau2, Vblk);
   count_launch();
   return cudaGetLastError();
@@ -427,7 +425,8 @@ cudaError_t q2_apply(int n, int b, int g, const double* Vblk, double* Z, long lo
     const size_t smem = sizeof(double) * (kQ2Stages * (size_t)kQ2Stage +
                                           (size_t)8 * cg * nw * kQ2LDN) +
                         2 * kQ2Stages * sizeof(unsigned long long);
-    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaError_t ae = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (ae != cudaSuccess) return ae;
     kern<<<(unsigned)ceil_div(ncols, 8 * cg * nw), 32 * (nw + 1), smem, s>>>(n, b, maxsteps, Vblk,
                                                                             Z, ldz, ncols);
     count_launch();

@@ -3,6 +3,7 @@
 // with bse_last_error().
 #include <cstdio>
 #include <cstring>
+#include <mutex>
 #include <string>
 #include "../../include/bse_b200.h"
 #include "comm.cuh"
@@ -94,7 +95,7 @@ int bse_potrf_dev(int64_t n, double* dA, int64_t lda, void* stream, bse_info* in
   cudaStream_t s = (cudaStream_t)stream;
   bse::DevStatus* st = nullptr;
   BSE_TRY_CUDA(cudaMallocAsync((void**)&st, sizeof(bse::DevStatus), s), "alloc status");
-  bse::DevStatus h0{-1, 0, 0.0, 0.0};
+  bse::DevStatus h0{-1, 0, 0.0, HUGE_VAL};
   BSE_TRY_CUDA(cudaMemcpyAsync(st, &h0, sizeof(h0), cudaMemcpyHostToDevice, s), "status init");
   double* inv = nullptr;
   cudaError_t e = cudaMallocAsync((void**)&inv, sizeof(double) * bse::potrf_inv_cache_doubles((int)n), s);
@@ -109,6 +110,12 @@ int bse_potrf_dev(int64_t n, double* dA, int64_t lda, void* stream, bse_info* in
     if (info) { info->pivot_index = h.info; info->pivot_value = h.value; info->failed_factor = 0; }
     return fail(BSE_NOT_POSITIVE_DEFINITE, "matrix is not positive definite");
   }
+  if (info) {
+    info->pivot_index = -1;
+    info->pivot_value = 0.0;
+    info->failed_factor = -1;
+    info->min_pivot = n > 0 ? h.aux : 0.0;
+  }
   return BSE_OK;
 }
 
@@ -117,14 +124,59 @@ size_t bse_solve_workspace_bytes(int64_t n, int flags) {
 }
 
 static int map_solve_status(const bse::SolveStatus& st, bse_info* info) {
-  if (st.code == 0) return BSE_OK;
   if (info) {
     info->pivot_index = st.pivot_index;
     info->pivot_value = st.pivot_value;
     info->failed_factor = st.failed_factor;
+    info->min_pivot = st.min_pivot;
   }
-  return fail(BSE_NOT_POSITIVE_DEFINITE, st.failed_factor == 1 ? "A+B is not positive definite"
-                                                               : "A-B is not positive definite");
+  switch (st.code) {
+    case 0: return BSE_OK;
+    case 2: return fail(BSE_NO_CONVERGENCE, "divide and conquer: a secular root did not converge");
+    case 5: return fail(BSE_SPECTRUM_NOT_POSITIVE,
+                        "all eigenvalues must be strictly positive (A+B and A-B factor, but "
+                        "L^T (A+B) L has a non-positive eigenvalue in floating point)");
+    default:
+      return fail(BSE_NOT_POSITIVE_DEFINITE, st.failed_factor == 1 ? "A+B is not positive definite"
+                                                                   : "A-B is not positive definite");
+  }
+}
+
+// Flags accepted by the solve entries: BSE_FLAG_NATIVE_FP64 only.  Values-only
+// is a bse_syevd_dev mode (the recovery of X needs the eigenvectors).
+static int check_solve_flags(int flags) {
+  if (flags & ~BSE_FLAG_NATIVE_FP64)
+    return fail(BSE_BAD_ARGUMENT, "unsupported flag for a solve (only BSE_FLAG_NATIVE_FP64)");
+  return BSE_OK;
+}
+
+// Library-owned stream-ordered pool for the host entries' device buffers
+// (one per device).  Freed blocks stay reserved in THIS pool between calls
+// (a 0 release threshold would unmap ~20 n^2 doubles every solve); the
+// device's default pool, which torch or other libraries may use, is left
+// untouched.  bse_release_cached_memory() trims it.
+static cudaError_t host_pool(cudaMemPool_t* out) {
+  static cudaMemPool_t pools[64] = {};
+  static std::mutex mu;
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  std::lock_guard<std::mutex> lk(mu);
+  if (!pools[dev & 63]) {
+    cudaMemPoolProps props{};
+    props.allocType = cudaMemAllocationTypePinned;
+    props.handleTypes = cudaMemHandleTypeNone;
+    props.location.type = cudaMemLocationTypeDevice;
+    props.location.id = dev;
+    cudaMemPool_t p;
+    if ((e = cudaMemPoolCreate(&p, &props)) != cudaSuccess) return e;
+    uint64_t thr = UINT64_MAX;
+    if ((e = cudaMemPoolSetAttribute(p, cudaMemPoolAttrReleaseThreshold, &thr)) != cudaSuccess)
+      return e;
+    pools[dev & 63] = p;
+  }
+  *out = pools[dev & 63];
+  return cudaSuccess;
 }
 
 int bse_solve_spd_pair_dev(int64_t n, const double* dM, int64_t ldm, const double* dK,
@@ -133,6 +185,7 @@ int bse_solve_spd_pair_dev(int64_t n, const double* dM, int64_t ldm, const doubl
                            bse_info* info) {
   if (n < 0 || ldm < n || ldk < n || ldx1 < n || ldx2 < n)
     return fail(BSE_BAD_ARGUMENT, "bad dimension");
+  if (check_solve_flags(flags) != BSE_OK) return BSE_BAD_ARGUMENT;
   if (n > 0 && work_bytes < bse::solve_bytes((int)n, flags))
     return fail(BSE_BAD_ARGUMENT, "workspace too small (see bse_solve_workspace_bytes)");
   bse::SolveStatus st{};
@@ -147,20 +200,10 @@ int bse_solve_spd_pair_host(int64_t n, const double* M, int64_t ldm, const doubl
                             int64_t ldx2, int flags, bse_info* info) {
   if (n < 0 || ldm < n || ldk < n || ldx1 < n || ldx2 < n)
     return fail(BSE_BAD_ARGUMENT, "bad dimension");
+  if (check_solve_flags(flags) != BSE_OK) return BSE_BAD_ARGUMENT;
   if (n == 0) return BSE_OK;
-  // keep freed workspace in the stream-ordered pool between calls (the
-  // default release threshold of 0 would unmap ~14 n^2 doubles every call)
-  static bool pool_set[64] = {false};
-  int dev = 0;
-  cudaGetDevice(&dev);
-  if (dev < 64 && !pool_set[dev]) {
-    cudaMemPool_t pool;
-    if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
-      uint64_t thr = UINT64_MAX;
-      cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
-    }
-    pool_set[dev] = true;
-  }
+  cudaMemPool_t pool;
+  BSE_TRY_CUDA(host_pool(&pool), "memory pool");
   cudaStream_t s, s2;
   BSE_TRY_CUDA(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking), "stream");
   BSE_TRY_CUDA(cudaStreamCreateWithFlags(&s2, cudaStreamNonBlocking), "stream");
@@ -171,7 +214,7 @@ int bse_solve_spd_pair_host(int64_t n, const double* M, int64_t ldm, const doubl
   const size_t wb = bse::solve_bytes((int)n, flags);
   const size_t lam_bytes = ((sizeof(double) * n + 255) / 256) * 256;
   char* buf = nullptr;
-  cudaError_t e = cudaMallocAsync((void**)&buf, 4 * mat + lam_bytes + wb, s);
+  cudaError_t e = cudaMallocFromPoolAsync((void**)&buf, 4 * mat + lam_bytes + wb, pool, s);
   if (e != cudaSuccess) {
     cudaStreamDestroy(s);
     cudaStreamDestroy(s2);
@@ -240,9 +283,19 @@ int bse_syevd_dev(int64_t n, double* dA, int64_t lda, double* dW, double* dZ, in
   if (n < 0 || lda < n || ldz < n) return fail(BSE_BAD_ARGUMENT, "bad dimension");
   if (n > 0 && work_bytes < bse::syevd_bytes((int)n, flags))
     return fail(BSE_BAD_ARGUMENT, "workspace too small (see bse_syevd_workspace_bytes)");
-  BSE_TRY_CUDA(bse::syevd((int)n, dA, lda, dW, dZ, ldz, dWork, work_bytes, flags,
-                          (cudaStream_t)stream),
-               "syevd");
+  if (flags & ~(BSE_FLAG_VALUES_ONLY | BSE_FLAG_NATIVE_FP64))
+    return fail(BSE_BAD_ARGUMENT, "unsupported flag for bse_syevd_dev");
+  if (n == 0) return BSE_OK;
+  cudaStream_t s = (cudaStream_t)stream;
+  int* conv = nullptr;
+  BSE_TRY_CUDA(cudaMallocAsync((void**)&conv, sizeof(int), s), "alloc flag");
+  cudaError_t e = bse::syevd((int)n, dA, lda, dW, dZ, ldz, dWork, work_bytes, flags, s, 0, -1, conv);
+  int h = 0;
+  if (e == cudaSuccess) e = cudaMemcpyAsync(&h, conv, sizeof(int), cudaMemcpyDeviceToHost, s);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+  cudaFreeAsync(conv, s);
+  BSE_TRY_CUDA(e, "syevd");
+  if (h) return fail(BSE_NO_CONVERGENCE, "syevd: the tridiagonal eigensolver did not converge");
   return BSE_OK;
 }
 
@@ -257,7 +310,12 @@ int bse_stedc_dev(int64_t n, double* dD, double* dE, double* dQ, int64_t ldq, vo
   if (work_bytes < bse::stedc_bytes((int)n)) return fail(BSE_BAD_ARGUMENT, "workspace too small");
   bse::Arena a{static_cast<char*>(dWork), work_bytes, 0, false};
   bse::StedcWork w = bse::stedc_carve(a, (int)n);
-  BSE_TRY_CUDA(bse::stedc((int)n, dD, dE, dD, dQ, ldq, w, (cudaStream_t)stream), "stedc");
+  cudaStream_t s = (cudaStream_t)stream;
+  BSE_TRY_CUDA(bse::stedc((int)n, dD, dE, dD, dQ, ldq, w, s), "stedc");
+  int h = 0;
+  BSE_TRY_CUDA(cudaMemcpyAsync(&h, w.fail, sizeof(int), cudaMemcpyDeviceToHost, s), "stedc flag");
+  BSE_TRY_CUDA(cudaStreamSynchronize(s), "stedc sync");
+  if (h) return fail(BSE_NO_CONVERGENCE, "stedc: a secular root did not converge");
   return BSE_OK;
 }
 
@@ -311,7 +369,19 @@ int bse_profile_read(int max_stages, double* ms, char* names) {
   return k;
 }
 
+int bse_profile_count(void) {
+  const bse::StageLog& L = bse::stage_log();
+  return L.used > 1 ? L.used - 1 : 0;
+}
+
 long long bse_launch_count(void) { return bse::launch_counter().load(); }
+
+int bse_release_cached_memory(void) {
+  cudaMemPool_t pool;
+  BSE_TRY_CUDA(host_pool(&pool), "memory pool");
+  BSE_TRY_CUDA(cudaMemPoolTrimTo(pool, 0), "trim");
+  return BSE_OK;
+}
 
 int bse_peak_fp64(int which, int blocks, int iters, int reps, double* flops, double* ms) {
   double* sink = nullptr;
@@ -406,7 +476,7 @@ int bse_solve_spd_pair_dist_dev(bse_comm* comm, int64_t n, const double* dM, int
                                 int64_t ldx1, double* dX2, int64_t ldx2, void* dWork,
                                 size_t work_bytes, int flags, void* stream, bse_info* info) {
   if (!comm) return fail(BSE_BAD_ARGUMENT, "null communicator");
-  if (flags & BSE_FLAG_VALUES_ONLY) return fail(BSE_BAD_ARGUMENT, "values-only is single-GPU");
+  if (check_solve_flags(flags) != BSE_OK) return BSE_BAD_ARGUMENT;
   if (n < 0 || ldm < n || ldk < n || ldx1 < n || ldx2 < n)
     return fail(BSE_BAD_ARGUMENT, "bad dimension");
   if (n > 0 && work_bytes < bse::solve_bytes((int)n, flags))

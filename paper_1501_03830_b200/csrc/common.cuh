@@ -130,6 +130,30 @@ BSE_DEV void st_release(int* p, int v) {
 
 BSE_HD long long ceil_div(long long a, long long b) { return (a + b - 1) / b; }
 
+// One-time per-kernel setup that applies to the CURRENT device only
+// (cudaFuncSetAttribute): one bit per device ordinal, so a process that later
+// solves on another device repeats the setup there.
+struct PerDeviceOnce {
+  std::atomic<unsigned long long> bits{0};
+  static int ordinal() {
+    int d = 0;
+    cudaGetDevice(&d);
+    return d & 63;
+  }
+  bool needed() const { return !((bits.load(std::memory_order_acquire) >> ordinal()) & 1ull); }
+  void mark() { bits.fetch_or(1ull << ordinal(), std::memory_order_acq_rel); }
+};
+
+// Raise a kernel's dynamic shared-memory limit once per device; returns the
+// runtime's error (not swallowed).
+template <class F>
+inline cudaError_t set_smem_limit(PerDeviceOnce& once, F* kern, int bytes) {
+  if (!once.needed()) return cudaSuccess;
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+  if (e == cudaSuccess) once.mark();
+  return e;
+}
+
 // Host-side count of kernel launches issued by this library (bench evidence).
 inline std::atomic<long long>& launch_counter() {
   static std::atomic<long long> c{0};

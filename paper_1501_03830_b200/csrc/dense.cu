@@ -83,6 +83,14 @@ __global__ void __launch_bounds__(2 * kLeaf) potf2_kernel(double* A, long long l
     }
   }
   __syncthreads();
+  if (threadIdx.x == 0 && n > 0) {
+    // smallest pivot L_jj^2 of this leaf -> st->aux (positive doubles order
+    // like their bit patterns, so an integer atomicMin is a double min)
+    double mn = dsq[0] * dsq[0];
+    for (int j = 1; j < n; ++j) mn = fmin(mn, dsq[j] * dsq[j]);
+    atomicMin(reinterpret_cast<unsigned long long*>(&st->aux),
+              (unsigned long long)__double_as_longlong(mn));
+  }
   // scale: L_rc = T_rc / sqrt(T_cc), write back
   for (int idx = threadIdx.x; idx < kLeaf * kLeaf; idx += blockDim.x) {
     const int i = idx & (kLeaf - 1), c = idx >> 6;  // i fastest: coalesced
@@ -234,12 +242,9 @@ __global__ void symmetrize_kernel(double* A, long long lda, int n) {
 constexpr size_t kLeafSmem = 2 * kLeaf * kLds * sizeof(double);
 
 template <auto Kern>
-void ensure_smem() {
-  static bool done = false;  // one flag per kernel
-  if (!done) {
-    cudaFuncSetAttribute(Kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kLeafSmem);
-    done = true;
-  }
+cudaError_t ensure_smem() {
+  static PerDeviceOnce once;  // one flag set per kernel, one bit per device
+  return set_smem_limit(once, Kern, (int)kLeafSmem);
 }
 
 // Per-device scratch for leaf inverses (64 x 64), allocated once.
@@ -373,7 +378,7 @@ static cudaError_t potrf_rec(double* A, long long lda, int n, int off, DevStatus
     // a leaf still owing pieces: deliver them (in column order) first
     for (int L = 1; hook && L <= hook->depth; ++L)
       if ((e = hook->fn(hook->ctx, L, s)) != cudaSuccess) return e;
-    ensure_smem<potf2_kernel>();
+    if ((e = ensure_smem<potf2_kernel>()) != cudaSuccess) return e;
     potf2_kernel<<<1, 2 * kLeaf, kLeafSmem, s>>>(A, lda, n, off, st, inv);
     count_launch();
     return cudaGetLastError();

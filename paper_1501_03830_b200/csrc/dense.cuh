@@ -12,7 +12,7 @@ struct DevStatus {
   int info;       // -1: ok; >= 0: index of the first non-positive pivot
   int conv_fail;  // nonzero: an iterative kernel did not converge
   double value;   // failing pivot value
-  double aux;     // spare (e.g. pivot margin)
+  double aux;     // min pivot L_jj^2 (initialise to +inf; atomicMin over the leaves)
 };
 
 // In-place lower Cholesky of the n x n matrix A (column-major, lda); the

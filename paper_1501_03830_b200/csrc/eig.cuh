@@ -112,6 +112,7 @@ struct StedcWork {
   void* oz = nullptr;            // emulated-FP64 workspace for the top merges (optional)
   size_t oz_bytes = 0;
   double* scal = nullptr;  // scaling scalar(s)
+  int* fail = nullptr;     // set nonzero when a secular root misses its bound (reset per stedc)
 };
 size_t stedc_bytes(int n);
 StedcWork stedc_carve(Arena& a, int n);
@@ -120,16 +121,21 @@ cudaError_t stedc(int n, double* d, double* e, double* w, double* Q, long long l
                   const StedcWork& ws, cudaStream_t s);
 
 // Values only: ascending eigenvalues of the tridiagonal by Sturm bisection.
+// *fail (device int, may be null) is set nonzero when a value's bracket does
+// not reach the convergence width of kernels.py:275-299 or is not finite.
 cudaError_t tridiag_values(int n, const double* d, const double* e, double* w, double* scratch3,
-                           cudaStream_t s);
+                           cudaStream_t s, int* fail = nullptr);
 
 // Full pipeline on a symmetric matrix (lower triangle of A read, destroyed).
 size_t syevd_bytes(int n, int flags);
 // zc0/zc1: back-transform only Z columns [zc0, zc1) (the column shard of a
 // distributed solve; D&C still produces every column).  zc1 < 0 means n.
+// conv_out (device int, may be null): nonzero after the call completes when
+// the tridiagonal eigensolver did not converge (maps to BSE_NO_CONVERGENCE,
+// the analogue of kernels.ConvergenceError, kernels.py:403-419).
 cudaError_t syevd(int n, double* A, long long lda, double* w, double* Z, long long ldz,
                   void* work, size_t work_bytes, int flags, cudaStream_t s, int zc0 = 0,
-                  int zc1 = -1);
+                  int zc1 = -1, int* conv_out = nullptr);
 
 int device_sm_count();
 

@@ -256,8 +256,8 @@ template <int BM, int BN, int BK, int WM, int WN, int STAGES, bool TA, bool TB, 
 cudaError_t launch(const GemmProblem* single, const GemmProblem* grouped, int count, int maxM,
                    int maxN, cudaStream_t s) {
   using C = Cfg<BM, BN, BK, WM, WN, STAGES, TA, TB>;
-  static bool attr_done = false;  // per-instantiation, set once per process
-  if (!attr_done) {
+  static PerDeviceOnce attr_once;  // per instantiation, per device
+  if (attr_once.needed()) {
     cudaError_t e = cudaFuncSetAttribute(gemm_single_kernel<BM, BN, BK, WM, WN, STAGES, TA, TB, VEC, true>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM);
     if (e != cudaSuccess) return e;
@@ -267,7 +267,7 @@ cudaError_t launch(const GemmProblem* single, const GemmProblem* grouped, int co
     e = cudaFuncSetAttribute(gemm_grouped_kernel<BM, BN, BK, WM, WN, STAGES, TA, TB, VEC>,
                              cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM);
     if (e != cudaSuccess) return e;
-    attr_done = true;
+    attr_once.mark();
   }
   dim3 grid((unsigned)ceil_div(maxM, BM), (unsigned)ceil_div(maxN, BN), (unsigned)count);
   if (grid.x == 0 || grid.y == 0 || count == 0) return cudaSuccess;

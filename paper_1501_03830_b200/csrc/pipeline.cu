@@ -146,7 +146,8 @@ size_t syevd_bytes(int n, int flags) {
 }
 
 cudaError_t syevd(int n, double* A, long long lda, double* w, double* Z, long long ldz,
-                  void* work, size_t work_bytes, int flags, cudaStream_t s, int zc0, int zc1) {
+                  void* work, size_t work_bytes, int flags, cudaStream_t s, int zc0, int zc1,
+                  int* conv_out) {
   if (n <= 0) return cudaSuccess;
   Arena a{static_cast<char*>(work), work_bytes, 0, false};
   SyevdWork ws = carve_syevd(a, n, flags);
@@ -166,7 +167,8 @@ cudaError_t syevd(int n, double* A, long long lda, double* w, double* Z, long lo
     return e;
   if (flags & 0x1) {  // BSE_FLAG_VALUES_ONLY: no vectors, no back-transforms
     stage_mark("values", s);
-    return tridiag_values(n, ws.d, ws.e, w, ws.dc.scal, s);
+    if (conv_out && (e = cudaMemsetAsync(conv_out, 0, sizeof(int), s)) != cudaSuccess) return e;
+    return tridiag_values(n, ws.d, ws.e, w, ws.dc.scal, s, conv_out);
   }
   // The Q2 blocks (from the bulge-chasing reflectors) and the Q1 group T
   // factors (from the SY2SB panels) do not depend on the divide and conquer:
@@ -188,6 +190,9 @@ cudaError_t syevd(int n, double* A, long long lda, double* w, double* Z, long lo
   if ((e = cudaStreamWaitEvent(side.hp, side.hp_fork, 0)) != cudaSuccess) return e;
   stage_mark("stedc", side.hp);
   if ((e = stedc(n, ws.d, ws.e, w, Z, ldz, ws.dc, side.hp)) != cudaSuccess) return e;
+  if (conv_out && (e = cudaMemcpyAsync(conv_out, ws.dc.fail, sizeof(int), cudaMemcpyDeviceToDevice,
+                                       side.hp)) != cudaSuccess)
+    return e;
   if ((e = cudaEventRecord(side.hp_join, side.hp)) != cudaSuccess) return e;
   if ((e = cudaStreamWaitEvent(s, side.hp_join, 0)) != cudaSuccess) return e;
   if (mode == 2) {
@@ -364,6 +369,42 @@ cudaError_t rows_out_hook(void* ctx, int r0, int r1, cudaStream_t s) {
                            cudaMemcpyDeviceToHost, o.hout->stream);
 }
 
+// Definiteness failure report (after K's Cholesky failed, or after W lost
+// definiteness): the reference factors A+B first (solvers.py:97-98), so M is
+// probed and reported if it fails; else K's failure, else a non-positive
+// spectrum of W with both factors definite (code 5).
+cudaError_t definiteness_failure(int n, const double* M, long long ldm, const SolveWork& w,
+                                 const DevStatus& hk, cudaStream_t s, SolveStatus* out) {
+  cudaError_t e;
+  const long long ld = w.ld;
+  copy_lower_kernel<<<nb_all(n), 256, 0, s>>>(n, M, ldm, w.W, ld);
+  count_launch();
+  DevStatus* stm = &w.st[1];
+  const DevStatus h0{-1, 0, 0.0, HUGE_VAL};
+  if ((e = cudaMemcpyAsync(stm, &h0, sizeof(DevStatus), cudaMemcpyHostToDevice, s)) != cudaSuccess)
+    return e;
+  if ((e = potrf_lower(w.W, ld, n, stm, s)) != cudaSuccess) return e;
+  DevStatus hm;
+  if ((e = cudaMemcpyAsync(&hm, stm, sizeof(hm), cudaMemcpyDeviceToHost, s)) != cudaSuccess) return e;
+  if ((e = cudaStreamSynchronize(s)) != cudaSuccess) return e;
+  out->code = 1;
+  if (hm.info >= 0) {
+    out->failed_factor = 1;
+    out->pivot_index = hm.info;
+    out->pivot_value = hm.value;
+  } else if (hk.info >= 0) {
+    out->failed_factor = 0;
+    out->pivot_index = hk.info;
+    out->pivot_value = hk.value;
+  } else {
+    out->code = 5;  // M and K definite, but some lambda^2 <= 0 in floating point
+    out->failed_factor = -1;
+    out->pivot_index = -1;
+    out->pivot_value = 0.0;
+  }
+  return cudaSuccess;
+}
+
 }  // namespace
 
 void kpieces_plan(int n, int depth, KPieces* kp) {
@@ -402,6 +443,7 @@ cudaError_t solve_spd_pair(int n, const double* M, long long ldm, const double* 
   out->pivot_index = -1;
   out->pivot_value = 0.0;
   out->failed_factor = -1;
+  out->min_pivot = 0.0;
   if (n <= 0) return cudaSuccess;
   Arena a{static_cast<char*>(work), work_bytes, 0, false};
   SolveWork w = carve_solve(a, n, flags);
@@ -410,7 +452,7 @@ cudaError_t solve_spd_pair(int n, const double* M, long long ldm, const double* 
   const long long tot = (long long)n * n;
   const unsigned nb = (unsigned)ceil_div(tot, 256);
   cudaError_t e;
-  DevStatus h0[2] = {{-1, 0, 0.0, 0.0}, {-1, 0, 0.0, 0.0}};
+  DevStatus h0[2] = {{-1, 0, 0.0, HUGE_VAL}, {-1, 0, 0.0, HUGE_VAL}};
   if ((e = cudaMemcpyAsync(w.st, h0, sizeof(h0), cudaMemcpyHostToDevice, s)) != cudaSuccess) return e;
   // 1. K = L L^T
   stage_mark("potrf", s);
@@ -440,6 +482,16 @@ cudaError_t solve_spd_pair(int n, const double* M, long long ldm, const double* 
       return e;
   }
   if (m_ready && (e = cudaStreamWaitEvent(s, m_ready, 0)) != cudaSuccess) return e;
+  {
+    // K's definiteness is known now: stop before any further O(n^3) work
+    // (one host sync; the reference raises from cholesky() at this point,
+    // solvers.py:97-98, after probing A+B first)
+    DevStatus hk;
+    if ((e = cudaMemcpyAsync(&hk, &w.st[0], sizeof(hk), cudaMemcpyDeviceToHost, s)) != cudaSuccess)
+      return e;
+    if ((e = cudaStreamSynchronize(s)) != cudaSuccess) return e;
+    if (hk.info >= 0) return definiteness_failure(n, M, ldm, w, hk, s, out);
+  }
   stage_mark("congruence", s);
   // Distributed: this rank forms the column block [c0, c1) of T1 and W, then
   // every block is broadcast from its owner (the only exchange before the
@@ -498,7 +550,7 @@ cudaError_t solve_spd_pair(int n, const double* M, long long ldm, const double* 
   // D&C are replicated; only this rank's eigenvector columns (output columns
   // [c0, c1) = Z columns [n - c1, n - c0)) are back-transformed.
   if ((e = syevd(n, w.W, ld, w.lam2, w.T1, ld, w.eig, w.eig_bytes, flags, s, (int)(n - c1),
-                 (int)(n - c0))) != cudaSuccess)
+                 (int)(n - c0), &w.st[0].conv_fail)) != cudaSuccess)
     return e;
   stage_mark("recover", s);
   // 4. descending order; v = Z Lam into W, Z reversed into Zr
@@ -574,31 +626,17 @@ cudaError_t solve_spd_pair(int n, const double* M, long long ldm, const double* 
 
   if ((e = cudaMemcpyAsync(hs, w.st, sizeof(hs), cudaMemcpyDeviceToHost, s)) != cudaSuccess) return e;
   if ((e = cudaStreamSynchronize(s)) != cudaSuccess) return e;
-  if (hs[0].info >= 0 || hs[1].conv_fail) {
-    // Definiteness failure: the reference factors A+B first (solvers.py:97-98),
-    // so probe M before reporting K.
-    copy_lower_kernel<<<nb, 256, 0, s>>>(n, M, ldm, w.W, ld);
-    count_launch();
-    DevStatus* stm = &w.st[1];
-    if ((e = cudaMemcpyAsync(stm, h0, sizeof(DevStatus), cudaMemcpyHostToDevice, s)) != cudaSuccess) return e;
-    if ((e = potrf_lower(w.W, ld, n, stm, s)) != cudaSuccess) return e;
-    DevStatus hm;
-    if ((e = cudaMemcpyAsync(&hm, stm, sizeof(hm), cudaMemcpyDeviceToHost, s)) != cudaSuccess) return e;
-    if ((e = cudaStreamSynchronize(s)) != cudaSuccess) return e;
-    out->code = 1;
-    if (hm.info >= 0) {
-      out->failed_factor = 1;
-      out->pivot_index = hm.info;
-      out->pivot_value = hm.value;
-    } else if (hs[0].info >= 0) {
-      out->failed_factor = 0;
-      out->pivot_index = hs[0].info;
-      out->pivot_value = hs[0].value;
-    } else {
-      out->failed_factor = 1;  // M numerically PD but W lost definiteness
-      out->pivot_index = -1;
-      out->pivot_value = 0.0;
-    }
+  out->min_pivot = hs[0].aux;
+  if (hs[0].conv_fail) {
+    // a secular root of the divide and conquer missed its bound
+    // (kernels.ConvergenceError, kernels.py:403-419)
+    out->code = 2;
+    return cudaSuccess;
+  }
+  if (hs[1].conv_fail) {
+    // W = L^T M L lost definiteness: M is probed (A+B first, as the
+    // reference); if M factors, the spectrum itself is not positive
+    return definiteness_failure(n, M, ldm, w, hs[0], s, out);
   }
   return cudaSuccess;
 }

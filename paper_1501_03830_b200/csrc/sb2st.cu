@@ -447,13 +447,8 @@ cudaError_t sb2st(double* AB, int ldab, int n, int b, double* d, double* e, doub
   if (n > 2) {
     if ((err = cudaMemsetAsync(progress, 0, sizeof(int) * 2 * (size_t)n, s)) != cudaSuccess) return err;
     const size_t smem = sizeof(SbfSmem);
-    static bool attr = false;
-    if (!attr) {
-      err = cudaFuncSetAttribute(sb2st_fused_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 (int)smem);
-      if (err != cudaSuccess) return err;
-      attr = true;
-    }
+    static PerDeviceOnce attr;
+    if ((err = set_smem_limit(attr, sb2st_fused_kernel, (int)smem)) != cudaSuccess) return err;
     // one CTA per SM: the kernel is latency-bound and one resident step per
     // SM keeps every hand-off on an otherwise idle SM
     const int grid = std::max(1, std::min(n - 2, num_sms));

@@ -30,10 +30,12 @@ SideStream& side_stream();
 double launch_peak(int which, int blocks, int iters, double* sink, cudaStream_t s);
 
 struct SolveStatus {
-  int code;            // 0 ok, 1 not positive definite
+  int code;            // 0 ok, 1 not positive definite, 2 no convergence,
+                       // 5 spectrum not positive (M, K definite; some lambda^2 <= 0)
   long long pivot_index;
   double pivot_value;
   int failed_factor;   // 0: K (A-B), 1: M (A+B)
+  double min_pivot;    // min_j L_jj^2 of K's factor (code 0)
 };
 
 // Host-entry upload of K by column pieces (see PotrfHook): piece 0 =

@@ -187,6 +187,10 @@ __global__ void __launch_bounds__(kDcThreads) dc_prepare_kernel(
 // One thread per root left the top merges at ~3 warps per SM, latency-bound
 // on the dependent FP64 reciprocals.
 constexpr int kSecLanes = 8;
+// iteration budget per root: the safeguarded rational step converges in a
+// handful of sweeps (LAPACK's dlaed4 gives up after 30 and fails the whole
+// dstedc); a root still unconverged after 200 is reported, not returned
+constexpr int kSecMaxIter = 200;
 
 __device__ __forceinline__ double group_sum(double v, unsigned mask) {
 #pragma unroll
@@ -234,7 +238,8 @@ __global__ void dc_secular_kernel(Level L, int n, StedcWork w) {
   const double d0 = dk[org];
   const double dl = dk[pl] - d0, dr = dk[pr] - d0;
   double t = 0.5 * (a + b);
-  for (int it = 0; it < 60; ++it) {
+  bool conv = false;
+  for (int it = 0; it < kSecMaxIter; ++it) {
     double psi = 0.0, dpsi = 0.0, phi = 0.0, dphi = 0.0;
     for (int j = lane; j <= pl; j += kSecLanes) {
       const double inv = 1.0 / ((dk[j] - d0) - t);
@@ -256,9 +261,9 @@ __global__ void dc_secular_kernel(Level L, int n, StedcWork w) {
     // rounding-error bound of the computed f (cf. dlaed4's ERRETM): once |f|
     // is below it the iterate is a root to working accuracy
     const double erretm = 8.0 * rho * (fabs(psi) + fabs(phi)) + 2.0;
-    if (fabs(f) <= kEps * erretm) break;
+    if (fabs(f) <= kEps * erretm) { conv = true; break; }
     if (f > 0.0) b = t; else a = t;
-    if (b - a <= 2.0 * kEps * fmax(fabs(a), fabs(b))) { t = 0.5 * (a + b); break; }
+    if (b - a <= 2.0 * kEps * fmax(fabs(a), fabs(b))) { t = 0.5 * (a + b); conv = true; break; }
     const double P0 = dl - t, Q0 = dr - t;
     const double b1 = dpsi * P0 * P0, a1 = psi - dpsi * P0;
     const double b2 = dphi * Q0 * Q0, a2 = phi - dphi * Q0;
@@ -276,9 +281,12 @@ __global__ void dc_secular_kernel(Level L, int n, StedcWork w) {
     if (!(tn > a && tn < b)) tn = 0.5 * (a + b);
     const bool done = fabs(tn - t) <= 2.0 * kEps * fabs(tn);
     t = tn;
-    if (done) break;
+    if (done) { conv = true; break; }
   }
   if (lane != 0) return;
+  // the bracket never reached working accuracy (or the data are not finite):
+  // reported as BSE_NO_CONVERGENCE rather than returned silently
+  if (w.fail && (!conv || !isfinite(t))) atomicOr(w.fail, 1);
   w.org[lo + i] = org;
   w.tau[lo + i] = t;
   w.val[lo + i] = d0 + t;
@@ -472,11 +480,14 @@ __global__ void copy_matrix_kernel(int rows, int cols, const double* src, long l
 // (kernels.py:275-299).
 __global__ void sturm_bisect_kernel(int n, const double* __restrict__ d,
                                     const double* __restrict__ e, double* __restrict__ w,
-                                    const double* __restrict__ bounds) {
+                                    const double* __restrict__ bounds, int* fail) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
   const double pivmin = bounds[2];
   double lo = bounds[0], hi = bounds[1];
+  // like the reference (kernels.py:275-299, <= 160 halvings then the
+  // midpoint), running out of halvings is not an error; a non-finite bracket
+  // (NaN/Inf in d or e) is
   for (int it = 0; it < 200; ++it) {
     if (!(hi - lo > 2.0 * kEps * (fabs(lo) + fabs(hi)) + 2.0 * kSafmin)) break;
     const double x = 0.5 * (lo + hi);
@@ -491,6 +502,7 @@ __global__ void sturm_bisect_kernel(int n, const double* __restrict__ d,
     }
     if (cnt > i) hi = x; else lo = x;
   }
+  if (fail && !(isfinite(lo) && isfinite(hi))) atomicOr(fail, 1);
   w[i] = 0.5 * (lo + hi);
 }
 
@@ -528,11 +540,11 @@ __global__ void gershgorin_kernel(int n, const double* d, const double* e, doubl
 }  // namespace
 
 cudaError_t tridiag_values(int n, const double* d, const double* e, double* w, double* scratch3,
-                           cudaStream_t s) {
+                           cudaStream_t s, int* fail) {
   if (n <= 0) return cudaSuccess;
   gershgorin_kernel<<<1, 1024, 0, s>>>(n, d, e, scratch3);
   count_launch();
-  sturm_bisect_kernel<<<(unsigned)ceil_div(n, 128), 128, 0, s>>>(n, d, e, w, scratch3);
+  sturm_bisect_kernel<<<(unsigned)ceil_div(n, 128), 128, 0, s>>>(n, d, e, w, scratch3, fail);
   count_launch();
   return cudaGetLastError();
 }
@@ -566,6 +578,7 @@ StedcWork stedc_carve(Arena& a, int n) {
   w.counts = a.take<int>(3 * (size_t)n + 3);
   w.probs = a.take<GemmProblem>(2 * (size_t)n + 2);
   w.scal = a.take<double>(4);
+  w.fail = a.take<int>(4);
   return w;
 }
 
@@ -581,6 +594,7 @@ cudaError_t stedc(int n, double* d, double* e, double* wout, double* Q, long lon
   if (n <= 0) return cudaSuccess;
   cudaError_t err;
   const long long ld = ws.ld;
+  if (ws.fail && (err = cudaMemsetAsync(ws.fail, 0, sizeof(int), s)) != cudaSuccess) return err;
   absmax_kernel<<<1, 1024, 0, s>>>(n, d, e, ws.scal);
   count_launch();
   dc_init_kernel<<<(unsigned)ceil_div(n, 256), 256, 0, s>>>(n, d, e, ws.Da, ws.Qa, ld, ws.scal);

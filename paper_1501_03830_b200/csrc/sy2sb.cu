@@ -247,12 +247,14 @@ cudaError_t panel_qr(double* P, long long ldp, int m, int bw, double* V, long lo
   const int G = (int)ceil_div(m, R);
   if (G > num_sms) return cudaErrorInvalidValue;
   const size_t smem = panel_smem_bytes(R, bw);
-  static size_t attr[3] = {0, 0, 0};
+  // largest limit set so far, per (variant, device): the attribute is per device
+  static std::atomic<size_t> attr[3][64];
   void* fn = rpt == 1 ? (void*)panel_qr_kernel<1> : (void*)panel_qr_kernel<2>;
-  if (smem > attr[rpt]) {
+  std::atomic<size_t>& lim = attr[rpt][PerDeviceOnce::ordinal()];
+  if (smem > lim.load()) {
     cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
-    attr[rpt] = smem;
+    lim.store(smem);
   }
   cudaError_t e = cudaMemsetAsync(bar, 0, sizeof(unsigned), s);
   if (e != cudaSuccess) return e;

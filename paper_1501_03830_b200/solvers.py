@@ -18,8 +18,8 @@ import numpy as np
 from . import _lib
 from .device import (colmajor_empty, from_device_colmajor, ptr, require_cuda, stream_ptr,
                      to_device_colmajor, view_colmajor)
-from .types import (EPS, BseOperator, NotPositiveDefinite, PositiveEigensystem,
-                    conditioning_warnings)
+from .types import (EPS, BseOperator, ConvergenceError, NotPositiveDefinite,
+                    PositiveEigensystem, conditioning_warnings)
 
 _WHAT_M = "the definiteness embedding M"
 
@@ -48,14 +48,28 @@ def solve_pair_device(Mt, ldm: int, Kt, ldk: int, n: int, flags: int = 0):
     st = lib.bse_solve_spd_pair_dev(n, ptr(Mt), ldm, ptr(Kt), ldk, ptr(lam), ptr(X1), ld,
                                     ptr(X2), ld, ptr(work), wb, flags, stream_ptr(dev),
                                     C.byref(info))
+    raise_for_status(st, info, "bse_solve_spd_pair_dev")
+    return lam[:n], X1, X2, ld
+
+
+def raise_for_status(st: int, info, where: str) -> None:
+    """Map a C-ABI status to the reference's exceptions (kernels.py:25-36,
+    core.py:159-160): 1 -> NotPositiveDefinite("A+B" | "A-B"), 2 ->
+    ConvergenceError, 3 and 5 -> ValueError, 4 -> RuntimeError."""
+    if st == _lib.BSE_OK:
+        return
     if st == _lib.BSE_NOT_POSITIVE_DEFINITE:
         err = NotPositiveDefinite(int(info.pivot_index), float(info.pivot_value),
                                   "A+B" if info.failed_factor == 1 else "A-B")
         err.failed_factor = int(info.failed_factor)
         raise err
-    if st != _lib.BSE_OK:
-        raise RuntimeError(f"bse_solve_spd_pair_dev failed ({st}): {_lib.last_error()}")
-    return lam[:n], X1, X2, ld
+    if st == _lib.BSE_NO_CONVERGENCE:
+        raise ConvergenceError(f"{where}: {_lib.last_error()}")
+    if st == _lib.BSE_SPECTRUM_NOT_POSITIVE:
+        raise ValueError("all eigenvalues must be strictly positive")
+    if st == _lib.BSE_BAD_ARGUMENT:
+        raise ValueError(f"{where}: {_lib.last_error()}")
+    raise RuntimeError(f"{where} failed ({st}): {_lib.last_error()}")
 
 
 def _device():
@@ -272,8 +286,7 @@ def syevd_values_device(At, lda: int, n: int):
     work = torch.empty(max(int(wb), 1), dtype=torch.uint8, device=dev)
     st = lib.bse_syevd_dev(n, ptr(At), lda, ptr(w), 0, n, ptr(work), wb, _lib.FLAG_VALUES_ONLY,
                            stream_ptr(dev))
-    if st != _lib.BSE_OK:
-        raise RuntimeError(f"bse_syevd_dev failed ({st}): {_lib.last_error()}")
+    raise_for_status(st, None, "bse_syevd_dev")
     return w[:n]
 
 
