@@ -267,56 +267,146 @@ class ClockSampler:
                 "samples": len(sm)}
 
 
-def run_ours_cfg1(args):
-    """BASELINE config 1: complex Hermitian BSE n = 2048 (real embedding
-    N = 4096), all eigenpairs incl. the complex extraction and the
-    biorthogonality polish -- the solve_complex device path."""
+def run_ours_complex(args):
+    """BASELINE config 1 (complex n = 2048) or 3 (complex n = 16384; real
+    embedding N = 32768): all eigenpairs, X1/X2 and the complex extraction.
+    value: bse_solve_complex_dev on device-resident A, B (CUDA events);
+    e2e: the public drop-in call solve_complex(op) on host numpy arrays
+    (uploads, the solve and the downloads inside the timed region)."""
     import numpy as np
     import torch
 
     import paper_1501_03830_b200 as bg
-    from paper_1501_03830_b200 import configs, solvers
-    from paper_1501_03830_b200.device import to_device_colmajor
+    from paper_1501_03830_b200 import _lib, configs
+    from paper_1501_03830_b200.device import ptr
 
     rank, local_rank, world = env_rank()
     torch.cuda.set_device(local_rank)
     dev = torch.device("cuda", local_rank)
-    n = 2048
-    a, b, _, a_vals = configs.complex_operator(n, seed=1 + rank)
-    op = bg.make_operator(a, b, kind="complex")
-    m, k = solvers.real_embedding(op)
-    Mt, ldm = to_device_colmajor(m, dev)
-    Kt, ldk = to_device_colmajor(k, dev)
+    lib = _lib.load(strict=True)
+    c = configs.CONFIGS[args.config]
+    n = args.n or c["n"]
+    A, B, _, a_vals = configs.torch_complex_operator(n, seed=args.config, lo=c["lo"], hi=c["hi"],
+                                                     bnorm=c["bnorm"], device=dev)
+    stream = torch.cuda.current_stream(dev)
+    sp = stream.cuda_stream
+    X1 = torch.empty((n, n), dtype=torch.complex128, device=dev)
+    X2 = torch.empty((n, n), dtype=torch.complex128, device=dev)
+    lam = torch.empty(n, dtype=torch.float64, device=dev)
+    wb = lib.bse_solve_complex_workspace_bytes(n, 0)
+    work = torch.empty(wb, dtype=torch.uint8, device=dev)
+    info = _lib.BseInfo()
 
     def step():
-        lam2, X1, X2, ld = solvers.solve_pair_device(Mt, ldm, Kt, ldk, 2 * n)
-        return solvers._select_and_polish(lam2, X1, X2, ld, n, dev)
+        st = lib.bse_solve_complex_dev(n, ptr(A), n, ptr(B), n, ptr(lam), ptr(X1), n, ptr(X2), n,
+                                       ptr(work), wb, 0, sp, C.byref(info))
+        if st != 0:
+            raise RuntimeError(f"complex solve failed ({st}): {_lib.last_error()}")
 
+    fl, msv = C.c_double(), C.c_double()
+    lib.bse_peak_fp64(0, 296, 20000, 5, C.byref(fl), C.byref(msv))
+    fp64_peak = fl.value / (msv.value * 1e-3) / 1e12
     for _ in range(args.warmup):
         step()
     torch.cuda.synchronize(dev)
-    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    ev0.record()
-    for _ in range(args.steps):
-        lam, X1c, X2c = step()
-    ev1.record()
+    clocks = ClockSampler(local_rank)
+    time.sleep(0.3)
+    launches0 = lib.bse_launch_count()
+    evs = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps + 1)]
+    evs[0].record(stream)
+    for i in range(args.steps):
+        if i == args.steps - 1:
+            lib.bse_profile_enable(1)
+        step()
+        evs[i + 1].record(stream)
     torch.cuda.synchronize(dev)
-    ms = ev0.elapsed_time(ev1) / args.steps
-    ok = bool(np.all(lam > 0) and bg.dos_dominance(lam, a_vals))
-    if rank == 0:
-        print(json.dumps({
-            "metric": "full BSE eigenpair time-to-solution (s)", "value": ms / 1e3, "unit": "s",
-            "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
-            "higher_is_better": False, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-            "data": "synthetic (BASELINE cfg1 recipe, numpy PCG64 seed 1)",
-            "config": {"workload": "cfg1 complex BSE n=2048 (real embedding N=4096), all "
-                                   "eigenpairs + complex extraction + biorthogonality polish",
-                       "n": n, "parallelism": "single GPU"},
-            "tflops_canonical": alg_flops(2 * n) / (ms / 1e3) / 1e12,
-            "reference_measured_s": 366.0,
-            "reference_note": "reference solve_complex at this config took 366 s on the survey "
-                              "host (SURVEY 6, BASELINE.md 2)",
-            "sanity_lambda_positive_tda": ok}), flush=True)
+    launches = lib.bse_launch_count() - launches0
+    clk = clocks.stop()
+    ms = evs[0].elapsed_time(evs[-1]) / args.steps
+    cnt = lib.bse_profile_count()
+    msarr = (C.c_double * max(cnt, 1))()
+    names = C.create_string_buffer(32 * max(cnt, 1))
+    got = lib.bse_profile_read(cnt, msarr, names)
+    lib.bse_profile_enable(0)
+    stages = {}
+    for i in range(got):
+        nm = names.raw[32 * i:32 * (i + 1)].split(b"\0")[0].decode()
+        if nm != "end":
+            stages[nm] = stages.get(nm, 0.0) + msarr[i]
+    clusters = int(info.clusters)
+    del work
+    torch.cuda.empty_cache()
+    # verification on every pair (outside the timed region; torch complex
+    # GEMMs): H x_j = lam_j x_j with H = [[A, B], [-conj B, -conj A]],
+    # X1^H X1 - X2^H X2 = I, positivity / order, the TDA bound lam_j <= a_j
+    lamc = lam.to(torch.complex128)
+    r_top = A @ X1 + B @ X2 - X1 * lamc
+    r_bot = -(B.conj() @ X1) - A.conj() @ X2 - X2 * lamc
+    res = torch.sqrt((r_top.abs() ** 2).sum(0) + (r_bot.abs() ** 2).sum(0))
+    xn = torch.sqrt((X1.abs() ** 2).sum(0) + (X2.abs() ** 2).sum(0))
+    del r_top, r_bot
+    hn = float(lam[0])  # ||H||_2 >= lam_max; the gate uses lam_max ||x||
+    pair_res = float((res / (hn * xn)).max())
+    G = X1.conj().T @ X1 - X2.conj().T @ X2
+    G.diagonal().sub_(1.0)
+    bio = float(torch.linalg.matrix_norm(G))
+    del G
+    lam_h = lam.cpu().numpy()
+    tda = bool(bg.dos_dominance(lam_h, a_vals.cpu().numpy()))
+    verification = {"max_pair_residual": pair_res, "biorthogonality_fro": bio,
+                    "pairs_checked": n, "lambda_positive_desc":
+                        bool(np.all(lam_h > 0) and np.all(np.diff(lam_h) <= 0)),
+                    "tda_bound": tda,
+                    "gate": "<= 1e-13 n and <= 1e-12 n (SURVEY 8c(8)); lam_j(H) <= lam_j(A)"}
+    verification["pass"] = bool(pair_res <= 1e-13 * n and bio <= 1e-12 * n and tda and
+                                verification["lambda_positive_desc"])
+    # e2e through the public API: host numpy in, host numpy out
+    e2e = None
+    if args.e2e_steps > 0:
+        a_h = A.cpu().numpy()
+        b_h = B.cpu().numpy()
+        del A, B, X1, X2, lamc, res, xn
+        torch.cuda.empty_cache()
+        op = bg.make_operator(a_h, b_h, kind="complex")
+        bg.solve_complex(op)  # warm the library's memory pool
+        t0 = time.perf_counter()
+        for _ in range(args.e2e_steps):
+            pos = bg.solve_complex(op)
+        e2e_s = (time.perf_counter() - t0) / args.e2e_steps
+        e2e = {"value": e2e_s, "unit": "s", "h2d_bytes_per_step": 2 * 16 * n * n,
+               "d2h_bytes_per_step": 2 * 16 * n * n + 8 * n,
+               "path": "solve_complex(op) (numpy complex128 A, B -> PositiveEigensystem)",
+               "max_rel_lambda_diff_vs_device": float(np.max(np.abs(pos.lambda_plus - lam_h)
+                                                             / lam_h))}
+    cpu = None
+    if not args.no_cpu_baseline and args.config == 3:
+        v, cores, sample, _ = cpu_reference_sample(n, inputs=(a_h, b_h, (0.2, 19.0)))
+        cpu = {"value": v, "unit": "s", "cores": cores, "kind": "port", "sample": sample}
+    N = 2 * n
+    band = 64
+    sb_ms = stages.get("sb2st", 0.0)
+    bw = None
+    if sb_ms:
+        by = 8.0 * (band + 1) * N * N
+        bw = {"sb2st": {"bytes": by, "ms": sb_ms, "gbs": by / (sb_ms * 1e-3) / 1e9,
+                        "frac_of_hbm": by / (sb_ms * 1e-3) / 1e9 / hbm_peak()[0]}}
+    line = {
+        "metric": "full BSE eigenpair time-to-solution (s)", "value": ms / 1e3, "unit": "s",
+        "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
+        "higher_is_better": False, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": f"synthetic (BASELINE cfg{args.config} recipe, torch Philox on GPU)",
+        "config": {"workload": f"cfg{args.config} complex BSE n={n} (real embedding N={N}), all "
+                               f"eigenpairs + X1/X2 + complex extraction",
+                   "n": n, "parallelism": "single GPU",
+                   "l2": f"inputs {16 * n * n / 2**30:.1f} GiB each (> 126 MB L2 at n >= 4096)"},
+        "tflops_canonical": alg_flops(N) / (ms / 1e3) / 1e12,
+        "fp64_peak_tflops": fp64_peak,
+        "stages_ms": {k: round(v, 3) for k, v in stages.items()},
+        "bandwidth_stages": bw,
+        "e2e": e2e, "cpu_baseline": cpu, "gpu_launches": int(launches), "clocks": clk,
+        "verification": verification, "clusters_resolved": clusters,
+    }
+    print(json.dumps(line), flush=True)
     return 0
 
 
@@ -620,21 +710,27 @@ def main():
     ap.add_argument("--steps", type=int, default=3)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
-    ap.add_argument("--n", type=int, default=16384)
+    ap.add_argument("--n", type=int, default=None,
+                    help="problem size (default: the config's n)")
     ap.add_argument("--e2e-steps", type=int, default=1)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-verify", action="store_true")
     ap.add_argument("--no-native", action="store_true",
                     help="skip the all-DMMA (BSE_FLAG_NATIVE_FP64) comparison solve")
-    ap.add_argument("--config", type=int, default=2, choices=[1, 2],
-                    help="2 (default): real n=16384 headline; 1: complex n=2048 side line")
+    ap.add_argument("--config", type=int, default=2, choices=[1, 2, 3],
+                    help="2 (default): real n=16384 headline; 1: complex n=2048; "
+                         "3: complex n=16384 (real embedding 32768)")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3  # timing rule: >= 3 warm-up steps
     if args.impl == "reference":
+        if args.n is None:
+            args.n = 16384
         return run_reference(args)
-    if args.config == 1:
-        return run_ours_cfg1(args)
+    if args.config in (1, 3):
+        return run_ours_complex(args)
+    if args.n is None:
+        args.n = 16384
     return run_ours(args)
 
 

@@ -56,7 +56,7 @@ typedef struct bse_info {
   int64_t pivot_index;  /* first non-positive Cholesky pivot (status 1), else -1 */
   double pivot_value;   /* its value */
   int32_t failed_factor;/* 0: K = A - B, 1: M = A + B, -1: none */
-  int32_t reserved;
+  int32_t clusters;     /* complex solves: clusters resolved by pivoted Gram-Schmidt */
   double min_pivot;     /* status 0: min_j L_jj^2 of the factor of K (bse_potrf_dev: of A) */
 } bse_info;
 
@@ -87,6 +87,29 @@ int bse_solve_spd_pair_dev(int64_t n, const double* dM, int64_t ldm, const doubl
 int bse_solve_spd_pair_host(int64_t n, const double* M, int64_t ldm, const double* K,
                             int64_t ldk, double* lam, double* X1, int64_t ldx1, double* X2,
                             int64_t ldx2, int flags, bse_info* info);
+
+/*
+ * Complex Hermitian BSE: the drop-in for solvers.solve_complex
+ * (pkg/src/bse/solvers.py:29-77) on complex operators.  A (Hermitian) and
+ * B (complex symmetric) are n x n complex128, interleaved (re, im), ROW-major
+ * (numpy C order) with leading dimensions in complex elements; X1, X2 are
+ * returned in the same layout, lam (n) descending and strictly positive, with
+ * X1^H X1 - X2^H X2 = I.  Internally: the real 2n x 2n embedding
+ * M' = A' + B', K' = A' - B' (D3), the product-form solve with one
+ * eigenvector per doubled eigenvalue back-transformed, and the complex
+ * extraction (pivoted Gram-Schmidt in x1^H y1 - x2^H y2 inside clusters of
+ * equal complex eigenvalues).  Definiteness failures report the pivots of
+ * the reference's cholesky(build_m) (status 1).
+ */
+size_t bse_solve_complex_workspace_bytes(int64_t n, int flags);
+int bse_solve_complex_dev(int64_t n, const double* dA, int64_t lda, const double* dB,
+                          int64_t ldb, double* dLam, double* dX1, int64_t ldx1, double* dX2,
+                          int64_t ldx2, void* dWork, size_t work_bytes, int flags, void* stream,
+                          bse_info* info);
+/* Same with host buffers (uploads, solve and downloads inside). */
+int bse_solve_complex_host(int64_t n, const double* A, int64_t lda, const double* B, int64_t ldb,
+                           double* lam, double* X1, int64_t ldx1, double* X2, int64_t ldx2,
+                           int flags, bse_info* info);
 
 /* In-place lower Cholesky (strict upper zeroed). */
 int bse_potrf_dev(int64_t n, double* dA, int64_t lda, void* stream, bse_info* info);

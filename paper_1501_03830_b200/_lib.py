@@ -26,7 +26,7 @@ FLAG_NATIVE_FP64 = 0x4
 
 class BseInfo(C.Structure):
     _fields_ = [("pivot_index", C.c_int64), ("pivot_value", C.c_double),
-                ("failed_factor", C.c_int32), ("reserved", C.c_int32),
+                ("failed_factor", C.c_int32), ("clusters", C.c_int32),
                 ("min_pivot", C.c_double)]
 
 
@@ -43,6 +43,11 @@ SIGNATURES = {
                                       C.c_size_t, _INT, _P, C.POINTER(BseInfo)]),
     "bse_solve_spd_pair_host": (_INT, [_I64, _P, _I64, _P, _I64, _P, _P, _I64, _P, _I64, _INT,
                                        C.POINTER(BseInfo)]),
+    "bse_solve_complex_workspace_bytes": (C.c_size_t, [_I64, _INT]),
+    "bse_solve_complex_dev": (_INT, [_I64, _P, _I64, _P, _I64, _P, _P, _I64, _P, _I64, _P,
+                                     C.c_size_t, _INT, _P, C.POINTER(BseInfo)]),
+    "bse_solve_complex_host": (_INT, [_I64, _P, _I64, _P, _I64, _P, _P, _I64, _P, _I64, _INT,
+                                      C.POINTER(BseInfo)]),
     "bse_potrf_dev": (_INT, [_I64, _P, _I64, _P, C.POINTER(BseInfo)]),
     "bse_syevd_workspace_bytes": (C.c_size_t, [_I64, _INT]),
     "bse_syevd_dev": (_INT, [_I64, _P, _I64, _P, _P, _I64, _P, C.c_size_t, _INT, _P]),

@@ -7,6 +7,7 @@
 #include <string>
 #include "../../include/bse_b200.h"
 #include "comm.cuh"
+#include "complex.cuh"
 #include "dense.cuh"
 #include "ozgemm.cuh"
 #include "solver.cuh"
@@ -129,6 +130,7 @@ static int map_solve_status(const bse::SolveStatus& st, bse_info* info) {
     info->pivot_value = st.pivot_value;
     info->failed_factor = st.failed_factor;
     info->min_pivot = st.min_pivot;
+    info->clusters = st.clusters;
   }
   switch (st.code) {
     case 0: return BSE_OK;
@@ -271,6 +273,82 @@ int bse_solve_spd_pair_host(int64_t n, const double* M, int64_t ldm, const doubl
     if (kp.ready[L]) cudaEventDestroy(kp.ready[L]);
   BSE_TRY_CUDA(e, "solve_host");
   BSE_TRY_CUDA(e2, "solve_host sync");
+  return map_solve_status(st, info);
+}
+
+/* ---- complex Hermitian BSE (solvers.solve_complex) ---------------------- */
+
+size_t bse_solve_complex_workspace_bytes(int64_t n, int flags) {
+  return n > 0 ? bse::complex_bytes((int)n, flags) : 0;
+}
+
+static int complex_args_ok(int64_t n, int64_t lda, int64_t ldb, int64_t ldx1, int64_t ldx2,
+                           int flags) {
+  if (n < 0 || lda < n || ldb < n || ldx1 < n || ldx2 < n)
+    return fail(BSE_BAD_ARGUMENT, "bad dimension");
+  if (n > (1 << 29)) return fail(BSE_BAD_ARGUMENT, "n too large");
+  return check_solve_flags(flags);
+}
+
+int bse_solve_complex_dev(int64_t n, const double* dA, int64_t lda, const double* dB,
+                          int64_t ldb, double* dLam, double* dX1, int64_t ldx1, double* dX2,
+                          int64_t ldx2, void* dWork, size_t work_bytes, int flags, void* stream,
+                          bse_info* info) {
+  if (complex_args_ok(n, lda, ldb, ldx1, ldx2, flags) != BSE_OK) return BSE_BAD_ARGUMENT;
+  if (n == 0) return BSE_OK;
+  if (work_bytes < bse::complex_bytes((int)n, flags))
+    return fail(BSE_BAD_ARGUMENT, "workspace too small (see bse_solve_complex_workspace_bytes)");
+  bse::Arena a{static_cast<char*>(dWork), work_bytes, 0, false};
+  const bse::ComplexCarve c = bse::carve_complex(a, (int)n, flags);
+  bse::SolveStatus st{};
+  BSE_TRY_CUDA(bse::solve_complex((int)n, (const double2*)dA, lda, (const double2*)dB, ldb, dLam,
+                                  nullptr, (double2*)dX1, ldx1, (double2*)dX2, ldx2, c, flags,
+                                  (cudaStream_t)stream, &st),
+               "solve_complex");
+  return map_solve_status(st, info);
+}
+
+int bse_solve_complex_host(int64_t n, const double* A, int64_t lda, const double* B, int64_t ldb,
+                           double* lam, double* X1, int64_t ldx1, double* X2, int64_t ldx2,
+                           int flags, bse_info* info) {
+  if (complex_args_ok(n, lda, ldb, ldx1, ldx2, flags) != BSE_OK) return BSE_BAD_ARGUMENT;
+  if (n == 0) return BSE_OK;
+  cudaMemPool_t pool;
+  BSE_TRY_CUDA(host_pool(&pool), "memory pool");
+  cudaStream_t s;
+  BSE_TRY_CUDA(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking), "stream");
+  const size_t wb = bse::complex_bytes((int)n, flags);
+  char* buf = nullptr;
+  cudaError_t e = cudaMallocFromPoolAsync((void**)&buf, wb, pool, s);
+  if (e != cudaSuccess) {
+    cudaStreamDestroy(s);
+    return cuda_fail(e, "alloc");
+  }
+  bse::Arena a{buf, wb, 0, false};
+  const bse::ComplexCarve c = bse::carve_complex(a, (int)n, flags);
+  // inputs and outputs live in the solve workspace region: A, B are consumed
+  // by the embedding before the solve starts, X1c, X2c are written after it
+  const size_t cb = 16 * (size_t)n * n;
+  double2* dA = reinterpret_cast<double2*>(c.ws);
+  double2* dB = reinterpret_cast<double2*>(c.ws + ((cb + 255) / 256) * 256);
+  double2* dX1 = dA;
+  double2* dX2 = dB;
+  const size_t row = 16 * (size_t)n;
+  e = cudaMemcpy2DAsync(dA, row, A, 16 * lda, row, n, cudaMemcpyHostToDevice, s);
+  if (e == cudaSuccess) e = cudaMemcpy2DAsync(dB, row, B, 16 * ldb, row, n, cudaMemcpyHostToDevice, s);
+  bse::SolveStatus st{};
+  if (e == cudaSuccess)
+    e = bse::solve_complex((int)n, dA, n, dB, n, nullptr, lam, dX1, n, dX2, n, c, flags, s, &st);
+  if (e == cudaSuccess && st.code == 0) {
+    e = cudaMemcpy2DAsync(X1, 16 * ldx1, dX1, row, row, n, cudaMemcpyDeviceToHost, s);
+    if (e == cudaSuccess)
+      e = cudaMemcpy2DAsync(X2, 16 * ldx2, dX2, row, row, n, cudaMemcpyDeviceToHost, s);
+  }
+  cudaFreeAsync(buf, s);
+  cudaError_t e2 = cudaStreamSynchronize(s);
+  cudaStreamDestroy(s);
+  BSE_TRY_CUDA(e, "solve_complex_host");
+  BSE_TRY_CUDA(e2, "solve_complex_host sync");
   return map_solve_status(st, info);
 }
 

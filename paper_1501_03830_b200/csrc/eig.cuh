@@ -126,6 +126,24 @@ cudaError_t stedc(int n, double* d, double* e, double* w, double* Q, long long l
 cudaError_t tridiag_values(int n, const double* d, const double* e, double* w, double* scratch3,
                            cudaStream_t s, int* fail = nullptr);
 
+// Column selection between the divide and conquer and the back-transforms
+// (the complex path: one eigenvector per doubled eigenvalue of the real
+// embedding is all the complex solution needs, so Q2/Q1 and the recovery run
+// on about half the columns).  After the D&C, syevd synchronises, copies the
+// ascending eigenvalues to the host and calls fn; fn returns the number of
+// selected columns (their Z indices in output order written to cols,
+// capacity n), or < 0 to skip the back-transforms (nsel is set to it).  The
+// selected columns are gathered into dst[:, 0:nsel] and back-transformed
+// there; Z keeps the D&C vectors.
+struct ZSelect {
+  int (*fn)(void* ctx, const double* w_host, int n, int* cols) = nullptr;
+  void* ctx = nullptr;
+  double* dst = nullptr;
+  long long lddst = 0;
+  int* dcols = nullptr;  // device copy of cols (n ints)
+  int nsel = 0;          // out
+};
+
 // Full pipeline on a symmetric matrix (lower triangle of A read, destroyed).
 size_t syevd_bytes(int n, int flags);
 // zc0/zc1: back-transform only Z columns [zc0, zc1) (the column shard of a
@@ -135,7 +153,7 @@ size_t syevd_bytes(int n, int flags);
 // the analogue of kernels.ConvergenceError, kernels.py:403-419).
 cudaError_t syevd(int n, double* A, long long lda, double* w, double* Z, long long ldz,
                   void* work, size_t work_bytes, int flags, cudaStream_t s, int zc0 = 0,
-                  int zc1 = -1, int* conv_out = nullptr);
+                  int zc1 = -1, int* conv_out = nullptr, ZSelect* sel = nullptr);
 
 int device_sm_count();
 

@@ -138,6 +138,17 @@ SyevdWork carve_syevd(Arena& a, int n, int flags) {
 
 }  // namespace
 
+namespace {
+// dst(:, c) = Z(:, cols[c])  (n rows, nsel columns)
+__global__ void gather_cols_kernel(int n, int nsel, const double* Z, long long ldz,
+                                   const int* cols, double* dst, long long ldd) {
+  const long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (idx >= (long long)n * nsel) return;
+  const int r = (int)(idx % n), c = (int)(idx / n);
+  dst[r + (long long)c * ldd] = Z[r + (long long)cols[c] * ldz];
+}
+}  // namespace
+
 size_t syevd_bytes(int n, int flags) {
   Arena a;
   a.dry = true;
@@ -147,7 +158,7 @@ size_t syevd_bytes(int n, int flags) {
 
 cudaError_t syevd(int n, double* A, long long lda, double* w, double* Z, long long ldz,
                   void* work, size_t work_bytes, int flags, cudaStream_t s, int zc0, int zc1,
-                  int* conv_out) {
+                  int* conv_out, ZSelect* sel) {
   if (n <= 0) return cudaSuccess;
   Arena a{static_cast<char*>(work), work_bytes, 0, false};
   SyevdWork ws = carve_syevd(a, n, flags);
@@ -199,6 +210,34 @@ cudaError_t syevd(int n, double* A, long long lda, double* w, double* Z, long lo
     stage_mark("q1_build", s);
     if ((e = q1_build(n, b, ws.Vall, ws.ldv, ws.Tall, ws.q1, s)) != cudaSuccess) return e;
   }
+  if (sel) {
+    // eigenvalues to the host, choose the columns, gather them into sel->dst
+    stage_mark("z_select", s);
+    std::vector<double> wh(n);
+    std::vector<int> cols(n);
+    if ((e = cudaMemcpyAsync(wh.data(), w, sizeof(double) * n, cudaMemcpyDeviceToHost, s)) !=
+        cudaSuccess)
+      return e;
+    if ((e = cudaStreamSynchronize(s)) != cudaSuccess) return e;
+    sel->nsel = sel->fn(sel->ctx, wh.data(), n, cols.data());
+    if (sel->nsel <= 0) return cudaSuccess;
+    if ((e = cudaMemcpyAsync(sel->dcols, cols.data(), sizeof(int) * sel->nsel,
+                             cudaMemcpyHostToDevice, s)) != cudaSuccess)
+      return e;
+    const long long cnt = (long long)n * sel->nsel;
+    gather_cols_kernel<<<(unsigned)ceil_div(cnt, 256), 256, 0, s>>>(n, sel->nsel, Z, ldz,
+                                                                    sel->dcols, sel->dst,
+                                                                    sel->lddst);
+    count_launch();
+    if ((e = cudaGetLastError()) != cudaSuccess) return e;
+    // the host vectors must outlive the async copy: wait for it here (the
+    // gather is queued behind it, so this costs no bubble on the device)
+    if ((e = cudaStreamSynchronize(s)) != cudaSuccess) return e;
+    Z = sel->dst;
+    ldz = sel->lddst;
+    zc0 = 0;
+    zc1 = sel->nsel;
+  }
   stage_mark("q2_build_wait", s);
   if ((e = cudaStreamWaitEvent(s, side.join, 0)) != cudaSuccess) return e;
   if (zc1 < 0) zc1 = n;
@@ -221,6 +260,7 @@ struct SolveWork {
   double* lam2;
   double* linv;
   DevStatus* st;
+  int* cols;  // ZSelect column indices
   void* eig; size_t eig_bytes;
   void* oz; size_t oz_bytes;  // emulated-FP64 workspace (aliases eig when it fits)
   OzWork oz_trsm;             // separate: the TRMM's L slices stay live across blocks
@@ -238,6 +278,7 @@ SolveWork carve_solve(Arena& a, int n, int flags) {
   w.lam2 = a.take<double>(n);
   w.linv = a.take<double>(potrf_inv_cache_doubles(n));
   w.st = a.take<DevStatus>(2);
+  w.cols = a.take<int>(n);
   w.eig_bytes = syevd_bytes(n, flags);
   w.eig = a.take<char>(w.eig_bytes);
   w.oz_bytes = use_oz(n, flags) ? ozgemm_bytes(n, n, n, kRecoverBlock) : 0;
@@ -304,6 +345,19 @@ __global__ void scale_reverse_kernel(int n, int c0, int nc, const double* Z, lon
   const double z = Z[r + (long long)src * ldz];
   Zr[r + (long long)c * ld] = z;
   V[r + (long long)c * ld] = z * lam;
+}
+
+// Selected columns: V(:, c) = Zr(:, c) * lam_c, lam_out[c] = lam_c with
+// lam_c = sqrt(lam2[cols[c]]) (> 0, checked by the selector).
+__global__ void scale_selected_kernel(int n, int nsel, const double* Zr, long long ld,
+                                      const double* lam2, const int* cols, double* V,
+                                      double* lam_out) {
+  const long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (idx >= (long long)n * nsel) return;
+  const int r = (int)(idx % n), c = (int)(idx / n);
+  const double lm = sqrt(lam2[cols[c]]);
+  if (r == 0) lam_out[c] = lm;
+  V[r + (long long)c * ld] = Zr[r + (long long)c * ld] * lm;
 }
 
 // X1 = (u + v) / (2 sqrt(lam)), X2 = (u - v) / (2 sqrt(lam))  (n rows, ncols columns)
@@ -438,12 +492,13 @@ cudaError_t solve_spd_pair(int n, const double* M, long long ldm, const double* 
                            double* lam, double* X1, long long ldx1, double* X2, long long ldx2,
                            void* work, size_t work_bytes, int flags, cudaStream_t s,
                            SolveStatus* out, cudaEvent_t m_ready, const HostOut* hout,
-                           Comm* comm, const KPieces* k_pieces) {
+                           Comm* comm, const KPieces* k_pieces, ZSelect* zsel) {
   out->code = 0;
   out->pivot_index = -1;
   out->pivot_value = 0.0;
   out->failed_factor = -1;
   out->min_pivot = 0.0;
+  out->clusters = 0;
   if (n <= 0) return cudaSuccess;
   Arena a{static_cast<char*>(work), work_bytes, 0, false};
   SolveWork w = carve_solve(a, n, flags);
@@ -549,13 +604,41 @@ cudaError_t solve_spd_pair(int n, const double* M, long long ldm, const double* 
   // 3. W = Z diag(lam^2) Z^T (ascending lam^2); Z into T1.  The reduction and
   // D&C are replicated; only this rank's eigenvector columns (output columns
   // [c0, c1) = Z columns [n - c1, n - c0)) are back-transformed.
+  if (zsel) {
+    if (world > 1) return cudaErrorInvalidValue;  // selection is a single-GPU mode
+    zsel->dst = w.Zr;
+    zsel->lddst = ld;
+    zsel->dcols = w.cols;
+  }
   if ((e = syevd(n, w.W, ld, w.lam2, w.T1, ld, w.eig, w.eig_bytes, flags, s, (int)(n - c1),
-                 (int)(n - c0), &w.st[0].conv_fail)) != cudaSuccess)
+                 (int)(n - c0), &w.st[0].conv_fail, zsel)) != cudaSuccess)
     return e;
+  if (zsel && zsel->nsel <= 0) {
+    // the selector refused the spectrum (non-positive or non-finite lambda^2):
+    // a D&C convergence failure, else the definiteness report (M is intact)
+    DevStatus hs[2];
+    if ((e = cudaMemcpyAsync(hs, w.st, sizeof(hs), cudaMemcpyDeviceToHost, s)) != cudaSuccess)
+      return e;
+    if ((e = cudaStreamSynchronize(s)) != cudaSuccess) return e;
+    out->min_pivot = hs[0].aux;
+    if (hs[0].conv_fail) {
+      out->code = 2;
+      return cudaSuccess;
+    }
+    return definiteness_failure(n, M, ldm, w, hs[0], s, out);
+  }
   stage_mark("recover", s);
-  // 4. descending order; v = Z Lam into W, Z reversed into Zr
   int* bad = reinterpret_cast<int*>(&w.st[1].conv_fail);
-  {
+  if (zsel) {
+    // selected columns (already in output order in Zr): v = Zr Lam into W
+    c0 = 0;
+    c1 = zsel->nsel;
+    const long long tot_sh = (long long)n * zsel->nsel;
+    scale_selected_kernel<<<(unsigned)ceil_div(tot_sh, 256), 256, 0, s>>>(
+        n, zsel->nsel, w.Zr, ld, w.lam2, w.cols, w.W, lam);
+    count_launch();
+  } else {
+    // 4. descending order; v = Z Lam into W, Z reversed into Zr
     const long long tot_sh = std::max<long long>((long long)n * nc, n);
     scale_reverse_kernel<<<(unsigned)ceil_div(tot_sh, 256), 256, 0, s>>>(
         n, (int)c0, nc, w.T1, ld, w.lam2, w.Zr, w.W, ld, lam, bad);

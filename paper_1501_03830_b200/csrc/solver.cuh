@@ -36,6 +36,7 @@ struct SolveStatus {
   double pivot_value;
   int failed_factor;   // 0: K (A-B), 1: M (A+B)
   double min_pivot;    // min_j L_jj^2 of K's factor (code 0)
+  int clusters;        // complex path: clusters resolved by pivoted Gram-Schmidt
 };
 
 // Host-entry upload of K by column pieces (see PotrfHook): piece 0 =
@@ -68,7 +69,7 @@ cudaError_t solve_spd_pair(int n, const double* M, long long ldm, const double* 
                            void* work, size_t work_bytes, int flags, cudaStream_t s,
                            SolveStatus* out, cudaEvent_t m_ready = nullptr,
                            const HostOut* hout = nullptr, Comm* comm = nullptr,
-                           const KPieces* k_pieces = nullptr);
+                           const KPieces* k_pieces = nullptr, ZSelect* zsel = nullptr);
 
 cudaError_t absorption(int n, const double* lam, const double* X1c, long long ldx1,
                        const double* X2c, long long ldx2, const double* dr, const double* dl,

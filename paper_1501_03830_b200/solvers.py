@@ -6,8 +6,7 @@ Both run the north-star product form on the GPU: M = A+B, K = A-B (or their
 W = L^T M L = Z Lam^2 Z^T, X1,2 = (L Z +- L^{-T} Z Lam) Lam^{-1/2} / 2.
 Torch is used for device memory, streams and index plumbing only; every
 floating-point stage (Cholesky, congruence, eigensolver, back-transforms,
-recovery, biorthogonality polish GEMMs, absorption) is a kernel of
-libbse_b200.so.  There is no CPU fallback: without a CUDA device these raise.
+recovery, complex extraction, absorption) is a kernel of libbse_b200.so.  There is no CPU fallback: without a CUDA device these raise.
 """
 from __future__ import annotations
 
@@ -18,7 +17,7 @@ import numpy as np
 from . import _lib
 from .device import (colmajor_empty, from_device_colmajor, ptr, require_cuda, stream_ptr,
                      to_device_colmajor, view_colmajor)
-from .types import (EPS, BseOperator, ConvergenceError, NotPositiveDefinite,
+from .types import (BseOperator, ConvergenceError, NotPositiveDefinite,
                     PositiveEigensystem, conditioning_warnings)
 
 _WHAT_M = "the definiteness embedding M"
@@ -117,161 +116,47 @@ def real_embedding(op: BseOperator):
     return 0.5 * (m + m.T), 0.5 * (k + k.T)
 
 
-def _real_embedding_device(op: BseOperator, dev):
-    """real_embedding() formed on the device from one upload of A and B:
-    the same IEEE operations as the host version (bitwise equal), without
-    host-side block assembly and transposes of 2n x 2n arrays.  M', K' are
-    exactly symmetric, so their row-major tensors are their column-major
-    buffers."""
+def solve_complex_device(A, B, n: int, flags: int = 0):
+    """Core device call (C ABI bse_solve_complex_dev) on torch complex128
+    tensors A, B (n x n, row-major = torch's layout).  Returns torch tensors
+    (lam descending (n,), X1, X2 (n x n complex128)) or raises like the
+    reference (NotPositiveDefinite names the definiteness embedding M)."""
     torch = require_cuda()
-    n = op.n
-    N = 2 * n
-
-    def up(x):
-        x = np.asarray(x)
-        return torch.from_numpy(x if x.flags.writeable else x.copy()).to(dev)
-
-    A, B = up(op.a), up(op.b)
-    ar, ai, br, bi = A.real, A.imag, B.real, B.imag
-    out = []
-    for sgn in (1.0, -1.0):  # M' = A' + B', K' = A' - B'
-        T = torch.empty((N, N), dtype=torch.float64, device=dev)
-        T[:n, :n] = ar + sgn * br
-        T[:n, n:] = -ai + sgn * bi
-        T[n:, :n] = ai + sgn * bi
-        T[n:, n:] = ar - sgn * br
-        T = 0.5 * (T + T.T)
-        buf, ld = colmajor_empty(N, N, dev)
-        buf[:N, :N].copy_(T)
-        del T
-        out.append((buf, ld))
-    del A, B
-    return out
+    lib = _lib.load()
+    dev = A.device
+    A = A.contiguous()
+    B = B.contiguous()
+    X1 = torch.empty((n, n), dtype=torch.complex128, device=dev)
+    X2 = torch.empty((n, n), dtype=torch.complex128, device=dev)
+    lam = torch.empty(max(n, 1), dtype=torch.float64, device=dev)
+    wb = lib.bse_solve_complex_workspace_bytes(n, flags)
+    work = torch.empty(max(int(wb), 1), dtype=torch.uint8, device=dev)
+    info = _lib.BseInfo()
+    st = lib.bse_solve_complex_dev(n, ptr(A), n, ptr(B), n, ptr(lam), ptr(X1), n, ptr(X2), n,
+                                   ptr(work), wb, flags, stream_ptr(dev), C.byref(info))
+    if st == _lib.BSE_NOT_POSITIVE_DEFINITE:
+        raise NotPositiveDefinite(int(info.pivot_index), float(info.pivot_value), _WHAT_M)
+    raise_for_status(st, info, "bse_solve_complex_dev")
+    return lam[:n], X1, X2
 
 
-def _select_and_polish(lam2, X1, X2, ld, n, dev):
-    """Complex eigenvectors from the doubled real spectrum of the 2n-embedding.
-
-    Every complex eigenvalue appears twice; one real vector per pair maps to
-    x = r1[:n] + i r1[n:], y = r2[:n] - i r2[n:].  Within clusters of
-    (nearly) equal complex eigenvalues, k independent vectors are chosen by
-    pivoted Gram-Schmidt in the indefinite product <x, y> = x1^H y1 - x2^H y2
-    (positive definite on the positive-lambda subspace), mirroring the
-    reference's _pivoted_orthonormal (kernels.py:644-674).  A GEMM-only
-    biorthogonality polish X <- X (1.5 I - G / 2), G = X1^H X1 - X2^H X2, then
-    restores Y^H X = I to O(eps) (D3)."""
-    torch = require_cuda()
-    N = 2 * n
-    lam2_h = lam2.cpu().numpy()
-    x1 = view_colmajor(X1, N, N)  # (N x N) torch views, columns = eigenvectors
-    x2 = view_colmajor(X2, N, N)
-    # cluster detection on the host (O(N) scalars)
-    scale = max(1.0, float(np.max(np.abs(lam2_h))))
-    dtol = 20.0 * N * EPS * scale
-    sel = []
-    lam = []
-    start = 0
-    while start < N:
-        stop = start + 1
-        while stop < N and lam2_h[stop - 1] - lam2_h[stop] <= dtol:
-            stop += 1
-        size = stop - start
-        k = size // 2
-        if size == 2:
-            sel.append(start)
-            lam.append(0.5 * (lam2_h[start] + lam2_h[start + 1]))
-        else:
-            # pivoted Gram-Schmidt in the indefinite product (device tensors)
-            cand1 = torch.complex(x1[:n, start:stop], x1[n:, start:stop])
-            cand2 = torch.complex(x2[:n, start:stop], -x2[n:, start:stop])
-            chosen1, chosen2 = [], []
-            w1, w2 = cand1.clone(), cand2.clone()
-            for _ in range(max(k, 1)):
-                nrm = (w1.abs() ** 2).sum(0) - (w2.abs() ** 2).sum(0)
-                j = int(torch.argmax(nrm))
-                s = torch.sqrt(torch.clamp(nrm[j], min=1e-300))
-                u1, u2 = w1[:, j] / s, w2[:, j] / s
-                chosen1.append(u1)
-                chosen2.append(u2)
-                coef = (u1.conj() @ w1) - (u2.conj() @ w2)
-                w1 = w1 - torch.outer(u1, coef)
-                w2 = w2 - torch.outer(u2, coef)
-            sel.append((start, stop, torch.stack(chosen1, 1), torch.stack(chosen2, 1)))
-            vals = lam2_h[start:stop]
-            for t in range(max(k, 1)):
-                lam.append(float(np.mean(vals[2 * t:2 * t + 2])) if 2 * t + 1 < size else float(vals[-1]))
-        start = stop
-    # assemble planar complex X1c, X2c (n x n) on device: one gather for all
-    # simple pairs, cluster blocks copied in place
-    X1c = torch.empty((n, n), dtype=torch.complex128, device=dev)
-    X2c = torch.empty((n, n), dtype=torch.complex128, device=dev)
-    simple_out, simple_src, col = [], [], 0
-    blocks = []
-    for s in sel:
-        if isinstance(s, int):
-            simple_out.append(col)
-            simple_src.append(s)
-            col += 1
-        else:
-            k = s[2].shape[1]
-            blocks.append((col, s[2], s[3]))
-            col += k
-    if simple_src:
-        src = torch.tensor(simple_src, device=dev)
-        dst = torch.tensor(simple_out, device=dev)
-        X1c[:, dst] = torch.complex(x1[:n, src], x1[n:, src])
-        X2c[:, dst] = torch.complex(x2[:n, src], -x2[n:, src])
-    for c0, b1, b2 in blocks:
-        k = min(b1.shape[1], n - c0)
-        if k > 0:
-            X1c[:, c0:c0 + k] = b1[:, :k]
-            X2c[:, c0:c0 + k] = b2[:, :k]
-    lam = np.array(lam[:n])
-    X1c, X2c = polish(X1c, X2c)
-    return lam, X1c, X2c
-
-
-def polish(X1c, X2c):
-    """Biorthogonality polish with the library's DMMA GEMM (complex products
-    as stacked real GEMMs): G = X1^H X1 - X2^H X2; X <- X (1.5 I - 0.5 G)."""
-    torch = require_cuda()
-    n = X1c.shape[0]
-    dev = X1c.device
-    # column-major planar stacks: P = [X1r; X1i; X2r; X2i] (4n x n)
-    P, ldp = colmajor_empty(4 * n, n, dev)
-    Q, _ = colmajor_empty(4 * n, n, dev)
-    R, _ = colmajor_empty(4 * n, n, dev)
-    pv, qv, rv = view_colmajor(P, 4 * n, n), view_colmajor(Q, 4 * n, n), view_colmajor(R, 4 * n, n)
-    parts = (X1c.real, X1c.imag, X2c.real, X2c.imag)
-    for i, blk in enumerate(parts):
-        pv[i * n:(i + 1) * n] = blk
-    qv[:2 * n] = pv[:2 * n]
-    qv[2 * n:] = -pv[2 * n:]
-    rv[0:n], rv[n:2 * n], rv[2 * n:3 * n], rv[3 * n:] = parts[1], -parts[0], -parts[3], parts[2]
-    # Gr = P^T Q, Gi = P^T R  (n x n)
-    Gr, ldg = colmajor_empty(n, n, dev)
-    Gi, _ = colmajor_empty(n, n, dev)
-    _gemm(1, 0, n, n, 4 * n, 1.0, ptr(P), ldp, ptr(Q), ldp, 0.0, ptr(Gr), ldg)
-    _gemm(1, 0, n, n, 4 * n, 1.0, ptr(P), ldp, ptr(R), ldp, 0.0, ptr(Gi), ldg)
-    # F_big = [[Fr, Fi], [-Fi, Fr]] with F = 1.5 I - 0.5 G
-    Fb, ldf = colmajor_empty(2 * n, 2 * n, dev)
-    fv = view_colmajor(Fb, 2 * n, 2 * n)
-    gr, gi = view_colmajor(Gr, n, n), view_colmajor(Gi, n, n)
-    eye = torch.eye(n, dtype=torch.float64, device=dev)
-    fr = 1.5 * eye - 0.5 * gr
-    fi = -0.5 * gi
-    fv[:n, :n] = fr
-    fv[:n, n:] = fi
-    fv[n:, :n] = -fi
-    fv[n:, n:] = fr
-    # Xs = [X1r X1i; X2r X2i] (2n x 2n) ; Xs_new = Xs F_big
-    Xs, ldx = colmajor_empty(2 * n, 2 * n, dev)
-    xv = view_colmajor(Xs, 2 * n, 2 * n)
-    xv[:n, :n], xv[:n, n:], xv[n:, :n], xv[n:, n:] = parts[0], parts[1], parts[2], parts[3]
-    Out, _ = colmajor_empty(2 * n, 2 * n, dev)
-    _gemm(0, 0, 2 * n, 2 * n, 2 * n, 1.0, ptr(Xs), ldx, ptr(Fb), ldf, 0.0, ptr(Out), ldx)
-    ov = view_colmajor(Out, 2 * n, 2 * n)
-    return torch.complex(ov[:n, :n], ov[:n, n:]), torch.complex(ov[n:, :n], ov[n:, n:])
+def _solve_complex_host(a: np.ndarray, b: np.ndarray, n: int, flags: int = 0):
+    """Host entry (bse_solve_complex_host): numpy complex128 in, numpy out;
+    uploads, the solve and the downloads happen inside the library."""
+    require_cuda()
+    lib = _lib.load()
+    a = np.ascontiguousarray(a, dtype=np.complex128)
+    b = np.ascontiguousarray(b, dtype=np.complex128)
+    lam = np.empty(n)
+    x1 = np.empty((n, n), dtype=np.complex128)
+    x2 = np.empty((n, n), dtype=np.complex128)
+    info = _lib.BseInfo()
+    st = lib.bse_solve_complex_host(n, a.ctypes.data, n, b.ctypes.data, n, lam.ctypes.data,
+                                    x1.ctypes.data, n, x2.ctypes.data, n, flags, C.byref(info))
+    if st == _lib.BSE_NOT_POSITIVE_DEFINITE:
+        raise NotPositiveDefinite(int(info.pivot_index), float(info.pivot_value), _WHAT_M)
+    raise_for_status(st, info, "bse_solve_complex_host")
+    return lam, x1, x2
 
 
 def syevd_values_device(At, lda: int, n: int):
@@ -328,7 +213,9 @@ def tda_gap_report(op: BseOperator, workers: int = 1):
 def solve_complex(op: BseOperator, workers: int = 1) -> PositiveEigensystem:
     """Structure-preserving solve (reference: solvers.py:29-77).  ``workers``
     is accepted for signature compatibility; the output is independent of it.
-    Real operators run the n x n product form directly (SURVEY 8b routing)."""
+    Real operators run the n x n product form directly (SURVEY 8b routing);
+    complex ones go through bse_solve_complex_host (real 2n embedding, one
+    eigenvector per doubled eigenvalue, complex extraction on the device)."""
     del workers
     n = op.n
     if n == 0:
@@ -350,15 +237,53 @@ def solve_complex(op: BseOperator, workers: int = 1) -> PositiveEigensystem:
         return PositiveEigensystem(lambda_plus=lam_h, x1=x1.astype(np.complex128),
                                    x2=x2.astype(np.complex128),
                                    warnings=conditioning_warnings(lam_h))
-    N = 2 * n
-    (Mt, ldm), (Kt, ldk) = _real_embedding_device(op, dev)
-    try:
-        lam2, X1, X2, ld = solve_pair_device(Mt, ldm, Kt, ldk, N)
-    except NotPositiveDefinite as err:
-        raise NotPositiveDefinite(err.pivot_index, err.pivot_value, _WHAT_M) from None
-    lam, X1c, X2c = _select_and_polish(lam2, X1, X2, ld, n, dev)
-    return PositiveEigensystem(lambda_plus=lam, x1=X1c.cpu().numpy(), x2=X2c.cpu().numpy(),
-                               warnings=conditioning_warnings(lam))
+    lam, x1, x2 = _solve_complex_host(op.a, op.b, n)
+    return PositiveEigensystem(lambda_plus=lam, x1=x1, x2=x2, warnings=conditioning_warnings(lam))
+
+
+def solve_oracle(op: BseOperator) -> np.ndarray:
+    """Cross-check solver through the generalized Hermitian-definite route
+    (reference: solvers.solve_oracle, solvers.py:116-133): Omega =
+    [[A, B], [conj B, conj A]] = L L^H, eigenvalues of L^H diag(I, -I) L
+    (similar to H), all 2n, descending; the +- pairing is not enforced.  On
+    the GPU: Omega's interleaved real embedding (each entry z -> [[Re z,
+    -Im z], [Im z, Re z]], so Cholesky pivot 2j is Omega's pivot j), the
+    library's Cholesky, one DMMA GEMM for L^T S L and the values-only
+    two-stage eigensolver; every eigenvalue comes out twice."""
+    torch = require_cuda()
+    n = op.n
+    if n == 0:
+        return np.zeros(0)
+    dev = _device()
+    A = torch.from_numpy(np.array(op.a)).to(dev)
+    B = torch.from_numpy(np.array(op.b)).to(dev)
+    om = torch.cat([torch.cat([A, B], 1), torch.cat([B.conj(), A.conj()], 1)], 0)
+    om = 0.5 * (om + om.conj().T)
+    m = 2 * n
+    N = 2 * m
+    emb = torch.empty((m, 2, m, 2), dtype=torch.float64, device=dev)
+    emb[:, 0, :, 0] = om.real
+    emb[:, 0, :, 1] = -om.imag
+    emb[:, 1, :, 0] = om.imag
+    emb[:, 1, :, 1] = om.real
+    Lt, ld = colmajor_empty(N, N, dev)
+    Lt[:N, :N].copy_(emb.reshape(N, N).T)  # column-major buffer of the (symmetric) embedding
+    del emb, om, A, B
+    lib = _lib.load()
+    info = _lib.BseInfo()
+    st = lib.bse_potrf_dev(N, ptr(Lt), ld, stream_ptr(dev), C.byref(info))
+    if st == _lib.BSE_NOT_POSITIVE_DEFINITE:
+        raise NotPositiveDefinite(int(info.pivot_index) // 2, float(info.pivot_value), "Omega")
+    raise_for_status(st, info, "bse_potrf_dev")
+    # T = S L (S = -1 on the rows of Omega's second block), K = L^T T
+    T, _ = colmajor_empty(N, N, dev)
+    T.copy_(Lt)
+    view_colmajor(T, N, N)[m:, :] *= -1.0
+    K, _ = colmajor_empty(N, N, dev)
+    _gemm(1, 0, N, N, N, 1.0, ptr(Lt), ld, ptr(T), ld, 0.0, ptr(K), ld)
+    del T, Lt
+    w = syevd_values_device(K, ld, N).cpu().numpy()[::-1]
+    return 0.5 * (w[0::2] + w[1::2])
 
 
 def _potrf_margin(m: np.ndarray, dev):

@@ -59,3 +59,29 @@ def absorption_spectrum(pos: PositiveEigensystem, dip: DipoleData, grid=None,
         raise ValueError("invalid eigensystem: |y_j^H x_j| below 1e-8")
     return SpectrumCurve(omegas=grid, values=values.cpu().numpy(), sigma=float(sigma),
                          kind="absorption", normalization_defect=float(defect) if n else 0.0)
+
+
+def spectral_density(lam, grid=None, sigma: float = DEFAULT_SIGMA) -> SpectrumCurve:
+    """Broadened density of states phi(omega) = (1/N) sum_j N(omega -
+    lambda_j; sigma) over all supplied eigenvalues (reference:
+    spectra.spectral_density, spectra.py:99-117).  O(N x window) host
+    post-processing of eigenvalues already on the host (no eigenvectors)."""
+    lam = np.atleast_1d(np.asarray(lam, dtype=np.float64))
+    if lam.size == 0:
+        raise ValueError("empty spectrum")
+    if not sigma > 0.0:
+        raise ValueError("sigma must be positive")
+    if grid is None:
+        grid = default_grid(lam, sigma)
+    grid = np.asarray(grid, dtype=np.float64)
+    out = np.zeros(grid.shape[0])
+    wpeak = (1.0 / lam.shape[0]) * (1.0 / (np.sqrt(2.0 * np.pi) * sigma))  # (w * peak)
+    reach = 8.0 * sigma
+    for c in lam:  # accumulated in eigenvalue order, truncated at 8 sigma (spectra.py:81-96)
+        i0 = int(np.searchsorted(grid, c - reach, side="left"))
+        i1 = int(np.searchsorted(grid, c + reach, side="right"))
+        if i0 == i1:
+            continue
+        t = (grid[i0:i1] - c) / sigma
+        out[i0:i1] += wpeak * np.exp(-0.5 * t * t)
+    return SpectrumCurve(omegas=grid, values=out, sigma=float(sigma), kind="dos")
