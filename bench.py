@@ -339,18 +339,8 @@ def run_ours_complex(args):
     # verification on every pair (outside the timed region; torch complex
     # GEMMs): H x_j = lam_j x_j with H = [[A, B], [-conj B, -conj A]],
     # X1^H X1 - X2^H X2 = I, positivity / order, the TDA bound lam_j <= a_j
-    lamc = lam.to(torch.complex128)
-    r_top = A @ X1 + B @ X2 - X1 * lamc
-    r_bot = -(B.conj() @ X1) - A.conj() @ X2 - X2 * lamc
-    res = torch.sqrt((r_top.abs() ** 2).sum(0) + (r_bot.abs() ** 2).sum(0))
-    xn = torch.sqrt((X1.abs() ** 2).sum(0) + (X2.abs() ** 2).sum(0))
-    del r_top, r_bot
-    hn = float(lam[0])  # ||H||_2 >= lam_max; the gate uses lam_max ||x||
-    pair_res = float((res / (hn * xn)).max())
-    G = X1.conj().T @ X1 - X2.conj().T @ X2
-    G.diagonal().sub_(1.0)
-    bio = float(torch.linalg.matrix_norm(G))
-    del G
+    from paper_1501_03830_b200.verify import complex_pair_residuals
+    pair_res, bio = complex_pair_residuals(A, B, lam, X1, X2)
     lam_h = lam.cpu().numpy()
     tda = bool(bg.dos_dominance(lam_h, a_vals.cpu().numpy()))
     verification = {"max_pair_residual": pair_res, "biorthogonality_fro": bio,
@@ -365,7 +355,7 @@ def run_ours_complex(args):
     if args.e2e_steps > 0:
         a_h = A.cpu().numpy()
         b_h = B.cpu().numpy()
-        del A, B, X1, X2, lamc, res, xn
+        del A, B, X1, X2
         torch.cuda.empty_cache()
         op = bg.make_operator(a_h, b_h, kind="complex")
         bg.solve_complex(op)  # warm the library's memory pool

@@ -76,3 +76,33 @@ def pair_residual_report(op: BseOperator, pos: PositiveEigensystem,
     hn = float(pos.lambda_plus[0]) if h_norm is None else float(h_norm)
     ratios = (res / (hn * xn)).cpu().numpy()
     return PairResidualReport(ratios=ratios, biorthogonality=float(bio), h_norm=hn)
+
+
+def complex_pair_residuals(A, B, lam, X1, X2):
+    """Per-pair gates for a complex solution on the device (torch complex
+    GEMMs; verification, not the solve path): returns (max_j |H x_j -
+    lam_j x_j| / (lam_max |x_j|), |X1^H X1 - X2^H X2 - I|_F) with
+    H = [[A, B], [-conj B, -conj A]] (core.py:235-242)."""
+    torch = require_cuda()
+    lamc = lam.to(torch.complex128)
+    rt = A @ X1 + B @ X2 - X1 * lamc
+    rb = -(B.conj() @ X1) - A.conj() @ X2 - X2 * lamc
+    res = torch.sqrt((rt.abs() ** 2).sum(0) + (rb.abs() ** 2).sum(0))
+    del rt, rb
+    xn = torch.sqrt((X1.abs() ** 2).sum(0) + (X2.abs() ** 2).sum(0))
+    G = X1.conj().T @ X1 - X2.conj().T @ X2
+    G.diagonal().sub_(1.0)
+    return float((res / (lam[0] * xn)).max()), float(torch.linalg.matrix_norm(G))
+
+
+def solution_report(op: BseOperator, pos: PositiveEigensystem):
+    """(max pair residual ratio, biorthogonality defect) of a host solution,
+    for either kind (the per-pair form of core.residual_metrics)."""
+    if op.kind == "real":
+        rep = pair_residual_report(op, pos)
+        return rep.max_ratio, rep.biorthogonality
+    torch = require_cuda()
+    dev = torch.device("cuda", torch.cuda.current_device())
+    up = lambda x: torch.from_numpy(np.ascontiguousarray(x)).to(dev)  # noqa: E731
+    return complex_pair_residuals(up(op.a), up(op.b), up(pos.lambda_plus), up(pos.x1),
+                                  up(pos.x2))

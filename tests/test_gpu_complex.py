@@ -18,17 +18,9 @@ EPS = np.finfo(float).eps
 
 
 def verify_device(A, B, lam, X1, X2):
-    """Per-pair residual / (lam_max |x|), |X1^H X1 - X2^H X2 - I|_F (torch)."""
-    import torch
-    lamc = lam.to(torch.complex128)
-    rt = A @ X1 + B @ X2 - X1 * lamc
-    rb = -(B.conj() @ X1) - A.conj() @ X2 - X2 * lamc
-    res = torch.sqrt((rt.abs() ** 2).sum(0) + (rb.abs() ** 2).sum(0))
-    del rt, rb
-    xn = torch.sqrt((X1.abs() ** 2).sum(0) + (X2.abs() ** 2).sum(0))
-    G = X1.conj().T @ X1 - X2.conj().T @ X2
-    G.diagonal().sub_(1.0)
-    return float((res / (lam[0] * xn)).max()), float(torch.linalg.matrix_norm(G))
+    """Per-pair residual / (lam_max |x|), |X1^H X1 - X2^H X2 - I|_F."""
+    from paper_1501_03830_b200.verify import complex_pair_residuals
+    return complex_pair_residuals(A, B, lam, X1, X2)
 
 
 def principal_angle_max(x_new, x_ref):
