@@ -608,6 +608,26 @@ def run_ours(args):
                         else "pinned host M, K -> every rank; bse_solve_spd_pair_dist_dev; "
                              "rank 0 lam, X1, X2 -> pinned host")}
 
+    # the drop-in Python API a user calls: solve_real(op) on host numpy arrays
+    # (complex128 BseOperator blocks in, complex128 X1/X2 out), one solve
+    e2e_drop_in = None
+    if rank == 0 and world == 1 and args.e2e_steps > 0 and not args.no_drop_in:
+        import paper_1501_03830_b200 as bg
+        a_h = (0.5 * (Mh + Kh)).numpy()
+        b_h = (0.5 * (Mh - Kh)).numpy()
+        op = bg.make_operator(a_h, b_h, kind="real")
+        del a_h, b_h
+        torch.cuda.synchronize(dev)
+        t0 = time.perf_counter()
+        pos = bg.solve_real(op)
+        t_drop = time.perf_counter() - t0
+        e2e_drop_in = {"value": t_drop, "unit": "s", "path": "solve_real(op): numpy complex128 "
+                       "A, B -> PositiveEigensystem (complex128 X1, X2)",
+                       "h2d_bytes_per_step": 2 * 8 * n * n, "d2h_bytes_per_step": 2 * 16 * n * n,
+                       "max_rel_lambda_diff_vs_host_entry": float(
+                           np.max(np.abs(pos.lambda_plus - lamh.numpy()) / lamh.numpy()))}
+        del op, pos
+
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         v, cores, sample, _ = cpu_reference_sample(n)
@@ -683,6 +703,7 @@ def run_ours(args):
         "native_fp64_solve": native,
         "cpu_baseline": cpu,
         "e2e": e2e,
+        "e2e_drop_in": e2e_drop_in,
         "gpu_launches": int(launches),
         "clocks": clk,
         "sanity_lambda_positive_desc": ok,
@@ -705,6 +726,8 @@ def main():
     ap.add_argument("--e2e-steps", type=int, default=1)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-verify", action="store_true")
+    ap.add_argument("--no-drop-in", action="store_true",
+                    help="skip the solve_real(op) drop-in API timing")
     ap.add_argument("--no-native", action="store_true",
                     help="skip the all-DMMA (BSE_FLAG_NATIVE_FP64) comparison solve")
     ap.add_argument("--config", type=int, default=2, choices=[1, 2, 3],

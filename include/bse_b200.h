@@ -169,6 +169,13 @@ int bse_ozgemm_dev(int transA, int transB, int64_t M, int64_t N, int64_t K, doub
 int bse_trsm_dev(int kind, int64_t n, const double* dL, int64_t ldl, double* dB, int64_t ldb,
                  int64_t m, void* stream);
 
+/* Large host <-> device copies of PAGEABLE host memory (numpy arrays) through
+ * the library's pinned staging ring with multi-threaded host copies; 2-D with
+ * byte pitches.  to_device != 0: host -> device (returns once the data is on
+ * the device), else device -> host (returns once dst is complete). */
+int bse_memcpy2d_staged(int to_device, void* dst, size_t dpitch, const void* src, size_t spitch,
+                        size_t width_bytes, size_t rows, void* stream);
+
 /* Instrumentation (bench/profiling): stage timing with CUDA events recorded
  * on the solve stream, and the number of kernels this library has launched. */
 int bse_profile_enable(int on);

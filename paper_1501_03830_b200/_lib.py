@@ -65,6 +65,8 @@ SIGNATURES = {
     "bse_trsm_dev": (_INT, [_INT, _I64, _P, _I64, _P, _I64, _I64, _P]),
     "bse_profile_enable": (_INT, [_INT]),
     "bse_profile_read": (_INT, [_INT, C.POINTER(_D), C.c_char_p]),
+    "bse_memcpy2d_staged": (_INT, [_INT, _P, C.c_size_t, _P, C.c_size_t, C.c_size_t,
+                                   C.c_size_t, _P]),
     "bse_profile_count": (_INT, []),
     "bse_launch_count": (C.c_longlong, []),
     "bse_release_cached_memory": (_INT, []),

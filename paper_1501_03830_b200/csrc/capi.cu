@@ -9,6 +9,7 @@
 #include "comm.cuh"
 #include "complex.cuh"
 #include "dense.cuh"
+#include "hostio.cuh"
 #include "ozgemm.cuh"
 #include "solver.cuh"
 
@@ -327,22 +328,24 @@ int bse_solve_complex_host(int64_t n, const double* A, int64_t lda, const double
   bse::Arena a{buf, wb, 0, false};
   const bse::ComplexCarve c = bse::carve_complex(a, (int)n, flags);
   // inputs and outputs live in the solve workspace region: A, B are consumed
-  // by the embedding before the solve starts, X1c, X2c are written after it
-  const size_t cb = 16 * (size_t)n * n;
+  // by the embedding before the solve starts; X1c, X2c are written after it,
+  // behind the extraction scratch
+  const size_t cb = ((16 * (size_t)n * n + 255) / 256) * 256;
   double2* dA = reinterpret_cast<double2*>(c.ws);
-  double2* dB = reinterpret_cast<double2*>(c.ws + ((cb + 255) / 256) * 256);
-  double2* dX1 = dA;
-  double2* dX2 = dB;
+  double2* dB = reinterpret_cast<double2*>(c.ws + cb);
+  char* outs = c.ws + ((c.scratch_bytes + 255) / 256) * 256;
+  double2* dX1 = reinterpret_cast<double2*>(outs);
+  double2* dX2 = reinterpret_cast<double2*>(outs + cb);
   const size_t row = 16 * (size_t)n;
-  e = cudaMemcpy2DAsync(dA, row, A, 16 * lda, row, n, cudaMemcpyHostToDevice, s);
-  if (e == cudaSuccess) e = cudaMemcpy2DAsync(dB, row, B, 16 * ldb, row, n, cudaMemcpyHostToDevice, s);
+  // pageable numpy buffers: pinned staging ring, multi-threaded host copies
+  e = bse::h2d_staged(dA, row, A, 16 * lda, row, n, s);
+  if (e == cudaSuccess) e = bse::h2d_staged(dB, row, B, 16 * ldb, row, n, s);
   bse::SolveStatus st{};
   if (e == cudaSuccess)
     e = bse::solve_complex((int)n, dA, n, dB, n, nullptr, lam, dX1, n, dX2, n, c, flags, s, &st);
   if (e == cudaSuccess && st.code == 0) {
-    e = cudaMemcpy2DAsync(X1, 16 * ldx1, dX1, row, row, n, cudaMemcpyDeviceToHost, s);
-    if (e == cudaSuccess)
-      e = cudaMemcpy2DAsync(X2, 16 * ldx2, dX2, row, row, n, cudaMemcpyDeviceToHost, s);
+    e = bse::d2h_staged(X1, 16 * ldx1, dX1, row, row, n, s);
+    if (e == cudaSuccess) e = bse::d2h_staged(X2, 16 * ldx2, dX2, row, row, n, s);
   }
   cudaFreeAsync(buf, s);
   cudaError_t e2 = cudaStreamSynchronize(s);
@@ -445,6 +448,15 @@ int bse_profile_read(int max_stages, double* ms, char* names) {
   }
   L.used = 0;
   return k;
+}
+
+int bse_memcpy2d_staged(int to_device, void* dst, size_t dpitch, const void* src, size_t spitch,
+                        size_t width_bytes, size_t rows, void* stream) {
+  cudaStream_t s = (cudaStream_t)stream;
+  cudaError_t e = to_device ? bse::h2d_staged(dst, dpitch, src, spitch, width_bytes, rows, s)
+                            : bse::d2h_staged(dst, dpitch, src, spitch, width_bytes, rows, s);
+  BSE_TRY_CUDA(e, "memcpy2d_staged");
+  return BSE_OK;
 }
 
 int bse_profile_count(void) {

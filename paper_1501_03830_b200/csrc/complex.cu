@@ -77,37 +77,20 @@ __global__ void __launch_bounds__(kT * 8) embed_kernel(int n, const double2* __r
 
 // Simple pairs: output column dst takes selected real column src[dst]:
 //   X1c(i, dst) = X1r(i, s) + i X1r(n + i, s),  X2c(i, dst) = X2r(i, s) - i X2r(n + i, s)
-// Tiles of 32 rows x 32 output columns: read column-major (coalesced along i),
-// write row-major complex (coalesced along dst).
-__global__ void __launch_bounds__(kT * 8) extract_simple_kernel(
-    int n, const int* __restrict__ src, const double* __restrict__ X1r,
-    const double* __restrict__ X2r, long long ld, double2* X1c, long long ldx1, double2* X2c,
-    long long ldx2) {
-  __shared__ double2 t1[kT][kT + 1], t2[kT][kT + 1];
-  const int i0 = blockIdx.y * kT, d0 = blockIdx.x * kT;
-  const int tx = threadIdx.x;
-  for (int ty = threadIdx.y; ty < kT; ty += blockDim.y) {
-    const int i = i0 + tx, dst = d0 + ty;
-    double2 v1 = make_double2(0.0, 0.0), v2 = v1;
-    if (i < n && dst < n) {
-      const int s = src[dst];
-      if (s >= 0) {
-        const double* c1 = X1r + (long long)s * ld;
-        const double* c2 = X2r + (long long)s * ld;
-        v1 = make_double2(c1[i], c1[n + i]);
-        v2 = make_double2(c2[i], -c2[n + i]);
-      }
-    }
-    t1[ty][tx] = v1;
-    t2[ty][tx] = v2;
-  }
-  __syncthreads();
-  for (int ty = threadIdx.y; ty < kT; ty += blockDim.y) {
-    const int i = i0 + ty, dst = d0 + tx;
-    if (i >= n || dst >= n || src[dst] < 0) continue;
-    X1c[(long long)i * ldx1 + dst] = t1[tx][ty];
-    X2c[(long long)i * ldx2 + dst] = t2[tx][ty];
-  }
+// into COLUMN-major complex scratch (ldc), coalesced on both sides.
+__global__ void extract_simple_kernel(int n, const int* __restrict__ src,
+                                      const double* __restrict__ X1r,
+                                      const double* __restrict__ X2r, long long ld, double2* X1c,
+                                      double2* X2c, long long ldc) {
+  const long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (idx >= (long long)n * n) return;
+  const int i = (int)(idx % n), dst = (int)(idx / n);
+  const int s = src[dst];
+  if (s < 0) return;
+  const double* c1 = X1r + (long long)s * ld;
+  const double* c2 = X2r + (long long)s * ld;
+  X1c[(long long)dst * ldc + i] = make_double2(c1[i], c1[n + i]);
+  X2c[(long long)dst * ldc + i] = make_double2(c2[i], -c2[n + i]);
 }
 
 // Clusters: one CTA each.  Candidates = the cluster's selected real columns
@@ -137,7 +120,7 @@ __device__ double cl_block_sum(double v, double* red) {
 
 __global__ void __launch_bounds__(kClThreads) extract_cluster_kernel(
     int n, const Cluster* __restrict__ cls, double* X1r, double* X2r, long long ld, double2* X1c,
-    long long ldx1, double2* X2c, long long ldx2) {
+    double2* X2c, long long ldc) {
   __shared__ double red[33];
   __shared__ double nrm[kMaxClusterCand];
   __shared__ unsigned char used[kMaxClusterCand];
@@ -171,8 +154,8 @@ __global__ void __launch_bounds__(kClThreads) extract_cluster_kernel(
     const int dst = cl.dst0 + t;
     for (int i = threadIdx.x; i < n; i += blockDim.x) {
       u1[i] /= sc; u1[n + i] /= sc; u2[i] /= sc; u2[n + i] /= sc;
-      X1c[(long long)i * ldx1 + dst] = make_double2(u1[i], u1[n + i]);
-      X2c[(long long)i * ldx2 + dst] = make_double2(u2[i], -u2[n + i]);
+      X1c[(long long)dst * ldc + i] = make_double2(u1[i], u1[n + i]);
+      X2c[(long long)dst * ldc + i] = make_double2(u2[i], -u2[n + i]);
     }
     __syncthreads();
     if (threadIdx.x == 0) used[j] = 1;
@@ -210,6 +193,125 @@ __global__ void __launch_bounds__(kClThreads) extract_cluster_kernel(
   }
 }
 
+
+// Biorthogonality polish, banded.  Picking one real vector per doubled
+// eigenvalue keeps the D&C's orthogonality only up to the mixing of nearby
+// eigenpairs (x_j picks up O(eps |W| / gap) of its neighbours' partner
+// vectors, which Z's orthogonality no longer cancels), so the indefinite Gram
+// G = X1^H X1 - X2^H X2 deviates from I essentially on a band around the
+// diagonal (sorted eigenvalues: close values are adjacent).  One Newton-Schulz
+// step X <- X (1.5 I - 0.5 G) restricted to |j - k| <= kPolW removes it at
+// O(n^2 kPolW) cost (the full-matrix polish is 32 n^3).
+constexpr int kPolW = 16;  // band half-width
+constexpr int kPolT = 32;  // output columns per CTA
+constexpr int kPolR = 16;  // rows per shared-memory chunk (Gram)
+constexpr int kPolRA = 8;  // rows per shared-memory chunk (apply; 48 KB static limit)
+constexpr int kPolThreads = 256;
+
+BSE_DEV double2 cmul_conj_a(double2 a, double2 b) {  // conj(a) * b
+  return make_double2(a.x * b.x + a.y * b.y, a.x * b.y - a.y * b.x);
+}
+
+// G[d * (W+1) + o] = x_d^H x_{d+o} (indefinite product), o = 0..W
+__global__ void __launch_bounds__(kPolThreads) band_gram_kernel(int n, const double2* __restrict__ X1,
+                                                                const double2* __restrict__ X2,
+                                                                long long ldc, double2* G) {
+  constexpr int NC = kPolT + kPolW;
+  constexpr int NP = kPolT * (kPolW + 1);
+  constexpr int PPT = (NP + kPolThreads - 1) / kPolThreads;
+  __shared__ double2 s1[kPolR][NC + 1], s2[kPolR][NC + 1];
+  const int d0 = blockIdx.x * kPolT;
+  double2 acc[PPT];
+#pragma unroll
+  for (int q = 0; q < PPT; ++q) acc[q] = make_double2(0.0, 0.0);
+  for (int r0 = 0; r0 < n; r0 += kPolR) {
+    __syncthreads();
+    for (int idx = threadIdx.x; idx < kPolR * NC; idx += blockDim.x) {
+      const int i = idx % kPolR, c = idx / kPolR;
+      const int col = d0 + c, row = r0 + i;
+      const bool ok = col < n && row < n;
+      s1[i][c] = ok ? X1[(long long)col * ldc + row] : make_double2(0.0, 0.0);
+      s2[i][c] = ok ? X2[(long long)col * ldc + row] : make_double2(0.0, 0.0);
+    }
+    __syncthreads();
+#pragma unroll
+    for (int q = 0; q < PPT; ++q) {
+      const int p = threadIdx.x + q * kPolThreads;
+      if (p >= NP) break;
+      const int dd = p / (kPolW + 1), o = p % (kPolW + 1);
+#pragma unroll 4
+      for (int i = 0; i < kPolR; ++i) {
+        const double2 u = cmul_conj_a(s1[i][dd], s1[i][dd + o]);
+        const double2 v = cmul_conj_a(s2[i][dd], s2[i][dd + o]);
+        acc[q].x += u.x - v.x;
+        acc[q].y += u.y - v.y;
+      }
+    }
+  }
+#pragma unroll
+  for (int q = 0; q < PPT; ++q) {
+    const int p = threadIdx.x + q * kPolThreads;
+    if (p >= NP) break;
+    const int d = d0 + p / (kPolW + 1), o = p % (kPolW + 1);
+    if (d < n) G[(long long)d * (kPolW + 1) + o] = (d + o < n) ? acc[q] : make_double2(0.0, 0.0);
+  }
+}
+
+// Out(i, d) = sum_{k = d-W}^{d+W} X(i, k) F_kd, F = 1.5 I - 0.5 G, written
+// ROW-major (the caller's layout), coalesced along d.
+__global__ void __launch_bounds__(kPolThreads) band_apply_kernel(
+    int n, const double2* __restrict__ X1, const double2* __restrict__ X2, long long ldc,
+    const double2* __restrict__ G, double2* O1, long long ldo1, double2* O2, long long ldo2) {
+  constexpr int NC = kPolT + 2 * kPolW;
+  constexpr int NO = 2 * kPolW + 1;
+  __shared__ double2 F[NO][kPolT];  // F[o][dd]: coefficient of column d0 + dd + o - W
+  __shared__ double2 s1[kPolRA][NC + 1], s2[kPolRA][NC + 1];
+  const int d0 = blockIdx.x * kPolT;
+  for (int idx = threadIdx.x; idx < NO * kPolT; idx += blockDim.x) {
+    const int o = idx / kPolT, dd = idx % kPolT;
+    const int d = d0 + dd, k = d + o - kPolW;
+    double2 f = make_double2(0.0, 0.0);
+    if (d < n && k >= 0 && k < n) {
+      // G_kd = x_k^H x_d: stored as G[k][d - k] when k <= d, else conj(G[d][k - d])
+      double2 g = k <= d ? G[(long long)k * (kPolW + 1) + (d - k)]
+                         : G[(long long)d * (kPolW + 1) + (k - d)];
+      if (k > d) g.y = -g.y;
+      f = make_double2((k == d ? 1.5 : 0.0) - 0.5 * g.x, -0.5 * g.y);
+    }
+    F[o][dd] = f;
+  }
+  const int dd = threadIdx.x % kPolT;        // this thread's output column
+  const int ig = threadIdx.x / kPolT;        // and rows ig, ig + 8, ...
+  constexpr int RG = kPolThreads / kPolT;    // 8 row groups
+  for (int r0 = 0; r0 < n; r0 += kPolRA) {
+    __syncthreads();
+    for (int idx = threadIdx.x; idx < kPolRA * NC; idx += blockDim.x) {
+      const int i = idx % kPolRA, c = idx / kPolRA;
+      const int col = d0 - kPolW + c, row = r0 + i;
+      const bool ok = col >= 0 && col < n && row < n;
+      s1[i][c] = ok ? X1[(long long)col * ldc + row] : make_double2(0.0, 0.0);
+      s2[i][c] = ok ? X2[(long long)col * ldc + row] : make_double2(0.0, 0.0);
+    }
+    __syncthreads();
+    const int d = d0 + dd;
+    for (int i = ig; i < kPolRA; i += RG) {
+      const int row = r0 + i;
+      if (row >= n || d >= n) continue;
+      double2 a1 = make_double2(0.0, 0.0), a2 = a1;
+#pragma unroll
+      for (int o = 0; o < NO; ++o) {
+        const double2 f = F[o][dd];
+        const double2 x1 = s1[i][dd + o], x2 = s2[i][dd + o];
+        a1.x += x1.x * f.x - x1.y * f.y;
+        a1.y += x1.x * f.y + x1.y * f.x;
+        a2.x += x2.x * f.x - x2.y * f.y;
+        a2.y += x2.x * f.y + x2.y * f.x;
+      }
+      O1[(long long)row * ldo1 + d] = a1;
+      O2[(long long)row * ldo2 + d] = a2;
+    }
+  }
+}
 
 // Host-side plan built by the column selector from the doubled spectrum.
 struct ComplexPlan {
@@ -277,7 +379,12 @@ ComplexCarve carve_complex(Arena& a, int n, int flags) {
   c.lam2 = a.take<double>(N);
   c.src = a.take<int>(n);
   c.cls = a.take<char>(sizeof(Cluster) * (size_t)(n + 1));
-  c.ws_bytes = solve_bytes(N, flags);
+  // the solve workspace doubles as the extraction scratch once the solve is
+  // done: two n x n complex column-major blocks and the band Gram, then (host
+  // entry only) room for the outputs
+  const size_t cb = 16 * (size_t)n * n;
+  c.scratch_bytes = 2 * cb + 16 * (size_t)n * (kPolW + 1) + 512;
+  c.ws_bytes = std::max(solve_bytes(N, flags), c.scratch_bytes + 2 * cb + 512);
   c.ws = a.take<char>(c.ws_bytes);
   return c;
 }
@@ -320,16 +427,28 @@ cudaError_t solve_complex(int n, const double2* A, long long lda, const double2*
   if (ncl > 0 && (e = cudaMemcpyAsync(c.cls, plan.cls.data(), sizeof(Cluster) * ncl,
                                       cudaMemcpyHostToDevice, s)) != cudaSuccess)
     return e;
+  // scratch (column-major complex, ld n) and the band Gram in the dead solve
+  // workspace
+  double2* S1 = reinterpret_cast<double2*>(c.ws);
+  double2* S2 = S1 + (size_t)n * n;
+  double2* G = S2 + (size_t)n * n;
   {
-    const dim3 grid((unsigned)ceil_div(n, kT), (unsigned)ceil_div(n, kT));
-    extract_simple_kernel<<<grid, dim3(kT, 8), 0, s>>>(n, c.src, c.K, c.M, c.ld, X1c, ldx1, X2c,
-                                                       ldx2);
+    const long long tot = (long long)n * n;
+    extract_simple_kernel<<<(unsigned)ceil_div(tot, 256), 256, 0, s>>>(n, c.src, c.K, c.M, c.ld,
+                                                                      S1, S2, n);
     count_launch();
   }
   if (ncl > 0) {
     extract_cluster_kernel<<<ncl, kClThreads, 0, s>>>(n, reinterpret_cast<const Cluster*>(c.cls),
-                                                      c.K, c.M, c.ld, X1c, ldx1, X2c, ldx2);
+                                                      c.K, c.M, c.ld, S1, S2, n);
     count_launch();
+  }
+  stage_mark("polish", s);
+  {
+    const unsigned g = (unsigned)ceil_div(n, kPolT);
+    band_gram_kernel<<<g, kPolThreads, 0, s>>>(n, S1, S2, n, G);
+    band_apply_kernel<<<g, kPolThreads, 0, s>>>(n, S1, S2, n, G, X1c, ldx1, X2c, ldx2);
+    count_launch(2);
   }
   if ((e = cudaGetLastError()) != cudaSuccess) return e;
   if (lam_dev &&

@@ -19,8 +19,9 @@ struct ComplexCarve {
   double* lam2;   // N
   int* src;       // n
   char* cls;      // cluster descriptors
-  char* ws;       // solve workspace (solve_bytes(N))
+  char* ws;       // solve workspace (solve_bytes(N)); extraction scratch after the solve
   size_t ws_bytes;
+  size_t scratch_bytes;  // extraction scratch at the start of ws
 };
 ComplexCarve carve_complex(Arena& a, int n, int flags);
 size_t complex_bytes(int n, int flags);

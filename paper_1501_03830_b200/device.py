@@ -82,3 +82,38 @@ def mask_array(ma=None, mb=None, mc=None):
             lo, hi, unit = m
             out += [-big if lo is None else lo, big if hi is None else hi, unit]
     return (C.c_int32 * 9)(*out)
+
+
+def upload_colmajor(a: np.ndarray, device):
+    """Column-major device copy of a float64 host matrix: the C-order storage
+    goes up as stored through the library's pinned staging ring
+    (bse_memcpy2d_staged) and is transposed on the device; returns (tensor, ld)."""
+    torch = _torch()
+    a = np.ascontiguousarray(a, dtype=np.float64)
+    rows, cols = a.shape
+    t, ld = colmajor_empty(rows, cols, device, zero=True)
+    if rows and cols:
+        tmp = torch.empty((rows, cols), dtype=torch.float64, device=device)
+        st = _lib.load().bse_memcpy2d_staged(1, tmp.data_ptr(), 8 * cols, a.ctypes.data, 8 * cols,
+                                            8 * cols, rows,
+                                            torch.cuda.current_stream(device).cuda_stream)
+        check(st, "bse_memcpy2d_staged")
+        t[:cols, :rows].copy_(tmp.T)
+        del tmp
+    return t, ld
+
+
+def download_complex(t, rows: int, cols: int) -> np.ndarray:
+    """numpy complex128 (rows x cols, C order) of the column-major real device
+    matrix in ``t`` (imaginary part 0): transposed and widened on the device,
+    then copied through the staging ring (bse_memcpy2d_staged)."""
+    torch = _torch()
+    out = np.empty((rows, cols), dtype=np.complex128)
+    if rows and cols:
+        dev = torch.zeros((rows, cols), dtype=torch.complex128, device=t.device)
+        torch.view_as_real(dev)[..., 0].copy_(view_colmajor(t, rows, cols))
+        st = _lib.load().bse_memcpy2d_staged(0, out.ctypes.data, 16 * cols, dev.data_ptr(),
+                                            16 * cols, 16 * cols, rows,
+                                            torch.cuda.current_stream(t.device).cuda_stream)
+        check(st, "bse_memcpy2d_staged")
+    return out

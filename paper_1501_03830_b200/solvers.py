@@ -15,8 +15,8 @@ import ctypes as C
 import numpy as np
 
 from . import _lib
-from .device import (colmajor_empty, from_device_colmajor, ptr, require_cuda, stream_ptr,
-                     to_device_colmajor, view_colmajor)
+from .device import (colmajor_empty, download_complex, ptr, require_cuda, stream_ptr,
+                     to_device_colmajor, upload_colmajor, view_colmajor)
 from .types import (BseOperator, ConvergenceError, NotPositiveDefinite,
                     PositiveEigensystem, conditioning_warnings)
 
@@ -90,16 +90,25 @@ def solve_real(op: BseOperator) -> PositiveEigensystem:
     n = op.n
     if n == 0:
         return PositiveEigensystem(lambda_plus=np.zeros(0), x1=np.zeros((0, 0)), x2=np.zeros((0, 0)))
+    lam_h, x1, x2 = _solve_real_pair(op)
+    return PositiveEigensystem(lambda_plus=lam_h, x1=x1, x2=x2,
+                               warnings=conditioning_warnings(lam_h))
+
+
+def _solve_real_pair(op: BseOperator):
+    """(lam, X1, X2 complex128 C-order) of the real product form: M = A+B,
+    K = A-B uploaded through the staging ring (lower triangles read, as the
+    reference's cholesky), the device solve, X transposed and widened to
+    complex128 on the device and downloaded through the staging ring."""
+    n = op.n
     dev = _device()
     m, k = _real_pair(op)
-    Mt, ldm = to_device_colmajor(m, dev)
-    Kt, ldk = to_device_colmajor(k, dev)
+    Mt, ldm = upload_colmajor(m, dev)
+    Kt, ldk = upload_colmajor(k, dev)
     lam, X1, X2, _ = solve_pair_device(Mt, ldm, Kt, ldk, n)
+    del Mt, Kt
     lam_h = lam.cpu().numpy()
-    x1 = from_device_colmajor(X1, n, n)
-    x2 = from_device_colmajor(X2, n, n)
-    return PositiveEigensystem(lambda_plus=lam_h, x1=x1.astype(np.complex128),
-                               x2=x2.astype(np.complex128), warnings=conditioning_warnings(lam_h))
+    return lam_h, download_complex(X1, n, n), download_complex(X2, n, n)
 
 
 def real_embedding(op: BseOperator):
@@ -222,20 +231,13 @@ def solve_complex(op: BseOperator, workers: int = 1) -> PositiveEigensystem:
         return PositiveEigensystem(lambda_plus=np.zeros(0), x1=np.zeros((0, 0)), x2=np.zeros((0, 0)))
     dev = _device()
     if op.kind == "real":
-        m, k = _real_pair(op)
-        Mt, ldm = to_device_colmajor(m, dev)
-        Kt, ldk = to_device_colmajor(k, dev)
         try:
-            lam, X1, X2, _ = solve_pair_device(Mt, ldm, Kt, ldk, n)
+            lam_h, x1, x2 = _solve_real_pair(op)
         except NotPositiveDefinite as err:
             # build_m = diag(A+B, A-B): A-B pivots are offset by n
             idx = err.pivot_index if err.failed_factor == 1 else n + err.pivot_index
             raise NotPositiveDefinite(idx, err.pivot_value, _WHAT_M) from None
-        lam_h = lam.cpu().numpy()
-        x1 = from_device_colmajor(X1, n, n)
-        x2 = from_device_colmajor(X2, n, n)
-        return PositiveEigensystem(lambda_plus=lam_h, x1=x1.astype(np.complex128),
-                                   x2=x2.astype(np.complex128),
+        return PositiveEigensystem(lambda_plus=lam_h, x1=x1, x2=x2,
                                    warnings=conditioning_warnings(lam_h))
     lam, x1, x2 = _solve_complex_host(op.a, op.b, n)
     return PositiveEigensystem(lambda_plus=lam, x1=x1, x2=x2, warnings=conditioning_warnings(lam))

@@ -53,3 +53,70 @@ def random_spd_real(n, seed):
 def random_rotation(n, seed):
     q, r = np.linalg.qr(np.random.default_rng(seed).standard_normal((n, n)))
     return q * np.sign(np.diagonal(r))
+
+
+# ---------------------------------------------------------------------------
+# SURVEY 8c parity procedure (steps 3-5): eigenvectors equal up to a unit
+# phase for isolated eigenvalues, within n eps |W| / gap_j(lambda^2); for
+# clusters, principal angles between the spans against the same bound with
+# the gap to the rest of the spectrum.  |W| = lambda_1^2 (W = L^T M L).
+EPS = float(np.finfo(np.float64).eps)
+
+
+def principal_angle(x_new, x_ref):
+    """Largest principal angle between span(x_new) and span(x_ref)."""
+    qa, _ = np.linalg.qr(x_new)
+    qb, _ = np.linalg.qr(x_ref)
+    s = np.linalg.svd(qa.conj().T @ qb, compute_uv=False)
+    return float(np.arccos(np.clip(s.min(), -1.0, 1.0)))
+
+
+def vector_parity(lam, x_new, x_ref, n_scale, cluster_rtol=None, factor=1.0):
+    """Assert the 8c(4)/(5) gates; returns (worst singleton ratio err/tol,
+    worst cluster ratio) for reporting.  lam descending (positive); columns of
+    x_* are the 2n-vectors [x1; x2]."""
+    lam = np.asarray(lam, dtype=np.float64)
+    l2 = lam ** 2
+    wn = l2[0]
+    if cluster_rtol is None:
+        cluster_rtol = 1e3 * n_scale * EPS
+    # clusters in lambda^2 (relative to |W|)
+    groups, i = [], 0
+    while i < l2.shape[0]:
+        j = i + 1
+        while j < l2.shape[0] and l2[j - 1] - l2[j] <= cluster_rtol * wn:
+            j += 1
+        groups.append((i, j))
+        i = j
+    worst_s = worst_c = 0.0
+    for gi, (i, j) in enumerate(groups):
+        left = l2[groups[gi - 1][1] - 1] - l2[i] if gi > 0 else np.inf
+        right = l2[j - 1] - l2[groups[gi + 1][0]] if gi + 1 < len(groups) else np.inf
+        gap = max(min(left, right), 1e-300)
+        tol = factor * n_scale * EPS * wn / gap
+        if j - i == 1:
+            a, b = x_ref[:, i], x_new[:, i]
+            c = np.vdot(a, b)
+            c = c / abs(c) if abs(c) > 0 else 1.0
+            err = np.linalg.norm(b - c * a) / np.linalg.norm(a)
+            assert err <= max(tol, 1e-13), ("singleton", i, err, tol)
+            worst_s = max(worst_s, err / tol)
+        else:
+            ang = principal_angle(x_new[:, i:j], x_ref[:, i:j])
+            assert ang <= max(tol, 1e-13), ("cluster", i, j, ang, tol)
+            worst_c = max(worst_c, ang / tol)
+    return worst_s, worst_c
+
+
+def lapack_solution(m, k):
+    """Independent LAPACK route for a real pair (M, K): K = L L^T,
+    W = L^T M L = Z Lam^2 Z^T, X1,2 = (L Z +- L^-T Z Lam) Lam^-1/2 / 2."""
+    low = np.linalg.cholesky(k)
+    w = low.T @ m @ low
+    l2, z = np.linalg.eigh(0.5 * (w + w.T))
+    l2, z = l2[::-1], z[:, ::-1]
+    lam = np.sqrt(l2)
+    u = low @ z
+    v = np.linalg.solve(low.T, z * lam)
+    sc = 0.5 / np.sqrt(lam)
+    return lam, (u + v) * sc, (u - v) * sc

@@ -1,0 +1,120 @@
+"""Parity at the stated tolerances: the reference's acceptance
+criteria 1-4 (test_acceptance.py:31-104) with its seeds and generator
+(random_bse, core.py:245-278), eigenvector parity at n eps |W| / gap(lambda^2)
+with principal angles inside clusters against an independent LAPACK route on
+cfg4-recipe (clustered) instances, and a graded-operand stress test of the
+emulated-FP64 engine against BSE_FLAG_NATIVE_FP64."""
+import numpy as np
+import pytest
+
+import paper_1501_03830_b200 as bg
+from paper_1501_03830_b200 import _lib, configs
+from paper_1501_03830_b200.device import from_device_colmajor, to_device_colmajor
+
+from conftest import lapack_solution, vector_parity
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.mark.parametrize("n", [32, 128, 512])
+def test_criterion_1_ten_seeds(dev, n):
+    """r1, r2 <= 5e-14 for 10 seeds at n = 32, 128, 512 (test_acceptance.py:31-43)."""
+    worst = 0.0
+    for seed in range(10):
+        op = configs.random_bse(n, seed)
+        r1, r2 = bg.residual_metrics(op, bg.expand_full(op, bg.solve_complex(op)))
+        worst = max(worst, r1, r2)
+    assert worst <= 5e-14, worst
+
+
+def test_criterion_2_oracle_equivalence(dev):
+    """solve_complex vs solve_oracle over 50 seeds (n <= 64) and solve_real
+    vs solve_complex over 50 real seeds: 1e-12 relative to |H|
+    (test_acceptance.py:46-66)."""
+    worst = worst_real = 0.0
+    for seed in range(50):
+        n = int(np.random.default_rng(seed).integers(2, 65))
+        op = configs.random_bse(n, seed)
+        lam = bg.solve_complex(op).lambda_plus
+        oracle = bg.solve_oracle(op)[:n]
+        worst = max(worst, float(np.max(np.abs(lam - oracle)) / lam[0]))
+    for seed in range(50):
+        n = int(np.random.default_rng(1000 + seed).integers(2, 65))
+        op = configs.random_bse(n, seed, kind="real")
+        lam_c = bg.solve_complex(op).lambda_plus
+        lam_r = bg.solve_real(op).lambda_plus
+        worst_real = max(worst_real, float(np.max(np.abs(lam_r - lam_c)) / lam_c[0]))
+    assert worst <= 1e-12 and worst_real <= 1e-12, (worst, worst_real)
+
+
+def test_criterion_3_structure_preservation(dev):
+    """Bitwise +- pairing of the expanded spectrum; the oracle route has a
+    measurable pairing defect (test_acceptance.py:69-86)."""
+    for seed in range(5):
+        op = configs.random_bse(24, seed)
+        full = bg.expand_full(op, bg.solve_complex(op))
+        assert np.array_equal(full.lam[24:], -full.lam[:24]) and full.lam.dtype == np.float64
+    defects = [float(np.max(np.abs(v + v[::-1])))
+               for v in (bg.solve_oracle(configs.random_bse(24, s)) for s in range(8))]
+    assert max(defects) > 0.0
+
+
+def test_criterion_4_tda_bound(dev):
+    """100 instances, n <= 64: min_j (lam_j(A) - lam_j(H)) >= -1e-12 |A|_2
+    and dos dominance (test_acceptance.py:89-104)."""
+    worst = np.inf
+    for seed in range(100):
+        n = int(np.random.default_rng(seed).integers(2, 65))
+        op = configs.random_bse(n, seed)
+        lam_h = bg.solve_complex(op).lambda_plus
+        lam_a = bg.hermitian_eigvals(op.a)
+        worst = min(worst, float(np.min(lam_a - lam_h) / np.max(np.abs(lam_a))))
+        assert bg.dos_dominance(lam_h, lam_a)
+    assert worst >= -1e-12, worst
+
+
+@pytest.mark.parametrize("n", [2048, 4608])
+def test_cfg4_recipe_vectors_vs_lapack(dev, n):
+    """cfg4 recipe (256 clusters, 1e-6 relative spread): every eigenvector
+    within n eps |W| / gap(lambda^2) of LAPACK's, or -- inside the clusters
+    -- the cluster's span within principal angle n eps |W| / gap to the
+    rest.  n = 4608 runs the emulated-FP64 engine."""
+    a, b, _ = configs.config_operator(4, n=n)
+    op = bg.make_operator(a, b, kind="real")
+    pos = bg.solve_real(op)
+    lam_ref, x1r, x2r = lapack_solution(a + b, a - b)
+    assert np.max(np.abs(pos.lambda_plus - lam_ref) / lam_ref) <= 1e-10
+    ws, wc = vector_parity(lam_ref, np.vstack([pos.x1.real, pos.x2.real]),
+                           np.vstack([x1r, x2r]), n)
+    assert ws <= 1.0 and wc <= 1.0
+
+
+def test_graded_operand_emulated_vs_native(dev):
+    """Rows of K spanning 30 binades (kappa(K) ~ 1e10): the emulated-FP64
+    engine (per-row power-of-two scaling, Ozaki scheme II) must agree with the
+    all-DMMA path and meet the per-pair gates."""
+    n = 4608
+    rng = np.random.default_rng(12)
+    q = configs.haar_orthogonal(rng, n)
+    c = (q * rng.uniform(1.0, 10.0, n)) @ q.T
+    dsc = 2.0 ** (15.0 * np.linspace(0.0, 1.0, n))  # D C D: rows span 30 binades
+    k = dsc[:, None] * c * dsc[None, :]
+    k = 0.5 * (k + k.T)
+    q2 = configs.haar_orthogonal(rng, n)
+    m = (q2 * rng.uniform(1.0, 10.0, n)) @ q2.T
+    m = 0.5 * (m + m.T)
+    Mt, ldm = to_device_colmajor(m, dev)
+    Kt, ldk = to_device_colmajor(k, dev)
+    lam_e, X1e, X2e, ld = bg.solve_pair_device(Mt, ldm, Kt, ldk, n)
+    lam_n, X1n, X2n, _ = bg.solve_pair_device(Mt, ldm, Kt, ldk, n, flags=_lib.FLAG_NATIVE_FP64)
+    le, ln = lam_e.cpu().numpy(), lam_n.cpu().numpy()
+    assert np.max(np.abs(le - ln) / ln) <= 1e-10
+    from paper_1501_03830_b200.verify import pair_residuals_device
+    for lam, X1, X2 in ((lam_e, X1e, X2e), (lam_n, X1n, X2n)):
+        res, xn, bio = pair_residuals_device(n, Mt, ldm, Kt, ldk, lam, X1, ld, X2, ld)
+        assert float((res / (lam[0] * xn)).max()) <= 1e-13 * n
+        assert float(bio) <= 1e-12 * n
+    # eigenvectors of the two engines agree at the 8c(4) bound
+    x_e = np.vstack([from_device_colmajor(X1e, n, n), from_device_colmajor(X2e, n, n)])
+    x_n = np.vstack([from_device_colmajor(X1n, n, n), from_device_colmajor(X2n, n, n)])
+    vector_parity(ln, x_e, x_n, n)

@@ -11,6 +11,8 @@ import paper_1501_03830_b200 as bg
 from oracle import bse_oracle as orc
 from paper_1501_03830_b200 import configs
 
+from conftest import vector_parity
+
 pytestmark = pytest.mark.gpu
 G = Path(__file__).resolve().parent / "golden"
 
@@ -24,21 +26,9 @@ def x_full(pos):
 
 
 def assert_vectors_match(lam, x_new, x_ref, n_scale):
-    """Columns equal up to a unit phase: tolerance scales
-    as n eps |W| / gap."""
-    lam = np.asarray(lam)
-    gaps = np.empty_like(lam)
-    d = np.abs(np.diff(lam))
-    gaps[:] = np.inf
-    gaps[:-1] = np.minimum(gaps[:-1], d)
-    gaps[1:] = np.minimum(gaps[1:], d)
-    for j in range(lam.shape[0]):
-        a, b = x_ref[:, j], x_new[:, j]
-        c = np.vdot(a, b)
-        c = c / abs(c) if abs(c) > 0 else 1.0
-        err = np.linalg.norm(b - c * a) / np.linalg.norm(a)
-        rel_gap = gaps[j] / max(lam[0], 1e-300)
-        assert err <= max(1e-12, 1e2 * n_scale * 2.2e-16 / max(rel_gap, 1e-16)), (j, err, rel_gap)
+    """n eps |W| / gap(lambda^2) per isolated vector,
+    principal angles inside clusters (conftest.vector_parity)."""
+    vector_parity(lam, x_new, x_ref, n_scale)
 
 
 def test_complex_1x1_analytic(dev):
