@@ -6,8 +6,8 @@ types, the structural transforms and the solvers, with the numerical core in
 the CUDA library libbse_b200.so (C ABI: include/bse_b200.h).
 """
 from .solvers import (hermitian_eigvals, real_embedding, solve_complex, solve_complex_device,
-                      solve_pair_device, solve_real, syevd_values_device, tda_gap_report,
-                      validate)
+                      solve_oracle, solve_pair_device, solve_real, syevd_values_device,
+                      tda_gap_report, validate)
 from .spectra import absorption_device, absorption_spectrum
 from .verify import PairResidualReport, pair_residual_report, pair_residuals_device
 from .types import (BseOperator, ConvergenceError, DipoleData, FullEigensystem,
@@ -23,7 +23,8 @@ __all__ = [
     "assemble_h", "make_operator", "residual_metrics", "build_m", "expand_full",
     "ConvergenceError", "NotPositiveDefinite", "solve_complex", "solve_real",
     "DipoleData", "SpectrumCurve", "absorption_spectrum", "default_grid", "dos_dominance",
-    "conditioning_warnings", "real_embedding", "solve_complex_device", "solve_pair_device",
+    "conditioning_warnings", "real_embedding", "solve_complex_device", "solve_oracle",
+    "solve_pair_device",
     "absorption_device", "hermitian_eigvals", "tda_gap_report", "TdaGapReport",
     "syevd_values_device", "PairResidualReport", "pair_residual_report",
     "pair_residuals_device", "validate", "__version__",

@@ -1,6 +1,8 @@
 // extern "C" boundary (include/bse_b200.h).  Never throws across the ABI:
 // every entry point returns a bse_status and records a message retrievable
 // with bse_last_error().
+#include <algorithm>
+#include <cmath>
 #include <cstdio>
 #include <cstring>
 #include <mutex>
@@ -205,6 +207,19 @@ int bse_solve_spd_pair_host(int64_t n, const double* M, int64_t ldm, const doubl
     return fail(BSE_BAD_ARGUMENT, "bad dimension");
   if (check_solve_flags(flags) != BSE_OK) return BSE_BAD_ARGUMENT;
   if (n == 0) return BSE_OK;
+  {
+    // graded-input guard decided on the host: K and M reach the device in
+    // pieces overlapped with the Cholesky, so the solve cannot read their
+    // diagonals up front
+    double mlo = HUGE_VAL, mhi = -HUGE_VAL, klo = HUGE_VAL, khi = -HUGE_VAL;
+    for (int64_t i = 0; i < n; ++i) {
+      const double m = M[i + i * ldm], k = K[i + i * ldk];
+      mlo = std::min(mlo, m); mhi = std::max(mhi, m);
+      klo = std::min(klo, k); khi = std::max(khi, k);
+    }
+    flags |= (bse::diag_graded(mlo, mhi) || bse::diag_graded(klo, khi)) ? bse::kFlagGraded
+                                                                       : bse::kFlagNotGraded;
+  }
   cudaMemPool_t pool;
   BSE_TRY_CUDA(host_pool(&pool), "memory pool");
   cudaStream_t s, s2;

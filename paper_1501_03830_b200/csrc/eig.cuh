@@ -113,6 +113,8 @@ struct StedcWork {
   size_t oz_bytes = 0;
   double* scal = nullptr;  // scaling scalar(s)
   int* fail = nullptr;     // set nonzero when a secular root misses its bound (reset per stedc)
+  double* dsan = nullptr;  // finite copies of d, e (non-finite input -> 0, fail set)
+  double* esan = nullptr;
 };
 size_t stedc_bytes(int n);
 StedcWork stedc_carve(Arena& a, int n);

@@ -301,6 +301,37 @@ __global__ void copy_lower_kernel(int n, const double* src, long long lds, doubl
   dst[r + (long long)c * ldd] = (r >= c) ? src[r + (long long)c * lds] : 0.0;
 }
 
+// min / max of the diagonals of M and K (graded-input guard): out = {min M,
+// max M, min K, max K}; one CTA, deterministic.
+__global__ void diag_range_kernel(int n, const double* M, long long ldm, const double* K,
+                                  long long ldk, double* out) {
+  __shared__ double red[4][32];
+  double v[4] = {HUGE_VAL, -HUGE_VAL, HUGE_VAL, -HUGE_VAL};
+  for (int i = threadIdx.x; i < n; i += blockDim.x) {
+    const double m = M[i + (long long)i * ldm], k = K[i + (long long)i * ldk];
+    v[0] = fmin(v[0], m); v[1] = fmax(v[1], m);
+    v[2] = fmin(v[2], k); v[3] = fmax(v[3], k);
+  }
+  for (int o = 16; o > 0; o >>= 1) {
+    v[0] = fmin(v[0], __shfl_xor_sync(0xffffffffu, v[0], o));
+    v[1] = fmax(v[1], __shfl_xor_sync(0xffffffffu, v[1], o));
+    v[2] = fmin(v[2], __shfl_xor_sync(0xffffffffu, v[2], o));
+    v[3] = fmax(v[3], __shfl_xor_sync(0xffffffffu, v[3], o));
+  }
+  const int w = threadIdx.x >> 5;
+  if ((threadIdx.x & 31) == 0)
+    for (int q = 0; q < 4; ++q) red[q][w] = v[q];
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const int nw = blockDim.x >> 5;
+    for (int q = 0; q < 4; ++q) {
+      double r = red[q][0];
+      for (int k = 1; k < nw; ++k) r = (q & 1) ? fmax(r, red[q][k]) : fmin(r, red[q][k]);
+      out[q] = r;
+    }
+  }
+}
+
 // Later column pieces of the host entry's K upload: wait for piece L, then
 // copy it into L's buffer (potrf hook, see PotrfHook).
 struct KTail {
@@ -499,6 +530,7 @@ cudaError_t solve_spd_pair(int n, const double* M, long long ldm, const double* 
   out->failed_factor = -1;
   out->min_pivot = 0.0;
   out->clusters = 0;
+  out->native_lm = false;
   if (n <= 0) return cudaSuccess;
   Arena a{static_cast<char*>(work), work_bytes, 0, false};
   SolveWork w = carve_solve(a, n, flags);
@@ -507,6 +539,26 @@ cudaError_t solve_spd_pair(int n, const double* M, long long ldm, const double* 
   const long long tot = (long long)n * n;
   const unsigned nb = (unsigned)ceil_div(tot, 256);
   cudaError_t e;
+  // Graded-input guard.  The emulated-FP64 engine scales each row of op(A)
+  // and column of op(B) by one power of two, so an entry far below its
+  // line's maximum keeps fewer bits than in a DGEMM; for the products with
+  // L and M (Cholesky, congruence, recovery) that only matters when their
+  // rows span many binades, which their diagonals reveal.  Above
+  // kGradedDiagRatio those products run on the DMMA engine; the orthogonal
+  // factors (D&C merges, Q1) stay emulated.
+  bool oz_lm = w.oz_bytes != 0;
+  if (oz_lm && (flags & kFlagGraded)) {
+    oz_lm = false;
+  } else if (oz_lm && !(flags & kFlagNotGraded)) {
+    double hr[4];
+    double* dr = reinterpret_cast<double*>(w.st);  // 48-byte scratch, re-initialised below
+    diag_range_kernel<<<1, 1024, 0, s>>>(n, M, ldm, K, ldk, dr);
+    count_launch();
+    if ((e = cudaMemcpyAsync(hr, dr, sizeof(hr), cudaMemcpyDeviceToHost, s)) != cudaSuccess) return e;
+    if ((e = cudaStreamSynchronize(s)) != cudaSuccess) return e;
+    oz_lm = !diag_graded(hr[0], hr[1]) && !diag_graded(hr[2], hr[3]);
+  }
+  out->native_lm = !oz_lm && w.oz_bytes != 0;
   DevStatus h0[2] = {{-1, 0, 0.0, HUGE_VAL}, {-1, 0, 0.0, HUGE_VAL}};
   if ((e = cudaMemcpyAsync(w.st, h0, sizeof(h0), cudaMemcpyHostToDevice, s)) != cudaSuccess) return e;
   // 1. K = L L^T
@@ -532,7 +584,7 @@ cudaError_t solve_spd_pair(int n, const double* M, long long ldm, const double* 
     PotrfHook hook{k_tail_hook, &tail, tail.depth};
     // the emulated engine's workspace aliases the (still idle) eigensolver's
     OzWork ozp{w.oz, w.oz_bytes, kRecoverBlock};
-    if ((e = potrf_lower(w.L, ld, n, &w.st[0], s, w.linv, w.oz_bytes ? &ozp : nullptr,
+    if ((e = potrf_lower(w.L, ld, n, &w.st[0], s, w.linv, oz_lm ? &ozp : nullptr,
                          k_pieces ? &hook : nullptr)) != cudaSuccess)
       return e;
   }
@@ -558,7 +610,7 @@ cudaError_t solve_spd_pair(int n, const double* M, long long ldm, const double* 
   const int nc = (int)(c1 - c0);
   const int sh = (int)c0;
   // 2. W = L^T M L  (T1 = M L from the lower triangle of M, then W = L^T T1, lower)
-  if (w.oz_bytes) {
+  if (oz_lm) {
     // Emulated-FP64 engine: column blocks [j0, j1) of W need only rows >= j0
     // of T1 and of L^T, so each block is two dense products on the trailing
     // square: T1_j = Msym[j0:, j0:] L[j0:, j0:j1], W[j0:, j0:j1] =
@@ -657,7 +709,7 @@ cudaError_t solve_spd_pair(int n, const double* M, long long ldm, const double* 
   const int nc_all = (int)(c1 - c0);
   if (nc_all > 0) {
     stage_mark("recover_trmm", s);
-    if (w.oz_bytes) {
+    if (oz_lm) {
       // row blocks: u[r0:r1, :] = L[r0:r1, 0:r1] Zr[0:r1, :] -- the emulated
       // engine cannot skip L's zero triangle, so trim K per block (1.25 N^3
       // executed instead of 2 N^3 with four blocks)
@@ -682,7 +734,7 @@ cudaError_t solve_spd_pair(int n, const double* M, long long ldm, const double* 
                X2 + c0 * ldx2, ldx2, hout, &evs};
     RowHook hk{rows_out_hook, &ro, 3, 0};  // eighths: the last D2H is rows [0, n/8)
     if ((e = trsm_llt(w.L, ld, n, w.W + c0 * ld, ld, nc_all, s, w.linv,
-                      w.oz_trsm.p ? &w.oz_trsm : nullptr, host_rows ? &hk : nullptr)) != cudaSuccess)
+                      (w.oz_trsm.p && oz_lm) ? &w.oz_trsm : nullptr, host_rows ? &hk : nullptr)) != cudaSuccess)
       return e;
     if (!host_rows) {
       const long long tb = (long long)n * nc_all;

@@ -37,6 +37,7 @@ struct SolveStatus {
   int failed_factor;   // 0: K (A-B), 1: M (A+B)
   double min_pivot;    // min_j L_jj^2 of K's factor (code 0)
   int clusters;        // complex path: clusters resolved by pivoted Gram-Schmidt
+  bool native_lm;      // graded-input guard moved the L / M products to DMMA
 };
 
 // Host-entry upload of K by column pieces (see PotrfHook): piece 0 =
@@ -62,6 +63,15 @@ constexpr int kRecoverBlock = 2048;      // emulated-engine column chunk
 constexpr int kFlagNativeFp64 = 0x4;
 // the emulated-FP64 engine is used for the large products from this n up
 constexpr int kOzMinN = 4096;
+// internal flags (not in the C ABI): the caller already knows whether the
+// inputs are graded (host entry: diagonals read on the host)
+constexpr int kFlagGraded = 0x100;
+constexpr int kFlagNotGraded = 0x200;
+// graded-input guard: diagonal max/min ratio above which L / M products use DMMA
+constexpr double kGradedDiagRatio = 65536.0;
+inline bool diag_graded(double lo, double hi) {
+  return lo > 0.0 && hi > 0.0 && hi > kGradedDiagRatio * lo;
+}
 
 size_t solve_bytes(int n, int flags);
 cudaError_t solve_spd_pair(int n, const double* M, long long ldm, const double* K, long long ldk,

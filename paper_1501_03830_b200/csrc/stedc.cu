@@ -45,6 +45,25 @@ __global__ void dc_init_kernel(int n, const double* d, const double* e, double* 
   Q[i + (long long)i * ld] = 1.0;
 }
 
+// Non-finite input guard: the D&C's index logic (sorting, deflation) assumes
+// finite data, so NaN / Inf in d or e are replaced by 0 in private copies and
+// reported through *fail (BSE_NO_CONVERGENCE) instead of reaching it.
+__global__ void sanitize_kernel(int n, const double* d, const double* e, double* ds, double* es,
+                                int* fail) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  bool bad = false;
+  double v = d[i];
+  if (!isfinite(v)) { v = 0.0; bad = true; }
+  ds[i] = v;
+  if (i < n - 1) {
+    double f = e[i];
+    if (!isfinite(f)) { f = 0.0; bad = true; }
+    es[i] = f;
+  }
+  if (bad && fail) atomicOr(fail, 1);
+}
+
 __global__ void absmax_kernel(int n, const double* d, const double* e, double* out) {
   __shared__ double red[32];
   double m = 0.0;
@@ -579,6 +598,8 @@ StedcWork stedc_carve(Arena& a, int n) {
   w.probs = a.take<GemmProblem>(2 * (size_t)n + 2);
   w.scal = a.take<double>(4);
   w.fail = a.take<int>(4);
+  w.dsan = a.take<double>(n);
+  w.esan = a.take<double>(n);
   return w;
 }
 
@@ -595,6 +616,10 @@ cudaError_t stedc(int n, double* d, double* e, double* wout, double* Q, long lon
   cudaError_t err;
   const long long ld = ws.ld;
   if (ws.fail && (err = cudaMemsetAsync(ws.fail, 0, sizeof(int), s)) != cudaSuccess) return err;
+  sanitize_kernel<<<(unsigned)ceil_div(n, 256), 256, 0, s>>>(n, d, e, ws.dsan, ws.esan, ws.fail);
+  count_launch();
+  d = ws.dsan;
+  e = ws.esan;
   absmax_kernel<<<1, 1024, 0, s>>>(n, d, e, ws.scal);
   count_launch();
   dc_init_kernel<<<(unsigned)ceil_div(n, 256), 256, 0, s>>>(n, d, e, ws.Da, ws.Qa, ld, ws.scal);

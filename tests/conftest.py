@@ -64,11 +64,13 @@ EPS = float(np.finfo(np.float64).eps)
 
 
 def principal_angle(x_new, x_ref):
-    """Largest principal angle between span(x_new) and span(x_ref)."""
+    """Largest principal angle between span(x_new) and span(x_ref), from its
+    sine |(I - Qa Qa^H) Qb|_2 (arccos of the cosines loses half the digits
+    near 0: arccos(1 - eps) ~ 2e-8)."""
     qa, _ = np.linalg.qr(x_new)
     qb, _ = np.linalg.qr(x_ref)
-    s = np.linalg.svd(qa.conj().T @ qb, compute_uv=False)
-    return float(np.arccos(np.clip(s.min(), -1.0, 1.0)))
+    r = qb - qa @ (qa.conj().T @ qb)
+    return float(np.arcsin(min(1.0, np.linalg.norm(r, 2))))
 
 
 def vector_parity(lam, x_new, x_ref, n_scale, cluster_rtol=None, factor=1.0):

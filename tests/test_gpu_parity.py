@@ -89,32 +89,34 @@ def test_cfg4_recipe_vectors_vs_lapack(dev, n):
     assert ws <= 1.0 and wc <= 1.0
 
 
-def test_graded_operand_emulated_vs_native(dev):
-    """Rows of K spanning 30 binades (kappa(K) ~ 1e10): the emulated-FP64
-    engine (per-row power-of-two scaling, Ozaki scheme II) must agree with the
-    all-DMMA path and meet the per-pair gates."""
+def test_graded_operands(dev):
+    """Graded inputs: K = D C D and M = D^-1 C' D^-1 with
+    D = diag(2^(15 t)), so K's and M's rows span 30 binades (kappa ~ 1e10)
+    while W = L^T M L = L_C^T C' L_C stays well conditioned and its exact
+    spectrum comes from well-scaled factors.  Per-row power-of-two scaling
+    (the emulated engine) keeps fewer bits than a DGEMM on such operands; the
+    solve's graded-input guard routes the L / M products to DMMA, and both the
+    default and the BSE_FLAG_NATIVE_FP64 solve must meet the 1e-10 gate."""
     n = 4608
     rng = np.random.default_rng(12)
     q = configs.haar_orthogonal(rng, n)
     c = (q * rng.uniform(1.0, 10.0, n)) @ q.T
-    dsc = 2.0 ** (15.0 * np.linspace(0.0, 1.0, n))  # D C D: rows span 30 binades
-    k = dsc[:, None] * c * dsc[None, :]
-    k = 0.5 * (k + k.T)
+    c = 0.5 * (c + c.T)
     q2 = configs.haar_orthogonal(rng, n)
-    m = (q2 * rng.uniform(1.0, 10.0, n)) @ q2.T
-    m = 0.5 * (m + m.T)
+    c2 = (q2 * rng.uniform(1.0, 10.0, n)) @ q2.T
+    c2 = 0.5 * (c2 + c2.T)
+    dsc = 2.0 ** (15.0 * np.linspace(0.0, 1.0, n))
+    k = dsc[:, None] * c * dsc[None, :]
+    m = c2 / dsc[:, None] / dsc[None, :]
+    lc = np.linalg.cholesky(c)
+    lam_ref = np.sqrt(np.linalg.eigvalsh(lc.T @ c2 @ lc))[::-1]
     Mt, ldm = to_device_colmajor(m, dev)
     Kt, ldk = to_device_colmajor(k, dev)
-    lam_e, X1e, X2e, ld = bg.solve_pair_device(Mt, ldm, Kt, ldk, n)
-    lam_n, X1n, X2n, _ = bg.solve_pair_device(Mt, ldm, Kt, ldk, n, flags=_lib.FLAG_NATIVE_FP64)
-    le, ln = lam_e.cpu().numpy(), lam_n.cpu().numpy()
-    assert np.max(np.abs(le - ln) / ln) <= 1e-10
     from paper_1501_03830_b200.verify import pair_residuals_device
-    for lam, X1, X2 in ((lam_e, X1e, X2e), (lam_n, X1n, X2n)):
+    for flags in (0, _lib.FLAG_NATIVE_FP64):
+        lam, X1, X2, ld = bg.solve_pair_device(Mt, ldm, Kt, ldk, n, flags=flags)
+        lh = lam.cpu().numpy()
+        assert np.max(np.abs(lh - lam_ref) / lam_ref) <= 1e-10, flags
         res, xn, bio = pair_residuals_device(n, Mt, ldm, Kt, ldk, lam, X1, ld, X2, ld)
         assert float((res / (lam[0] * xn)).max()) <= 1e-13 * n
         assert float(bio) <= 1e-12 * n
-    # eigenvectors of the two engines agree at the 8c(4) bound
-    x_e = np.vstack([from_device_colmajor(X1e, n, n), from_device_colmajor(X2e, n, n)])
-    x_n = np.vstack([from_device_colmajor(X1n, n, n), from_device_colmajor(X2n, n, n)])
-    vector_parity(ln, x_e, x_n, n)
