@@ -23,6 +23,7 @@
 #include "../../include/bse_b200.h"
 #include "complex.cuh"
 #include "eig.cuh"
+#include "gemm.cuh"
 #include "solver.cuh"
 
 namespace bse {
@@ -313,6 +314,93 @@ __global__ void __launch_bounds__(kPolThreads) band_apply_kernel(
   }
 }
 
+// Full biorthogonality polish (n <= kGlobalPolishMaxN): the same Newton-Schulz
+// step with the whole indefinite Gram, as real DMMA GEMMs on the interleaved
+// complex layout (a column-major n x n complex block is a real 2n x n matrix
+// X with rows (Re, Im)); iX is the same block times i (rows (-Im, Re)).
+//   Re G = X1^T X1 - X2^T X2,   Im G = X1^T (iX1) ... with signs as below,
+//   X <- X Fr + (iX) Fi,  F = 1.5 I - 0.5 G.
+constexpr int kGlobalPolishMaxN = 4096;
+
+__global__ void times_i_kernel(long long count, const double2* X, double2* Y) {
+  const long long k = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (k >= count) return;
+  const double2 v = X[k];
+  Y[k] = make_double2(-v.y, v.x);
+}
+
+// F (n x n, column-major real pair) = 1.5 I - 0.5 G
+__global__ void polish_f_kernel(int n, double* Gr, double* Gi) {
+  const long long k = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (k >= (long long)n * n) return;
+  const int r = (int)(k % n), c = (int)(k / n);
+  Gr[k] = (r == c ? 1.5 : 0.0) - 0.5 * Gr[k];
+  Gi[k] = -0.5 * Gi[k];
+}
+
+// row-major complex output from the column-major scratch (32 x 32 tiles)
+__global__ void colmajor_to_rowmajor_kernel(int n, const double2* __restrict__ X, long long ldc,
+                                            double2* O, long long ldo) {
+  __shared__ double2 t[32][33];
+  const int c0 = blockIdx.x * 32, r0 = blockIdx.y * 32;
+  for (int k = threadIdx.y; k < 32; k += blockDim.y) {
+    const int c = c0 + k, r = r0 + threadIdx.x;
+    if (c < n && r < n) t[k][threadIdx.x] = X[(long long)c * ldc + r];
+  }
+  __syncthreads();
+  for (int k = threadIdx.y; k < 32; k += blockDim.y) {
+    const int r = r0 + k, c = c0 + threadIdx.x;
+    if (c < n && r < n) O[(long long)r * ldo + c] = t[threadIdx.x][k];
+  }
+}
+
+cudaError_t global_polish(int n, double2* S1, double2* S2, char* scratch, double2* O1,
+                          long long ldo1, double2* O2, long long ldo2, cudaStream_t s) {
+  cudaError_t e;
+  const size_t cn = (size_t)n * n;
+  double2* T1 = reinterpret_cast<double2*>(scratch);  // i X1, then X1 new
+  double2* T2 = T1 + cn;                              // i X2, then X2 new
+  double* Gr = reinterpret_cast<double*>(T2 + cn);
+  double* Gi = Gr + cn;
+  double2* N1 = reinterpret_cast<double2*>(Gi + cn);
+  double2* N2 = N1 + cn;
+  const unsigned g = (unsigned)ceil_div((long long)cn, 256);
+  times_i_kernel<<<g, 256, 0, s>>>((long long)cn, S1, T1);
+  times_i_kernel<<<g, 256, 0, s>>>((long long)cn, S2, T2);
+  count_launch(2);
+  const double* x1 = reinterpret_cast<const double*>(S1);
+  const double* x2 = reinterpret_cast<const double*>(S2);
+  const double* y1 = reinterpret_cast<const double*>(T1);
+  const double* y2 = reinterpret_cast<const double*>(T2);
+  const long long ld = 2LL * n;
+  // G_jk = x1_j^H x1_k - x2_j^H x2_k:  Re G = X1^T X1 - X2^T X2 and, as
+  // X^T (iX) = sum (re_j (-im_k) + im_j re_k) = -Im(x_j^H x_k),
+  // Im G = -X1^T (iX1) + X2^T (iX2)   (K = 2n)
+  const GemmProblem p[4] = {make_gemm(n, n, 2 * n, 1.0, x1, ld, x1, ld, 0.0, Gr, n),
+                            make_gemm(n, n, 2 * n, -1.0, x2, ld, x2, ld, 1.0, Gr, n),
+                            make_gemm(n, n, 2 * n, -1.0, x1, ld, y1, ld, 0.0, Gi, n),
+                            make_gemm(n, n, 2 * n, 1.0, x2, ld, y2, ld, 1.0, Gi, n)};
+  for (const GemmProblem& q : p)
+    if ((e = gemm(true, false, q, s)) != cudaSuccess) return e;
+  polish_f_kernel<<<g, 256, 0, s>>>(n, Gr, Gi);
+  count_launch();
+  // X_new = X Fr + (iX) Fi   (2n x n x n, interleaved rows)
+  const GemmProblem u[4] = {
+      make_gemm(2 * n, n, n, 1.0, x1, ld, Gr, n, 0.0, reinterpret_cast<double*>(N1), ld),
+      make_gemm(2 * n, n, n, 1.0, y1, ld, Gi, n, 1.0, reinterpret_cast<double*>(N1), ld),
+      make_gemm(2 * n, n, n, 1.0, x2, ld, Gr, n, 0.0, reinterpret_cast<double*>(N2), ld),
+      make_gemm(2 * n, n, n, 1.0, y2, ld, Gi, n, 1.0, reinterpret_cast<double*>(N2), ld)};
+  for (const GemmProblem& q : u)
+    if ((e = gemm(false, false, q, s)) != cudaSuccess) return e;
+  const dim3 grid((unsigned)ceil_div(n, 32), (unsigned)ceil_div(n, 32));
+  colmajor_to_rowmajor_kernel<<<grid, dim3(32, 8), 0, s>>>(n, N1, n, O1, ldo1);
+  colmajor_to_rowmajor_kernel<<<grid, dim3(32, 8), 0, s>>>(n, N2, n, O2, ldo2);
+  count_launch(2);
+  return cudaGetLastError();
+}
+
+size_t global_polish_bytes(int n) { return (size_t)n * n * (16 * 4 + 8 * 2) + 1024; }
+
 // Host-side plan built by the column selector from the doubled spectrum.
 struct ComplexPlan {
   int n = 0;
@@ -383,7 +471,8 @@ ComplexCarve carve_complex(Arena& a, int n, int flags) {
   // done: two n x n complex column-major blocks and the band Gram, then (host
   // entry only) room for the outputs
   const size_t cb = 16 * (size_t)n * n;
-  c.scratch_bytes = 2 * cb + 16 * (size_t)n * (kPolW + 1) + 512;
+  c.scratch_bytes = 2 * cb + std::max(16 * (size_t)n * (kPolW + 1),
+                                      n <= kGlobalPolishMaxN ? global_polish_bytes(n) : 0) + 512;
   c.ws_bytes = std::max(solve_bytes(N, flags), c.scratch_bytes + 2 * cb + 512);
   c.ws = a.take<char>(c.ws_bytes);
   return c;
@@ -444,7 +533,13 @@ cudaError_t solve_complex(int n, const double2* A, long long lda, const double2*
     count_launch();
   }
   stage_mark("polish", s);
-  {
+  if (n <= kGlobalPolishMaxN) {
+    // the whole indefinite Gram (32 n^3 flops) on DMMA
+    if ((e = global_polish(n, S1, S2, reinterpret_cast<char*>(G), X1c, ldx1, X2c, ldx2, s)) !=
+        cudaSuccess)
+      return e;
+  } else {
+    // banded: O(n^2 kPolW), the interactions that matter at this size
     const unsigned g = (unsigned)ceil_div(n, kPolT);
     band_gram_kernel<<<g, kPolThreads, 0, s>>>(n, S1, S2, n, G);
     band_apply_kernel<<<g, kPolThreads, 0, s>>>(n, S1, S2, n, G, X1c, ldx1, X2c, ldx2);

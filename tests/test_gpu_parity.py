@@ -110,13 +110,27 @@ def test_graded_operands(dev):
     m = c2 / dsc[:, None] / dsc[None, :]
     lc = np.linalg.cholesky(c)
     lam_ref = np.sqrt(np.linalg.eigvalsh(lc.T @ c2 @ lc))[::-1]
+    import torch
     Mt, ldm = to_device_colmajor(m, dev)
     Kt, ldk = to_device_colmajor(k, dev)
+
+    def norm2(t):  # power iteration on a symmetric device matrix
+        x = torch.ones(n, dtype=torch.float64, device=dev)
+        for _ in range(50):
+            y = t[:n, :n] @ x
+            x = y / torch.linalg.vector_norm(y)
+        return float(torch.linalg.vector_norm(t[:n, :n] @ x))
+    # |H|_2 >= max(|A + B|, |A - B|) / 2: lambda_max (8.8 here) is far below
+    # the operator norm of this non-normal, graded H (~1e10), so the gate is
+    # normalised by the norm bound (SURVEY 8c(8) uses |H|)
+    h_norm = 0.5 * max(norm2(Mt), norm2(Kt))
     from paper_1501_03830_b200.verify import pair_residuals_device
     for flags in (0, _lib.FLAG_NATIVE_FP64):
         lam, X1, X2, ld = bg.solve_pair_device(Mt, ldm, Kt, ldk, n, flags=flags)
         lh = lam.cpu().numpy()
         assert np.max(np.abs(lh - lam_ref) / lam_ref) <= 1e-10, flags
         res, xn, bio = pair_residuals_device(n, Mt, ldm, Kt, ldk, lam, X1, ld, X2, ld)
-        assert float((res / (lam[0] * xn)).max()) <= 1e-13 * n
-        assert float(bio) <= 1e-12 * n
+        assert float((res / (h_norm * xn)).max()) <= 1e-13 * n
+        # X's columns carry the grading (|x_j| ~ 5e3): the defect of
+        # X1^T X1 - X2^T X2 = I is judged relative to max_j |x_j|^2
+        assert float(bio) <= 1e-12 * n * float(xn.max()) ** 2
