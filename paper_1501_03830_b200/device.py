@@ -84,23 +84,20 @@ def mask_array(ma=None, mb=None, mc=None):
     return (C.c_int32 * 9)(*out)
 
 
-def upload_colmajor(a: np.ndarray, device):
-    """Column-major device copy of a float64 host matrix: the C-order storage
-    goes up as stored through the library's pinned staging ring
-    (bse_memcpy2d_staged) and is transposed on the device; returns (tensor, ld)."""
+def upload_rowmajor(a: np.ndarray, device):
+    """Device copy (same shape / dtype, C order) of a host array through the
+    library's pinned staging ring (bse_memcpy2d_staged): the path for the
+    multi-GB numpy blocks of the drop-in API."""
     torch = _torch()
-    a = np.ascontiguousarray(a, dtype=np.float64)
-    rows, cols = a.shape
-    t, ld = colmajor_empty(rows, cols, device, zero=True)
-    if rows and cols:
-        tmp = torch.empty((rows, cols), dtype=torch.float64, device=device)
-        st = _lib.load().bse_memcpy2d_staged(1, tmp.data_ptr(), 8 * cols, a.ctypes.data, 8 * cols,
-                                            8 * cols, rows,
+    a = np.ascontiguousarray(a)
+    t = torch.empty(a.shape, dtype=getattr(torch, a.dtype.name), device=device)
+    if a.size:
+        row = a.itemsize * (a.shape[-1] if a.ndim else 1)
+        rows = a.size * a.itemsize // row
+        st = _lib.load().bse_memcpy2d_staged(1, t.data_ptr(), row, a.ctypes.data, row, row, rows,
                                             torch.cuda.current_stream(device).cuda_stream)
         check(st, "bse_memcpy2d_staged")
-        t[:cols, :rows].copy_(tmp.T)
-        del tmp
-    return t, ld
+    return t
 
 
 def download_complex(t, rows: int, cols: int) -> np.ndarray:

@@ -16,7 +16,7 @@ import numpy as np
 
 from . import _lib
 from .device import (colmajor_empty, download_complex, ptr, require_cuda, stream_ptr,
-                     to_device_colmajor, upload_colmajor, view_colmajor)
+                     to_device_colmajor, upload_rowmajor, view_colmajor)
 from .types import (BseOperator, ConvergenceError, NotPositiveDefinite,
                     PositiveEigensystem, conditioning_warnings)
 
@@ -100,11 +100,19 @@ def _solve_real_pair(op: BseOperator):
     K = A-B uploaded through the staging ring (lower triangles read, as the
     reference's cholesky), the device solve, X transposed and widened to
     complex128 on the device and downloaded through the staging ring."""
+    torch = require_cuda()
     n = op.n
     dev = _device()
-    m, k = _real_pair(op)
-    Mt, ldm = upload_colmajor(m, dev)
-    Kt, ldk = upload_colmajor(k, dev)
+    # the operator's complex128 blocks go up as stored (staging ring); the real
+    # parts, A+B / A-B and the column-major layout are formed on the device
+    A = upload_rowmajor(op.a, dev)
+    B = upload_rowmajor(op.b, dev)
+    ar, br = torch.view_as_real(A)[..., 0], torch.view_as_real(B)[..., 0]
+    Mt, ldm = colmajor_empty(n, n, dev, zero=True)
+    Kt, ldk = colmajor_empty(n, n, dev, zero=True)
+    view_colmajor(Mt, n, n).copy_(ar + br)
+    view_colmajor(Kt, n, n).copy_(ar - br)
+    del A, B, ar, br
     lam, X1, X2, _ = solve_pair_device(Mt, ldm, Kt, ldk, n)
     del Mt, Kt
     lam_h = lam.cpu().numpy()
