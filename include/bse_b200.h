@@ -231,6 +231,44 @@ int bse_solve_spd_pair_dist_dev(bse_comm* comm, int64_t n, const double* dM, int
                                 int64_t ldx1, double* dX2, int64_t ldx2, void* dWork,
                                 size_t work_bytes, int flags, void* stream, bse_info* info);
 
+
+/*
+ * Memory-distributed multi-GPU solve (csrc/dist.cu).
+ * Same contract as bse_solve_spd_pair_dev -- the sharded form of
+ * solvers.solve_real (pkg/src/bse/solvers.py:80-109) and of the paper's
+ * distributed algorithm -- but no rank ever holds an
+ * N x N matrix: M, K -> L, T1 = M L, W = L^T M L, the SY2SB reflectors and
+ * X1, X2 are laid out block-cyclically by COLUMN TILES of width nb (the
+ * 1 x Q grid of the 2-D block-cyclic family: global column tile J lives on
+ * rank J mod Q with all its rows), and the divide and conquer's eigenvector
+ * matrix by contiguous ROW blocks (bse_shard_range).  Per-rank dense storage
+ * is O(n^2 / Q); the band, the tridiagonal data and the bulge-chasing
+ * reflectors (n^2 doubles) are replicated.
+ *
+ * Called collectively.  dMloc, dKloc: this rank's bse_bc_local_cols columns
+ * (n rows each; lower triangle of the global matrices referenced; local
+ * column lc is global column bse_bc_global_col(lc)).  dLam: all n eigenvalues
+ * (descending) on every rank.  dX1loc, dX2loc: this rank's columns of X1, X2
+ * in the same layout (solution column c pairs with dLam[c]).  nb: a multiple
+ * of 64 (BASELINE: 512 for cfg2/cfg3, 1024 for cfg4).  Exchanges: panel
+ * broadcasts (Cholesky, SUMMA congruence, SY2SB reflectors, Q1 panel groups,
+ * recovery), sums (each SY2SB panel's A22 V; band; D&C boundary rows) and
+ * one transposition of the tridiagonal eigenvectors.
+ */
+int64_t bse_bc_local_cols(int64_t n, int nb, int world, int rank);
+int64_t bse_bc_global_col(int64_t local_col, int nb, int world, int rank);
+/* Workspace of one rank; *distributed / *replicated (may be NULL) split it
+ * into the O(n^2 / Q) part and the replicated part. */
+size_t bse_solve_bc_workspace_bytes(int64_t n, int nb, int world, int rank, int flags,
+                                    size_t* distributed, size_t* replicated);
+int bse_solve_spd_pair_bc_dev(bse_comm* comm, int64_t n, int nb, const double* dMloc, int64_t ldm,
+                              const double* dKloc, int64_t ldk, double* dLam, double* dX1loc,
+                              int64_t ldx1, double* dX2loc, int64_t ldx2, void* dWork,
+                              size_t work_bytes, int flags, void* stream, bse_info* info);
+/* Sum of `count` doubles at dptr over all ranks, in place (exposed for tests
+ * of the transports). */
+int bse_comm_allreduce_sum_dev(bse_comm* comm, double* dptr, size_t count, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

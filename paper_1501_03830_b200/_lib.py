@@ -81,6 +81,14 @@ SIGNATURES = {
     "bse_comm_allgather_cols_dev": (_INT, [_P, _P, _I64, _I64, _P]),
     "bse_solve_spd_pair_dist_dev": (_INT, [_P, _I64, _P, _I64, _P, _I64, _P, _P, _I64, _P, _I64,
                                            _P, C.c_size_t, _INT, _P, C.POINTER(BseInfo)]),
+    # memory-distributed multi-GPU solve (block-cyclic column tiles)
+    "bse_bc_local_cols": (_I64, [_I64, _INT, _INT, _INT]),
+    "bse_bc_global_col": (_I64, [_I64, _INT, _INT, _INT]),
+    "bse_solve_bc_workspace_bytes": (C.c_size_t, [_I64, _INT, _INT, _INT, _INT,
+                                                  C.POINTER(C.c_size_t), C.POINTER(C.c_size_t)]),
+    "bse_solve_spd_pair_bc_dev": (_INT, [_P, _I64, _INT, _P, _I64, _P, _I64, _P, _P, _I64, _P,
+                                         _I64, _P, C.c_size_t, _INT, _P, C.POINTER(BseInfo)]),
+    "bse_comm_allreduce_sum_dev": (_INT, [_P, _P, C.c_size_t, _P]),
 }
 
 _lib = None

@@ -50,7 +50,7 @@ BSE_DEV int refl_len(int n, int b, int s, int j) {
 __global__ void __launch_bounds__(256) q2_build_kernel(int n, int b, int g, int maxsteps,
                                                        const double* __restrict__ V2,
                                                        const double* __restrict__ tau2,
-                                                       double* __restrict__ Vblk) {
+                                                       double* __restrict__ Vblk, int g_base) {
   extern __shared__ double sm[];
   const int HB = q2_hb(b, g);
   const int LV = HB + 1, LG = g + 1;
@@ -58,10 +58,11 @@ __global__ void __launch_bounds__(256) q2_build_kernel(int n, int b, int g, int 
   double* G = V + LV * g;         // g x g gram, [c*LG + a]
   double* T = G + LG * g;         // g x g, [c*LG + k]
   double* tau = T + LG * g;       // g
-  const int j = blockIdx.x, gi = blockIdx.y;
+  // Vblk holds the blocks of groups g_base, g_base + 1, ... (all groups: 0)
+  const int j = blockIdx.x, gi = g_base + blockIdx.y;
   const int s0 = gi * g;
   const int tid = threadIdx.x;
-  const size_t blk = (size_t)gi * maxsteps + j;
+  const size_t blk = (size_t)blockIdx.y * maxsteps + j;
   double* Vout = Vblk + blk * kQ2Stage;
   for (int idx = tid; idx < HB * g; idx += blockDim.x) {
     const int r = idx % HB, c = idx / HB;
@@ -206,7 +207,11 @@ BSE_DEV void q2_block_t(double (&acc)[CG][NT][2], const double* sV, const double
 template <int P, int NW, int CG>
 __global__ void __launch_bounds__(32 * (NW + 1), 1) q2_apply_pair_kernel(
     int n, int b, int maxsteps, const double* __restrict__ Vblk, double* __restrict__ Z,
-    long long ldz, int ncols) {
+    long long ldz, int ncols, int g_hi, int g_lo) {
+  // applies the blocks of sweep groups g_hi, g_hi - 1, ..., g_lo (a suffix of
+  // the full walk when called range by range, top range first; Vblk holds the
+  // blocks of group g_lo onwards).  The whole transform: g_hi = ngroups - 1,
+  // g_lo = 0.
   constexpr int G = kQ2G;
   constexpr int STAGE = kQ2Stage;
   constexpr int LDN = kQ2LDN;
@@ -243,7 +248,7 @@ __global__ void __launch_bounds__(32 * (NW + 1), 1) q2_apply_pair_kernel(
         ga -= P;
         j = 0;
         wh = 0;
-        return ga >= 0;
+        return ga >= g_lo;
       }
       if (ga - wh >= 0 && j < steps_of(ga - wh)) return true;
     }
@@ -257,16 +262,16 @@ __global__ void __launch_bounds__(32 * (NW + 1), 1) q2_apply_pair_kernel(
     mbar_fence_init();
   }
   __syncthreads();
-  if (ngroups <= 0) return;
+  if (ngroups <= 0 || g_hi < g_lo) return;
   if (warp == NW) {
     // producer: one bulk copy per block, in the consumers' order
     if (lane == 0) {
-      int ga = ngroups - 1, j = 0, wh = 0;
+      int ga = g_hi, j = 0, wh = 0;
       for (unsigned blkno = 0, st = 0, use = 0;; ++blkno) {
         // stage st is being filled for the use-th time: wait for the
         // consumers' release of its (use-1)-th fill
         if (use > 0) mbar_wait(&empty[st], (use - 1) & 1);
-        const size_t blk = (size_t)(ga - wh) * maxsteps + j;
+        const size_t blk = (size_t)(ga - wh - g_lo) * maxsteps + j;
         mbar_arrive_expect_tx(&full[st], kStageBytes);
         bulk_g2s(sm + st * STAGE, Vblk + blk * STAGE, kStageBytes, &full[st]);
         if (!advance(ga, j, wh)) break;
@@ -288,7 +293,7 @@ __global__ void __launch_bounds__(32 * (NW + 1), 1) q2_apply_pair_kernel(
   // contiguous bytes), and only a warp-level sync guards sZn
 
   double acc[CG][NT][2];
-  int ga = ngroups - 1, j = 0, wh = 0, stage = 0;
+  int ga = g_hi, j = 0, wh = 0, stage = 0;
   unsigned use = 0;  // fills of `stage` consumed so far
   bool pair_start = true;
   for (;;) {
@@ -399,27 +404,37 @@ size_t q2_block_doubles(int n, int b, int g) {
   return (size_t)ngroups * maxsteps * kQ2Stage;
 }
 
+int q2_groups(int n, int g) { return n <= 2 ? 0 : (int)ceil_div(n - 2, g); }
+
+size_t q2_range_doubles(int n, int b, int ngr) {
+  return (size_t)std::max(ngr, 1) * sb2st_maxsteps(n, b) * kQ2Stage;
+}
+
 cudaError_t q2_build(int n, int b, int g, const double* V2, const double* tau2, double* Vblk,
-                     cudaStream_t s) {
+                     cudaStream_t s, int g_lo, int g_hi) {
   if (n <= 2) return cudaSuccess;
   if (b != 64 || g != kQ2G || q2_hb(b, g) != kQ2HB) return cudaErrorInvalidValue;
   const int maxsteps = sb2st_maxsteps(n, b);
-  const int ngroups = (int)ceil_div(n - 2, g);
+  if (g_hi < 0) g_hi = (int)ceil_div(n - 2, g) - 1;
+  if (g_hi < g_lo) return cudaSuccess;
+  const int ngroups = g_hi - g_lo + 1;
   const int HB = q2_hb(b, g);
   const size_t smem = sizeof(double) * ((size_t)(HB + 1) * g + 2 * (size_t)(g + 1) * g + g);
   static PerDeviceOnce attr;
   cudaError_t ae = set_smem_limit(attr, q2_build_kernel, 200 * 1024);
   if (ae != cudaSuccess) return ae;
-  q2_build_kernel<<<dim3(maxsteps, ngroups), 256, smem, s>>>(n, b, g, maxsteps, V2, tau2, Vblk);
+  q2_build_kernel<<<dim3(maxsteps, ngroups), 256, smem, s>>>(n, b, g, maxsteps, V2, tau2, Vblk, g_lo);
   count_launch();
   return cudaGetLastError();
 }
 
 cudaError_t q2_apply(int n, int b, int g, const double* Vblk, double* Z, long long ldz, int ncols,
-                     cudaStream_t s) {
+                     cudaStream_t s, int g_lo, int g_hi) {
   if (n <= 2 || ncols <= 0) return cudaSuccess;
   if (b != 64 || g != kQ2G || q2_hb(b, g) != kQ2HB) return cudaErrorInvalidValue;
   const int maxsteps = sb2st_maxsteps(n, b);
+  if (g_hi < 0) g_hi = (int)ceil_div(n - 2, g) - 1;
+  if (g_hi < g_lo) return cudaSuccess;
   const int sms = device_sm_count();
   auto launch = [&](auto kern, int nw, int cg) {
     const size_t smem = sizeof(double) * (kQ2Stages * (size_t)kQ2Stage +
@@ -427,8 +442,8 @@ cudaError_t q2_apply(int n, int b, int g, const double* Vblk, double* Z, long lo
                         2 * kQ2Stages * sizeof(unsigned long long);
     cudaError_t ae = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (ae != cudaSuccess) return ae;
-    kern<<<(unsigned)ceil_div(ncols, 8 * cg * nw), 32 * (nw + 1), smem, s>>>(n, b, maxsteps, Vblk,
-                                                                            Z, ldz, ncols);
+    kern<<<(unsigned)ceil_div(ncols, 8 * cg * nw), 32 * (nw + 1), smem, s>>>(
+        n, b, maxsteps, Vblk, Z, ldz, ncols, g_hi, g_lo);
     count_launch();
     return cudaGetLastError();
   };
@@ -449,15 +464,11 @@ size_t q1_oz_bytes(int n, int b, int ncols, int group) {
                    ozgemm_bytes(kb, ncols, kb, c)});
 }
 
-namespace {
-
 int q1_panels(int n, int b) {
   int np = 0;
   while (n - np * b - b >= 2) ++np;
   return np;
 }
-
-}  // namespace
 
 size_t q1_tg_doubles(int n, int b, int group) {
   const int np = q1_panels(n, b);
@@ -480,16 +491,95 @@ size_t q1_vt_doubles(int n, int b, int group) {
   return std::max<size_t>(tot, 1);
 }
 
+// T_g of one group of k panels (kb = k b columns of V, m rows; Tp = the
+// panels' b x b factors back to back): T_g = [[T_A, -T_A (V_A^T V_B) T_B],
+// [0, T_B]] by pairwise merging, bottom-up: blocks A = [a0, a0+h), B =
+// [a0+h, a0+h+hb) of an already merged level combine as T_AB = -T_A X_AB T_B
+// with X = V^T V (strict block-upper part, one product per group).  VT
+// (optional, m x kb): V T_g.
+cudaError_t q1_group_build(int k, int b, int m, const double* V, long long ldv, const double* Tp,
+                           double* Tg, double* VT, const Q1Scratch& w, cudaStream_t s) {
+  const int kb = k * b;
+  cudaError_t e;
+  if ((e = cudaMemsetAsync(Tg, 0, sizeof(double) * kb * kb, s)) != cudaSuccess) return e;
+  for (int j = 0; j < k; ++j) {
+    if ((e = cudaMemcpy2DAsync(Tg + (long long)j * b + (long long)j * b * kb, kb * sizeof(double),
+                               Tp + (size_t)j * b * b, b * sizeof(double), b * sizeof(double), b,
+                               cudaMemcpyDeviceToDevice, s)) != cudaSuccess)
+      return e;
+  }
+  if (k > 1) {
+    GemmProblem gx = make_gemm(kb, kb, m, 1.0, V, ldv, V, ldv, 0.0, w.x, kb);
+    gx.mc = Mask::strict_upper();  // covers every block above the diagonal blocks
+    if (w.oz_side && (double)kb * kb * m >= kOzMinWork)
+      e = ozgemm(true, false, gx, w.oz_side, w.oz_side_bytes, kQ1OzChunk, s);
+    else
+      e = gemm(true, false, gx, s);
+    if (e != cudaSuccess) return e;
+  }
+  for (int h = b; h < kb; h *= 2) {
+    for (int a0 = 0; a0 + h < kb; a0 += 2 * h) {
+      const int c0 = a0 + h, hb = std::min(h, kb - c0);
+      // tmp = T_A X_AB   (h x hb)
+      GemmProblem g1 = make_gemm(h, hb, h, 1.0, Tg + a0 + (long long)a0 * kb, kb,
+                                 w.x + a0 + (long long)c0 * kb, kb, 0.0, w.tmp, h);
+      g1.ma = Mask::upper();
+      if ((e = gemm(false, false, g1, s)) != cudaSuccess) return e;
+      // T_g[A, B] = -tmp T_B
+      GemmProblem g2 = make_gemm(h, hb, hb, -1.0, w.tmp, h, Tg + c0 + (long long)c0 * kb, kb,
+                                 0.0, Tg + a0 + (long long)c0 * kb, kb);
+      g2.mb = Mask::upper();
+      if ((e = gemm(false, false, g2, s)) != cudaSuccess) return e;
+    }
+  }
+  if (VT) {
+    // V T_g once per group here (off the critical path), so the apply is two
+    // products instead of three
+    GemmProblem gv = make_gemm(m, kb, kb, 1.0, V, ldv, Tg, kb, 0.0, VT, m);
+    gv.mb = Mask::upper();
+    if (w.oz_side && (double)m * kb * kb >= kOzMinWork)
+      e = ozgemm(false, false, gv, w.oz_side, w.oz_side_bytes, kQ1OzChunk, s);
+    else
+      e = gemm(false, false, gv, s);
+    if (e != cudaSuccess) return e;
+  }
+  return cudaSuccess;
+}
+
+// Zs (m x ncols) <- (I - V T_g V^T) Zs for one group.
+cudaError_t q1_group_apply(int kb, int m, const double* V, long long ldv, const double* Tg,
+                           const double* VT, double* Zs, long long ldz, int ncols,
+                           const Q1Scratch& w, cudaStream_t s) {
+  cudaError_t e;
+  // one product on the INT8 engine when it is large enough to pay for the
+  // slicing and reconstruction passes
+  auto mul = [&](bool ta, const GemmProblem& g) {
+    if (w.oz && (double)g.M * g.N * g.K >= kOzMinWork)
+      return ozgemm(ta, false, g, w.oz, w.oz_bytes, kQ1OzChunk, s);
+    return gemm(ta, false, g, s);
+  };
+  // Y = V^T Zs (kb x ncols)
+  GemmProblem g3 = make_gemm(kb, ncols, m, 1.0, V, ldv, Zs, ldz, 0.0, w.y, kb);
+  if ((e = mul(true, g3)) != cudaSuccess) return e;
+  if (VT) {
+    // Zs -= (V T_g) Y
+    GemmProblem g5 = make_gemm(m, ncols, kb, -1.0, VT, m, w.y, kb, 1.0, Zs, ldz);
+    return mul(false, g5);
+  }
+  // Y2 = T_g Y; Zs -= V Y2
+  GemmProblem g4 = make_gemm(kb, ncols, kb, 1.0, Tg, kb, w.y, kb, 0.0, w.y2, kb);
+  g4.ma = Mask::upper();
+  if ((e = mul(false, g4)) != cudaSuccess) return e;
+  GemmProblem g5 = make_gemm(m, ncols, kb, -1.0, V, ldv, w.y2, kb, 1.0, Zs, ldz);
+  return mul(false, g5);
+}
+
 cudaError_t q1_build(int n, int b, const double* Vall, long long ldv, const double* Tall,
                      const Q1Scratch& w, cudaStream_t s) {
-  // Panels are merged in groups of w.group (compact-WY of the product,
-  // T_g = [[T_A, -T_A (V_A^T V_B) T_B], [0, T_B]]) so the applying GEMMs run
-  // with K = group*b instead of b.  T_g by pairwise merging, bottom-up:
-  // blocks A = [a0, a0+h), B = [a0+h, a0+h+hb) of an already merged level
-  // combine as T_AB = -T_A X_AB T_B with X = V^T V (strict block-upper part,
-  // one product per group, on the emulated engine with its own workspace:
-  // this runs on a side stream next to the divide and conquer, whose top
-  // merges use the shared one).
+  // Panels are merged in groups of w.group (compact-WY of the product) so the
+  // applying GEMMs run with K = group*b instead of b.  X = V^T V runs on the
+  // emulated engine with its own workspace: this runs on a side stream next
+  // to the divide and conquer, whose top merges use the shared one.
   // Vall must be zero outside the reflectors (syevd memsets it before SY2SB).
   const int np = q1_panels(n, b), G = w.group;
   cudaError_t e = cudaSuccess;
@@ -499,49 +589,10 @@ cudaError_t q1_build(int n, int b, const double* Vall, long long ldv, const doub
     const int p0 = std::max(0, pend - G), k = pend - p0, kb = k * b;
     const int r0 = (p0 + 1) * b, m = n - r0;
     const double* V = Vall + r0 + (long long)(p0 * b) * ldv;  // m x kb
-    if ((e = cudaMemsetAsync(Tg, 0, sizeof(double) * kb * kb, s)) != cudaSuccess) return e;
-    for (int j = 0; j < k; ++j) {
-      if ((e = cudaMemcpy2DAsync(Tg + (long long)j * b + (long long)j * b * kb, kb * sizeof(double),
-                                 Tall + (size_t)(p0 + j) * b * b, b * sizeof(double),
-                                 b * sizeof(double), b, cudaMemcpyDeviceToDevice, s)) != cudaSuccess)
-        return e;
-    }
-    if (k > 1) {
-      GemmProblem gx = make_gemm(kb, kb, m, 1.0, V, ldv, V, ldv, 0.0, w.x, kb);
-      gx.mc = Mask::strict_upper();  // covers every block above the diagonal blocks
-      if (w.oz_side && (double)kb * kb * m >= kOzMinWork)
-        e = ozgemm(true, false, gx, w.oz_side, w.oz_side_bytes, kQ1OzChunk, s);
-      else
-        e = gemm(true, false, gx, s);
-      if (e != cudaSuccess) return e;
-    }
-    for (int h = b; h < kb; h *= 2) {
-      for (int a0 = 0; a0 + h < kb; a0 += 2 * h) {
-        const int c0 = a0 + h, hb = std::min(h, kb - c0);
-        // tmp = T_A X_AB   (h x hb)
-        GemmProblem g1 = make_gemm(h, hb, h, 1.0, Tg + a0 + (long long)a0 * kb, kb,
-                                   w.x + a0 + (long long)c0 * kb, kb, 0.0, w.tmp, h);
-        g1.ma = Mask::upper();
-        if ((e = gemm(false, false, g1, s)) != cudaSuccess) return e;
-        // T_g[A, B] = -tmp T_B
-        GemmProblem g2 = make_gemm(h, hb, hb, -1.0, w.tmp, h, Tg + c0 + (long long)c0 * kb, kb,
-                                   0.0, Tg + a0 + (long long)c0 * kb, kb);
-        g2.mb = Mask::upper();
-        if ((e = gemm(false, false, g2, s)) != cudaSuccess) return e;
-      }
-    }
-    if (w.vt) {
-      // V T_g once per group here (off the critical path), so the apply is two
-      // products instead of three
-      GemmProblem gv = make_gemm(m, kb, kb, 1.0, V, ldv, Tg, kb, 0.0, VT, m);
-      gv.mb = Mask::upper();
-      if (w.oz_side && (double)m * kb * kb >= kOzMinWork)
-        e = ozgemm(false, false, gv, w.oz_side, w.oz_side_bytes, kQ1OzChunk, s);
-      else
-        e = gemm(false, false, gv, s);
-      if (e != cudaSuccess) return e;
-      VT += (size_t)m * kb;
-    }
+    if ((e = q1_group_build(k, b, m, V, ldv, Tall + (size_t)p0 * b * b, Tg, w.vt ? VT : nullptr, w,
+                            s)) != cudaSuccess)
+      return e;
+    if (w.vt) VT += (size_t)m * kb;
     Tg += (size_t)kb * kb;
   }
   return e;
@@ -551,36 +602,16 @@ cudaError_t q1_apply(int n, int b, const double* Vall, long long ldv, double* Z,
                      int ncols, const Q1Scratch& w, cudaStream_t s) {
   const int np = q1_panels(n, b), G = w.group;
   cudaError_t e = cudaSuccess;
-  // one product on the INT8 engine when it is large enough to pay for the
-  // slicing and reconstruction passes
-  auto mul = [&](bool ta, const GemmProblem& g) {
-    if (w.oz && (double)g.M * g.N * g.K >= kOzMinWork)
-      return ozgemm(ta, false, g, w.oz, w.oz_bytes, kQ1OzChunk, s);
-    return gemm(ta, false, g, s);
-  };
   const double* Tg = w.tg;
   const double* VT = w.vt;
   for (int pend = np; pend > 0; pend -= G) {
     const int p0 = std::max(0, pend - G), k = pend - p0, kb = k * b;
     const int r0 = (p0 + 1) * b, m = n - r0;
     const double* V = Vall + r0 + (long long)(p0 * b) * ldv;  // m x kb
-    double* Zs = Z + r0;
-    // Y = V^T Zs (kb x ncols)
-    GemmProblem g3 = make_gemm(kb, ncols, m, 1.0, V, ldv, Zs, ldz, 0.0, w.y, kb);
-    if ((e = mul(true, g3)) != cudaSuccess) return e;
-    if (w.vt) {
-      // Zs -= (V T_g) Y
-      GemmProblem g5 = make_gemm(m, ncols, kb, -1.0, VT, m, w.y, kb, 1.0, Zs, ldz);
-      if ((e = mul(false, g5)) != cudaSuccess) return e;
-      VT += (size_t)m * kb;
-    } else {
-      // Y2 = T_g Y; Zs -= V Y2
-      GemmProblem g4 = make_gemm(kb, ncols, kb, 1.0, Tg, kb, w.y, kb, 0.0, w.y2, kb);
-      g4.ma = Mask::upper();
-      if ((e = mul(false, g4)) != cudaSuccess) return e;
-      GemmProblem g5 = make_gemm(m, ncols, kb, -1.0, V, ldv, w.y2, kb, 1.0, Zs, ldz);
-      if ((e = mul(false, g5)) != cudaSuccess) return e;
-    }
+    if ((e = q1_group_apply(kb, m, V, ldv, Tg, w.vt ? VT : nullptr, Z + r0, ldz, ncols, w, s)) !=
+        cudaSuccess)
+      return e;
+    if (w.vt) VT += (size_t)m * kb;
     Tg += (size_t)kb * kb;
   }
   return e;

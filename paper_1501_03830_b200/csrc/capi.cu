@@ -14,6 +14,7 @@
 #include "hostio.cuh"
 #include "ozgemm.cuh"
 #include "solver.cuh"
+#include "dist.cuh"
 
 namespace {
 thread_local std::string g_last_error;
@@ -595,6 +596,67 @@ int bse_solve_spd_pair_dist_dev(bse_comm* comm, int64_t n, const double* dM, int
     return fail(BSE_CUDA_ERROR, "solve_dist: " + (why.empty() ? std::string(cudaGetErrorString(e)) : why));
   }
   return map_solve_status(st, info);
+}
+
+/* ---- memory-distributed multi-GPU solve (block-cyclic column tiles) ------ */
+
+static bool bc_args_ok(int64_t n, int nb, int world, int rank) {
+  return n >= 0 && n < (1ll << 31) && nb >= 64 && nb % 64 == 0 && world >= 1 && rank >= 0 &&
+         rank < world;
+}
+
+int64_t bse_bc_local_cols(int64_t n, int nb, int world, int rank) {
+  if (!bc_args_ok(n, nb, world, rank)) return -1;
+  bse::BcLayout lay;
+  lay.n = (int)n; lay.nb = nb; lay.world = world; lay.rank = rank;
+  return lay.ncols_of(rank);
+}
+
+int64_t bse_bc_global_col(int64_t local_col, int nb, int world, int rank) {
+  if (local_col < 0 || !bc_args_ok(0, nb, world, rank)) return -1;
+  return ((local_col / nb) * world + rank) * (int64_t)nb + local_col % nb;
+}
+
+size_t bse_solve_bc_workspace_bytes(int64_t n, int nb, int world, int rank, int flags,
+                                    size_t* distributed, size_t* replicated) {
+  if (!bc_args_ok(n, nb, world, rank)) return 0;
+  const bse::DistBytes b = bse::dist_solve_bytes((int)n, nb, world, rank, flags);
+  if (distributed) *distributed = b.distributed;
+  if (replicated) *replicated = b.replicated;
+  return b.total;
+}
+
+int bse_solve_spd_pair_bc_dev(bse_comm* comm, int64_t n, int nb, const double* dMloc, int64_t ldm,
+                              const double* dKloc, int64_t ldk, double* dLam, double* dX1loc,
+                              int64_t ldx1, double* dX2loc, int64_t ldx2, void* dWork,
+                              size_t work_bytes, int flags, void* stream, bse_info* info) {
+  if (!comm) return fail(BSE_BAD_ARGUMENT, "null communicator");
+  if (check_solve_flags(flags) != BSE_OK) return BSE_BAD_ARGUMENT;
+  if (!bc_args_ok(n, nb, comm->impl->world, comm->impl->rank))
+    return fail(BSE_BAD_ARGUMENT, "bad dimension or tile (nb must be a multiple of 64)");
+  if (ldm < n || ldk < n || ldx1 < n || ldx2 < n) return fail(BSE_BAD_ARGUMENT, "bad leading dimension");
+  if (n > 0 && work_bytes < bse::dist_solve_bytes((int)n, nb, comm->impl->world, comm->impl->rank,
+                                                  flags).total)
+    return fail(BSE_BAD_ARGUMENT, "workspace too small (see bse_solve_bc_workspace_bytes)");
+  bse::SolveStatus st{};
+  cudaError_t e = bse::solve_spd_pair_bc(*comm->impl, (int)n, nb, dMloc, ldm, dKloc, ldk, dLam,
+                                         dX1loc, ldx1, dX2loc, ldx2, dWork, work_bytes, flags,
+                                         (cudaStream_t)stream, &st);
+  if (e != cudaSuccess) {
+    const std::string why = comm->impl->error();
+    return fail(BSE_CUDA_ERROR, "solve_bc: " + (why.empty() ? std::string(cudaGetErrorString(e)) : why));
+  }
+  return map_solve_status(st, info);
+}
+
+int bse_comm_allreduce_sum_dev(bse_comm* comm, double* dptr, size_t count, void* stream) {
+  if (!comm || (!dptr && count)) return fail(BSE_BAD_ARGUMENT, "bad argument");
+  cudaError_t e = comm->impl->allreduce_sum(dptr, count, (cudaStream_t)stream);
+  if (e != cudaSuccess) {
+    const std::string why = comm->impl->error();
+    return fail(BSE_CUDA_ERROR, "allreduce: " + (why.empty() ? std::string(cudaGetErrorString(e)) : why));
+  }
+  return BSE_OK;
 }
 
 }  // extern "C"

@@ -32,6 +32,8 @@ struct NcclApi {
   ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
   ncclResult_t (*Broadcast)(const void*, void*, size_t, ncclDataType_t, int, ncclComm_t,
                             cudaStream_t) = nullptr;
+  ncclResult_t (*AllReduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t,
+                            cudaStream_t) = nullptr;
   ncclResult_t (*GroupStart)() = nullptr;
   ncclResult_t (*GroupEnd)() = nullptr;
   const char* (*GetErrorString)(ncclResult_t) = nullptr;
@@ -53,11 +55,12 @@ const NcclApi& nccl() {
     api.CommInitRank = reinterpret_cast<decltype(api.CommInitRank)>(sym("ncclCommInitRank"));
     api.CommDestroy = reinterpret_cast<decltype(api.CommDestroy)>(sym("ncclCommDestroy"));
     api.Broadcast = reinterpret_cast<decltype(api.Broadcast)>(sym("ncclBroadcast"));
+    api.AllReduce = reinterpret_cast<decltype(api.AllReduce)>(sym("ncclAllReduce"));
     api.GroupStart = reinterpret_cast<decltype(api.GroupStart)>(sym("ncclGroupStart"));
     api.GroupEnd = reinterpret_cast<decltype(api.GroupEnd)>(sym("ncclGroupEnd"));
     api.GetErrorString = reinterpret_cast<decltype(api.GetErrorString)>(sym("ncclGetErrorString"));
     api.ok = api.GetUniqueId && api.CommInitRank && api.CommDestroy && api.Broadcast &&
-             api.GroupStart && api.GroupEnd && api.GetErrorString;
+             api.AllReduce && api.GroupStart && api.GroupEnd && api.GetErrorString;
     if (!api.ok) api.why = "libnccl.so.2 lacks a required symbol";
   });
   return api;
@@ -78,6 +81,9 @@ struct NcclComm final : Comm {
     return check(nccl().Broadcast(p, p, count, ncclFloat64, root, comm, s), "ncclBroadcast");
   }
   cudaError_t group_end(cudaStream_t) override { return check(nccl().GroupEnd(), "ncclGroupEnd"); }
+  cudaError_t allreduce_sum(double* p, size_t count, cudaStream_t s) override {
+    return check(nccl().AllReduce(p, p, count, ncclFloat64, ncclSum, comm, s), "ncclAllReduce");
+  }
 };
 
 // Host-staged broadcast: D2H of the root's block, the caller's host
@@ -105,6 +111,29 @@ struct HostComm final : Comm {
     }
     return cudaSuccess;
   }
+  // every rank's block goes round by the host broadcast and is added in rank
+  // order, so all ranks form the same bits
+  std::vector<double> acc, mine;
+  cudaError_t allreduce_sum(double* p, size_t count, cudaStream_t s) override {
+    cudaError_t e;
+    mine.resize(count);
+    acc.assign(count, 0.0);
+    if ((e = cudaMemcpyAsync(mine.data(), p, count * 8, cudaMemcpyDeviceToHost, s)) != cudaSuccess)
+      return e;
+    if ((e = cudaStreamSynchronize(s)) != cudaSuccess) return e;
+    for (int r = 0; r < world; ++r) {
+      buf.resize(count);
+      if (r == rank) std::memcpy(buf.data(), mine.data(), count * 8);
+      if (fn(ctx, buf.data(), count * 8, r) != 0) {
+        err = "host broadcast callback failed";
+        return cudaErrorUnknown;
+      }
+      for (size_t i = 0; i < count; ++i) acc[i] += buf[i];
+    }
+    if ((e = cudaMemcpyAsync(p, acc.data(), count * 8, cudaMemcpyHostToDevice, s)) != cudaSuccess)
+      return e;
+    return cudaStreamSynchronize(s);
+  }
 };
 
 // Measurement-only transport: behaves as rank `rank` of `world` but moves
@@ -112,6 +141,7 @@ struct HostComm final : Comm {
 // time exactly the kernels one rank of a P-GPU solve executes.
 struct SoloComm final : Comm {
   cudaError_t bcast(double*, size_t, int, cudaStream_t) override { return cudaSuccess; }
+  cudaError_t allreduce_sum(double*, size_t, cudaStream_t) override { return cudaSuccess; }
 };
 
 }  // namespace

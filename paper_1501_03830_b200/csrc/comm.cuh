@@ -27,6 +27,10 @@ struct Comm {
   virtual cudaError_t group_begin() { return cudaSuccess; }
   virtual cudaError_t bcast(double* dptr, size_t count, int root, cudaStream_t s) = 0;
   virtual cudaError_t group_end(cudaStream_t s) { (void)s; return cudaSuccess; }
+  // Sum of `count` doubles at dptr over all ranks, in place, the same bits on
+  // every rank (panel products of the distributed band reduction, gathers of
+  // disjoint pieces padded with zeros).
+  virtual cudaError_t allreduce_sum(double* dptr, size_t count, cudaStream_t s) = 0;
   virtual std::string error() const { return err; }
   std::string err;
 };

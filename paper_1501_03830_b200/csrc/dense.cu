@@ -431,6 +431,13 @@ cudaError_t potrf_lower(double* A, long long lda, int n, DevStatus* st, cudaStre
   return zero_strict_upper(A, lda, n, s);
 }
 
+cudaError_t potrf_lower_at(double* A, long long lda, int n, int off, DevStatus* st, cudaStream_t s) {
+  if (n <= 0) return cudaSuccess;
+  cudaError_t e = potrf_rec(A, lda, n, off, st, s, nullptr, nullptr, nullptr);
+  if (e != cudaSuccess) return e;
+  return zero_strict_upper(A, lda, n, s);
+}
+
 cudaError_t zero_strict_upper(double* A, long long lda, int n, cudaStream_t s) {
   if (n <= 0) return cudaSuccess;
   zero_upper_kernel<<<dim3((unsigned)ceil_div(n, 256), (unsigned)n), 256, 0, s>>>(A, lda, n);

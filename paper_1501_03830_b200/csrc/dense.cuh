@@ -46,6 +46,11 @@ cudaError_t potrf_lower(double* A, long long lda, int n, DevStatus* st, cudaStre
                         double* inv_cache = nullptr, const OzWork* oz = nullptr,
                         const PotrfHook* hook = nullptr);
 
+// The same for a diagonal block whose first row/column is global index `off`
+// (a failing pivot is reported as off + j): the tile factorizations of the
+// distributed right-looking Cholesky.
+cudaError_t potrf_lower_at(double* A, long long lda, int n, int off, DevStatus* st, cudaStream_t s);
+
 // A (m x n) <- A * L^{-T}, L n x n lower (right, lower, transposed).
 cudaError_t trsm_rlt(const double* L, long long ldl, int n, double* A, long long lda, int m,
                      cudaStream_t s, const double* inv = nullptr, const OzWork* oz = nullptr);

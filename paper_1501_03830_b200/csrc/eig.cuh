@@ -34,6 +34,14 @@ cudaError_t sy2sb(double* A, long long lda, int n, int b, double* Vall, long lon
                   cudaEvent_t ev_panel = nullptr);
 cudaError_t extract_band(const double* A, long long lda, int n, int b, double* AB, int ldab,
                          cudaStream_t s);
+// SY2SB building blocks (also driven panel by panel by the distributed solve):
+// Householder QR of an m x bw panel (P <- R, explicit V and optional copy V2,
+// T), and W = X - 1/2 V (T^T (V^T X)), X = Y T with Y = A2 V in w.y.
+cudaError_t panel_qr(double* P, long long ldp, int m, int bw, double* V, long long ldv, double* V2,
+                     long long ldv2, double* T, double* red, unsigned* bar, int num_sms,
+                     cudaStream_t s);
+cudaError_t panel_w(int m, int bw, const double* V, long long ldv, const double* Tp, double* W,
+                    long long ldw, const Sy2sbScratch& w, cudaStream_t s);
 
 // Bulge chasing on the band (lower storage, ldab = 2b + 1): d, e out; reflectors
 // of sweep s, step j stored at V2[(s*maxsteps + j) * b], tau2[s*maxsteps + j].
@@ -45,10 +53,16 @@ cudaError_t sb2st(double* AB, int ldab, int n, int b, double* d, double* e, doub
 // compact-WY blocks (V and V*T, stored in q2_apply's shared-memory stage
 // layout); Vblk sized by q2_block_doubles().
 size_t q2_block_doubles(int n, int b, int g);
+// g_lo/g_hi: only the sweep groups [g_lo, g_hi] (g_hi < 0: the last group);
+// Vblk then holds that range's blocks (q2_range_doubles).  Applying the
+// ranges top range first, each of even length, equals the whole transform --
+// the distributed solve bounds its block storage that way.
+int q2_groups(int n, int g);
+size_t q2_range_doubles(int n, int b, int ngr);
 cudaError_t q2_build(int n, int b, int g, const double* V2, const double* tau2, double* Vblk,
-                     cudaStream_t s);
+                     cudaStream_t s, int g_lo = 0, int g_hi = -1);
 cudaError_t q2_apply(int n, int b, int g, const double* Vblk, double* Z, long long ldz, int ncols,
-                     cudaStream_t s);
+                     cudaStream_t s, int g_lo = 0, int g_hi = -1);
 
 // Q1 back-transform: Z <- Q1 Z using the SY2SB panels, merged `group` at a
 // time into one compact-WY block (kQ1Group on the DMMA engine; kQ1GroupOz
@@ -75,6 +89,14 @@ struct Q1Scratch {
 size_t q1_oz_bytes(int n, int b, int ncols, int group);
 size_t q1_tg_doubles(int n, int b, int group);
 size_t q1_vt_doubles(int n, int b, int group);
+// One group of k panels: T_g (kb x kb, kb = k b) from the panels' T factors Tp
+// and V (m x kb), optionally VT = V T_g; and its application to Zs (m x ncols).
+int q1_panels(int n, int b);
+cudaError_t q1_group_build(int k, int b, int m, const double* V, long long ldv, const double* Tp,
+                           double* Tg, double* VT, const Q1Scratch& w, cudaStream_t s);
+cudaError_t q1_group_apply(int kb, int m, const double* V, long long ldv, const double* Tg,
+                           const double* VT, double* Zs, long long ldz, int ncols,
+                           const Q1Scratch& w, cudaStream_t s);
 // T_g of every panel group (may run on a side stream; own emulated workspace).
 cudaError_t q1_build(int n, int b, const double* Vall, long long ldv, const double* Tall,
                      const Q1Scratch& w, cudaStream_t s);
@@ -115,9 +137,20 @@ struct StedcWork {
   int* fail = nullptr;     // set nonzero when a secular root misses its bound (reset per stedc)
   double* dsan = nullptr;  // finite copies of d, e (non-finite input -> 0, fail set)
   double* esan = nullptr;
+  // Row-distributed mode (dist.cu): this rank holds rows [row0, row1) of every
+  // eigenvector block (Qa, Qb are (row1 - row0) x n with leading dimension
+  // ld); U is ldu x ucols and a level whose U is wider is processed in column
+  // chunks; the children's boundary rows come through zrow, summed over the
+  // ranks by zrow_reduce.  Defaults: all rows, ldu = ld, ucols = n.
+  int row0 = 0, row1 = -1;
+  long long ldu = 0;
+  int ucols = 0;
+  double* zrow = nullptr;
+  cudaError_t (*zrow_reduce)(void* ctx, double* zrow, int n, cudaStream_t s) = nullptr;
+  void* zrow_ctx = nullptr;
 };
 size_t stedc_bytes(int n);
-StedcWork stedc_carve(Arena& a, int n);
+StedcWork stedc_carve(Arena& a, int n, int rows = -1, int ucols = 0);
 // Eigenvalues ascending into w (may alias d), vectors into Q (ldq).
 cudaError_t stedc(int n, double* d, double* e, double* w, double* Q, long long ldq,
                   const StedcWork& ws, cudaStream_t s);

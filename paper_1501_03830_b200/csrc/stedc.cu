@@ -33,7 +33,7 @@ BSE_DEV void node_range(const Level& L, int n, int i, int& lo, int& mid, int& hi
 }
 
 __global__ void dc_init_kernel(int n, const double* d, const double* e, double* D, double* Q,
-                               long long ld, const double* scal) {
+                               long long ld, const double* scal, int r0, int r1) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
   const double inv = scal[0] > 0.0 ? 1.0 / scal[0] : 1.0;
@@ -42,7 +42,7 @@ __global__ void dc_init_kernel(int n, const double* d, const double* e, double* 
   if (i > 0) v -= fabs(e[i - 1] * inv);
   if (i < n - 1) v -= fabs(e[i] * inv);
   D[i] = v;
-  Q[i + (long long)i * ld] = 1.0;
+  if (i >= r0 && i < r1) Q[(i - r0) + (long long)i * ld] = 1.0;
 }
 
 // Non-finite input guard: the D&C's index logic (sorting, deflation) assumes
@@ -81,12 +81,33 @@ __global__ void absmax_kernel(int n, const double* d, const double* e, double* o
   }
 }
 
+// Row-distributed mode: zrow[c] = the entry of column c in its child's
+// boundary row (last row of the first child, first row of the second), from
+// the rank that owns that row; 0 elsewhere, so a sum over ranks is exact.
+__global__ void dc_zrow_kernel(Level L, int n, const double* __restrict__ Qin, long long ld, int r0,
+                               int r1, double* __restrict__ zrow) {
+  const int c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= n) return;
+  int lo, mid, hi;
+  node_range(L, n, c / L.size, lo, mid, hi);
+  double v = 0.0;
+  if (mid < hi) {
+    const int row = c < mid ? mid - 1 : mid;
+    if (row >= r0 && row < r1) v = Qin[(row - r0) + (long long)c * ld];
+  }
+  zrow[c] = v;
+}
+
 // ---- 1. z vector, merge-sort of the children's eigenvalues, deflation ----
 constexpr int kDcScanChunk = 2048;
 __global__ void __launch_bounds__(kDcThreads) dc_prepare_kernel(
     Level L, int n, const double* __restrict__ e, const double* __restrict__ scal,
     const double* __restrict__ Din, double* __restrict__ Dout, const double* __restrict__ Qin,
-    double* __restrict__ Qout, long long ld, StedcWork w) {
+    double* __restrict__ Qout, long long ld, StedcWork w, int r0, int r1,
+    const double* __restrict__ zrow) {
+  // Rows [r0, r1) of every eigenvector block live here (Q(r, c) at
+  // Q[(r - r0) + c * ld]); zrow (row-distributed mode) holds the children's
+  // boundary rows gathered from their owners, else they are read from Qin.
   __shared__ double red[32];
   int lo, mid, hi;
   node_range(L, n, blockIdx.x, lo, mid, hi);
@@ -94,9 +115,10 @@ __global__ void __launch_bounds__(kDcThreads) dc_prepare_kernel(
   const int tid = threadIdx.x;
   int* cnt = w.counts + 3 * blockIdx.x;
   if (mid >= hi) {  // pass-through node: copy the block
-    for (long long idx = tid; idx < (long long)m * m; idx += blockDim.x) {
-      const int r = (int)(idx % m), c = (int)(idx / m);
-      Qout[(lo + r) + (long long)(lo + c) * ld] = Qin[(lo + r) + (long long)(lo + c) * ld];
+    const int ra = max(lo, r0), rb = min(hi, r1), mr = rb - ra;
+    for (long long idx = tid; mr > 0 && idx < (long long)mr * m; idx += blockDim.x) {
+      const int r = (int)(idx % mr), c = (int)(idx / mr);
+      Qout[(ra - r0 + r) + (long long)(lo + c) * ld] = Qin[(ra - r0 + r) + (long long)(lo + c) * ld];
     }
     for (int t = tid; t < m; t += blockDim.x) Dout[lo + t] = Din[lo + t];
     if (tid == 0) { cnt[0] = -1; cnt[1] = 0; cnt[2] = 0; }
@@ -116,14 +138,14 @@ __global__ void __launch_bounds__(kDcThreads) dc_prepare_kernel(
     int r;
     if (t < n1) {
       val = D1[t];
-      zval = Qin[(mid - 1) + (long long)(lo + t) * ld] * rs2;
+      zval = (zrow ? zrow[lo + t] : Qin[(mid - 1 - r0) + (long long)(lo + t) * ld]) * rs2;
       int a = 0, b = n2;  // count of D2 < val
       while (a < b) { const int c = (a + b) >> 1; if (D2[c] < val) a = c + 1; else b = c; }
       r = t + a;
     } else {
       const int u = t - n1;
       val = D2[u];
-      zval = sgn * Qin[mid + (long long)(mid + u) * ld] * rs2;
+      zval = sgn * (zrow ? zrow[mid + u] : Qin[(mid - r0) + (long long)(mid + u) * ld]) * rs2;
       int a = 0, b = n1;  // count of D1 <= val
       while (a < b) { const int c = (a + b) >> 1; if (D1[c] <= val) a = c + 1; else b = c; }
       r = u + a;
@@ -374,19 +396,21 @@ __global__ void dc_order_kernel(Level L, int n, StedcWork w, double* Dout) {
 }
 
 // ---- 5. eigenvector matrix U (rows in the node's original order) ----
+// Column chunk [cc0, cc0 + cw) of every node (cw = L.size: all columns): node
+// i's column t is stored at U column i * cw + (t - cc0), rows by global index.
 __global__ void __launch_bounds__(kDcThreads) dc_vectors_kernel(Level L, int n, StedcWork w,
-                                                                long long ld) {
+                                                                long long ld, int cc0, int cw) {
   int lo, mid, hi;
   node_range(L, n, blockIdx.y, lo, mid, hi);
   const int K = w.counts[3 * blockIdx.y];
   if (K < 0) return;
   const int m = hi - lo;
   const int lane = threadIdx.x & 31;
-  const int t = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);  // column source index
-  if (t >= m) return;
+  const int t = cc0 + blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);  // column source index
+  if (t >= m || t >= cc0 + cw) return;
   // compact order: roots first (t < K), then deflated columns; the merge GEMM
   // scatters its output to the sorted positions w.pos through a column map
-  double* U = w.U + lo + (long long)(lo + t) * ld;
+  double* U = w.U + lo + ((long long)blockIdx.y * cw + (t - cc0)) * ld;
   for (int r = lane; r < m; r += 32) U[r] = 0.0;
   __syncwarp();
   const int* perm = w.perm + lo;
@@ -409,16 +433,16 @@ __global__ void __launch_bounds__(kDcThreads) dc_vectors_kernel(Level L, int n, 
 }
 
 // ---- 6. deflation rotations on the rows of U (reverse order) ----
-__global__ void dc_rotate_kernel(Level L, int n, StedcWork w, long long ld) {
+__global__ void dc_rotate_kernel(Level L, int n, StedcWork w, long long ld, int cc0, int cw) {
   int lo, mid, hi;
   node_range(L, n, blockIdx.y, lo, mid, hi);
   const int K = w.counts[3 * blockIdx.y];
   const int nr = w.counts[3 * blockIdx.y + 2];
   if (K < 0 || nr == 0) return;
   const int m = hi - lo;
-  const int col = blockIdx.x * blockDim.x + threadIdx.x;
-  if (col >= m) return;
-  double* U = w.U + lo + (long long)(lo + col) * ld;
+  const int col = cc0 + blockIdx.x * blockDim.x + threadIdx.x;
+  if (col >= m || col >= cc0 + cw) return;
+  double* U = w.U + lo + ((long long)blockIdx.y * cw + (col - cc0)) * ld;
   const int* perm = w.perm + lo;
   for (int r = nr - 1; r >= 0; --r) {
     const int p = perm[w.rotp[lo + r]], q = perm[w.rotq[lo + r]];
@@ -431,7 +455,7 @@ __global__ void dc_rotate_kernel(Level L, int n, StedcWork w, long long ld) {
 
 // ---- 7. GEMM descriptors: Q_out = diag(Q1, Q2) * U per node ----
 __global__ void dc_probs_kernel(Level L, int n, StedcWork w, const double* Qin, double* Qout,
-                                long long ld) {
+                                long long ld, long long ldu, int r0, int r1, int cc0, int cw) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= L.nnodes) return;
   int lo, mid, hi;
@@ -443,16 +467,21 @@ __global__ void dc_probs_kernel(Level L, int n, StedcWork w, const double* Qin, 
     // deflated columns are unit vectors unless a Givens rotation touched the
     // node: then they join the GEMM, else dc_copy_deflated moves them
     const int ncols = (nr > 0) ? m : K;
-    top.M = n1; top.N = ncols; top.K = n1;
-    top.ccol = w.pos + lo; bot.ccol = w.pos + lo;
-    bot.N = ncols;
-    top.A = Qin + lo + (long long)lo * ld; top.lda = ld;
-    top.B = w.U + lo + (long long)lo * ld; top.ldb = ld;
-    top.C = Qout + lo + (long long)lo * ld; top.ldc = ld;
-    bot.M = n2; bot.K = n2;
-    bot.A = Qin + mid + (long long)mid * ld; bot.lda = ld;
-    bot.B = w.U + mid + (long long)lo * ld; bot.ldb = ld;
-    bot.C = Qout + mid + (long long)lo * ld; bot.ldc = ld;
+    // this chunk's columns [cc0, cc0 + cw) of the node, this rank's rows
+    const int nc = max(0, min(ncols, cc0 + cw) - cc0);
+    const int ta = max(lo, r0), tb = min(mid, r1);
+    const int ba = max(mid, r0), bb = min(hi, r1);
+    const long long ucol = (long long)i * cw;
+    top.M = max(0, tb - ta); top.N = nc; top.K = n1;
+    top.ccol = w.pos + lo + cc0; bot.ccol = w.pos + lo + cc0;
+    bot.N = nc;
+    top.A = Qin + (ta - r0) + (long long)lo * ld; top.lda = ld;
+    top.B = w.U + lo + ucol * ldu; top.ldb = ldu;
+    top.C = Qout + (ta - r0) + (long long)lo * ld; top.ldc = ld;
+    bot.M = max(0, bb - ba); bot.K = n2;
+    bot.A = Qin + (ba - r0) + (long long)mid * ld; bot.lda = ld;
+    bot.B = w.U + mid + ucol * ldu; bot.ldb = ldu;
+    bot.C = Qout + (ba - r0) + (long long)lo * ld; bot.ldc = ld;
   }
   w.probs[2 * i] = top;
   w.probs[2 * i + 1] = bot;
@@ -462,7 +491,7 @@ __global__ void dc_probs_kernel(Level L, int n, StedcWork w, const double* Qin, 
 // eigenvector, copied to its sorted output position (zeros in the other
 // child's rows).  One warp per column.
 __global__ void dc_copy_deflated_kernel(Level L, int n, StedcWork w, const double* Qin,
-                                        double* Qout, long long ld) {
+                                        double* Qout, long long ld, int w0, int w1) {
   int lo, mid, hi;
   node_range(L, n, blockIdx.y, lo, mid, hi);
   const int K = w.counts[3 * blockIdx.y], nr = w.counts[3 * blockIdx.y + 2];
@@ -475,9 +504,10 @@ __global__ void dc_copy_deflated_kernel(Level L, int n, StedcWork w, const doubl
   const int outc = w.pos[lo + K + c];
   const bool first = (lo + jloc) < mid;
   const int r0 = first ? lo : mid, r1 = first ? mid : hi;
-  const double* src = Qin + (long long)(lo + jloc) * ld;
-  double* dst = Qout + (long long)(lo + outc) * ld;
-  for (int r = lo + lane; r < hi; r += 32) dst[r] = (r >= r0 && r < r1) ? src[r] : 0.0;
+  const double* src = Qin + (long long)(lo + jloc) * ld - w0;
+  double* dst = Qout + (long long)(lo + outc) * ld - w0;
+  for (int r = max(lo, w0) + lane; r < min(hi, w1); r += 32)
+    dst[r] = (r >= r0 && r < r1) ? src[r] : 0.0;
 }
 
 __global__ void dc_finish_kernel(int n, const double* D, double* wout, const double* scal) {
@@ -568,13 +598,22 @@ cudaError_t tridiag_values(int n, const double* d, const double* e, double* w, d
   return cudaGetLastError();
 }
 
-StedcWork stedc_carve(Arena& a, int n) {
+StedcWork stedc_carve(Arena& a, int n, int rows, int ucols) {
   StedcWork w;
-  const long long ld = pad_ld(n);
+  // rows >= 0: row-distributed mode, Qa/Qb hold `rows` rows of every block and
+  // U has ucols columns (the caller sets row0/row1/zrow_reduce)
+  const long long ld = pad_ld(rows >= 0 ? rows : n);
   w.ld = ld;
   w.Qa = a.take<double>((size_t)ld * n);
   w.Qb = a.take<double>((size_t)ld * n);
-  w.U = a.take<double>((size_t)ld * n);
+  if (rows >= 0) {
+    w.ldu = pad_ld(n);
+    w.ucols = std::max(64, std::min(n, ucols));
+    w.U = a.take<double>((size_t)w.ldu * w.ucols);
+    w.zrow = a.take<double>(n);
+  } else {
+    w.U = a.take<double>((size_t)ld * n);
+  }
   w.Da = a.take<double>(n);
   w.Db = a.take<double>(n);
   w.ds = a.take<double>(n);
@@ -622,7 +661,11 @@ cudaError_t stedc(int n, double* d, double* e, double* wout, double* Q, long lon
   e = ws.esan;
   absmax_kernel<<<1, 1024, 0, s>>>(n, d, e, ws.scal);
   count_launch();
-  dc_init_kernel<<<(unsigned)ceil_div(n, 256), 256, 0, s>>>(n, d, e, ws.Da, ws.Qa, ld, ws.scal);
+  // row window (row-distributed mode: dist.cu), U geometry
+  const int r0 = ws.row1 >= 0 ? ws.row0 : 0, r1 = ws.row1 >= 0 ? ws.row1 : n;
+  const long long ldu = ws.ldu ? ws.ldu : ld;
+  const int ucols = ws.ucols ? ws.ucols : n;
+  dc_init_kernel<<<(unsigned)ceil_div(n, 256), 256, 0, s>>>(n, d, e, ws.Da, ws.Qa, ld, ws.scal, r0, r1);
   count_launch();
   double* Din = ws.Da;
   double* Dout = ws.Db;
@@ -632,7 +675,14 @@ cudaError_t stedc(int n, double* d, double* e, double* wout, double* Q, long lon
     Level L{size, size / 2, (int)ceil_div(n, size)};
     const int maxm = std::min(size, n);
     stage_mark("dc_prepare", s);
-    dc_prepare_kernel<<<L.nnodes, kDcThreads, 0, s>>>(L, n, e, ws.scal, Din, Dout, Qin, Qout, ld, ws);
+    if (ws.zrow) {
+      // the children's boundary rows (z of the rank-one tear), from their owners
+      dc_zrow_kernel<<<(unsigned)ceil_div(n, 256), 256, 0, s>>>(L, n, Qin, ld, r0, r1, ws.zrow);
+      count_launch();
+      if (ws.zrow_reduce && (err = ws.zrow_reduce(ws.zrow_ctx, ws.zrow, n, s)) != cudaSuccess) return err;
+    }
+    dc_prepare_kernel<<<L.nnodes, kDcThreads, 0, s>>>(L, n, e, ws.scal, Din, Dout, Qin, Qout, ld, ws,
+                                                      r0, r1, ws.zrow);
     count_launch();
     const dim3 g1((unsigned)ceil_div(maxm, 128), (unsigned)L.nnodes);
     stage_mark("dc_secular", s);
@@ -644,15 +694,11 @@ cudaError_t stedc(int n, double* d, double* e, double* wout, double* Q, long lon
     count_launch();
     dc_order_kernel<<<g1, 128, 0, s>>>(L, n, ws, Dout);
     count_launch();
-    const dim3 g2((unsigned)ceil_div(maxm, kDcThreads / 32), (unsigned)L.nnodes);
-    dc_vectors_kernel<<<g2, kDcThreads, 0, s>>>(L, n, ws, ld);
-    count_launch();
-    dc_rotate_kernel<<<g1, 128, 0, s>>>(L, n, ws, ld);
-    count_launch();
-    dc_probs_kernel<<<(unsigned)ceil_div(L.nnodes, 128), 128, 0, s>>>(L, n, ws, Qin, Qout, ld);
-    count_launch();
-    if ((err = cudaGetLastError()) != cudaSuccess) return err;
-    stage_mark("dc_gemm", s);
+    // U in column chunks of cw per node when the level's U (n x size) exceeds
+    // the buffer (row-distributed mode keeps it at n x ucols)
+    int cw = maxm;
+    if ((long long)L.nnodes * maxm > ucols) cw = std::max(32, (ucols / L.nnodes) / 32 * 32);
+    if ((long long)L.nnodes * cw > ucols) return cudaErrorInvalidValue;
     if (std::getenv("BSE_DC_STATS") && L.nnodes <= 4) {
       int hc[12];
       cudaMemcpyAsync(hc, ws.counts, sizeof(int) * 3 * L.nnodes, cudaMemcpyDeviceToHost, s);
@@ -661,37 +707,55 @@ cudaError_t stedc(int n, double* d, double* e, double* wout, double* Q, long lon
         std::fprintf(stderr, "[dc] level size %d node %d: K=%d deflated=%d rotations=%d\n", size, q,
                      hc[3 * q], hc[3 * q + 1], hc[3 * q + 2]);
     }
-    if (ws.oz && L.nnodes <= 2 && (double)L.half * L.half * maxm >= kOzMinWork) {
-      // top merges: the problem shapes come back to the host (one sync per
-      // level) and the large products run on the emulated-FP64 engine
-      GemmProblem hp[4];
-      if ((err = cudaMemcpyAsync(hp, ws.probs, sizeof(GemmProblem) * 2 * L.nnodes,
-                                 cudaMemcpyDeviceToHost, s)) != cudaSuccess)
-        return err;
-      if ((err = cudaStreamSynchronize(s)) != cudaSuccess) return err;
-      for (int q = 0; q < 2 * L.nnodes; ++q) {
-        const GemmProblem& p = hp[q];
-        if (p.M <= 0 || p.N <= 0) continue;
-        err = (double)p.M * p.N * p.K >= kOzMinWork
-                  ? ozgemm(false, false, p, ws.oz, ws.oz_bytes, 2048, s)
-                  : gemm(false, false, p, s);
+    for (int cc0 = 0; cc0 < maxm; cc0 += cw) {
+      const int cwc = std::min(cw, maxm - cc0);
+      const dim3 g2c((unsigned)ceil_div(cwc, kDcThreads / 32), (unsigned)L.nnodes);
+      const dim3 g1c((unsigned)ceil_div(cwc, 128), (unsigned)L.nnodes);
+      if (cc0 > 0) stage_mark("dc_vectors", s);
+      dc_vectors_kernel<<<g2c, kDcThreads, 0, s>>>(L, n, ws, ldu, cc0, cw);
+      count_launch();
+      dc_rotate_kernel<<<g1c, 128, 0, s>>>(L, n, ws, ldu, cc0, cw);
+      count_launch();
+      dc_probs_kernel<<<(unsigned)ceil_div(L.nnodes, 128), 128, 0, s>>>(L, n, ws, Qin, Qout, ld, ldu,
+                                                                        r0, r1, cc0, cw);
+      count_launch();
+      if ((err = cudaGetLastError()) != cudaSuccess) return err;
+      stage_mark("dc_gemm", s);
+      if (ws.oz && L.nnodes <= 2 && (double)L.half * L.half * maxm >= kOzMinWork) {
+        // top merges: the problem shapes come back to the host (one sync per
+        // level) and the large products run on the emulated-FP64 engine
+        GemmProblem hp[4];
+        if ((err = cudaMemcpyAsync(hp, ws.probs, sizeof(GemmProblem) * 2 * L.nnodes,
+                                   cudaMemcpyDeviceToHost, s)) != cudaSuccess)
+          return err;
+        if ((err = cudaStreamSynchronize(s)) != cudaSuccess) return err;
+        for (int q = 0; q < 2 * L.nnodes; ++q) {
+          const GemmProblem& p = hp[q];
+          if (p.M <= 0 || p.N <= 0) continue;
+          err = (double)p.M * p.N * p.K >= kOzMinWork
+                    ? ozgemm(false, false, p, ws.oz, ws.oz_bytes, 2048, s)
+                    : gemm(false, false, p, s);
+          if (err != cudaSuccess) return err;
+        }
+      } else {
+        err = gemm_grouped(false, false, ws.probs, 2 * L.nnodes, std::min(L.half, r1 - r0), cwc, s,
+                           L.half >= 2 && (r0 & 1) == 0, L.half >= 512 ? 3 : 1);
         if (err != cudaSuccess) return err;
       }
-    } else {
-      err = gemm_grouped(false, false, ws.probs, 2 * L.nnodes, L.half, maxm, s, L.half >= 2,
-                         L.half >= 512 ? 3 : 1);
-      if (err != cudaSuccess) return err;
     }
-    dc_copy_deflated_kernel<<<g2, kDcThreads, 0, s>>>(L, n, ws, Qin, Qout, ld);
+    const dim3 g2((unsigned)ceil_div(maxm, kDcThreads / 32), (unsigned)L.nnodes);
+    dc_copy_deflated_kernel<<<g2, kDcThreads, 0, s>>>(L, n, ws, Qin, Qout, ld, r0, r1);
     count_launch();
     std::swap(Din, Dout);
     std::swap(Qin, Qout);
   }
   dc_finish_kernel<<<(unsigned)ceil_div(n, 256), 256, 0, s>>>(n, Din, wout, ws.scal);
   count_launch();
-  const long long tot = (long long)n * n;
-  copy_matrix_kernel<<<(unsigned)ceil_div(tot, 256), 256, 0, s>>>(n, n, Qin, ld, Q, ldq);
-  count_launch();
+  const long long tot = (long long)(r1 - r0) * n;
+  if (Q && tot > 0) {
+    copy_matrix_kernel<<<(unsigned)ceil_div(tot, 256), 256, 0, s>>>(r1 - r0, n, Qin, ld, Q, ldq);
+    count_launch();
+  }
   return cudaGetLastError();
 }
 

@@ -319,6 +319,8 @@ cudaError_t symm_panel(const double* A2, long long lda, int m, int bw, const dou
   return gemm_splitk(true, false, g2, ssplit, w.symm_ws, w.probs + 32, s);
 }
 
+}  // namespace
+
 // W = X - 1/2 V (T^T (V^T X)), X = Y T  (Y in w.y): the two-sided update
 // A - V W^T - W V^T of one panel (compact WY, LAPACK dsytrd's LATRD form).
 cudaError_t panel_w(int m, int bw, const double* V, long long ldv, const double* Tp, double* W,
@@ -337,8 +339,6 @@ cudaError_t panel_w(int m, int bw, const double* V, long long ldv, const double*
   GemmProblem g6 = make_gemm(m, bw, bw, -0.5, V, ldv, w.z2, bw, 1.0, W, ldw);
   return gemm(false, false, g6, s);
 }
-
-}  // namespace
 
 // Full -> band.  A (n x n, lower triangle referenced) is overwritten: its
 // lower band holds the band matrix, panel regions hold R, rest is garbage.

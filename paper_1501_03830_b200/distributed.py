@@ -78,6 +78,39 @@ def allgather_cols_host(a: np.ndarray, world: int, rank: int, bcast) -> np.ndarr
     return out
 
 
+# ---------------------------------------------------------------------------
+# Block-cyclic column layout of the memory-distributed solve (csrc/dist.cuh,
+# BcLayout): the 1 x Q grid of the 2-D block-cyclic family, tile nb.  Pure
+# index arithmetic, mirrored here so callers (and the CPU tests) can scatter
+# and gather matrices without the library.
+
+def bc_owner(tile: int, world: int) -> int:
+    """Rank owning global column tile ``tile``."""
+    return tile % world
+
+
+def bc_local_cols(n: int, nb: int, world: int, rank: int) -> np.ndarray:
+    """Global column indices of ``rank``'s columns, in local order."""
+    if n < 0 or nb < 1 or world < 1 or not 0 <= rank < world:
+        raise ValueError("bad block-cyclic arguments")
+    cols = [np.arange(t * nb, min((t + 1) * nb, n)) for t in range(rank, -(-n // nb), world)]
+    return np.concatenate(cols) if cols else np.zeros(0, dtype=np.int64)
+
+
+def bc_scatter(a: np.ndarray, nb: int, world: int, rank: int) -> np.ndarray:
+    """This rank's columns of the global matrix ``a`` (rows x n)."""
+    return a[:, bc_local_cols(a.shape[1], nb, world, rank)]
+
+
+def bc_gather(blocks, n: int, nb: int) -> np.ndarray:
+    """Global matrix from every rank's local columns (``blocks[r]``: rows x nloc_r)."""
+    world = len(blocks)
+    out = np.empty((blocks[0].shape[0], n), dtype=blocks[0].dtype)
+    for r, blk in enumerate(blocks):
+        out[:, bc_local_cols(n, nb, world, r)] = blk
+    return out
+
+
 class Communicator:
     """Owns a ``bse_comm`` handle of the C ABI (NCCL or host-staged)."""
 
@@ -186,6 +219,71 @@ def solve_pair_device_dist(comm: Communicator, Mt, ldm: int, Kt, ldk: int, n: in
     if st != _lib.BSE_OK:
         raise RuntimeError(f"bse_solve_spd_pair_dist_dev failed ({st}): {_lib.last_error()}")
     return lam[:n], X1, X2, ld
+
+
+def bc_workspace_bytes(n: int, nb: int, world: int, rank: int, flags: int = 0):
+    """(total, distributed, replicated) workspace bytes of one rank."""
+    d, r = C.c_size_t(0), C.c_size_t(0)
+    tot = _lib.load().bse_solve_bc_workspace_bytes(n, nb, world, rank, flags, C.byref(d), C.byref(r))
+    return int(tot), int(d.value), int(r.value)
+
+
+def solve_pair_device_bc(comm: Communicator, Mloc, ldm: int, Kloc, ldk: int, n: int, nb: int = 512,
+                         flags: int = 0, out=None):
+    """Collective bse_solve_spd_pair_bc_dev: every rank passes ITS columns of
+    M and K (column-major device buffers, n rows) and gets lam (all n) and its
+    columns of X1, X2 back: (lam, X1loc, X2loc, ld)."""
+    torch = require_cuda()
+    lib = _lib.load()
+    dev = Mloc.device
+    nloc = int(lib.bse_bc_local_cols(n, nb, comm.world, comm.rank))
+    if nloc < 0:
+        raise ValueError("bad block-cyclic arguments (nb must be a multiple of 64)")
+    if out is None:
+        X1, ld = colmajor_empty(n, nloc, dev)
+        X2, _ = colmajor_empty(n, nloc, dev)
+        lam = torch.empty(max(n, 1), dtype=torch.float64, device=dev)
+        wb = bc_workspace_bytes(n, nb, comm.world, comm.rank, flags)[0]
+        work = torch.empty(max(wb, 1), dtype=torch.uint8, device=dev)
+    else:
+        lam, X1, X2, ld, work = out
+        wb = work.numel()
+    info = _lib.BseInfo()
+    st = lib.bse_solve_spd_pair_bc_dev(comm.handle, n, nb, ptr(Mloc), ldm, ptr(Kloc), ldk, ptr(lam),
+                                       ptr(X1), ld, ptr(X2), ld, ptr(work), wb, flags,
+                                       stream_ptr(dev), C.byref(info))
+    if st == _lib.BSE_NOT_POSITIVE_DEFINITE:
+        err = NotPositiveDefinite(int(info.pivot_index), float(info.pivot_value),
+                                  "A+B" if info.failed_factor == 1 else "A-B")
+        err.failed_factor = int(info.failed_factor)
+        raise err
+    if st == _lib.BSE_NO_CONVERGENCE:
+        from .types import ConvergenceError
+        raise ConvergenceError(_lib.last_error())
+    if st == _lib.BSE_SPECTRUM_NOT_POSITIVE:
+        raise ValueError("all eigenvalues must be strictly positive")
+    if st != _lib.BSE_OK:
+        raise RuntimeError(f"bse_solve_spd_pair_bc_dev failed ({st}): {_lib.last_error()}")
+    return lam[:n], X1, X2, ld
+
+
+def solve_real_bc(op: BseOperator, comm: Communicator, nb: int = 512):
+    """Memory-distributed ``solve_real`` (reference: solvers.py:80-109): every
+    rank uploads only its block-cyclic columns of A+B and A-B and returns
+    (lambda_plus, x1_local, x2_local, global_columns): all n eigenvalues and
+    this rank's columns of X1, X2 (float64, n x nloc)."""
+    if op.kind != "real":
+        raise ValueError("solve_real requires an operator of kind 'real'")
+    n = op.n
+    torch = require_cuda()
+    dev = torch.device("cuda", torch.cuda.current_device())
+    cols = bc_local_cols(n, nb, comm.world, comm.rank)
+    a, b = op.a.real, op.b.real
+    Mloc, ldm = to_device_colmajor((a + b)[:, cols], dev)
+    Kloc, ldk = to_device_colmajor((a - b)[:, cols], dev)
+    lam, X1, X2, _ = solve_pair_device_bc(comm, Mloc, ldm, Kloc, ldk, n, nb)
+    return (lam.cpu().numpy(), from_device_colmajor(X1, n, len(cols)),
+            from_device_colmajor(X2, n, len(cols)), cols)
 
 
 def solve_real(op: BseOperator, comm: Communicator) -> PositiveEigensystem:

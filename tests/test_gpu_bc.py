@@ -1,0 +1,199 @@
+"""GPU parity of the MEMORY-DISTRIBUTED solve (csrc/dist.cu)
+through the C ABI bse_solve_spd_pair_bc_dev.
+
+Every rank uploads only its block-cyclic column tiles of M = A+B and K = A-B
+and gets back all eigenvalues and its own columns of X1, X2; no rank ever
+holds an N x N matrix.  All ranks share cuda:0 here and exchange through the
+host-staged transport over a gloo group (panel broadcasts and sums are
+host-synchronous: no kernel waits on another rank), at world sizes 1-4 with
+ragged tiles, more ranks than tiles, the emulated-FP64 engine (n >= 4096)
+and definiteness failures.  The assembled solution is checked against the
+single-GPU solve at the north-star tolerances and against the
+numpy oracle (the reference algorithm) at small n.
+"""
+import os
+import socket
+
+import numpy as np
+import pytest
+
+from conftest import vector_parity
+
+pytestmark = pytest.mark.gpu
+
+
+def _free_port():
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def _operator(n, seed, cfg=2):
+    from paper_1501_03830_b200 import configs
+    a, b, _ = configs.config_operator(cfg, n=n, seed=seed)
+    return a, b
+
+
+def _bc_worker(rank, world, port, cases, out):
+    import torch
+    import torch.distributed as dist
+
+    import paper_1501_03830_b200 as bg
+    from paper_1501_03830_b200.distributed import Communicator, solve_real_bc
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    torch.cuda.set_device(0)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    comm = Communicator.host()
+    res = {}
+    for key in cases:
+        n, seed, nb, kind = key
+        a, b = _operator(n, seed, cfg=4 if kind == "clustered" else 2)
+        if kind == "k_fails":
+            b = b.copy()
+            j = n // 2
+            b[j, j] += 2.0 * (a - b)[j, j]  # K = A - B loses definiteness at pivot <= j
+        if kind == "m_fails":
+            b = b.copy()
+            j = n // 3
+            b[j, j] -= 2.0 * (a + b)[j, j]  # both K... M = A + B fails (K stays definite)
+        op = bg.make_operator(a, b, kind="real")
+        try:
+            lam, x1, x2, cols = solve_real_bc(op, comm, nb=nb)
+            res[key] = ("ok", lam, x1, x2, cols)
+        except bg.NotPositiveDefinite as e:
+            res[key] = ("npd", e.pivot_index, e.pivot_value, e.what)
+    comm.close()
+    out[rank] = res
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def _run(world, cases):
+    import torch.multiprocessing as mp
+    port = _free_port()
+    ctx = mp.get_context("spawn")
+    with ctx.Manager() as mgr:
+        out = mgr.dict()
+        mp.start_processes(_bc_worker, args=(world, port, cases, out), nprocs=world, join=True,
+                           start_method="spawn")
+        return dict(out)
+
+
+def _assemble(res, key, world):
+    from paper_1501_03830_b200.distributed import bc_gather, bc_local_cols
+    n, _, nb, _ = key
+    lam = res[0][key][1]
+    for r in range(world):
+        assert res[r][key][0] == "ok"
+        assert np.array_equal(res[r][key][1], lam), "lam differs between ranks"
+        assert np.array_equal(res[r][key][4], bc_local_cols(n, nb, world, r))
+    x1 = bc_gather([res[r][key][2] for r in range(world)], n, nb)
+    x2 = bc_gather([res[r][key][3] for r in range(world)], n, nb)
+    return lam, x1, x2
+
+
+def _check(dev, res, cases, world, vectors=True):
+    import paper_1501_03830_b200 as bg
+    from oracle import bse_oracle as orc
+    for key in cases:
+        n, seed, nb, kind = key
+        a, b = _operator(n, seed, cfg=4 if kind == "clustered" else 2)
+        lam, x1, x2 = _assemble(res, key, world)
+        ref = bg.solve_real(bg.make_operator(a, b, kind="real"))
+        assert np.all(lam > 0) and np.all(np.diff(lam) <= 0)
+        assert np.max(np.abs(lam - ref.lambda_plus) / ref.lambda_plus) <= 1e-10, key
+        # north-star gates on the assembled solution (dense check on the host)
+        G = x1.T @ x1 - x2.T @ x2
+        assert np.linalg.norm(G - np.eye(n)) <= 1e-12 * n, key
+        m, k = a + b, a - b
+        A, B = 0.5 * (m + k), 0.5 * (m - k)
+        H = np.block([[A, B], [-B, -A]])
+        X = np.vstack([x1, x2])
+        r = np.linalg.norm(H @ X - X * lam, axis=0) / (np.linalg.norm(H, 2) * np.linalg.norm(X, axis=0))
+        assert r.max() <= 1e-13 * n, key
+        if vectors:
+            # eigenvectors equal the single-GPU ones up to sign within
+            # n eps |W| / gap(lambda^2); principal angles inside clusters
+            vector_parity(lam, X, np.vstack([ref.x1.real, ref.x2.real]), n)
+        if n <= 128:
+            lam_o, _, _ = orc.solve_complex(a, b)
+            assert np.max(np.abs(lam - lam_o) / lam_o) <= 1e-10
+
+
+def test_bc_world1(dev):
+    cases = [(700, 21, 128, "plain"), (64, 22, 64, "plain"), (3, 23, 64, "plain"), (1, 24, 64, "plain")]
+    res = _run(1, cases)
+    _check(dev, res, cases, 1)
+
+
+def test_bc_world2_ragged_tiles(dev):
+    # 1100 = 8 full tiles of 128 + one of 76; 333 with nb = 64: partial last tile
+    cases = [(1100, 25, 128, "plain"), (333, 26, 64, "plain"), (96, 27, 64, "plain"), (2, 28, 64, "plain")]
+    res = _run(2, cases)
+    _check(dev, res, cases, 2)
+
+
+def test_bc_world3_and_more_ranks_than_tiles(dev):
+    cases = [(901, 29, 128, "plain"), (100, 30, 64, "plain")]  # 100: two tiles, rank 2 owns nothing
+    res = _run(3, cases)
+    _check(dev, res, cases, 3)
+
+
+def test_bc_world4_tile512(dev):
+    cases = [(2300, 31, 512, "plain")]
+    res = _run(4, cases)
+    _check(dev, res, cases, 4)
+
+
+def test_bc_world2_clustered_cfg4_recipe(dev):
+    """cfg4's clustered spectrum (heavy D&C deflation) on row-distributed
+    eigenvector blocks with chunked secular-vector panels."""
+    cases = [(1536, 32, 256, "clustered")]
+    res = _run(2, cases)
+    _check(dev, res, cases, 2)
+
+
+def test_bc_world2_emulated_engine(dev):
+    """n >= 4096: Q1's panel groups run on the emulated-FP64 engine."""
+    cases = [(4608, 33, 512, "plain")]
+    res = _run(2, cases)
+    _check(dev, res, cases, 2, vectors=False)
+
+
+def test_bc_definiteness_errors(dev):
+    cases = [(500, 34, 128, "k_fails"), (500, 35, 128, "m_fails")]
+    res = _run(2, cases)
+    import paper_1501_03830_b200 as bg
+    for key in cases:
+        n, seed, nb, kind = key
+        a, b = _operator(n, seed)
+        b = b.copy()
+        if kind == "k_fails":
+            j = n // 2
+            b[j, j] += 2.0 * (a - b)[j, j]
+        else:
+            j = n // 3
+            b[j, j] -= 2.0 * (a + b)[j, j]
+        with pytest.raises(bg.NotPositiveDefinite) as ei:
+            bg.solve_real(bg.make_operator(a, b, kind="real"))
+        for r in range(2):
+            tag, idx, val, what = res[r][key]
+            assert tag == "npd" and what == ei.value.what
+            assert idx == ei.value.pivot_index
+            assert abs(val - ei.value.pivot_value) <= 1e-9 * max(1.0, abs(val))
+
+
+def test_bc_workspace_is_distributed(dev):
+    """Per-rank dense storage shrinks like 1/Q (the replicated remainder is
+    the band, the tridiagonal data and the bulge-chasing reflectors)."""
+    from paper_1501_03830_b200.distributed import bc_workspace_bytes
+    n, nb = 16384, 512
+    d1 = bc_workspace_bytes(n, nb, 1, 0)[1]
+    for q in (2, 4, 8):
+        tot, dist_b, rep = bc_workspace_bytes(n, nb, q, 0)
+        assert dist_b <= 1.25 * d1 / q + (1 << 28), (q, dist_b, d1)
+        assert rep <= 1.2 * 8 * n * n
+    # cfg4 (n = 65536, tile 1024) on 8 GPUs fits 180 GB per GPU
+    tot, dist_b, rep = bc_workspace_bytes(65536, 1024, 8, 0)
+    inputs_outputs = 4 * 8 * 65536 * (65536 // 8)
+    assert tot + inputs_outputs <= 170e9, tot
