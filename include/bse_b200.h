@@ -165,6 +165,12 @@ int bse_gemm_dev(int transA, int transB, int64_t M, int64_t N, int64_t K, double
 int bse_ozgemm_dev(int transA, int transB, int64_t M, int64_t N, int64_t K, double alpha,
                    const double* dA, int64_t lda, const double* dB, int64_t ldb, double beta,
                    double* dC, int64_t ldc, const int32_t* masks, int64_t chunk, void* stream);
+/* Contraction kernel of the emulated engine: 0 = hand-written tcgen05 kind::i8
+ * kernel on CTA pairs with the residue-reducing epilogue (csrc/i8mma.cu, the
+ * default), 1 = the same on single CTAs, 2 = CUTLASS kernel with INT32 residue
+ * planes (kept for A/B measurements).  Returns the previous setting; out of
+ * range values only query. */
+int bse_oz_set_engine(int engine);
 /* kind: 0 = A L^{-T} (right), 1 = L^{-T} B (left, trans), 2 = L^{-1} B (left) */
 int bse_trsm_dev(int kind, int64_t n, const double* dL, int64_t ldl, double* dB, int64_t ldb,
                  int64_t m, void* stream);

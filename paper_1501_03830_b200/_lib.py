@@ -62,6 +62,7 @@ SIGNATURES = {
                             _P, _P]),
     "bse_ozgemm_dev": (_INT, [_INT, _INT, _I64, _I64, _I64, _D, _P, _I64, _P, _I64, _D, _P, _I64,
                               _P, _I64, _P]),
+    "bse_oz_set_engine": (_INT, [_INT]),
     "bse_trsm_dev": (_INT, [_INT, _I64, _P, _I64, _P, _I64, _I64, _P]),
     "bse_profile_enable": (_INT, [_INT]),
     "bse_profile_read": (_INT, [_INT, C.POINTER(_D), C.c_char_p]),

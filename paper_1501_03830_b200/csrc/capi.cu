@@ -83,6 +83,8 @@ int bse_ozgemm_dev(int transA, int transB, int64_t M, int64_t N, int64_t K, doub
   return BSE_OK;
 }
 
+int bse_oz_set_engine(int engine) { return bse::oz_set_engine(engine); }
+
 int bse_trsm_dev(int kind, int64_t n, const double* dL, int64_t ldl, double* dB, int64_t ldb,
                  int64_t m, void* stream) {
   cudaStream_t s = (cudaStream_t)stream;

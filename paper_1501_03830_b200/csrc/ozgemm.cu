@@ -19,9 +19,11 @@
 // (orthogonal / triangular factors with bounded row ranges); tests compare it
 // against the DMMA engine and float64 numpy.
 #include <algorithm>
+#include <atomic>
 #include <cmath>
 #include <cstdint>
 #include <cstdio>
+#include <cstdlib>
 #include "cutlass/cutlass.h"
 #include "cute/tensor.hpp"
 #include "cutlass/epilogue/collective/collective_builder.hpp"
@@ -30,6 +32,7 @@
 #include "cutlass/gemm/dispatch_policy.hpp"
 #include "cutlass/gemm/kernel/gemm_universal.hpp"
 #include "cutlass/util/packed_stride.hpp"
+#include "i8mma.cuh"
 #include "ozgemm.cuh"
 
 namespace bse {
@@ -319,6 +322,72 @@ __global__ void __launch_bounds__(256) crt_kernel(int M, int N, int Mp, const in
   }
 }
 
+// The same reconstruction from the byte planes written by the hand-written
+// tcgen05 kernel (i8mma.cu): v_t = R[t][j][i] in [0, m_t) already reduced, one
+// 32-bit word per plane holds rows i0..i0+3 of column j.
+__global__ void __launch_bounds__(256) crt8_kernel(int M, int N, const uint8_t* __restrict__ r8,
+                                                   long long ldr, long long plane,
+                                                   const int* __restrict__ sa,
+                                                   const int* __restrict__ sb, double alpha,
+                                                   double beta, double* __restrict__ C,
+                                                   long long ldc, int col0, Mask mc,
+                                                   const int* __restrict__ ccol) {
+  const int M4 = (M + 3) >> 2;
+  const long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (idx >= (long long)M4 * N) return;
+  const int i0 = (int)(idx % M4) * 4, j = (int)(idx / M4);
+  const int dj = col0 + j;
+  if (dj - (i0 + 3) > mc.hi || dj - i0 < mc.lo) return;
+  const uint8_t* p = r8 + (long long)j * ldr + i0;
+  double a[4][4];
+#pragma unroll
+  for (int e = 0; e < 4; ++e) a[e][0] = a[e][1] = a[e][2] = a[e][3] = 0.0;
+#pragma unroll
+  for (int t = 0; t < kMods; ++t) {
+    const uint32_t w = __ldcs(reinterpret_cast<const uint32_t*>(p + t * plane));
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      const uint32_t v = (w >> (8 * e)) & 0xFFu;
+      const double dv = __hiloint2double(0x43300000, (int)v) - 4503599627370496.0;  // 2^52
+      a[e][0] = fma(dv, c_crt.q[t][0], a[e][0]);
+      a[e][1] = fma(dv, c_crt.q[t][1], a[e][1]);
+      a[e][2] = fma(dv, c_crt.q[t][2], a[e][2]);
+      a[e][3] = fma(dv, c_crt.q[t][3], a[e][3]);
+    }
+  }
+  constexpr double k32 = 4294967296.0, k64 = k32 * k32, k96 = k64 * k32;
+  double* cd = C + (long long)(ccol ? ccol[dj] : dj) * ldc;
+  const int sj = sb[j];
+#pragma unroll
+  for (int e = 0; e < 4; ++e) {
+    const int i = i0 + e;
+    const int d = dj - i;
+    if (i >= M || d < mc.lo || d > mc.hi) continue;
+    const double q = rint(fma(a[e][3], k96, fma(a[e][2], k64, a[e][1] * k32)) * c_crt.inv_p);
+    const double r0 = fma(-q, c_crt.p[0], a[e][0]), r1 = fma(-q, c_crt.p[1], a[e][1]);
+    const double r2 = fma(-q, c_crt.p[2], a[e][2]), r3 = fma(-q, c_crt.p[3], a[e][3]);
+    const double cp = ((r3 * k96 + r2 * k64) + r1 * k32) + r0;
+    double v = alpha * scale2(cp, -(sa[i] + sj));
+    if (beta != 0.0) v += beta * cd[i];
+    cd[i] = v;
+  }
+}
+
+// Contraction engine: 0 = hand-written tcgen05 kernel on CTA pairs (default),
+// 1 = the same on single CTAs, 2 = the CUTLASS kernel with INT32 planes (kept
+// for A/B measurements: BSE_OZ_ENGINE).
+std::atomic<int> g_oz_engine{-1};
+int oz_engine() {
+  int v = g_oz_engine.load(std::memory_order_relaxed);
+  if (v < 0) {
+    const char* e = std::getenv("BSE_OZ_ENGINE");
+    v = e ? std::atoi(e) : 0;
+    if (v < 0 || v > 2) v = 0;
+    g_oz_engine.store(v, std::memory_order_relaxed);
+  }
+  return v;
+}
+
 long long r16(long long x) { return (x + 15) / 16 * 16; }
 
 bool g_const_ready[64] = {};
@@ -351,6 +420,12 @@ cudaError_t init_const() {
 }
 
 }  // namespace
+
+int oz_set_engine(int engine) {
+  const int prev = oz_engine();
+  if (engine >= 0 && engine <= 2) g_oz_engine.store(engine, std::memory_order_relaxed);
+  return prev;
+}
 
 size_t ozgemm_bytes(int M, int N, int K, int chunk) {
   const long long Mp = r16(M), Kp = r16(K), Np = r16(std::min(N, chunk));
@@ -428,12 +503,24 @@ cudaError_t ozgemm(bool transA, bool transB, const GemmProblem& p, void* work, s
       if (mb.hi != kNoMaskHi) mb.hi += j0;
     }
     if ((e = split(!transB, nc, bsrc, p.ldb, mb, b8, ncp, sb, mxb)) != cudaSuccess) return e;
-    if ((e = i8_gemm_batched((int)Mp, (int)ncp, (int)Kp, kMods, a8, b8, c32, s)) != cudaSuccess)
-      return e;
     const long long tot = (long long)((M + 3) / 4) * nc;
-    crt_kernel<<<(unsigned)ceil_div(tot, 256), 256, 0, s>>>(M, nc, (int)Mp, c32, Mp * ncp, sa, sb,
-                                                           p.alpha, p.beta, p.C, p.ldc, j0, p.mc,
-                                                           p.ccol);
+    if (oz_engine() == 2) {
+      if ((e = i8_gemm_batched((int)Mp, (int)ncp, (int)Kp, kMods, a8, b8, c32, s)) != cudaSuccess)
+        return e;
+      crt_kernel<<<(unsigned)ceil_div(tot, 256), 256, 0, s>>>(M, nc, (int)Mp, c32, Mp * ncp, sa, sb,
+                                                             p.alpha, p.beta, p.C, p.ldc, j0, p.mc,
+                                                             p.ccol);
+    } else {
+      // byte planes R[t][j][i] in the c32 region (a quarter of it)
+      uint8_t* r8 = reinterpret_cast<uint8_t*>(c32);
+      const long long ldr = (M + 31) / 32 * 32;
+      if ((e = i8mma_residues(M, nc, (int)Kp, a8, Mp, b8, ncp, r8, ldr, j0, p.mc.lo, p.mc.hi,
+                              oz_engine() == 0, s)) != cudaSuccess)
+        return e;
+      crt8_kernel<<<(unsigned)ceil_div(tot, 256), 256, 0, s>>>(M, nc, r8, ldr, ncp * ldr, sa, sb,
+                                                              p.alpha, p.beta, p.C, p.ldc, j0, p.mc,
+                                                              p.ccol);
+    }
     count_launch();
     if ((e = cudaGetLastError()) != cudaSuccess) return e;
   }

@@ -15,6 +15,11 @@ size_t ozgemm_bytes(int M, int N, int K, int chunk);
 cudaError_t ozgemm(bool transA, bool transB, const GemmProblem& p, void* work, size_t work_bytes,
                    int chunk, cudaStream_t s, bool reuse_a = false);
 
+// Contraction kernel behind the engine: 0 = hand-written tcgen05 kernel on CTA
+// pairs (default), 1 = the same on single CTAs, 2 = CUTLASS kernel + INT32
+// planes (A/B measurements).  Returns the previous setting.
+int oz_set_engine(int engine);
+
 // Products at least this large (M N K) go to the emulated engine.
 constexpr double kOzMinWork = 1024.0 * 1024.0 * 1024.0 * 64.0;
 

@@ -397,9 +397,11 @@ __global__ void dc_order_kernel(Level L, int n, StedcWork w, double* Dout) {
 
 // ---- 5. eigenvector matrix U (rows in the node's original order) ----
 // Column chunk [cc0, cc0 + cw) of every node (cw = L.size: all columns): node
-// i's column t is stored at U column i * cw + (t - cc0), rows by global index.
+// i's column t is stored at U column (i % slots) * cw + (t - cc0), rows by
+// global index: nodes sharing a column slot own disjoint rows of U.
 __global__ void __launch_bounds__(kDcThreads) dc_vectors_kernel(Level L, int n, StedcWork w,
-                                                                long long ld, int cc0, int cw) {
+                                                                long long ld, int cc0, int cw,
+                                                                int slots) {
   int lo, mid, hi;
   node_range(L, n, blockIdx.y, lo, mid, hi);
   const int K = w.counts[3 * blockIdx.y];
@@ -410,7 +412,7 @@ __global__ void __launch_bounds__(kDcThreads) dc_vectors_kernel(Level L, int n, 
   if (t >= m || t >= cc0 + cw) return;
   // compact order: roots first (t < K), then deflated columns; the merge GEMM
   // scatters its output to the sorted positions w.pos through a column map
-  double* U = w.U + lo + ((long long)blockIdx.y * cw + (t - cc0)) * ld;
+  double* U = w.U + lo + ((long long)(blockIdx.y % slots) * cw + (t - cc0)) * ld;
   for (int r = lane; r < m; r += 32) U[r] = 0.0;
   __syncwarp();
   const int* perm = w.perm + lo;
@@ -433,7 +435,8 @@ __global__ void __launch_bounds__(kDcThreads) dc_vectors_kernel(Level L, int n, 
 }
 
 // ---- 6. deflation rotations on the rows of U (reverse order) ----
-__global__ void dc_rotate_kernel(Level L, int n, StedcWork w, long long ld, int cc0, int cw) {
+__global__ void dc_rotate_kernel(Level L, int n, StedcWork w, long long ld, int cc0, int cw,
+                                 int slots) {
   int lo, mid, hi;
   node_range(L, n, blockIdx.y, lo, mid, hi);
   const int K = w.counts[3 * blockIdx.y];
@@ -442,7 +445,7 @@ __global__ void dc_rotate_kernel(Level L, int n, StedcWork w, long long ld, int 
   const int m = hi - lo;
   const int col = cc0 + blockIdx.x * blockDim.x + threadIdx.x;
   if (col >= m || col >= cc0 + cw) return;
-  double* U = w.U + lo + ((long long)blockIdx.y * cw + (col - cc0)) * ld;
+  double* U = w.U + lo + ((long long)(blockIdx.y % slots) * cw + (col - cc0)) * ld;
   const int* perm = w.perm + lo;
   for (int r = nr - 1; r >= 0; --r) {
     const int p = perm[w.rotp[lo + r]], q = perm[w.rotq[lo + r]];
@@ -455,7 +458,8 @@ __global__ void dc_rotate_kernel(Level L, int n, StedcWork w, long long ld, int 
 
 // ---- 7. GEMM descriptors: Q_out = diag(Q1, Q2) * U per node ----
 __global__ void dc_probs_kernel(Level L, int n, StedcWork w, const double* Qin, double* Qout,
-                                long long ld, long long ldu, int r0, int r1, int cc0, int cw) {
+                                long long ld, long long ldu, int r0, int r1, int cc0, int cw,
+                                int slots) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= L.nnodes) return;
   int lo, mid, hi;
@@ -471,7 +475,7 @@ __global__ void dc_probs_kernel(Level L, int n, StedcWork w, const double* Qin, 
     const int nc = max(0, min(ncols, cc0 + cw) - cc0);
     const int ta = max(lo, r0), tb = min(mid, r1);
     const int ba = max(mid, r0), bb = min(hi, r1);
-    const long long ucol = (long long)i * cw;
+    const long long ucol = (long long)(i % slots) * cw;
     top.M = max(0, tb - ta); top.N = nc; top.K = n1;
     top.ccol = w.pos + lo + cc0; bot.ccol = w.pos + lo + cc0;
     bot.N = nc;
@@ -694,11 +698,14 @@ cudaError_t stedc(int n, double* d, double* e, double* wout, double* Q, long lon
     count_launch();
     dc_order_kernel<<<g1, 128, 0, s>>>(L, n, ws, Dout);
     count_launch();
-    // U in column chunks of cw per node when the level's U (n x size) exceeds
-    // the buffer (row-distributed mode keeps it at n x ucols)
-    int cw = maxm;
-    if ((long long)L.nnodes * maxm > ucols) cw = std::max(32, (ucols / L.nnodes) / 32 * 32);
-    if ((long long)L.nnodes * cw > ucols) return cudaErrorInvalidValue;
+    // U (block diagonal: node i owns rows [lo, hi)) lives in a ldu x ucols
+    // buffer of column slots cw wide; node i uses slot i % slots -- nodes
+    // sharing a slot own disjoint rows.  A level whose nodes are wider than
+    // the buffer (row-distributed mode keeps it at n x ucols) is processed in
+    // column chunks of cw.
+    const int cw = maxm <= ucols ? maxm : std::max(32, ucols / 32 * 32);
+    if (cw > ucols) return cudaErrorInvalidValue;
+    const int slots = std::max(1, ucols / cw);
     if (std::getenv("BSE_DC_STATS") && L.nnodes <= 4) {
       int hc[12];
       cudaMemcpyAsync(hc, ws.counts, sizeof(int) * 3 * L.nnodes, cudaMemcpyDeviceToHost, s);
@@ -712,12 +719,12 @@ cudaError_t stedc(int n, double* d, double* e, double* wout, double* Q, long lon
       const dim3 g2c((unsigned)ceil_div(cwc, kDcThreads / 32), (unsigned)L.nnodes);
       const dim3 g1c((unsigned)ceil_div(cwc, 128), (unsigned)L.nnodes);
       if (cc0 > 0) stage_mark("dc_vectors", s);
-      dc_vectors_kernel<<<g2c, kDcThreads, 0, s>>>(L, n, ws, ldu, cc0, cw);
+      dc_vectors_kernel<<<g2c, kDcThreads, 0, s>>>(L, n, ws, ldu, cc0, cw, slots);
       count_launch();
-      dc_rotate_kernel<<<g1c, 128, 0, s>>>(L, n, ws, ldu, cc0, cw);
+      dc_rotate_kernel<<<g1c, 128, 0, s>>>(L, n, ws, ldu, cc0, cw, slots);
       count_launch();
       dc_probs_kernel<<<(unsigned)ceil_div(L.nnodes, 128), 128, 0, s>>>(L, n, ws, Qin, Qout, ld, ldu,
-                                                                        r0, r1, cc0, cw);
+                                                                        r0, r1, cc0, cw, slots);
       count_launch();
       if ((err = cudaGetLastError()) != cudaSuccess) return err;
       stage_mark("dc_gemm", s);

@@ -100,3 +100,50 @@ def test_ozgemm_orthogonal_product_keeps_orthogonality(dev):
     q, _ = np.linalg.qr(rng.standard_normal((n, n)))
     got = _oz(dev, 1, 0, q, q, np.zeros((n, n)), 1.0, 0.0, chunk=512)
     assert np.max(np.abs(got - np.eye(n))) <= 5e-15 * np.sqrt(n)
+
+
+@pytest.mark.parametrize("engine", [0, 1])
+@pytest.mark.parametrize("M,N,K,chunk", [(1, 1, 1, 0), (33, 70, 17, 0), (300, 129, 1000, 0),
+                                         (513, 700, 256, 256), (1024, 1500, 4100, 512),
+                                         (2304, 2050, 640, 0)])
+def test_tcgen05_kernel_bitwise_vs_library_kernel(dev, engine, M, N, K, chunk):
+    """The 16 integer products are exact on either kernel, so the hand-written
+    tcgen05 contraction (byte residues from its epilogue, csrc/i8mma.cu; CTA
+    pairs = 0, single CTAs = 1) must reproduce the CUTLASS kernel + INT32
+    planes (engine 2) bit for bit, including ragged tiles, K tails and column
+    chunks."""
+    lib = _lib.load()
+    rng = np.random.default_rng(M + 3 * N + 7 * K)
+    a = rng.standard_normal((M, K)) * np.exp(rng.uniform(-8, 8, (M, 1)))
+    b = rng.standard_normal((K, N))
+    c = rng.standard_normal((M, N))
+    prev = lib.bse_oz_set_engine(2)
+    try:
+        ref = _oz(dev, 0, 0, a, b, c, 1.0, 0.25, chunk=chunk)
+        lib.bse_oz_set_engine(engine)
+        got = _oz(dev, 0, 0, a, b, c, 1.0, 0.25, chunk=chunk)
+    finally:
+        lib.bse_oz_set_engine(prev)
+    assert np.array_equal(got, ref)
+
+
+@pytest.mark.parametrize("engine", [0, 1])
+def test_tcgen05_kernel_output_band(dev, engine):
+    """Tiles entirely outside the output band are skipped by the kernel (the
+    symmetric rank-k updates of the reduction only need the lower triangle)."""
+    lib = _lib.load()
+    M = N = 900
+    K = 300
+    rng = np.random.default_rng(11)
+    a = rng.standard_normal((M, K))
+    b = rng.standard_normal((K, N))
+    c = rng.standard_normal((M, N))
+    masks = mask_array(None, None, (None, 0, 0))
+    prev = lib.bse_oz_set_engine(engine)
+    try:
+        got = _oz(dev, 0, 0, a, b, c, -1.0, 1.0, masks=masks)
+    finally:
+        lib.bse_oz_set_engine(prev)
+    ref = np.where(np.tril(np.ones((M, N), bool)), c - a @ b, c)
+    assert np.max(np.abs(got - ref)) <= 1e-12
+    assert np.array_equal(np.triu(got, 1), np.triu(c, 1))

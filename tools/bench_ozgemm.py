@@ -23,6 +23,8 @@ ap.add_argument("--ta", type=int, default=0)
 ap.add_argument("--tb", type=int, default=0)
 ap.add_argument("--chunk", type=int, default=4096)
 ap.add_argument("--reps", type=int, default=3)
+ap.add_argument("--engines", default="2,1,0", help="emulated-engine kernels to time (bse_oz_set_engine)")
+ap.add_argument("--no-dmma", action="store_true")
 a = ap.parse_args()
 m, n, k = a.m, a.n, a.k
 lib = _lib.load()
@@ -46,7 +48,7 @@ def oz():
                               None, a.chunk, stream_ptr()) == 0, _lib.last_error()
 
 
-for name, fn in (("dmma", dmma), ("ozaki-int8", oz)):
+def timed(name, fn):
     fn()
     torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -56,7 +58,20 @@ for name, fn in (("dmma", dmma), ("ozaki-int8", oz)):
     e1.record()
     torch.cuda.synchronize()
     ms = e0.elapsed_time(e1) / a.reps
-    print(f"{name:11s} m={m} n={n} k={k} ta={a.ta} tb={a.tb}: {ms:8.3f} ms, "
+    print(f"{name:18s} m={m} n={n} k={k} ta={a.ta} tb={a.tb}: {ms:8.3f} ms, "
           f"{2 * m * n * k / ms / 1e9:7.2f} TFLOP/s (FP64-equivalent)", flush=True)
-d = (C0 - C1).abs().max().item()
-print(f"max |dmma - ozaki| = {d:.3e}  (max |C| = {C0.abs().max().item():.3e})")
+
+
+if not a.no_dmma:
+    timed("dmma", dmma)
+ref = None
+for eng in [int(x) for x in a.engines.split(",")]:
+    lib.bse_oz_set_engine(eng)
+    timed(f"ozaki engine {eng}", oz)
+    if ref is None:
+        ref = C1.clone()
+    else:
+        print(f"  bitwise equal to the first engine: {bool(torch.equal(ref, C1))}")
+if not a.no_dmma:
+    d = (C0 - C1).abs().max().item()
+    print(f"max |dmma - ozaki| = {d:.3e}  (max |C| = {C0.abs().max().item():.3e})")
