@@ -715,6 +715,221 @@ def run_ours(args):
     return 0
 
 
+def run_ours_bc(args):
+    """N > 1: the memory-distributed solve (csrc/dist.cu).
+    Every rank holds only its block-cyclic column tiles of M and K, all n
+    eigenvalues and its own columns of X1, X2; panels are broadcast and the
+    panel products summed over NCCL (NVLink / NVSwitch).  --transport host
+    runs the same code over the host-staged transport (ranks may share one
+    GPU: the only way to exercise N > 1 on a one-GPU box)."""
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    from paper_1501_03830_b200 import _lib, configs
+    from paper_1501_03830_b200.device import ptr
+    from paper_1501_03830_b200.distributed import (Communicator, bc_local_cols,
+                                                   bc_workspace_bytes)
+
+    rank, local_rank, world = env_rank()
+    ndev = torch.cuda.device_count()
+    transport = args.transport or ("nccl" if ndev >= world else "host")
+    dev_index = local_rank % max(ndev, 1)
+    torch.cuda.set_device(dev_index)
+    dev = torch.device("cuda", dev_index)
+    if transport == "nccl":
+        dist.init_process_group("nccl", device_id=dev)
+        comm = Communicator.nccl()
+    else:
+        dist.init_process_group("gloo")
+        comm = Communicator.host()
+    rdev = dev if transport == "nccl" else None  # where timing reductions live
+    lib = _lib.load(strict=True)
+    n, nb = args.n, args.nb
+    stream = torch.cuda.current_stream(dev)
+    sp = stream.cuda_stream
+    cols = bc_local_cols(n, nb, world, rank)
+    nloc = len(cols)
+    ld = n + (n & 1)
+
+    def local_tiles():
+        # the seeded cfg2 operator is generated in full (identical on every
+        # rank) and only this rank's column tiles are kept (S, D symmetric:
+        # row c of the row-major tensor is column cols[c])
+        S, D, _ = configs.torch_real_operator(n, seed=SEED, spectrum="loguniform", lo=0.1,
+                                              hi=100.0, device=dev)
+        idx = torch.as_tensor(cols, device=dev, dtype=torch.long)
+        Ml = torch.zeros((max(nloc, 1), ld), dtype=torch.float64, device=dev)
+        Kl = torch.zeros((max(nloc, 1), ld), dtype=torch.float64, device=dev)
+        if nloc:
+            Ml[:nloc, :n].copy_(S[idx])
+            Kl[:nloc, :n].copy_(D[idx])
+        return S, D, Ml, Kl
+
+    S, D, Mloc, Kloc = local_tiles()
+    del S, D
+    torch.cuda.empty_cache()
+    X1 = torch.empty((max(nloc, 1), ld), dtype=torch.float64, device=dev)
+    X2 = torch.empty((max(nloc, 1), ld), dtype=torch.float64, device=dev)
+    lam = torch.empty(n, dtype=torch.float64, device=dev)
+    wb, wb_dist, wb_rep = bc_workspace_bytes(n, nb, world, rank, 0)
+    work = torch.empty(wb, dtype=torch.uint8, device=dev)
+    info = _lib.BseInfo()
+
+    def step():
+        st = lib.bse_solve_spd_pair_bc_dev(comm.handle, n, nb, ptr(Mloc), ld, ptr(Kloc), ld,
+                                           ptr(lam), ptr(X1), ld, ptr(X2), ld, ptr(work), wb, 0,
+                                           sp, C.byref(info))
+        if st != 0:
+            raise RuntimeError(f"distributed solve failed ({st}): {_lib.last_error()}")
+
+    fl, ms = C.c_double(), C.c_double()
+    lib.bse_peak_fp64(0, 296, 20000, 5, C.byref(fl), C.byref(ms))
+    fp64_peak = fl.value / (ms.value * 1e-3) / 1e12
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize(dev)
+    clocks = ClockSampler(dev_index)
+    time.sleep(0.3)
+    launches0 = lib.bse_launch_count()
+    dist.barrier()
+    torch.cuda.synchronize(dev)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for i in range(args.steps):
+        if i == args.steps - 1:
+            lib.bse_profile_enable(1)
+        step()
+    e1.record(stream)
+    torch.cuda.synchronize(dev)
+    dist.barrier()
+    launches = lib.bse_launch_count() - launches0
+    clk = clocks.stop()
+    ms_step = max_over_ranks(e0.elapsed_time(e1) / args.steps, dist, rdev)
+    cnt = lib.bse_profile_count()
+    msarr = (C.c_double * max(cnt, 1))()
+    names = C.create_string_buffer(32 * max(cnt, 1))
+    got = lib.bse_profile_read(cnt, msarr, names)
+    lib.bse_profile_enable(0)
+    stages = {}
+    for i in range(got):
+        nm = names.raw[32 * i:32 * (i + 1)].split(b"\0")[0].decode()
+        if nm != "end":
+            stages[nm] = stages.get(nm, 0.0) + msarr[i]
+
+    # verification of the last timed solve on this rank's columns (outside the
+    # timed region; own FP64 GEMM kernels): with u = x1 - x2, v = x1 + x2,
+    #   K u = lam v and M v = lam u   <=>   H [x1; x2] = lam [x1; x2]
+    lam_h = lam.cpu().numpy()
+    ok = bool(np.all(lam_h > 0) and np.all(np.diff(lam_h) <= 0))
+    verification = None
+    if not args.no_verify:
+        del work
+        torch.cuda.empty_cache()
+        S, D, _, _ = local_tiles()
+        Sf = torch.zeros((n, ld), dtype=torch.float64, device=dev)
+        Df = torch.zeros((n, ld), dtype=torch.float64, device=dev)
+        Sf[:, :n].copy_(S)
+        Df[:, :n].copy_(D)
+        del S, D
+        worst = 0.0
+        bio = 0.0
+        if nloc:
+            lamloc = lam[torch.as_tensor(cols, device=dev, dtype=torch.long)]
+            U = X1 - X2
+            V = X1 + X2
+            P = torch.empty_like(U)
+            for (A_, in_, oth) in ((Df, U, V), (Sf, V, U)):
+                st = lib.bse_gemm_dev(0, 0, n, nloc, n, 1.0, ptr(A_), ld, ptr(in_), ld, 0.0,
+                                      ptr(P), ld, None, sp)
+                assert st == 0, _lib.last_error()
+                r = (P[:nloc, :n] - lamloc[:, None] * oth[:nloc, :n]).norm(dim=1)
+                xn = torch.sqrt(X1[:nloc, :n].norm(dim=1) ** 2 + X2[:nloc, :n].norm(dim=1) ** 2)
+                worst = max(worst, float((r / (lam[0] * xn)).max().item()))
+            G = torch.empty((nloc, nloc + (nloc & 1)), dtype=torch.float64, device=dev)
+            lib.bse_gemm_dev(1, 0, nloc, nloc, n, 1.0, ptr(X1), ld, ptr(X1), ld, 0.0, ptr(G),
+                             G.shape[1], None, sp)
+            lib.bse_gemm_dev(1, 0, nloc, nloc, n, -1.0, ptr(X2), ld, ptr(X2), ld, 1.0, ptr(G),
+                             G.shape[1], None, sp)
+            bio = float((G[:, :nloc] - torch.eye(nloc, dtype=torch.float64, device=dev)).norm().item())
+        t = torch.tensor([worst, bio], dtype=torch.float64, device=rdev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        verification = {"max_pair_residual": float(t[0]), "local_biorthogonality_fro": float(t[1]),
+                        "gate": "<= 1e-13 n and <= 1e-12 n on every rank's columns (SURVEY 8c(8))",
+                        "pass": bool(float(t[0]) <= 1e-13 * n and float(t[1]) <= 1e-12 * n)}
+        del Sf, Df
+        torch.cuda.empty_cache()
+        work = torch.empty(wb, dtype=torch.uint8, device=dev)
+
+    # ---- e2e: pinned host tiles -> device, solve, lam and this rank's X back ----
+    e2e = None
+    if args.e2e_steps > 0:
+        Mh = torch.empty(Mloc.shape, dtype=torch.float64, pin_memory=True)
+        Kh = torch.empty(Kloc.shape, dtype=torch.float64, pin_memory=True)
+        Mh.copy_(Mloc)
+        Kh.copy_(Kloc)
+        lamh = torch.empty(n, dtype=torch.float64, pin_memory=True)
+        X1h = torch.empty(X1.shape, dtype=torch.float64, pin_memory=True)
+        X2h = torch.empty(X2.shape, dtype=torch.float64, pin_memory=True)
+
+        def e2e_step():
+            Mloc.copy_(Mh, non_blocking=True)
+            Kloc.copy_(Kh, non_blocking=True)
+            step()
+            lamh.copy_(lam, non_blocking=True)
+            X1h.copy_(X1, non_blocking=True)
+            X2h.copy_(X2, non_blocking=True)
+            torch.cuda.synchronize(dev)
+        e2e_step()
+        dist.barrier()
+        t0 = time.perf_counter()
+        for _ in range(args.e2e_steps):
+            e2e_step()
+        e2e_s = max_over_ranks((time.perf_counter() - t0) / args.e2e_steps, dist, rdev)
+        e2e = {"value": e2e_s, "unit": "s", "h2d_bytes_per_step": 2 * n * n * 8,
+               "d2h_bytes_per_step": (2 * n * n + world * n) * 8,
+               "path": "per rank: pinned host column tiles of M, K -> device; "
+                       "bse_solve_spd_pair_bc_dev; lam and the rank's X1, X2 columns -> pinned host"}
+    mem = {"workspace_total": wb, "workspace_distributed": wb_dist, "workspace_replicated": wb_rep,
+           "inputs": 2 * Mloc.numel() * 8, "outputs": (2 * X1.numel() + n) * 8,
+           "single_gpu_workspace": int(lib.bse_solve_workspace_bytes(n, 0)) + 4 * n * ld * 8}
+    mem["total"] = mem["workspace_total"] + mem["inputs"] + mem["outputs"]
+    comm.close()
+    if rank != 0:
+        dist.destroy_process_group()
+        return 0
+    q2 = stages.get("q2_apply", 0.0)
+    roof = None
+    if q2 > 0 and nloc:
+        fl_q2 = 2.0 * n * n * nloc
+        ach = fl_q2 / (q2 * 1e-3) / 1e12
+        roof = {"bound": "tensor", "kernel": "q2_apply (this rank's columns)", "achieved": ach,
+                "peak": fp64_peak, "unit": "TFLOP/s", "frac": ach / fp64_peak, "traffic": None,
+                "peak_source": "measured in-run FP64 DMMA probe", "flops_per_launch": fl_q2}
+    solve_s = ms_step / 1e3
+    line = {
+        "metric": "full BSE eigenpair time-to-solution (s)", "value": solve_s, "unit": "s",
+        "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step,
+        "higher_is_better": False, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (BASELINE cfg2 recipe, torch Philox on GPU, identical on every rank)",
+        "config": {"workload": f"cfg2 real BSE n={n} (H {2 * n}x{2 * n}), log-uniform [0.1,100] "
+                               f"spectra, all eigenpairs + X1/X2",
+                   "n": n,
+                   "parallelism": f"memory-distributed 1x{world} block-cyclic column tiles "
+                                  f"(nb={nb}); transport {transport}",
+                   "l2": f"per-rank inputs {mem['inputs'] / 2**30:.1f} GiB > 126 MB L2 (no flush needed)"},
+        "tflops": alg_flops(n) / solve_s / 1e12, "fp64_peak_tflops": fp64_peak,
+        "frac_of_fp64_peak": alg_flops(n) / solve_s / 1e12 / (fp64_peak * world),
+        "stages_ms": {k: round(v, 3) for k, v in stages.items()},
+        "roofline": roof, "memory_per_rank_bytes": mem, "cpu_baseline": None, "e2e": e2e,
+        "gpu_launches": int(launches), "clocks": clk, "sanity_lambda_positive_desc": ok,
+        "verification": verification,
+    }
+    print(json.dumps(line), flush=True)
+    dist.destroy_process_group()
+    return 0
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -730,6 +945,12 @@ def main():
                     help="skip the solve_real(op) drop-in API timing")
     ap.add_argument("--no-native", action="store_true",
                     help="skip the all-DMMA (BSE_FLAG_NATIVE_FP64) comparison solve")
+    ap.add_argument("--nb", type=int, default=512, help="N > 1: block-cyclic tile width (cfg2: 512)")
+    ap.add_argument("--transport", choices=["nccl", "host"], default=None,
+                    help="N > 1: nccl (default when every rank has its own GPU) or the "
+                         "host-staged transport (ranks may share a GPU)")
+    ap.add_argument("--replicated", action="store_true",
+                    help="N > 1: the round-1 column-sharded solve with replicated operands")
     ap.add_argument("--config", type=int, default=2, choices=[1, 2, 3],
                     help="2 (default): real n=16384 headline; 1: complex n=2048; "
                          "3: complex n=16384 (real embedding 32768)")
@@ -744,6 +965,8 @@ def main():
         return run_ours_complex(args)
     if args.n is None:
         args.n = 16384
+    if env_rank()[2] > 1 and not args.replicated:
+        return run_ours_bc(args)
     return run_ours(args)
 
 

@@ -604,7 +604,8 @@ cudaError_t solve_spd_pair_bc(Comm& comm, int n, int nb, const double* Mloc, lon
     PhaseB pb = carve_b(sa, n, nb, lay.ntiles_of(lay.rank));
     BSE_TRY(sy2sb_bc(comm, lay, w.WZ, w.TV, ld, nloc, w.Tall, pb, sms, s));
   }
-  // 3b. band -> tridiagonal, replicated on the gathered band
+  // 3b. band -> tridiagonal on the gathered band: rank 0 chases the bulges and
+  // broadcasts d, e and the reflectors
   stage_mark("sb2st", s);
   BSE_TRY(cudaMemsetAsync(w.AB, 0, sizeof(double) * w.ldab * n, s));
   if (nloc > 0) {
@@ -612,7 +613,7 @@ cudaError_t solve_spd_pair_bc(Comm& comm, int n, int nb, const double* Mloc, lon
     count_launch();
   }
   if (world > 1) BSE_TRY(comm.allreduce_sum(w.AB, (size_t)w.ldab * n, s));
-  BSE_TRY(sb2st(w.AB, w.ldab, n, b, w.d, w.e, w.V2, w.tau2, w.progress, sms, s));
+  BSE_TRY(sb2st_shared(&comm, w.AB, w.ldab, n, b, w.d, w.e, w.V2, w.tau2, w.progress, sms, s));
   // 3c. tridiagonal divide and conquer on row blocks, then the transposition
   // into this rank's solution columns (into WZ: W is dead)
   stage_mark("stedc", s);

@@ -186,9 +186,19 @@ size_t syevd_bytes(int n, int flags);
 // conv_out (device int, may be null): nonzero after the call completes when
 // the tridiagonal eigensolver did not converge (maps to BSE_NO_CONVERGENCE,
 // the analogue of kernels.ConvergenceError, kernels.py:403-419).
+// comm (replicated multi-rank callers): the bulge chasing runs on rank 0 only
+// and d, e and its reflectors are broadcast, so every rank back-transforms
+// with the same bits (and ranks sharing one GPU in tests never time-slice the
+// persistent SB2ST kernel).
+struct Comm;
 cudaError_t syevd(int n, double* A, long long lda, double* w, double* Z, long long ldz,
                   void* work, size_t work_bytes, int flags, cudaStream_t s, int zc0 = 0,
-                  int zc1 = -1, int* conv_out = nullptr, ZSelect* sel = nullptr);
+                  int zc1 = -1, int* conv_out = nullptr, ZSelect* sel = nullptr,
+                  Comm* comm = nullptr);
+// Band -> tridiagonal on rank 0 of comm (all ranks when comm is null or has
+// one rank), then d, e, V2, tau2 broadcast.
+cudaError_t sb2st_shared(Comm* comm, double* AB, int ldab, int n, int b, double* d, double* e,
+                         double* V2, double* tau2, int* progress, int num_sms, cudaStream_t s);
 
 int device_sm_count();
 

@@ -94,10 +94,10 @@ BSE_DEV void bar_wait(uint32_t a, uint32_t parity) {
   for (uint32_t it = 0;; ++it) {
     asm volatile(
         "{\n .reg .pred p;\n"
-        " mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%1], %2;\n"
+        " mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3;\n"
         " selp.u32 %0, 1, 0, p;\n}\n"
         : "=r"(done)
-        : "r"(a), "r"(parity)
+        : "r"(a), "r"(parity), "r"(0x989680u)  // suspend-time hint: the waiter sleeps in hardware
         : "memory");
     if (done) return;
     if ((it & 4095u) == 4095u) {

@@ -434,8 +434,43 @@ size_t ozgemm_bytes(int M, int N, int K, int chunk) {
   return a8 + b8 + c32 + 8 * (size_t)(Mp + Np) * 2 + 4096;
 }
 
+namespace {
+// BSE_OZ_TRACE=1: per-kernel CUDA-event times of every ozgemm call on stderr
+// (synchronises the stream; diagnostics only).
+struct OzTrace {
+  bool on;
+  cudaStream_t s;
+  cudaEvent_t ev[64];
+  const char* name[64];
+  int n = 0;
+  explicit OzTrace(cudaStream_t st) : s(st) {
+    static const bool env = std::getenv("BSE_OZ_TRACE") != nullptr;
+    on = env;
+  }
+  void mark(const char* what) {
+    if (!on || n >= 64) return;
+    cudaEventCreate(&ev[n]);
+    cudaEventRecord(ev[n], s);
+    name[n++] = what;
+  }
+  ~OzTrace() {
+    if (!on || n == 0) return;
+    cudaStreamSynchronize(s);
+    std::fprintf(stderr, "[oz]");
+    for (int i = 0; i + 1 < n; ++i) {
+      float ms = 0.f;
+      cudaEventElapsedTime(&ms, ev[i], ev[i + 1]);
+      std::fprintf(stderr, " %s %.3f", name[i], ms);
+    }
+    std::fprintf(stderr, "\n");
+    for (int i = 0; i < n; ++i) cudaEventDestroy(ev[i]);
+  }
+};
+}  // namespace
+
 cudaError_t ozgemm(bool transA, bool transB, const GemmProblem& p, void* work, size_t work_bytes,
                    int chunk, cudaStream_t s, bool reuse_a) {
+  OzTrace tr(s);
   if (p.M <= 0 || p.N <= 0) return cudaSuccess;
   cudaError_t e;
   if ((e = init_const()) != cudaSuccess) return e;
@@ -485,6 +520,7 @@ cudaError_t ozgemm(bool transA, bool transB, const GemmProblem& p, void* work, s
     return cudaGetLastError();
   };
   // op(A) rows: stored A is M x K (transA false: strided lines) or K x M (contiguous)
+  tr.mark("split_a");
   if (!reuse_a && (e = split(transA, M, p.A, p.lda, p.ma, a8, Mp, sa, mxa)) != cudaSuccess) return e;
   for (int j0 = 0; j0 < p.N; j0 += nc_max) {
     const int nc = std::min(nc_max, p.N - j0);
@@ -502,11 +538,14 @@ cudaError_t ozgemm(bool transA, bool transB, const GemmProblem& p, void* work, s
       if (mb.lo != kNoMaskLo) mb.lo += j0;
       if (mb.hi != kNoMaskHi) mb.hi += j0;
     }
+    tr.mark("split_b");
     if ((e = split(!transB, nc, bsrc, p.ldb, mb, b8, ncp, sb, mxb)) != cudaSuccess) return e;
+    tr.mark("mma");
     const long long tot = (long long)((M + 3) / 4) * nc;
     if (oz_engine() == 2) {
       if ((e = i8_gemm_batched((int)Mp, (int)ncp, (int)Kp, kMods, a8, b8, c32, s)) != cudaSuccess)
         return e;
+      tr.mark("crt");
       crt_kernel<<<(unsigned)ceil_div(tot, 256), 256, 0, s>>>(M, nc, (int)Mp, c32, Mp * ncp, sa, sb,
                                                              p.alpha, p.beta, p.C, p.ldc, j0, p.mc,
                                                              p.ccol);
@@ -517,6 +556,7 @@ cudaError_t ozgemm(bool transA, bool transB, const GemmProblem& p, void* work, s
       if ((e = i8mma_residues(M, nc, (int)Kp, a8, Mp, b8, ncp, r8, ldr, j0, p.mc.lo, p.mc.hi,
                               oz_engine() == 0, s)) != cudaSuccess)
         return e;
+      tr.mark("crt");
       crt8_kernel<<<(unsigned)ceil_div(tot, 256), 256, 0, s>>>(M, nc, r8, ldr, ncp * ldr, sa, sb,
                                                               p.alpha, p.beta, p.C, p.ldc, j0, p.mc,
                                                               p.ccol);
@@ -524,6 +564,7 @@ cudaError_t ozgemm(bool transA, bool transB, const GemmProblem& p, void* work, s
     count_launch();
     if ((e = cudaGetLastError()) != cudaSuccess) return e;
   }
+  tr.mark("end");
   return cudaSuccess;
 }
 

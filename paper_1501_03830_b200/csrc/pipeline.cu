@@ -4,8 +4,10 @@
 // Step order follows the reference's solvers (solvers.py:46-77 / :97-104):
 // Cholesky -> congruence -> eigendecomposition -> back-transform -> scale.
 #include <algorithm>
+#include <cstdio>
 #include <cstdlib>
 #include <string>
+#include <unistd.h>
 #include <vector>
 #include "eig.cuh"
 #include "comm.cuh"
@@ -149,6 +151,50 @@ __global__ void gather_cols_kernel(int n, int nsel, const double* Z, long long l
 }
 }  // namespace
 
+namespace {
+// BSE_DEBUG_HASH=1: checksum of an intermediate on stderr (synchronises; the
+// determinism probe compares them between repetitions to find the first
+// stage whose output differs)
+void debug_hash(const char* name, const void* dptr, size_t bytes, cudaStream_t s) {
+  static const bool on = std::getenv("BSE_DEBUG_HASH") != nullptr;
+  if (!on || bytes == 0) return;
+  std::vector<unsigned char> h(bytes);
+  cudaMemcpyAsync(h.data(), dptr, bytes, cudaMemcpyDeviceToHost, s);
+  cudaStreamSynchronize(s);
+  unsigned long long x = 1469598103934665603ull;
+  const unsigned long long* q = reinterpret_cast<const unsigned long long*>(h.data());
+  for (size_t i = 0; i < bytes / 8; ++i) x = (x ^ q[i]) * 1099511628211ull;
+  std::fprintf(stderr, "[hash %d] %s %016llx\n", (int)getpid(), name, x);
+  if (const char* dir = std::getenv("BSE_DEBUG_DUMP")) {
+    if (bytes <= (1u << 22)) {  // small arrays only (d, e, w)
+      static int counter = 0;
+      const std::string path = std::string(dir) + "/" + name + "_" + std::to_string((int)getpid()) +
+                               "_" + std::to_string(counter++) + ".bin";
+      if (FILE* f = std::fopen(path.c_str(), "wb")) {
+        std::fwrite(h.data(), 1, bytes, f);
+        std::fclose(f);
+      }
+    }
+  }
+}
+}  // namespace
+
+cudaError_t sb2st_shared(Comm* comm, double* AB, int ldab, int n, int b, double* d, double* e,
+                         double* V2, double* tau2, int* progress, int num_sms, cudaStream_t s) {
+  cudaError_t err;
+  if (!comm || comm->world <= 1) return sb2st(AB, ldab, n, b, d, e, V2, tau2, progress, num_sms, s);
+  if (comm->rank == 0 &&
+      (err = sb2st(AB, ldab, n, b, d, e, V2, tau2, progress, num_sms, s)) != cudaSuccess)
+    return err;
+  const size_t steps = (size_t)sb2st_maxsteps(n, b);
+  if ((err = comm->group_begin()) != cudaSuccess) return err;
+  if ((err = comm->bcast(d, (size_t)n, 0, s)) != cudaSuccess) return err;
+  if ((err = comm->bcast(e, (size_t)n, 0, s)) != cudaSuccess) return err;
+  if ((err = comm->bcast(tau2, (size_t)n * steps, 0, s)) != cudaSuccess) return err;
+  if ((err = comm->bcast(V2, (size_t)n * steps * b, 0, s)) != cudaSuccess) return err;
+  return comm->group_end(s);
+}
+
 size_t syevd_bytes(int n, int flags) {
   Arena a;
   a.dry = true;
@@ -158,7 +204,7 @@ size_t syevd_bytes(int n, int flags) {
 
 cudaError_t syevd(int n, double* A, long long lda, double* w, double* Z, long long ldz,
                   void* work, size_t work_bytes, int flags, cudaStream_t s, int zc0, int zc1,
-                  int* conv_out, ZSelect* sel) {
+                  int* conv_out, ZSelect* sel, Comm* comm) {
   if (n <= 0) return cudaSuccess;
   Arena a{static_cast<char*>(work), work_bytes, 0, false};
   SyevdWork ws = carve_syevd(a, n, flags);
@@ -174,8 +220,15 @@ cudaError_t syevd(int n, double* A, long long lda, double* w, double* Z, long lo
     return e;
   stage_mark("sb2st", s);
   if ((e = extract_band(A, lda, n, b, ws.AB, ws.ldab, s)) != cudaSuccess) return e;
-  if ((e = sb2st(ws.AB, ws.ldab, n, b, ws.d, ws.e, ws.V2, ws.tau2, ws.progress, sms, s)) != cudaSuccess)
+  debug_hash("band", ws.AB, sizeof(double) * ws.ldab * n, s);
+  debug_hash("Tall", ws.Tall, sizeof(double) * (size_t)(n / b) * b * b, s);
+  debug_hash("Vall", ws.Vall, sizeof(double) * ws.ldv * n, s);
+  if ((e = sb2st_shared(comm, ws.AB, ws.ldab, n, b, ws.d, ws.e, ws.V2, ws.tau2, ws.progress, sms, s)) !=
+      cudaSuccess)
     return e;
+  debug_hash("d", ws.d, sizeof(double) * n, s);
+  debug_hash("e", ws.e, sizeof(double) * (n - 1), s);
+  debug_hash("tau2", ws.tau2, sizeof(double) * (size_t)n * sb2st_maxsteps(n, b), s);
   if (flags & 0x1) {  // BSE_FLAG_VALUES_ONLY: no vectors, no back-transforms
     stage_mark("values", s);
     if (conv_out && (e = cudaMemsetAsync(conv_out, 0, sizeof(int), s)) != cudaSuccess) return e;
@@ -197,15 +250,18 @@ cudaError_t syevd(int n, double* A, long long lda, double* w, double* Z, long lo
   if ((e = cudaEventRecord(side.join, sb)) != cudaSuccess) return e;
   // the D&C chain of small latency-bound kernels runs on a high-priority
   // stream so the side stream's CTAs never delay its next launch
+  static const bool dc_main = std::getenv("BSE_DC_MAIN") != nullptr;  // diagnostics: D&C on s
+  cudaStream_t sdc = dc_main ? s : side.hp;
   if ((e = cudaEventRecord(side.hp_fork, s)) != cudaSuccess) return e;
-  if ((e = cudaStreamWaitEvent(side.hp, side.hp_fork, 0)) != cudaSuccess) return e;
-  stage_mark("stedc", side.hp);
-  if ((e = stedc(n, ws.d, ws.e, w, Z, ldz, ws.dc, side.hp)) != cudaSuccess) return e;
+  if ((e = cudaStreamWaitEvent(sdc, side.hp_fork, 0)) != cudaSuccess) return e;
+  stage_mark("stedc", sdc);
+  if ((e = stedc(n, ws.d, ws.e, w, Z, ldz, ws.dc, sdc)) != cudaSuccess) return e;
   if (conv_out && (e = cudaMemcpyAsync(conv_out, ws.dc.fail, sizeof(int), cudaMemcpyDeviceToDevice,
-                                       side.hp)) != cudaSuccess)
+                                       sdc)) != cudaSuccess)
     return e;
-  if ((e = cudaEventRecord(side.hp_join, side.hp)) != cudaSuccess) return e;
+  if ((e = cudaEventRecord(side.hp_join, sdc)) != cudaSuccess) return e;
   if ((e = cudaStreamWaitEvent(s, side.hp_join, 0)) != cudaSuccess) return e;
+  debug_hash("w", w, sizeof(double) * n, s);
   if (mode == 2) {
     stage_mark("q1_build", s);
     if ((e = q1_build(n, b, ws.Vall, ws.ldv, ws.Tall, ws.q1, s)) != cudaSuccess) return e;
@@ -663,7 +719,7 @@ cudaError_t solve_spd_pair(int n, const double* M, long long ldm, const double* 
     zsel->dcols = w.cols;
   }
   if ((e = syevd(n, w.W, ld, w.lam2, w.T1, ld, w.eig, w.eig_bytes, flags, s, (int)(n - c1),
-                 (int)(n - c0), &w.st[0].conv_fail, zsel)) != cudaSuccess)
+                 (int)(n - c0), &w.st[0].conv_fail, zsel, world > 1 ? comm : nullptr)) != cudaSuccess)
     return e;
   if (zsel && zsel->nsel <= 0) {
     // the selector refused the spectrum (non-positive or non-finite lambda^2):

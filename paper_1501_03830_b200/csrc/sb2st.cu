@@ -18,6 +18,7 @@ constexpr int kDone = 0x7fffffff;
 constexpr int kSlots = kMaxPanel * kMaxPanel / kSbThreads;  // 16 block slots per thread
 
 __constant__ int c_sb_trace_s0;  // first traced sweep (BSE_SB2ST_TRACE)
+__constant__ int c_sb_mode;      // diagnostics (BSE_SB2ST_MODE): 1 CTA-wide full publish, 2 acquire polls
 
 BSE_DEV unsigned long long gtimer() {
   unsigned long long t;
@@ -68,8 +69,22 @@ BSE_DEV int colA(int q, int i) { return 8 * (i >> 1) + 2 * q + (i & 1); }
 // phase C (lanes: 4 columns x 4 quarters per half-warp) row pattern
 BSE_DEV int rowC(int q, int i) { return 16 * (i >> 2) + 2 * (i & 3) + (q & 1) + 8 * (q >> 1); }
 
+// Diagnostics (BSE_SB2ST_MODE bits 4/8/16/32): a pseudo-random delay of up to
+// ~16 us keyed by (sweep, step, site) to perturb the hand-off timing.
+BSE_DEV void dbg_delay(int bit, int s, int j) {
+  if (!(c_sb_mode & bit)) return;
+  unsigned h = (unsigned)(s * 2654435761u) ^ (unsigned)(j * 40503u) ^ (unsigned)(bit * 97u);
+  h ^= h >> 13; h *= 0x5bd1e995u; h ^= h >> 15;
+  if ((h & 7u) == 0) __nanosleep((h >> 8) & 0x3fffu);
+}
+
 // Acquire-poll one counter (thread 0).  No barrier.
 BSE_DEV void poll_counter(const int* ctr, int need) {
+  if (c_sb_mode & 2) {
+    while (ld_acquire(ctr) < need) {
+    }
+    return;
+  }
   if (ld_relaxed(ctr) < need) {
     while (ld_relaxed(ctr) < need) {
     }
@@ -225,6 +240,7 @@ __global__ void __launch_bounds__(kSbThreads) sb2st_fused_kernel(double* AB, int
       // late wait, overlapping the arrival of this step's staged bulk; then
       // mirror D and load the late row (disjoint positions, one barrier)
       if (has_pred && tid == 0) poll_counter(late + s - 1, j + 2);
+      if (tid == 0) dbg_delay(32, s, j);
       cp_async_wait<0>();
       __syncthreads();
       if (trs) T(1);
@@ -299,6 +315,8 @@ __global__ void __launch_bounds__(kSbThreads) sb2st_fused_kernel(double* AB, int
       const double gm = warp_sum(sm.tt[lane] * vn[lane] + sm.tt[lane + 32] * vn[lane + 32]);
       const double al = -0.5 * taun * gm;
       if (warp == 0) {
+        if (lane == 0) dbg_delay(4, s, j);
+        __syncwarp();
         // publish the successor's late data: row 0 of O'' and D''(0, 0)
 #pragma unroll
         for (int h = 0; h < 2; ++h) {
@@ -324,6 +342,8 @@ __global__ void __launch_bounds__(kSbThreads) sb2st_fused_kernel(double* AB, int
         if (lane == 0) tau2[(long long)s * maxsteps + j] = taun;
       }
       // D: the bulk of O'' and D'' (rows >= 1)
+      if (lane == 0) dbg_delay(8, s, j + warp);
+      __syncwarp();
       if (lq == kMaxPanel && lp == kMaxPanel) {
         const int c = kMaxPanel - 1 - (tid >> 2), kq = tid & 3;
         double* od = AB + (long long)(p0 + c) * ldab + (q0 - p0 - c);
@@ -391,16 +411,25 @@ __global__ void __launch_bounds__(kSbThreads) sb2st_fused_kernel(double* AB, int
       }
       // each warp publishes its own bulk stores: full[s] reaches
       // kBulkWarps * (j + 1) once step j is completely stored
-      __syncwarp();
-      if (lane == 0) {
-        __threadfence();
-        atomicAdd(full + s, 1);
+      if (c_sb_mode & 1) {
+        __syncthreads();
+        if (tid == 0) {
+          __threadfence();
+          atomicAdd(full + s, kBulkWarps);
+        }
+      } else {
+        __syncwarp();
+        if (lane == 0) {
+          __threadfence();
+          atomicAdd(full + s, 1);
+        }
       }
       if (trs) T(5);
       if (warp != 0 && has_next) {
         // warps 1..7: stage step j+1's bulk into the other buffer (needs the
         // predecessor's step j+1 fully stored) -- after our own bulk, so our
         // `full` is never held back by our predecessor
+        if (tid == 32) dbg_delay(16, s, j);
         if (has_pred && tid == 32) poll_counter(full + s - 1, kBulkWarps * (j + 2));
         if (trs32) T(7);
         named_bar(1, kSbThreads - 32);
@@ -459,6 +488,8 @@ cudaError_t sb2st(double* AB, int ldab, int n, int b, double* d, double* e, doub
     int ts0 = want_trace ? std::atoi(tenv) : 0;
     ts0 = std::max(0, std::min(ts0, n - 4));
     cudaMemcpyToSymbolAsync(c_sb_trace_s0, &ts0, sizeof(int), 0, cudaMemcpyHostToDevice, s);
+    static const int sb_mode = std::getenv("BSE_SB2ST_MODE") ? std::atoi(std::getenv("BSE_SB2ST_MODE")) : 0;
+    cudaMemcpyToSymbolAsync(c_sb_mode, &sb_mode, sizeof(int), 0, cudaMemcpyHostToDevice, s);
     const size_t tsz = (size_t)2 * maxsteps * 16;
     if (want_trace) {
       cudaMalloc(&trace, sizeof(unsigned long long) * tsz);
