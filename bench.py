@@ -955,6 +955,12 @@ def main():
                     help="2 (default): real n=16384 headline; 1: complex n=2048; "
                          "3: complex n=16384 (real embedding 32768)")
     args = ap.parse_args()
+    # under torchrun, "--n" is an ambiguous prefix of the launcher's own options:
+    # BSE_BENCH_N / BSE_BENCH_TRANSPORT carry the same settings there
+    if args.n is None and os.environ.get("BSE_BENCH_N"):
+        args.n = int(os.environ["BSE_BENCH_N"])
+    if args.transport is None and os.environ.get("BSE_BENCH_TRANSPORT"):
+        args.transport = os.environ["BSE_BENCH_TRANSPORT"]
     if args.warmup < 3:
         args.warmup = 3  # timing rule: >= 3 warm-up steps
     if args.impl == "reference":

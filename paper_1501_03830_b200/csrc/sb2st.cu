@@ -179,8 +179,20 @@ BSE_DEV void mirror_d(double* Db, int lq) {
 }
 
 // The late positions (D's last row and O(lq-1, lp-1)), after the late wait.
+//
+// One more position of a FULL block's last row is not covered by the two
+// counters: O(lq-1, lp-2).  It is column 0, row 1 of the O block of sweep
+// s-2's step j+1 -- an entry that sweep annihilates, so its bulk store writes
+// 0 there -- and sweep s-1 never touches it.  Sweep s-1's step j only waits
+// for sweep s-2's step j+1 ROW 0 (`late`), not for its bulk, so the staged
+// copy of that entry may still hold the fill-in that sweep s-3 left there
+// when sweep s-2 is descheduled between its two stores (observed under
+// time-sliced GPU sharing, and reproduced by delaying the bulk stores).  Its
+// final value is exactly 0 by construction, so it is set here instead of read.
+// (The entries further left in that row were zeroed by sweeps s-3, s-4, ...,
+// whose bulk stores are ordered before this step through `full`.)
 BSE_DEV void late_load(double* Db, double* Ob, const double* AB, int ldab, int q0, int lq, int p0,
-                       int lp) {
+                       int lp, int b) {
   const int tid = threadIdx.x, rl = lq - 1;
   if (tid < kMaxPanel) {
     const int c = tid;
@@ -189,6 +201,8 @@ BSE_DEV void late_load(double* Db, double* Ob, const double* AB, int ldab, int q
     Db[rl * kLd2 + c] = x;
   } else if (tid == kMaxPanel) {
     Ob[(lp - 1) * kLd2 + rl] = __ldcg(AB + (long long)(p0 + lp - 1) * ldab + (q0 + rl - p0 - lp + 1));
+  } else if (tid == kMaxPanel + 1) {
+    if (lq == b && lp >= 2) Ob[(lp - 2) * kLd2 + rl] = 0.0;
   }
 }
 
@@ -245,7 +259,7 @@ __global__ void __launch_bounds__(kSbThreads) sb2st_fused_kernel(double* AB, int
       __syncthreads();
       if (trs) T(1);
       mirror_d(Db, lq);
-      late_load(Db, Ob, AB, ldab, q0, lq, p0, lp);
+      late_load(Db, Ob, AB, ldab, q0, lq, p0, lp, b);
       __syncthreads();
       if (trs) T(2);
       // A: w = tau O v
@@ -342,7 +356,8 @@ __global__ void __launch_bounds__(kSbThreads) sb2st_fused_kernel(double* AB, int
         if (lane == 0) tau2[(long long)s * maxsteps + j] = taun;
       }
       // D: the bulk of O'' and D'' (rows >= 1)
-      if (lane == 0) dbg_delay(8, s, j + warp);
+      if (lane == 0 && (!(c_sb_mode & 128) || warp == 0) && (!(c_sb_mode & 256) || warp != 0))
+        dbg_delay(8, s, (c_sb_mode & 64) ? j : j + warp);
       __syncwarp();
       if (lq == kMaxPanel && lp == kMaxPanel) {
         const int c = kMaxPanel - 1 - (tid >> 2), kq = tid & 3;
