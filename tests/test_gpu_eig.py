@@ -93,3 +93,60 @@ def test_syevd_clustered(dev):
     assert np.abs(w - np.sort(vals)).max() <= 1e-12 * 10
     assert np.abs(a @ Z - Z * w).max() <= 1e-12 * 10
     assert np.abs(Z.T @ Z - np.eye(n)).max() <= 1e-12
+
+
+_SB2ST_HASH_SCRIPT = r"""
+import hashlib, sys
+import numpy as np, torch
+sys.path.insert(0, {root!r})
+from paper_1501_03830_b200 import _lib
+from paper_1501_03830_b200.device import check, colmajor_empty, ptr, stream_ptr, to_device_colmajor
+dev = torch.device("cuda", 0)
+lib = _lib.load()
+n = 2000
+rng = np.random.default_rng(5)
+a = rng.standard_normal((n, n)); a = a + a.T
+out = []
+for _ in range(3):
+    da, lda = to_device_colmajor(a, dev)
+    Z, ldz = colmajor_empty(n, n, dev)
+    w = torch.empty(n, dtype=torch.float64, device=dev)
+    wb = lib.bse_syevd_workspace_bytes(n, 1)
+    work = torch.empty(wb, dtype=torch.uint8, device=dev)
+    check(lib.bse_syevd_dev(n, ptr(da), lda, ptr(w), ptr(Z), ldz, ptr(work), wb, 1, stream_ptr()), "syevd")
+    torch.cuda.synchronize()
+    out.append(hashlib.sha1(w.cpu().numpy().tobytes()).hexdigest())
+print("HASHES", *out)
+"""
+
+
+def test_sb2st_result_independent_of_handoff_timing(dev):
+    """Regression for the cross-sweep race fixed in round 2:
+    with pseudo-random delays of up to 16 us injected before the bulk stores of
+    warps 1-7 (BSE_SB2ST_MODE=264) -- which made every run differ before the
+    fix -- the band -> tridiagonal stage must give bit-identical eigenvalues,
+    equal to the undisturbed run's.  (The mode is read once per process, hence
+    the subprocesses.)"""
+    import os
+    import subprocess
+    import sys
+    from pathlib import Path
+    root = str(Path(__file__).resolve().parents[1])
+    script = _SB2ST_HASH_SCRIPT.format(root=root)
+
+    def run(mode):
+        env = dict(os.environ)
+        env.pop("BSE_SB2ST_MODE", None)
+        if mode:
+            env["BSE_SB2ST_MODE"] = str(mode)
+        res = subprocess.run([sys.executable, "-c", script], env=env, capture_output=True, text=True,
+                             timeout=600)
+        assert res.returncode == 0, res.stderr[-2000:]
+        line = [ln for ln in res.stdout.splitlines() if ln.startswith("HASHES")][-1]
+        return line.split()[1:]
+
+    plain = run(0)
+    delayed = run(264)
+    uniform = run(72)
+    assert len(set(plain)) == 1
+    assert set(delayed) == set(plain) and set(uniform) == set(plain)

@@ -147,3 +147,31 @@ def test_tcgen05_kernel_output_band(dev, engine):
     ref = np.where(np.tril(np.ones((M, N), bool)), c - a @ b, c)
     assert np.max(np.abs(got - ref)) <= 1e-12
     assert np.array_equal(np.triu(got, 1), np.triu(c, 1))
+
+
+@pytest.mark.parametrize("engine", [0, 1])
+def test_tcgen05_fp32_residue_path_extremes(dev, engine):
+    """K <= 256 takes the epilogue's FP32 reduction: accumulators at the ends of
+    its range (|c| = K * 2^14 when every residue is -128, i.e. constant rows
+    whose scaled value is 128 mod m) must still reduce exactly -- compared bit
+    for bit with the INT32-plane path."""
+    lib = _lib.load()
+    for K in (256, 255, 130, 64):
+        M, N = 300, 260
+        rng = np.random.default_rng(K)
+        # rows of constants (every entry of a line equal to its maximum) and a
+        # few random ones: constant lines hit the same residue in every slot
+        a = np.repeat(rng.integers(1, 2 ** 20, (M, 1)).astype(float), K, axis=1)
+        b = np.repeat(rng.integers(1, 2 ** 20, (1, N)).astype(float), K, axis=0)
+        a[::7] = rng.standard_normal((a[::7].shape))
+        b[:, ::5] = rng.standard_normal((b[:, ::5].shape))
+        c = np.zeros((M, N))
+        prev = lib.bse_oz_set_engine(2)
+        try:
+            ref = _oz(dev, 0, 0, a, b, c, 1.0, 0.0)
+            lib.bse_oz_set_engine(engine)
+            got = _oz(dev, 0, 0, a, b, c, 1.0, 0.0)
+        finally:
+            lib.bse_oz_set_engine(prev)
+        assert np.array_equal(got, ref), K
+        assert np.max(np.abs(got - a @ b)) <= 1e-12 * np.max(np.abs(a @ b))
