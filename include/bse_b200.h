@@ -249,7 +249,8 @@ int bse_solve_spd_pair_dist_dev(bse_comm* comm, int64_t n, const double* dM, int
  * rank J mod Q with all its rows), and the divide and conquer's eigenvector
  * matrix by contiguous ROW blocks (bse_shard_range).  Per-rank dense storage
  * is O(n^2 / Q); the band, the tridiagonal data and the bulge-chasing
- * reflectors (n^2 doubles) are replicated.
+ * reflectors (n^2 doubles) are replicated (the bulge chasing itself runs on
+ * rank 0, which broadcasts its output).
  *
  * Called collectively.  dMloc, dKloc: this rank's bse_bc_local_cols columns
  * (n rows each; lower triangle of the global matrices referenced; local
