@@ -71,7 +71,9 @@ BSE_DEV int rowC(int q, int i) { return 16 * (i >> 2) + 2 * (i & 3) + (q & 1) + 
 
 // Diagnostics (BSE_SB2ST_MODE bits 4/8/16/32): a pseudo-random delay of up to
 // ~16 us keyed by (sweep, step, site) to perturb the hand-off timing.
+template <bool kDiag>
 BSE_DEV void dbg_delay(int bit, int s, int j) {
+  if constexpr (!kDiag) return;
   if (!(c_sb_mode & bit)) return;
   unsigned h = (unsigned)(s * 2654435761u) ^ (unsigned)(j * 40503u) ^ (unsigned)(bit * 97u);
   h ^= h >> 13; h *= 0x5bd1e995u; h ^= h >> 15;
@@ -79,8 +81,9 @@ BSE_DEV void dbg_delay(int bit, int s, int j) {
 }
 
 // Acquire-poll one counter (thread 0).  No barrier.
+template <bool kDiag>
 BSE_DEV void poll_counter(const int* ctr, int need) {
-  if (c_sb_mode & 2) {
+  if (kDiag && (c_sb_mode & 2)) {
     while (ld_acquire(ctr) < need) {
     }
     return;
@@ -210,6 +213,10 @@ BSE_DEV void named_bar(int id, int nthreads) {
   asm volatile("bar.sync %0, %1;\n" ::"r"(id), "r"(nthreads) : "memory");
 }
 
+// kDiag: the BSE_SB2ST_MODE diagnostics (delay injection, alternative
+// publication / polls) are compiled into a separate instance, so the
+// production kernel carries none of their checks.
+template <bool kDiag>
 __global__ void __launch_bounds__(kSbThreads) sb2st_fused_kernel(double* AB, int ldab, int n,
                                                                  int b, double* V2, double* tau2,
                                                                  int maxsteps, int* progress,
@@ -239,7 +246,7 @@ __global__ void __launch_bounds__(kSbThreads) sb2st_fused_kernel(double* AB, int
     int lq = q1 - q0 + 1;
     // prologue: step 0's bulk into buffer 0
     __syncthreads();  // the previous sweep is done with both buffers
-    if (has_pred && tid == 0) poll_counter(full + s - 1, kBulkWarps);
+    if (has_pred && tid == 0) poll_counter<kDiag>(full + s - 1, kBulkWarps);
     __syncthreads();
     stage_bulk(sm.D[0] + (q0 & 1), sm.O[0] + (q0 & 1), AB, ldab, q0, lq, p0, lp, tid, kSbThreads);
     cp_async_commit();
@@ -253,8 +260,8 @@ __global__ void __launch_bounds__(kSbThreads) sb2st_fused_kernel(double* AB, int
       if (trs) T(0);
       // late wait, overlapping the arrival of this step's staged bulk; then
       // mirror D and load the late row (disjoint positions, one barrier)
-      if (has_pred && tid == 0) poll_counter(late + s - 1, j + 2);
-      if (tid == 0) dbg_delay(32, s, j);
+      if (has_pred && tid == 0) poll_counter<kDiag>(late + s - 1, j + 2);
+      if (tid == 0) dbg_delay<kDiag>(32, s, j);
       cp_async_wait<0>();
       __syncthreads();
       if (trs) T(1);
@@ -329,7 +336,7 @@ __global__ void __launch_bounds__(kSbThreads) sb2st_fused_kernel(double* AB, int
       const double gm = warp_sum(sm.tt[lane] * vn[lane] + sm.tt[lane + 32] * vn[lane + 32]);
       const double al = -0.5 * taun * gm;
       if (warp == 0) {
-        if (lane == 0) dbg_delay(4, s, j);
+        if (lane == 0) dbg_delay<kDiag>(4, s, j);
         __syncwarp();
         // publish the successor's late data: row 0 of O'' and D''(0, 0)
 #pragma unroll
@@ -356,9 +363,11 @@ __global__ void __launch_bounds__(kSbThreads) sb2st_fused_kernel(double* AB, int
         if (lane == 0) tau2[(long long)s * maxsteps + j] = taun;
       }
       // D: the bulk of O'' and D'' (rows >= 1)
-      if (lane == 0 && (!(c_sb_mode & 128) || warp == 0) && (!(c_sb_mode & 256) || warp != 0))
-        dbg_delay(8, s, (c_sb_mode & 64) ? j : j + warp);
-      __syncwarp();
+      if constexpr (kDiag) {
+        if (lane == 0 && (!(c_sb_mode & 128) || warp == 0) && (!(c_sb_mode & 256) || warp != 0))
+          dbg_delay<kDiag>(8, s, (c_sb_mode & 64) ? j : j + warp);
+        __syncwarp();
+      }
       if (lq == kMaxPanel && lp == kMaxPanel) {
         const int c = kMaxPanel - 1 - (tid >> 2), kq = tid & 3;
         double* od = AB + (long long)(p0 + c) * ldab + (q0 - p0 - c);
@@ -426,7 +435,7 @@ __global__ void __launch_bounds__(kSbThreads) sb2st_fused_kernel(double* AB, int
       }
       // each warp publishes its own bulk stores: full[s] reaches
       // kBulkWarps * (j + 1) once step j is completely stored
-      if (c_sb_mode & 1) {
+      if (kDiag && (c_sb_mode & 1)) {
         __syncthreads();
         if (tid == 0) {
           __threadfence();
@@ -444,8 +453,8 @@ __global__ void __launch_bounds__(kSbThreads) sb2st_fused_kernel(double* AB, int
         // warps 1..7: stage step j+1's bulk into the other buffer (needs the
         // predecessor's step j+1 fully stored) -- after our own bulk, so our
         // `full` is never held back by our predecessor
-        if (tid == 32) dbg_delay(16, s, j);
-        if (has_pred && tid == 32) poll_counter(full + s - 1, kBulkWarps * (j + 2));
+        if (tid == 32) dbg_delay<kDiag>(16, s, j);
+        if (has_pred && tid == 32) poll_counter<kDiag>(full + s - 1, kBulkWarps * (j + 2));
         if (trs32) T(7);
         named_bar(1, kSbThreads - 32);
         const int nsh = nq0 & 1;
@@ -491,8 +500,11 @@ cudaError_t sb2st(double* AB, int ldab, int n, int b, double* d, double* e, doub
   if (n > 2) {
     if ((err = cudaMemsetAsync(progress, 0, sizeof(int) * 2 * (size_t)n, s)) != cudaSuccess) return err;
     const size_t smem = sizeof(SbfSmem);
-    static PerDeviceOnce attr;
-    if ((err = set_smem_limit(attr, sb2st_fused_kernel, (int)smem)) != cudaSuccess) return err;
+    static PerDeviceOnce attr, attr_diag;
+    static const int sb_mode = std::getenv("BSE_SB2ST_MODE") ? std::atoi(std::getenv("BSE_SB2ST_MODE")) : 0;
+    if ((err = sb_mode ? set_smem_limit(attr_diag, sb2st_fused_kernel<true>, (int)smem)
+                       : set_smem_limit(attr, sb2st_fused_kernel<false>, (int)smem)) != cudaSuccess)
+      return err;
     // one CTA per SM: the kernel is latency-bound and one resident step per
     // SM keeps every hand-off on an otherwise idle SM
     const int grid = std::max(1, std::min(n - 2, num_sms));
@@ -503,8 +515,7 @@ cudaError_t sb2st(double* AB, int ldab, int n, int b, double* d, double* e, doub
     int ts0 = want_trace ? std::atoi(tenv) : 0;
     ts0 = std::max(0, std::min(ts0, n - 4));
     cudaMemcpyToSymbolAsync(c_sb_trace_s0, &ts0, sizeof(int), 0, cudaMemcpyHostToDevice, s);
-    static const int sb_mode = std::getenv("BSE_SB2ST_MODE") ? std::atoi(std::getenv("BSE_SB2ST_MODE")) : 0;
-    cudaMemcpyToSymbolAsync(c_sb_mode, &sb_mode, sizeof(int), 0, cudaMemcpyHostToDevice, s);
+    if (sb_mode) cudaMemcpyToSymbolAsync(c_sb_mode, &sb_mode, sizeof(int), 0, cudaMemcpyHostToDevice, s);
     const size_t tsz = (size_t)2 * maxsteps * 16;
     if (want_trace) {
       cudaMalloc(&trace, sizeof(unsigned long long) * tsz);
@@ -512,7 +523,9 @@ cudaError_t sb2st(double* AB, int ldab, int n, int b, double* d, double* e, doub
     }
     void* args[] = {&AB, &ldab, &n, &b, &V2, &tau2, &maxsteps, &progress, &trace};
     count_launch();
-    err = cudaLaunchCooperativeKernel((const void*)sb2st_fused_kernel, dim3(grid), dim3(kSbThreads),
+    err = cudaLaunchCooperativeKernel(sb_mode ? (const void*)sb2st_fused_kernel<true>
+                                              : (const void*)sb2st_fused_kernel<false>,
+                                      dim3(grid), dim3(kSbThreads),
                                       args, smem, s);
     if (err != cudaSuccess) return err;
     if (want_trace) {
