@@ -732,6 +732,10 @@ def run_ours_bc(args):
                                                    bc_workspace_bytes)
 
     rank, local_rank, world = env_rank()
+    os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+    os.environ.setdefault("MASTER_PORT", "29517")
+    os.environ.setdefault("RANK", str(rank))
+    os.environ.setdefault("WORLD_SIZE", str(world))
     ndev = torch.cuda.device_count()
     transport = args.transport or ("nccl" if ndev >= world else "host")
     dev_index = local_rank % max(ndev, 1)
@@ -949,6 +953,8 @@ def main():
     ap.add_argument("--transport", choices=["nccl", "host"], default=None,
                     help="N > 1: nccl (default when every rank has its own GPU) or the "
                          "host-staged transport (ranks may share a GPU)")
+    ap.add_argument("--bc", action="store_true",
+                    help="run the memory-distributed solve even at N = 1 (one rank owning every tile)")
     ap.add_argument("--replicated", action="store_true",
                     help="N > 1: the round-1 column-sharded solve with replicated operands")
     ap.add_argument("--config", type=int, default=2, choices=[1, 2, 3],
@@ -971,7 +977,7 @@ def main():
         return run_ours_complex(args)
     if args.n is None:
         args.n = 16384
-    if env_rank()[2] > 1 and not args.replicated:
+    if (env_rank()[2] > 1 and not args.replicated) or args.bc:
         return run_ours_bc(args)
     return run_ours(args)
 

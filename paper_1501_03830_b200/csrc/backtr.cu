@@ -511,7 +511,7 @@ cudaError_t q1_group_build(int k, int b, int m, const double* V, long long ldv, 
   if (k > 1) {
     GemmProblem gx = make_gemm(kb, kb, m, 1.0, V, ldv, V, ldv, 0.0, w.x, kb);
     gx.mc = Mask::strict_upper();  // covers every block above the diagonal blocks
-    if (w.oz_side && (double)kb * kb * m >= kOzMinWork)
+    if (w.oz_side && (double)kb * kb * m >= oz_min_work())
       e = ozgemm(true, false, gx, w.oz_side, w.oz_side_bytes, kQ1OzChunk, s);
     else
       e = gemm(true, false, gx, s);
@@ -537,7 +537,7 @@ cudaError_t q1_group_build(int k, int b, int m, const double* V, long long ldv, 
     // products instead of three
     GemmProblem gv = make_gemm(m, kb, kb, 1.0, V, ldv, Tg, kb, 0.0, VT, m);
     gv.mb = Mask::upper();
-    if (w.oz_side && (double)m * kb * kb >= kOzMinWork)
+    if (w.oz_side && (double)m * kb * kb >= oz_min_work())
       e = ozgemm(false, false, gv, w.oz_side, w.oz_side_bytes, kQ1OzChunk, s);
     else
       e = gemm(false, false, gv, s);
@@ -554,7 +554,7 @@ cudaError_t q1_group_apply(int kb, int m, const double* V, long long ldv, const 
   // one product on the INT8 engine when it is large enough to pay for the
   // slicing and reconstruction passes
   auto mul = [&](bool ta, const GemmProblem& g) {
-    if (w.oz && (double)g.M * g.N * g.K >= kOzMinWork)
+    if (w.oz && (double)g.M * g.N * g.K >= oz_min_work())
       return ozgemm(ta, false, g, w.oz, w.oz_bytes, kQ1OzChunk, s);
     return gemm(ta, false, g, s);
   };

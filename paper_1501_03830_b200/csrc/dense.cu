@@ -2,6 +2,7 @@
 // GEMM.  Recursion halves the problem so every off-diagonal update is one
 // large GEMM (the blocked right-looking counterpart of the reference's
 // left-looking GEMV loop, kernels.py:43-65).
+#include <cstdlib>
 #include "dense.cuh"
 #include "ozgemm.cuh"
 
@@ -269,7 +270,7 @@ size_t potrf_inv_cache_doubles(int n) { return (size_t)ceil_div(n, kLeaf) * kLea
 // C-block update on the emulated-FP64 engine when it is given and the
 // product is large enough, else on the DMMA engine
 static cudaError_t update(bool ta, bool tb, const GemmProblem& p, const OzWork* oz, cudaStream_t s) {
-  if (oz && oz->p && (double)p.M * p.N * p.K >= kOzMinWork)
+  if (oz && oz->p && (double)p.M * p.N * p.K >= oz_min_work())
     return ozgemm(ta, tb, p, oz->p, oz->bytes, oz->chunk, s);
   return gemm(ta, tb, p, s);
 }
@@ -401,23 +402,15 @@ static cudaError_t potrf_rec(double* A, long long lda, int n, int off, DevStatus
   // A22 -= A21 A21^T (lower triangle only)
   double* A21 = A + n1;
   double* A22 = A + n1 + n1 * lda;
-  if (oz && oz->p && (double)n2 * n2 * n1 >= 4.0 * kOzMinWork) {
-    // the emulated engine cannot skip the upper triangle: 2 x 2 output blocks
-    // (two lower-masked diagonal blocks + one full block) do 3/4 of the work
-    const int h = ((n2 / 2 + kLeaf - 1) / kLeaf) * kLeaf, h2 = n2 - h;
-    GemmProblem c11 = make_gemm(h, h, n1, -1.0, A21, lda, A21, lda, 1.0, A22, lda);
-    c11.mc = Mask::lower();
-    GemmProblem c21 = make_gemm(h2, h, n1, -1.0, A21 + h, lda, A21, lda, 1.0, A22 + h, lda);
-    GemmProblem c22 = make_gemm(h2, h2, n1, -1.0, A21 + h, lda, A21 + h, lda, 1.0,
-                                A22 + h + (long long)h * lda, lda);
-    c22.mc = Mask::lower();
-    if ((e = update(false, true, c11, oz, s)) != cudaSuccess) return e;
-    if ((e = update(false, true, c21, oz, s)) != cudaSuccess) return e;
-    if ((e = update(false, true, c22, oz, s)) != cudaSuccess) return e;
-  } else {
+  {
+    // lower triangle only: the DMMA engine skips masked tiles, and so does the
+    // emulated engine's contraction kernel (256-wide tiles above the diagonal
+    // are never issued; the CRT pass skips masked entries)
     GemmProblem p = make_gemm(n2, n2, n1, -1.0, A21, lda, A21, lda, 1.0, A22, lda);
     p.mc = Mask::lower();
-    if ((e = update(false, true, p, oz, s)) != cudaSuccess) return e;
+    static const bool half_rule = std::getenv("BSE_POTRF_OZ_OLD") == nullptr;
+    const bool big = (double)n2 * n2 * n1 >= (half_rule ? 2.0 : 4.0) * oz_min_work();
+    if ((e = big ? update(false, true, p, oz, s) : gemm(false, true, p, s)) != cudaSuccess) return e;
   }
   return potrf_rec(A + n1 + n1 * lda, lda, n2, off + n1, st, s,
                    inv ? inv + (size_t)(n1 / kLeaf) * kLeaf * kLeaf : nullptr, oz);

@@ -421,6 +421,14 @@ cudaError_t init_const() {
 
 }  // namespace
 
+double oz_min_work() {
+  static const double v = [] {
+    const char* e = std::getenv("BSE_OZ_MIN_WORK_LOG2");
+    return std::ldexp(1.0, e ? std::atoi(e) : 34);
+  }();
+  return v;
+}
+
 int oz_set_engine(int engine) {
   const int prev = oz_engine();
   if (engine >= 0 && engine <= 2) g_oz_engine.store(engine, std::memory_order_relaxed);

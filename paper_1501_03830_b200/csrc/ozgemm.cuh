@@ -21,6 +21,9 @@ cudaError_t ozgemm(bool transA, bool transB, const GemmProblem& p, void* work, s
 int oz_set_engine(int engine);
 
 // Products at least this large (M N K) go to the emulated engine.
-constexpr double kOzMinWork = 1024.0 * 1024.0 * 1024.0 * 64.0;
+// (2^34 by default -- retuned in round 2 for the byte-plane CRT and the
+// tile-skipping contraction kernel: 2^36 -> 2^34 is worth 8-10 ms of the cfg2
+// solve; BSE_OZ_MIN_WORK_LOG2 overrides it for tuning)
+double oz_min_work();
 
 }  // namespace bse

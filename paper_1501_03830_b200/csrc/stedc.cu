@@ -728,10 +728,12 @@ cudaError_t stedc(int n, double* d, double* e, double* wout, double* Q, long lon
       count_launch();
       if ((err = cudaGetLastError()) != cudaSuccess) return err;
       stage_mark("dc_gemm", s);
-      if (ws.oz && L.nnodes <= 2 && (double)L.half * L.half * maxm >= kOzMinWork) {
+      static const int oz_nodes =
+          std::getenv("BSE_DC_OZ_NODES") ? std::min(8, std::atoi(std::getenv("BSE_DC_OZ_NODES"))) : 2;
+      if (ws.oz && L.nnodes <= oz_nodes && (double)L.half * L.half * maxm >= oz_min_work()) {
         // top merges: the problem shapes come back to the host (one sync per
         // level) and the large products run on the emulated-FP64 engine
-        GemmProblem hp[4];
+        GemmProblem hp[16];
         if ((err = cudaMemcpyAsync(hp, ws.probs, sizeof(GemmProblem) * 2 * L.nnodes,
                                    cudaMemcpyDeviceToHost, s)) != cudaSuccess)
           return err;
@@ -739,7 +741,7 @@ cudaError_t stedc(int n, double* d, double* e, double* wout, double* Q, long lon
         for (int q = 0; q < 2 * L.nnodes; ++q) {
           const GemmProblem& p = hp[q];
           if (p.M <= 0 || p.N <= 0) continue;
-          err = (double)p.M * p.N * p.K >= kOzMinWork
+          err = (double)p.M * p.N * p.K >= oz_min_work()
                     ? ozgemm(false, false, p, ws.oz, ws.oz_bytes, 2048, s)
                     : gemm(false, false, p, s);
           if (err != cudaSuccess) return err;
