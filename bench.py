@@ -412,6 +412,7 @@ def run_ours(args):
     torch.cuda.set_device(local_rank)
     dev = torch.device("cuda", local_rank)
     if world > 1:
+        os.environ.setdefault("NCCL_DEBUG_FILE", "/dev/stderr")  # stdout carries the JSON line only
         dist.init_process_group("nccl", device_id=dev)
     lib = _lib.load(strict=True)
     n = args.n
@@ -732,6 +733,7 @@ def run_ours_bc(args):
                                                    bc_workspace_bytes)
 
     rank, local_rank, world = env_rank()
+    os.environ.setdefault("NCCL_DEBUG_FILE", "/dev/stderr")  # stdout carries the JSON line only
     os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
     os.environ.setdefault("MASTER_PORT", "29517")
     os.environ.setdefault("RANK", str(rank))

@@ -19,7 +19,28 @@ constexpr int kQ2Group = 32;
 constexpr int kQ2RangeGroups = 64;  // sweep groups per Q2 block range (even)
 constexpr int kQ1Cols = 4096;       // columns of V per Q1 group on the emulated engine
 
+constexpr int kDistOzChunk = 2048;   // output columns per emulated-engine pass
+
 int q1_group_tiles(int nb, bool oz) { return oz ? std::max(1, kQ1Cols / nb) : 1; }
+
+// Large products of the distributed stages go to the emulated-FP64 engine
+// (same rule as the single-GPU pipeline: at least oz_min_work multiply-adds
+// and a workspace that holds the call), the rest to the DMMA engine.
+struct OzBuf {
+  void* p = nullptr;
+  size_t bytes = 0;
+};
+cudaError_t mm(bool ta, bool tb, const GemmProblem& g, const OzBuf& oz, cudaStream_t s) {
+  if (g.M <= 0 || g.N <= 0) return cudaSuccess;
+  if (oz.p && g.K > 0 && (double)g.M * g.N * g.K >= oz_min_work() &&
+      ozgemm_bytes(g.M, g.N, g.K, kDistOzChunk) <= oz.bytes)
+    return ozgemm(ta, tb, g, oz.p, oz.bytes, kDistOzChunk, s);
+  return gemm(ta, tb, g, s);
+}
+// workspace for every panel product of shape (n x cols x nb) or (nb x cols x n)
+size_t panel_oz_bytes(int n, int nb, int cols) {
+  return std::max(ozgemm_bytes(n, cols, nb, kDistOzChunk), ozgemm_bytes(nb, cols, n, kDistOzChunk));
+}
 bool dist_oz(int n, int flags) { return !(flags & kFlagNativeFp64) && n >= kOzMinN; }
 
 // ---------------------------------------------------------------------------
@@ -209,7 +230,7 @@ struct DistWork {
 };
 
 // scratch layouts of the phases (dry arenas give the sizes)
-struct PhaseA { double* P; };                       // Cholesky, congruence, recovery panels
+struct PhaseA { double* P; OzBuf oz; };                       // Cholesky, congruence, recovery panels
 struct PhaseB {                                     // SY2SB
   double* TVW;   // [T (b^2) | V (ldv b) | W (ldv b)]
   double* WV;    // [W | V]
@@ -221,11 +242,15 @@ struct PhaseD { StedcWork dc; double* Zrow; long long ldzr; };
 struct PhaseE1 { double* TB; };
 struct PhaseE2 { double* Vblk; };
 struct PhaseE3 { double* Vg; double* Tg; Q1Scratch q1; };
-struct PhaseE4 { double* P; double* Bu; double* Bv; };
+struct PhaseE4 { double* P; double* Bu; double* Bv; OzBuf oz; };
 
-PhaseA carve_a(Arena& a, int n, int nb) {
+PhaseA carve_a(Arena& a, int n, int nb, int nlmax = 0, bool oz = false) {
   PhaseA p{};
   p.P = a.take<double>((size_t)pad_ld(n) * nb);
+  if (oz && nlmax > 0) {
+    p.oz.bytes = panel_oz_bytes(n, nb, nlmax);
+    p.oz.p = a.take<char>(p.oz.bytes);
+  }
   return p;
 }
 
@@ -251,9 +276,14 @@ PhaseB carve_b(Arena& a, int n, int nb, int ntl) {
   return p;
 }
 
-PhaseD carve_d(Arena& a, int n, int nrmax, int ucols) {
+PhaseD carve_d(Arena& a, int n, int nrmax, int ucols, bool oz = false) {
   PhaseD p{};
   p.dc = stedc_carve(a, n, nrmax, ucols);
+  if (oz) {
+    // top merges on the emulated engine: (rows of this rank) x (U chunk) x n/2
+    p.dc.oz_bytes = ozgemm_bytes(std::max(nrmax, 1), p.dc.ucols, (n + 1) / 2, 2048);
+    p.dc.oz = a.take<char>(p.dc.oz_bytes);
+  }
   p.ldzr = pad_ld(nrmax);
   p.Zrow = a.take<double>((size_t)p.ldzr * n);
   return p;
@@ -293,12 +323,16 @@ PhaseE3 carve_e3(Arena& a, int n, int nb, int nlmax, bool oz) {
   return p;
 }
 
-PhaseE4 carve_e4(Arena& a, int n, int nb, int nlmax) {
+PhaseE4 carve_e4(Arena& a, int n, int nb, int nlmax, bool oz = false) {
   PhaseE4 p{};
   const long long ld = pad_ld(n);
   p.P = a.take<double>((size_t)ld * nb);
   p.Bu = a.take<double>((size_t)ld * std::max(nlmax, 1));
   p.Bv = a.take<double>((size_t)ld * std::max(nlmax, 1));
+  if (oz && nlmax > 0) {
+    p.oz.bytes = panel_oz_bytes(n, nb, nlmax);
+    p.oz.p = a.take<char>(p.oz.bytes);
+  }
   return p;
 }
 
@@ -345,15 +379,15 @@ DistWork carve_dist(Arena& a, const BcLayout& lay, int flags) {
   int ntlmax = 0;
   for (int r = 0; r < world; ++r) ntlmax = std::max(ntlmax, lay.ntiles_of(r));
   size_t sb = 0;
-  sb = std::max(sb, dry_bytes([&](Arena& x) { carve_a(x, n, lay.nb); }));
+  sb = std::max(sb, dry_bytes([&](Arena& x) { carve_a(x, n, lay.nb, w.nlmax, oz); }));
   sb = std::max(sb, dry_bytes([&](Arena& x) { carve_b(x, n, lay.nb, ntlmax); }));
   sb = std::max(sb, dry_bytes([&](Arena& x) {
-    carve_d(x, n, w.nrmax, w.nlmax);
+    carve_d(x, n, w.nrmax, w.nlmax, oz);
     carve_e1(x, n, w.nrmax);  // the transposition reads Zrow (phase D) through TB
   }));
   sb = std::max(sb, dry_bytes([&](Arena& x) { carve_e2(x, n); }));
   sb = std::max(sb, dry_bytes([&](Arena& x) { carve_e3(x, n, lay.nb, w.nlmax, oz); }));
-  sb = std::max(sb, dry_bytes([&](Arena& x) { carve_e4(x, n, lay.nb, w.nlmax); }));
+  sb = std::max(sb, dry_bytes([&](Arena& x) { carve_e4(x, n, lay.nb, w.nlmax, oz); }));
   w.scratch_bytes = sb + 4096;
   w.scratch = a.take<char>(w.scratch_bytes);
   return w;
@@ -422,7 +456,7 @@ cudaError_t reduce_status(Comm& comm, const BcLayout& lay, const DevStatus* st, 
 // to rows >= k and stril(M_k)^T L to rows of tile k), then W[i, :] = L_i^T T1.
 cudaError_t congruence_bc(Comm& comm, const BcLayout& lay, const double* M, long long ldm,
                           const double* L, double* T1, double* W, long long ld, int nloc,
-                          double* P, cudaStream_t s) {
+                          double* P, const OzBuf& oz, cudaStream_t s) {
   const int T = lay.ntiles(), n = lay.n, nb = lay.nb;
   if (nloc > 0) BSE_TRY(cudaMemsetAsync(T1, 0, sizeof(double) * ld * nloc, s));
   for (int k = 0; k < T; ++k) {
@@ -435,10 +469,10 @@ cudaError_t congruence_bc(Comm& comm, const BcLayout& lay, const double* M, long
     if (nc == 0) continue;
     GemmProblem ga = make_gemm(m, nc, kb, 1.0, P, ldp, L + r0, ld, 1.0, T1 + r0, ld);
     ga.ma = Mask::lower();
-    BSE_TRY(gemm(false, false, ga, s));
+    BSE_TRY(mm(false, false, ga, oz, s));
     GemmProblem gb = make_gemm(kb, nc, m, 1.0, P, ldp, L + r0, ld, 1.0, T1 + r0, ld);
     gb.ma = Mask::strict_lower();
-    BSE_TRY(gemm(true, false, gb, s));
+    BSE_TRY(mm(true, false, gb, oz, s));
   }
   if (nloc > 0) BSE_TRY(cudaMemsetAsync(W, 0, sizeof(double) * ld * nloc, s));
   for (int i = 0; i < T; ++i) {
@@ -451,7 +485,7 @@ cudaError_t congruence_bc(Comm& comm, const BcLayout& lay, const double* M, long
     if (nc == 0) continue;
     GemmProblem g = make_gemm(ib, nc, m, 1.0, P, ldp, T1 + r0, ld, 0.0, W + r0, ld);
     g.ma = Mask::lower();
-    BSE_TRY(gemm(true, false, g, s));
+    BSE_TRY(mm(true, false, g, oz, s));
   }
   return cudaSuccess;
 }
@@ -567,7 +601,7 @@ cudaError_t solve_spd_pair_bc(Comm& comm, int n, int nb, const double* Mloc, lon
   stage_mark("potrf", s);
   {
     Arena sa = scratch();
-    PhaseA pa = carve_a(sa, n, nb);
+    PhaseA pa = carve_a(sa, n, nb, w.nlmax, oz);
     if (nloc > 0) {
       copy_lower_bc_kernel<<<blocks_for((long long)n * nloc), 256, 0, s>>>(lay, nloc, Kloc, ldk, w.L, ld);
       count_launch();
@@ -595,7 +629,7 @@ cudaError_t solve_spd_pair_bc(Comm& comm, int n, int nb, const double* Mloc, lon
     }
     // 2. W = L^T M L
     stage_mark("congruence", s);
-    BSE_TRY(congruence_bc(comm, lay, Mloc, ldm, w.L, w.TV, w.WZ, ld, nloc, pa.P, s));
+    BSE_TRY(congruence_bc(comm, lay, Mloc, ldm, w.L, w.TV, w.WZ, ld, nloc, pa.P, pa.oz, s));
   }
   // 3a. full -> band
   stage_mark("sy2sb", s);
@@ -621,7 +655,7 @@ cudaError_t solve_spd_pair_bc(Comm& comm, int n, int nb, const double* Mloc, lon
     long long r0, r1;
     shard_range(n, world, lay.rank, &r0, &r1);
     Arena sa = scratch();
-    PhaseD pd = carve_d(sa, n, w.nrmax, w.nlmax);
+    PhaseD pd = carve_d(sa, n, w.nrmax, w.nlmax, oz);
     PhaseE1 pe = carve_e1(sa, n, w.nrmax);
     if (!pe.TB) return cudaErrorMemoryAllocation;
     pd.dc.row0 = (int)r0;
@@ -693,7 +727,7 @@ cudaError_t solve_spd_pair_bc(Comm& comm, int n, int nb, const double* Mloc, lon
   stage_mark("recover", s);
   {
     Arena sa = scratch();
-    PhaseE4 pe = carve_e4(sa, n, nb, w.nlmax);
+    PhaseE4 pe = carve_e4(sa, n, nb, w.nlmax, oz);
     const int T = lay.ntiles();
     if (nloc > 0) {
       BSE_TRY(cudaMemsetAsync(pe.Bu, 0, sizeof(double) * ld * nloc, s));
@@ -710,11 +744,11 @@ cudaError_t solve_spd_pair_bc(Comm& comm, int n, int nb, const double* Mloc, lon
       if (nloc == 0) continue;
       GemmProblem gu = make_gemm(m, nloc, kb, 1.0, pe.P, ldp, w.WZ + r0, ld, 1.0, pe.Bu + r0, ld);
       gu.ma = Mask::lower();
-      BSE_TRY(gemm(false, false, gu, s));
+      BSE_TRY(mm(false, false, gu, pe.oz, s));
       if (m > kb) {
         GemmProblem gv = make_gemm(kb, nloc, m - kb, -1.0, pe.P + kb, ldp, pe.Bv + r0 + kb, ld, 1.0,
                                    pe.Bv + r0, ld);
-        BSE_TRY(gemm(true, false, gv, s));
+        BSE_TRY(mm(true, false, gv, pe.oz, s));
       }
       BSE_TRY(trsm_llt(pe.P, ldp, kb, pe.Bv + r0, ld, nloc, s));
     }
