@@ -373,7 +373,7 @@ DistWork carve_dist(Arena& a, const BcLayout& lay, int flags) {
   const int maxsteps = sb2st_maxsteps(n, b);
   w.V2 = a.take<double>((size_t)n * maxsteps * b);
   w.tau2 = a.take<double>((size_t)n * maxsteps);
-  w.progress = a.take<int>(2 * (size_t)n);
+  w.progress = a.take<int>(sb2st_progress_ints(n, b));  // sweep counters + hand-off mailboxes (sb2st)
   w.replicated = a.used - rep0;
   const bool oz = dist_oz(n, flags);
   int ntlmax = 0;

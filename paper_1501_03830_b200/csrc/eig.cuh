@@ -46,6 +46,8 @@ cudaError_t panel_w(int m, int bw, const double* V, long long ldv, const double*
 // Bulge chasing on the band (lower storage, ldab = 2b + 1): d, e out; reflectors
 // of sweep s, step j stored at V2[(s*maxsteps + j) * b], tau2[s*maxsteps + j].
 int sb2st_maxsteps(int n, int b);
+// ints behind `progress`: two counters per sweep + the hand-off mailbox ring
+size_t sb2st_progress_ints(int n, int b);
 cudaError_t sb2st(double* AB, int ldab, int n, int b, double* d, double* e, double* V2,
                   double* tau2, int* progress, int num_sms, cudaStream_t s);
 

@@ -106,7 +106,7 @@ SyevdWork carve_syevd(Arena& a, int n, int flags) {
   const int maxsteps = sb2st_maxsteps(n, b);
   w.V2 = a.take<double>((size_t)n * maxsteps * b);
   w.tau2 = a.take<double>((size_t)n * maxsteps);
-  w.progress = a.take<int>(2 * (size_t)n);  // full + late counters (sb2st)
+  w.progress = a.take<int>(sb2st_progress_ints(n, b));  // sweep counters + hand-off mailboxes (sb2st)
   const size_t qb = q2_block_doubles(n, b, kQ2Group);
   w.Vblk = a.take<double>(qb);
   const bool oz = !(flags & kFlagNativeFp64) && !(flags & 0x1) && n >= kOzMinN;

@@ -50,9 +50,47 @@ BSE_DEV unsigned long long gtimer() {
 // 16-byte accesses on rows with (q0 + r) even.  Shared blocks use an even
 // leading dimension (66) shifted by q0 & 1 so the parities line up, and the
 // matvec index patterns below are bank-conflict free for that stride.
+//
+// Hand-off mailboxes.  The late data of a step (b + 1 doubles) does not travel
+// through the band and a release/acquire counter (store, fence, flag, poll,
+// fence, load: two dependent L2 round trips plus two fences on the chain
+// that paces the whole wavefront) but through a per-(sweep, step) mailbox of
+// self-validating 16-byte slots {bits, bits ^ tag(sweep, step)}: the
+// producer's warp 0 stores them without any fence, the consumer's threads
+// poll their own slot until the two halves agree with the tag.  Each 8-byte
+// half is written atomically, so a torn or stale slot never validates (tags
+// are 64-bit hashes, unique per call; the ring is cleared per call).  Values
+// handed over this way are NOT written to the band by the producer: the
+// consumer's own bulk store rewrites exactly those positions (row lq - 1 of
+// its blocks), so no store of the producer can race with it.  Steps without
+// a consumer (step 0, the last sweep) publish to the band as before; a
+// consumer whose predecessor has no step j + 1 waits for the predecessor to
+// finish (`late` == kDone) and reads the band.
 constexpr int kLd2 = 66;
 constexpr int kPairSlots = 34;  // 16-byte row-pair slots per column (33 used)
 constexpr int kBulkWarps = kSbThreads / 32;  // every warp stores part of the bulk
+constexpr int kMailSlots = kMaxPanel + 2;    // slot 0: O(0, 0); 1..lp-1: O(0, c); lp: D(0, 0)
+constexpr int kMailRing = 160;               // sweeps (> resident CTAs + 1)
+constexpr int kSbMaxGrid = kMailRing - 4;
+
+BSE_DEV unsigned long long mail_tag(int s, int j) {
+  unsigned long long x = ((unsigned long long)(unsigned)s << 24) ^ (unsigned long long)(unsigned)j;
+  x += 0x9e3779b97f4a7c15ull;
+  x = (x ^ (x >> 30)) * 0xbf58476d1ce4e5b9ull;
+  x = (x ^ (x >> 27)) * 0x94d049bb133111ebull;
+  return (x ^ (x >> 31)) | 1ull;
+}
+BSE_DEV void mail_put(unsigned long long* slot, double v, unsigned long long tag) {
+  const unsigned long long bits = (unsigned long long)__double_as_longlong(v);
+  asm volatile("st.global.v2.u64 [%0], {%1, %2};\n" ::"l"(slot), "l"(bits), "l"(bits ^ tag) : "memory");
+}
+BSE_DEV double mail_get(const unsigned long long* slot, unsigned long long tag) {
+  unsigned long long lo, hi;
+  do {
+    asm volatile("ld.relaxed.gpu.global.v2.u64 {%0, %1}, [%2];\n" : "=l"(lo), "=l"(hi) : "l"(slot) : "memory");
+  } while ((lo ^ hi) != tag);
+  return __longlong_as_double((long long)lo);
+}
 
 struct SbfSmem {
   double D[2][kMaxPanel * kLd2 + 2];  // double-buffered: step j+1 stages while j computes
@@ -170,17 +208,6 @@ BSE_DEV void stage_bulk(double* Db, double* Ob, const double* AB, int ldab, int 
   }
 }
 
-// D's strict upper triangle from the lower one (except the late row lq - 1).
-BSE_DEV void mirror_d(double* Db, int lq) {
-  const int rl = lq - 1;
-#pragma unroll 4
-  for (int k = 0; k < kSlots; ++k) {
-    const int idx = threadIdx.x + k * kSbThreads;
-    const int r = idx & (kMaxPanel - 1), c = idx >> 6;
-    if (r < c && c != rl) Db[c * kLd2 + r] = Db[r * kLd2 + c];
-  }
-}
-
 // The late positions (D's last row and O(lq-1, lp-1)), after the late wait.
 //
 // One more position of a FULL block's last row is not covered by the two
@@ -199,9 +226,7 @@ BSE_DEV void late_load(double* Db, double* Ob, const double* AB, int ldab, int q
   const int tid = threadIdx.x, rl = lq - 1;
   if (tid < kMaxPanel) {
     const int c = tid;
-    const double x = c <= rl ? __ldcg(AB + (long long)(q0 + c) * ldab + (rl - c)) : 0.0;
-    Db[c * kLd2 + rl] = x;
-    Db[rl * kLd2 + c] = x;
+    if (c <= rl) Db[c * kLd2 + rl] = __ldcg(AB + (long long)(q0 + c) * ldab + (rl - c));
   } else if (tid == kMaxPanel) {
     Ob[(lp - 1) * kLd2 + rl] = __ldcg(AB + (long long)(p0 + lp - 1) * ldab + (q0 + rl - p0 - lp + 1));
   } else if (tid == kMaxPanel + 1) {
@@ -220,6 +245,7 @@ template <bool kDiag>
 __global__ void __launch_bounds__(kSbThreads) sb2st_fused_kernel(double* AB, int ldab, int n,
                                                                  int b, double* V2, double* tau2,
                                                                  int maxsteps, int* progress,
+                                                                 unsigned long long* mail,
                                                                  unsigned long long* trace) {
   extern __shared__ __align__(16) unsigned char raw[];
   SbfSmem& sm = *reinterpret_cast<SbfSmem*>(raw);
@@ -260,13 +286,30 @@ __global__ void __launch_bounds__(kSbThreads) sb2st_fused_kernel(double* AB, int
       if (trs) T(0);
       // late wait, overlapping the arrival of this step's staged bulk; then
       // mirror D and load the late row (disjoint positions, one barrier)
-      if (has_pred && tid == 0) poll_counter<kDiag>(late + s - 1, j + 2);
+      // the predecessor has a step j + 1 exactly when this block is full
+      const bool mailed = has_pred && lq == b;
+      double lx = 0.0;
+      if (mailed) {
+        const unsigned long long* box =
+            mail + ((size_t)((s - 1) % kMailRing) * maxsteps + (j + 1)) * (2 * kMailSlots);
+        const unsigned long long tag = mail_tag(s - 1, j + 1);
+        if (tid < b) lx = mail_get(box + 2 * (tid + 1), tag);          // D(lq-1, tid)
+        else if (tid == kMaxPanel) lx = mail_get(box, tag);            // O(lq-1, lp-1)
+      } else if (has_pred && tid == 0) {
+        poll_counter<kDiag>(late + s - 1, kDone);
+      }
       if (tid == 0) dbg_delay<kDiag>(32, s, j);
       cp_async_wait<0>();
       __syncthreads();
       if (trs) T(1);
-      mirror_d(Db, lq);
-      late_load(Db, Ob, AB, ldab, q0, lq, p0, lp, b);
+      if (mailed) {
+        const int rl = lq - 1;
+        if (tid < b) Db[tid * kLd2 + rl] = lx;
+        else if (tid == kMaxPanel) Ob[(lp - 1) * kLd2 + rl] = lx;
+        else if (tid == kMaxPanel + 1 && lp >= 2) Ob[(lp - 2) * kLd2 + rl] = 0.0;
+      } else {
+        late_load(Db, Ob, AB, ldab, q0, lq, p0, lp, b);
+      }
       __syncthreads();
       if (trs) T(2);
       // A: w = tau O v
@@ -309,14 +352,22 @@ __global__ void __launch_bounds__(kSbThreads) sb2st_fused_kernel(double* AB, int
       }
       // C: t = taun D vn, y = taun (O^T vn - v swv)
       {
-        double tc = 0.0, gc = 0.0;
+        // D holds its lower triangle only: column mi from the diagonal down
+        // (this phase's pattern) plus row mi left of the diagonal (phase A's
+        // pattern) -- both conflict-free, no mirrored copy needed
+        double tc = 0.0, gc = 0.0, ta = 0.0;
 #pragma unroll
         for (int i = 0; i < 16; ++i) {
           const int r = rowC(q, i);
           const double vr = vn[r];
-          tc += Db[mi * kLd2 + r] * vr;
+          const double dl = r >= mi ? Db[mi * kLd2 + r] : 0.0;
+          tc += dl * vr;
           gc += Ob[mi * kLd2 + r] * vr;
+          const int c = colA(q, i);
+          const double du = c < mi ? Db[c * kLd2 + mi] : 0.0;
+          ta += du * vn[c];
         }
+        tc += ta;
         tc += __shfl_xor_sync(0xffffffffu, tc, 1);
         tc += __shfl_xor_sync(0xffffffffu, tc, 2);
         gc += __shfl_xor_sync(0xffffffffu, gc, 1);
@@ -338,20 +389,25 @@ __global__ void __launch_bounds__(kSbThreads) sb2st_fused_kernel(double* AB, int
       if (warp == 0) {
         if (lane == 0) dbg_delay<kDiag>(4, s, j);
         __syncwarp();
-        // publish the successor's late data: row 0 of O'' and D''(0, 0)
+        // the successor's late data: row 0 of O'' and D''(0, 0) -- into the
+        // mailbox when sweep s + 1 has a step j - 1 to consume it, else into
+        // the band (ordered by this warp's `full` arrival below)
+        const bool tomail = j >= 1 && s + 1 <= n - 3;
+        unsigned long long* box = mail + ((size_t)(s % kMailRing) * maxsteps + j) * (2 * kMailSlots);
+        const unsigned long long tag = mail_tag(s, j);
 #pragma unroll
         for (int h = 0; h < 2; ++h) {
           const int c = lane + 32 * h;
           if (c < lp) {
             const double val = c == 0 ? betan : Ob[c * kLd2] - sm.w[0] * v[c] - sm.y[c];
-            AB[(long long)(p0 + c) * ldab + (q0 - p0 - c)] = val;
+            if (tomail) mail_put(box + 2 * c, val, tag);
+            else AB[(long long)(p0 + c) * ldab + (q0 - p0 - c)] = val;
           }
         }
-        if (lane == 0) AB[(long long)q0 * ldab] = Db[0] - 2.0 * (sm.tt[0] + al);
-        __syncwarp();
         if (lane == 0) {
-          __threadfence();
-          st_release(late + s, j + 1);
+          const double val = Db[0] - 2.0 * (sm.tt[0] + al);
+          if (tomail) mail_put(box + 2 * lp, val, tag);
+          else AB[(long long)q0 * ldab] = val;
           if (trs) T(4);
         }
       }
@@ -493,12 +549,22 @@ __global__ void band_to_tridiag_kernel(const double* AB, int ldab, int n, double
 
 int sb2st_maxsteps(int n, int b) { return (int)ceil_div(n, b) + 1; }
 
+static size_t mail_offset_ints(int n) { return ((2 * (size_t)n + 3) / 4) * 4; }
+
+size_t sb2st_progress_ints(int n, int b) {
+  const size_t sweeps = (size_t)std::min(std::max(n, 1), kMailRing);
+  return mail_offset_ints(n) + sweeps * sb2st_maxsteps(n, b) * kMailSlots * 4;
+}
+
 cudaError_t sb2st(double* AB, int ldab, int n, int b, double* d, double* e, double* V2,
                   double* tau2, int* progress, int num_sms, cudaStream_t s) {
   if (n <= 0) return cudaSuccess;
   cudaError_t err;
   if (n > 2) {
-    if ((err = cudaMemsetAsync(progress, 0, sizeof(int) * 2 * (size_t)n, s)) != cudaSuccess) return err;
+    if ((err = cudaMemsetAsync(progress, 0, sizeof(int) * sb2st_progress_ints(n, b), s)) != cudaSuccess)
+      return err;
+    // mailboxes: 16-byte aligned, behind the 2n counters
+    unsigned long long* mail = reinterpret_cast<unsigned long long*>(progress + mail_offset_ints(n));
     const size_t smem = sizeof(SbfSmem);
     static PerDeviceOnce attr, attr_diag;
     static const int sb_mode = std::getenv("BSE_SB2ST_MODE") ? std::atoi(std::getenv("BSE_SB2ST_MODE")) : 0;
@@ -507,7 +573,7 @@ cudaError_t sb2st(double* AB, int ldab, int n, int b, double* d, double* e, doub
       return err;
     // one CTA per SM: the kernel is latency-bound and one resident step per
     // SM keeps every hand-off on an otherwise idle SM
-    const int grid = std::max(1, std::min(n - 2, num_sms));
+    const int grid = std::max(1, std::min(n - 2, std::min(num_sms, kSbMaxGrid)));
     int maxsteps = sb2st_maxsteps(n, b);
     unsigned long long* trace = nullptr;
     const char* tenv = std::getenv("BSE_SB2ST_TRACE");
@@ -521,7 +587,7 @@ cudaError_t sb2st(double* AB, int ldab, int n, int b, double* d, double* e, doub
       cudaMalloc(&trace, sizeof(unsigned long long) * tsz);
       cudaMemsetAsync(trace, 0, sizeof(unsigned long long) * tsz, s);
     }
-    void* args[] = {&AB, &ldab, &n, &b, &V2, &tau2, &maxsteps, &progress, &trace};
+    void* args[] = {&AB, &ldab, &n, &b, &V2, &tau2, &maxsteps, &progress, &mail, &trace};
     count_launch();
     err = cudaLaunchCooperativeKernel(sb_mode ? (const void*)sb2st_fused_kernel<true>
                                               : (const void*)sb2st_fused_kernel<false>,
