@@ -76,6 +76,10 @@ BSE_DEV void bulk_g2s(void* dst, const void* src, unsigned bytes, unsigned long 
       ::"r"(smem_u32(dst)), "l"(src), "r"(bytes), "r"(smem_u32(bar)) : "memory");
 }
 
+// orders this thread's earlier generic-proxy accesses (here: an acquire of
+// data other CTAs stored) before its later async-proxy (bulk copy) accesses
+BSE_DEV void fence_proxy_async() { asm volatile("fence.proxy.async;\n" ::: "memory"); }
+
 // ---------------------------------------------------------------------------
 // Reductions
 BSE_DEV double warp_sum(double v) {

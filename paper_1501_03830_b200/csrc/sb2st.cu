@@ -5,8 +5,10 @@
 // counters per sweep), so ~N/(2b) sweeps are in flight at once.  The band
 // (ldab = 2b + 1 doubles per column) stays L2-resident; every reflector is
 // stored for the Q2 back-transform.
+#include <cuda.h>
 #include <cstdio>
 #include <cstdlib>
+#include <cstring>
 #include <vector>
 #include "eig.cuh"
 
@@ -67,7 +69,6 @@ BSE_DEV unsigned long long gtimer() {
 // consumer whose predecessor has no step j + 1 waits for the predecessor to
 // finish (`late` == kDone) and reads the band.
 constexpr int kLd2 = 66;
-constexpr int kPairSlots = 34;  // 16-byte row-pair slots per column (33 used)
 constexpr int kBulkWarps = kSbThreads / 32;  // every warp stores part of the bulk
 constexpr int kMailSlots = kMaxPanel + 2;    // slot 0: O(0, 0); 1..lp-1: O(0, c); lp: D(0, 0)
 constexpr int kMailRing = 160;               // sweeps (> resident CTAs + 1)
@@ -93,13 +94,16 @@ BSE_DEV double mail_get(const unsigned long long* slot, unsigned long long tag) 
 }
 
 struct SbfSmem {
-  double D[2][kMaxPanel * kLd2 + 2];  // double-buffered: step j+1 stages while j computes
-  double O[2][kMaxPanel * kLd2 + 2];
+  // double-buffered: step j+1 stages while j computes; every buffer starts
+  // 128-byte aligned (tensor-copy destination)
+  alignas(128) double D[2][kMaxPanel * kLd2 + 16];
+  alignas(128) double O[2][kMaxPanel * kLd2 + 16];
   double vbuf[2][kMaxPanel];
   double vnw[kSbThreads / 32][kMaxPanel];
   double w[kMaxPanel];
   double y[kMaxPanel];
   double tt[kMaxPanel];
+  unsigned long long mbar[2];  // bulk-copy staging of full blocks, one per buffer
 };
 
 // phase A (lanes: 4 rows x 4 quarters per half-warp) column pattern
@@ -133,79 +137,34 @@ BSE_DEV void poll_counter(const int* ctr, int need) {
   fence_acquire();
 }
 
-// 16-byte L2-only async copy of `bytes` (0, 8 or 16) with zero fill: band
-// lines never enter L1, so no stale-L1 hazard across CTAs.
-BSE_DEV void cp_async16_n(void* smem, const void* gmem, int bytes) {
-  unsigned sa = static_cast<unsigned>(__cvta_generic_to_shared(smem));
-  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(sa), "l"(gmem), "r"(bytes));
-}
-
 BSE_DEV void st_global_v2(double* p, double a, double b) {
   asm volatile("st.global.v2.f64 [%0], {%1, %2};\n" ::"l"(p), "d"(a), "d"(b) : "memory");
 }
 
-// Issue the bulk of a step's staging (everything but the late positions, which
-// are loaded stale and overwritten after the late wait) into (Db, Ob), which
-// are already shifted by q0 & 1.  Threads t0, t0 + nt, ... of a 256-slot grid.
-BSE_DEV void stage_bulk(double* Db, double* Ob, const double* AB, int ldab, int q0, int lq, int p0,
-                        int lp, int t0, int nt) {
-  const int sh = q0 & 1;
-  if (lq == kMaxPanel && lp == kMaxPanel) {
-    // full blocks: 4 slots per column, 16-byte row pairs, no zero fill (D's
-    // strict upper triangle is mirrored afterwards)
-    for (int t = t0; t < kSbThreads; t += nt) {
-      const int c = t >> 2, kq = t & 3;
-      const double* osrc = AB + (long long)(p0 + c) * ldab + (q0 - p0 - c);
-      const double* dsrc = AB + (long long)(q0 + c) * ldab - c;
-      double* od = Ob + c * kLd2;
-      double* dd = Db + c * kLd2;
-#pragma unroll
-      for (int i = 0; i < 9; ++i) {
-        const int k = kq + 4 * i;
-        if (k <= 32) {
-          const int r0 = 2 * k - sh;
-          const int bytes = k < 32 ? 16 : (sh ? 8 : 0);
-          if (bytes) {
-            cp_async16_n(od + r0, osrc + r0, bytes);
-            if (r0 + 1 >= c) cp_async16_n(dd + r0, dsrc + r0, bytes);
-          }
-        }
-      }
-    }
-  } else {
-    constexpr int kTotal = 2 * kMaxPanel * kPairSlots;
-    for (int t = t0; t < kTotal; t += nt) {
-      const bool isO = t >= kMaxPanel * kPairSlots;
-      const int u = isO ? t - kMaxPanel * kPairSlots : t;
-      const int c = u / kPairSlots, k = u - kPairSlots * c;
-      const int r0 = 2 * k - sh;
-      if (r0 >= kMaxPanel) continue;
-      double* dst = (isO ? Ob : Db) + c * kLd2 + r0;
-      const double* src = isO ? AB + (long long)(p0 + c) * ldab + (q0 + r0 - p0 - c)
-                              : AB + (long long)(q0 + c) * ldab + (r0 - c);
-      // need: the row must come from this copy; zero: the row must read 0;
-      // other rows (row -1/64 padding, D's upper triangle) are don't-care.
-      const int r1 = r0 + 1;
-      bool need0, need1, zero0, zero1;
-      if (isO) {
-        need0 = r0 >= 0 && r0 < lq && c < lp;
-        need1 = r1 < kMaxPanel && r1 < lq && c < lp;
-        zero0 = r0 >= 0 && !need0;
-        zero1 = r1 < kMaxPanel && !need1;
-      } else {
-        need0 = r0 >= 0 && r0 >= c && r0 < lq;
-        need1 = r1 < kMaxPanel && r1 >= c && r1 < lq;
-        zero0 = r0 >= 0 && r0 >= c && !need0;
-        zero1 = r1 < kMaxPanel && r1 >= c && !need1;
-      }
-      int bytes;
-      if (need1) bytes = 16;
-      else if (need0) bytes = 8;
-      else if (zero0 || zero1) bytes = 0;
-      else continue;
-      cp_async16_n(dst, bytes ? src : AB, bytes);
-    }
-  }
+// Staging.  With ldab - 1 = 2b the band is a 2-D tensor T[j][x] at 2b j + x
+// (rows overlap: x runs past 2b), in which a block is the box x in
+// [q0 - sh, q0 - sh + kLd2), j in [c0, c0 + 64) -- exactly the shared-memory
+// layout above (kLd2 doubles per column: the 16-byte aligned superset of its
+// rows).  One thread issues two tensor copies per step that complete on the
+// buffer's mbarrier: no per-thread copy instructions, no commit/wait groups.
+// The box is always the full 64 x 64 block: ragged blocks (step 0's single
+// column of O, the last steps of a sweep) bring in other finite band entries,
+// or zeros past column n - 1, which only ever meet exact zeros of v / vn or
+// land in rows and columns the stores mask out; D's strict upper triangle is
+// never read.
+constexpr unsigned kBlockBytes = kMaxPanel * kLd2 * sizeof(double);
+BSE_DEV void tma_load_2d(void* dst, const CUtensorMap* map, unsigned long long* bar, int x, int j) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%3, %4}], [%2];\n" ::"r"(smem_u32(dst)), "l"(map), "r"(smem_u32(bar)), "r"(x), "r"(j)
+      : "memory");
+}
+BSE_DEV void stage_tma(double* Dbuf, double* Obuf, unsigned long long* bar, const CUtensorMap* map,
+                       int nq0, int q0) {
+  const int x = nq0 - (nq0 & 1);
+  mbar_arrive_expect_tx(bar, 2 * kBlockBytes);
+  tma_load_2d(Obuf, map, bar, x, q0);
+  tma_load_2d(Dbuf, map, bar, x, nq0);
 }
 
 // The late positions (D's last row and O(lq-1, lp-1)), after the late wait.
@@ -237,18 +196,24 @@ BSE_DEV void late_load(double* Db, double* Ob, const double* AB, int ldab, int q
 BSE_DEV void named_bar(int id, int nthreads) {
   asm volatile("bar.sync %0, %1;\n" ::"r"(id), "r"(nthreads) : "memory");
 }
+BSE_DEV void named_bar_arrive(int id, int nthreads) {
+  asm volatile("bar.arrive %0, %1;\n" ::"r"(id), "r"(nthreads) : "memory");
+}
+// barrier of the 8 compute warps (the staging warp never joins it)
+BSE_DEV void cta_sync() { named_bar(3, kSbThreads); }
 
 // kDiag: the BSE_SB2ST_MODE diagnostics (delay injection, alternative
 // publication / polls) are compiled into a separate instance, so the
 // production kernel carries none of their checks.
 template <bool kDiag>
-__global__ void __launch_bounds__(kSbThreads) sb2st_fused_kernel(double* AB, int ldab, int n,
+__global__ void __launch_bounds__(kSbThreads + 32) sb2st_fused_kernel(const __grid_constant__ CUtensorMap tmap,
+                                                                 double* AB, int ldab, int n,
                                                                  int b, double* V2, double* tau2,
                                                                  int maxsteps, int* progress,
                                                                  unsigned long long* mail,
                                                                  unsigned long long* trace) {
-  extern __shared__ __align__(16) unsigned char raw[];
-  SbfSmem& sm = *reinterpret_cast<SbfSmem*>(raw);
+  extern __shared__ __align__(128) unsigned char raw[];
+  SbfSmem& sm = *reinterpret_cast<SbfSmem*>(raw + ((128u - (smem_u32(raw) & 127u)) & 127u));
   const int tid = threadIdx.x;
   const int lane = tid & 31, warp = tid >> 5;
   const int mi = warp * 8 + (lane >> 2);  // row (A) / column (C) owned by this quarter-thread
@@ -259,26 +224,69 @@ __global__ void __launch_bounds__(kSbThreads) sb2st_fused_kernel(double* AB, int
   int* full = progress;
   int* late = progress + n;
   if (tid < kMaxPanel) sm.vbuf[0][tid] = sm.vbuf[1][tid] = 0.0;
+  if (tid == 0) {
+    mbar_init(&sm.mbar[0], 1);
+    mbar_init(&sm.mbar[1], 1);
+    mbar_fence_init();
+  }
+  unsigned ph[2] = {0u, 0u};  // mbarrier phases (CTA-uniform)
+  __syncthreads();  // all nine warps: the mbarriers are initialised
+
+  // Staging warp.  The blocks of step j+1 can be fetched as soon as the
+  // predecessor has stored its step j+1 and this sweep is done with step
+  // j-1's buffer -- usually in the middle of step j's bulk store.  None of the
+  // compute warps can poll for that moment without holding up its share of the
+  // step, so a ninth warp does: it replays the step geometry, takes one
+  // named-barrier arrival per staging from the compute warps (buffer free),
+  // polls the predecessor's `full` counter and issues the two tensor copies.
+  if (warp == kSbThreads / 32) {
+    for (int s = blockIdx.x; s < n - 2; s += gridDim.x) {
+      const bool trp = trace != nullptr && (s == ts0 || s == ts0 + 1) && lane == 0;
+      ts = s;
+      const bool has_pred = s > 0;
+      int p0 = s, q0 = s + 1, q1 = min(s + b, n - 1);
+      for (int j = 0;; ++j) {
+        // stage step j into buffer j & 1: O at columns p0.., D at columns q0..
+        tj = j > 0 ? j - 1 : 0;
+        named_bar(2, kSbThreads + 32);
+        if (lane == 0) {
+          dbg_delay<kDiag>(16, s, j);
+          if (has_pred) poll_counter<kDiag>(full + s - 1, kBulkWarps * (j + 1));
+          fence_proxy_async();
+          if (trp && j > 0) T(7);
+          stage_tma(sm.D[j & 1], sm.O[j & 1], &sm.mbar[j & 1], &tmap, q0, p0);
+          if (trp && j > 0) T(8);
+        }
+        __syncwarp();
+        if (q1 + 1 > n - 1) break;
+        p0 = q0;
+        q0 = q1 + 1;
+        q1 = min(q1 + b, n - 1);
+      }
+    }
+    return;
+  }
 
   for (int s = blockIdx.x; s < n - 2; s += gridDim.x) {
     const bool trw = trace != nullptr && (s == ts0 || s == ts0 + 1);
     const bool trs = trw && tid == 0;
-    const bool trs32 = trw && tid == 32;
     ts = s;
     const bool has_pred = s > 0;
     int p0 = s, lp = 1;
     double tau = 0.0;
     int q0 = s + 1, q1 = min(s + b, n - 1);
     int lq = q1 - q0 + 1;
-    // prologue: step 0's bulk into buffer 0
-    __syncthreads();  // the previous sweep is done with both buffers
-    if (has_pred && tid == 0) poll_counter<kDiag>(full + s - 1, kBulkWarps);
-    __syncthreads();
-    stage_bulk(sm.D[0] + (q0 & 1), sm.O[0] + (q0 & 1), AB, ldab, q0, lq, p0, lp, tid, kSbThreads);
-    cp_async_commit();
+    cta_sync();  // the previous sweep is done with both buffers
+    named_bar_arrive(2, kSbThreads + 32);  // stage step 0
     for (int j = 0;; ++j) {
       const int cur = j & 1;
       const int sh = q0 & 1;
+      // next step's geometry
+      const int nq0 = q1 + 1;
+      const bool has_next = nq0 <= n - 1;
+      const int nq1 = min(q1 + b, n - 1);
+      const int nlq = nq1 - nq0 + 1;
+
       double* Db = sm.D[cur] + sh;
       double* Ob = sm.O[cur] + sh;
       const double* v = sm.vbuf[j & 1];
@@ -299,8 +307,11 @@ __global__ void __launch_bounds__(kSbThreads) sb2st_fused_kernel(double* AB, int
         poll_counter<kDiag>(late + s - 1, kDone);
       }
       if (tid == 0) dbg_delay<kDiag>(32, s, j);
-      cp_async_wait<0>();
-      __syncthreads();
+      mbar_wait(&sm.mbar[cur], ph[cur]);  // this step's blocks have landed
+      ph[cur] ^= 1u;
+      cta_sync();
+      // every compute warp is past step j-1: its buffer may be refilled
+      if (has_next) named_bar_arrive(2, kSbThreads + 32);
       if (trs) T(1);
       if (mailed) {
         const int rl = lq - 1;
@@ -310,7 +321,7 @@ __global__ void __launch_bounds__(kSbThreads) sb2st_fused_kernel(double* AB, int
       } else {
         late_load(Db, Ob, AB, ldab, q0, lq, p0, lp, b);
       }
-      __syncthreads();
+      cta_sync();
       if (trs) T(2);
       // A: w = tau O v
       {
@@ -326,7 +337,7 @@ __global__ void __launch_bounds__(kSbThreads) sb2st_fused_kernel(double* AB, int
         }
         if (q == 0) sm.w[mi] = tau * a;
       }
-      __syncthreads();
+      cta_sync();
       // B: vn = house(O[:, 0] - w), per warp
       double* vn = sm.vnw[warp];
       double taun = 0.0, betan;
@@ -377,13 +388,8 @@ __global__ void __launch_bounds__(kSbThreads) sb2st_fused_kernel(double* AB, int
           sm.y[mi] = taun * (gc - v[mi] * swv);
         }
       }
-      __syncthreads();
+      cta_sync();
       if (trs) T(3);
-      // next step's geometry
-      const int nq0 = q1 + 1;
-      const bool has_next = nq0 <= n - 1;
-      const int nq1 = min(q1 + b, n - 1);
-      const int nlq = nq1 - nq0 + 1;
       const double gm = warp_sum(sm.tt[lane] * vn[lane] + sm.tt[lane + 32] * vn[lane + 32]);
       const double al = -0.5 * taun * gm;
       if (warp == 0) {
@@ -418,81 +424,59 @@ __global__ void __launch_bounds__(kSbThreads) sb2st_fused_kernel(double* AB, int
         sm.vbuf[(j + 1) & 1][lane + 32] = vn[lane + 32];
         if (lane == 0) tau2[(long long)s * maxsteps + j] = taun;
       }
-      // D: the bulk of O'' and D'' (rows >= 1)
+      // D: the bulk of O'' and D'' (rows >= 1).  Lane l owns the 16-byte row
+      // pair k = l + sh (rows 2k - sh, 2k - sh + 1: with the parity shift the
+      // 32 pairs cover rows 1 .. 63) and keeps its row terms in registers;
+      // warp w walks the columns w, 8 + w, ... (every warp the same share of
+      // D's triangle), whose terms are broadcast loads.  One store instruction
+      // writes 512 contiguous bytes of a band column.
       if constexpr (kDiag) {
         if (lane == 0 && (!(c_sb_mode & 128) || warp == 0) && (!(c_sb_mode & 256) || warp != 0))
           dbg_delay<kDiag>(8, s, (c_sb_mode & 64) ? j : j + warp);
         __syncwarp();
       }
-      if (lq == kMaxPanel && lp == kMaxPanel) {
-        const int c = kMaxPanel - 1 - (tid >> 2), kq = tid & 3;
-        double* od = AB + (long long)(p0 + c) * ldab + (q0 - p0 - c);
-        double* dd = AB + (long long)(q0 + c) * ldab - c;
-        const double vc = v[c], yc = sm.y[c];
-        const double vnc = vn[c], w2c = sm.tt[c] + al * vnc;
-        const int dlo = c > 1 ? c : 1;
+      {
+        const int r0 = 2 * lane + sh, r1 = r0 + 1;  // r0 >= 0, r1 <= 64
+        const bool in0 = r0 >= 1 && r0 < lq, in1 = r1 < lq;
+        const int r1c = r1 < kMaxPanel ? r1 : kMaxPanel - 1;
+        const double w0 = sm.w[r0], w1 = sm.w[r1c];
+        const double vn0 = vn[r0], vn1 = vn[r1c];
+        const double u0 = sm.tt[r0] + al * vn0, u1 = sm.tt[r1c] + al * vn1;
 #pragma unroll
-        for (int i = 0; i < 9; ++i) {
-          const int k = kq + 4 * i;
-          if (k <= 32) {
-            const int r0 = 2 * k - sh, r1 = r0 + 1;
-            const bool in0 = r0 >= 1 && r0 < kMaxPanel, in1 = r1 >= 1 && r1 < kMaxPanel;
+        for (int i = 0; i < kMaxPanel / kBulkWarps; ++i) {
+          const int c = kBulkWarps * i + warp;
+          if (c < lp) {
             double o0 = 0.0, o1 = 0.0;
             if (c > 0) {
-              if (in0) o0 = Ob[c * kLd2 + r0] - sm.w[r0] * vc - vn[r0] * yc;
-              if (in1) o1 = Ob[c * kLd2 + r1] - sm.w[r1] * vc - vn[r1] * yc;
+              const double2 ov = *reinterpret_cast<const double2*>(Ob + c * kLd2 + r0);
+              const double vc = v[c], yc = sm.y[c];
+              o0 = ov.x - w0 * vc - vn0 * yc;
+              o1 = ov.y - w1 * vc - vn1 * yc;
             }
+            double* od = AB + (long long)(p0 + c) * ldab + (q0 - p0 - c);
             if (in0 && in1) st_global_v2(od + r0, o0, o1);
             else if (in0) od[r0] = o0;
             else if (in1) od[r1] = o1;
-            const bool d0 = in0 && r0 >= dlo, d1 = in1 && r1 >= dlo;
-            double e0 = 0.0, e1 = 0.0;
-            if (d0) e0 = Db[c * kLd2 + r0] - (vn[r0] * w2c + (sm.tt[r0] + al * vn[r0]) * vnc);
-            if (d1) e1 = Db[c * kLd2 + r1] - (vn[r1] * w2c + (sm.tt[r1] + al * vn[r1]) * vnc);
-            if (d0 && d1) st_global_v2(dd + r0, e0, e1);
-            else if (d0) dd[r0] = e0;
-            else if (d1) dd[r1] = e1;
           }
-        }
-      } else {
-        constexpr int kTotal = 2 * kMaxPanel * kPairSlots;
-        for (int t = tid; t < kTotal; t += kSbThreads) {
-          const bool isO = t >= kMaxPanel * kPairSlots;
-          const int u = isO ? t - kMaxPanel * kPairSlots : t;
-          const int c = u / kPairSlots, k = u - kPairSlots * c;
-          const int r0 = 2 * k - sh, r1 = r0 + 1;
-          if (r0 >= lq) continue;
-          double val0 = 0.0, val1 = 0.0;
-          bool ok0, ok1;
-          double* dst;
-          if (isO) {
-            if (c >= lp) continue;
-            ok0 = r0 >= 1;
-            ok1 = r1 >= 1 && r1 < lq;
-            dst = AB + (long long)(p0 + c) * ldab + (q0 + r0 - p0 - c);
-            if (c > 0) {
-              const double vc = v[c], yc = sm.y[c];
-              if (ok0) val0 = Ob[c * kLd2 + r0] - sm.w[r0] * vc - vn[r0] * yc;
-              if (ok1) val1 = Ob[c * kLd2 + r1] - sm.w[r1] * vc - vn[r1] * yc;
+          if (c < lq) {
+            const bool d0 = in0 && r0 >= c, d1 = in1 && r1 >= c;
+            if (d0 || d1) {
+              const double2 dv = *reinterpret_cast<const double2*>(Db + c * kLd2 + r0);
+              const double vnc = vn[c], w2c = sm.tt[c] + al * vnc;
+              const double e0 = dv.x - (vn0 * w2c + u0 * vnc);
+              const double e1 = dv.y - (vn1 * w2c + u1 * vnc);
+              double* dd = AB + (long long)(q0 + c) * ldab - c;
+              if (d0 && d1) st_global_v2(dd + r0, e0, e1);
+              else if (d0) dd[r0] = e0;
+              else dd[r1] = e1;
             }
-          } else {
-            ok0 = r0 >= 1 && r0 >= c;
-            ok1 = r1 >= 1 && r1 >= c && r1 < lq;
-            if (!ok0 && !ok1) continue;
-            dst = AB + (long long)(q0 + c) * ldab + (r0 - c);
-            const double vc = vn[c], w2c = sm.tt[c] + al * vc;
-            if (ok0) val0 = Db[c * kLd2 + r0] - (vn[r0] * w2c + (sm.tt[r0] + al * vn[r0]) * vc);
-            if (ok1) val1 = Db[c * kLd2 + r1] - (vn[r1] * w2c + (sm.tt[r1] + al * vn[r1]) * vc);
           }
-          if (ok0 && ok1) st_global_v2(dst, val0, val1);
-          else if (ok0) dst[0] = val0;
-          else if (ok1) dst[1] = val1;
         }
       }
       // each warp publishes its own bulk stores: full[s] reaches
       // kBulkWarps * (j + 1) once step j is completely stored
       if (kDiag && (c_sb_mode & 1)) {
-        __syncthreads();
+        cta_sync();
         if (tid == 0) {
           __threadfence();
           atomicAdd(full + s, kBulkWarps);
@@ -505,20 +489,6 @@ __global__ void __launch_bounds__(kSbThreads) sb2st_fused_kernel(double* AB, int
         }
       }
       if (trs) T(5);
-      if (warp != 0 && has_next) {
-        // warps 1..7: stage step j+1's bulk into the other buffer (needs the
-        // predecessor's step j+1 fully stored) -- after our own bulk, so our
-        // `full` is never held back by our predecessor
-        if (tid == 32) dbg_delay<kDiag>(16, s, j);
-        if (has_pred && tid == 32) poll_counter<kDiag>(full + s - 1, kBulkWarps * (j + 2));
-        if (trs32) T(7);
-        named_bar(1, kSbThreads - 32);
-        const int nsh = nq0 & 1;
-        stage_bulk(sm.D[cur ^ 1] + nsh, sm.O[cur ^ 1] + nsh, AB, ldab, nq0, nlq, q0, lq, tid - 32,
-                   kSbThreads - 32);
-        cp_async_commit();
-        if (trs32) T(8);
-      }
       tau = taun;
       if (!has_next) break;
       if (trs) T(6);
@@ -528,7 +498,7 @@ __global__ void __launch_bounds__(kSbThreads) sb2st_fused_kernel(double* AB, int
       q1 = nq1;
       lq = nlq;
     }
-    __syncthreads();
+    cta_sync();
     if (tid == 0) {
       __threadfence();
       st_release(late + s, kDone);
@@ -549,6 +519,37 @@ __global__ void band_to_tridiag_kernel(const double* AB, int ldab, int n, double
 
 int sb2st_maxsteps(int n, int b) { return (int)ceil_div(n, b) + 1; }
 
+// The band as the 2-D tensor T[j][x] = AB[(ldab - 1) j + x] (see stage_tma).
+static bool band_map(CUtensorMap* map, double* AB, int ldab, int n) {
+  using EncodeFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
+                                const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
+                                const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                                CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+  static EncodeFn encode = [] {
+    void* fn = nullptr;
+    cudaDriverEntryPointQueryResult qr;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &qr) != cudaSuccess ||
+        qr != cudaDriverEntryPointSuccess)
+      fn = nullptr;
+    return reinterpret_cast<EncodeFn>(fn);
+  }();
+  if (!encode) return false;
+  // x never exceeds n + kLd2; the boxes issued stay inside the allocation
+  const cuuint64_t dims[2] = {(cuuint64_t)n + 2 * kMaxPanel, (cuuint64_t)n};
+  const cuuint64_t strides[1] = {(cuuint64_t)(ldab - 1) * sizeof(double)};
+  const cuuint32_t box[2] = {(cuuint32_t)kLd2, (cuuint32_t)kMaxPanel};
+  const cuuint32_t estr[2] = {1u, 1u};
+  const CUresult r = encode(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, AB, dims, strides, box, estr,
+                            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                            CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  static bool warned = false;
+  if (r != CUDA_SUCCESS && !warned) {
+    warned = true;
+    std::fprintf(stderr, "[bse] sb2st: tensor map rejected (%d), staging with per-thread copies\n", (int)r);
+  }
+  return r == CUDA_SUCCESS;
+}
+
 static size_t mail_offset_ints(int n) { return ((2 * (size_t)n + 3) / 4) * 4; }
 
 size_t sb2st_progress_ints(int n, int b) {
@@ -565,7 +566,7 @@ cudaError_t sb2st(double* AB, int ldab, int n, int b, double* d, double* e, doub
       return err;
     // mailboxes: 16-byte aligned, behind the 2n counters
     unsigned long long* mail = reinterpret_cast<unsigned long long*>(progress + mail_offset_ints(n));
-    const size_t smem = sizeof(SbfSmem);
+    const size_t smem = sizeof(SbfSmem) + 128;
     static PerDeviceOnce attr, attr_diag;
     static const int sb_mode = std::getenv("BSE_SB2ST_MODE") ? std::atoi(std::getenv("BSE_SB2ST_MODE")) : 0;
     if ((err = sb_mode ? set_smem_limit(attr_diag, sb2st_fused_kernel<true>, (int)smem)
@@ -587,11 +588,13 @@ cudaError_t sb2st(double* AB, int ldab, int n, int b, double* d, double* e, doub
       cudaMalloc(&trace, sizeof(unsigned long long) * tsz);
       cudaMemsetAsync(trace, 0, sizeof(unsigned long long) * tsz, s);
     }
-    void* args[] = {&AB, &ldab, &n, &b, &V2, &tau2, &maxsteps, &progress, &mail, &trace};
+    CUtensorMap tmap;
+    if (b != kMaxPanel || !band_map(&tmap, AB, ldab, n)) return cudaErrorNotSupported;
+    void* args[] = {&tmap, &AB, &ldab, &n, &b, &V2, &tau2, &maxsteps, &progress, &mail, &trace};
     count_launch();
     err = cudaLaunchCooperativeKernel(sb_mode ? (const void*)sb2st_fused_kernel<true>
                                               : (const void*)sb2st_fused_kernel<false>,
-                                      dim3(grid), dim3(kSbThreads),
+                                      dim3(grid), dim3(kSbThreads + 32),
                                       args, smem, s);
     if (err != cudaSuccess) return err;
     if (want_trace) {
