@@ -81,6 +81,30 @@ BSE_DEV void bulk_g2s(void* dst, const void* src, unsigned bytes, unsigned long 
 BSE_DEV void fence_proxy_async() { asm volatile("fence.proxy.async;\n" ::: "memory"); }
 
 // ---------------------------------------------------------------------------
+// Self-validating 16-byte mailbox slots {bits, bits ^ tag}: a value handed
+// from one CTA to another without fences or a separate flag.  Each 8-byte
+// half is written atomically, so a torn or stale slot never validates
+// against the reader's tag (64-bit hashes of the slot's use); readers poll.
+BSE_DEV unsigned long long mail_tag(int s, int j) {
+  unsigned long long x = ((unsigned long long)(unsigned)s << 24) ^ (unsigned long long)(unsigned)j;
+  x += 0x9e3779b97f4a7c15ull;
+  x = (x ^ (x >> 30)) * 0xbf58476d1ce4e5b9ull;
+  x = (x ^ (x >> 27)) * 0x94d049bb133111ebull;
+  return (x ^ (x >> 31)) | 1ull;
+}
+BSE_DEV void mail_put(unsigned long long* slot, double v, unsigned long long tag) {
+  const unsigned long long bits = (unsigned long long)__double_as_longlong(v);
+  asm volatile("st.global.v2.u64 [%0], {%1, %2};\n" ::"l"(slot), "l"(bits), "l"(bits ^ tag) : "memory");
+}
+BSE_DEV double mail_get(const unsigned long long* slot, unsigned long long tag) {
+  unsigned long long lo, hi;
+  do {
+    asm volatile("ld.relaxed.gpu.global.v2.u64 {%0, %1}, [%2];\n" : "=l"(lo), "=l"(hi) : "l"(slot) : "memory");
+  } while ((lo ^ hi) != tag);
+  return __longlong_as_double((long long)lo);
+}
+
+// ---------------------------------------------------------------------------
 // Reductions
 BSE_DEV double warp_sum(double v) {
 #pragma unroll

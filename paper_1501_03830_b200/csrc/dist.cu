@@ -267,7 +267,7 @@ PhaseB carve_b(Arena& a, int n, int nb, int ntl) {
   p.sc.y = p.Y;
   p.sc.z = a.take<double>(2 * (size_t)b * b);
   p.sc.z2 = a.take<double>((size_t)b * b);
-  p.sc.red = a.take<double>(2 * 192 * (2 + 2 * (size_t)b));
+  p.sc.red = a.take<double>(4 * 192 * (2 + 2 * (size_t)b));  // 2 x 16-byte mailbox slots
   p.sc.bar = a.take<unsigned>(4);
   p.sc.splitk_ws = a.take<double>(64 * (size_t)b * b);
   p.sc.probs = a.take<GemmProblem>(128);

@@ -94,7 +94,7 @@ SyevdWork carve_syevd(Arena& a, int n, int flags) {
   w.sc.y = a.take<double>((size_t)ld * b);
   w.sc.z = a.take<double>(2 * (size_t)b * b);
   w.sc.z2 = a.take<double>((size_t)b * b);
-  w.sc.red = a.take<double>(2 * 192 * (2 + 2 * (size_t)b));
+  w.sc.red = a.take<double>(4 * 192 * (2 + 2 * (size_t)b));  // 2 x 16-byte mailbox slots
   w.sc.bar = a.take<unsigned>(4);
   w.sc.splitk_ws = a.take<double>(64 * (size_t)b * b);
   w.sc.symm_ws = a.take<double>((size_t)kSymmSplits * ld * b);

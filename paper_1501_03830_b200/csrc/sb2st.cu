@@ -74,25 +74,6 @@ constexpr int kMailSlots = kMaxPanel + 2;    // slot 0: O(0, 0); 1..lp-1: O(0, c
 constexpr int kMailRing = 160;               // sweeps (> resident CTAs + 1)
 constexpr int kSbMaxGrid = kMailRing - 4;
 
-BSE_DEV unsigned long long mail_tag(int s, int j) {
-  unsigned long long x = ((unsigned long long)(unsigned)s << 24) ^ (unsigned long long)(unsigned)j;
-  x += 0x9e3779b97f4a7c15ull;
-  x = (x ^ (x >> 30)) * 0xbf58476d1ce4e5b9ull;
-  x = (x ^ (x >> 27)) * 0x94d049bb133111ebull;
-  return (x ^ (x >> 31)) | 1ull;
-}
-BSE_DEV void mail_put(unsigned long long* slot, double v, unsigned long long tag) {
-  const unsigned long long bits = (unsigned long long)__double_as_longlong(v);
-  asm volatile("st.global.v2.u64 [%0], {%1, %2};\n" ::"l"(slot), "l"(bits), "l"(bits ^ tag) : "memory");
-}
-BSE_DEV double mail_get(const unsigned long long* slot, unsigned long long tag) {
-  unsigned long long lo, hi;
-  do {
-    asm volatile("ld.relaxed.gpu.global.v2.u64 {%0, %1}, [%2];\n" : "=l"(lo), "=l"(hi) : "l"(slot) : "memory");
-  } while ((lo ^ hi) != tag);
-  return __longlong_as_double((long long)lo);
-}
-
 struct SbfSmem {
   // double-buffered: step j+1 stages while j computes; every buffer starts
   // 128-byte aligned (tensor-copy destination)

@@ -10,6 +10,7 @@
 // 4/3 N^3 flops, all on the FP64 tensor pipe.
 #include <cooperative_groups.h>
 #include <algorithm>
+#include <atomic>
 #include <cstdio>
 #include <cstdlib>
 #include "eig.cuh"
@@ -19,28 +20,12 @@ namespace {
 
 constexpr int kPanelThreads = 256;
 
-BSE_DEV void grid_barrier(unsigned* ctr, unsigned target) {
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    __threadfence();
-    atomicAdd(ctr, 1u);
-    while (true) {
-      unsigned v;
-      asm volatile("ld.acquire.gpu.global.u32 %0, [%1];\n" : "=r"(v) : "l"(ctr) : "memory");
-      if (v >= target) break;
-      __nanosleep(40);
-    }
-    __threadfence();
-  }
-  __syncthreads();
-}
-
 // Householder QR of the m x bw panel P (column-major, ldp), rows split over
 // gridDim.x CTAs; CTA c owns rows [c*R, c*R + R) with R = RPT * 256 and
 // thread t owns rows t, t + 256, ... (row-major slab in smem, stride bw+1:
 // a warp touching one column of 32 consecutive rows is conflict-free).
 // Per column j: one fused CTA reduction (products of every column with x_j,
-// ||tail||^2, the owner's row j) -> one grid barrier -> a fixed-order sum of
+// ||tail||^2, the owner's row j) -> mailbox exchange -> a fixed-order sum of
 // the G partials -> rank-1 update of the thread's own rows.  Outputs:
 //   P  <- R in its upper bw x bw triangle, zeros below
 //   V  (ldv), V2 (ldv2): explicit unit-lower-trapezoidal reflectors
@@ -49,7 +34,7 @@ template <int RPT>
 __global__ void __launch_bounds__(kPanelThreads) panel_qr_kernel(
     double* __restrict__ P, long long ldp, int m, int bw, double* __restrict__ V, long long ldv,
     double* __restrict__ V2, long long ldv2, double* __restrict__ T, double* __restrict__ red,
-    unsigned* bar, unsigned long long* trace) {
+    unsigned epoch, unsigned long long* trace) {
   constexpr int R = RPT * kPanelThreads;
   constexpr int LS = kMaxPanel + 1;   // row stride
   constexpr int L = 2 + 2 * kMaxPanel;
@@ -60,6 +45,7 @@ __global__ void __launch_bounds__(kPanelThreads) panel_qr_kernel(
   double* wv = tot + L;                   // w_k / y_i
   double* Ts = wv + kMaxPanel;            // T (CTA 0), [j*bw + i]
   __shared__ double sc[4];
+  __shared__ double gsum[3][2 + kMaxPanel];  // part sums of the exchange
   const bool tr = trace != nullptr && blockIdx.x == 0 && threadIdx.x == 0;
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -118,8 +104,14 @@ __global__ void __launch_bounds__(kPanelThreads) panel_qr_kernel(
     }
     __syncthreads();
     // CTA partial: [0] tail, [1] x0 (owner), [2+k] dots, [2+bw+k] owner's row j
-    double* slot = red + (size_t)(j & 1) * G * L;
     const bool owner = (j >= r0 && j < r0 + rows);
+    // The exchange across CTAs goes through self-validating mailbox slots
+    // (common.cuh), double-buffered by column parity: every CTA stores its L
+    // partials and then polls the others' -- no grid barrier, no fences, one
+    // L2 round trip.  A CTA can only be two columns ahead of another after
+    // that one has read the buffer being reused.
+    unsigned long long* box = reinterpret_cast<unsigned long long*>(red) + (size_t)(j & 1) * G * L * 2;
+    const unsigned long long tag = mail_tag((int)epoch, j);
     for (int t = tid; t < L; t += blockDim.x) {
       double v;
       if (t == 1) {
@@ -131,25 +123,53 @@ __global__ void __launch_bounds__(kPanelThreads) panel_qr_kernel(
 #pragma unroll
         for (int w = 0; w < 8; ++w) v += wpart[w * L + t];
       }
-      if (G > 1) slot[(size_t)cta * L + t] = v;
+      if (G > 1) mail_put(box + 2 * ((size_t)cta * L + t), v, tag);
       else tot[t] = v;
     }
     if (tr) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t1));
     if (G > 1) {
-      grid_barrier(bar, (unsigned)G * (unsigned)(j + 1));
-      if (tr) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t2));
-      for (int t = tid; t < L; t += blockDim.x) {
-        double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
-        int c = 0;
-        for (; c + 4 <= G; c += 4) {
-          a0 += __ldcg(slot + (size_t)(c + 0) * L + t);
-          a1 += __ldcg(slot + (size_t)(c + 1) * L + t);
-          a2 += __ldcg(slot + (size_t)(c + 2) * L + t);
-          a3 += __ldcg(slot + (size_t)(c + 3) * L + t);
+      // sums over the CTAs (fixed order): values [0, NV) by three threads each
+      // (a third of the CTAs, up to 24 loads in flight); the first 64 of these
+      // threads also fetch the owner's row (one more load in the same batch)
+      constexpr int NV = 2 + kMaxPanel;
+      constexpr int NP = 3, CH = 24;
+      auto ld2 = [](unsigned long long& a, unsigned long long& b, const unsigned long long* sl) {
+        asm volatile("ld.relaxed.gpu.global.v2.u64 {%0, %1}, [%2];\n" : "=l"(a), "=l"(b) : "l"(sl) : "memory");
+      };
+      if (tid < NP * NV) {
+        const int t = tid % NV, part = tid / NV;
+        const int per = (G + NP - 1) / NP;
+        const int lo = part * per, hi = min(G, lo + per);
+        const bool own = tid < kMaxPanel;
+        const unsigned long long* osl = box + 2 * ((size_t)(j / R) * L + NV + tid);
+        unsigned long long ol = 0, oh = 0;
+        if (own) ld2(ol, oh, osl);
+        double acc = 0.0;
+        for (int c0 = lo; c0 < hi; c0 += CH) {
+          unsigned long long l[CH], h[CH];
+          bool ok;
+          do {
+            ok = true;
+#pragma unroll
+            for (int u = 0; u < CH; ++u)
+              if (c0 + u < hi) ld2(l[u], h[u], box + 2 * ((size_t)(c0 + u) * L + t));
+#pragma unroll
+            for (int u = 0; u < CH; ++u)
+              if (c0 + u < hi) ok = ok && ((l[u] ^ h[u]) == tag);
+          } while (!ok);
+#pragma unroll
+          for (int u = 0; u < CH; ++u)
+            if (c0 + u < hi) acc += __longlong_as_double((long long)l[u]);
         }
-        for (; c < G; ++c) a0 += __ldcg(slot + (size_t)c * L + t);
-        tot[t] = (a0 + a1) + (a2 + a3);
+        gsum[part][t] = acc;
+        if (own) {
+          while ((ol ^ oh) != tag) ld2(ol, oh, osl);
+          tot[NV + tid] = __longlong_as_double((long long)ol);
+        }
       }
+      if (tr) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t2));
+      __syncthreads();
+      if (tid < NV) tot[tid] = (gsum[0][tid] + gsum[1][tid]) + gsum[2][tid];
     }
     __syncthreads();
     if (tr) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t3));
@@ -256,8 +276,10 @@ cudaError_t panel_qr(double* P, long long ldp, int m, int bw, double* V, long lo
     if (e != cudaSuccess) return e;
     lim.store(smem);
   }
-  cudaError_t e = cudaMemsetAsync(bar, 0, sizeof(unsigned), s);
-  if (e != cudaSuccess) return e;
+  (void)bar;  // the exchange needs no barrier counter
+  // tags are unique per launch: the mailbox buffer is reused without clearing
+  static std::atomic<unsigned> epoch_ctr{1};
+  unsigned epoch = epoch_ctr.fetch_add(1);
   static unsigned long long* trace = nullptr;
   static int traced = 0;
   const bool want = std::getenv("BSE_PANEL_TRACE") != nullptr && traced == 0 && m > 8000;
@@ -267,7 +289,7 @@ cudaError_t panel_qr(double* P, long long ldp, int m, int bw, double* V, long lo
     cudaMemsetAsync(trace, 0, sizeof(unsigned long long) * 5 * 64, s);
     tptr = trace;
   }
-  void* args[] = {&P, &ldp, &m, &bw, &V, &ldv, &V2, &ldv2, &T, &red, &bar, &tptr};
+  void* args[] = {&P, &ldp, &m, &bw, &V, &ldv, &V2, &ldv2, &T, &red, &epoch, &tptr};
   count_launch();
   cudaError_t le;
   if (G == 1)

@@ -53,7 +53,10 @@ def main():
             nm = names.raw[32 * i:32 * (i + 1)].split(b"\0")[0].decode()
             st[nm] = st.get(nm, 0.0) + ms[i]
         hashes.append(hashlib.sha1(w.cpu().numpy().tobytes()).hexdigest()[:12])
-        line = f"rep {rep}: sb2st {st.get('sb2st', float('nan')):.2f} ms  hash {hashes[-1]}"
+        line = (f"rep {rep}: sb2st {st.get('sb2st', float('nan')):.2f} ms  sy2sb panel "
+                f"{st.get('sy2sb_panel', float('nan')):.2f} symm {st.get('sy2sb_symm', float('nan')):.2f} "
+                f"small {st.get('sy2sb_small', float('nan')):.2f} syr2k {st.get('sy2sb_syr2k', float('nan')):.2f} ms"
+                f"  hash {hashes[-1]}")
         if args.check:
             e1 = abs(float(w.sum()) - tr) / (abs(tr) + fro2 ** 0.5)
             e2 = abs(float((w * w).sum()) - fro2) / fro2
