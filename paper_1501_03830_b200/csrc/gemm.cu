@@ -230,6 +230,7 @@ BSE_DEV void gemm_tile(const GemmProblem& p, int m0, int n0, double* smem) {
         double v = alpha * acc[i][j][e];
         if (beta != 0.0 && !cpre) v += beta * *cp;
         *cp = v;
+        if (p.mirror && gn < gm) p.C[gn + (long long)gm * p.ldc] = v;
       }
     }
   }

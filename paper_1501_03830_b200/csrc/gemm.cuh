@@ -37,6 +37,7 @@ struct GemmProblem {
   double alpha = 1.0, beta = 0.0;
   Mask ma, mb, mc;
   const int* ccol = nullptr;  // optional column map: C column n is written at ccol[n]
+  bool mirror = false;        // also store every strictly-lower C(m, n) at C(n, m) (symmetric result)
 };
 
 // Single problem.  transA/transB: op(X) = X^T.

@@ -422,8 +422,12 @@ cudaError_t sy2sb(double* A, long long lda, int n, int b, double* Vall, long lon
     stage_mark("sy2sb_symm", s);
     // both SYMMs of the pair read the trailing matrix as it stands now (the
     // second one on its stale sub-block A3): mirror its lower triangle once
+    // (mirrored once for the first pair; afterwards the trailing update's
+    // epilogue stores both triangles of the next pair's A2)
     const bool full = sy2sb_full_symm();
-    if (full && (e = symmetrize_from_lower(A2, lda, m, s)) != cudaSuccess) return e;
+    static const bool epi_mirror = std::getenv("BSE_SY2SB_NO_EPI_MIRROR") == nullptr;  // A/B switch
+    if (full && (p == 0 || !epi_mirror) && (e = symmetrize_from_lower(A2, lda, m, s)) != cudaSuccess)
+      return e;
     if ((e = symm_panel(A2, lda, m, bw, sV1, lw, w, s, full)) != cudaSuccess) return e;
     if ((e = panel_w(m, bw, sV1, lw, Tp1, sW1, lw, w, s)) != cudaSuccess) return e;
     if ((e = copy_cols(sW1c, sW1, m)) != cudaSuccess) return e;
@@ -492,10 +496,12 @@ cudaError_t sy2sb(double* A, long long lda, int n, int b, double* Vall, long lon
       GemmProblem gb = make_gemm(m2 - b, m2 - b, 4 * bw, -1.0, sV1 + 2 * b, lw, sW1c + 2 * b, lw,
                                  1.0, A3 + b + (long long)b * lda, lda);
       gb.mc = Mask::lower();
+      gb.mirror = full && epi_mirror;
       if ((e = gemm(false, true, gb, s)) != cudaSuccess) return e;
     } else {
       GemmProblem g7 = make_gemm(m2, m2, 4 * bw, -1.0, sV1 + b, lw, sW1c + b, lw, 1.0, A3, lda);
       g7.mc = Mask::lower();
+      g7.mirror = full && epi_mirror;
       if ((e = gemm(false, true, g7, s)) != cudaSuccess) return e;
     }
   }
