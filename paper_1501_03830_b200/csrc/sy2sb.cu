@@ -62,26 +62,25 @@ __global__ void __launch_bounds__(kPanelThreads) panel_qr_kernel(
     for (int idx = tid; idx < bw * bw; idx += blockDim.x) Ts[idx] = 0.0;
   __syncthreads();
 
-  // per-thread products of every column with x_j over the owned rows with
-  // global index >= j, and ||x_j tail||^2: computed here for column 0, then
-  // carried from the fused update below (one pass over the slab per column)
-  double pk[kMaxPanel];
-  double tail = 0.0;
-#pragma unroll
-  for (int k = 0; k < kMaxPanel; ++k) pk[k] = 0.0;
-  for (int q = 0; q < RPT; ++q) {
-    const int r = tid + q * kPanelThreads;
-    if (r < rows) {
-      const double* row = S + r * LS;
-      const double xj = row[0];
-#pragma unroll
-      for (int k = 0; k < kMaxPanel; ++k) pk[k] += row[k] * xj;
-      if (r0 + r > 0) tail += xj * xj;
-    }
-  }
   for (int j = 0; j < bw; ++j) {
     unsigned long long t0 = 0, t1 = 0, t2 = 0, t3 = 0;
     if (tr) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+    // ---- per-thread products over owned rows with global index >= j ----
+    double pk[kMaxPanel];
+    double tail = 0.0;
+#pragma unroll
+    for (int k = 0; k < kMaxPanel; ++k) pk[k] = 0.0;
+    for (int q = 0; q < RPT; ++q) {
+      const int r = tid + q * kPanelThreads;
+      const int gr = r0 + r;
+      if (r < rows && gr >= j) {
+        const double* row = S + r * LS;
+        const double xj = row[j];
+#pragma unroll
+        for (int k = 0; k < kMaxPanel; ++k) pk[k] += row[k] * xj;
+        if (gr > j) tail += xj * xj;
+      }
+    }
     // warp reduce-scatter butterfly over the 64 products (62 shuffles per
     // lane instead of 64 full reductions): after step o the lanes with bit o
     // set keep the upper half of the remaining values
@@ -191,41 +190,19 @@ __global__ void __launch_bounds__(kPanelThreads) panel_qr_kernel(
     const double tau = sc[0], beta = sc[1], scale = sc[2];
     if (tid < bw) wv[tid] = (tot[2 + tid] - beta * tot[2 + kMaxPanel + tid]) * scale;
     __syncthreads();
-    // ---- rank-1 update of the owned rows (columns > j), store v_j; the same
-    // pass forms the next column's products from the updated rows ----
-#pragma unroll
-    for (int k = 0; k < kMaxPanel; ++k) pk[k] = 0.0;
-    tail = 0.0;
-    {
-      const bool act = tau != 0.0;
-      const bool nxt = j + 1 < bw;
-      for (int q = 0; q < RPT; ++q) {
-        const int r = tid + q * kPanelThreads;
-        const int gr = r0 + r;
-        if (r < rows && gr >= j) {
-          double* row = S + r * LS;
-          // v_j's entry of this row (tau = 0: H = I, the column below the pivot is zero)
-          const double vr = act ? ((gr == j) ? 1.0 : row[j] * scale) : 0.0;
+    // ---- rank-1 update of the owned rows (columns > j), store v_j ----
+    for (int q = 0; q < RPT; ++q) {
+      const int r = tid + q * kPanelThreads;
+      const int gr = r0 + r;
+      if (r < rows && gr >= j) {
+        double* row = S + r * LS;
+        if (tau != 0.0) {
+          const double vr = (gr == j) ? 1.0 : row[j] * scale;
           const double tv = tau * vr;
-          const bool contrib = nxt && gr > j;
-          double xn = 0.0;  // this row's entry of the next pivot column, after the update
-          if (contrib) xn = row[j + 1] - tv * wv[j + 1];
-#pragma unroll
-          for (int k = 0; k < kMaxPanel; ++k) {
-            double rk = row[k];
-            if (k > j && k < bw) {
-              if (act) {
-                rk -= tv * wv[k];
-                row[k] = rk;
-              }
-            } else if (k == j) {
-              rk = vr;
-            }
-            pk[k] += rk * xn;
-          }
-          if (act) row[j] = (gr == j) ? beta : vr;
-          else if (gr > j) row[j] = 0.0;
-          if (contrib && gr > j + 1) tail += xn * xn;
+          for (int k = j + 1; k < bw; ++k) row[k] -= tv * wv[k];
+          row[j] = (gr == j) ? beta : vr;
+        } else if (gr > j) {
+          row[j] = 0.0;
         }
       }
     }
