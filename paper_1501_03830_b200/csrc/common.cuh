@@ -156,6 +156,13 @@ BSE_DEV void st_release(int* p, int v) {
   asm volatile("st.release.gpu.global.s32 [%0], %1;\n" ::"l"(p), "r"(v) : "memory");
 }
 
+// release increment: orders this thread's earlier writes (and, through a
+// preceding warp barrier, its warp's) before the add, without the acquire half
+// of a full fence (no L1 invalidate)
+BSE_DEV void red_release_add(int* p, int v) {
+  asm volatile("red.release.gpu.global.add.s32 [%0], %1;\n" ::"l"(p), "r"(v) : "memory");
+}
+
 BSE_HD long long ceil_div(long long a, long long b) { return (a + b - 1) / b; }
 
 // One-time per-kernel setup that applies to the CURRENT device only

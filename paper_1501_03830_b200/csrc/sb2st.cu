@@ -210,7 +210,7 @@ __global__ void __launch_bounds__(kSbThreads + 32) sb2st_fused_kernel(const __gr
     mbar_init(&sm.mbar[1], 1);
     mbar_fence_init();
   }
-  unsigned ph[2] = {0u, 0u};  // mbarrier phases (CTA-uniform)
+  unsigned phb = 0u;  // mbarrier phase bits, one per buffer (CTA-uniform; a bit mask stays in a register)
   __syncthreads();  // all nine warps: the mbarriers are initialised
 
   // Staging warp.  The blocks of step j+1 can be fetched as soon as the
@@ -288,8 +288,8 @@ __global__ void __launch_bounds__(kSbThreads + 32) sb2st_fused_kernel(const __gr
         poll_counter<kDiag>(late + s - 1, kDone);
       }
       if (tid == 0) dbg_delay<kDiag>(32, s, j);
-      mbar_wait(&sm.mbar[cur], ph[cur]);  // this step's blocks have landed
-      ph[cur] ^= 1u;
+      mbar_wait(&sm.mbar[cur], (phb >> cur) & 1u);  // this step's blocks have landed
+      phb ^= 1u << cur;
       cta_sync();
       // every compute warp is past step j-1: its buffer may be refilled
       if (has_next) named_bar_arrive(2, kSbThreads + 32);
@@ -464,10 +464,7 @@ __global__ void __launch_bounds__(kSbThreads + 32) sb2st_fused_kernel(const __gr
         }
       } else {
         __syncwarp();
-        if (lane == 0) {
-          __threadfence();
-          atomicAdd(full + s, 1);
-        }
+        if (lane == 0) red_release_add(full + s, 1);
       }
       if (trs) T(5);
       tau = taun;
