@@ -324,10 +324,19 @@ __global__ void __launch_bounds__(kSbThreads + 32) sb2st_fused_kernel(const __gr
       double taun = 0.0, betan;
       double swv;
       {
-        const double x0 = lane < lq ? Ob[lane] - sm.w[lane] : 0.0;
-        const double x1 = lane + 32 < lq ? Ob[lane + 32] - sm.w[lane + 32] : 0.0;
-        const double ss = warp_sum((lane >= 1 ? x0 * x0 : 0.0) + x1 * x1);
+        const double wl0 = sm.w[lane], wl1 = sm.w[lane + 32];
+        const double x0 = lane < lq ? Ob[lane] - wl0 : 0.0;
+        const double x1 = lane + 32 < lq ? Ob[lane + 32] - wl1 : 0.0;
+        // ||x[1:]||^2 and w[1:] . x[1:] reduced together (one shuffle latency chain)
+        double ss = (lane >= 1 ? x0 * x0 : 0.0) + x1 * x1;
+        double wx = (lane >= 1 ? wl0 * x0 : 0.0) + wl1 * x1;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+          ss += __shfl_xor_sync(0xffffffffu, ss, o);
+          wx += __shfl_xor_sync(0xffffffffu, wx, o);
+        }
         const double alpha = __shfl_sync(0xffffffffu, x0, 0);
+        const double w00 = __shfl_sync(0xffffffffu, wl0, 0);
         betan = alpha;
         double scale = 0.0;
         if (ss > 0.0) {
@@ -339,7 +348,7 @@ __global__ void __launch_bounds__(kSbThreads + 32) sb2st_fused_kernel(const __gr
         const double vn1 = x1 * scale;
         vn[lane] = vn0;
         vn[lane + 32] = vn1;
-        swv = warp_sum(sm.w[lane] * vn0 + sm.w[lane + 32] * vn1);
+        swv = w00 + scale * wx;  // w . vn with vn = [1; scale x[1:]]
         __syncwarp();
       }
       // C: t = taun D vn, y = taun (O^T vn - v swv)
@@ -347,19 +356,25 @@ __global__ void __launch_bounds__(kSbThreads + 32) sb2st_fused_kernel(const __gr
         // D holds its lower triangle only: column mi from the diagonal down
         // (this phase's pattern) plus row mi left of the diagonal (phase A's
         // pattern) -- both conflict-free, no mirrored copy needed
-        double tc = 0.0, gc = 0.0, ta = 0.0;
+        double tc = 0.0, gc = 0.0, ta = 0.0, tc1 = 0.0, gc1 = 0.0, ta1 = 0.0;
 #pragma unroll
-        for (int i = 0; i < 16; ++i) {
-          const int r = rowC(q, i);
-          const double vr = vn[r];
+        for (int i = 0; i < 16; i += 2) {
+          const int r = rowC(q, i), r2 = rowC(q, i + 1);
+          const double vr = vn[r], vr2 = vn[r2];
           const double dl = r >= mi ? Db[mi * kLd2 + r] : 0.0;
+          const double dl2 = r2 >= mi ? Db[mi * kLd2 + r2] : 0.0;
           tc += dl * vr;
+          tc1 += dl2 * vr2;
           gc += Ob[mi * kLd2 + r] * vr;
-          const int c = colA(q, i);
+          gc1 += Ob[mi * kLd2 + r2] * vr2;
+          const int c = colA(q, i), c2 = colA(q, i + 1);
           const double du = c < mi ? Db[c * kLd2 + mi] : 0.0;
+          const double du2 = c2 < mi ? Db[c2 * kLd2 + mi] : 0.0;
           ta += du * vn[c];
+          ta1 += du2 * vn[c2];
         }
-        tc += ta;
+        tc = (tc + tc1) + (ta + ta1);
+        gc += gc1;
         tc += __shfl_xor_sync(0xffffffffu, tc, 1);
         tc += __shfl_xor_sync(0xffffffffu, tc, 2);
         gc += __shfl_xor_sync(0xffffffffu, gc, 1);
