@@ -99,7 +99,6 @@ BSE_DEV void gemm_tile(const GemmProblem& p, int m0, int n0, double* smem) {
   // the C read overlaps the pipeline prologue (exact for alpha = +-1)
   const bool cpre = p.beta != 0.0 && (p.alpha == 1.0 || p.alpha == -1.0) && K <= 512;
   {
-    const double f = cpre ? p.beta / p.alpha : 0.0;
     const int klq = (threadIdx.x & 31) & 3, rlq = (threadIdx.x & 31) >> 2;
     const int wmq = (threadIdx.x >> 5) % C::WARPS_M, wnq = (threadIdx.x >> 5) / C::WARPS_M;
 #pragma unroll
@@ -117,11 +116,14 @@ BSE_DEV void gemm_tile(const GemmProblem& p, int m0, int n0, double* smem) {
               const int d = gn - gm;
               ok = d >= p.mc.lo && d <= p.mc.hi;
             }
-            if (ok) v = f * p.C[gm + (long long)(p.ccol ? p.ccol[gn] : gn) * p.ldc];
+            // raw load: the scaling by f waits until the prologue's copies
+            // are in flight (below), so no warp stalls on C before them
+            if (ok) v = p.C[gm + (long long)(p.ccol ? p.ccol[gn] : gn) * p.ldc];
           }
           acc[i][j][e] = v;
         }
   }
+  const double cscale = cpre ? p.beta / p.alpha : 1.0;
 
   auto load_stage = [&](int st, int kt) {
     double* sA = smem + st * C::STAGE;
@@ -137,6 +139,25 @@ BSE_DEV void gemm_tile(const GemmProblem& p, int m0, int n0, double* smem) {
   for (int s = 0; s < STAGES - 1; ++s) {
     if (s < ntiles) load_stage(s, s);
     cp_async_commit();
+  }
+
+  if (cpre && cscale != 1.0) {
+    // acc = f C.  The empty volatile asm keeps these after the (volatile)
+    // cp.async prologue; f = -1 (every trailing update of SY2SB / POTRF) flips
+    // the sign bit on the integer pipe instead of a DMUL that would queue
+    // behind the co-resident CTA's DMMAs on the FP64 pipe.
+    const bool flip = cscale == -1.0;
+#pragma unroll
+    for (int i = 0; i < MI; ++i)
+#pragma unroll
+      for (int j = 0; j < NJ; ++j)
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          asm volatile("" : "+d"(acc[i][j][e]));
+          const double v = acc[i][j][e];
+          acc[i][j][e] = flip ? __hiloint2double(__double2hiint(v) ^ (int)0x80000000, __double2loint(v))
+                              : v * cscale;
+        }
   }
 
   const bool maskA_on = MASKED && p.ma.active(), maskB_on = MASKED && p.mb.active();
